@@ -1,0 +1,178 @@
+/*
+ * gr4ad.h -- C ABI of the B200 LazyAR beam-serving library (libgr4ad.so).
+ *
+ * This is the drop-in boundary for the reference's serving hot path.  The
+ * reference has no native FFI for it; its boundary is the Python call
+ *   adrec.serving.beam.beam_search(model, context, schedule, shared_kv=True,
+ *       precut=True, counter=None, value_rerank=False, buckets=None,
+ *       trunk_depth=None)                     (pkg/src/adrec/serving/beam.py:112-143)
+ * and the only native precedent is the Cython quantizer module
+ * (pkg/src/adrec/_kernels/_core.pyx:15-67: typed memoryviews in, new arrays
+ * out).  The entry points below are what a ctypes/cffi binding of that path
+ * binds; each cites the reference function it replaces.
+ *
+ * Conventions
+ *  - plain C types only; every float pointer is DEVICE memory holding fp32
+ *    unless a field says "host";
+ *  - the caller owns all memory: weights, inputs, outputs and one workspace
+ *    blob sized by gr4ad_workspace_bytes();
+ *  - no global mutable state: calls are reentrant with one stream per thread;
+ *    the last error message is thread-local;
+ *  - functions return gr4ad_status; argument errors carry the reference's
+ *    ValueError messages (beam.py:125-132,155-156) via gr4ad_last_error().
+ */
+#ifndef GR4AD_H_
+#define GR4AD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GR4AD_ABI_VERSION 1
+#define GR4AD_MAX_LEVELS 8
+#define GR4AD_MAX_LAYERS 32
+#define GR4AD_MAX_BEAM 8192 /* per-request selection width handled on chip */
+
+typedef enum {
+  GR4AD_OK = 0,
+  GR4AD_ERR_VALUE = 1,     /* maps to ValueError (reference argument errors) */
+  GR4AD_ERR_UNSUPPORTED = 2,
+  GR4AD_ERR_WORKSPACE = 3, /* workspace too small */
+  GR4AD_ERR_CUDA = 4       /* maps to RuntimeError */
+} gr4ad_status;
+
+/* DecoderConfig (pkg/src/adrec/model/decoder.py:32-51). */
+typedef struct {
+  int feat_dim;
+  int d;
+  int d_ff;
+  int n_layers;
+  int trunk_depth;
+  int n_levels;
+  int n_value_buckets;
+  int vocab[GR4AD_MAX_LEVELS];
+} gr4ad_dims;
+
+/* Per-layer parameters of decoder_layer (layers.py:66-119), reference layout
+ * (row-vector convention x @ W, W stored (in, out) row-major). */
+typedef struct {
+  const float *ln1_g, *ln1_b;
+  const float *cross_Wq; /* (d, d) */
+  const float *cross_Wo; /* (d, d) */
+  const float *ln2_g, *ln2_b;
+  const float *self_Wqkv; /* (d, 3d) = [Wq | Wk | Wv] */
+  const float *self_Wo;   /* (d, d) */
+  const float *ln3_g, *ln3_b;
+  const float *ffn_W1, *ffn_b1; /* (d, d_ff), (d_ff) */
+  const float *ffn_W2, *ffn_b2; /* (d_ff, d), (d) */
+} gr4ad_layer;
+
+/* DecoderModel.params (decoder.py:71-107), resident per snapshot version. */
+typedef struct {
+  const float *ctx_W, *ctx_b; /* (F, d), (d) */
+  const float *pos;           /* (T+1, d) */
+  const float *bos;           /* (d) */
+  const float *emb[GR4AD_MAX_LEVELS];  /* (V_t, d) */
+  const float *head[GR4AD_MAX_LEVELS]; /* (d, V_t) */
+  const float *head_value;             /* (d, n_value_buckets) */
+  const float *fuse_Wg;                /* (d, d) */
+  const float *fuse_Wf;                /* (2d, d) */
+  const float *cross_kv_W; /* (d, 2*L*d) = [Wk_0 | Wv_0 | Wk_1 | Wv_1 | ...] */
+  gr4ad_layer layer[GR4AD_MAX_LAYERS];
+} gr4ad_weights;
+
+/* One batch of independent requests (one beam_search call each). */
+typedef struct {
+  int n_requests;
+  const int *ctx_len;   /* host [n_requests]: S_b (> 0) */
+  const int *widths;    /* host [n_requests * n_levels]: schedule widths */
+  int trunk_depth;      /* -1: model default; 0 <= K < n_layers otherwise */
+  int value_rerank;     /* beam.py:214-217, 258-288 */
+  const float *value_reps; /* device [n_value_buckets]: EcpmBuckets.representatives,
+                              padded with its last entry (beam.py:281-285) */
+  /* optional valid-SID prefix masking (no reference
+   * counterpart): per level t, sorted unique mixed-radix keys of the valid
+   * (t+1)-token prefixes.  NULL entries disable masking at that level. */
+  const int64_t *valid_prefix[GR4AD_MAX_LEVELS];
+  const int *valid_prefix_count; /* host [n_levels] */
+} gr4ad_batch;
+
+/* Results: for request b, count[b] entries in selection order (or value
+ * re-rank order): tokens[(b*max_out + j)*n_levels + t], score[b*max_out + j].
+ * Scores are the fp32 beam scores widened to double (value re-rank scores are
+ * computed in double, as E[bucket value] * exp(cum) underflows fp32). */
+typedef struct {
+  int max_out;   /* >= max over b of the final (clamped) width */
+  int *count;    /* device [n_requests] */
+  int *tokens;   /* device [n_requests * max_out * n_levels] */
+  double *score; /* device [n_requests * max_out] */
+} gr4ad_results;
+
+int gr4ad_abi_version(void);
+const char *gr4ad_last_error(void);
+const char *gr4ad_status_string(int status);
+
+/* Workspace bytes and the result-row bound (max_out) for a batch. */
+int gr4ad_workspace_bytes(const gr4ad_dims *dims, const gr4ad_batch *batch,
+                          size_t *bytes, int *max_out);
+
+/* Full LazyAR beam decode of a batch (beam.py:112-218 + 258-288 per request):
+ * context projection (decoder.py:134-140) when `features` is non-NULL,
+ * otherwise `context` is the projected X; shared encoder K/V for all layers
+ * (beam.py:98-109); trunk (beam.py:159-163); T level steps; optional value
+ * re-rank.  features: (sum S_b, F); context: (sum S_b, d), row-concatenated
+ * per request.  No host round-trip: every shape is fixed by `batch`. */
+int gr4ad_beam_search(const gr4ad_dims *dims, const gr4ad_weights *w,
+                      const gr4ad_batch *batch, const float *features,
+                      const float *context, gr4ad_results *out, void *workspace,
+                      size_t workspace_bytes, void *stream);
+
+/* Split form for CUDA-graph capture: gr4ad_prepare uploads the batch's
+ * integer plan (row offsets, capacities, ancestor tables) into the
+ * workspace; gr4ad_beam_search_run then issues only kernels (no host
+ * copies, no synchronisation) and may be captured and replayed for any
+ * inputs of the same batch shape. */
+int gr4ad_prepare(const gr4ad_dims *dims, const gr4ad_batch *batch, void *workspace,
+                  size_t workspace_bytes, void *stream);
+int gr4ad_beam_search_run(const gr4ad_dims *dims, const gr4ad_weights *w,
+                          const gr4ad_batch *batch, const float *features,
+                          const float *context, gr4ad_results *out, void *workspace,
+                          size_t workspace_bytes, void *stream);
+
+/* Context projection X = F W_c + b_c (decoder.py:134-140): (rows, F) -> (rows, d). */
+int gr4ad_context_process(const gr4ad_dims *dims, const gr4ad_weights *w,
+                          const float *features, int rows, float *x, void *stream);
+
+/* Shared encoder K/V for layers lo..hi-1 (beam.py:98-109):
+ * kv[(r, 2*(i-lo)+{0,1})] row-major (rows, 2*(hi-lo)*d). */
+int gr4ad_encoder_kv(const gr4ad_dims *dims, const gr4ad_weights *w,
+                     const float *x, int rows, int lo, int hi, float *kv,
+                     void *stream);
+
+/* Batched pre-cut selection (beam.py:50-89 topk_precut/_precut_arrays and
+ * beam.py:37-47 topk_global -- identical results): for problem p,
+ * candidates prev_scores[p*b + i] + logprobs[(p*b + i)*v + j], top k under
+ * (-score, beam, token).  Writes beam/token/score[p*k + j], count[p]. */
+int gr4ad_topk_precut(const float *prev_scores, const float *logprobs,
+                      int n_problems, int b, int v, int k, int *out_beam,
+                      int *out_token, float *out_score, int *out_count,
+                      void *workspace, size_t workspace_bytes, void *stream);
+size_t gr4ad_topk_workspace_bytes(int n_problems, int b, int v);
+
+/* Fused codebook projection + log-softmax + score accumulation + top-k for
+ * one level (beam.py:198-201): states (n_problems*b, d) @ head (d, v),
+ * log-softmax per row, + prev_scores, then top-k as gr4ad_topk_precut. */
+int gr4ad_project_topk(const float *states, const float *head, int d,
+                       const float *prev_scores, int n_problems, int b, int v,
+                       int k, int *out_beam, int *out_token, float *out_score,
+                       int *out_count, void *workspace, size_t workspace_bytes,
+                       void *stream);
+size_t gr4ad_project_topk_workspace_bytes(int n_problems, int b, int v);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GR4AD_H_ */

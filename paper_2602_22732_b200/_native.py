@@ -1,0 +1,110 @@
+"""ctypes binding of libgr4ad.so (include/gr4ad.h).
+
+The product path has no CPU fallback: importing this module raises if the
+sm_100a library is missing, and every entry point raises on a non-OK status
+(``ValueError`` for the reference's argument errors, ``RuntimeError`` for
+CUDA failures) -- mirroring how ``beam_search`` raises (beam.py:125-132).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgr4ad.so")
+
+MAX_LEVELS = 8
+MAX_LAYERS = 32
+MAX_BEAM = 8192
+
+OK, ERR_VALUE, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA = range(5)
+
+EXPORTS = (
+    "gr4ad_abi_version", "gr4ad_last_error", "gr4ad_status_string",
+    "gr4ad_workspace_bytes", "gr4ad_beam_search", "gr4ad_prepare",
+    "gr4ad_beam_search_run", "gr4ad_context_process", "gr4ad_encoder_kv",
+    "gr4ad_topk_precut", "gr4ad_topk_workspace_bytes", "gr4ad_project_topk",
+    "gr4ad_project_topk_workspace_bytes",
+)
+
+_P = C.c_void_p
+
+
+class Dims(C.Structure):
+    _fields_ = [("feat_dim", C.c_int), ("d", C.c_int), ("d_ff", C.c_int),
+                ("n_layers", C.c_int), ("trunk_depth", C.c_int), ("n_levels", C.c_int),
+                ("n_value_buckets", C.c_int), ("vocab", C.c_int * MAX_LEVELS)]
+
+
+class Layer(C.Structure):
+    _fields_ = [(n, _P) for n in (
+        "ln1_g", "ln1_b", "cross_Wq", "cross_Wo", "ln2_g", "ln2_b", "self_Wqkv",
+        "self_Wo", "ln3_g", "ln3_b", "ffn_W1", "ffn_b1", "ffn_W2", "ffn_b2")]
+
+
+class Weights(C.Structure):
+    _fields_ = [("ctx_W", _P), ("ctx_b", _P), ("pos", _P), ("bos", _P),
+                ("emb", _P * MAX_LEVELS), ("head", _P * MAX_LEVELS),
+                ("head_value", _P), ("fuse_Wg", _P), ("fuse_Wf", _P),
+                ("cross_kv_W", _P), ("layer", Layer * MAX_LAYERS)]
+
+
+class Batch(C.Structure):
+    _fields_ = [("n_requests", C.c_int), ("ctx_len", C.POINTER(C.c_int)),
+                ("widths", C.POINTER(C.c_int)), ("trunk_depth", C.c_int),
+                ("value_rerank", C.c_int), ("value_reps", _P),
+                ("valid_prefix", _P * MAX_LEVELS),
+                ("valid_prefix_count", C.POINTER(C.c_int))]
+
+
+class Results(C.Structure):
+    _fields_ = [("max_out", C.c_int), ("count", _P), ("tokens", _P), ("score", _P)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+    lib = C.CDLL(LIB_PATH)
+    for name in EXPORTS:
+        getattr(lib, name)  # AttributeError if an export is missing
+    lib.gr4ad_last_error.restype = C.c_char_p
+    lib.gr4ad_status_string.restype = C.c_char_p
+    lib.gr4ad_status_string.argtypes = [C.c_int]
+    lib.gr4ad_workspace_bytes.argtypes = [C.POINTER(Dims), C.POINTER(Batch),
+                                          C.POINTER(C.c_size_t), C.POINTER(C.c_int)]
+    run_args = [C.POINTER(Dims), C.POINTER(Weights), C.POINTER(Batch), _P, _P,
+                C.POINTER(Results), _P, C.c_size_t, _P]
+    lib.gr4ad_beam_search.argtypes = run_args
+    lib.gr4ad_beam_search_run.argtypes = run_args
+    lib.gr4ad_prepare.argtypes = [C.POINTER(Dims), C.POINTER(Batch), _P, C.c_size_t, _P]
+    lib.gr4ad_context_process.argtypes = [C.POINTER(Dims), C.POINTER(Weights), _P, C.c_int,
+                                          _P, _P]
+    lib.gr4ad_encoder_kv.argtypes = [C.POINTER(Dims), C.POINTER(Weights), _P, C.c_int,
+                                     C.c_int, C.c_int, _P, _P]
+    lib.gr4ad_topk_precut.argtypes = [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P,
+                                      _P, _P, _P, C.c_size_t, _P]
+    lib.gr4ad_topk_workspace_bytes.restype = C.c_size_t
+    lib.gr4ad_topk_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
+    lib.gr4ad_project_topk.argtypes = [_P, _P, C.c_int, _P, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, _P, _P, _P, _P, _P, C.c_size_t, _P]
+    lib.gr4ad_project_topk_workspace_bytes.restype = C.c_size_t
+    lib.gr4ad_project_topk_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
+    if lib.gr4ad_abi_version() != 1:
+        raise ImportError("libgr4ad ABI version mismatch")
+    return lib
+
+
+lib = _load()
+
+
+def check(status):
+    if status == OK:
+        return
+    msg = lib.gr4ad_last_error().decode(errors="replace")
+    if status == ERR_VALUE:
+        raise ValueError(msg)
+    kind = lib.gr4ad_status_string(status).decode()
+    raise RuntimeError(f"libgr4ad: {kind}: {msg}")

@@ -1,0 +1,561 @@
+// C ABI of libgr4ad: batch planning, workspace layout and the per-level
+// orchestration of the LazyAR beam decode (beam.py:112-288).
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace gr {
+
+static thread_local char g_err[512] = "";
+
+int set_err(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// ---------------------------------------------------------------------------
+// plan: every shape of the batch decode, fixed on the host before launch
+// ---------------------------------------------------------------------------
+struct Plan {
+  int B = 0, T = 0, L = 0, K = 0, n_pos = 0, d = 0, dff = 0, F = 0, nb = 0, stride = 0;
+  int V[GR4AD_MAX_LEVELS] = {};
+  int Vmax = 0;
+  long long S_tot = 0;
+  int S_max = 0;
+  bool rerank = false;
+  int n_lv = 0;  // levels with rows: T+1
+  std::vector<int> ctx_off, ctx_len, eff, cap, row_off;
+  long long R[GR4AD_MAX_LEVELS + 1] = {};
+  long long hist_off[GR4AD_MAX_LEVELS + 2] = {};
+  int maxcap[GR4AD_MAX_LEVELS + 1] = {};
+  long long H = 0, Rw = 0;
+  long long max_cand[GR4AD_MAX_LEVELS] = {};
+  int max_out = 0;
+
+  // workspace layout: byte offsets
+  size_t o_ctx_off, o_ctx_len, o_eff, o_cap, o_row_off, o_live, o_row_req;
+  size_t o_trow_off, o_trows, o_trow_req, o_tanc, o_tnpos;
+  size_t o_tok, o_anc, o_cum, o_prefix;
+  size_t o_X, o_KV, o_Ht, o_QKVt;
+  size_t o_Hs, o_N, o_Q, o_A, o_U, o_Fb, o_SC, o_LG, o_rinfo, o_vlog;
+  size_t o_hist;  // (L-K) consecutive (H, 3d) buffers
+  size_t table_bytes, total;
+};
+
+static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
+  if (!dm || !bt) return set_err(GR4AD_ERR_VALUE, "null dims/batch");
+  if (dm->n_levels < 1 || dm->n_levels > GR4AD_MAX_LEVELS)
+    return set_err(GR4AD_ERR_UNSUPPORTED, "n_levels=%d (max %d)", dm->n_levels, GR4AD_MAX_LEVELS);
+  if (dm->n_layers < 1 || dm->n_layers > GR4AD_MAX_LAYERS)
+    return set_err(GR4AD_ERR_UNSUPPORTED, "n_layers=%d (max %d)", dm->n_layers, GR4AD_MAX_LAYERS);
+  if (dm->d < 1 || dm->d_ff < 1 || dm->feat_dim < 1 || dm->n_value_buckets < 1)
+    return set_err(GR4AD_ERR_VALUE, "bad model dimensions");
+  p.B = bt->n_requests;
+  if (p.B < 0) return set_err(GR4AD_ERR_VALUE, "n_requests < 0");
+  p.T = dm->n_levels;
+  p.L = dm->n_layers;
+  p.K = bt->trunk_depth >= 0 ? bt->trunk_depth : dm->trunk_depth;
+  if (!(0 <= p.K && p.K < p.L))
+    return set_err(GR4AD_ERR_VALUE, "trunk_depth must satisfy 0 <= K < n_layers");
+  p.d = dm->d;
+  p.dff = dm->d_ff;
+  p.F = dm->feat_dim;
+  p.nb = dm->n_value_buckets;
+  p.rerank = bt->value_rerank != 0;
+  p.n_pos = p.T + (p.rerank ? 1 : 0);
+  p.stride = p.T + 1;
+  p.n_lv = p.T + 1;
+  for (int t = 0; t < p.T; ++t) {
+    p.V[t] = dm->vocab[t];
+    if (p.V[t] < 1) return set_err(GR4AD_ERR_VALUE, "level_vocab_sizes must be positive");
+    p.Vmax = std::max(p.Vmax, p.V[t]);
+  }
+  const int B = p.B, T = p.T;
+  p.ctx_off.assign(B, 0);
+  p.ctx_len.assign(B, 0);
+  for (int b = 0; b < B; ++b) {
+    int s = bt->ctx_len[b];
+    if (s <= 0) return set_err(GR4AD_ERR_VALUE, "empty context");
+    p.ctx_off[b] = (int)p.S_tot;
+    p.ctx_len[b] = s;
+    p.S_tot += s;
+    p.S_max = std::max(p.S_max, s);
+  }
+  // effective widths (beam.py:134-139) and row capacities per level
+  p.eff.assign((size_t)T * B, 0);
+  p.cap.assign((size_t)(T + 1) * B, 0);
+  p.row_off.assign((size_t)(T + 1) * B, 0);
+  for (int b = 0; b < B; ++b) {
+    long long reach = 1;
+    p.cap[b] = 1;
+    for (int t = 0; t < T; ++t) {
+      int w = bt->widths[(size_t)b * T + t];
+      if (w < 1) return set_err(GR4AD_ERR_VALUE, "beam widths must be positive");
+      reach = std::min(reach * (long long)p.V[t], 1LL << 40);
+      long long e = std::min((long long)w, reach);
+      if (e > GR4AD_MAX_BEAM)
+        return set_err(GR4AD_ERR_UNSUPPORTED, "effective width %lld exceeds %d", e, GR4AD_MAX_BEAM);
+      p.eff[(size_t)t * B + b] = (int)e;
+      long long live = p.cap[(size_t)t * B + b];
+      long long cand = live * p.V[t];
+      if (cand >= 0xFFFFFFFFLL)
+        return set_err(GR4AD_ERR_UNSUPPORTED, "%lld candidates in one request", cand);
+      p.max_cand[t] = std::max(p.max_cand[t], cand);
+      p.cap[(size_t)(t + 1) * B + b] = (int)std::min(e, cand);
+    }
+  }
+  long long h = 0;
+  for (int t = 0; t <= T; ++t) {
+    long long r = 0;
+    int mc = 0;
+    for (int b = 0; b < B; ++b) {
+      p.row_off[(size_t)t * B + b] = (int)r;
+      r += p.cap[(size_t)t * B + b];
+      mc = std::max(mc, p.cap[(size_t)t * B + b]);
+    }
+    p.R[t] = r;
+    p.maxcap[t] = mc;
+    p.hist_off[t] = h;
+    h += r;
+  }
+  p.hist_off[T + 1] = h;
+  p.H = h;
+  p.max_out = p.maxcap[T];
+  long long rw = (long long)B * p.n_pos;
+  for (int t = 0; t < T; ++t) rw = std::max(rw, p.R[t]);
+  if (p.rerank) rw = std::max(rw, p.R[T]);
+  p.Rw = std::max(rw, 1LL);
+  if (p.H >= (1LL << 31) || p.S_tot >= (1LL << 31))
+    return set_err(GR4AD_ERR_UNSUPPORTED, "batch too large");
+
+  // ---- workspace layout ----
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = align_up(o + bytes);
+    return r;
+  };
+  const size_t I = sizeof(int), Fl = sizeof(float);
+  p.o_ctx_off = take(I * B);
+  p.o_ctx_len = take(I * B);
+  p.o_eff = take(I * (size_t)T * B);
+  p.o_cap = take(I * (size_t)(T + 1) * B);
+  p.o_row_off = take(I * (size_t)(T + 1) * B);
+  p.o_live = take(I * (size_t)(T + 1) * B);
+  p.o_row_req = take(I * p.H);
+  p.o_trow_off = take(I * B);
+  p.o_trows = take(I * B);
+  p.o_trow_req = take(I * (size_t)B * p.n_pos);
+  p.o_tanc = take(I * (size_t)B * p.n_pos * p.n_pos);
+  p.o_tnpos = take(I * (size_t)B * p.n_pos);
+  p.table_bytes = o;
+  p.o_tok = take(I * p.H);
+  p.o_anc = take(I * p.H * p.stride);
+  p.o_cum = take(Fl * p.H);
+  p.o_prefix = take(sizeof(long long) * p.H);
+  const size_t d = p.d;
+  p.o_X = take(Fl * p.S_tot * d);
+  p.o_KV = take(Fl * p.S_tot * 2 * p.L * d);
+  p.o_Ht = take(Fl * (size_t)B * p.n_pos * d);
+  p.o_QKVt = take(Fl * (size_t)B * p.n_pos * 3 * d);
+  p.o_Hs = take(Fl * p.Rw * d);
+  p.o_N = take(Fl * p.Rw * d);
+  p.o_Q = take(Fl * p.Rw * d);
+  p.o_A = take(Fl * p.Rw * d);
+  p.o_U = take(Fl * p.Rw * 2 * d);
+  p.o_Fb = take(Fl * p.Rw * p.dff);
+  p.o_SC = take(Fl * p.Rw * p.S_max);
+  p.o_LG = take(Fl * p.Rw * std::max(p.Vmax, p.nb));
+  p.o_rinfo = take(sizeof(float2) * p.Rw);
+  p.o_vlog = take(Fl * std::max(p.R[T], 1LL) * p.nb);
+  p.o_hist = take(Fl * p.H * 3 * d * (size_t)(p.L - p.K));
+  p.total = o;
+  return GR4AD_OK;
+}
+
+template <typename T>
+static T *at(void *ws, size_t off) {
+  return reinterpret_cast<T *>(static_cast<char *>(ws) + off);
+}
+
+static int upload_tables(const Plan &p, void *ws, cudaStream_t st) {
+  const int B = p.B, T = p.T;
+  std::vector<int> host(p.table_bytes / sizeof(int), 0);
+  auto put = [&](size_t off, const int *src, size_t n) {
+    memcpy(reinterpret_cast<char *>(host.data()) + off, src, n * sizeof(int));
+  };
+  put(p.o_ctx_off, p.ctx_off.data(), B);
+  put(p.o_ctx_len, p.ctx_len.data(), B);
+  put(p.o_eff, p.eff.data(), (size_t)T * B);
+  put(p.o_cap, p.cap.data(), (size_t)(T + 1) * B);
+  put(p.o_row_off, p.row_off.data(), (size_t)(T + 1) * B);
+  int *live = reinterpret_cast<int *>(reinterpret_cast<char *>(host.data()) + p.o_live);
+  for (int b = 0; b < B; ++b) live[b] = 1;
+  int *row_req = reinterpret_cast<int *>(reinterpret_cast<char *>(host.data()) + p.o_row_req);
+  for (int t = 0; t <= T; ++t)
+    for (int b = 0; b < B; ++b) {
+      long long g0 = p.hist_off[t] + p.row_off[(size_t)t * B + b];
+      for (int j = 0; j < p.cap[(size_t)t * B + b]; ++j) row_req[g0 + j] = b;
+    }
+  int *trow_off = reinterpret_cast<int *>(reinterpret_cast<char *>(host.data()) + p.o_trow_off);
+  int *trows = reinterpret_cast<int *>(reinterpret_cast<char *>(host.data()) + p.o_trows);
+  int *trow_req = reinterpret_cast<int *>(reinterpret_cast<char *>(host.data()) + p.o_trow_req);
+  int *tanc = reinterpret_cast<int *>(reinterpret_cast<char *>(host.data()) + p.o_tanc);
+  int *tnpos = reinterpret_cast<int *>(reinterpret_cast<char *>(host.data()) + p.o_tnpos);
+  const int np = p.n_pos;
+  for (int b = 0; b < B; ++b) {
+    trow_off[b] = b * np;
+    trows[b] = np;
+    for (int q = 0; q < np; ++q) {
+      int r = b * np + q;
+      trow_req[r] = b;
+      tnpos[r] = q + 1;
+      for (int tau = 0; tau < np; ++tau) tanc[(size_t)r * np + tau] = b * np + std::min(tau, q);
+    }
+  }
+  GR_CUDA(cudaMemcpyAsync(ws, host.data(), p.table_bytes, cudaMemcpyHostToDevice, st));
+  return GR4AD_OK;
+}
+
+__global__ void tile_rows_kernel(const float *src, int n_src, int d, float *dst, long long rows) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * d) return;
+  long long r = i / d;
+  int j = (int)(i - r * d);
+  dst[i] = src[(r % n_src) * d + j];
+}
+
+// one pre-LN decoder layer over a row set (layers.py:66-119)
+struct RowSet {
+  int rows;           // rows in the set
+  int max_group_rows; // max rows of one request
+  const int *g_row_off, *g_rows, *row_req;
+  float *qkv;         // (*, 3d) q/k/v buffer (self-attention history)
+  long long hist_row0;
+  const int *anc;
+  int anc_stride;
+  int npos_u;
+  const int *npos_row;
+};
+
+static int layer_forward(const Plan &p, const gr4ad_weights *w, int i, float *Hs,
+                         const RowSet &rs, void *ws, const float *KV, cudaStream_t st) {
+  const int d = p.d, R = rs.rows;
+  const gr4ad_layer &Lw = w->layer[i];
+  float *N = at<float>(ws, p.o_N), *Q = at<float>(ws, p.o_Q), *A = at<float>(ws, p.o_A);
+  float *SC = at<float>(ws, p.o_SC), *Fb = at<float>(ws, p.o_Fb);
+  const int *ctx_off = at<int>(ws, p.o_ctx_off), *ctx_len = at<int>(ws, p.o_ctx_len);
+  const long long ldkv = 2LL * p.L * d;
+  // cross-attention into the beam-shared context KV (layers.py:82-90)
+  GR_TRY(ln_rows(Hs, d, N, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
+  GR_TRY(gemm(plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), false, EPI_STORE, st));
+  GemmArgs qk{};
+  qk.A = Q; qk.lda = d;
+  qk.B = KV + (size_t)(2 * i) * d; qk.ldb = ldkv;
+  qk.C = SC; qk.ldc = p.S_max;
+  qk.M = rs.max_group_rows; qk.N = p.S_max; qk.K = d;
+  qk.alpha = 1.0f / sqrtf((float)d);
+  qk.groups = p.B; qk.mode = GM_QK;
+  qk.g_row_off = rs.g_row_off; qk.g_rows = rs.g_rows;
+  qk.g_ctx_off = ctx_off; qk.g_ctx_len = ctx_len;
+  GR_TRY(gemm(qk, true, EPI_STORE, st));
+  GR_TRY(softmax_rows(SC, p.S_max, R, rs.row_req, ctx_len, st));
+  GemmArgs pv = qk;
+  pv.A = SC; pv.lda = p.S_max;
+  pv.B = KV + (size_t)(2 * i + 1) * d; pv.ldb = ldkv;
+  pv.C = A; pv.ldc = d;
+  pv.M = rs.max_group_rows; pv.N = d; pv.K = p.S_max;
+  pv.alpha = 1.f; pv.mode = GM_PV;
+  GR_TRY(gemm(pv, false, EPI_STORE, st));
+  GemmArgs o = plain_gemm(A, d, Lw.cross_Wo, d, Hs, d, R, d, d);
+  o.R = Hs; o.ldr = d;
+  GR_TRY(gemm(o, false, EPI_RESID, st));
+  // self-attention over decoded positions (layers.py:92-113)
+  GR_TRY(ln_rows(Hs, d, N, d, Lw.ln2_g, Lw.ln2_b, R, d, st));
+  float *qkv_rows = rs.qkv + rs.hist_row0 * 3 * d;
+  GR_TRY(gemm(plain_gemm(N, d, Lw.self_Wqkv, 3 * d, qkv_rows, 3 * d, R, 3 * d, d), false,
+              EPI_STORE, st));
+  GR_TRY(self_attn(rs.qkv, 3LL * d, d, rs.anc, rs.anc_stride, (int)rs.hist_row0, R,
+                   rs.npos_u, rs.npos_row, A, d, st));
+  GemmArgs so = plain_gemm(A, d, Lw.self_Wo, d, Hs, d, R, d, d);
+  so.R = Hs; so.ldr = d;
+  GR_TRY(gemm(so, false, EPI_RESID, st));
+  // position-wise FFN (layers.py:115-118)
+  GR_TRY(ln_rows(Hs, d, N, d, Lw.ln3_g, Lw.ln3_b, R, d, st));
+  GemmArgs f1 = plain_gemm(N, d, Lw.ffn_W1, p.dff, Fb, p.dff, R, p.dff, d);
+  f1.bias = Lw.ffn_b1;
+  GR_TRY(gemm(f1, false, EPI_BIAS_GELU, st));
+  GemmArgs f2 = plain_gemm(Fb, p.dff, Lw.ffn_W2, d, Hs, d, R, d, p.dff);
+  f2.bias = Lw.ffn_b2; f2.R = Hs; f2.ldr = d;
+  GR_TRY(gemm(f2, false, EPI_BIAS_RESID, st));
+  return GR4AD_OK;
+}
+
+static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
+                    const gr4ad_batch *bt, const float *features, const float *context,
+                    gr4ad_results *out, void *ws, cudaStream_t st) {
+  const int B = p.B, T = p.T, d = p.d, K = p.K;
+  if (B == 0) return GR4AD_OK;
+  int *eff = at<int>(ws, p.o_eff), *cap = at<int>(ws, p.o_cap);
+  int *row_off = at<int>(ws, p.o_row_off), *live = at<int>(ws, p.o_live);
+  int *row_req = at<int>(ws, p.o_row_req);
+  int *tok = at<int>(ws, p.o_tok), *anc = at<int>(ws, p.o_anc);
+  float *cum = at<float>(ws, p.o_cum);
+  long long *prefix = at<long long>(ws, p.o_prefix);
+  float *KV = at<float>(ws, p.o_KV), *Ht = at<float>(ws, p.o_Ht);
+  float *Hs = at<float>(ws, p.o_Hs), *U = at<float>(ws, p.o_U);
+  float *LG = at<float>(ws, p.o_LG);
+  float2 *rinfo = at<float2>(ws, p.o_rinfo);
+  float *hist = at<float>(ws, p.o_hist);
+  const size_t hist_layer = (size_t)p.H * 3 * d;
+
+  // context projection (decoder.py:134-140)
+  const float *X = context;
+  if (features) {
+    float *Xw = at<float>(ws, p.o_X);
+    GemmArgs g = plain_gemm(features, p.F, w->ctx_W, d, Xw, d, (int)p.S_tot, d, p.F);
+    g.bias = w->ctx_b;
+    GR_TRY(gemm(g, false, EPI_BIAS, st));
+    X = Xw;
+  }
+  if (!X) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
+  // encoder K/V of every layer, once per request (beam.py:98-109; layers.py:85-87)
+  GR_TRY(gemm(plain_gemm(X, d, w->cross_kv_W, 2LL * p.L * d, KV, 2LL * p.L * d, (int)p.S_tot,
+                         2 * p.L * d, d),
+              false, EPI_STORE, st));
+  GR_TRY(init_level0(B, live, cum, prefix, anc, p.stride, tok, st));
+
+  // trunk: K layers over the n_pos position rows, shared by all beams (beam.py:159-163)
+  if (K > 0) {
+    long long rows = (long long)B * p.n_pos;
+    tile_rows_kernel<<<ceil_div(rows * d, 256), 256, 0, st>>>(w->pos, p.n_pos, d, Ht, rows);
+    GR_LAUNCH_CHECK();
+    RowSet rs{};
+    rs.rows = (int)rows;
+    rs.max_group_rows = p.n_pos;
+    rs.g_row_off = at<int>(ws, p.o_trow_off);
+    rs.g_rows = at<int>(ws, p.o_trows);
+    rs.row_req = at<int>(ws, p.o_trow_req);
+    rs.qkv = at<float>(ws, p.o_QKVt);
+    rs.hist_row0 = 0;
+    rs.anc = at<int>(ws, p.o_tanc);
+    rs.anc_stride = p.n_pos;
+    rs.npos_row = at<int>(ws, p.o_tnpos);
+    for (int i = 0; i < K; ++i) GR_TRY(layer_forward(p, w, i, Ht, rs, ws, KV, st));
+  }
+
+  const int last = p.rerank ? T : T - 1;
+  for (int t = 0; t <= last; ++t) {
+    const int R = (int)p.R[t];
+    const long long h0 = p.hist_off[t];
+    // token input + gated fusion (beam.py:180-191; layers.py:129-133)
+    const float *emb_prev = t > 0 ? w->emb[t - 1] : nullptr;
+    if (K > 0) {
+      GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, nullptr, U, nullptr, st));
+      GemmArgs gg = plain_gemm(U + d, 2LL * d, w->fuse_Wg, d, U, 2LL * d, R, d, d);
+      gg.vec = Ht + (size_t)t * d;
+      gg.vec_ld = (long long)p.n_pos * d;
+      gg.row_req = row_req + h0;
+      GR_TRY(gemm(gg, false, EPI_MULVEC, st));
+      GR_TRY(gemm(plain_gemm(U, 2LL * d, w->fuse_Wf, d, Hs, d, R, d, 2 * d), false, EPI_STORE,
+                  st));
+    } else {
+      GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, w->pos + (size_t)t * d, nullptr,
+                         Hs, st));
+    }
+    // head layers K..L-1 against the shared context KV (beam.py:243-255)
+    RowSet rs{};
+    rs.rows = R;
+    rs.max_group_rows = p.maxcap[t];
+    rs.g_row_off = row_off + (size_t)t * B;
+    rs.g_rows = cap + (size_t)t * B;
+    rs.row_req = row_req + h0;
+    rs.hist_row0 = h0;
+    rs.anc = anc;
+    rs.anc_stride = p.stride;
+    rs.npos_u = t + 1;
+    rs.npos_row = nullptr;
+    for (int i = K; i < p.L; ++i) {
+      rs.qkv = hist + (size_t)(i - K) * hist_layer;
+      GR_TRY(layer_forward(p, w, i, Hs, rs, ws, KV, st));
+    }
+    if (t == T) {  // value re-rank step (beam.py:258-288)
+      float *vlog = at<float>(ws, p.o_vlog);
+      GR_TRY(gemm(plain_gemm(Hs, d, w->head_value, p.nb, vlog, p.nb, R, p.nb, d), false,
+                  EPI_STORE, st));
+      break;
+    }
+    // codebook projection + log-softmax + score accumulation + top-k (beam.py:198-210)
+    const int V = p.V[t];
+    GR_TRY(gemm(plain_gemm(Hs, d, w->head[t], V, LG, V, R, V, d), false, EPI_STORE, st));
+    GR_TRY(row_lse(LG, V, R, V, rinfo, st));
+    if (bt->valid_prefix[t]) {
+      GR_TRY(mask_rows(LG, V, R, V, prefix + h0,
+                       reinterpret_cast<const long long *>(bt->valid_prefix[t]),
+                       bt->valid_prefix_count[t], st));
+    }
+    SelectArgs sa{};
+    sa.logits = LG; sa.ld = V; sa.V = V; sa.level = t;
+    sa.rowinfo = rinfo; sa.cum = cum;
+    sa.row_off = row_off + (size_t)t * B;
+    sa.live = live + (size_t)t * B;
+    sa.eff = eff + (size_t)t * B;
+    sa.hist_off = (int)h0;
+    sa.out_row_off = row_off + (size_t)(t + 1) * B;
+    sa.out_cap = cap + (size_t)(t + 1) * B;
+    sa.out_live = live + (size_t)(t + 1) * B;
+    sa.out_hist_off = (int)p.hist_off[t + 1];
+    sa.tok = tok; sa.cum_out = cum; sa.prefix = prefix; sa.anc = anc;
+    sa.anc_stride = p.stride;
+    GR_TRY(topk_select(sa, B, 0, 0, p.max_cand[t], st));
+  }
+  GR_TRY(collect_results(B, T, row_off + (size_t)T * B, live + (size_t)T * B,
+                         (int)p.hist_off[T], tok, anc, p.stride, cum,
+                         p.rerank ? at<float>(ws, p.o_vlog) : nullptr, p.nb, bt->value_reps,
+                         out->max_out, out->count, out->tokens, out->score, st));
+  return GR4AD_OK;
+}
+
+}  // namespace gr
+
+using namespace gr;
+
+extern "C" {
+
+int gr4ad_abi_version(void) { return GR4AD_ABI_VERSION; }
+
+const char *gr4ad_last_error(void) { return g_err; }
+
+const char *gr4ad_status_string(int s) {
+  switch (s) {
+    case GR4AD_OK: return "ok";
+    case GR4AD_ERR_VALUE: return "invalid argument";
+    case GR4AD_ERR_UNSUPPORTED: return "unsupported shape";
+    case GR4AD_ERR_WORKSPACE: return "workspace too small";
+    case GR4AD_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+int gr4ad_workspace_bytes(const gr4ad_dims *dims, const gr4ad_batch *batch, size_t *bytes,
+                          int *max_out) {
+  Plan p;
+  GR_TRY(make_plan(dims, batch, p));
+  if (bytes) *bytes = p.total;
+  if (max_out) *max_out = p.max_out;
+  return GR4AD_OK;
+}
+
+int gr4ad_prepare(const gr4ad_dims *dims, const gr4ad_batch *batch, void *workspace,
+                  size_t workspace_bytes, void *stream) {
+  Plan p;
+  GR_TRY(make_plan(dims, batch, p));
+  if (workspace_bytes < p.total)
+    return set_err(GR4AD_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, p.total);
+  return upload_tables(p, workspace, (cudaStream_t)stream);
+}
+
+int gr4ad_beam_search_run(const gr4ad_dims *dims, const gr4ad_weights *w,
+                          const gr4ad_batch *batch, const float *features, const float *context,
+                          gr4ad_results *out, void *workspace, size_t workspace_bytes,
+                          void *stream) {
+  Plan p;
+  GR_TRY(make_plan(dims, batch, p));
+  if (workspace_bytes < p.total)
+    return set_err(GR4AD_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, p.total);
+  if (!out || out->max_out < p.max_out)
+    return set_err(GR4AD_ERR_VALUE, "results.max_out < %d", p.max_out);
+  if (p.rerank && !batch->value_reps)
+    return set_err(GR4AD_ERR_VALUE, "value_rerank requires bucket representatives");
+  return run_plan(p, dims, w, batch, features, context, out, workspace, (cudaStream_t)stream);
+}
+
+int gr4ad_beam_search(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4ad_batch *batch,
+                      const float *features, const float *context, gr4ad_results *out,
+                      void *workspace, size_t workspace_bytes, void *stream) {
+  GR_TRY(gr4ad_prepare(dims, batch, workspace, workspace_bytes, stream));
+  return gr4ad_beam_search_run(dims, w, batch, features, context, out, workspace,
+                               workspace_bytes, stream);
+}
+
+int gr4ad_context_process(const gr4ad_dims *dims, const gr4ad_weights *w, const float *features,
+                          int rows, float *x, void *stream) {
+  GemmArgs g = plain_gemm(features, dims->feat_dim, w->ctx_W, dims->d, x, dims->d, rows,
+                          dims->d, dims->feat_dim);
+  g.bias = w->ctx_b;
+  return gemm(g, false, EPI_BIAS, (cudaStream_t)stream);
+}
+
+int gr4ad_encoder_kv(const gr4ad_dims *dims, const gr4ad_weights *w, const float *x, int rows,
+                     int lo, int hi, float *kv, void *stream) {
+  if (!(0 <= lo && lo <= hi && hi <= dims->n_layers))
+    return set_err(GR4AD_ERR_VALUE, "layer range [%d, %d) outside [0, %d)", lo, hi,
+                   dims->n_layers);
+  const int d = dims->d;
+  const long long ldw = 2LL * dims->n_layers * d;
+  return gemm(plain_gemm(x, d, w->cross_kv_W + (size_t)2 * lo * d, ldw, kv,
+                         2LL * (hi - lo) * d, rows, 2 * (hi - lo) * d, d),
+              false, EPI_STORE, (cudaStream_t)stream);
+}
+
+size_t gr4ad_topk_workspace_bytes(int n_problems, int b, int v) { return 256; }
+
+int gr4ad_topk_precut(const float *prev_scores, const float *logprobs, int n_problems, int b,
+                      int v, int k, int *out_beam, int *out_token, float *out_score,
+                      int *out_count, void *workspace, size_t workspace_bytes, void *stream) {
+  if (n_problems < 0 || b < 1 || v < 1 || k < 1)
+    return set_err(GR4AD_ERR_VALUE, "bad selection shape");
+  long long n = (long long)b * v;
+  if (std::min((long long)k, n) > GR4AD_MAX_BEAM)
+    return set_err(GR4AD_ERR_UNSUPPORTED, "k %d exceeds %d", k, GR4AD_MAX_BEAM);
+  if (n >= 0xFFFFFFFFLL) return set_err(GR4AD_ERR_UNSUPPORTED, "too many candidates");
+  SelectArgs sa{};
+  sa.logits = logprobs; sa.ld = v; sa.V = v;
+  sa.cum = prev_scores;
+  sa.o_beam = out_beam; sa.o_token = out_token; sa.o_score = out_score;
+  sa.o_count = out_count; sa.o_k = k;
+  return topk_select(sa, n_problems, b, k, n, (cudaStream_t)stream);
+}
+
+size_t gr4ad_project_topk_workspace_bytes(int n_problems, int b, int v) {
+  size_t rows = (size_t)n_problems * b;
+  return align_up(rows * v * sizeof(float)) + align_up(rows * sizeof(float2));
+}
+
+int gr4ad_project_topk(const float *states, const float *head, int d, const float *prev_scores,
+                       int n_problems, int b, int v, int k, int *out_beam, int *out_token,
+                       float *out_score, int *out_count, void *workspace,
+                       size_t workspace_bytes, void *stream) {
+  if (n_problems < 0 || b < 1 || v < 1 || k < 1 || d < 1)
+    return set_err(GR4AD_ERR_VALUE, "bad projection shape");
+  if (workspace_bytes < gr4ad_project_topk_workspace_bytes(n_problems, b, v))
+    return set_err(GR4AD_ERR_WORKSPACE, "workspace too small");
+  long long n = (long long)b * v;
+  if (std::min((long long)k, n) > GR4AD_MAX_BEAM)
+    return set_err(GR4AD_ERR_UNSUPPORTED, "k %d exceeds %d", k, GR4AD_MAX_BEAM);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rows = n_problems * b;
+  float *LG = static_cast<float *>(workspace);
+  float2 *ri = reinterpret_cast<float2 *>(static_cast<char *>(workspace) +
+                                          align_up((size_t)rows * v * sizeof(float)));
+  GR_TRY(gemm(plain_gemm(states, d, head, v, LG, v, rows, v, d), false, EPI_STORE, st));
+  GR_TRY(row_lse(LG, v, rows, v, ri, st));
+  SelectArgs sa{};
+  sa.logits = LG; sa.ld = v; sa.V = v;
+  sa.rowinfo = ri; sa.cum = prev_scores;
+  sa.o_beam = out_beam; sa.o_token = out_token; sa.o_score = out_score;
+  sa.o_count = out_count; sa.o_k = k;
+  return topk_select(sa, n_problems, b, k, n, st);
+}
+
+}  // extern "C"

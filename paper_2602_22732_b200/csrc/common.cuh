@@ -1,0 +1,59 @@
+// Shared device helpers for libgr4ad (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+
+#include "gr4ad.h"
+
+namespace gr {
+
+// thread-local error text (the C side keeps no other state)
+int set_err(int code, const char *fmt, ...);
+
+#define GR_TRY(expr)                                                          \
+  do {                                                                        \
+    int _s = (expr);                                                          \
+    if (_s != GR4AD_OK) return _s;                                            \
+  } while (0)
+
+#define GR_CUDA(expr)                                                         \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess)                                                    \
+      return ::gr::set_err(GR4AD_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, \
+                           #expr, cudaGetErrorString(_e));                    \
+  } while (0)
+
+#define GR_LAUNCH_CHECK() GR_CUDA(cudaGetLastError())
+
+// order-preserving float <-> uint32 (larger float -> larger key)
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// tanh-GELU exactly as autodiff.py:301-306 (0.5*a*(1+tanh(c*(a+0.044715 a^3))))
+__device__ __forceinline__ float gelu_tanh(float a) {
+  const float c = 0.7978845608028654f;  // sqrt(2/pi)
+  return 0.5f * a * (1.0f + tanhf((a + 0.044715f * a * a * a) * c));
+}
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace gr

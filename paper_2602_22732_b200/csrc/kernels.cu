@@ -1,0 +1,715 @@
+// Row-wise kernels and the exact per-request top-k of the beam step.
+#include "kernels.cuh"
+
+namespace gr {
+
+// ---------------------------------------------------------------------------
+// LayerNorm (layers.py:38-43): warp per row
+// ---------------------------------------------------------------------------
+__global__ void ln_rows_kernel(const float *__restrict__ x, long long ldx, float *y,
+                               long long ldy, const float *__restrict__ g,
+                               const float *__restrict__ b, int rows, int d) {
+  int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const float *xr = x + (long long)w * ldx;
+  float s = 0.f;
+  for (int j = lane; j < d; j += 32) s += xr[j];
+  float mean = warp_sum(s) / (float)d;
+  float v = 0.f;
+  for (int j = lane; j < d; j += 32) {
+    float c = xr[j] - mean;
+    v += c * c;
+  }
+  float var = warp_sum(v) / (float)d;
+  float inv = 1.0f / sqrtf(var + 1e-5f);
+  float *yr = y + (long long)w * ldy;
+  for (int j = lane; j < d; j += 32) yr[j] = (xr[j] - mean) * inv * g[j] + b[j];
+}
+
+int ln_rows(const float *x, long long ldx, float *y, long long ldy, const float *g,
+            const float *b, int rows, int d, cudaStream_t st) {
+  if (rows <= 0) return GR4AD_OK;
+  ln_rows_kernel<<<ceil_div(rows, 8), 256, 0, st>>>(x, ldx, y, ldy, g, b, rows, d);
+  GR_LAUNCH_CHECK();
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// softmax in place: exp(a - (max + log sum exp(a - max))) (autodiff.py:351-368)
+// ---------------------------------------------------------------------------
+__global__ void softmax_rows_kernel(float *s, long long ld, int rows,
+                                    const int *__restrict__ row_req,
+                                    const int *__restrict__ len) {
+  int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  int n = len[row_req[w]];
+  float *r = s + (long long)w * ld;
+  float mx = -INFINITY;
+  for (int j = lane; j < n; j += 32) mx = fmaxf(mx, r[j]);
+  mx = warp_max(mx);
+  float sum = 0.f;
+  for (int j = lane; j < n; j += 32) sum += expf(r[j] - mx);
+  float lse = logf(warp_sum(sum)) + mx;
+  for (int j = lane; j < n; j += 32) r[j] = expf(r[j] - lse);
+}
+
+int softmax_rows(float *s, long long ld, int rows, const int *row_req, const int *len,
+                 cudaStream_t st) {
+  if (rows <= 0) return GR4AD_OK;
+  softmax_rows_kernel<<<ceil_div(rows, 8), 256, 0, st>>>(s, ld, rows, row_req, len);
+  GR_LAUNCH_CHECK();
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// self-attention over the ancestor chain: block per row
+// ---------------------------------------------------------------------------
+constexpr int kMaxPos = GR4AD_MAX_LEVELS + 1;
+
+__global__ void __launch_bounds__(128)
+self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
+                 const int *__restrict__ anc, int stride, int hist_row0, int rows,
+                 int npos_u, const int *__restrict__ npos_row, float *out,
+                 long long ldo, float scale) {
+  int r = blockIdx.x;
+  if (r >= rows) return;
+  int g = hist_row0 + r;
+  int np = npos_row ? npos_row[r] : npos_u;
+  __shared__ int arow[kMaxPos];
+  __shared__ float red[kMaxPos][4];
+  __shared__ float p[kMaxPos];
+  if (threadIdx.x < np) arow[threadIdx.x] = anc[(long long)g * stride + threadIdx.x];
+  __syncthreads();
+  const float *q = qkv + (long long)g * ld3;
+  float acc[kMaxPos];
+#pragma unroll
+  for (int t = 0; t < kMaxPos; ++t) acc[t] = 0.f;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float qj = q[j];
+#pragma unroll
+    for (int t = 0; t < kMaxPos; ++t)
+      if (t < np) acc[t] = fmaf(qj, qkv[(long long)arow[t] * ld3 + d + j], acc[t]);
+  }
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int t = 0; t < kMaxPos; ++t) {
+    float v = warp_sum(acc[t]);
+    if (lane == 0 && t < np) red[t][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float sc[kMaxPos];
+    float mx = -INFINITY;
+    for (int t = 0; t < np; ++t) {
+      sc[t] = (red[t][0] + red[t][1] + red[t][2] + red[t][3]) * scale;
+      mx = fmaxf(mx, sc[t]);
+    }
+    float sum = 0.f;
+    for (int t = 0; t < np; ++t) sum += expf(sc[t] - mx);
+    float lse = logf(sum) + mx;
+    for (int t = 0; t < np; ++t) p[t] = expf(sc[t] - lse);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float o = 0.f;
+    for (int t = 0; t < np; ++t) o = fmaf(p[t], qkv[(long long)arow[t] * ld3 + 2 * d + j], o);
+    out[(long long)r * ldo + j] = o;
+  }
+}
+
+int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_stride,
+              int hist_row0, int rows, int npos_uniform, const int *npos_row,
+              float *out, long long ldo, cudaStream_t st) {
+  if (rows <= 0) return GR4AD_OK;
+  self_attn_kernel<<<rows, 128, 0, st>>>(qkv, ld3, d, anc, anc_stride, hist_row0, rows,
+                                         npos_uniform, npos_row, out, ldo,
+                                         1.0f / sqrtf((float)d));
+  GR_LAUNCH_CHECK();
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// level input (beam.py:180-191)
+// ---------------------------------------------------------------------------
+__global__ void level_input_kernel(int t, int rows, int d, const float *__restrict__ bos,
+                                   const float *__restrict__ emb_prev,
+                                   const int *__restrict__ tok,
+                                   const float *__restrict__ pos_t, float *U, float *H) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)rows * d) return;
+  int r = (int)(i / d), j = (int)(i - (long long)r * d);
+  float s = (t == 0) ? bos[j] : emb_prev[(long long)tok[r] * d + j];
+  if (U) U[(long long)r * 2 * d + d + j] = s;
+  if (H) H[(long long)r * d + j] = s + pos_t[j];
+}
+
+int level_input(int t, int rows, int d, const float *bos, const float *emb_prev,
+                const int *tok, const float *pos_t, float *U, float *H,
+                cudaStream_t st) {
+  long long n = (long long)rows * d;
+  if (n <= 0) return GR4AD_OK;
+  level_input_kernel<<<ceil_div(n, 256), 256, 0, st>>>(t, rows, d, bos, emb_prev, tok,
+                                                       pos_t, U, H);
+  GR_LAUNCH_CHECK();
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// row (max, log sum exp) (beam.py:92-95): block per row
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128)
+row_lse_kernel(const float *__restrict__ logits, long long ld, int rows, int V,
+               float2 *info) {
+  int r = blockIdx.x;
+  if (r >= rows) return;
+  const float *x = logits + (long long)r * ld;
+  __shared__ float red[4];
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float mx = -INFINITY;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) mx = fmaxf(mx, x[j]);
+  mx = warp_max(mx);
+  if (lane == 0) red[wid] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
+  float s = 0.f;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) s += expf(x[j] - mx);
+  s = warp_sum(s);
+  if (lane == 0) red[wid] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) info[r] = make_float2(mx, logf(red[0] + red[1] + red[2] + red[3]));
+}
+
+int row_lse(const float *logits, long long ld, int rows, int V, float2 *info,
+            cudaStream_t st) {
+  if (rows <= 0) return GR4AD_OK;
+  row_lse_kernel<<<rows, 128, 0, st>>>(logits, ld, rows, V, info);
+  GR_LAUNCH_CHECK();
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// valid-SID prefix mask: block per row
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int lower_bound64(const long long *a, int n, long long key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void mask_rows_kernel(float *logits, long long ld, int rows, int V,
+                                 const long long *__restrict__ prefix,
+                                 const long long *__restrict__ valid, int n_valid) {
+  extern __shared__ unsigned bits[];
+  int r = blockIdx.x;
+  if (r >= rows) return;
+  int words = (V + 31) / 32;
+  for (int i = threadIdx.x; i < words; i += blockDim.x) bits[i] = 0u;
+  __shared__ int lo, hi;
+  long long base = prefix[r] * (long long)V;
+  if (threadIdx.x == 0) {
+    lo = lower_bound64(valid, n_valid, base);
+    hi = lower_bound64(valid, n_valid, base + V);
+  }
+  __syncthreads();
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    int v = (int)(valid[i] - base);
+    atomicOr(&bits[v >> 5], 1u << (v & 31));
+  }
+  __syncthreads();
+  float *x = logits + (long long)r * ld;
+  for (int v = threadIdx.x; v < V; v += blockDim.x)
+    if (!((bits[v >> 5] >> (v & 31)) & 1u)) x[v] = -INFINITY;
+}
+
+int mask_rows(float *logits, long long ld, int rows, int V, const long long *prefix,
+              const long long *valid, int n_valid, cudaStream_t st) {
+  if (rows <= 0) return GR4AD_OK;
+  size_t sm = sizeof(unsigned) * ((V + 31) / 32);
+  mask_rows_kernel<<<rows, 256, sm, st>>>(logits, ld, rows, V, prefix, valid, n_valid);
+  GR_LAUNCH_CHECK();
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// exact per-request top-k under (-score, row, token) (beam.py:30-89)
+//
+// One CTA per request.  Keys are order-preserving uint32 images of the fp32
+// candidate score cum[r] + (logit - max_r) - log_sum_r.  Three radix passes
+// (11/11/10 bits) find the exact k-th key T and how many candidates equal
+// to T must be kept; a collect pass keeps every key > T and the
+// lowest-(row, token) keys == T; a bitonic sort of the k survivors on
+// (key desc, flat index asc) gives the reference order.  When the request's
+// candidate set fits in shared memory the keys are cached there after the
+// first pass.
+// ---------------------------------------------------------------------------
+constexpr int kSelThreads = 1024;
+constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kCacheKeys = 28 * 1024;  // 112 KB of cached keys
+
+struct SelCtx {
+  const float *logits;
+  long long ld;
+  const float2 *rowinfo;
+  const float *cum;
+  int row0, n_rows, V, hist0;
+};
+
+__device__ __forceinline__ uint32_t sel_key(const SelCtx &c, int r, int v, float cr,
+                                            float2 ri) {
+  float lg = c.logits[(long long)(c.row0 + r) * c.ld + v];
+  float lp = c.rowinfo ? ((lg - ri.x) - ri.y) : lg;
+  return f2ord(cr + lp);
+}
+
+template <bool CACHE>
+__device__ void sel_pass_hist(const SelCtx &c, uint32_t *keys, unsigned *hist, int shift,
+                              uint32_t pmask, uint32_t prefix, uint32_t bmask) {
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int cur = -1;
+  unsigned cnt = 0;
+  for (int r = wid; r < c.n_rows; r += kSelWarps) {
+    float cr = 0.f;
+    float2 ri = make_float2(0.f, 0.f);
+    if (!CACHE || shift == 21) {
+      cr = c.cum[c.hist0 + c.row0 + r];
+      if (c.rowinfo) ri = c.rowinfo[c.row0 + r];
+    }
+    for (int v = lane; v < c.V; v += 32) {
+      uint32_t u;
+      long long fi = (long long)r * c.V + v;
+      if (CACHE && shift != 21) {
+        u = keys[fi];
+      } else {
+        u = sel_key(c, r, v, cr, ri);
+        if (CACHE) keys[fi] = u;
+      }
+      if ((u & pmask) == prefix) {
+        int bin = (int)((u >> shift) & bmask);
+        if (bin == cur) {
+          ++cnt;
+        } else {
+          if (cnt) atomicAdd(&hist[cur], cnt);
+          cur = bin;
+          cnt = 1;
+        }
+      }
+    }
+  }
+  if (cnt) atomicAdd(&hist[cur], cnt);
+}
+
+// find bin b with (count of bins above b) < need <= (count above) + hist[b];
+// returns b and writes the count above into *above.
+__device__ int sel_find_bin(unsigned *hist, int nbins, unsigned need, unsigned *above_out,
+                            unsigned *scan) {
+  // suffix sums over bins (descending): scan[i] = sum_{j > i} hist[j]
+  int tid = threadIdx.x;
+  int per = (nbins + kSelThreads - 1) / kSelThreads;  // 2 for 2048 bins
+  unsigned local = 0;
+  for (int i = 0; i < per; ++i) {
+    int b = nbins - 1 - (tid * per + i);
+    if (b >= 0) local += hist[b];
+  }
+  // exclusive scan of `local` over threads in order (block-wide)
+  int lane = tid & 31, wid = tid >> 5;
+  unsigned x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __shared__ unsigned wsum[kSelWarps];
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned s = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    wsum[lane] = s;  // inclusive
+  }
+  __syncthreads();
+  unsigned excl = x - local + (wid > 0 ? wsum[wid - 1] : 0u);
+  unsigned run = excl;
+  for (int i = 0; i < per; ++i) {
+    int b = nbins - 1 - (tid * per + i);
+    if (b >= 0) {
+      unsigned h = hist[b];
+      if (run < need && need <= run + h) {
+        scan[0] = (unsigned)b;
+        scan[1] = run;
+      }
+      run += h;
+    }
+  }
+  __syncthreads();
+  *above_out = scan[1];
+  int b = (int)scan[0];
+  __syncthreads();
+  return b;
+}
+
+template <bool CACHE>
+__global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs a, int u_rows, int u_k) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(smem);  // GR4AD_MAX_BEAM
+  unsigned *hist = reinterpret_cast<unsigned *>(sbuf + GR4AD_MAX_BEAM);    // 2048
+  uint32_t *keys = reinterpret_cast<uint32_t *>(hist + 2048);              // kCacheKeys
+  __shared__ unsigned scan[2];
+  __shared__ unsigned wcnt[kSelWarps];
+  __shared__ unsigned s_gt_pos, s_nfin;
+
+  const int b = blockIdx.x;
+  SelCtx c;
+  c.logits = a.logits;
+  c.ld = a.ld;
+  c.rowinfo = a.rowinfo;
+  c.cum = a.cum;
+  c.V = a.V;
+  c.hist0 = a.hist_off;
+  c.row0 = a.row_off ? a.row_off[b] : b * u_rows;
+  c.n_rows = a.live ? a.live[b] : u_rows;
+  const long long n_cand = (long long)c.n_rows * c.V;
+  int want = a.eff ? a.eff[b] : u_k;
+  const int k = (int)min((long long)want, n_cand);
+  const int tid = threadIdx.x;
+
+  uint32_t T = 0, pmask = 0;
+  unsigned need = (unsigned)k;
+  unsigned eq_total = 0;
+  if (k > 0) {
+    const int shifts[3] = {21, 10, 0};
+    const int widths[3] = {11, 11, 10};
+    for (int pass = 0; pass < 3; ++pass) {
+      int nb = 1 << widths[pass];
+      for (int i = tid; i < nb; i += kSelThreads) hist[i] = 0u;
+      __syncthreads();
+      sel_pass_hist<CACHE>(c, keys, hist, shifts[pass], pmask, T, (uint32_t)(nb - 1));
+      __syncthreads();
+      unsigned above;
+      int bin = sel_find_bin(hist, nb, need, &above, scan);
+      eq_total = hist[bin];
+      need -= above;
+      T |= (uint32_t)bin << shifts[pass];
+      pmask |= (uint32_t)(nb - 1) << shifts[pass];
+      __syncthreads();
+    }
+  }
+  // need = number of keys == T to keep (lowest flat indices); eq_total = all keys == T
+  const bool all_eq = (need == eq_total);
+  const unsigned n_gt = (unsigned)k - need;
+  int wid = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_gt_pos = 0;
+  // per-row ordered tie ranks: rows are visited in order r = wid, wid+32, ...;
+  // pass A counts ties per row (only when some ties must be dropped).
+  // Row counts are kept in the sort buffer tail region (cleared below).
+  unsigned *row_eq = hist;  // reused: per-row tie counts, 2048 rows per chunk
+  const bool ordered = !all_eq && k > 0;
+  __syncthreads();
+  if (k > 0) {
+    if (!ordered) {
+      for (int r = wid; r < c.n_rows; r += kSelWarps) {
+        float cr = 0.f;
+        float2 ri = make_float2(0.f, 0.f);
+        if (!CACHE) {
+          cr = c.cum[c.hist0 + c.row0 + r];
+          if (c.rowinfo) ri = c.rowinfo[c.row0 + r];
+        }
+        for (int v0 = 0; v0 < c.V; v0 += 32) {
+          int v = v0 + lane;
+          uint32_t u = 0;
+          bool in = v < c.V;
+          if (in) u = CACHE ? keys[(long long)r * c.V + v] : sel_key(c, r, v, cr, ri);
+          bool take = in && u >= T;
+          unsigned m = __ballot_sync(0xffffffffu, take);
+          if (m) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(&s_gt_pos, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (take) {
+              unsigned pos = base + __popc(m & ((1u << lane) - 1u));
+              unsigned fi = (unsigned)((long long)r * c.V + v);
+              sbuf[pos] = ((unsigned long long)u << 32) | (0xFFFFFFFFu - fi);
+            }
+          }
+        }
+      }
+    } else {
+      // ordered tie handling: process rows in chunks of 2048 (row_eq counts)
+      unsigned eq_base = 0;  // ties taken by earlier chunks
+      for (int r0 = 0; r0 < c.n_rows; r0 += 2048) {
+        int r1 = min(c.n_rows, r0 + 2048);
+        for (int i = tid; i < 2048; i += kSelThreads) row_eq[i] = 0u;
+        __syncthreads();
+        for (int r = r0 + wid; r < r1; r += kSelWarps) {
+          float cr = 0.f;
+          float2 ri = make_float2(0.f, 0.f);
+          if (!CACHE) {
+            cr = c.cum[c.hist0 + c.row0 + r];
+            if (c.rowinfo) ri = c.rowinfo[c.row0 + r];
+          }
+          unsigned n = 0;
+          for (int v0 = 0; v0 < c.V; v0 += 32) {
+            int v = v0 + lane;
+            uint32_t u = 0;
+            bool in = v < c.V;
+            if (in) u = CACHE ? keys[(long long)r * c.V + v] : sel_key(c, r, v, cr, ri);
+            n += __popc(__ballot_sync(0xffffffffu, in && u == T));
+          }
+          if (lane == 0) row_eq[r - r0] = n;
+        }
+        __syncthreads();
+        // exclusive scan of row_eq[0 .. r1-r0) (serial by thread 0; <= 2048 rows)
+        if (tid == 0) {
+          unsigned run = eq_base;
+          for (int i = 0; i < r1 - r0; ++i) {
+            unsigned h = row_eq[i];
+            row_eq[i] = run;
+            run += h;
+          }
+          scan[0] = run;
+        }
+        __syncthreads();
+        for (int r = r0 + wid; r < r1; r += kSelWarps) {
+          float cr = 0.f;
+          float2 ri = make_float2(0.f, 0.f);
+          if (!CACHE) {
+            cr = c.cum[c.hist0 + c.row0 + r];
+            if (c.rowinfo) ri = c.rowinfo[c.row0 + r];
+          }
+          unsigned rank = row_eq[r - r0];
+          for (int v0 = 0; v0 < c.V; v0 += 32) {
+            int v = v0 + lane;
+            uint32_t u = 0;
+            bool in = v < c.V;
+            if (in) u = CACHE ? keys[(long long)r * c.V + v] : sel_key(c, r, v, cr, ri);
+            bool gt = in && u > T;
+            bool eq = in && u == T;
+            unsigned me = __ballot_sync(0xffffffffu, eq);
+            unsigned myrank = rank + __popc(me & ((1u << lane) - 1u));
+            bool take_eq = eq && myrank < need;
+            unsigned mg = __ballot_sync(0xffffffffu, gt);
+            unsigned base = 0;
+            if (mg) {
+              if (lane == 0) base = atomicAdd(&s_gt_pos, __popc(mg));
+              base = __shfl_sync(0xffffffffu, base, 0);
+            }
+            unsigned fi = (unsigned)((long long)r * c.V + v);
+            if (gt) {
+              unsigned pos = base + __popc(mg & ((1u << lane) - 1u));
+              sbuf[pos] = ((unsigned long long)u << 32) | (0xFFFFFFFFu - fi);
+            }
+            if (take_eq) sbuf[n_gt + myrank] = ((unsigned long long)u << 32) | (0xFFFFFFFFu - fi);
+            rank += __popc(me);
+          }
+        }
+        eq_base = scan[0];
+        __syncthreads();
+      }
+    }
+  }
+  __syncthreads();
+  // bitonic sort of sbuf[0..n2) descending
+  int n2 = 1;
+  while (n2 < k) n2 <<= 1;
+  for (int i = k + tid; i < n2; i += kSelThreads) sbuf[i] = 0ull;
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < n2 / 2; i += kSelThreads) {
+        int lo = 2 * i - (i & (stride - 1));
+        int hi = lo + stride;
+        bool desc = (lo & size) == 0;
+        unsigned long long x = sbuf[lo], y = sbuf[hi];
+        if ((x < y) == desc) {
+          sbuf[lo] = y;
+          sbuf[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // outputs
+  const uint32_t kNegInf = 0x007FFFFFu;  // f2ord(-inf)
+  if (tid == 0) s_nfin = 0;
+  __syncthreads();
+  unsigned nf = 0;
+  for (int j = tid; j < k; j += kSelThreads) nf += ((uint32_t)(sbuf[j] >> 32) != kNegInf);
+  atomicAdd(&s_nfin, nf);
+  __syncthreads();
+  if (a.o_beam) {  // standalone selection: keep -inf like topk_precut
+    for (int j = tid; j < k; j += kSelThreads) {
+      unsigned long long e = sbuf[j];
+      unsigned fi = 0xFFFFFFFFu - (unsigned)(e & 0xFFFFFFFFull);
+      a.o_beam[(long long)b * a.o_k + j] = (int)(fi / c.V);
+      a.o_token[(long long)b * a.o_k + j] = (int)(fi % c.V);
+      a.o_score[(long long)b * a.o_k + j] = ord2f((uint32_t)(e >> 32));
+    }
+    if (tid == 0) a.o_count[b] = k;
+    return;
+  }
+  const int nfin = (int)s_nfin;
+  const int cap = a.out_cap[b];
+  const int orow0 = a.out_row_off[b];
+  const int t = a.level;
+  const int st = a.anc_stride;
+  for (int j = tid; j < cap; j += kSelThreads) {
+    int jj = (j < nfin) ? j : 0;
+    int parent = 0, tok = 0;
+    float sc = -INFINITY;
+    if (nfin > 0) {
+      unsigned long long e = sbuf[jj];
+      unsigned fi = 0xFFFFFFFFu - (unsigned)(e & 0xFFFFFFFFull);
+      parent = (int)(fi / c.V);
+      tok = (int)(fi % c.V);
+      if (j < nfin) sc = ord2f((uint32_t)(e >> 32));
+    }
+    long long gp = (long long)a.hist_off + c.row0 + parent;
+    long long gn = (long long)a.out_hist_off + orow0 + j;
+    a.tok[gn] = tok;
+    a.cum_out[gn] = sc;
+    a.prefix[gn] = a.prefix[gp] * (long long)c.V + tok;
+    for (int tau = 0; tau <= t; ++tau) a.anc[gn * st + tau] = a.anc[gp * st + tau];
+    a.anc[gn * st + t + 1] = (int)gn;
+  }
+  if (tid == 0) a.out_live[b] = nfin;
+}
+
+int topk_select(const SelectArgs &a, int n_requests, int u_rows, int u_k,
+                       long long max_cand, cudaStream_t st) {
+  if (n_requests <= 0) return GR4AD_OK;
+  bool cache = max_cand <= kCacheKeys;
+  size_t sm = sizeof(unsigned long long) * GR4AD_MAX_BEAM + sizeof(unsigned) * 2048 +
+              (cache ? sizeof(uint32_t) * kCacheKeys : 0);
+  if (cache) {
+    GR_CUDA(cudaFuncSetAttribute(topk_select_kernel<true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    topk_select_kernel<true><<<n_requests, kSelThreads, sm, st>>>(a, u_rows, u_k);
+  } else {
+    GR_CUDA(cudaFuncSetAttribute(topk_select_kernel<false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    topk_select_kernel<false><<<n_requests, kSelThreads, sm, st>>>(a, u_rows, u_k);
+  }
+  GR_LAUNCH_CHECK();
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// level-0 rows
+// ---------------------------------------------------------------------------
+__global__ void init_level0_kernel(int B, int *live0, float *cum, long long *prefix, int *anc,
+                                   int stride, int *tok) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  live0[b] = 1;
+  cum[b] = 0.f;
+  prefix[b] = 0;
+  tok[b] = 0;
+  anc[(long long)b * stride] = b;
+}
+
+int init_level0(int n_requests, int *live0, float *cum, long long *prefix, int *anc,
+                int anc_stride, int *tok, cudaStream_t st) {
+  if (n_requests <= 0) return GR4AD_OK;
+  init_level0_kernel<<<ceil_div(n_requests, 256), 256, 0, st>>>(n_requests, live0, cum, prefix,
+                                                                anc, anc_stride, tok);
+  GR_LAUNCH_CHECK();
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// results (beam.py:212-213) + value re-rank (beam.py:258-288): block per request
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512)
+collect_kernel(int T, const int *__restrict__ row_off_T, const int *__restrict__ live_T,
+               int hist_off_T, const int *__restrict__ tok, const int *__restrict__ anc,
+               int stride, const float *__restrict__ cum, const float *__restrict__ vlogits,
+               int nb, const float *__restrict__ reps, int max_out, int *count,
+               int *tokens, double *score) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double *key = reinterpret_cast<double *>(smem);
+  int *idx = reinterpret_cast<int *>(key + GR4AD_MAX_BEAM);
+  const int b = blockIdx.x;
+  const int n = live_T[b];
+  const int row0 = row_off_T[b];
+  const int tid = threadIdx.x;
+  if (tid == 0) count[b] = n;
+  if (!vlogits) {
+    for (int j = tid; j < n; j += blockDim.x) {
+      long long g = (long long)hist_off_T + row0 + j;
+      for (int t = 0; t < T; ++t)
+        tokens[((long long)b * max_out + j) * T + t] = tok[anc[g * stride + t + 1]];
+      score[(long long)b * max_out + j] = (double)cum[g];
+    }
+    return;
+  }
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  for (int j = tid; j < n2; j += blockDim.x) {
+    if (j < n) {
+      const float *lg = vlogits + (long long)(row0 + j) * nb;
+      double mx = -INFINITY;
+      for (int q = 0; q < nb; ++q) mx = fmax(mx, (double)lg[q]);
+      double s = 0.0;
+      for (int q = 0; q < nb; ++q) s += exp((double)lg[q] - mx);
+      double lse = log(s);
+      double ev = 0.0;
+      for (int q = 0; q < nb; ++q) ev += exp(((double)lg[q] - mx) - lse) * (double)reps[q];
+      long long g = (long long)hist_off_T + row0 + j;
+      key[j] = ev * exp((double)cum[g]);
+      idx[j] = j;
+    } else {
+      key[j] = -INFINITY;
+      idx[j] = 0x7fffffff;
+    }
+  }
+  __syncthreads();
+  // bitonic: order by (key desc, idx asc)
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride2 = size >> 1; stride2 > 0; stride2 >>= 1) {
+      for (int i = tid; i < n2 / 2; i += blockDim.x) {
+        int lo = 2 * i - (i & (stride2 - 1));
+        int hi = lo + stride2;
+        bool desc = (lo & size) == 0;
+        double kx = key[lo], ky = key[hi];
+        int ix = idx[lo], iy = idx[hi];
+        bool x_before_y = (kx > ky) || (kx == ky && ix < iy);
+        if (x_before_y != desc) {
+          key[lo] = ky; key[hi] = kx;
+          idx[lo] = iy; idx[hi] = ix;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int j = tid; j < n; j += blockDim.x) {
+    long long g = (long long)hist_off_T + row0 + idx[j];
+    for (int t = 0; t < T; ++t)
+      tokens[((long long)b * max_out + j) * T + t] = tok[anc[g * stride + t + 1]];
+    score[(long long)b * max_out + j] = key[j];
+  }
+}
+
+int collect_results(int n_requests, int T, const int *row_off_T, const int *live_T,
+                    int hist_off_T, const int *tok, const int *anc, int anc_stride,
+                    const float *cum, const float *vlogits, int nb, const float *reps,
+                    int max_out, int *count, int *tokens, double *score, cudaStream_t st) {
+  if (n_requests <= 0) return GR4AD_OK;
+  size_t sm = vlogits ? (sizeof(double) + sizeof(int)) * GR4AD_MAX_BEAM : 0;
+  if (sm) GR_CUDA(cudaFuncSetAttribute(collect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sm));
+  collect_kernel<<<n_requests, 512, sm, st>>>(T, row_off_T, live_T, hist_off_T, tok, anc,
+                                              anc_stride, cum, vlogits, nb, reps, max_out,
+                                              count, tokens, score);
+  GR_LAUNCH_CHECK();
+  return GR4AD_OK;
+}
+
+}  // namespace gr

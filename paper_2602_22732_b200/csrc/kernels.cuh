@@ -1,0 +1,86 @@
+// Row-wise and selection kernels of the beam step (declarations).
+#pragma once
+#include "common.cuh"
+
+namespace gr {
+
+// LN over rows (layers.py:38-43): y = (x - mean) * (var + 1e-5)^-1/2 * g + b
+int ln_rows(const float *x, long long ldx, float *y, long long ldy, const float *g,
+            const float *b, int rows, int d, cudaStream_t st);
+
+// in-place softmax (autodiff.py:362-368) of row r over its first len[req(r)]
+// columns; row_req maps rows to groups.
+int softmax_rows(float *s, long long ld, int rows, const int *row_req,
+                 const int *len, cudaStream_t st);
+
+// self-attention of each row over its ancestor chain (layers.py:101-113 with
+// the history gathered by beam.py:247-248): positions anc[g*stride + tau],
+// tau < npos (npos_row[r] or npos_uniform); q/k/v in a (*, 3d) buffer.
+int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_stride,
+              int hist_row0, int rows, int npos_uniform, const int *npos_row,
+              float *out, long long ldo, cudaStream_t st);
+
+// level input (beam.py:180-191): s = bos (t==0) or emb_{t-1}[tok]; K>0 writes
+// s into U[:, d:2d]; K==0 writes H = s + pos[t].
+int level_input(int t, int rows, int d, const float *bos, const float *emb_prev,
+                const int *tok, const float *pos_t, float *U, float *H,
+                cudaStream_t st);
+
+// per-row (max, log sum exp(x - max)) (beam.py:92-95)
+int row_lse(const float *logits, long long ld, int rows, int V, float2 *info,
+            cudaStream_t st);
+
+// valid-SID prefix mask: logits[r][v] = -inf unless prefix[r]*V + v is a
+// valid key (sorted array). SURVEY §8f row 2 (no reference counterpart).
+int mask_rows(float *logits, long long ld, int rows, int V, const long long *prefix,
+              const long long *valid, int n_valid, cudaStream_t st);
+
+struct SelectArgs {
+  // candidates of level t
+  const float *logits;
+  long long ld;
+  int V;
+  int level;
+  const float2 *rowinfo;  // per level row
+  const float *cum;       // per history row
+  const int *row_off;     // [B] row offset (within level t)
+  const int *live;        // [B] live rows of request (level t)
+  const int *eff;         // [B] effective width
+  int hist_off;           // history row of level row 0
+  // outputs: level t+1
+  const int *out_row_off;  // [B]
+  const int *out_cap;      // [B]
+  int *out_live;           // [B]
+  int out_hist_off;
+  int *tok;                // per history row
+  float *cum_out;          // per history row (== cum buffer)
+  long long *prefix;       // per history row (mixed-radix prefix key)
+  int *anc;                // per history row * anc_stride
+  int anc_stride;
+  // standalone (gr4ad_topk_precut) outputs, used when tok == nullptr
+  int *o_beam, *o_token;
+  float *o_score;
+  int *o_count;
+  int o_k;
+  // scratch: per-request candidate buffer for large candidate sets
+  unsigned long long *scratch;
+  long long scratch_per_req;
+};
+
+// u_rows/u_k: uniform rows and k per request when row_off/live/eff are NULL;
+// max_cand: max candidates of one request (decides the shared-memory key cache)
+int topk_select(const SelectArgs &a, int n_requests, int u_rows, int u_k,
+                long long max_cand, cudaStream_t st);
+
+// level-0 rows: live=1, cum=0, prefix=0, anc[g][0]=g
+int init_level0(int n_requests, int *live0, float *cum, long long *prefix, int *anc,
+                int anc_stride, int *tok, cudaStream_t st);
+
+// results (beam.py:212-213) and value re-rank (beam.py:258-288)
+int collect_results(int n_requests, int T, const int *row_off_T, const int *live_T,
+                    int hist_off_T, const int *tok, const int *anc, int anc_stride,
+                    const float *cum, const float *vlogits, int nb,
+                    const float *reps, int max_out, int *count, int *tokens,
+                    double *score, cudaStream_t st);
+
+}  // namespace gr

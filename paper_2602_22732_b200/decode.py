@@ -1,0 +1,150 @@
+"""Batched LazyAR beam decode on one GPU (the engine under ``beam_search``).
+
+A :class:`BeamDecoder` owns one batch shape -- request count, context
+lengths and per-request width schedules (DBS widths may differ per
+request) -- and the device buffers for it: the workspace sized by
+``gr4ad_workspace_bytes`` and the result arrays.  ``run`` issues the whole
+decode (encoder K/V, trunk, T level steps, top-k + in-place compaction,
+optional value re-rank) on the current stream with no host round-trip, so
+it can be captured once into a CUDA graph and replayed per batch.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .device import _stream_handle, device_weights, dims_of, require_cuda
+
+
+def effective_widths(widths, vocab_sizes):
+    """Width clamp to the reachable prefix count (beam.py:134-139)."""
+    eff, reach = [], 1
+    for w, v in zip(widths, vocab_sizes):
+        reach = min(reach * v, 1 << 40)
+        eff.append(min(int(w), reach))
+    return eff
+
+
+def live_rows(eff, vocab_sizes):
+    """Rows entering each level (and surviving the last), no masking."""
+    live = [1]
+    for e, v in zip(eff, vocab_sizes):
+        live.append(min(e, live[-1] * v))
+    return live
+
+
+def prefix_keys(valid_sids, vocab_sizes):
+    """Per level t: sorted unique mixed-radix keys of valid (t+1)-prefixes."""
+    T = len(vocab_sizes)
+    keys = [set() for _ in range(T)]
+    for sid in valid_sids:
+        toks = getattr(sid, "tokens", sid)
+        k = 0
+        for t in range(T):
+            k = k * int(vocab_sizes[t]) + int(toks[t])
+            keys[t].add(k)
+    return [np.array(sorted(s), dtype=np.int64) for s in keys]
+
+
+class BeamDecoder:
+    def __init__(self, model, ctx_lens, widths, trunk_depth=None, value_rerank=False,
+                 representatives=None, valid_sids=None, device=None):
+        self.device = require_cuda(device)
+        cfg = model.config
+        self.cfg = cfg
+        self.T = cfg.n_levels
+        self.weights = device_weights(model, self.device)
+        self.dims = dims_of(cfg)
+        B = len(ctx_lens)
+        self.n_requests = B
+        self.ctx_lens = [int(s) for s in ctx_lens]
+        w = np.asarray(widths, dtype=np.int32).reshape(B, self.T)
+        self.widths = w
+        self._ctx = (C.c_int * max(B, 1))(*self.ctx_lens)
+        self._w = (C.c_int * max(B * self.T, 1))(*w.ravel().tolist())
+        bt = N.Batch()
+        bt.n_requests = B
+        bt.ctx_len = self._ctx
+        bt.widths = self._w
+        bt.trunk_depth = -1 if trunk_depth is None else int(trunk_depth)
+        bt.value_rerank = 1 if value_rerank else 0
+        self._keep = []
+        if value_rerank:
+            if representatives is None:
+                raise ValueError("value_rerank requires buckets (representatives)")
+            reps = np.asarray(representatives, dtype=np.float64).ravel()
+            nb = cfg.n_value_buckets
+            if reps.size < nb:  # beam.py:281-284
+                reps = np.concatenate([reps, np.full(nb - reps.size, reps[-1])])
+            rt = torch.from_numpy(reps[:nb].astype(np.float32)).to(self.device)
+            self._keep.append(rt)
+            bt.value_reps = C.c_void_p(rt.data_ptr())
+        self._vcount = (C.c_int * N.MAX_LEVELS)()
+        if valid_sids is not None:
+            for t, keys in enumerate(prefix_keys(valid_sids, cfg.level_vocab_sizes)):
+                kt = torch.from_numpy(keys if keys.size else np.zeros(1, np.int64)).to(self.device)
+                self._keep.append(kt)
+                bt.valid_prefix[t] = C.c_void_p(kt.data_ptr())
+                self._vcount[t] = int(keys.size)
+        bt.valid_prefix_count = self._vcount
+        self.batch = bt
+        nbytes, max_out = C.c_size_t(), C.c_int()
+        N.check(N.lib.gr4ad_workspace_bytes(C.byref(self.dims), C.byref(bt), C.byref(nbytes),
+                                            C.byref(max_out)))
+        self.workspace_bytes = nbytes.value
+        self.max_out = max(max_out.value, 1)
+        self.workspace = torch.empty(max(self.workspace_bytes, 256), dtype=torch.uint8,
+                                     device=self.device)
+        self.count = torch.zeros(max(B, 1), dtype=torch.int32, device=self.device)
+        self.tokens = torch.zeros(max(B, 1) * self.max_out * self.T, dtype=torch.int32,
+                                  device=self.device)
+        self.score = torch.zeros(max(B, 1) * self.max_out, dtype=torch.float64,
+                                 device=self.device)
+        res = N.Results()
+        res.max_out = self.max_out
+        res.count = C.c_void_p(self.count.data_ptr())
+        res.tokens = C.c_void_p(self.tokens.data_ptr())
+        res.score = C.c_void_p(self.score.data_ptr())
+        self.results_struct = res
+        N.check(N.lib.gr4ad_prepare(C.byref(self.dims), C.byref(bt),
+                                    C.c_void_p(self.workspace.data_ptr()),
+                                    self.workspace_bytes, _stream_handle(self.device)))
+        self.graph = None
+        self._graph_inputs = None
+
+    # -- launch ----------------------------------------------------------
+    def run(self, features=None, context=None):
+        """features: (sum S, feat_dim) fp32 CUDA tensor, or context: (sum S, d)."""
+        f = C.c_void_p(features.data_ptr()) if features is not None else None
+        x = C.c_void_p(context.data_ptr()) if context is not None else None
+        N.check(N.lib.gr4ad_beam_search_run(
+            C.byref(self.dims), C.byref(self.weights.struct), C.byref(self.batch), f, x,
+            C.byref(self.results_struct), C.c_void_p(self.workspace.data_ptr()),
+            self.workspace_bytes, _stream_handle(self.device)))
+
+    def capture(self, features=None, context=None, warmup=1):
+        """Capture ``run`` on static input tensors into a CUDA graph."""
+        for _ in range(warmup):
+            self.run(features, context)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run(features, context)
+        self.graph = g
+        self._graph_inputs = (features, context)
+        return g
+
+    def replay(self):
+        self.graph.replay()
+
+    # -- results -----------------------------------------------------------
+    def host_results(self):
+        count = self.count.cpu().numpy()[: self.n_requests]
+        toks = self.tokens.cpu().numpy().reshape(-1, self.max_out, self.T)
+        score = self.score.cpu().numpy().reshape(-1, self.max_out)
+        return [[(tuple(int(v) for v in toks[b, j]), float(score[b, j]))
+                 for j in range(int(count[b]))] for b in range(self.n_requests)]
