@@ -1,0 +1,470 @@
+"""GR4AD LazyAR beam-serving benchmark (BASELINE.json metric:
+requests/sec and p50/p99 latency per request (top-K SIDs) vs roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3]
+    python bench.py --impl reference ...        # reference CPU path (oracle port)
+
+A step is one batched decode of one batch of synthetic requests (SURVEY
+§8d): random-init weights (DecoderModel(cfg), seed 2) and i.i.d. N(0,1)
+features, one batch per GPU (weak scaling: the per-GPU batch is fixed).
+`value` times the decode with inputs resident in HBM (CUDA-graph replay,
+L2 flushed between steps); `e2e` times the C-ABI path with host buffers:
+pinned features -> device, decode, results -> pinned host, every step.
+Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # SURVEY §8d.  model: (feat_dim, d, d_ff, L, K, vocab, n_buckets); S; widths; batch
+    "c1": dict(model=(16, 16, 32, 2, 1, (256, 256, 256), 4), S=256, widths=(32, 32, 32),
+               batch=64, name="C1: small LazyAR d16/L2/K1, V=256^3, S=256, beam 32, batch 64"),
+    "c2": dict(model=(16, 16, 32, 2, 1, (256, 256, 256), 4), S=256, widths=(64, 128, 256),
+               batch=512, name="C2: small LazyAR d16/L2/K1, V=256^3, S=256, DBW 64->128->256, "
+                               "batch 512"),
+    "c3": dict(model=(16, 1024, 2048, 8, 5, (4096, 4096, 4096), 4), S=1024,
+               widths=(512, 512, 512), batch=256,
+               name="C3: LazyAR d1024/L8/K5, V=4096^3, S=1024, beam 512, batch 256"),
+}
+
+
+def _flops_per_request(cfg, S, widths):
+    """SURVEY §8d algorithmic FLOPs per request (live rows only)."""
+    F, d, dff, L, K, V, _ = cfg
+    T = len(V)
+    eff, reach = [], 1
+    for w, v in zip(widths, V):
+        reach *= v
+        eff.append(min(w, reach))
+    rows = [1]
+    for e, v in zip(eff, V):
+        rows.append(min(e, rows[-1] * v))
+    fl = 2 * S * F * d + 4 * L * S * d * d
+    fl += T * K * 2 * (6 * d * d + 2 * S * d + 2 * d * dff)
+    for t in range(T):
+        r = rows[t]
+        fl += r * (6 * d * d + (L - K) * 2 * (6 * d * d + 2 * S * d + 2 * d * dff
+                                              + 2 * (t + 1) * d) + 2 * d * V[t])
+    return fl
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7
+                          for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle port of the reference CPU path
+# ---------------------------------------------------------------------------
+
+def _oracle_worker(args):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    cfgt, S, widths, ids = args
+    from oracle import beam_oracle as orc
+    cfg = orc.OracleConfig(*cfgt[:6], cfgt[6], seed=2)
+    params = _oracle_params(cfg)
+    out = []
+    for i in ids:
+        f = np.random.default_rng(1000 + i).normal(size=(S, cfg.feat_dim))
+        t0 = time.perf_counter()
+        orc.beam_search(params, cfg, orc.context_process(f, params), widths)
+        out.append(time.perf_counter() - t0)
+    return out
+
+
+_PARAMS = {}
+
+
+def _oracle_params(cfg):
+    from oracle import beam_oracle as orc
+    key = cfg
+    if key not in _PARAMS:
+        _PARAMS[key] = orc.init_params(cfg)
+    return _PARAMS[key]
+
+
+def _pool_init():
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+
+
+def cpu_reference_run(cfgd, n_requests, cores):
+    """Time the oracle port over n_requests with `cores` processes."""
+    import multiprocessing as mp
+    ids = list(range(n_requests))
+    chunks = [ids[i::cores] for i in range(cores)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_pool_init) as pool:
+        # warm the per-process weight init outside the timed region
+        pool.map(_oracle_worker, [(cfgd["model"], cfgd["S"], cfgd["widths"], [])] * cores)
+        t0 = time.perf_counter()
+        lat = pool.map(_oracle_worker, [(cfgd["model"], cfgd["S"], cfgd["widths"], c)
+                                        for c in chunks if c])
+        dt = time.perf_counter() - t0
+    lat = [x for part in lat for x in part]
+    return n_requests / dt, dt, lat
+
+
+def run_reference(args, cfgd):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    # size a step to ~5-20 s of CPU work: probe one request single-threaded
+    _pool_init()
+    probe = _oracle_worker((cfgd["model"], cfgd["S"], cfgd["widths"], [0]))[0]
+    step_s = min(8.0, max(1.0, 120.0 / max(args.steps, 1)))
+    per_step = max(cores, int(round(step_s * cores / max(probe, 1e-3))))
+    per_step = min(per_step, 64 * cores)
+    if args.config == "c3":
+        per_step = cores
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_reference_run(cfgd, cores, cores)
+    rates, lats = [], []
+    for _ in range(args.steps):
+        r, _, lat = cpu_reference_run(cfgd, per_step, cores)
+        rates.append(r)
+        lats.extend(lat)
+    value = statistics.mean(rates)
+    sample = f"{per_step} requests/step x {args.steps} steps, {cores} processes x 1 BLAS thread"
+    line = {"metric": "requests/sec", "value": value, "unit": "req/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * per_step / value, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfgd["name"], "batch": per_step,
+                       "parallelism": f"cpu x{cores}"},
+            "latency_ms": {"p50": 1000 * float(np.percentile(lats, 50)),
+                           "p99": 1000 * float(np.percentile(lats, 99))},
+            "cpu_baseline": {"value": value, "unit": "req/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "req/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# roofline of the dominant kernel (live CUDA-event timing per kernel class)
+# ---------------------------------------------------------------------------
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained"), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def class_work(cfgd):
+    """Algorithmic work per decode of one batch, per kernel class:
+    ('flop', n) or ('byte', n).  Live rows only."""
+    F, d, dff, L, K, V, nb = cfgd["model"]
+    B, S, widths = cfgd["batch"], cfgd["S"], cfgd["widths"]
+    T = len(V)
+    eff, reach = [], 1
+    for w, v in zip(widths, V):
+        reach *= v
+        eff.append(min(w, reach))
+    rows = [1]
+    for e, v in zip(eff, V):
+        rows.append(min(e, rows[-1] * v))
+    R = [B * r for r in rows]
+    n_trunk = B * T if K > 0 else 0
+    head_rows = sum(R[:T])
+    layer_rows = K * n_trunk + (L - K) * head_rows
+    gemm = B * (2 * S * F * d + 4 * L * S * d * d) + layer_rows * (12 * d * d + 4 * d * dff)
+    gemm += sum(R[t] * ((6 * d * d if K > 0 else 0) + 2 * d * V[t]) for t in range(T))
+    attn = layer_rows * 4 * S * d
+    topk = sum(R[t] * V[t] * 4 + R[t] * 12 + R[t + 1] * (20 + 8 * (t + 2)) for t in range(T))
+    soft = layer_rows * S * 8
+    ln = layer_rows * 3 * 8 * d
+    sattn = K * n_trunk * 4 * (2 * d + 2 * d * T) + (L - K) * sum(
+        R[t] * 4 * (2 * d + 2 * d * (t + 1)) for t in range(T))
+    lse = sum(R[t] * (V[t] * 4 + 8) for t in range(T))
+    return {"gemm": ("flop", gemm), "attn_gemm": ("flop", attn), "topk_select": ("byte", topk),
+            "softmax": ("byte", soft), "layernorm": ("byte", ln), "self_attn": ("byte", sattn),
+            "row_lse": ("byte", lse)}
+
+
+def roofline_for(dec, feats, cfgd, dev):
+    import ctypes as C
+
+    import torch
+
+    from paper_2602_22732_b200 import _native as N
+    nk = len(N.KERNEL_CLASSES)
+    ms = (C.c_double * nk)()
+    cnt = (C.c_longlong * nk)()
+    reps = 3
+    for _ in range(reps):
+        dec.run(features=feats)  # warm, outside the profiled window
+    torch.cuda.synchronize(dev)
+    N.lib.gr4ad_profile_begin()
+    for _ in range(reps):
+        dec.run(features=feats)
+    N.check(N.lib.gr4ad_profile_end(ms, cnt, nk))
+    total = sum(ms[i] for i in range(nk))
+    work = class_work(cfgd)
+    hbm, bf16, bf16_sus, src = _peaks()
+    classes = {}
+    for i, name in enumerate(N.KERNEL_CLASSES):
+        if cnt[i] == 0:
+            continue
+        rec = {"ms_per_step": ms[i] / reps, "share": ms[i] / total if total else 0.0,
+               "launches_per_step": cnt[i] // reps}
+        if name in work:
+            kind, amount = work[name]
+            if kind == "flop":
+                rec["achieved_tflops"] = amount / (ms[i] / reps / 1e3) / 1e12
+            else:
+                rec["achieved_gbs"] = amount / (ms[i] / reps / 1e3) / 1e9
+        classes[name] = rec
+    dom = max(classes, key=lambda k: classes[k]["ms_per_step"])
+    rec = classes[dom]
+    kind, amount = work.get(dom, ("byte", 0))
+    per_launch_s = rec["ms_per_step"] / 1e3 / max(rec["launches_per_step"], 1)
+    per_launch = amount / max(rec["launches_per_step"], 1)
+    if kind == "flop":
+        achieved = per_launch / per_launch_s / 1e12
+        peak, unit, bound = bf16, "TFLOP/s", "tensor"
+    else:
+        achieved = per_launch / per_launch_s / 1e9
+        peak, unit, bound = hbm, "GB/s", "hbm"
+    return {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "traffic": None, "peak_source": src,
+            "algorithmic_per_launch": per_launch, "launch_ms": per_launch_s * 1e3,
+            "classes": classes,
+            "note": "fp32 CUDA-core path: GEMM classes are reported against the bf16 "
+                    "tensor peak; per-class times are CUDA events on the launching stream"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    args = ap.parse_args()
+    cfgd = dict(CONFIGS[args.config])
+    if args.batch:
+        cfgd["batch"] = args.batch
+    if args.impl == "reference":
+        run_reference(args, cfgd)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2602_22732_b200 import _native as N
+    from paper_2602_22732_b200.decode import BeamDecoder
+    from paper_2602_22732_b200.model import DecoderConfig, DecoderModel
+
+    F, d, dff, L, K, V, nb = cfgd["model"]
+    cfg = DecoderConfig(F, d, dff, L, K, V, nb, seed=2)
+    model = DecoderModel(cfg)
+    B, S, widths = cfgd["batch"], cfgd["S"], cfgd["widths"]
+    dec = BeamDecoder(model, [S] * B, [widths] * B, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    feats = torch.randn((B * S, F), generator=gen, device=dev, dtype=torch.float32)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    N.lib.gr4ad_take_launch_count()
+    dec.run(features=feats)
+    launches_per_step = int(N.lib.gr4ad_take_launch_count())
+    torch.cuda.synchronize(dev)
+    if not args.no_graph:
+        dec.capture(features=feats)
+    step = dec.replay if not args.no_graph else (lambda: dec.run(features=feats))
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- device-resident throughput ------------------------------------
+    clocks = ClockSampler(local)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()
+        starts[i].record()
+        step()
+        ends[i].record()
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tot_ms = torch.tensor([sum(step_ms)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(tot_ms.item()) / args.steps
+    value = world * B / (ms_per_step / 1000.0)
+
+    # ---- end to end through the C ABI with host buffers --------------------
+    host_f = feats.cpu().pin_memory()
+    h_count = torch.empty_like(dec.count, device="cpu").pin_memory()
+    h_tok = torch.empty_like(dec.tokens, device="cpu").pin_memory()
+    h_score = torch.empty_like(dec.score, device="cpu").pin_memory()
+    h2d = host_f.numel() * host_f.element_size()
+    d2h = sum(t.numel() * t.element_size() for t in (h_count, h_tok, h_score))
+
+    def e2e_step():
+        feats.copy_(host_f, non_blocking=True)
+        step()
+        h_count.copy_(dec.count, non_blocking=True)
+        h_tok.copy_(dec.tokens, non_blocking=True)
+        h_score.copy_(dec.score, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    if world > 1:
+        dist.barrier()
+    lat = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        e2e_step()
+        lat.append(time.perf_counter() - t0)
+    e2e_tot = torch.tensor([sum(lat)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * args.steps / float(e2e_tot.item())
+    clk = clocks.stop()
+
+    # ---- results sanity (gathered: NCCL only moves results/stats) ------------
+    cnt = dec.count[:B].to(torch.int64).sum().reshape(1)
+    if world > 1:
+        dist.all_reduce(cnt)
+    flops = _flops_per_request(cfgd["model"], S, widths)
+
+    line = None
+    if rank == 0:
+        roof = roofline_for(dec, feats, cfgd, dev)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cores = os.cpu_count() or 1
+            n = cores * (8 if args.config != "c3" else 1)
+            if args.config == "c3":
+                n = cores
+            rate, dt, _ = cpu_reference_run(cfgd, n, cores)
+            cpu = {"value": rate, "unit": "req/s", "cores": cores, "kind": "port",
+                   "sample": f"{n} {args.config.upper()} requests (oracle port, float64 numpy, "
+                             f"{cores} processes x 1 BLAS thread), {dt:.1f} s"}
+        line = {
+            "metric": "requests/sec", "value": value, "unit": "req/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (random-init weights seed 2, N(0,1) features)",
+            "config": {"workload": cfgd["name"], "batch_per_gpu": B, "global_batch": B * world,
+                       "ctx_len": S, "widths": list(widths),
+                       "parallelism": f"user-sharded x{world} (replicas, no data-path collective)",
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "cuda_graph": not args.no_graph},
+            "latency_ms": {"p50": 1000 * float(np.percentile(lat, 50)),
+                           "p99": 1000 * float(np.percentile(lat, 99)),
+                           "note": "e2e batch latency (every request of a batch completes "
+                                   "together)"},
+            "device_step_ms": {"p50": float(np.percentile(step_ms, 50)),
+                               "p99": float(np.percentile(step_ms, 99))},
+            "e2e": {"value": e2e_value, "unit": "req/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches_per_step * args.steps,
+            "launches_per_step": launches_per_step,
+            "algorithmic_tflops": flops * value / 1e12,
+            "results_per_step": int(cnt.item()),
+            "clocks": clk,
+            "wall_s_timed": wall,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -114,6 +114,17 @@ typedef struct {
 int gr4ad_abi_version(void);
 const char *gr4ad_last_error(void);
 const char *gr4ad_status_string(int status);
+/* Kernel launches issued by the calling thread since the last call (the
+ * bench's gpu_launches evidence; thread-local like the error text). */
+long long gr4ad_take_launch_count(void);
+
+/* Live per-kernel-class timing for the bench's roofline: between begin and
+ * end every launch made by the calling thread is bracketed by CUDA events on
+ * its stream; end() synchronises and returns per-class total ms and launch
+ * counts.  Classes: 0 gemm, 1 attention gemm, 2 top-k, 3 softmax,
+ * 4 layernorm, 5 self-attention, 6 row log-sum-exp, 7 small, 8 collect. */
+void gr4ad_profile_begin(void);
+int gr4ad_profile_end(double *ms, long long *launches, int n_classes);
 
 /* Workspace bytes and the result-row bound (max_out) for a batch. */
 int gr4ad_workspace_bytes(const gr4ad_dims *dims, const gr4ad_batch *batch,

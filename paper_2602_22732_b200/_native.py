@@ -20,8 +20,12 @@ MAX_BEAM = 8192
 
 OK, ERR_VALUE, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA = range(5)
 
+KERNEL_CLASSES = ("gemm", "attn_gemm", "topk_select", "softmax", "layernorm", "self_attn",
+                  "row_lse", "small", "collect")
+
 EXPORTS = (
     "gr4ad_abi_version", "gr4ad_last_error", "gr4ad_status_string",
+    "gr4ad_take_launch_count", "gr4ad_profile_begin", "gr4ad_profile_end",
     "gr4ad_workspace_bytes", "gr4ad_beam_search", "gr4ad_prepare",
     "gr4ad_beam_search_run", "gr4ad_context_process", "gr4ad_encoder_kv",
     "gr4ad_topk_precut", "gr4ad_topk_workspace_bytes", "gr4ad_project_topk",
@@ -73,6 +77,8 @@ def _load():
     lib.gr4ad_last_error.restype = C.c_char_p
     lib.gr4ad_status_string.restype = C.c_char_p
     lib.gr4ad_status_string.argtypes = [C.c_int]
+    lib.gr4ad_take_launch_count.restype = C.c_longlong
+    lib.gr4ad_profile_end.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.c_int]
     lib.gr4ad_workspace_bytes.argtypes = [C.POINTER(Dims), C.POINTER(Batch),
                                           C.POINTER(C.c_size_t), C.POINTER(C.c_int)]
     run_args = [C.POINTER(Dims), C.POINTER(Weights), C.POINTER(Batch), _P, _P,

@@ -12,6 +12,31 @@
 namespace gr {
 
 static thread_local char g_err[512] = "";
+static thread_local long long g_launches = 0;
+
+void count_launch() { ++g_launches; }
+
+// live per-class kernel timing: CUDA events recorded on the launching stream
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+};
+static thread_local bool g_prof_on = false;
+static thread_local std::vector<ProfRec> *g_prof = nullptr;
+
+void prof_begin(int cls, cudaStream_t st) {
+  if (!g_prof_on) return;
+  ProfRec r{cls, nullptr, nullptr};
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, st);
+  g_prof->push_back(r);
+}
+
+void prof_end(int cls, cudaStream_t st) {
+  if (!g_prof_on || g_prof->empty()) return;
+  cudaEventRecord(g_prof->back().b, st);
+}
 
 int set_err(int code, const char *fmt, ...) {
   va_list ap;
@@ -338,8 +363,7 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
   // trunk: K layers over the n_pos position rows, shared by all beams (beam.py:159-163)
   if (K > 0) {
     long long rows = (long long)B * p.n_pos;
-    tile_rows_kernel<<<ceil_div(rows * d, 256), 256, 0, st>>>(w->pos, p.n_pos, d, Ht, rows);
-    GR_LAUNCH_CHECK();
+    GR_LAUNCH(KC_SMALL, st, tile_rows_kernel<<<ceil_div(rows * d, 256), 256, 0, st>>>(w->pos, p.n_pos, d, Ht, rows));
     RowSet rs{};
     rs.rows = (int)rows;
     rs.max_group_rows = p.n_pos;
@@ -435,6 +459,44 @@ extern "C" {
 int gr4ad_abi_version(void) { return GR4AD_ABI_VERSION; }
 
 const char *gr4ad_last_error(void) { return g_err; }
+
+void gr4ad_profile_begin(void) {
+  if (!g_prof) g_prof = new std::vector<ProfRec>();
+  for (auto &r : *g_prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof->clear();
+  g_prof_on = true;
+}
+
+int gr4ad_profile_end(double *ms, long long *launches, int n_classes) {
+  g_prof_on = false;
+  for (int c = 0; c < n_classes; ++c) {
+    ms[c] = 0.0;
+    launches[c] = 0;
+  }
+  if (!g_prof) return GR4AD_OK;
+  for (auto &r : *g_prof) {
+    GR_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    GR_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    if (r.cls >= 0 && r.cls < n_classes) {
+      ms[r.cls] += t;
+      launches[r.cls] += 1;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof->clear();
+  return GR4AD_OK;
+}
+
+long long gr4ad_take_launch_count(void) {
+  long long n = g_launches;
+  g_launches = 0;
+  return n;
+}
 
 const char *gr4ad_status_string(int s) {
   switch (s) {

@@ -26,7 +26,35 @@ int set_err(int code, const char *fmt, ...);
                            #expr, cudaGetErrorString(_e));                    \
   } while (0)
 
-#define GR_LAUNCH_CHECK() GR_CUDA(cudaGetLastError())
+// Kernel classes for the live per-class timing hooks (gr4ad_profile_*).
+enum KernelClass {
+  KC_GEMM = 0,       // projections, FFN, codebook logits, encoder K/V
+  KC_ATTN_GEMM = 1,  // grouped cross-attention Q.K^T / P.V over the shared KV
+  KC_TOPK = 2,       // exact per-request top-k + compaction
+  KC_SOFTMAX = 3,
+  KC_LAYERNORM = 4,
+  KC_SELF_ATTN = 5,
+  KC_ROW_LSE = 6,
+  KC_SMALL = 7,      // inputs, tiling, init, masks
+  KC_COLLECT = 8,
+  KC_COUNT = 9
+};
+
+// Launch bookkeeping (thread-local, like the error text): a launch counter
+// and, when enabled, a CUDA event pair recorded on the launching stream
+// around every launch.
+void count_launch();
+void prof_begin(int cls, cudaStream_t st);
+void prof_end(int cls, cudaStream_t st);
+
+#define GR_LAUNCH(cls, st, ...)          \
+  do {                                   \
+    ::gr::prof_begin((cls), (st));       \
+    __VA_ARGS__;                         \
+    ::gr::prof_end((cls), (st));         \
+    ::gr::count_launch();                \
+    GR_CUDA(cudaGetLastError());         \
+  } while (0)
 
 // order-preserving float <-> uint32 (larger float -> larger key)
 __device__ __forceinline__ uint32_t f2ord(float f) {

@@ -7,6 +7,8 @@ template <int BM, int BN, int BK, int TM, int TN, bool TB>
 static int launch_epi(const GemmArgs &a, int epi, cudaStream_t st) {
   dim3 grid(ceil_div(a.N, BN), ceil_div(a.M, BM), a.groups);
   dim3 block((BM / TM) * (BN / TN));
+  const int cls = (a.mode == GM_PLAIN) ? KC_GEMM : KC_ATTN_GEMM;
+  prof_begin(cls, st);
   switch (epi) {
     case EPI_STORE: gemm_f32_kernel<BM, BN, BK, TM, TN, TB, EPI_STORE><<<grid, block, 0, st>>>(a); break;
     case EPI_BIAS: gemm_f32_kernel<BM, BN, BK, TM, TN, TB, EPI_BIAS><<<grid, block, 0, st>>>(a); break;
@@ -16,7 +18,9 @@ static int launch_epi(const GemmArgs &a, int epi, cudaStream_t st) {
     case EPI_MULVEC: gemm_f32_kernel<BM, BN, BK, TM, TN, TB, EPI_MULVEC><<<grid, block, 0, st>>>(a); break;
     default: return set_err(GR4AD_ERR_UNSUPPORTED, "gemm epilogue %d", epi);
   }
-  GR_LAUNCH_CHECK();
+  prof_end(cls, st);
+  count_launch();
+  GR_CUDA(cudaGetLastError());
   return GR4AD_OK;
 }
 

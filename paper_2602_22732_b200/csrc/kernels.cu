@@ -29,8 +29,7 @@ __global__ void ln_rows_kernel(const float *__restrict__ x, long long ldx, float
 int ln_rows(const float *x, long long ldx, float *y, long long ldy, const float *g,
             const float *b, int rows, int d, cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;
-  ln_rows_kernel<<<ceil_div(rows, 8), 256, 0, st>>>(x, ldx, y, ldy, g, b, rows, d);
-  GR_LAUNCH_CHECK();
+  GR_LAUNCH(KC_LAYERNORM, st, ln_rows_kernel<<<ceil_div(rows, 8), 256, 0, st>>>(x, ldx, y, ldy, g, b, rows, d));
   return GR4AD_OK;
 }
 
@@ -56,8 +55,7 @@ __global__ void softmax_rows_kernel(float *s, long long ld, int rows,
 int softmax_rows(float *s, long long ld, int rows, const int *row_req, const int *len,
                  cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;
-  softmax_rows_kernel<<<ceil_div(rows, 8), 256, 0, st>>>(s, ld, rows, row_req, len);
-  GR_LAUNCH_CHECK();
+  GR_LAUNCH(KC_SOFTMAX, st, softmax_rows_kernel<<<ceil_div(rows, 8), 256, 0, st>>>(s, ld, rows, row_req, len));
   return GR4AD_OK;
 }
 
@@ -121,10 +119,9 @@ int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_st
               int hist_row0, int rows, int npos_uniform, const int *npos_row,
               float *out, long long ldo, cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;
-  self_attn_kernel<<<rows, 128, 0, st>>>(qkv, ld3, d, anc, anc_stride, hist_row0, rows,
+  GR_LAUNCH(KC_SELF_ATTN, st, self_attn_kernel<<<rows, 128, 0, st>>>(qkv, ld3, d, anc, anc_stride, hist_row0, rows,
                                          npos_uniform, npos_row, out, ldo,
-                                         1.0f / sqrtf((float)d));
-  GR_LAUNCH_CHECK();
+                                         1.0f / sqrtf((float)d)));
   return GR4AD_OK;
 }
 
@@ -148,9 +145,8 @@ int level_input(int t, int rows, int d, const float *bos, const float *emb_prev,
                 cudaStream_t st) {
   long long n = (long long)rows * d;
   if (n <= 0) return GR4AD_OK;
-  level_input_kernel<<<ceil_div(n, 256), 256, 0, st>>>(t, rows, d, bos, emb_prev, tok,
-                                                       pos_t, U, H);
-  GR_LAUNCH_CHECK();
+  GR_LAUNCH(KC_SMALL, st, level_input_kernel<<<ceil_div(n, 256), 256, 0, st>>>(t, rows, d, bos, emb_prev, tok,
+                                                       pos_t, U, H));
   return GR4AD_OK;
 }
 
@@ -183,8 +179,7 @@ row_lse_kernel(const float *__restrict__ logits, long long ld, int rows, int V,
 int row_lse(const float *logits, long long ld, int rows, int V, float2 *info,
             cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;
-  row_lse_kernel<<<rows, 128, 0, st>>>(logits, ld, rows, V, info);
-  GR_LAUNCH_CHECK();
+  GR_LAUNCH(KC_ROW_LSE, st, row_lse_kernel<<<rows, 128, 0, st>>>(logits, ld, rows, V, info));
   return GR4AD_OK;
 }
 
@@ -230,8 +225,7 @@ int mask_rows(float *logits, long long ld, int rows, int V, const long long *pre
               const long long *valid, int n_valid, cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;
   size_t sm = sizeof(unsigned) * ((V + 31) / 32);
-  mask_rows_kernel<<<rows, 256, sm, st>>>(logits, ld, rows, V, prefix, valid, n_valid);
-  GR_LAUNCH_CHECK();
+  GR_LAUNCH(KC_SMALL, st, mask_rows_kernel<<<rows, 256, sm, st>>>(logits, ld, rows, V, prefix, valid, n_valid));
   return GR4AD_OK;
 }
 
@@ -591,13 +585,12 @@ int topk_select(const SelectArgs &a, int n_requests, int u_rows, int u_k,
   if (cache) {
     GR_CUDA(cudaFuncSetAttribute(topk_select_kernel<true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    topk_select_kernel<true><<<n_requests, kSelThreads, sm, st>>>(a, u_rows, u_k);
+    GR_LAUNCH(KC_TOPK, st, topk_select_kernel<true><<<n_requests, kSelThreads, sm, st>>>(a, u_rows, u_k));
   } else {
     GR_CUDA(cudaFuncSetAttribute(topk_select_kernel<false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    topk_select_kernel<false><<<n_requests, kSelThreads, sm, st>>>(a, u_rows, u_k);
+    GR_LAUNCH(KC_TOPK, st, topk_select_kernel<false><<<n_requests, kSelThreads, sm, st>>>(a, u_rows, u_k));
   }
-  GR_LAUNCH_CHECK();
   return GR4AD_OK;
 }
 
@@ -618,9 +611,8 @@ __global__ void init_level0_kernel(int B, int *live0, float *cum, long long *pre
 int init_level0(int n_requests, int *live0, float *cum, long long *prefix, int *anc,
                 int anc_stride, int *tok, cudaStream_t st) {
   if (n_requests <= 0) return GR4AD_OK;
-  init_level0_kernel<<<ceil_div(n_requests, 256), 256, 0, st>>>(n_requests, live0, cum, prefix,
-                                                                anc, anc_stride, tok);
-  GR_LAUNCH_CHECK();
+  GR_LAUNCH(KC_SMALL, st, init_level0_kernel<<<ceil_div(n_requests, 256), 256, 0, st>>>(n_requests, live0, cum, prefix,
+                                                                anc, anc_stride, tok));
   return GR4AD_OK;
 }
 
@@ -705,10 +697,9 @@ int collect_results(int n_requests, int T, const int *row_off_T, const int *live
   size_t sm = vlogits ? (sizeof(double) + sizeof(int)) * GR4AD_MAX_BEAM : 0;
   if (sm) GR_CUDA(cudaFuncSetAttribute(collect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sm));
-  collect_kernel<<<n_requests, 512, sm, st>>>(T, row_off_T, live_T, hist_off_T, tok, anc,
+  GR_LAUNCH(KC_COLLECT, st, collect_kernel<<<n_requests, 512, sm, st>>>(T, row_off_T, live_T, hist_off_T, tok, anc,
                                               anc_stride, cum, vlogits, nb, reps, max_out,
-                                              count, tokens, score);
-  GR_LAUNCH_CHECK();
+                                              count, tokens, score));
   return GR4AD_OK;
 }
 
