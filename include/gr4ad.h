@@ -98,6 +98,11 @@ typedef struct {
    * (t+1)-token prefixes.  NULL entries disable masking at that level. */
   const int64_t *valid_prefix[GR4AD_MAX_LEVELS];
   const int *valid_prefix_count; /* host [n_levels] */
+  /* 0: auto (fused per-request kernel when the request's working set fits
+   * on chip -- d in {16,32}, d_ff <= 64, S <= 512, widths <= 2048, no
+   * masking -- else the layered batch path); 1: force layered; 2: force
+   * fused (GR4AD_ERR_UNSUPPORTED if not eligible). */
+  int decode_path;
 } gr4ad_batch;
 
 /* Results: for request b, count[b] entries in selection order (or value
@@ -122,7 +127,8 @@ long long gr4ad_take_launch_count(void);
  * end every launch made by the calling thread is bracketed by CUDA events on
  * its stream; end() synchronises and returns per-class total ms and launch
  * counts.  Classes: 0 gemm, 1 attention gemm, 2 top-k, 3 softmax,
- * 4 layernorm, 5 self-attention, 6 row log-sum-exp, 7 small, 8 collect. */
+ * 4 layernorm, 5 self-attention, 6 row log-sum-exp, 7 small, 8 collect,
+ * 9 fused small-model decode. */
 void gr4ad_profile_begin(void);
 int gr4ad_profile_end(double *ms, long long *launches, int n_classes);
 

@@ -21,7 +21,7 @@ MAX_BEAM = 8192
 OK, ERR_VALUE, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA = range(5)
 
 KERNEL_CLASSES = ("gemm", "attn_gemm", "topk_select", "softmax", "layernorm", "self_attn",
-                  "row_lse", "small", "collect")
+                  "row_lse", "small", "collect", "fused_decode")
 
 EXPORTS = (
     "gr4ad_abi_version", "gr4ad_last_error", "gr4ad_status_string",
@@ -59,7 +59,9 @@ class Batch(C.Structure):
                 ("widths", C.POINTER(C.c_int)), ("trunk_depth", C.c_int),
                 ("value_rerank", C.c_int), ("value_reps", _P),
                 ("valid_prefix", _P * MAX_LEVELS),
-                ("valid_prefix_count", C.POINTER(C.c_int))]
+                ("valid_prefix_count", C.POINTER(C.c_int)), ("decode_path", C.c_int)]
+
+PATH_AUTO, PATH_LAYERED, PATH_FUSED = 0, 1, 2
 
 
 class Results(C.Structure):

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "fused_small.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
 
@@ -75,7 +76,75 @@ struct Plan {
   size_t o_Hs, o_N, o_Q, o_A, o_U, o_Fb, o_SC, o_LG, o_rinfo, o_vlog;
   size_t o_hist;  // (L-K) consecutive (H, 3d) buffers
   size_t table_bytes, total;
+  // fused small-model path
+  bool fused = false;
+  int f_KS = 0, f_Hrows = 0;
+  int f_hoff[GR4AD_MAX_LEVELS + 2] = {}, f_moff[GR4AD_MAX_LEVELS + 2] = {};
+  int f_s[11] = {};  // smem offsets (floats): X KV TR TQ hist par tok cum bins scr sort
+  size_t f_smem = 0;
+  long long f_keys_per_req = 0;
+  size_t o_keys = 0, o_wT = 0;
 };
+
+static long long fused_wT_floats(const Plan &p) {
+  const long long D = p.d;
+  return p.L * (6 * D * D + 2 * D * p.dff) + 3 * D * D + 2LL * p.L * D * D + D * p.F +
+         (long long)p.nb * D + 64;
+}
+
+// Shared-memory plan of the fused per-request kernel; false if it does not fit.
+static bool plan_fused(Plan &p) {
+  const int D = p.d;
+  if (!(D == 16 || D == 32) || !(p.dff == D || p.dff == 2 * D) || p.S_max > 32 * D ||
+      p.nb > D || p.L > 32)
+    return false;
+  for (int t = 0; t < p.T; ++t)
+    if (p.V[t] % 4 != 0 || p.V[t] / 4 > 8 * D) return false;
+  int kmax = 1;
+  for (int t = 0; t < p.T; ++t) {
+    if (p.maxcap[t + 1] > 2048) return false;
+    kmax = std::max(kmax, p.maxcap[t + 1]);
+  }
+  int n2 = 1;
+  while (n2 < kmax) n2 <<= 1;
+  const int KS = D + 4;
+  const int last = p.rerank ? p.T : p.T - 1;
+  long long hrows = 0, mrows = 0;
+  for (int t = 0; t <= p.T; ++t) {
+    p.f_moff[t] = (int)mrows;
+    mrows += p.maxcap[t];
+    if (t <= last) {
+      p.f_hoff[t] = (int)hrows;
+      hrows += p.maxcap[t];
+    }
+  }
+  long long o = 0;
+  auto take = [&](long long floats) {
+    long long r = o;
+    o += (floats + 3) / 4 * 4;
+    return (int)r;
+  };
+  p.f_s[0] = take((long long)p.S_max * KS);
+  p.f_s[1] = take((long long)std::max(p.L - p.K, 1) * 2 * p.S_max * KS);
+  p.f_s[2] = take((long long)p.n_pos * D);
+  p.f_s[3] = take((long long)p.n_pos * 3 * D);
+  p.f_s[4] = take((long long)(p.L - p.K) * hrows * 2 * D);
+  p.f_s[5] = take(mrows);
+  p.f_s[6] = take(mrows);
+  p.f_s[7] = take(mrows);
+  p.f_s[8] = take(2048);
+  p.f_s[9] = take(64);
+  p.f_s[10] = take(2LL * n2);
+  size_t bytes = (size_t)o * sizeof(float);
+  if (bytes > 220 * 1024) return false;
+  p.f_KS = KS;
+  p.f_Hrows = (int)hrows;
+  p.f_smem = bytes;
+  long long kpr = 1;
+  for (int t = 0; t < p.T; ++t) kpr = std::max(kpr, (long long)p.maxcap[t] * p.V[t]);
+  p.f_keys_per_req = kpr;
+  return true;
+}
 
 static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   if (!dm || !bt) return set_err(GR4AD_ERR_VALUE, "null dims/batch");
@@ -162,6 +231,11 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   p.Rw = std::max(rw, 1LL);
   if (p.H >= (1LL << 31) || p.S_tot >= (1LL << 31))
     return set_err(GR4AD_ERR_UNSUPPORTED, "batch too large");
+  bool masked = false;
+  for (int t = 0; t < T; ++t) masked |= bt->valid_prefix[t] != nullptr;
+  if (bt->decode_path != 1 && !masked && B > 0) p.fused = plan_fused(p);
+  if (bt->decode_path == 2 && !p.fused)
+    return set_err(GR4AD_ERR_UNSUPPORTED, "fused decode path not eligible for this batch");
 
   // ---- workspace layout ----
   size_t o = 0;
@@ -184,6 +258,12 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   p.o_tanc = take(I * (size_t)B * p.n_pos * p.n_pos);
   p.o_tnpos = take(I * (size_t)B * p.n_pos);
   p.table_bytes = o;
+  if (p.fused) {
+    p.o_keys = take(sizeof(uint32_t) * (size_t)B * p.f_keys_per_req);
+    p.o_wT = take(sizeof(float) * (size_t)fused_wT_floats(p));
+    p.total = o;
+    return GR4AD_OK;
+  }
   p.o_tok = take(I * p.H);
   p.o_anc = take(I * p.H * p.stride);
   p.o_cum = take(Fl * p.H);
@@ -331,6 +411,67 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
                     gr4ad_results *out, void *ws, cudaStream_t st) {
   const int B = p.B, T = p.T, d = p.d, K = p.K;
   if (B == 0) return GR4AD_OK;
+  if (p.fused) {
+    FusedArgs f{};
+    f.w = *w;
+    if (!features && !context) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
+    // transposed weight copies (row = output neuron) for float4 row products
+    {
+      const int D = d, L = p.L;
+      float *wt = at<float>(ws, p.o_wT);
+      size_t o = 0;
+      FusedPrep pr{};
+      auto job = [&](const float *src, int rows, int cols) -> const float * {
+        float *dst = wt + o;
+        o += ((size_t)rows * cols + 3) / 4 * 4;
+        if (pr.n == FusedPrep::kMax) {
+          if (fused_prep_launch(pr, st) != GR4AD_OK) return nullptr;
+          pr.n = 0;
+        }
+        pr.src[pr.n] = src; pr.dst[pr.n] = dst; pr.rows[pr.n] = rows; pr.cols[pr.n] = cols;
+        ++pr.n;
+        return dst;
+      };
+      for (int i = 0; i < L; ++i) {
+        const gr4ad_layer &Lw = w->layer[i];
+        f.lt[i].cqT = job(Lw.cross_Wq, D, D);
+        f.lt[i].coT = job(Lw.cross_Wo, D, D);
+        f.lt[i].sqkvT = job(Lw.self_Wqkv, D, 3 * D);
+        f.lt[i].soT = job(Lw.self_Wo, D, D);
+        f.lt[i].w1T = job(Lw.ffn_W1, D, p.dff);
+        f.lt[i].w2T = job(Lw.ffn_W2, p.dff, D);
+      }
+      f.fuseT.wgT = job(w->fuse_Wg, D, D);
+      f.fuseT.wfT = job(w->fuse_Wf, 2 * D, D);
+      f.kvT = job(w->cross_kv_W, D, 2 * L * D);
+      f.ctxT = job(w->ctx_W, p.F, D);
+      f.hvT = job(w->head_value, D, p.nb);
+      GR_TRY(fused_prep_launch(pr, st));
+    }
+    f.features = features;
+    f.context = context;
+    f.ctx_off = at<int>(ws, p.o_ctx_off);
+    f.ctx_len = at<int>(ws, p.o_ctx_len);
+    f.eff = at<int>(ws, p.o_eff);
+    f.value_reps = bt->value_reps;
+    f.B = B; f.D = d; f.F = p.F; f.dff = p.dff; f.L = p.L; f.K = K; f.T = T;
+    f.nb = p.nb; f.n_pos = p.n_pos; f.rerank = p.rerank ? 1 : 0;
+    for (int t = 0; t < T; ++t) f.V[t] = p.V[t];
+    f.Vmax = p.Vmax;
+    f.S_max = p.S_max; f.KS = p.f_KS; f.Hrows = p.f_Hrows;
+    for (int t = 0; t < GR4AD_MAX_LEVELS + 2; ++t) {
+      f.hoff[t] = p.f_hoff[t];
+      f.moff[t] = p.f_moff[t];
+    }
+    f.s_X = p.f_s[0]; f.s_KV = p.f_s[1]; f.s_TR = p.f_s[2]; f.s_TQ = p.f_s[3];
+    f.s_hist = p.f_s[4]; f.s_par = p.f_s[5]; f.s_tok = p.f_s[6]; f.s_cum = p.f_s[7];
+    f.s_bins = p.f_s[8]; f.s_scr = p.f_s[9]; f.s_sort = p.f_s[10];
+    f.keys = at<uint32_t>(ws, p.o_keys);
+    f.keys_per_req = p.f_keys_per_req;
+    f.max_out = out->max_out;
+    f.out_count = out->count; f.out_tokens = out->tokens; f.out_score = out->score;
+    return fused_small_launch(f, B, p.f_smem, st);
+  }
   int *eff = at<int>(ws, p.o_eff), *cap = at<int>(ws, p.o_cap);
   int *row_off = at<int>(ws, p.o_row_off), *live = at<int>(ws, p.o_live);
   int *row_req = at<int>(ws, p.o_row_req);

@@ -37,7 +37,8 @@ enum KernelClass {
   KC_ROW_LSE = 6,
   KC_SMALL = 7,      // inputs, tiling, init, masks
   KC_COLLECT = 8,
-  KC_COUNT = 9
+  KC_FUSED = 9,      // fused small-model per-request decode
+  KC_COUNT = 10
 };
 
 // Launch bookkeeping (thread-local, like the error text): a launch counter

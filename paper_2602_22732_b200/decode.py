@@ -51,8 +51,10 @@ def prefix_keys(valid_sids, vocab_sizes):
 
 
 class BeamDecoder:
+    PATHS = {"auto": 0, "layered": 1, "fused": 2}
+
     def __init__(self, model, ctx_lens, widths, trunk_depth=None, value_rerank=False,
-                 representatives=None, valid_sids=None, device=None):
+                 representatives=None, valid_sids=None, device=None, path="auto"):
         self.device = require_cuda(device)
         cfg = model.config
         self.cfg = cfg
@@ -91,6 +93,7 @@ class BeamDecoder:
                 bt.valid_prefix[t] = C.c_void_p(kt.data_ptr())
                 self._vcount[t] = int(keys.size)
         bt.valid_prefix_count = self._vcount
+        bt.decode_path = self.PATHS[path]
         self.batch = bt
         nbytes, max_out = C.c_size_t(), C.c_int()
         N.check(N.lib.gr4ad_workspace_bytes(C.byref(self.dims), C.byref(bt), C.byref(nbytes),

@@ -132,8 +132,11 @@ def beam_search(model, context, schedule, shared_kv=True, precut=True, counter=N
 
 def beam_search_batch(model, contexts=None, schedules=None, features=None, shared_kv=True,
                       precut=True, counter=None, value_rerank=False, buckets=None,
-                      trunk_depth=None, valid_sids=None):
+                      trunk_depth=None, valid_sids=None, path="auto"):
     """Batched ``beam_search``: one result list per request.
+
+    ``path`` picks the decode kernel: "auto" (fused per-request kernel
+    when the working set fits on chip, else layered), "layered" or "fused".
 
     ``contexts`` are projected X matrices, or ``features`` raw (S, F)
     feature matrices (the context projection then runs on the GPU, as the
@@ -181,7 +184,7 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
             raise ValueError("value_rerank requires buckets")
         reps = getattr(buckets, "representatives", buckets)
     dec = BeamDecoder(model, lens, per, trunk_depth=k_depth, value_rerank=value_rerank,
-                      representatives=reps, valid_sids=valid_sids, device=dev)
+                      representatives=reps, valid_sids=valid_sids, device=dev, path=path)
     dec.run(features=f, context=x)
     out = dec.host_results()
     vocab = tuple(cfg.level_vocab_sizes)

@@ -107,27 +107,57 @@ def test_golden_precut(golden_small):
     assert reordered <= 3, f"{reordered} pre-cut instances reordered by fp32 ranking"
 
 
-def _batch_parity(widths, n_req, label):
+def _batch_parity(widths, n_req, label, path="auto", rerank=False, k_depth=None):
     M, S = _pkg()
     model = _model(M, C1_MODEL)
     params = {k: v.data for k, v in model.params.items()}
     feats = [c_features(i, 256) for i in range(n_req)]
-    got = S.beam_search_batch(model, features=feats, schedules=S.BeamSchedule(widths, widths[-1]))
+    reps = np.array([0.5, 1.0, 1.7, 2.4])
+    got = S.beam_search_batch(model, features=feats, schedules=S.BeamSchedule(widths, widths[-1]),
+                              path=path, value_rerank=rerank, buckets=reps if rerank else None,
+                              trunk_depth=k_depth)
     errs = []
     for i in range(n_req):
-        want = orc.beam_search(params, C1_MODEL, orc.context_process(feats[i], params), widths)
+        want = orc.beam_search(params, C1_MODEL, orc.context_process(feats[i], params), widths,
+                               value_rerank=rerank, representatives=reps, trunk_depth=k_depth)
         errs.append(check_parity(want, [(sid.tokens, s) for sid, s in got[i]], f"{label}[{i}]"))
     return max(errs)
 
 
-def test_c1_batch_matches_oracle():
-    err = _batch_parity(C1_WIDTHS, 16, "C1")
-    print(f"C1 max abs score error {err:.3e}")
+@pytest.mark.parametrize("path", ["fused", "layered"])
+def test_c1_batch_matches_oracle(path):
+    err = _batch_parity(C1_WIDTHS, 16, "C1", path)
+    print(f"C1 ({path}) max abs score error {err:.3e}")
 
 
-def test_c2_batch_matches_oracle():
-    err = _batch_parity(C2_WIDTHS, 8, "C2")
-    print(f"C2 max abs score error {err:.3e}")
+@pytest.mark.parametrize("path", ["fused", "layered"])
+def test_c2_batch_matches_oracle(path):
+    err = _batch_parity(C2_WIDTHS, 8, "C2", path)
+    print(f"C2 ({path}) max abs score error {err:.3e}")
+
+
+@pytest.mark.parametrize("path", ["fused", "layered"])
+@pytest.mark.parametrize("k_depth", [0, 1])
+def test_c2_rerank_and_vanilla(path, k_depth):
+    _batch_parity((16, 48, 96), 4, "C2rr", path, rerank=True, k_depth=k_depth)
+    _batch_parity((16, 48, 96), 4, "C2k", path, rerank=False, k_depth=k_depth)
+
+
+def test_fused_ragged_and_d32():
+    """Fused kernel with d=32, ragged S and per-request widths, 3 layers."""
+    M, S = _pkg()
+    ocfg = orc.OracleConfig(8, 32, 64, 3, 2, (64, 32, 128), 3, 21)
+    model = _model(M, ocfg)
+    params = {k: v.data for k, v in model.params.items()}
+    rng = np.random.default_rng(5)
+    feats = [rng.normal(size=(int(rng.integers(1, 200)), 8)) for _ in range(12)]
+    widths = [(int(rng.integers(1, 40)), int(rng.integers(1, 200)), int(rng.integers(1, 300)))
+              for _ in range(12)]
+    for path in ("fused", "layered"):
+        got = S.beam_search_batch(model, features=feats, schedules=widths, path=path)
+        for i in range(12):
+            want = orc.beam_search(params, ocfg, orc.context_process(feats[i], params), widths[i])
+            check_parity(want, [(sid.tokens, s) for sid, s in got[i]], f"{path}[{i}]")
 
 
 def test_c2_golden_reference(golden_small):
@@ -215,6 +245,11 @@ def test_full_size_c2_batch_properties():
     model = _model(M, C1_MODEL)
     feats = [c_features(i, 256) for i in range(512)]
     got = S.beam_search_batch(model, features=feats, schedules=S.BeamSchedule(C2_WIDTHS, 256))
+    lay = S.beam_search_batch(model, features=feats[:64], schedules=S.BeamSchedule(C2_WIDTHS, 256),
+                              path="layered")
+    for a_, b_ in zip(got[:64], lay):  # both kernels: same lists up to fp32 near-ties
+        check_parity([(sid.tokens, s) for sid, s in b_], [(sid.tokens, s) for sid, s in a_],
+                     "fused-vs-layered")
     assert len(got) == 512
     for res in got:
         assert len(res) == 256
