@@ -124,11 +124,14 @@ static bool plan_fused(Plan &p) {
     o += (floats + 3) / 4 * 4;
     return (int)r;
   };
-  p.f_s[0] = take((long long)p.S_max * KS);
+  // the projected context is dead once every K/V is built, before the first
+  // history write: X and the self-KV history share one region
+  const long long hist_floats = (long long)(p.L - p.K) * hrows * 2 * D;
+  p.f_s[0] = take(std::max((long long)p.S_max * KS, hist_floats));
   p.f_s[1] = take((long long)std::max(p.L - p.K, 1) * 2 * p.S_max * KS);
   p.f_s[2] = take((long long)p.n_pos * D);
   p.f_s[3] = take((long long)p.n_pos * 3 * D);
-  p.f_s[4] = take((long long)(p.L - p.K) * hrows * 2 * D);
+  p.f_s[4] = p.f_s[0];
   p.f_s[5] = take(mrows);
   p.f_s[6] = take(mrows);
   p.f_s[7] = take(mrows);
@@ -261,6 +264,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   if (p.fused) {
     p.o_keys = take(sizeof(uint32_t) * (size_t)B * p.f_keys_per_req);
     p.o_wT = take(sizeof(float) * (size_t)fused_wT_floats(p));
+    take(sizeof(long long) * 16 * (size_t)B);  // per-request phase stamps (timing builds)
     p.total = o;
     return GR4AD_OK;
   }
@@ -470,6 +474,8 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     f.keys_per_req = p.f_keys_per_req;
     f.max_out = out->max_out;
     f.out_count = out->count; f.out_tokens = out->tokens; f.out_score = out->score;
+    f.dbg = reinterpret_cast<long long *>(static_cast<char *>(ws) + p.total -
+                                          (size_t)B * 16 * sizeof(long long));
     return fused_small_launch(f, B, p.f_smem, st);
   }
   int *eff = at<int>(ws, p.o_eff), *cap = at<int>(ws, p.o_cap);

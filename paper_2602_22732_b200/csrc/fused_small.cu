@@ -18,7 +18,7 @@ namespace gr {
 
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -245,8 +245,21 @@ __global__ void fused_prep_kernel(FusedPrep p) {
   }
 }
 
+#ifdef GR_FUSED_TIMING
+#define GR_STAMP(i)                                                             \
+  do {                                                                          \
+    if (threadIdx.x == 0) {                                                     \
+      long long _t;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                   \
+      a.dbg[blockIdx.x * 16 + (i)] = _t;                                        \
+    }                                                                           \
+  } while (0)
+#else
+#define GR_STAMP(i) do {} while (0)
+#endif
+
 template <int G, int MAXM, int VCH>
-__global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
   extern __shared__ __align__(16) float sm[];
   constexpr int D = G;
   constexpr int RPW = 32 / G;  // rows per warp
@@ -272,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(FusedArgs a) {
   unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(sm + a.s_sort);
   uint32_t *keys = a.keys + (size_t)b * a.keys_per_req;
   const int KVS = a.S_max * KS;
+  GR_STAMP(0);
 
   // ---- context projection X = F W_c + b_c (decoder.py:134-140) -------------
   for (int e = tid; e < S * D; e += kThreads) {
@@ -310,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(FusedArgs a) {
     }
   };
 
+  GR_STAMP(1);
   // ---- trunk: K layers over the n_pos position rows (beam.py:159-163) -------
   const int np = a.n_pos;
   if (K > 0) {
@@ -382,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(FusedArgs a) {
     }
   }
   __syncthreads();
+  GR_STAMP(2);
   // head-layer K/V, built once and shared by every beam (beam.py:165-169)
   for (int i = K; i < L; ++i) build_kv(i, i - K);
   if (tid == 0) {
@@ -391,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(FusedArgs a) {
   }
   __syncthreads();
 
+  GR_STAMP(3);
   const int last = a.rerank ? T : T - 1;
   int live = 1;
   for (int t = 0; t <= last; ++t) {
@@ -541,6 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(FusedArgs a) {
     }
     if (hcnt) atomicAdd(&hist[hcur], hcnt);
     __syncthreads();
+    GR_STAMP(4 + 2 * t);
 
     if (t == T) {  // re-rank output: sort rows by (rank desc, row asc)
       double *key = reinterpret_cast<double *>(sbuf);
@@ -698,6 +716,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(FusedArgs a) {
     }
     live = k;
     __syncthreads();
+    GR_STAMP(5 + 2 * t);
   }
   // results (beam.py:212-213)
   for (int j = tid; j < live; j += kThreads) {
@@ -709,6 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(FusedArgs a) {
     a.out_score[(size_t)b * a.max_out + j] = (double)cum[a.moff[T] + j];
   }
   if (tid == 0) a.out_count[b] = live;
+  GR_STAMP(15);
 }
 
 int fused_prep_launch(const FusedPrep &p, cudaStream_t st) {

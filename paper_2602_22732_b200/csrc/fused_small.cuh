@@ -46,6 +46,7 @@ struct FusedArgs {
   int max_out;
   int *out_count, *out_tokens;
   double *out_score;
+  long long *dbg;  // GR_FUSED_TIMING builds: [B][16] globaltimer stamps
 };
 
 int fused_prep_launch(const FusedPrep &p, cudaStream_t st);
