@@ -98,10 +98,12 @@ typedef struct {
    * (t+1)-token prefixes.  NULL entries disable masking at that level. */
   const int64_t *valid_prefix[GR4AD_MAX_LEVELS];
   const int *valid_prefix_count; /* host [n_levels] */
-  /* 0: auto (fused per-request kernel when the request's working set fits
-   * on chip -- d in {16,32}, d_ff <= 64, S <= 512, widths <= 2048, no
-   * masking -- else the layered batch path); 1: force layered; 2: force
-   * fused (GR4AD_ERR_UNSUPPORTED if not eligible). */
+  /* 0: auto -- the fused per-request kernel when a request's working set
+   * fits on chip (d in {16,32}, d_ff in {d,2d}, S <= 32d, widths <= 2048,
+   * no masking), else the layered batch path, with tcgen05 3xTF32 GEMMs
+   * when d >= 64 (and d, d_ff, F, V multiples of 4); 1: layered with
+   * CUDA-core GEMMs; 2: fused; 3: layered with tcgen05 GEMMs.  Forcing an
+   * ineligible path returns GR4AD_ERR_UNSUPPORTED. */
   int decode_path;
 } gr4ad_batch;
 
@@ -168,6 +170,13 @@ int gr4ad_context_process(const gr4ad_dims *dims, const gr4ad_weights *w,
 int gr4ad_encoder_kv(const gr4ad_dims *dims, const gr4ad_weights *w,
                      const float *x, int rows, int lo, int hi, float *kv,
                      void *stream);
+
+/* C = A . BT^T in fp32 (A: (M, K), BT: (N, K), row-major with the given
+ * leading dimensions) -- the GEMM the decode uses internally, exposed for
+ * numerics tests.  backend 0: CUDA-core fp32; 1: tcgen05 3xTF32 (fp32
+ * accumulation in TMEM; needs 16-B aligned rows). */
+int gr4ad_gemm(const float *A, long long lda, const float *BT, long long ldb, float *C,
+               long long ldc, int M, int N, int K, int backend, void *stream);
 
 /* Batched pre-cut selection (beam.py:50-89 topk_precut/_precut_arrays and
  * beam.py:37-47 topk_global -- identical results): for problem p,

@@ -8,6 +8,7 @@
 
 #include "fused_small.cuh"
 #include "gemm.cuh"
+#include "gemm_tc.cuh"
 #include "kernels.cuh"
 
 namespace gr {
@@ -61,6 +62,8 @@ struct Plan {
   bool rerank = false;
   int n_lv = 0;  // levels with rows: T+1
   std::vector<int> ctx_off, ctx_len, eff, cap, row_off;
+  std::vector<int> in_off;  // caller's row offsets (contiguous input)
+  long long S_in = 0;       // caller's total context rows
   long long R[GR4AD_MAX_LEVELS + 1] = {};
   long long hist_off[GR4AD_MAX_LEVELS + 2] = {};
   int maxcap[GR4AD_MAX_LEVELS + 1] = {};
@@ -69,13 +72,19 @@ struct Plan {
   int max_out = 0;
 
   // workspace layout: byte offsets
+  size_t o_in_off = 0;
   size_t o_ctx_off, o_ctx_len, o_eff, o_cap, o_row_off, o_live, o_row_req;
   size_t o_trow_off, o_trows, o_trow_req, o_tanc, o_tnpos;
   size_t o_tok, o_anc, o_cum, o_prefix;
-  size_t o_X, o_KV, o_Ht, o_QKVt;
+  size_t o_X, o_KV, o_Ht, o_QKVt, o_Fin = 0;
   size_t o_Hs, o_N, o_Q, o_A, o_U, o_Fb, o_SC, o_LG, o_rinfo, o_vlog;
   size_t o_hist;  // (L-K) consecutive (H, 3d) buffers
   size_t table_bytes, total;
+  // tensor-core layered path
+  bool tc = false;
+  long long sc_ld = 0, vt_ld = 0;
+  size_t o_VT = 0, o_WT = 0;
+  long long wt_floats = 0;
   // fused small-model path
   bool fused = false;
   int f_KS = 0, f_Hrows = 0;
@@ -178,14 +187,19 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
     p.Vmax = std::max(p.Vmax, p.V[t]);
   }
   const int B = p.B, T = p.T;
+  // each request's context rows start at a 32-row boundary in the layered
+  // buffers (X, K/V, V^T) so tensor-map tiles never straddle requests
   p.ctx_off.assign(B, 0);
   p.ctx_len.assign(B, 0);
+  p.in_off.assign(B, 0);
   for (int b = 0; b < B; ++b) {
     int s = bt->ctx_len[b];
     if (s <= 0) return set_err(GR4AD_ERR_VALUE, "empty context");
+    p.in_off[b] = (int)p.S_in;
     p.ctx_off[b] = (int)p.S_tot;
     p.ctx_len[b] = s;
-    p.S_tot += s;
+    p.S_in += s;
+    p.S_tot += (s + 31) / 32 * 32;
     p.S_max = std::max(p.S_max, s);
   }
   // effective widths (beam.py:134-139) and row capacities per level
@@ -239,6 +253,29 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   if (bt->decode_path != 1 && !masked && B > 0) p.fused = plan_fused(p);
   if (bt->decode_path == 2 && !p.fused)
     return set_err(GR4AD_ERR_UNSUPPORTED, "fused decode path not eligible for this batch");
+  if (!p.fused) {
+    bool ok = p.d % 4 == 0 && p.dff % 4 == 0 && p.F % 4 == 0;
+    for (int t = 0; t < T; ++t) ok &= p.V[t] % 4 == 0;
+    p.tc = ok && (bt->decode_path == 3 || (bt->decode_path == 0 && p.d >= 64));
+    if (bt->decode_path == 3 && !ok)
+      return set_err(GR4AD_ERR_UNSUPPORTED, "tensor-core path needs d, d_ff, F, V multiples of 4");
+  }
+  p.sc_ld = (p.S_max + 3) / 4 * 4;
+  p.vt_ld = (p.S_tot + 3) / 4 * 4;
+  if (p.tc) {
+    const long long D = p.d;
+    p.wt_floats = 0;
+    auto add = [&](long long n) { p.wt_floats += (n + 63) / 64 * 64; };
+    add(D * p.F);
+    add(2LL * p.L * D * D);
+    add(D * D);
+    add(2 * D * D);
+    for (int t = 0; t < T; ++t) add((long long)p.V[t] * D);
+    add((long long)p.nb * D);
+    for (int i = 0; i < p.L; ++i) {
+      add(D * D); add(D * D); add(3 * D * D); add(D * D); add(p.dff * D); add(D * p.dff);
+    }
+  }
 
   // ---- workspace layout ----
   size_t o = 0;
@@ -249,6 +286,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   };
   const size_t I = sizeof(int), Fl = sizeof(float);
   p.o_ctx_off = take(I * B);
+  p.o_in_off = take(I * B);
   p.o_ctx_len = take(I * B);
   p.o_eff = take(I * (size_t)T * B);
   p.o_cap = take(I * (size_t)(T + 1) * B);
@@ -274,6 +312,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   p.o_prefix = take(sizeof(long long) * p.H);
   const size_t d = p.d;
   p.o_X = take(Fl * p.S_tot * d);
+  p.o_Fin = take(Fl * p.S_tot * p.F);
   p.o_KV = take(Fl * p.S_tot * 2 * p.L * d);
   p.o_Ht = take(Fl * (size_t)B * p.n_pos * d);
   p.o_QKVt = take(Fl * (size_t)B * p.n_pos * 3 * d);
@@ -283,11 +322,15 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   p.o_A = take(Fl * p.Rw * d);
   p.o_U = take(Fl * p.Rw * 2 * d);
   p.o_Fb = take(Fl * p.Rw * p.dff);
-  p.o_SC = take(Fl * p.Rw * p.S_max);
+  p.o_SC = take(Fl * p.Rw * p.sc_ld);
   p.o_LG = take(Fl * p.Rw * std::max(p.Vmax, p.nb));
   p.o_rinfo = take(sizeof(float2) * p.Rw);
   p.o_vlog = take(Fl * std::max(p.R[T], 1LL) * p.nb);
   p.o_hist = take(Fl * p.H * 3 * d * (size_t)(p.L - p.K));
+  if (p.tc) {
+    p.o_VT = take(Fl * (size_t)p.L * d * p.vt_ld);
+    p.o_WT = take(Fl * (size_t)p.wt_floats);
+  }
   p.total = o;
   return GR4AD_OK;
 }
@@ -304,6 +347,7 @@ static int upload_tables(const Plan &p, void *ws, cudaStream_t st) {
     memcpy(reinterpret_cast<char *>(host.data()) + off, src, n * sizeof(int));
   };
   put(p.o_ctx_off, p.ctx_off.data(), B);
+  put(p.o_in_off, p.in_off.data(), B);
   put(p.o_ctx_len, p.ctx_len.data(), B);
   put(p.o_eff, p.eff.data(), (size_t)T * B);
   put(p.o_cap, p.cap.data(), (size_t)(T + 1) * B);
@@ -357,56 +401,128 @@ struct RowSet {
   const int *npos_row;
 };
 
-static int layer_forward(const Plan &p, const gr4ad_weights *w, int i, float *Hs,
-                         const RowSet &rs, void *ws, const float *KV, cudaStream_t st) {
+// K-major (out, in) copies of the weights for the tensor-core path
+struct LayerT {
+  const float *cq, *co, *sqkv, *so, *w1, *w2;
+};
+struct WeightsT {
+  const float *ctx, *kv, *wg, *wf, *hv;
+  const float *head[GR4AD_MAX_LEVELS];
+  LayerT layer[GR4AD_MAX_LAYERS];
+};
+
+static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, WeightsT &wt,
+                          cudaStream_t st) {
+  float *base = at<float>(ws, p.o_WT);
+  long long o = 0;
+  int rc = GR4AD_OK;
+  // dst (cols x rows) = src (rows x cols)^T
+  auto tr = [&](const float *src, int rows, int cols) -> const float * {
+    float *dst = base + o;
+    o += ((long long)rows * cols + 63) / 64 * 64;
+    if (rc == GR4AD_OK) rc = transpose(src, cols, dst, rows, rows, cols, st);
+    return dst;
+  };
+  const int d = p.d;
+  wt.ctx = tr(w->ctx_W, p.F, d);
+  wt.kv = tr(w->cross_kv_W, d, 2 * p.L * d);
+  wt.wg = tr(w->fuse_Wg, d, d);
+  wt.wf = tr(w->fuse_Wf, 2 * d, d);
+  for (int t = 0; t < p.T; ++t) wt.head[t] = tr(w->head[t], d, p.V[t]);
+  wt.hv = tr(w->head_value, d, p.nb);
+  for (int i = 0; i < p.L; ++i) {
+    const gr4ad_layer &Lw = w->layer[i];
+    wt.layer[i].cq = tr(Lw.cross_Wq, d, d);
+    wt.layer[i].co = tr(Lw.cross_Wo, d, d);
+    wt.layer[i].sqkv = tr(Lw.self_Wqkv, d, 3 * d);
+    wt.layer[i].so = tr(Lw.self_Wo, d, d);
+    wt.layer[i].w1 = tr(Lw.ffn_W1, d, p.dff);
+    wt.layer[i].w2 = tr(Lw.ffn_W2, p.dff, d);
+  }
+  return rc;
+}
+
+// C = epi(A (M x K) . W (K x N)); W in reference layout (ldb = N), WT its
+// K-major copy for the tensor-core path (a_rows = rows covered by A's map)
+static int dense(const Plan &p, const GemmArgs &g, const float *WT, long long a_rows, int epi,
+                 cudaStream_t st) {
+  if (p.tc && WT && tc_eligible(g.lda, g.K, g.K, g.A, WT)) {
+    TcArgs t{};
+    static_cast<GemmArgs &>(t) = g;
+    t.B = WT;
+    t.ldb = g.K;
+    return gemm_tc(t, a_rows, g.K, g.N, g.K, epi, st);
+  }
+  return gemm(g, false, epi, st);
+}
+
+static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *wt, int i,
+                         float *Hs, const RowSet &rs, void *ws, const float *KV,
+                         const float *VT, cudaStream_t st) {
   const int d = p.d, R = rs.rows;
   const gr4ad_layer &Lw = w->layer[i];
+  const LayerT *LT = wt ? &wt->layer[i] : nullptr;
   float *N = at<float>(ws, p.o_N), *Q = at<float>(ws, p.o_Q), *A = at<float>(ws, p.o_A);
   float *SC = at<float>(ws, p.o_SC), *Fb = at<float>(ws, p.o_Fb);
   const int *ctx_off = at<int>(ws, p.o_ctx_off), *ctx_len = at<int>(ws, p.o_ctx_len);
   const long long ldkv = 2LL * p.L * d;
   // cross-attention into the beam-shared context KV (layers.py:82-90)
   GR_TRY(ln_rows(Hs, d, N, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
-  GR_TRY(gemm(plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), false, EPI_STORE, st));
+  GR_TRY(dense(p, plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), LT ? LT->cq : nullptr, R,
+               EPI_STORE, st));
   GemmArgs qk{};
   qk.A = Q; qk.lda = d;
   qk.B = KV + (size_t)(2 * i) * d; qk.ldb = ldkv;
-  qk.C = SC; qk.ldc = p.S_max;
+  qk.C = SC; qk.ldc = p.sc_ld;
   qk.M = rs.max_group_rows; qk.N = p.S_max; qk.K = d;
   qk.alpha = 1.0f / sqrtf((float)d);
   qk.groups = p.B; qk.mode = GM_QK;
   qk.g_row_off = rs.g_row_off; qk.g_rows = rs.g_rows;
   qk.g_ctx_off = ctx_off; qk.g_ctx_len = ctx_len;
-  GR_TRY(gemm(qk, true, EPI_STORE, st));
-  GR_TRY(softmax_rows(SC, p.S_max, R, rs.row_req, ctx_len, st));
+  if (p.tc && tc_eligible(qk.lda, qk.ldb, d, qk.A, qk.B)) {
+    TcArgs t{};
+    static_cast<GemmArgs &>(t) = qk;
+    GR_TRY(gemm_tc(t, R, d, p.S_tot, d, EPI_STORE, st));
+  } else {
+    GR_TRY(gemm(qk, true, EPI_STORE, st));
+  }
+  GR_TRY(softmax_rows(SC, p.sc_ld, R, rs.row_req, ctx_len, st));
   GemmArgs pv = qk;
-  pv.A = SC; pv.lda = p.S_max;
-  pv.B = KV + (size_t)(2 * i + 1) * d; pv.ldb = ldkv;
+  pv.A = SC; pv.lda = p.sc_ld;
   pv.C = A; pv.ldc = d;
   pv.M = rs.max_group_rows; pv.N = d; pv.K = p.S_max;
   pv.alpha = 1.f; pv.mode = GM_PV;
-  GR_TRY(gemm(pv, false, EPI_STORE, st));
+  if (p.tc && VT) {
+    TcArgs t{};
+    static_cast<GemmArgs &>(t) = pv;
+    t.B = VT + (size_t)i * d * p.vt_ld;
+    t.ldb = p.vt_ld;
+    GR_TRY(gemm_tc(t, R, p.sc_ld, d, p.vt_ld, EPI_STORE, st));
+  } else {
+    pv.B = KV + (size_t)(2 * i + 1) * d; pv.ldb = ldkv;
+    GR_TRY(gemm(pv, false, EPI_STORE, st));
+  }
   GemmArgs o = plain_gemm(A, d, Lw.cross_Wo, d, Hs, d, R, d, d);
   o.R = Hs; o.ldr = d;
-  GR_TRY(gemm(o, false, EPI_RESID, st));
+  GR_TRY(dense(p, o, LT ? LT->co : nullptr, R, EPI_RESID, st));
   // self-attention over decoded positions (layers.py:92-113)
   GR_TRY(ln_rows(Hs, d, N, d, Lw.ln2_g, Lw.ln2_b, R, d, st));
   float *qkv_rows = rs.qkv + rs.hist_row0 * 3 * d;
-  GR_TRY(gemm(plain_gemm(N, d, Lw.self_Wqkv, 3 * d, qkv_rows, 3 * d, R, 3 * d, d), false,
-              EPI_STORE, st));
+  GR_TRY(dense(p, plain_gemm(N, d, Lw.self_Wqkv, 3 * d, qkv_rows, 3 * d, R, 3 * d, d),
+               LT ? LT->sqkv : nullptr, R, EPI_STORE, st));
   GR_TRY(self_attn(rs.qkv, 3LL * d, d, rs.anc, rs.anc_stride, (int)rs.hist_row0, R,
                    rs.npos_u, rs.npos_row, A, d, st));
   GemmArgs so = plain_gemm(A, d, Lw.self_Wo, d, Hs, d, R, d, d);
   so.R = Hs; so.ldr = d;
-  GR_TRY(gemm(so, false, EPI_RESID, st));
+  GR_TRY(dense(p, so, LT ? LT->so : nullptr, R, EPI_RESID, st));
   // position-wise FFN (layers.py:115-118)
   GR_TRY(ln_rows(Hs, d, N, d, Lw.ln3_g, Lw.ln3_b, R, d, st));
   GemmArgs f1 = plain_gemm(N, d, Lw.ffn_W1, p.dff, Fb, p.dff, R, p.dff, d);
   f1.bias = Lw.ffn_b1;
-  GR_TRY(gemm(f1, false, EPI_BIAS_GELU, st));
+  GR_TRY(dense(p, f1, LT ? LT->w1 : nullptr, R, EPI_BIAS_GELU, st));
   GemmArgs f2 = plain_gemm(Fb, p.dff, Lw.ffn_W2, d, Hs, d, R, d, p.dff);
   f2.bias = Lw.ffn_b2; f2.R = Hs; f2.ldr = d;
-  GR_TRY(gemm(f2, false, EPI_BIAS_RESID, st));
+  GR_TRY(dense(p, f2, LT ? LT->w2 : nullptr, R, EPI_BIAS_RESID, st));
   return GR4AD_OK;
 }
 
@@ -454,7 +570,7 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     }
     f.features = features;
     f.context = context;
-    f.ctx_off = at<int>(ws, p.o_ctx_off);
+    f.ctx_off = at<int>(ws, p.o_in_off);
     f.ctx_len = at<int>(ws, p.o_ctx_len);
     f.eff = at<int>(ws, p.o_eff);
     f.value_reps = bt->value_reps;
@@ -490,21 +606,50 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
   float2 *rinfo = at<float2>(ws, p.o_rinfo);
   float *hist = at<float>(ws, p.o_hist);
   const size_t hist_layer = (size_t)p.H * 3 * d;
+  WeightsT wt_store;
+  const WeightsT *wt = nullptr;
+  float *VT = nullptr;
+  if (p.tc) {
+    GR_TRY(prep_weights_t(p, w, ws, wt_store, st));
+    wt = &wt_store;
+    VT = at<float>(ws, p.o_VT);
+  }
 
-  // context projection (decoder.py:134-140)
-  const float *X = context;
-  if (features) {
+  // context projection (decoder.py:134-140) on 32-row-aligned request blocks
+  if (!features && !context) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
+  const int *in_off = at<int>(ws, p.o_in_off), *ctx_off_d = at<int>(ws, p.o_ctx_off);
+  const int *ctx_len_d = at<int>(ws, p.o_ctx_len);
+  const float *X = at<float>(ws, p.o_X);
+  if (!features) {
+    GR_TRY(pad_rows(context, in_off, ctx_off_d, ctx_len_d, B, d, at<float>(ws, p.o_X), st));
+  } else {
+    float *Fin = at<float>(ws, p.o_Fin);
+    GR_TRY(pad_rows(features, in_off, ctx_off_d, ctx_len_d, B, p.F, Fin, st));
+    features = Fin;
     float *Xw = at<float>(ws, p.o_X);
     GemmArgs g = plain_gemm(features, p.F, w->ctx_W, d, Xw, d, (int)p.S_tot, d, p.F);
     g.bias = w->ctx_b;
-    GR_TRY(gemm(g, false, EPI_BIAS, st));
-    X = Xw;
+    GR_TRY(dense(p, g, wt ? wt->ctx : nullptr, p.S_tot, EPI_BIAS, st));
   }
-  if (!X) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
-  // encoder K/V of every layer, once per request (beam.py:98-109; layers.py:85-87)
-  GR_TRY(gemm(plain_gemm(X, d, w->cross_kv_W, 2LL * p.L * d, KV, 2LL * p.L * d, (int)p.S_tot,
-                         2 * p.L * d, d),
-              false, EPI_STORE, st));
+  // encoder K/V of every layer, once per request (beam.py:98-109; layers.py:85-87);
+  // on the tensor-core path the epilogue also writes V^T for the P.V GEMMs
+  {
+    GemmArgs g = plain_gemm(X, d, w->cross_kv_W, 2LL * p.L * d, KV, 2LL * p.L * d, (int)p.S_tot,
+                            2 * p.L * d, d);
+    if (p.tc && tc_eligible(g.lda, d, d, X, wt->kv)) {
+      TcArgs t{};
+      static_cast<GemmArgs &>(t) = g;
+      t.B = wt->kv;
+      t.ldb = d;
+      t.vt = VT;
+      t.vt_ld = p.vt_ld;
+      t.kv_d = d;
+      GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * p.L * d, d, EPI_KV_SPLIT, st));
+    } else {
+      if (p.tc) return set_err(GR4AD_ERR_UNSUPPORTED, "tensor-core path: unaligned context");
+      GR_TRY(gemm(g, false, EPI_STORE, st));
+    }
+  }
   GR_TRY(init_level0(B, live, cum, prefix, anc, p.stride, tok, st));
 
   // trunk: K layers over the n_pos position rows, shared by all beams (beam.py:159-163)
@@ -522,7 +667,7 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     rs.anc = at<int>(ws, p.o_tanc);
     rs.anc_stride = p.n_pos;
     rs.npos_row = at<int>(ws, p.o_tnpos);
-    for (int i = 0; i < K; ++i) GR_TRY(layer_forward(p, w, i, Ht, rs, ws, KV, st));
+    for (int i = 0; i < K; ++i) GR_TRY(layer_forward(p, w, wt, i, Ht, rs, ws, KV, VT, st));
   }
 
   const int last = p.rerank ? T : T - 1;
@@ -537,9 +682,9 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       gg.vec = Ht + (size_t)t * d;
       gg.vec_ld = (long long)p.n_pos * d;
       gg.row_req = row_req + h0;
-      GR_TRY(gemm(gg, false, EPI_MULVEC, st));
-      GR_TRY(gemm(plain_gemm(U, 2LL * d, w->fuse_Wf, d, Hs, d, R, d, 2 * d), false, EPI_STORE,
-                  st));
+      GR_TRY(dense(p, gg, wt ? wt->wg : nullptr, R, EPI_MULVEC, st));
+      GR_TRY(dense(p, plain_gemm(U, 2LL * d, w->fuse_Wf, d, Hs, d, R, d, 2 * d),
+                   wt ? wt->wf : nullptr, R, EPI_STORE, st));
     } else {
       GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, w->pos + (size_t)t * d, nullptr,
                          Hs, st));
@@ -558,17 +703,18 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     rs.npos_row = nullptr;
     for (int i = K; i < p.L; ++i) {
       rs.qkv = hist + (size_t)(i - K) * hist_layer;
-      GR_TRY(layer_forward(p, w, i, Hs, rs, ws, KV, st));
+      GR_TRY(layer_forward(p, w, wt, i, Hs, rs, ws, KV, VT, st));
     }
     if (t == T) {  // value re-rank step (beam.py:258-288)
       float *vlog = at<float>(ws, p.o_vlog);
-      GR_TRY(gemm(plain_gemm(Hs, d, w->head_value, p.nb, vlog, p.nb, R, p.nb, d), false,
-                  EPI_STORE, st));
+      GR_TRY(dense(p, plain_gemm(Hs, d, w->head_value, p.nb, vlog, p.nb, R, p.nb, d),
+                   wt ? wt->hv : nullptr, R, EPI_STORE, st));
       break;
     }
     // codebook projection + log-softmax + score accumulation + top-k (beam.py:198-210)
     const int V = p.V[t];
-    GR_TRY(gemm(plain_gemm(Hs, d, w->head[t], V, LG, V, R, V, d), false, EPI_STORE, st));
+    GR_TRY(dense(p, plain_gemm(Hs, d, w->head[t], V, LG, V, R, V, d),
+                 wt ? wt->head[t] : nullptr, R, EPI_STORE, st));
     GR_TRY(row_lse(LG, V, R, V, rinfo, st));
     if (bt->valid_prefix[t]) {
       GR_TRY(mask_rows(LG, V, R, V, prefix + h0,
@@ -715,6 +861,20 @@ int gr4ad_encoder_kv(const gr4ad_dims *dims, const gr4ad_weights *w, const float
   return gemm(plain_gemm(x, d, w->cross_kv_W + (size_t)2 * lo * d, ldw, kv,
                          2LL * (hi - lo) * d, rows, 2 * (hi - lo) * d, d),
               false, EPI_STORE, (cudaStream_t)stream);
+}
+
+int gr4ad_gemm(const float *A, long long lda, const float *BT, long long ldb, float *C,
+               long long ldc, int M, int N, int K, int backend, void *stream) {
+  if (M < 0 || N < 0 || K < 1) return set_err(GR4AD_ERR_VALUE, "bad gemm shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (backend == 1) {
+    if (!tc_eligible(lda, ldb, K, A, BT))
+      return set_err(GR4AD_ERR_UNSUPPORTED, "tcgen05 gemm needs 16-B aligned K-major rows");
+    TcArgs t{};
+    static_cast<GemmArgs &>(t) = plain_gemm(A, lda, BT, ldb, C, ldc, M, N, K);
+    return gemm_tc(t, M, K, N, K, EPI_STORE, st);
+  }
+  return gemm(plain_gemm(A, lda, BT, ldb, C, ldc, M, N, K), true, EPI_STORE, st);
 }
 
 size_t gr4ad_topk_workspace_bytes(int n_problems, int b, int v) { return 256; }

@@ -18,7 +18,8 @@ enum GemmEpi {
   EPI_BIAS_GELU = 2,  // C = gelu(acc + bias[n])
   EPI_RESID = 3,      // C = R + acc
   EPI_BIAS_RESID = 4, // C = R + (acc + bias[n])
-  EPI_MULVEC = 5      // C = vec[req(r)][n] * acc   (fuse gate m * (s W_g))
+  EPI_MULVEC = 5,     // C = vec[req(r)][n] * acc   (fuse gate m * (s W_g))
+  EPI_KV_SPLIT = 6    // C = acc, and the V half of each layer also written transposed
 };
 
 struct GemmArgs {

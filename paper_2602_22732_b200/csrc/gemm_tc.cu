@@ -1,0 +1,384 @@
+// tcgen05 (5th-gen tensor core) GEMM in 3xTF32 for sm_100a.
+//
+//   C = epi(alpha * A . B^T)      A: (M, K) fp32, B: (N, K) fp32, both K-major
+//
+// fp32-faithful on tensor cores: each operand x is split into
+// hi = x with the low 13 mantissa bits cleared (exactly a tf32 value) and
+// lo = x - hi (exact in fp32), and the product is accumulated as
+// hi.hi + hi.lo + lo.hi in fp32 in TMEM (the dropped lo.lo term is ~2^-22
+// relative).  This keeps the beam scores within ~1e-6 of float64, which the
+// list-identity parity rule needs (SURVEY §7 hard part 1); plain TF32 or
+// BF16 inputs reorder most beam lists.
+//
+// Pipeline per CTA (one 128 x BN output tile, K in 32-float steps):
+//   warp 0   TMA producer: fp32 A/B tiles -> smem (SWIZZLE_128B), mbarrier tx
+//   warps 4-7 converters: split each landed tile in place into hi + lo buffers,
+//            fence.proxy.async, arrive
+//   warp 1   TMEM allocator + single-thread MMA issuer: 3 tcgen05.mma per
+//            8-deep k-step, tcgen05.commit frees the stage
+//   warps 4-7 epilogue: tcgen05.ld 32x32b the 128 x BN fp32 accumulator,
+//            bias / GELU / residual / gate / K|V^T split, store.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+
+#include "gemm.cuh"
+#include "gemm_tc.cuh"
+
+namespace gr {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // 32 fp32 = one 128-B swizzle row
+constexpr int kTcThreads = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// K-major SWIZZLE_128B smem matrix descriptor (rows of 128 B, 8-row atoms of
+// 1024 B): start>>4 | LBO=1 (16 B) | SBO=1024>>4 | version 1 | layout 2
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
+  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  lo = x - hi;
+}
+
+}  // namespace
+
+template <int BN, int STAGES, int EPI>
+__global__ void __launch_bounds__(kTcThreads, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B aligned tile region
+  unsigned char *smem = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int A_BYTES = BM * BK * 4;
+  constexpr int B_BYTES = BN * BK * 4;
+  constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+  uint64_t *conv = full + STAGES;
+  uint64_t *empty = conv + STAGES;
+  uint64_t *done = empty + STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.z;
+  int M = a.M, N = a.N, K = a.K;
+  int row_base = 0, b_row_base = 0, b_k_base = 0;
+  if (a.g_rows) {
+    row_base = a.g_row_off[g];
+    M = a.g_rows[g];
+    if (a.mode == GM_QK) {
+      N = a.g_ctx_len[g];
+      b_row_base = a.g_ctx_off[g];
+    } else if (a.mode == GM_PV) {
+      K = a.g_ctx_len[g];
+      b_k_base = a.g_ctx_off[g];
+    }
+  }
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= M || n0 >= N) return;
+  const int nk = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // TMEM: BN fp32 columns x 128 lanes
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+        unsigned char *st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+        tma_load_2d(st, &tmA, &full[s], kt * BK, row_base + m0);
+        tma_load_2d(st + 2 * A_BYTES, &tmB, &full[s], b_k_base + kt * BK, b_row_base + n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(BM >> 4) << 24);
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % STAGES;
+        mbar_wait(&conv[s], (kt / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t a_hi = st, a_lo = st + A_BYTES;
+        const uint32_t b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k) {
+          const uint32_t off = k * 32;  // 8 tf32 = 32 B along the swizzled row
+          const uint32_t acc0 = (kt > 0 || k > 0) ? 1u : 0u;
+          mma_tf32(tmem, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, acc0);
+          mma_tf32(tmem, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
+          mma_tf32(tmem, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, 1u);
+        }
+        mma_commit(&empty[s]);  // frees the stage when these MMAs complete
+      }
+      mma_commit(done);
+    }
+  } else if (warp >= 4) {
+    // ---- converters: split landed fp32 tiles into tf32 hi (in place) + lo
+    const int ct = threadIdx.x - 128;  // 0..127
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % STAGES;
+      mbar_wait(&full[s], (kt / STAGES) & 1);
+      unsigned char *st = smem + s * STAGE_BYTES;
+      float4 *ah = reinterpret_cast<float4 *>(st);
+      float4 *al = reinterpret_cast<float4 *>(st + A_BYTES);
+      float4 *bh = reinterpret_cast<float4 *>(st + 2 * A_BYTES);
+      float4 *bl = reinterpret_cast<float4 *>(st + 2 * A_BYTES + B_BYTES);
+#pragma unroll 4
+      for (int i = ct; i < A_BYTES / 16; i += 128) {
+        float4 x = ah[i], h, l;
+        split_tf32(x.x, h.x, l.x);
+        split_tf32(x.y, h.y, l.y);
+        split_tf32(x.z, h.z, l.z);
+        split_tf32(x.w, h.w, l.w);
+        ah[i] = h;
+        al[i] = l;
+      }
+#pragma unroll 4
+      for (int i = ct; i < B_BYTES / 16; i += 128) {
+        float4 x = bh[i], h, l;
+        split_tf32(x.x, h.x, l.x);
+        split_tf32(x.y, h.y, l.y);
+        split_tf32(x.z, h.z, l.z);
+        split_tf32(x.w, h.w, l.w);
+        bh[i] = h;
+        bl[i] = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[s]);
+    }
+    // ---- epilogue: TMEM -> registers -> global
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;
+    const int r = m0 + q * 32 + lane;  // this thread's output row (within group)
+    const long long grow = (long long)row_base + r;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), v);
+      if (r >= M) continue;
+      const int col0 = n0 + c * 32;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int col = col0 + j;
+        float x = v[j] * a.alpha;
+        if (col < N) {
+          if (EPI == EPI_BIAS) x = x + a.bias[col];
+          else if (EPI == EPI_BIAS_GELU) x = gelu_tanh(x + a.bias[col]);
+          else if (EPI == EPI_RESID) x = a.R[grow * a.ldr + col] + x;
+          else if (EPI == EPI_BIAS_RESID) x = a.R[grow * a.ldr + col] + (x + a.bias[col]);
+          else if (EPI == EPI_MULVEC) x = a.vec[(long long)a.row_req[grow] * a.vec_ld + col] * x;
+          if (EPI == EPI_KV_SPLIT) {
+            // [2i d, 2i d + d) -> K_i; [2i d + d, 2(i+1) d) -> also V_i^T (coalesced over rows)
+            const int layer = col / (2 * a.kv_d), w = col - layer * 2 * a.kv_d;
+            if (w >= a.kv_d)
+              a.vt[((long long)layer * a.kv_d + (w - a.kv_d)) * a.vt_ld + grow] = x;
+          }
+        }
+        v[j] = x;
+      }
+      float *crow = a.C + grow * a.ldc + col0;
+      if (col0 + 32 <= N && (a.ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(crow) % 16) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4 *>(crow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+        for (int j = 0; j < 32 && col0 + j < N; ++j) crow[j] = v[j];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps + launch
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  // resolved once (thread-safe static init); a driver entry point, not state
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 2-D fp32 K-major map: inner dim = cols (K), outer = rows; box 32 x box_rows
+static int make_map(CUtensorMap *m, const float *base, long long rows, long long cols, long long ld,
+                    int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return set_err(GR4AD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(GR4AD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return GR4AD_OK;
+}
+
+template <int BN, int STAGES>
+static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const TcArgs &a, int epi,
+                     cudaStream_t st) {
+  constexpr size_t smem = 1024 + (size_t)STAGES * (2 * BM * BK * 4 + 2 * BN * BK * 4) + 256;
+  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.groups);
+  const int cls = (a.mode == GM_PLAIN) ? KC_GEMM : KC_ATTN_GEMM;
+#define GR_TC_EPI(E)                                                                     \
+  case E: {                                                                              \
+    GR_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E>,                          \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    GR_LAUNCH(cls, st, gemm_tc_kernel<BN, STAGES, E><<<grid, kTcThreads, smem, st>>>(ma, mb, a)); \
+    return GR4AD_OK;                                                                     \
+  }
+  switch (epi) {
+    GR_TC_EPI(EPI_STORE)
+    GR_TC_EPI(EPI_BIAS)
+    GR_TC_EPI(EPI_BIAS_GELU)
+    GR_TC_EPI(EPI_RESID)
+    GR_TC_EPI(EPI_BIAS_RESID)
+    GR_TC_EPI(EPI_MULVEC)
+    GR_TC_EPI(EPI_KV_SPLIT)
+    default: return set_err(GR4AD_ERR_UNSUPPORTED, "tc epilogue %d", epi);
+  }
+#undef GR_TC_EPI
+}
+
+bool tc_eligible(long long lda, long long ldb, int K, const void *A, const void *B) {
+  return (lda % 4 == 0) && (ldb % 4 == 0) && (K % 4 == 0) &&
+         (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+}
+
+int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_rows,
+            long long b_cols, int epi, cudaStream_t st) {
+  if (a.M <= 0 || a.N <= 0 || a.groups <= 0) return GR4AD_OK;
+  static const bool trace = getenv("GR4AD_TRACE") != nullptr;  // debug aid (read-only)
+  if (trace)
+    fprintf(stderr, "gemm_tc M=%d N=%d K=%d groups=%d mode=%d epi=%d lda=%lld ldb=%lld ldc=%lld "
+                    "A=(%lld,%lld) B=(%lld,%lld)\n",
+            a.M, a.N, a.K, a.groups, a.mode, epi, a.lda, a.ldb, a.ldc, a_rows, a_cols, b_rows,
+            b_cols);
+  CUtensorMap ma, mb;
+  GR_TRY(make_map(&ma, a.A, a_rows, a_cols, a.lda, BM));
+  GR_TRY(make_map(&mb, a.B, b_rows, b_cols, a.ldb, 128));
+  return launch_tc<128, 3>(ma, mb, a, epi, st);
+}
+
+}  // namespace gr

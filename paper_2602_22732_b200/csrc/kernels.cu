@@ -1,4 +1,5 @@
 // Row-wise kernels and the exact per-request top-k of the beam step.
+#include "gemm_tc.cuh"
 #include "kernels.cuh"
 
 namespace gr {
@@ -50,6 +51,7 @@ __global__ void softmax_rows_kernel(float *s, long long ld, int rows,
   for (int j = lane; j < n; j += 32) sum += expf(r[j] - mx);
   float lse = logf(warp_sum(sum)) + mx;
   for (int j = lane; j < n; j += 32) r[j] = expf(r[j] - lse);
+  for (int j = n + lane; j < ld; j += 32) r[j] = 0.f;  // keeps P.V exact past S_b
 }
 
 int softmax_rows(float *s, long long ld, int rows, const int *row_req, const int *len,
@@ -591,6 +593,53 @@ int topk_select(const SelectArgs &a, int n_requests, int u_rows, int u_k,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     GR_LAUNCH(KC_TOPK, st, topk_select_kernel<false><<<n_requests, kSelThreads, sm, st>>>(a, u_rows, u_k));
   }
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// tiled transpose: dst (cols x rows) = src (rows x cols)^T
+// ---------------------------------------------------------------------------
+__global__ void transpose_kernel(const float *__restrict__ src, long long lds, float *dst,
+                                 long long ldd, int rows, int cols) {
+  __shared__ float tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    int r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = src[(long long)r * lds + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    int c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[(long long)c * ldd + r] = tile[threadIdx.x][i];
+  }
+}
+
+int transpose(const float *src, long long lds, float *dst, long long ldd, int rows, int cols,
+              cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return GR4AD_OK;
+  dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32));
+  GR_LAUNCH(KC_SMALL, st, transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, lds, dst, ldd, rows, cols));
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// request blocks -> 32-row-aligned blocks (zero padded): block per request
+// ---------------------------------------------------------------------------
+__global__ void pad_rows_kernel(const float *__restrict__ src, const int *__restrict__ in_off,
+                                const int *__restrict__ out_off, const int *__restrict__ len,
+                                int width, float *dst) {
+  const int b = blockIdx.x;
+  const int n = len[b], np = (n + 31) / 32 * 32;
+  const float *s = src + (long long)in_off[b] * width;
+  float *o = dst + (long long)out_off[b] * width;
+  for (long long e = threadIdx.x; e < (long long)np * width; e += blockDim.x)
+    o[e] = e < (long long)n * width ? s[e] : 0.f;
+}
+
+int pad_rows(const float *src, const int *in_off, const int *out_off, const int *len, int B,
+             int width, float *dst, cudaStream_t st) {
+  if (B <= 0) return GR4AD_OK;
+  GR_LAUNCH(KC_SMALL, st, pad_rows_kernel<<<B, 256, 0, st>>>(src, in_off, out_off, len, width, dst));
   return GR4AD_OK;
 }
 

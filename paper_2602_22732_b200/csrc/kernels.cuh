@@ -72,6 +72,11 @@ struct SelectArgs {
 int topk_select(const SelectArgs &a, int n_requests, int u_rows, int u_k,
                 long long max_cand, cudaStream_t st);
 
+// copy request blocks of `width`-wide rows from caller offsets to 32-row
+// aligned offsets, zero-filling the padding rows
+int pad_rows(const float *src, const int *in_off, const int *out_off, const int *len, int B,
+             int width, float *dst, cudaStream_t st);
+
 // level-0 rows: live=1, cum=0, prefix=0, anc[g][0]=g
 int init_level0(int n_requests, int *live0, float *cum, long long *prefix, int *anc,
                 int anc_stride, int *tok, cudaStream_t st);

@@ -135,8 +135,10 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
                       trunk_depth=None, valid_sids=None, path="auto"):
     """Batched ``beam_search``: one result list per request.
 
-    ``path`` picks the decode kernel: "auto" (fused per-request kernel
-    when the working set fits on chip, else layered), "layered" or "fused".
+    ``path`` picks the decode kernels: "auto" (the fused per-request kernel
+    when the working set fits on chip, else the layered batch path with
+    tcgen05 3xTF32 GEMMs for d >= 64, else CUDA-core GEMMs), "fused",
+    "tensor" (layered + tcgen05) or "layered" (layered + CUDA-core).
 
     ``contexts`` are projected X matrices, or ``features`` raw (S, F)
     feature matrices (the context projection then runs on the GPU, as the

@@ -1,0 +1,42 @@
+"""Numerics of the decode's GEMMs through the C ABI (gr4ad_gemm) against a
+float64 torch reference: the CUDA-core fp32 path and the tcgen05 3xTF32
+path must both be fp32-faithful (relative error ~1e-6, far below TF32's
+~1e-3), since beam lists depend on it (SURVEY §7 hard part 1)."""
+
+import ctypes as C
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(A, BT, backend):
+    from paper_2602_22732_b200 import _native as N
+    M, K = A.shape
+    Nn = BT.shape[0]
+    out = torch.empty((M, Nn), dtype=torch.float32, device=A.device)
+    N.check(N.lib.gr4ad_gemm(C.c_void_p(A.data_ptr()), A.stride(0), C.c_void_p(BT.data_ptr()),
+                             BT.stride(0), C.c_void_p(out.data_ptr()), out.stride(0), M, Nn, K,
+                             backend, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("shape", [(128, 128, 32), (256, 384, 1024), (1000, 1100, 1024),
+                                   (300, 4096, 1024), (77, 50, 36), (512, 1024, 2048)])
+@pytest.mark.parametrize("backend", [0, 1])
+def test_gemm_fp32_faithful(shape, backend):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    M, Nn, K = shape
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + Nn + K)
+    A = torch.randn((M, K), device="cuda", generator=g)
+    BT = torch.randn((Nn, K), device="cuda", generator=g) / K ** 0.5
+    got = _gemm(A, BT, backend).double()
+    ref = A.double() @ BT.double().T
+    scale = (A.double().abs() @ BT.double().abs().T)  # error bound scale per entry
+    rel = ((got - ref).abs() / scale.clamp_min(1e-30)).max().item()
+    print(f"backend {backend} shape {shape}: max scaled error {rel:.3e}")
+    # fp32 accumulation over K: ~K^0.5 * 2^-24 typical; 3xTF32 drops lo.lo (~2^-22)
+    assert rel < 1e-5, f"backend {backend} shape {shape}: max scaled error {rel:.3e}"

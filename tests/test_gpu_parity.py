@@ -124,19 +124,19 @@ def _batch_parity(widths, n_req, label, path="auto", rerank=False, k_depth=None)
     return max(errs)
 
 
-@pytest.mark.parametrize("path", ["fused", "layered"])
+@pytest.mark.parametrize("path", ["fused", "layered", "tensor"])
 def test_c1_batch_matches_oracle(path):
     err = _batch_parity(C1_WIDTHS, 16, "C1", path)
     print(f"C1 ({path}) max abs score error {err:.3e}")
 
 
-@pytest.mark.parametrize("path", ["fused", "layered"])
+@pytest.mark.parametrize("path", ["fused", "layered", "tensor"])
 def test_c2_batch_matches_oracle(path):
     err = _batch_parity(C2_WIDTHS, 8, "C2", path)
     print(f"C2 ({path}) max abs score error {err:.3e}")
 
 
-@pytest.mark.parametrize("path", ["fused", "layered"])
+@pytest.mark.parametrize("path", ["fused", "layered", "tensor"])
 @pytest.mark.parametrize("k_depth", [0, 1])
 def test_c2_rerank_and_vanilla(path, k_depth):
     _batch_parity((16, 48, 96), 4, "C2rr", path, rerank=True, k_depth=k_depth)
@@ -153,7 +153,7 @@ def test_fused_ragged_and_d32():
     feats = [rng.normal(size=(int(rng.integers(1, 200)), 8)) for _ in range(12)]
     widths = [(int(rng.integers(1, 40)), int(rng.integers(1, 200)), int(rng.integers(1, 300)))
               for _ in range(12)]
-    for path in ("fused", "layered"):
+    for path in ("fused", "layered", "tensor"):
         got = S.beam_search_batch(model, features=feats, schedules=widths, path=path)
         for i in range(12):
             want = orc.beam_search(params, ocfg, orc.context_process(feats[i], params), widths[i])
@@ -171,18 +171,21 @@ def test_c2_golden_reference(golden_small):
         check_parity(ref, [(sid.tokens, s) for sid, s in got], case["name"])
 
 
-def test_c3_golden_reference(golden_c3):
-    """Full C3 shape: d=1024, L=8, K=5, S=1024, V=4096^3, widths 512^3."""
+@pytest.mark.parametrize("path", ["tensor", "layered"])
+def test_c3_golden_reference(golden_c3, path):
+    """Full C3 shape: d=1024, L=8, K=5, S=1024, V=4096^3, widths 512^3, on
+    the tcgen05 3xTF32 path (auto for d >= 64) and the CUDA-core path."""
     M, S = _pkg()
     c = golden_c3["config"]
     cfg = M.DecoderConfig(c["feat_dim"], c["d"], c["d_ff"], c["n_layers"], c["trunk_depth"],
                           tuple(c["level_vocab_sizes"]), c["n_value_buckets"], c["seed"])
     model = M.DecoderModel(cfg)
     feats = c_features(golden_c3["request"], golden_c3["s_ctx"])
-    got = S.beam_search_batch(model, features=[feats], schedules=[tuple(golden_c3["widths"])])[0]
+    got = S.beam_search_batch(model, features=[feats], schedules=[tuple(golden_c3["widths"])],
+                              path=path)[0]
     ref = [(tuple(t), s) for t, s in zip(golden_c3["tokens"], golden_c3["scores"])]
     err = check_parity(ref, [(sid.tokens, s) for sid, s in got], "C3")
-    print(f"C3 max abs score error {err:.3e}")
+    print(f"C3 ({path}) max abs score error {err:.3e}")
 
 
 def test_ragged_batch_matches_single_requests():
@@ -275,3 +278,24 @@ def test_errors_mirror_reference():
         S.beam_search(model, np.ones((1, 4)), S.BeamSchedule((2,), 2))
     with pytest.raises(ValueError):
         S.beam_search(model, np.ones((1, 4)), S.BeamSchedule((2, 2), 2), trunk_depth=2)
+
+
+def test_tensor_path_mid_model():
+    """d=64 (auto picks the tcgen05 path), ragged S, value re-rank, K=0/K=2."""
+    M, S = _pkg()
+    ocfg = orc.OracleConfig(12, 64, 128, 4, 2, (128, 64, 256), 4, 31)
+    model = _model(M, ocfg)
+    params = {k: v.data for k, v in model.params.items()}
+    rng = np.random.default_rng(9)
+    feats = [rng.normal(size=(int(rng.integers(1, 130)), 12)) for _ in range(6)]
+    widths = [(int(rng.integers(1, 30)), int(rng.integers(1, 90)), int(rng.integers(1, 120)))
+              for _ in range(6)]
+    reps = np.array([0.2, 0.9, 1.5, 3.0])
+    for k_depth, rerank in ((2, False), (0, True), (3, True)):
+        got = S.beam_search_batch(model, features=feats, schedules=widths, trunk_depth=k_depth,
+                                  value_rerank=rerank, buckets=reps if rerank else None)
+        for i in range(6):
+            want = orc.beam_search(params, ocfg, orc.context_process(feats[i], params), widths[i],
+                                   trunk_depth=k_depth, value_rerank=rerank,
+                                   representatives=reps)
+            check_parity(want, [(sid.tokens, s) for sid, s in got[i]], f"d64 K={k_depth}[{i}]")
