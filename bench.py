@@ -40,6 +40,10 @@ CONFIGS = {
     "c3": dict(model=(16, 1024, 2048, 8, 5, (4096, 4096, 4096), 4), S=1024,
                widths=(512, 512, 512), batch=256,
                name="C3: LazyAR d1024/L8/K5, V=4096^3, S=1024, beam 512, batch 256"),
+    "c5": dict(model=(16, 1024, 2048, 8, 5, (4096, 4096, 4096), 4), S=1024,
+               widths=(64, 128, 256), batch=256,
+               name="C5: C3 model, production-shaped DBW 64->128->256, user-sharded, "
+                    "256 requests per GPU per step"),
 }
 
 
