@@ -87,28 +87,23 @@ struct Plan {
   long long wt_floats = 0;
   // fused small-model path
   bool fused = false;
-  int f_KS = 0, f_Hrows = 0;
+  int f_Hrows = 0, f_sort_cap = 0;
   int f_hoff[GR4AD_MAX_LEVELS + 2] = {}, f_moff[GR4AD_MAX_LEVELS + 2] = {};
-  int f_s[11] = {};  // smem offsets (floats): X KV TR TQ hist par tok cum bins scr sort
+  int f_s[12] = {};  // smem offsets (floats): X KV TR TQ hist par tok cum bins scr sort ws
   size_t f_smem = 0;
   long long f_keys_per_req = 0;
   size_t o_keys = 0, o_wT = 0;
 };
 
-static long long fused_wT_floats(const Plan &p) {
-  const long long D = p.d;
-  return p.L * (6 * D * D + 2 * D * p.dff) + 3 * D * D + 2LL * p.L * D * D + D * p.F +
-         (long long)p.nb * D + 64;
-}
 
 // Shared-memory plan of the fused per-request kernel; false if it does not fit.
 static bool plan_fused(Plan &p) {
   const int D = p.d;
-  if (!(D == 16 || D == 32) || !(p.dff == D || p.dff == 2 * D) || p.S_max > 32 * D ||
-      p.nb > D || p.L > 32)
+  if (!(D == 16 || D == 32) || !(p.dff == D || p.dff == 2 * D) || p.S_max > 256 ||
+      p.nb > 8 || p.L > 32)
     return false;
   for (int t = 0; t < p.T; ++t)
-    if (p.V[t] % 4 != 0 || p.V[t] / 4 > 8 * D) return false;
+    if (p.V[t] % 8 != 0 || p.V[t] > 256) return false;
   int kmax = 1;
   for (int t = 0; t < p.T; ++t) {
     if (p.maxcap[t + 1] > 2048) return false;
@@ -116,7 +111,8 @@ static bool plan_fused(Plan &p) {
   }
   int n2 = 1;
   while (n2 < kmax) n2 <<= 1;
-  const int KS = D + 4;
+  n2 = std::max(2 * n2, 1024);  // window selection collects up to sort_cap keys
+  p.f_sort_cap = n2;
   const int last = p.rerank ? p.T : p.T - 1;
   long long hrows = 0, mrows = 0;
   for (int t = 0; t <= p.T; ++t) {
@@ -136,8 +132,8 @@ static bool plan_fused(Plan &p) {
   // the projected context is dead once every K/V is built, before the first
   // history write: X and the self-KV history share one region
   const long long hist_floats = (long long)(p.L - p.K) * hrows * 2 * D;
-  p.f_s[0] = take(std::max((long long)p.S_max * KS, hist_floats));
-  p.f_s[1] = take((long long)std::max(p.L - p.K, 1) * 2 * p.S_max * KS);
+  p.f_s[0] = take(std::max((long long)256 * D, hist_floats));
+  p.f_s[1] = take((long long)std::max(p.L - p.K, 1) * 2 * D * 256);
   p.f_s[2] = take((long long)p.n_pos * D);
   p.f_s[3] = take((long long)p.n_pos * 3 * D);
   p.f_s[4] = p.f_s[0];
@@ -147,9 +143,9 @@ static bool plan_fused(Plan &p) {
   p.f_s[8] = take(2048);
   p.f_s[9] = take(64);
   p.f_s[10] = take(2LL * n2);
+  p.f_s[11] = take(8LL * 4 * 4 * D);  // 8 warps x 4 slots x (D x 4)
   size_t bytes = (size_t)o * sizeof(float);
   if (bytes > 220 * 1024) return false;
-  p.f_KS = KS;
   p.f_Hrows = (int)hrows;
   p.f_smem = bytes;
   long long kpr = 1;
@@ -301,7 +297,6 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   p.table_bytes = o;
   if (p.fused) {
     p.o_keys = take(sizeof(uint32_t) * (size_t)B * p.f_keys_per_req);
-    p.o_wT = take(sizeof(float) * (size_t)fused_wT_floats(p));
     take(sizeof(long long) * 16 * (size_t)B);  // per-request phase stamps (timing builds)
     p.total = o;
     return GR4AD_OK;
@@ -535,39 +530,6 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     FusedArgs f{};
     f.w = *w;
     if (!features && !context) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
-    // transposed weight copies (row = output neuron) for float4 row products
-    {
-      const int D = d, L = p.L;
-      float *wt = at<float>(ws, p.o_wT);
-      size_t o = 0;
-      FusedPrep pr{};
-      auto job = [&](const float *src, int rows, int cols) -> const float * {
-        float *dst = wt + o;
-        o += ((size_t)rows * cols + 3) / 4 * 4;
-        if (pr.n == FusedPrep::kMax) {
-          if (fused_prep_launch(pr, st) != GR4AD_OK) return nullptr;
-          pr.n = 0;
-        }
-        pr.src[pr.n] = src; pr.dst[pr.n] = dst; pr.rows[pr.n] = rows; pr.cols[pr.n] = cols;
-        ++pr.n;
-        return dst;
-      };
-      for (int i = 0; i < L; ++i) {
-        const gr4ad_layer &Lw = w->layer[i];
-        f.lt[i].cqT = job(Lw.cross_Wq, D, D);
-        f.lt[i].coT = job(Lw.cross_Wo, D, D);
-        f.lt[i].sqkvT = job(Lw.self_Wqkv, D, 3 * D);
-        f.lt[i].soT = job(Lw.self_Wo, D, D);
-        f.lt[i].w1T = job(Lw.ffn_W1, D, p.dff);
-        f.lt[i].w2T = job(Lw.ffn_W2, p.dff, D);
-      }
-      f.fuseT.wgT = job(w->fuse_Wg, D, D);
-      f.fuseT.wfT = job(w->fuse_Wf, 2 * D, D);
-      f.kvT = job(w->cross_kv_W, D, 2 * L * D);
-      f.ctxT = job(w->ctx_W, p.F, D);
-      f.hvT = job(w->head_value, D, p.nb);
-      GR_TRY(fused_prep_launch(pr, st));
-    }
     f.features = features;
     f.context = context;
     f.ctx_off = at<int>(ws, p.o_in_off);
@@ -577,18 +539,18 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     f.B = B; f.D = d; f.F = p.F; f.dff = p.dff; f.L = p.L; f.K = K; f.T = T;
     f.nb = p.nb; f.n_pos = p.n_pos; f.rerank = p.rerank ? 1 : 0;
     for (int t = 0; t < T; ++t) f.V[t] = p.V[t];
-    f.Vmax = p.Vmax;
-    f.S_max = p.S_max; f.KS = p.f_KS; f.Hrows = p.f_Hrows;
+    f.S_max = p.S_max; f.Hrows = p.f_Hrows;
     for (int t = 0; t < GR4AD_MAX_LEVELS + 2; ++t) {
       f.hoff[t] = p.f_hoff[t];
       f.moff[t] = p.f_moff[t];
     }
     f.s_X = p.f_s[0]; f.s_KV = p.f_s[1]; f.s_TR = p.f_s[2]; f.s_TQ = p.f_s[3];
     f.s_hist = p.f_s[4]; f.s_par = p.f_s[5]; f.s_tok = p.f_s[6]; f.s_cum = p.f_s[7];
-    f.s_bins = p.f_s[8]; f.s_scr = p.f_s[9]; f.s_sort = p.f_s[10];
+    f.s_bins = p.f_s[8]; f.s_scr = p.f_s[9]; f.s_sort = p.f_s[10]; f.s_ws = p.f_s[11];
     f.keys = at<uint32_t>(ws, p.o_keys);
     f.keys_per_req = p.f_keys_per_req;
     f.max_out = out->max_out;
+    f.sort_cap = p.f_sort_cap;
     f.out_count = out->count; f.out_tokens = out->tokens; f.out_score = out->score;
     f.dbg = reinterpret_cast<long long *>(static_cast<char *>(ws) + p.total -
                                           (size_t)B * 16 * sizeof(long long));

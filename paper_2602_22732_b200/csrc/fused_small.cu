@@ -1,17 +1,17 @@
 // Fused per-request LazyAR beam decode for small models (d in {16, 32}).
 //
-// One CTA owns one request for the whole decode (beam.py:146-218): context
-// projection (decoder.py:134-140), the beam-shared encoder K/V of every
-// layer kept in shared memory (beam.py:98-109), the trunk (beam.py:159-163),
-// then per level each group of G = d lanes owns one beam row (two rows per
-// warp at d = 16) and runs fuse -> head layers -> codebook logits ->
-// log-softmax keys with the row state in registers.  The self-KV history
-// lives in shared memory and is read through parent pointers (no copies,
-// beam.py:205-210), and an exact radix top-k over the level's candidates
-// compacts the beams in place.  Weights are read transposed (prepared once
-// per call into the workspace) so every row x matrix product uses float4
-// loads.  The C1/C2 working set (K/V 40 KB, history 25 KB) fits on chip:
-// the whole batch decode is two launches.
+// One CTA owns one request for the whole decode (beam.py:146-218):
+// context projection (decoder.py:134-140), the beam-shared encoder K/V of
+// every layer kept in shared memory (beam.py:98-109) as K^T / V^T, the trunk
+// (beam.py:159-163), then per level every warp owns four beam rows and runs
+// fuse -> head layers -> codebook logits -> log-softmax keys.  The four rows
+// are register-tiled: each lane owns 8 contiguous context keys (or 8 codebook
+// tokens) for all four rows, so every shared-memory K/V load and every head
+// weight load feeds 32 FMAs.  The self-KV history lives in shared memory and
+// is read through parent pointers (no copies, beam.py:205-210), and an exact
+// radix top-k over the level's candidates compacts the beams in place.
+// The C1/C2 working set (K^T/V^T 32 KB, history 25 KB) fits on chip: the
+// batch decode is one launch.
 #include "fused_small.cuh"
 
 namespace gr {
@@ -20,69 +20,22 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int RW = 4;    // beam rows per warp
+constexpr int SP = 256;  // context keys held per lane-row: 32 lanes x 8
 constexpr unsigned kFull = 0xffffffffu;
 
-template <int G>
-__device__ __forceinline__ float gsum(float v) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+// sum / max over the 8 lanes that share a row (lane >> 3)
+__device__ __forceinline__ float rsum(float v) {
+  v += __shfl_xor_sync(kFull, v, 4);
+  v += __shfl_xor_sync(kFull, v, 2);
+  v += __shfl_xor_sync(kFull, v, 1);
   return v;
 }
-template <int G>
-__device__ __forceinline__ float gmax(float v) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+__device__ __forceinline__ float rmax(float v) {
+  v = fmaxf(v, __shfl_xor_sync(kFull, v, 4));
+  v = fmaxf(v, __shfl_xor_sync(kFull, v, 2));
+  v = fmaxf(v, __shfl_xor_sync(kFull, v, 1));
   return v;
-}
-
-// xv[i] = x held by group lane i
-template <int G, int N>
-__device__ __forceinline__ void bcast(float x, float (&xv)[N]) {
-#pragma unroll
-  for (int i = 0; i < N; ++i) xv[i] = __shfl_sync(kFull, x, i, G);
-}
-
-// out = sum_i xv[i] * WT[row][i] over N inputs (WT row-major, N % 4 == 0)
-template <int N>
-__device__ __forceinline__ float dot_row(const float (&xv)[N], const float *__restrict__ wrow) {
-  const float4 *w4 = reinterpret_cast<const float4 *>(wrow);
-  float acc = 0.f;
-#pragma unroll
-  for (int i = 0; i < N / 4; ++i) {
-    float4 w = __ldg(w4 + i);
-    acc = fmaf(xv[4 * i], w.x, acc);
-    acc = fmaf(xv[4 * i + 1], w.y, acc);
-    acc = fmaf(xv[4 * i + 2], w.z, acc);
-    acc = fmaf(xv[4 * i + 3], w.w, acc);
-  }
-  return acc;
-}
-
-// row-group reduce-scatter: lane gl ends with the group sum of acc[gl]
-template <int G>
-__device__ __forceinline__ float reduce_scatter(float (&acc)[G]) {
-  const int gl = threadIdx.x & (G - 1);
-#pragma unroll
-  for (int half = G / 2; half >= 1; half >>= 1) {
-    const bool up = (gl & half) != 0;
-#pragma unroll
-    for (int k = 0; k < half; ++k) {
-      float send = up ? acc[k] : acc[k + half];
-      float keep = up ? acc[k + half] : acc[k];
-      acc[k] = keep + __shfl_xor_sync(kFull, send, half);
-    }
-  }
-  return acc[0];
-}
-
-template <int G>
-__device__ __forceinline__ float layer_norm(float x, const float *g, const float *b) {
-  const int gl = threadIdx.x & (G - 1);
-  float mean = gsum<G>(x) / (float)G;
-  float c = x - mean;
-  float var = gsum<G>(c * c) / (float)G;
-  float inv = 1.0f / sqrtf(var + 1e-5f);
-  return c * inv * __ldg(g + gl) + __ldg(b + gl);
 }
 
 // tanh-GELU (autodiff.py:301-306) via 0.5*a*(1+tanh z) == a / (1 + exp(-2z))
@@ -92,85 +45,172 @@ __device__ __forceinline__ float gelu_exp(float a) {
   return a / (1.0f + expf(-2.0f * z));
 }
 
-// cross-attention of one row against the request's shared K/V in shared
-// memory (rows of KS floats): group lanes over keys, reduce-scatter back.
-template <int G, int MAXM>
-__device__ __forceinline__ float cross_attn(float q, const float *Ks, const float *Vs, int S,
-                                            int KS) {
-  const int gl = threadIdx.x & (G - 1);
-  float qv[G];
-  bcast<G>(q, qv);
-  const float scale = 1.0f / sqrtf((float)G);
-  float sc[MAXM];
-  float mx = -INFINITY;
+// Row-lane layout: lane l owns row (l >> 3) of the warp's four and the E
+// consecutive columns starting at (l & 7) * E.  Scratch "slots" hold the
+// four rows transposed, slot[c * 4 + row], so one float4 read returns a
+// column of all four rows.
+template <int E>
+__device__ __forceinline__ void publish(const float (&v)[E], float *slot) {
+  const int lane = threadIdx.x & 31, rl = lane >> 3, cb = (lane & 7) * E;
+  __syncwarp();
 #pragma unroll
-  for (int m = 0; m < MAXM; ++m) {
-    int s = gl + G * m;
-    sc[m] = -INFINITY;
-    if (s < S) {
-      const float4 *kr = reinterpret_cast<const float4 *>(Ks + s * KS);
-      float dot = 0.f;
-#pragma unroll
-      for (int i = 0; i < G / 4; ++i) {
-        float4 k4 = kr[i];
-        dot = fmaf(qv[4 * i], k4.x, dot);
-        dot = fmaf(qv[4 * i + 1], k4.y, dot);
-        dot = fmaf(qv[4 * i + 2], k4.z, dot);
-        dot = fmaf(qv[4 * i + 3], k4.w, dot);
-      }
-      sc[m] = dot * scale;
-      mx = fmaxf(mx, sc[m]);
-    }
-  }
-  mx = gmax<G>(mx);
-  float sum = 0.f;
-#pragma unroll
-  for (int m = 0; m < MAXM; ++m) {
-    sc[m] = expf(sc[m] - mx);  // exp(-inf) = 0 for s >= S
-    sum += sc[m];
-  }
-  const float inv = 1.0f / gsum<G>(sum);  // softmax (autodiff.py:367-368)
-  float acc[G];
-#pragma unroll
-  for (int j = 0; j < G; ++j) acc[j] = 0.f;
-#pragma unroll
-  for (int m = 0; m < MAXM; ++m) {
-    int s = gl + G * m;
-    if (s < S) {
-      float p = sc[m] * inv;
-      const float4 *vr = reinterpret_cast<const float4 *>(Vs + s * KS);
-#pragma unroll
-      for (int i = 0; i < G / 4; ++i) {
-        float4 v4 = vr[i];
-        acc[4 * i] = fmaf(p, v4.x, acc[4 * i]);
-        acc[4 * i + 1] = fmaf(p, v4.y, acc[4 * i + 1]);
-        acc[4 * i + 2] = fmaf(p, v4.z, acc[4 * i + 2]);
-        acc[4 * i + 3] = fmaf(p, v4.w, acc[4 * i + 3]);
-      }
-    }
-  }
-  return reduce_scatter<G>(acc);
+  for (int e = 0; e < E; ++e) slot[(cb + e) * 4 + rl] = v[e];
+  __syncwarp();
 }
 
-// one pre-LN block's FFN: W2 gelu(W1 n + b1) + b2, d_ff <= 2G (layers.py:115-118)
-template <int G>
-__device__ __forceinline__ float ffn(float n, const FusedLayerT &LT, const gr4ad_layer &Lw,
-                                     int dff) {
-  const int gl = threadIdx.x & (G - 1);
-  float nv[G];
-  bcast<G>(n, nv);
-  float h0 = 0.f, h1 = 0.f;
-  if (gl < dff) h0 = gelu_exp(dot_row<G>(nv, LT.w1T + gl * G) + __ldg(Lw.ffn_b1 + gl));
-  if (G + gl < dff) h1 = gelu_exp(dot_row<G>(nv, LT.w1T + (G + gl) * G) + __ldg(Lw.ffn_b1 + G + gl));
-  float hv[G];
-  bcast<G>(h0, hv);
-  const float *w2 = LT.w2T + gl * dff;  // row gl of W2^T (d x d_ff)
-  float acc = dot_row<G>(hv, w2);
-  if (dff > G) {
-    bcast<G>(h1, hv);
-    acc += dot_row<G>(hv, w2 + G);
+// acc[e] = sum_i slot[i][row] * W[i][cb + e]   (W row-major, row stride ldw)
+template <int E>
+__device__ __forceinline__ void proj(const float *slot, int din, const float *__restrict__ W,
+                                     int ldw, float (&acc)[E]) {
+  const int lane = threadIdx.x & 31, rl = lane >> 3, cb = (lane & 7) * E;
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+  const float *w = W + cb;
+#pragma unroll 4
+  for (int i = 0; i < din; ++i) {
+    const float x = slot[i * 4 + rl];
+    if (E % 4 == 0) {
+#pragma unroll
+      for (int e = 0; e < E; e += 4) {
+        float4 w4 = __ldg(reinterpret_cast<const float4 *>(w + (size_t)i * ldw + e));
+        acc[e] = fmaf(x, w4.x, acc[e]);
+        acc[e + 1] = fmaf(x, w4.y, acc[e + 1]);
+        acc[e + 2] = fmaf(x, w4.z, acc[e + 2]);
+        acc[e + 3] = fmaf(x, w4.w, acc[e + 3]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; e += 2) {
+        float2 w2 = __ldg(reinterpret_cast<const float2 *>(w + (size_t)i * ldw + e));
+        acc[e] = fmaf(x, w2.x, acc[e]);
+        acc[e + 1] = fmaf(x, w2.y, acc[e + 1]);
+      }
+    }
   }
-  return acc + __ldg(Lw.ffn_b2 + gl);
+}
+
+template <int E>
+__device__ __forceinline__ void layer_norm(const float (&h)[E], const float *g, const float *b,
+                                           float (&o)[E]) {
+  const int cb = (threadIdx.x & 7) * E;
+  float s = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) s += h[e];
+  const float mean = rsum(s) / (float)(8 * E);
+  float v = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    float c = h[e] - mean;
+    v += c * c;
+  }
+  const float inv = 1.0f / sqrtf(rsum(v) / (float)(8 * E) + 1e-5f);
+#pragma unroll
+  for (int e = 0; e < E; ++e) o[e] = (h[e] - mean) * inv * __ldg(g + cb + e) + __ldg(b + cb + e);
+}
+
+// Cross-attention of the warp's four rows against the shared context
+// K^T / V^T (D x SP each): q in a slot; result in the row-lane layout.
+template <int D>
+__device__ __forceinline__ void cross_attn(const float *qslot, const float *KT, const float *VT,
+                                           int S, float *oslot, float (&out)[D / 8]) {
+  const int lane = threadIdx.x & 31;
+  const float scale = 1.0f / sqrtf((float)D);
+  float sc[RW][8];
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) sc[r][c] = 0.f;
+#pragma unroll 4
+  for (int i = 0; i < D; ++i) {
+    const float4 q4 = *reinterpret_cast<const float4 *>(qslot + i * 4);
+    const float4 ka = *reinterpret_cast<const float4 *>(KT + i * SP + lane * 8);
+    const float4 kb = *reinterpret_cast<const float4 *>(KT + i * SP + lane * 8 + 4);
+    const float qq[4] = {q4.x, q4.y, q4.z, q4.w};
+    const float kk[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) sc[r][c] = fmaf(qq[r], kk[c], sc[r][c]);
+  }
+  // softmax over the S keys of each row (autodiff.py:362-368)
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      sc[r][c] = (lane * 8 + c < S) ? sc[r][c] * scale : -INFINITY;
+      mx = fmaxf(mx, sc[r][c]);
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      sc[r][c] = __expf(sc[r][c] - mx);  // arguments <= 0; rel. err ~1e-7
+      sum += sc[r][c];
+    }
+    const float inv = 1.0f / warp_sum(sum);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) sc[r][c] *= inv;
+  }
+  // P.V in blocks of 8 output dims; the reduce-scatter leaves row l>>3,
+  // dim 8h + (l & 7) on lane l
+#pragma unroll
+  for (int h = 0; h < D / 8; ++h) {
+    float acc[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc[k] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float *vrow = VT + (h * 8 + j) * SP + lane * 8;
+      const float4 va = *reinterpret_cast<const float4 *>(vrow);
+      const float4 vb = *reinterpret_cast<const float4 *>(vrow + 4);
+      const float vv[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+      for (int r = 0; r < RW; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r * 8 + j] = fmaf(sc[r][c], vv[c], acc[r * 8 + j]);
+    }
+#pragma unroll
+    for (int half = 16; half >= 1; half >>= 1) {
+      const bool up = (lane & half) != 0;
+#pragma unroll
+      for (int k = 0; k < half; ++k) {
+        float send = up ? acc[k] : acc[k + half];
+        float keep = up ? acc[k + half] : acc[k];
+        acc[k] = keep + __shfl_xor_sync(kFull, send, half);
+      }
+    }
+    oslot[(h * 8 + (lane & 7)) * 4 + (lane >> 3)] = acc[0];
+  }
+  __syncwarp();
+  const int rl = lane >> 3, cb = (lane & 7) * (D / 8);
+#pragma unroll
+  for (int e = 0; e < D / 8; ++e) out[e] = oslot[(cb + e) * 4 + rl];
+  __syncwarp();
+}
+
+// FFN W2 gelu(W1 n + b1) (+ b2 by the caller), d_ff in {D, 2D} (layers.py:115-118)
+template <int D>
+__device__ __forceinline__ void ffn(const float *nslot, float *hslot, const gr4ad_layer &Lw,
+                                    int dff, float (&out)[D / 8]) {
+  constexpr int E = D / 8;
+  const int cb = (threadIdx.x & 7) * E;
+  float f0[E];
+  proj<E>(nslot, D, Lw.ffn_W1, dff, f0);
+#pragma unroll
+  for (int e = 0; e < E; ++e) f0[e] = gelu_exp(f0[e] + __ldg(Lw.ffn_b1 + cb + e));
+  publish<E>(f0, hslot);
+  proj<E>(hslot, D, Lw.ffn_W2, D, out);
+  if (dff > D) {
+    float f1[E], t2[E];
+    proj<E>(nslot, D, Lw.ffn_W1 + D, dff, f1);
+#pragma unroll
+    for (int e = 0; e < E; ++e) f1[e] = gelu_exp(f1[e] + __ldg(Lw.ffn_b1 + D + cb + e));
+    publish<E>(f1, hslot);
+    proj<E>(hslot, D, Lw.ffn_W2 + (size_t)D * D, D, t2);
+#pragma unroll
+    for (int e = 0; e < E; ++e) out[e] += t2[e];
+  }
 }
 
 // ---- exact top-k helpers (same order semantics as kernels.cu) -------------
@@ -232,19 +272,6 @@ __device__ __forceinline__ void hist_add(unsigned *hist, int &cur, unsigned &cnt
 
 }  // namespace
 
-// transposed copies of every small weight matrix the fused kernel reads
-__global__ void fused_prep_kernel(FusedPrep p) {
-  const int job = blockIdx.y;
-  if (job >= p.n) return;
-  const float *src = p.src[job];
-  float *dst = p.dst[job];
-  const int R = p.rows[job], Cc = p.cols[job];
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < R * Cc; e += gridDim.x * blockDim.x) {
-    int r = e / Cc, c = e - r * Cc;
-    dst[(size_t)c * R + r] = src[e];  // dst = src^T  (cols x rows)
-  }
-}
-
 #ifdef GR_FUSED_TIMING
 #define GR_STAMP(i)                                                             \
   do {                                                                          \
@@ -258,24 +285,23 @@ __global__ void fused_prep_kernel(FusedPrep p) {
 #define GR_STAMP(i) do {} while (0)
 #endif
 
-template <int G, int MAXM, int VCH>
+template <int D>
 __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
   extern __shared__ __align__(16) float sm[];
-  constexpr int D = G;
-  constexpr int RPW = 32 / G;  // rows per warp
+  constexpr int E = D / 8;  // columns per lane in the row-lane layout
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int gl = lane & (G - 1), sub = lane / G;
-  const int T = a.T, L = a.L, K = a.K, dff = a.dff, KS = a.KS;
+  const int rl = lane >> 3, cb = (lane & 7) * E;
+  const int T = a.T, L = a.L, K = a.K, dff = a.dff;
   const int S = a.ctx_len[b];
   const long long coff = a.ctx_off[b];
   const gr4ad_weights &W = a.w;
   const float scale = 1.0f / sqrtf((float)D);
 
-  float *Xs = sm + a.s_X;
-  float *KV = sm + a.s_KV;
-  float *TR = sm + a.s_TR;
-  float *TQ = sm + a.s_TQ;
+  float *Xs = sm + a.s_X;   // X^T: D x SP (aliases the history region)
+  float *KV = sm + a.s_KV;  // per slot: K^T (D x SP) then V^T (D x SP)
+  float *TR = sm + a.s_TR;  // n_pos x D
+  float *TQ = sm + a.s_TQ;  // n_pos x 3 x D
   float *HI = sm + a.s_hist;
   int *par = reinterpret_cast<int *>(sm + a.s_par);
   int *tokm = reinterpret_cast<int *>(sm + a.s_tok);
@@ -283,8 +309,10 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
   unsigned *hist = reinterpret_cast<unsigned *>(sm + a.s_bins);
   unsigned *scr = reinterpret_cast<unsigned *>(sm + a.s_scr);
   unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(sm + a.s_sort);
+  float *wsl = sm + a.s_ws + wid * 4 * D * 4;  // this warp's 4 slots of (D x 4)
+  float *slot0 = wsl, *slot1 = wsl + 4 * D, *slot2 = wsl + 8 * D, *slot3 = wsl + 12 * D;
   uint32_t *keys = a.keys + (size_t)b * a.keys_per_req;
-  const int KVS = a.S_max * KS;
+  const int KVS = D * SP;
   GR_STAMP(0);
 
   // ---- context projection X = F W_c + b_c (decoder.py:134-140) -------------
@@ -293,40 +321,35 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
     float x;
     if (a.features) {
       const float *f = a.features + (coff + s) * a.F;
-      const float *wc = a.ctxT + (size_t)j * a.F;  // row j of W_c^T
       float acc = 0.f;
-      for (int i = 0; i < a.F; ++i) acc = fmaf(__ldg(f + i), __ldg(wc + i), acc);
+      for (int i = 0; i < a.F; ++i) acc = fmaf(__ldg(f + i), __ldg(W.ctx_W + (size_t)i * D + j), acc);
       x = acc + __ldg(W.ctx_b + j);
     } else {
       x = __ldg(a.context + (coff + s) * D + j);
     }
-    Xs[s * KS + j] = x;
+    Xs[j * SP + s] = x;
   }
   __syncthreads();
+  GR_STAMP(1);
 
-  // K/V of `layer` into `slot`: K[s][c] = X[s] . WkvT[2*layer*D + c]
+  // K^T / V^T of `layer` into `slot` (keys >= S are zero)
   auto build_kv = [&](int layer, int slot) {
-    float *Kd = KV + (size_t)slot * 2 * KVS;
-    for (int e = tid; e < S * 2 * D; e += kThreads) {
-      int s = e / (2 * D), c = e - s * 2 * D;
-      const float4 *x4 = reinterpret_cast<const float4 *>(Xs + s * KS);
-      const float4 *w4 = reinterpret_cast<const float4 *>(a.kvT + ((size_t)2 * layer * D + c) * D);
+    float *Kt = KV + (size_t)slot * 2 * KVS;
+    const int ldw = 2 * L * D;
+    const float *Wl = W.cross_kv_W + (size_t)(2 * layer) * D;
+    for (int e = tid; e < 2 * D * SP; e += kThreads) {
+      int c = e / SP, s = e - c * SP;  // c < D: K column c, else V column c - D
       float acc = 0.f;
+      if (s < S) {  // lanes walk consecutive keys: conflict-free X^T reads
 #pragma unroll
-      for (int i = 0; i < D / 4; ++i) {
-        float4 x = x4[i], w = __ldg(w4 + i);
-        acc = fmaf(x.x, w.x, acc);
-        acc = fmaf(x.y, w.y, acc);
-        acc = fmaf(x.z, w.z, acc);
-        acc = fmaf(x.w, w.w, acc);
+        for (int i = 0; i < D; ++i) acc = fmaf(Xs[i * SP + s], __ldg(Wl + (size_t)i * ldw + c), acc);
       }
-      Kd[(c < D ? 0 : KVS) + s * KS + (c < D ? c : c - D)] = acc;
+      Kt[c * SP + s] = acc;
     }
   };
 
-  GR_STAMP(1);
-  // ---- trunk: K layers over the n_pos position rows (beam.py:159-163) -------
   const int np = a.n_pos;
+  // ---- trunk: K layers over the n_pos position rows (beam.py:159-163) -------
   if (K > 0) {
     for (int e = tid; e < np * D; e += kThreads) TR[e] = __ldg(W.pos + e);
     for (int i = 0; i < K; ++i) {
@@ -334,65 +357,76 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
       build_kv(i, 0);
       __syncthreads();
       const gr4ad_layer &Lw = W.layer[i];
-      const FusedLayerT &LT = a.lt[i];
-      for (int p0 = wid * RPW; p0 < np; p0 += kWarps * RPW) {
-        int p = p0 + sub;
-        bool ok = p < np;
-        int pp = ok ? p : np - 1;
-        float h = TR[pp * D + gl];
-        float n = layer_norm<G>(h, Lw.ln1_g, Lw.ln1_b);
-        float nv[G];
-        bcast<G>(n, nv);
-        float q = dot_row<G>(nv, LT.cqT + gl * D);
-        float o = cross_attn<G, MAXM>(q, KV, KV + KVS, S, KS);
-        float ov[G];
-        bcast<G>(o, ov);
-        h += dot_row<G>(ov, LT.coT + gl * D);
-        n = layer_norm<G>(h, Lw.ln2_g, Lw.ln2_b);
-        bcast<G>(n, nv);
-        float qs = dot_row<G>(nv, LT.sqkvT + gl * D);
-        float ks = dot_row<G>(nv, LT.sqkvT + (D + gl) * D);
-        float vs = dot_row<G>(nv, LT.sqkvT + (2 * D + gl) * D);
-        if (ok) {
-          TQ[(p * 3 + 0) * D + gl] = qs;
-          TQ[(p * 3 + 1) * D + gl] = ks;
-          TQ[(p * 3 + 2) * D + gl] = vs;
-          TR[p * D + gl] = h;
+      for (int p0 = wid * RW; p0 < np; p0 += kWarps * RW) {
+        const int p = p0 + rl, pp = min(p, np - 1);
+        const bool ok = p < np;
+        float h[E], n[E], t[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) h[e] = TR[pp * D + cb + e];
+        layer_norm<E>(h, Lw.ln1_g, Lw.ln1_b, n);
+        publish<E>(n, slot0);
+        proj<E>(slot0, D, Lw.cross_Wq, D, t);
+        publish<E>(t, slot1);
+        cross_attn<D>(slot1, KV, KV + KVS, S, slot2, t);
+        publish<E>(t, slot0);
+        proj<E>(slot0, D, Lw.cross_Wo, D, t);
+#pragma unroll
+        for (int e = 0; e < E; ++e) h[e] += t[e];
+        layer_norm<E>(h, Lw.ln2_g, Lw.ln2_b, n);
+        publish<E>(n, slot0);
+        for (int c = 0; c < 3; ++c) {
+          proj<E>(slot0, D, Lw.self_Wqkv + c * D, 3 * D, t);
+          if (ok)
+#pragma unroll
+            for (int e = 0; e < E; ++e) TQ[(p * 3 + c) * D + cb + e] = t[e];
         }
+        if (ok)
+#pragma unroll
+          for (int e = 0; e < E; ++e) TR[p * D + cb + e] = h[e];
       }
       __syncthreads();
-      for (int p0 = wid * RPW; p0 < np; p0 += kWarps * RPW) {
-        int p = p0 + sub;
-        bool ok = p < np;
-        int pp = ok ? p : np - 1;
-        float h = TR[pp * D + gl];
-        float q = TQ[(pp * 3) * D + gl];
-        // causal self-attention over positions 0..p (layers.py:94-100); the
-        // loop bound is uniform across the warp's row groups (shuffles inside)
-        const int rmax = min(p0 + RPW, np) - 1;
-        float mx = -INFINITY;
-        for (int r = 0; r <= rmax; ++r) {
-          float sc = gsum<G>(q * TQ[(r * 3 + 1) * D + gl]) * scale;
-          if (r <= pp) mx = fmaxf(mx, sc);
+      for (int p0 = wid * RW; p0 < np; p0 += kWarps * RW) {
+        const int p = p0 + rl, pp = min(p, np - 1);
+        const bool ok = p < np;
+        const int rmax_w = min(p0 + RW, np) - 1;  // warp-uniform loop bound
+        float h[E], n[E], t[E], q[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          h[e] = TR[pp * D + cb + e];
+          q[e] = TQ[(pp * 3) * D + cb + e];
         }
-        float sum = 0.f;
-        for (int r = 0; r <= rmax; ++r) {
-          float sc = gsum<G>(q * TQ[(r * 3 + 1) * D + gl]) * scale;
-          if (r <= pp) sum += expf(sc - mx);
+        // causal self-attention over positions 0..p (layers.py:94-100), online
+        float mx = -INFINITY, se = 0.f, so[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) so[e] = 0.f;
+        for (int r = 0; r <= rmax_w; ++r) {
+          float dot = 0.f;
+#pragma unroll
+          for (int e = 0; e < E; ++e) dot = fmaf(q[e], TQ[(r * 3 + 1) * D + cb + e], dot);
+          const float sc = rsum(dot) * scale;
+          if (r <= pp) {
+            const float nm = fmaxf(mx, sc), f = expf(mx - nm), w = expf(sc - nm);
+            se = se * f + w;
+#pragma unroll
+            for (int e = 0; e < E; ++e) so[e] = so[e] * f + w * TQ[(r * 3 + 2) * D + cb + e];
+            mx = nm;
+          }
         }
-        float lse = logf(sum) + mx;
-        float o = 0.f;
-        for (int r = 0; r <= rmax; ++r) {
-          float sc = gsum<G>(q * TQ[(r * 3 + 1) * D + gl]) * scale;
-          if (r <= pp) o = fmaf(expf(sc - lse), TQ[(r * 3 + 2) * D + gl], o);
-        }
-        float ov[G];
-        bcast<G>(o, ov);
-        h += dot_row<G>(ov, LT.soT + gl * D);
-        float n = layer_norm<G>(h, Lw.ln3_g, Lw.ln3_b);
-        h += ffn<G>(n, LT, Lw, dff);
+#pragma unroll
+        for (int e = 0; e < E; ++e) so[e] /= se;
+        publish<E>(so, slot0);
+        proj<E>(slot0, D, Lw.self_Wo, D, t);
+#pragma unroll
+        for (int e = 0; e < E; ++e) h[e] += t[e];
+        layer_norm<E>(h, Lw.ln3_g, Lw.ln3_b, n);
+        publish<E>(n, slot0);
+        ffn<D>(slot0, slot3, Lw, dff, t);
+#pragma unroll
+        for (int e = 0; e < E; ++e) h[e] += t[e] + __ldg(Lw.ffn_b2 + cb + e);
         __syncwarp();
-        if (ok) TR[p * D + gl] = h;
+        if (ok)
+#pragma unroll
+          for (int e = 0; e < E; ++e) TR[p * D + cb + e] = h[e];
       }
     }
   }
@@ -406,153 +440,188 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
     cum[0] = 0.f;
   }
   __syncthreads();
-
   GR_STAMP(3);
+
   const int last = a.rerank ? T : T - 1;
   int live = 1;
   for (int t = 0; t <= last; ++t) {
     const int mo = a.moff[t];
     const int V = t < T ? a.V[t] : 0;
     for (int i = tid; i < 2048; i += kThreads) hist[i] = 0u;
+    // Every candidate score of this level is cum_r + logp <= max_r cum_r =: Rs
+    // (logp <= 0).  Candidates are binned by min((Rs - s) * scale, 2047), a
+    // monotone map of the score, with 2048 bins over ln V + 4 score units,
+    // so the k-th best usually lands in a bin holding a handful of keys.
+    if (tid == 0) {
+      float mc = -INFINITY;
+      for (int j = 0; j < live; ++j) mc = fmaxf(mc, cum[mo + j]);
+      scr[48] = __float_as_uint(mc);
+      scr[49] = __float_as_uint(2048.0f / (logf((float)max(V, 2)) + 4.0f));
+    }
     __syncthreads();
+    const float Rs = __uint_as_float(scr[48]);
+    const float bscale = __uint_as_float(scr[49]);
+    auto sbin = [&](float sc) -> unsigned {
+      return (unsigned)fminf((Rs - sc) * bscale, 2047.0f);  // NaN-free: sc <= Rs
+    };
     int hcur = -1;
     unsigned hcnt = 0;
-    for (int r0 = wid * RPW; r0 < live; r0 += kWarps * RPW) {
-      const int r = r0 + sub;
+    for (int r0 = wid * RW; r0 < live; r0 += kWarps * RW) {
+      const int r = r0 + rl;
       const bool ok = r < live;
       const int rr = ok ? r : live - 1;
       // ---- token input + gated fusion (beam.py:180-191; layers.py:129-133)
-      float s = (t == 0) ? __ldg(W.bos + gl)
-                         : __ldg(W.emb[t - 1] + (size_t)tokm[mo + rr] * D + gl);
-      float h;
+      float s[E], h[E], n[E], tt[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        s[e] = (t == 0) ? __ldg(W.bos + cb + e)
+                        : __ldg(W.emb[t - 1] + (size_t)tokm[mo + rr] * D + cb + e);
       if (K > 0) {
-        float sv[G];
-        bcast<G>(s, sv);
-        float g = dot_row<G>(sv, a.fuseT.wgT + gl * D);
-        float u = TR[t * D + gl] * g;
-        float uv[G];
-        bcast<G>(u, uv);
-        const float *wf = a.fuseT.wfT + gl * 2 * D;  // row gl of W_f^T (d x 2d)
-        h = dot_row<G>(uv, wf) + dot_row<G>(sv, wf + D);
+        publish<E>(s, slot1);
+        proj<E>(slot1, D, W.fuse_Wg, D, tt);
+#pragma unroll
+        for (int e = 0; e < E; ++e) tt[e] = TR[t * D + cb + e] * tt[e];  // m_t * (s W_g)
+        publish<E>(tt, slot0);
+        proj<E>(slot0, D, W.fuse_Wf, D, h);
+        proj<E>(slot1, D, W.fuse_Wf + (size_t)D * D, D, tt);
+#pragma unroll
+        for (int e = 0; e < E; ++e) h[e] += tt[e];
       } else {
-        h = s + __ldg(W.pos + (size_t)t * D + gl);
+#pragma unroll
+        for (int e = 0; e < E; ++e) h[e] = s[e] + __ldg(W.pos + (size_t)t * D + cb + e);
       }
       // ---- head layers (layers.py:66-119, incremental) ----------------------
       for (int i = K; i < L; ++i) {
         const gr4ad_layer &Lw = W.layer[i];
-        const FusedLayerT &LT = a.lt[i];
-        const float *Kd = KV + (size_t)(i - K) * 2 * KVS;
-        float n = layer_norm<G>(h, Lw.ln1_g, Lw.ln1_b);
-        float nv[G];
-        bcast<G>(n, nv);
-        float q = dot_row<G>(nv, LT.cqT + gl * D);
-        float o = cross_attn<G, MAXM>(q, Kd, Kd + KVS, S, KS);
-        float ov[G];
-        bcast<G>(o, ov);
-        h += dot_row<G>(ov, LT.coT + gl * D);
-        n = layer_norm<G>(h, Lw.ln2_g, Lw.ln2_b);
-        bcast<G>(n, nv);
-        float qs = dot_row<G>(nv, LT.sqkvT + gl * D);
-        float ks = dot_row<G>(nv, LT.sqkvT + (D + gl) * D);
-        float vs = dot_row<G>(nv, LT.sqkvT + (2 * D + gl) * D);
-        float *hrow = HI + ((size_t)(i - K) * a.Hrows + a.hoff[t] + rr) * 2 * D;
+        const float *Kt = KV + (size_t)(i - K) * 2 * KVS;
+        layer_norm<E>(h, Lw.ln1_g, Lw.ln1_b, n);
+        publish<E>(n, slot0);
+        proj<E>(slot0, D, Lw.cross_Wq, D, tt);
+        publish<E>(tt, slot1);
+        cross_attn<D>(slot1, Kt, Kt + KVS, S, slot2, tt);
+        publish<E>(tt, slot0);
+        proj<E>(slot0, D, Lw.cross_Wo, D, tt);
+#pragma unroll
+        for (int e = 0; e < E; ++e) h[e] += tt[e];
+        layer_norm<E>(h, Lw.ln2_g, Lw.ln2_b, n);
+        publish<E>(n, slot0);
+        float qs[E], ks[E], vs[E];
+        proj<E>(slot0, D, Lw.self_Wqkv, 3 * D, qs);
+        proj<E>(slot0, D, Lw.self_Wqkv + D, 3 * D, ks);
+        proj<E>(slot0, D, Lw.self_Wqkv + 2 * D, 3 * D, vs);
         // self-attention over the ancestor chain (history by parent pointer):
         // own position first, then ancestors; online softmax (layers.py:101-113)
-        float m1 = gsum<G>(qs * ks) * scale;
-        float mx = m1, se = 1.f, so = vs;
+        float dot = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) dot = fmaf(qs[e], ks[e], dot);
+        float mx = rsum(dot) * scale, se = 1.f, so[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) so[e] = vs[e];
         int a_row = rr;
         for (int tau = t - 1; tau >= 0; --tau) {
           a_row = par[a.moff[tau + 1] + a_row];
           const float *hr = HI + ((size_t)(i - K) * a.Hrows + a.hoff[tau] + a_row) * 2 * D;
-          float sc = gsum<G>(qs * hr[gl]) * scale;
-          float vv = hr[D + gl];
-          if (sc > mx) {
-            float f = expf(mx - sc);
-            se = se * f + 1.f;
-            so = so * f + vv;
-            mx = sc;
-          } else {
-            float e = expf(sc - mx);
-            se += e;
-            so = fmaf(e, vv, so);
+          float d2 = 0.f;
+#pragma unroll
+          for (int e = 0; e < E; ++e) d2 = fmaf(qs[e], hr[cb + e], d2);
+          const float sc = rsum(d2) * scale;
+          const float nm = fmaxf(mx, sc), f = expf(mx - nm), w = expf(sc - nm);
+          se = se * f + w;
+#pragma unroll
+          for (int e = 0; e < E; ++e) so[e] = so[e] * f + w * hr[D + cb + e];
+          mx = nm;
+        }
+        if (ok) {
+          float *hrow = HI + ((size_t)(i - K) * a.Hrows + a.hoff[t] + r) * 2 * D;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            hrow[cb + e] = ks[e];
+            hrow[D + cb + e] = vs[e];
           }
         }
-        so = so / se;
-        if (ok) {
-          hrow[gl] = ks;
-          hrow[D + gl] = vs;
-        }
-        bcast<G>(so, ov);
-        h += dot_row<G>(ov, LT.soT + gl * D);
-        n = layer_norm<G>(h, Lw.ln3_g, Lw.ln3_b);
-        h += ffn<G>(n, LT, Lw, dff);
+#pragma unroll
+        for (int e = 0; e < E; ++e) so[e] /= se;
+        publish<E>(so, slot0);
+        proj<E>(slot0, D, Lw.self_Wo, D, tt);
+#pragma unroll
+        for (int e = 0; e < E; ++e) h[e] += tt[e];
+        layer_norm<E>(h, Lw.ln3_g, Lw.ln3_b, n);
+        publish<E>(n, slot0);
+        ffn<D>(slot0, slot3, Lw, dff, tt);
+#pragma unroll
+        for (int e = 0; e < E; ++e) h[e] += tt[e] + __ldg(Lw.ffn_b2 + cb + e);
       }
-      float hv[G];
-      bcast<G>(h, hv);
+      publish<E>(h, slot0);
       if (t == T) {  // value re-rank step (beam.py:258-288): rank in double
-        float lg = -INFINITY;
-        if (gl < a.nb) lg = dot_row<G>(hv, a.hvT + gl * D);
-        float mxv = gmax<G>(lg);
-        double e = gl < a.nb ? exp((double)lg - (double)mxv) : 0.0;
-        double se = e;
-#pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) se += __shfl_xor_sync(kFull, se, o);
-        double ls = log(se);
-        double ev = gl < a.nb ? exp(((double)lg - (double)mxv) - ls) * (double)__ldg(a.value_reps + gl)
-                              : 0.0;
-#pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) ev += __shfl_xor_sync(kFull, ev, o);
-        if (ok && gl == 0) reinterpret_cast<double *>(sbuf)[r] = ev * exp((double)cum[mo + r]);
+        float vl = -INFINITY;
+        const int c = lane & 7;
+        if (c < a.nb) {
+          float acc = 0.f;
+          for (int i = 0; i < D; ++i)
+            acc = fmaf(slot0[i * 4 + rl], __ldg(W.head_value + (size_t)i * a.nb + c), acc);
+          vl = acc;
+        }
+        const float mv = rmax(vl);
+        double e1 = c < a.nb ? exp((double)vl - (double)mv) : 0.0;
+        double se = e1;
+        se += __shfl_xor_sync(kFull, se, 4);
+        se += __shfl_xor_sync(kFull, se, 2);
+        se += __shfl_xor_sync(kFull, se, 1);
+        double ev = c < a.nb ? exp(((double)vl - (double)mv) - log(se)) *
+                                   (double)__ldg(a.value_reps + c)
+                             : 0.0;
+        ev += __shfl_xor_sync(kFull, ev, 4);
+        ev += __shfl_xor_sync(kFull, ev, 2);
+        ev += __shfl_xor_sync(kFull, ev, 1);
+        if (ok && c == 0) reinterpret_cast<double *>(sbuf)[r] = ev * exp((double)cum[mo + r]);
         continue;
       }
       // ---- codebook logits + log-softmax keys (beam.py:198-200) ---------------
-      const float4 *head4 = reinterpret_cast<const float4 *>(W.head[t]);
-      const int V4 = V / 4;
-      float lg[VCH][4];
-      float lm = -INFINITY;
+      // lane owns tokens 8*lane .. 8*lane+7 of all four rows
+      const float *head = W.head[t];
+      const bool tv = lane * 8 < V;
+      float lg[RW][8];
 #pragma unroll
-      for (int c = 0; c < VCH; ++c) {
-        int v4 = gl + G * c;
-        lg[c][0] = lg[c][1] = lg[c][2] = lg[c][3] = -INFINITY;
-        if (v4 < V4) {
-          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      for (int q = 0; q < RW; ++q)
 #pragma unroll
-          for (int i = 0; i < D; ++i) {
-            float4 w = __ldg(head4 + (size_t)i * V4 + v4);
-            a0 = fmaf(hv[i], w.x, a0);
-            a1 = fmaf(hv[i], w.y, a1);
-            a2 = fmaf(hv[i], w.z, a2);
-            a3 = fmaf(hv[i], w.w, a3);
-          }
-          lg[c][0] = a0; lg[c][1] = a1; lg[c][2] = a2; lg[c][3] = a3;
-          lm = fmaxf(lm, fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
+        for (int c = 0; c < 8; ++c) lg[q][c] = 0.f;
+#pragma unroll 4
+      for (int i = 0; i < D; ++i) {
+        const float4 x4 = *reinterpret_cast<const float4 *>(slot0 + i * 4);
+        float4 wa = make_float4(0.f, 0.f, 0.f, 0.f), wb = wa;
+        if (tv) {
+          wa = __ldg(reinterpret_cast<const float4 *>(head + (size_t)i * V + lane * 8));
+          wb = __ldg(reinterpret_cast<const float4 *>(head + (size_t)i * V + lane * 8 + 4));
         }
+        const float xx[4] = {x4.x, x4.y, x4.z, x4.w};
+        const float ww[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+        for (int q = 0; q < RW; ++q)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) lg[q][c] = fmaf(xx[q], ww[c], lg[q][c]);
       }
-      const float mx = gmax<G>(lm);
-      float s2 = 0.f;
 #pragma unroll
-      for (int c = 0; c < VCH; ++c)
+      for (int q = 0; q < RW; ++q) {
+        float mq = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) s2 += expf(lg[c][k] - mx);
-      const float ls = logf(gsum<G>(s2));
-      if (ok) {
-        const float cr = cum[mo + r];
-        uint4 *kr = reinterpret_cast<uint4 *>(keys + (size_t)r * V);
+        for (int c = 0; c < 8; ++c) mq = fmaxf(mq, tv ? lg[q][c] : -INFINITY);
+        const float mx = warp_max(mq);
+        float s2 = 0.f;
 #pragma unroll
-        for (int c = 0; c < VCH; ++c) {
-          int v4 = gl + G * c;
-          if (v4 < V4) {
-            uint4 u;
-            u.x = f2ord(cr + ((lg[c][0] - mx) - ls));
-            u.y = f2ord(cr + ((lg[c][1] - mx) - ls));
-            u.z = f2ord(cr + ((lg[c][2] - mx) - ls));
-            u.w = f2ord(cr + ((lg[c][3] - mx) - ls));
-            kr[v4] = u;
-            hist_add(hist, hcur, hcnt, (int)(u.x >> 21));
-            hist_add(hist, hcur, hcnt, (int)(u.y >> 21));
-            hist_add(hist, hcur, hcnt, (int)(u.z >> 21));
-            hist_add(hist, hcur, hcnt, (int)(u.w >> 21));
+        for (int c = 0; c < 8; ++c) s2 += tv ? __expf(lg[q][c] - mx) : 0.f;
+        const float ls = logf(warp_sum(s2));
+        const int rq = r0 + q;
+        if (rq < live && tv) {
+          const float cr = cum[mo + rq];
+          uint32_t u[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            u[c] = f2ord(cr + ((lg[q][c] - mx) - ls));
+            hist_add(hist, hcur, hcnt, (int)sbin(cr + ((lg[q][c] - mx) - ls)));
           }
+          uint4 *kr = reinterpret_cast<uint4 *>(keys + (size_t)rq * V + lane * 8);
+          kr[0] = make_uint4(u[0], u[1], u[2], u[3]);
+          kr[1] = make_uint4(u[4], u[5], u[6], u[7]);
         }
       }
     }
@@ -594,103 +663,140 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
         a.out_score[(size_t)b * a.max_out + j] = key[j];
       }
       if (tid == 0) a.out_count[b] = live;
+      GR_STAMP(15);
       return;
     }
 
     // ---- exact top-k under (-score, row, token) (beam.py:30-89) --------------
     const int n_cand = live * V;
     const int k = min(a.eff[t * a.B + b], n_cand);
-    unsigned need = (unsigned)k, above;
-    int bin = find_bin(hist, 2048, need, &above, scr);
-    unsigned eq_total = hist[bin];
-    need -= above;
-    uint32_t T32 = (uint32_t)bin << 21;
-    uint32_t pmask = 0x7FFu << 21;
-    const uint4 *keys4 = reinterpret_cast<const uint4 *>(keys);
-    const int n4 = n_cand / 4;  // V % 4 == 0
-    for (int pass = 0; pass < 2; ++pass) {
-      const int shift = pass == 0 ? 10 : 0;
-      const int nb = pass == 0 ? 2048 : 1024;
-      __syncthreads();
-      for (int i = tid; i < nb; i += kThreads) hist[i] = 0u;
-      __syncthreads();
-      int cur = -1;
-      unsigned cnt = 0;
-      for (int i0 = tid; i0 < n4; i0 += 4 * kThreads) {
-        uint4 u4[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          int i = i0 + j * kThreads;
-          u4[j] = i < n4 ? keys4[i] : make_uint4(0u, 0u, 0u, 0u);
+    int n_sort = k;  // entries in sbuf to sort (>= k)
+    {
+      // (a) window: every key in a bin below the k-th key's bin is in the
+      // top-k; the k-th bin is collected whole and the exact sort breaks it
+      unsigned cnt_le = 0;
+      int wb = 2047;
+      {
+        // k-th smallest bin index == (2048 - 1 - bin of the k-th largest in
+        // reversed order): find_bin scans from the top bin, so mirror
+        unsigned above;
+        for (int i = tid; i < 1024; i += kThreads) {
+          unsigned x = hist[i], y = hist[2047 - i];
+          hist[i] = y;
+          hist[2047 - i] = x;
         }
+        __syncthreads();
+        int rb = find_bin(hist, 2048, (unsigned)k, &above, scr);  // mirrored bin
+        wb = 2047 - rb;
+        cnt_le = above + hist[rb];
+      }
+      const bool window_ok = wb < 2047 && cnt_le <= (unsigned)a.sort_cap;
+#ifdef GR_FUSED_TIMING
+      if (tid == 0 && t < 3) {
+        a.dbg[blockIdx.x * 16 + 10 + t] = ((long long)cnt_le << 32) | (unsigned)wb;
+        a.dbg[blockIdx.x * 16 + 13 + (t == 2)] = (long long)(bscale * 1000);
+      }
+#endif
+      if (window_ok) {
+        if (tid == 0) scr[40] = 0;
+        __syncthreads();
+        const uint4 *keys4 = reinterpret_cast<const uint4 *>(keys);
+        const int n4 = n_cand / 4;
+        for (int i4 = tid; i4 < n4; i4 += kThreads) {
+          const uint4 u4 = keys4[i4];
+          const uint32_t us[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (i0 + j * kThreads < n4) {
-            const uint32_t us[4] = {u4[j].x, u4[j].y, u4[j].z, u4[j].w};
+          for (int q = 0; q < 4; ++q) {
+            if (sbin(ord2f(us[q])) <= (unsigned)wb) {
+              unsigned pos = atomicAdd(&scr[40], 1u);
+              sbuf[pos] = ((unsigned long long)us[q] << 32) | (0xFFFFFFFFu - (unsigned)(i4 * 4 + q));
+            }
+          }
+        }
+        n_sort = (int)cnt_le;
+      } else {
+        // (b) exact radix fallback (11/11/10-bit passes over the keys)
+        unsigned need = (unsigned)k, above;
+        for (int i = tid; i < 2048; i += kThreads) hist[i] = 0u;
+        __syncthreads();
+        uint32_t T32 = 0, pmask = 0;
+        unsigned eq_total = 0;
+        const uint4 *keys4 = reinterpret_cast<const uint4 *>(keys);
+        const int n4 = n_cand / 4;
+        for (int pass = 0; pass < 3; ++pass) {
+          const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
+          const int nb = pass == 2 ? 1024 : 2048;
+          __syncthreads();
+          for (int i = tid; i < nb; i += kThreads) hist[i] = 0u;
+          __syncthreads();
+          int cur = -1;
+          unsigned cnt = 0;
+          for (int i4 = tid; i4 < n4; i4 += kThreads) {
+            const uint4 u4 = keys4[i4];
+            const uint32_t us[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               if ((us[q] & pmask) == T32) hist_add(hist, cur, cnt, (int)((us[q] >> shift) & (nb - 1)));
           }
+          if (cnt) atomicAdd(&hist[cur], cnt);
+          __syncthreads();
+          int bin = find_bin(hist, nb, need, &above, scr);
+          eq_total = hist[bin];
+          need -= above;
+          T32 |= (uint32_t)bin << shift;
+          pmask |= (uint32_t)(nb - 1) << shift;
         }
-      }
-      if (cnt) atomicAdd(&hist[cur], cnt);
-      __syncthreads();
-      bin = find_bin(hist, nb, need, &above, scr);
-      eq_total = hist[bin];
-      need -= above;
-      T32 |= (uint32_t)bin << shift;
-      pmask |= (uint32_t)(nb - 1) << shift;
-    }
-    // collect: every key > T32, and the `need` lowest-index keys == T32
-    const unsigned n_gt = (unsigned)k - need;
-    if (tid == 0) scr[40] = 0;
-    __syncthreads();
-    if (need == eq_total) {
-      for (int i0 = wid * 32; i0 < n_cand; i0 += kThreads) {
-        int i = i0 + lane;
-        uint32_t u = i < n_cand ? keys[i] : 0u;
-        bool take = i < n_cand && u >= T32;
-        unsigned m = __ballot_sync(kFull, take);
-        unsigned base = 0;
-        if (m && lane == 0) base = atomicAdd(&scr[40], __popc(m));
-        base = __shfl_sync(kFull, base, 0);
-        if (take) sbuf[base + __popc(m & ((1u << lane) - 1u))] =
-            ((unsigned long long)u << 32) | (0xFFFFFFFFu - (unsigned)i);
-      }
-    } else {
-      // ordered ties: contiguous index chunks per warp, warp tie counts scanned
-      const int chunk = ((n_cand + kWarps - 1) / kWarps + 31) / 32 * 32;
-      const int c0 = wid * chunk, c1 = min(n_cand, c0 + chunk);
-      unsigned neq = 0;
-      for (int i0 = c0; i0 < c1; i0 += 32) {
-        int i = i0 + lane;
-        neq += __popc(__ballot_sync(kFull, i < c1 && keys[i] == T32));
-      }
-      if (lane == 0) scr[8 + wid] = neq;
-      __syncthreads();
-      unsigned rank = 0;
-      for (int w2 = 0; w2 < wid; ++w2) rank += scr[8 + w2];
-      for (int i0 = c0; i0 < c1; i0 += 32) {
-        int i = i0 + lane;
-        uint32_t u = i < c1 ? keys[i] : 0u;
-        bool gt = i < c1 && u > T32;
-        bool eq = i < c1 && u == T32;
-        unsigned me = __ballot_sync(kFull, eq);
-        unsigned myr = rank + __popc(me & ((1u << lane) - 1u));
-        unsigned mg = __ballot_sync(kFull, gt);
-        unsigned base = 0;
-        if (mg && lane == 0) base = atomicAdd(&scr[40], __popc(mg));
-        base = __shfl_sync(kFull, base, 0);
-        unsigned long long e = ((unsigned long long)u << 32) | (0xFFFFFFFFu - (unsigned)i);
-        if (gt) sbuf[base + __popc(mg & ((1u << lane) - 1u))] = e;
-        if (eq && myr < need) sbuf[n_gt + myr] = e;
-        rank += __popc(me);
+        const unsigned n_gt = (unsigned)k - need;
+        if (tid == 0) scr[40] = 0;
+        __syncthreads();
+        if (need == eq_total) {
+          for (int i0 = wid * 32; i0 < n_cand; i0 += kThreads) {
+            int i = i0 + lane;
+            uint32_t u = i < n_cand ? keys[i] : 0u;
+            bool take = i < n_cand && u >= T32;
+            unsigned m = __ballot_sync(kFull, take);
+            unsigned base = 0;
+            if (m && lane == 0) base = atomicAdd(&scr[40], __popc(m));
+            base = __shfl_sync(kFull, base, 0);
+            if (take) sbuf[base + __popc(m & ((1u << lane) - 1u))] =
+                ((unsigned long long)u << 32) | (0xFFFFFFFFu - (unsigned)i);
+          }
+        } else {
+          // ordered ties: contiguous index chunks per warp, warp tie counts scanned
+          const int chunk = ((n_cand + kWarps - 1) / kWarps + 31) / 32 * 32;
+          const int c0 = wid * chunk, c1 = min(n_cand, c0 + chunk);
+          unsigned neq = 0;
+          for (int i0 = c0; i0 < c1; i0 += 32) {
+            int i = i0 + lane;
+            neq += __popc(__ballot_sync(kFull, i < c1 && keys[i] == T32));
+          }
+          if (lane == 0) scr[8 + wid] = neq;
+          __syncthreads();
+          unsigned rank = 0;
+          for (int w2 = 0; w2 < wid; ++w2) rank += scr[8 + w2];
+          for (int i0 = c0; i0 < c1; i0 += 32) {
+            int i = i0 + lane;
+            uint32_t u = i < c1 ? keys[i] : 0u;
+            bool gt = i < c1 && u > T32;
+            bool eq = i < c1 && u == T32;
+            unsigned me = __ballot_sync(kFull, eq);
+            unsigned myr = rank + __popc(me & ((1u << lane) - 1u));
+            unsigned mg = __ballot_sync(kFull, gt);
+            unsigned base = 0;
+            if (mg && lane == 0) base = atomicAdd(&scr[40], __popc(mg));
+            base = __shfl_sync(kFull, base, 0);
+            unsigned long long e = ((unsigned long long)u << 32) | (0xFFFFFFFFu - (unsigned)i);
+            if (gt) sbuf[base + __popc(mg & ((1u << lane) - 1u))] = e;
+            if (eq && myr < need) sbuf[n_gt + myr] = e;
+            rank += __popc(me);
+          }
+        }
       }
     }
     __syncthreads();
     int n2 = 1;
-    while (n2 < k) n2 <<= 1;
-    for (int i = k + tid; i < n2; i += kThreads) sbuf[i] = 0ull;
+    while (n2 < n_sort) n2 <<= 1;
+    for (int i = n_sort + tid; i < n2; i += kThreads) sbuf[i] = 0ull;
     __syncthreads();
     for (int size = 2; size <= n2; size <<= 1)
       for (int st = size >> 1; st > 0; st >>= 1) {
@@ -731,36 +837,19 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
   GR_STAMP(15);
 }
 
-int fused_prep_launch(const FusedPrep &p, cudaStream_t st) {
-  if (p.n <= 0) return GR4AD_OK;
-  dim3 grid(8, p.n);
-  GR_LAUNCH(KC_SMALL, st, fused_prep_kernel<<<grid, 256, 0, st>>>(p));
-  return GR4AD_OK;
-}
-
 int fused_small_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st) {
   if (n_requests <= 0) return GR4AD_OK;
-  const int G = a.D;
-  const int m = (a.S_max + G - 1) / G;
-  const int vch = (a.Vmax / 4 + G - 1) / G;
-#define GR_FUSED_CASE(GG, MM, VV)                                                         \
-  if (G == GG && m <= MM && vch <= VV) {                                                  \
-    GR_CUDA(cudaFuncSetAttribute(fused_small_kernel<GG, MM, VV>,                          \
+#define GR_FUSED_CASE(DD)                                                                \
+  if (a.D == DD) {                                                                       \
+    GR_CUDA(cudaFuncSetAttribute(fused_small_kernel<DD>,                                 \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    GR_LAUNCH(KC_FUSED, st,                                                               \
-              fused_small_kernel<GG, MM, VV><<<n_requests, kThreads, smem, st>>>(a));     \
-    return GR4AD_OK;                                                                      \
+    GR_LAUNCH(KC_FUSED, st, fused_small_kernel<DD><<<n_requests, kThreads, smem, st>>>(a)); \
+    return GR4AD_OK;                                                                     \
   }
-  GR_FUSED_CASE(16, 16, 4)
-  GR_FUSED_CASE(16, 32, 4)
-  GR_FUSED_CASE(16, 16, 8)
-  GR_FUSED_CASE(16, 32, 8)
-  GR_FUSED_CASE(32, 8, 4)
-  GR_FUSED_CASE(32, 16, 4)
-  GR_FUSED_CASE(32, 8, 8)
-  GR_FUSED_CASE(32, 16, 8)
+  GR_FUSED_CASE(16)
+  GR_FUSED_CASE(32)
 #undef GR_FUSED_CASE
-  return set_err(GR4AD_ERR_UNSUPPORTED, "fused decode: d=%d S=%d V=%d", a.D, a.S_max, a.Vmax);
+  return set_err(GR4AD_ERR_UNSUPPORTED, "fused decode: d=%d", a.D);
 }
 
 }  // namespace gr
