@@ -237,7 +237,10 @@ def class_work(cfgd):
     n_trunk = B * T if K > 0 else 0
     head_rows = sum(R[:T])
     layer_rows = K * n_trunk + (L - K) * head_rows
-    gemm = B * (2 * S * F * d + 4 * L * S * d * d) + layer_rows * (12 * d * d + 4 * d * dff)
+    # executed: encoder K/V for the head layers only; trunk rows attend through
+    # (q Wk^T) X^T and (P X) Wv, i.e. 2 extra d x d products per trunk row
+    gemm = B * (2 * S * F * d + 4 * (L - K) * S * d * d) + layer_rows * (12 * d * d + 4 * d * dff)
+    gemm += K * n_trunk * 4 * d * d
     gemm += sum(R[t] * ((6 * d * d if K > 0 else 0) + 2 * d * V[t]) for t in range(T))
     attn = layer_rows * 4 * S * d
     topk = sum(R[t] * V[t] * 4 + R[t] * 12 + R[t + 1] * (20 + 8 * (t + 2)) for t in range(T))

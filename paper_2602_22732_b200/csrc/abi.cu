@@ -83,7 +83,7 @@ struct Plan {
   // tensor-core layered path
   bool tc = false;
   long long sc_ld = 0, vt_ld = 0;
-  size_t o_VT = 0, o_WT = 0;
+  size_t o_VT = 0, o_WT = 0, o_XT = 0;
   long long wt_floats = 0;
   // fused small-model path
   bool fused = false;
@@ -308,7 +308,9 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   const size_t d = p.d;
   p.o_X = take(Fl * p.S_tot * d);
   p.o_Fin = take(Fl * p.S_tot * p.F);
-  p.o_KV = take(Fl * p.S_tot * 2 * p.L * d);
+  // K/V are materialised for the head layers only: trunk rows (n_pos per
+  // request) attend through the reassociated (q Wk^T) X^T / (P X) Wv
+  p.o_KV = take(Fl * p.S_tot * 2 * (p.L - p.K) * d);
   p.o_Ht = take(Fl * (size_t)B * p.n_pos * d);
   p.o_QKVt = take(Fl * (size_t)B * p.n_pos * 3 * d);
   p.o_Hs = take(Fl * p.Rw * d);
@@ -323,7 +325,8 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   p.o_vlog = take(Fl * std::max(p.R[T], 1LL) * p.nb);
   p.o_hist = take(Fl * p.H * 3 * d * (size_t)(p.L - p.K));
   if (p.tc) {
-    p.o_VT = take(Fl * (size_t)p.L * d * p.vt_ld);
+    p.o_VT = take(Fl * (size_t)(p.L - p.K) * d * p.vt_ld);
+    p.o_XT = take(Fl * (size_t)d * p.vt_ld);
     p.o_WT = take(Fl * (size_t)p.wt_floats);
   }
   p.total = o;
@@ -451,6 +454,17 @@ static int dense(const Plan &p, const GemmArgs &g, const float *WT, long long a_
   return gemm(g, false, epi, st);
 }
 
+// C = epi(A (M x K) . B^T) with B given as an (N x K) row-major matrix
+static int dense_nk(const Plan &p, const GemmArgs &g, long long a_rows, long long b_rows, int epi,
+                    cudaStream_t st) {
+  if (p.tc && tc_eligible(g.lda, g.ldb, g.K, g.A, g.B)) {
+    TcArgs t{};
+    static_cast<GemmArgs &>(t) = g;
+    return gemm_tc(t, a_rows, g.K, b_rows, g.K, epi, st);
+  }
+  return gemm(g, true, epi, st);
+}
+
 static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *wt, int i,
                          float *Hs, const RowSet &rs, void *ws, const float *KV,
                          const float *VT, cudaStream_t st) {
@@ -460,14 +474,30 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   float *N = at<float>(ws, p.o_N), *Q = at<float>(ws, p.o_Q), *A = at<float>(ws, p.o_A);
   float *SC = at<float>(ws, p.o_SC), *Fb = at<float>(ws, p.o_Fb);
   const int *ctx_off = at<int>(ws, p.o_ctx_off), *ctx_len = at<int>(ws, p.o_ctx_len);
-  const long long ldkv = 2LL * p.L * d;
+  const int nh = p.L - p.K;  // layers whose context K/V are materialised
+  const long long ldkv = 2LL * nh * d;
+  const bool trunk = i < p.K;
+  const float *X = at<float>(ws, p.o_X);
+  const long long ldw = 2LL * p.L * d;
   // cross-attention into the beam-shared context KV (layers.py:82-90)
   GR_TRY(ln_rows(Hs, d, N, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
   GR_TRY(dense(p, plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), LT ? LT->cq : nullptr, R,
                EPI_STORE, st));
+  const float *qsrc = Q;
+  if (trunk) {
+    // trunk rows: q (X Wk)^T = (q Wk^T) X^T -- the trunk layers' K is never built
+    float *Q2 = N;
+    GemmArgs g = plain_gemm(Q, d, w->cross_kv_W + (size_t)(2 * i) * d, ldw, Q2, d, R, d, d);
+    GR_TRY(dense_nk(p, g, R, d, EPI_STORE, st));  // B = Wk as (N x K): Q2 = Q Wk^T
+    qsrc = Q2;
+  }
   GemmArgs qk{};
-  qk.A = Q; qk.lda = d;
-  qk.B = KV + (size_t)(2 * i) * d; qk.ldb = ldkv;
+  qk.A = qsrc; qk.lda = d;
+  if (trunk) {
+    qk.B = X; qk.ldb = d;
+  } else {
+    qk.B = KV + (size_t)(2 * (i - p.K)) * d; qk.ldb = ldkv;
+  }
   qk.C = SC; qk.ldc = p.sc_ld;
   qk.M = rs.max_group_rows; qk.N = p.S_max; qk.K = d;
   qk.alpha = 1.0f / sqrtf((float)d);
@@ -490,14 +520,24 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   if (p.tc && VT) {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = pv;
-    t.B = VT + (size_t)i * d * p.vt_ld;
+    t.B = trunk ? at<float>(ws, p.o_XT) : VT + (size_t)(i - p.K) * d * p.vt_ld;
     t.ldb = p.vt_ld;
     GR_TRY(gemm_tc(t, R, p.sc_ld, d, p.vt_ld, EPI_STORE, st));
   } else {
-    pv.B = KV + (size_t)(2 * i + 1) * d; pv.ldb = ldkv;
+    if (trunk) {
+      pv.B = X; pv.ldb = d;
+    } else {
+      pv.B = KV + (size_t)(2 * (i - p.K) + 1) * d; pv.ldb = ldkv;
+    }
     GR_TRY(gemm(pv, false, EPI_STORE, st));
   }
-  GemmArgs o = plain_gemm(A, d, Lw.cross_Wo, d, Hs, d, R, d, d);
+  const float *attn = A;
+  if (trunk) {  // (P X) Wv
+    GR_TRY(dense(p, plain_gemm(A, d, w->cross_kv_W + (size_t)(2 * i + 1) * d, ldw, Q, d, R, d, d),
+                 wt ? wt->kv + (size_t)(2 * i + 1) * d * d : nullptr, R, EPI_STORE, st));
+    attn = Q;
+  }
+  GemmArgs o = plain_gemm(attn, d, Lw.cross_Wo, d, Hs, d, R, d, d);
   o.R = Hs; o.ldr = d;
   GR_TRY(dense(p, o, LT ? LT->co : nullptr, R, EPI_RESID, st));
   // self-attention over decoded positions (layers.py:92-113)
@@ -593,20 +633,23 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     g.bias = w->ctx_b;
     GR_TRY(dense(p, g, wt ? wt->ctx : nullptr, p.S_tot, EPI_BIAS, st));
   }
-  // encoder K/V of every layer, once per request (beam.py:98-109; layers.py:85-87);
-  // on the tensor-core path the epilogue also writes V^T for the P.V GEMMs
+  // encoder K/V of the head layers, once per request and shared by every beam
+  // (beam.py:98-109); on the tensor-core path the epilogue also writes V^T
+  // for the P.V GEMMs, and X^T serves the trunk's (P X) products
   {
-    GemmArgs g = plain_gemm(X, d, w->cross_kv_W, 2LL * p.L * d, KV, 2LL * p.L * d, (int)p.S_tot,
-                            2 * p.L * d, d);
+    const int nh = p.L - K;
+    GemmArgs g = plain_gemm(X, d, w->cross_kv_W + (size_t)2 * K * d, 2LL * p.L * d, KV,
+                            2LL * nh * d, (int)p.S_tot, 2 * nh * d, d);
     if (p.tc && tc_eligible(g.lda, d, d, X, wt->kv)) {
       TcArgs t{};
       static_cast<GemmArgs &>(t) = g;
-      t.B = wt->kv;
+      t.B = wt->kv + (size_t)2 * K * d * d;
       t.ldb = d;
       t.vt = VT;
       t.vt_ld = p.vt_ld;
       t.kv_d = d;
-      GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * p.L * d, d, EPI_KV_SPLIT, st));
+      GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * nh * d, d, EPI_KV_SPLIT, st));
+      if (K > 0) GR_TRY(transpose(X, d, at<float>(ws, p.o_XT), p.vt_ld, (int)p.S_tot, d, st));
     } else {
       if (p.tc) return set_err(GR4AD_ERR_UNSUPPORTED, "tensor-core path: unaligned context");
       GR_TRY(gemm(g, false, EPI_STORE, st));
