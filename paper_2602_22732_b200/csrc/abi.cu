@@ -327,7 +327,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   if (p.tc) {
     p.o_VT = take(Fl * (size_t)(p.L - p.K) * d * p.vt_ld);
     p.o_XT = take(Fl * (size_t)d * p.vt_ld);
-    p.o_WT = take(Fl * (size_t)p.wt_floats);
+    p.o_WT = take(Fl * (size_t)p.wt_floats * 2);  // tf32 hi parts, then lo parts
   }
   p.total = o;
   return GR4AD_OK;
@@ -418,7 +418,7 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
   auto tr = [&](const float *src, int rows, int cols) -> const float * {
     float *dst = base + o;
     o += ((long long)rows * cols + 63) / 64 * 64;
-    if (rc == GR4AD_OK) rc = transpose(src, cols, dst, rows, rows, cols, st);
+    if (rc == GR4AD_OK) rc = transpose_split(src, cols, dst, dst + p.wt_floats, rows, rows, cols, st);
     return dst;
   };
   const int d = p.d;
@@ -448,6 +448,7 @@ static int dense(const Plan &p, const GemmArgs &g, const float *WT, long long a_
     TcArgs t{};
     static_cast<GemmArgs &>(t) = g;
     t.B = WT;
+    t.b_lo = WT + p.wt_floats;  // weights arrive pre-split (prep_weights_t)
     t.ldb = g.K;
     return gemm_tc(t, a_rows, g.K, g.N, g.K, epi, st);
   }
@@ -644,6 +645,7 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       TcArgs t{};
       static_cast<GemmArgs &>(t) = g;
       t.B = wt->kv + (size_t)2 * K * d * d;
+      t.b_lo = t.B + p.wt_floats;
       t.ldb = d;
       t.vt = VT;
       t.vt_ld = p.vt_ld;

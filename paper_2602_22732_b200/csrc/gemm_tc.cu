@@ -22,6 +22,8 @@
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "gemm.cuh"
 #include "gemm_tc.cuh"
 
@@ -128,12 +130,61 @@ __device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
 
 }  // namespace
 
-template <int BN, int STAGES, int EPI>
+struct TileInfo {
+  int m0, n0, M, N, K, row_base, b_row_base, b_k_base;
+  bool valid;
+};
+
+// tile -> (group, m-tile, n-tile); identical in every warp role
+__device__ __forceinline__ TileInfo tile_info(const TcArgs &a, int tile, int tiles_m, int tiles_n,
+                                              int bn) {
+  TileInfo ti;
+  const int per_g = tiles_m * tiles_n;
+  const int g = tile / per_g, r = tile - g * per_g;
+  const int tm = r / tiles_n, tn = r - tm * tiles_n;
+  ti.M = a.M; ti.N = a.N; ti.K = a.K;
+  ti.row_base = 0; ti.b_row_base = 0; ti.b_k_base = 0;
+  if (a.g_rows) {
+    ti.row_base = a.g_row_off[g];
+    ti.M = a.g_rows[g];
+    if (a.mode == GM_QK) {
+      ti.N = a.g_ctx_len[g];
+      ti.b_row_base = a.g_ctx_off[g];
+    } else if (a.mode == GM_PV) {
+      ti.K = a.g_ctx_len[g];
+      ti.b_k_base = a.g_ctx_off[g];
+    }
+  }
+  ti.m0 = tm * BM;
+  ti.n0 = tn * bn;
+  ti.valid = ti.m0 < ti.M && ti.n0 < ti.N;
+  return ti;
+}
+
+__device__ __forceinline__ void split_tile(float4 *hi, float4 *lo, int n4, int t, int nt) {
+#pragma unroll 4
+  for (int i = t; i < n4; i += nt) {
+    float4 x = hi[i], h, l;
+    split_tf32(x.x, h.x, l.x);
+    split_tf32(x.y, h.y, l.y);
+    split_tf32(x.z, h.z, l.z);
+    split_tf32(x.w, h.w, l.w);
+    hi[i] = h;
+    lo[i] = l;
+  }
+}
+
+// Persistent, warp-specialised: each CTA walks tiles blockIdx.x, +gridDim.x, ...
+// warp 0 TMA | warp 1 TMEM alloc + MMA issue | warps 2-3 tf32 split |
+// warps 4-7 epilogue.  Two TMEM accumulators (2 x BN columns) let the
+// epilogue of tile j overlap the MMAs of tile j+1.  BSPLIT: B arrives
+// already split (weights prepared once per call), only A is split here.
+template <int BN, int STAGES, int EPI, bool BSPLIT>
 __global__ void __launch_bounds__(kTcThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               TcArgs a) {
+               const __grid_constant__ CUtensorMap tmBlo, TcArgs a, int tiles_m, int tiles_n,
+               int n_tiles) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-B aligned tile region
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   constexpr int A_BYTES = BM * BK * 4;
@@ -142,41 +193,27 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
   uint64_t *conv = full + STAGES;
   uint64_t *empty = conv + STAGES;
-  uint64_t *done = empty + STAGES;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  uint64_t *accf = empty + STAGES;  // [2] accumulator ready
+  uint64_t *acce = accf + 2;        // [2] accumulator drained
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.z;
-  int M = a.M, N = a.N, K = a.K;
-  int row_base = 0, b_row_base = 0, b_k_base = 0;
-  if (a.g_rows) {
-    row_base = a.g_row_off[g];
-    M = a.g_rows[g];
-    if (a.mode == GM_QK) {
-      N = a.g_ctx_len[g];
-      b_row_base = a.g_ctx_off[g];
-    } else if (a.mode == GM_PV) {
-      K = a.g_ctx_len[g];
-      b_k_base = a.g_ctx_off[g];
-    }
-  }
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  if (m0 >= M || n0 >= N) return;
-  const int nk = (K + BK - 1) / BK;
-
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);
+      mbar_init(&conv[s], 2);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&accf[j], 1);
+      mbar_init(&acce[j], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {  // TMEM: BN fp32 columns x 128 lanes
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -186,119 +223,139 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
-      for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % STAGES;
-        if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
-        unsigned char *st = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-        tma_load_2d(st, &tmA, &full[s], kt * BK, row_base + m0);
-        tma_load_2d(st + 2 * A_BYTES, &tmB, &full[s], b_k_base + kt * BK, b_row_base + n0);
+      int kg = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN);
+        if (!ti.valid) continue;
+        const int nk = (ti.K + BK - 1) / BK;
+        for (int kt = 0; kt < nk; ++kt, ++kg) {
+          const int s = kg % STAGES;
+          if (kg >= STAGES) mbar_wait(&empty[s], ((kg / STAGES) - 1) & 1);
+          unsigned char *st = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], A_BYTES + (BSPLIT ? 2 : 1) * B_BYTES);
+          tma_load_2d(st, &tmA, &full[s], kt * BK, ti.row_base + ti.m0);
+          tma_load_2d(st + 2 * A_BYTES, &tmB, &full[s], ti.b_k_base + kt * BK,
+                      ti.b_row_base + ti.n0);
+          if (BSPLIT)
+            tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tmBlo, &full[s], ti.b_k_base + kt * BK,
+                        ti.b_row_base + ti.n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                  ((uint32_t)(BM >> 4) << 24);
-      for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % STAGES;
-        mbar_wait(&conv[s], (kt / STAGES) & 1);
+      int kg = 0, j = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN);
+        if (!ti.valid) continue;
+        const int acc = j & 1;
+        if (j >= 2) mbar_wait(&acce[acc], ((j >> 1) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-        const uint32_t a_hi = st, a_lo = st + A_BYTES;
-        const uint32_t b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+        const uint32_t d_tmem = tmem + (uint32_t)(acc * BN);
+        const int nk = (ti.K + BK - 1) / BK;
+        for (int kt = 0; kt < nk; ++kt, ++kg) {
+          const int s = kg % STAGES;
+          mbar_wait(&conv[s], (kg / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t a_hi = st, a_lo = st + A_BYTES;
+          const uint32_t b_hi = st + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 8; ++k) {
-          const uint32_t off = k * 32;  // 8 tf32 = 32 B along the swizzled row
-          const uint32_t acc0 = (kt > 0 || k > 0) ? 1u : 0u;
-          mma_tf32(tmem, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, acc0);
-          mma_tf32(tmem, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
-          mma_tf32(tmem, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, 1u);
-        }
-        mma_commit(&empty[s]);  // frees the stage when these MMAs complete
-      }
-      mma_commit(done);
-    }
-  } else if (warp >= 4) {
-    // ---- converters: split landed fp32 tiles into tf32 hi (in place) + lo
-    const int ct = threadIdx.x - 128;  // 0..127
-    for (int kt = 0; kt < nk; ++kt) {
-      const int s = kt % STAGES;
-      mbar_wait(&full[s], (kt / STAGES) & 1);
-      unsigned char *st = smem + s * STAGE_BYTES;
-      float4 *ah = reinterpret_cast<float4 *>(st);
-      float4 *al = reinterpret_cast<float4 *>(st + A_BYTES);
-      float4 *bh = reinterpret_cast<float4 *>(st + 2 * A_BYTES);
-      float4 *bl = reinterpret_cast<float4 *>(st + 2 * A_BYTES + B_BYTES);
-#pragma unroll 4
-      for (int i = ct; i < A_BYTES / 16; i += 128) {
-        float4 x = ah[i], h, l;
-        split_tf32(x.x, h.x, l.x);
-        split_tf32(x.y, h.y, l.y);
-        split_tf32(x.z, h.z, l.z);
-        split_tf32(x.w, h.w, l.w);
-        ah[i] = h;
-        al[i] = l;
-      }
-#pragma unroll 4
-      for (int i = ct; i < B_BYTES / 16; i += 128) {
-        float4 x = bh[i], h, l;
-        split_tf32(x.x, h.x, l.x);
-        split_tf32(x.y, h.y, l.y);
-        split_tf32(x.z, h.z, l.z);
-        split_tf32(x.w, h.w, l.w);
-        bh[i] = h;
-        bl[i] = l;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[s]);
-    }
-    // ---- epilogue: TMEM -> registers -> global
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3;
-    const int r = m0 + q * 32 + lane;  // this thread's output row (within group)
-    const long long grow = (long long)row_base + r;
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), v);
-      if (r >= M) continue;
-      const int col0 = n0 + c * 32;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int col = col0 + j;
-        float x = v[j] * a.alpha;
-        if (col < N) {
-          if (EPI == EPI_BIAS) x = x + a.bias[col];
-          else if (EPI == EPI_BIAS_GELU) x = gelu_tanh(x + a.bias[col]);
-          else if (EPI == EPI_RESID) x = a.R[grow * a.ldr + col] + x;
-          else if (EPI == EPI_BIAS_RESID) x = a.R[grow * a.ldr + col] + (x + a.bias[col]);
-          else if (EPI == EPI_MULVEC) x = a.vec[(long long)a.row_req[grow] * a.vec_ld + col] * x;
-          if (EPI == EPI_KV_SPLIT) {
-            // [2i d, 2i d + d) -> K_i; [2i d + d, 2(i+1) d) -> also V_i^T (coalesced over rows)
-            const int layer = col / (2 * a.kv_d), w = col - layer * 2 * a.kv_d;
-            if (w >= a.kv_d)
-              a.vt[((long long)layer * a.kv_d + (w - a.kv_d)) * a.vt_ld + grow] = x;
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint32_t off = k * 32;  // 8 tf32 = 32 B along the swizzled row
+            const uint32_t acc0 = (kt > 0 || k > 0) ? 1u : 0u;
+            mma_tf32(d_tmem, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, acc0);
+            mma_tf32(d_tmem, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
+            mma_tf32(d_tmem, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, 1u);
           }
+          mma_commit(&empty[s]);  // frees the stage when these MMAs complete
         }
-        v[j] = x;
+        mma_commit(&accf[acc]);
+        ++j;
       }
-      float *crow = a.C + grow * a.ldc + col0;
-      if (col0 + 32 <= N && (a.ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(crow) % 16) == 0) {
+    }
+  } else if (warp < 4) {
+    // ---- converters: split landed fp32 tiles into tf32 hi (in place) + lo
+    const int ct = threadIdx.x - 64;  // 0..63
+    int kg = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN);
+      if (!ti.valid) continue;
+      const int nk = (ti.K + BK - 1) / BK;
+      for (int kt = 0; kt < nk; ++kt, ++kg) {
+        const int s = kg % STAGES;
+        mbar_wait(&full[s], (kg / STAGES) & 1);
+        unsigned char *st = smem + s * STAGE_BYTES;
+        split_tile(reinterpret_cast<float4 *>(st), reinterpret_cast<float4 *>(st + A_BYTES),
+                   A_BYTES / 16, ct, 64);
+        if (!BSPLIT)
+          split_tile(reinterpret_cast<float4 *>(st + 2 * A_BYTES),
+                     reinterpret_cast<float4 *>(st + 2 * A_BYTES + B_BYTES), B_BYTES / 16, ct, 64);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+      }
+    }
+  } else {
+    // ---- epilogue: TMEM -> registers -> global
+    const int q = warp & 3;
+    int j = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN);
+      if (!ti.valid) continue;
+      const int acc = j & 1;
+      mbar_wait(&accf[acc], (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int r = ti.m0 + q * 32 + lane;
+      const long long grow = (long long)ti.row_base + r;
+      const int N = ti.N;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+        const int col0 = ti.n0 + c * 32;
+        if (r >= ti.M || col0 >= N) continue;
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          *reinterpret_cast<float4 *>(crow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-      } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) crow[j] = v[j];
+        for (int jj = 0; jj < 32; ++jj) {
+          const int col = col0 + jj;
+          float x = v[jj] * a.alpha;
+          if (col < N) {
+            if (EPI == EPI_BIAS) x = x + a.bias[col];
+            else if (EPI == EPI_BIAS_GELU) x = gelu_tanh(x + a.bias[col]);
+            else if (EPI == EPI_RESID) x = a.R[grow * a.ldr + col] + x;
+            else if (EPI == EPI_BIAS_RESID) x = a.R[grow * a.ldr + col] + (x + a.bias[col]);
+            else if (EPI == EPI_MULVEC) x = a.vec[(long long)a.row_req[grow] * a.vec_ld + col] * x;
+            if (EPI == EPI_KV_SPLIT) {
+              // [2i d, 2i d + d) -> K_i; [2i d + d, 2(i+1) d) -> also V_i^T (coalesced over rows)
+              const int layer = col / (2 * a.kv_d), w = col - layer * 2 * a.kv_d;
+              if (w >= a.kv_d)
+                a.vt[((long long)layer * a.kv_d + (w - a.kv_d)) * a.vt_ld + grow] = x;
+            }
+          }
+          v[jj] = x;
+        }
+        float *crow = a.C + grow * a.ldc + col0;
+        if (col0 + 32 <= N && (a.ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(crow) % 16) == 0) {
+#pragma unroll
+          for (int jj = 0; jj < 32; jj += 4)
+            *reinterpret_cast<float4 *>(crow + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+        } else {
+          for (int jj = 0; jj < 32 && col0 + jj < N; ++jj) crow[jj] = v[jj];
+        }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[acc]);
+      ++j;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
@@ -335,18 +392,27 @@ static int make_map(CUtensorMap *m, const float *base, long long rows, long long
   return GR4AD_OK;
 }
 
-template <int BN, int STAGES>
-static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const TcArgs &a, int epi,
-                     cudaStream_t st) {
+static int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+template <int BN, int STAGES, bool BSPLIT>
+static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl,
+                     const TcArgs &a, int epi, cudaStream_t st) {
   constexpr size_t smem = 1024 + (size_t)STAGES * (2 * BM * BK * 4 + 2 * BN * BK * 4) + 256;
-  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.groups);
+  const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
+  const int n_tiles = tiles_m * tiles_n * a.groups;
+  const int grid = std::min(n_tiles, num_sms());
   const int cls = (a.mode == GM_PLAIN) ? KC_GEMM : KC_ATTN_GEMM;
-#define GR_TC_EPI(E)                                                                     \
-  case E: {                                                                              \
-    GR_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E>,                          \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    GR_LAUNCH(cls, st, gemm_tc_kernel<BN, STAGES, E><<<grid, kTcThreads, smem, st>>>(ma, mb, a)); \
-    return GR4AD_OK;                                                                     \
+#define GR_TC_EPI(E)                                                                          \
+  case E: {                                                                                   \
+    GR_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E, BSPLIT>,                       \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
+    GR_LAUNCH(cls, st, gemm_tc_kernel<BN, STAGES, E, BSPLIT><<<grid, kTcThreads, smem, st>>>(   \
+                           ma, mb, mbl, a, tiles_m, tiles_n, n_tiles));                       \
+    return GR4AD_OK;                                                                          \
   }
   switch (epi) {
     GR_TC_EPI(EPI_STORE)
@@ -372,13 +438,21 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
   static const bool trace = getenv("GR4AD_TRACE") != nullptr;  // debug aid (read-only)
   if (trace)
     fprintf(stderr, "gemm_tc M=%d N=%d K=%d groups=%d mode=%d epi=%d lda=%lld ldb=%lld ldc=%lld "
-                    "A=(%lld,%lld) B=(%lld,%lld)\n",
+                    "A=(%lld,%lld) B=(%lld,%lld) presplit=%d\n",
             a.M, a.N, a.K, a.groups, a.mode, epi, a.lda, a.ldb, a.ldc, a_rows, a_cols, b_rows,
-            b_cols);
-  CUtensorMap ma, mb;
+            b_cols, a.b_lo != nullptr);
+  const bool wide = a.N >= 256;
+  const int box_n = wide ? 256 : 128;
+  CUtensorMap ma, mb, mbl;
   GR_TRY(make_map(&ma, a.A, a_rows, a_cols, a.lda, BM));
-  GR_TRY(make_map(&mb, a.B, b_rows, b_cols, a.ldb, 128));
-  return launch_tc<128, 3>(ma, mb, a, epi, st);
+  GR_TRY(make_map(&mb, a.B, b_rows, b_cols, a.ldb, box_n));
+  if (a.b_lo) {
+    GR_TRY(make_map(&mbl, a.b_lo, b_rows, b_cols, a.ldb, box_n));
+    return wide ? launch_tc<256, 2, true>(ma, mb, mbl, a, epi, st)
+                : launch_tc<128, 3, true>(ma, mb, mbl, a, epi, st);
+  }
+  return wide ? launch_tc<256, 2, false>(ma, mb, mb, a, epi, st)
+              : launch_tc<128, 3, false>(ma, mb, mb, a, epi, st);
 }
 
 }  // namespace gr

@@ -5,6 +5,7 @@
 namespace gr {
 
 struct TcArgs : GemmArgs {
+  const float *b_lo;  // optional: B pre-split, B holds tf32 hi parts and b_lo the rests
   float *vt;         // EPI_KV_SPLIT: V^T destination (L*d rows, vt_ld columns)
   long long vt_ld;
   int kv_d;
@@ -19,5 +20,8 @@ bool tc_eligible(long long lda, long long ldb, int K, const void *A, const void 
 // dst (cols x rows) = src (rows x cols)^T, both row-major with the given lds
 int transpose(const float *src, long long lds, float *dst, long long ldd, int rows, int cols,
               cudaStream_t st);
+// as transpose, writing the tf32 split of every element: dst_hi + dst_lo == src^T exactly
+int transpose_split(const float *src, long long lds, float *dst_hi, float *dst_lo, long long ldd,
+                    int rows, int cols, cudaStream_t st);
 
 }  // namespace gr

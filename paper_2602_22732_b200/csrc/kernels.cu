@@ -600,7 +600,7 @@ int topk_select(const SelectArgs &a, int n_requests, int u_rows, int u_k,
 // tiled transpose: dst (cols x rows) = src (rows x cols)^T
 // ---------------------------------------------------------------------------
 __global__ void transpose_kernel(const float *__restrict__ src, long long lds, float *dst,
-                                 long long ldd, int rows, int cols) {
+                                 float *dst_lo, long long ldd, int rows, int cols) {
   __shared__ float tile[32][33];
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
@@ -610,7 +610,16 @@ __global__ void transpose_kernel(const float *__restrict__ src, long long lds, f
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += 8) {
     int c = c0 + i, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) dst[(long long)c * ldd + r] = tile[threadIdx.x][i];
+    if (r < rows && c < cols) {
+      float x = tile[threadIdx.x][i];
+      if (dst_lo) {  // tf32 split: hi = x with 13 low mantissa bits cleared, lo = x - hi
+        float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+        dst[(long long)c * ldd + r] = hi;
+        dst_lo[(long long)c * ldd + r] = x - hi;
+      } else {
+        dst[(long long)c * ldd + r] = x;
+      }
+    }
   }
 }
 
@@ -618,7 +627,15 @@ int transpose(const float *src, long long lds, float *dst, long long ldd, int ro
               cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return GR4AD_OK;
   dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32));
-  GR_LAUNCH(KC_SMALL, st, transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, lds, dst, ldd, rows, cols));
+  GR_LAUNCH(KC_SMALL, st, transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, lds, dst, nullptr, ldd, rows, cols));
+  return GR4AD_OK;
+}
+
+int transpose_split(const float *src, long long lds, float *dst_hi, float *dst_lo, long long ldd,
+                    int rows, int cols, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return GR4AD_OK;
+  dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32));
+  GR_LAUNCH(KC_SMALL, st, transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, lds, dst_hi, dst_lo, ldd, rows, cols));
   return GR4AD_OK;
 }
 
