@@ -359,7 +359,6 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
   unsigned *hist = reinterpret_cast<unsigned *>(sbuf + GR4AD_MAX_BEAM);    // 2048
   uint32_t *keys = reinterpret_cast<uint32_t *>(hist + 2048);              // kCacheKeys
   __shared__ unsigned scan[2];
-  __shared__ unsigned wcnt[kSelWarps];
   __shared__ unsigned s_gt_pos, s_nfin;
 
   const int b = blockIdx.x;
@@ -377,10 +376,101 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
   const int k = (int)min((long long)want, n_cand);
   const int tid = threadIdx.x;
 
+  int wid = tid >> 5, lane = tid & 31;
+  // ---- (a) one-pass window selection -------------------------------------
+  // Candidate scores are cum_r + logp <= Rs := max_r cum_r.  Bin each by
+  // min((Rs - s) * scale, 2047) (monotone in s; 2048 bins over ln V + 4 score
+  // units); every candidate in a bin below the k-th candidate's bin is in
+  // the top-k, and that bin is collected whole, so one histogram pass and
+  // one collect pass feed an exact (key, index) sort.  Radix passes are the
+  // fallback when the window overflows.
+  bool window = false;
+  int n_sort = k;
+  __shared__ float s_red[kSelWarps];
+  if (k > 0) {
+    float mc = -INFINITY;
+    for (int r = tid; r < c.n_rows; r += kSelThreads) mc = fmaxf(mc, c.cum[c.hist0 + c.row0 + r]);
+    mc = warp_max(mc);
+    if (lane == 0) s_red[wid] = mc;
+    for (int i = tid; i < 2048; i += kSelThreads) hist[i] = 0u;
+    __syncthreads();
+    float Rs = -INFINITY;
+    for (int w = 0; w < kSelWarps; ++w) Rs = fmaxf(Rs, s_red[w]);
+    const float scale = 2048.0f / (logf((float)max(c.V, 2)) + 4.0f);
+    auto sbin = [&](float s) -> unsigned { return (unsigned)fminf((Rs - s) * scale, 2047.0f); };
+    int cur = -1;
+    unsigned cnt = 0;
+    for (int r = wid; r < c.n_rows; r += kSelWarps) {
+      const float cr = c.cum[c.hist0 + c.row0 + r];
+      const float2 ri = c.rowinfo ? c.rowinfo[c.row0 + r] : make_float2(0.f, 0.f);
+      for (int v = lane; v < c.V; v += 32) {
+        const float lg = c.logits[(long long)(c.row0 + r) * c.ld + v];
+        const float s = cr + (c.rowinfo ? ((lg - ri.x) - ri.y) : lg);
+        if (CACHE) keys[(long long)r * c.V + v] = f2ord(s);
+        const int bin = (int)sbin(s);
+        if (bin == cur) {
+          ++cnt;
+        } else {
+          if (cnt) atomicAdd(&hist[cur], cnt);
+          cur = bin;
+          cnt = 1;
+        }
+      }
+    }
+    if (cnt) atomicAdd(&hist[cur], cnt);
+    __syncthreads();
+    for (int i = tid; i < 1024; i += kSelThreads) {  // mirror: sel_find_bin scans from the top
+      unsigned x = hist[i], y = hist[2047 - i];
+      hist[i] = y;
+      hist[2047 - i] = x;
+    }
+    __syncthreads();
+    unsigned above;
+    const int rb = sel_find_bin(hist, 2048, (unsigned)k, &above, scan);
+    const int wb = 2047 - rb;
+    const unsigned cnt_le = above + hist[rb];
+    if (wb < 2047 && cnt_le <= (unsigned)GR4AD_MAX_BEAM) {
+      window = true;
+      n_sort = (int)cnt_le;
+      if (tid == 0) s_gt_pos = 0;
+      __syncthreads();
+      for (int r = wid; r < c.n_rows; r += kSelWarps) {
+        const float cr = c.cum[c.hist0 + c.row0 + r];
+        const float2 ri = c.rowinfo ? c.rowinfo[c.row0 + r] : make_float2(0.f, 0.f);
+        for (int v0 = 0; v0 < c.V; v0 += 32) {
+          const int v = v0 + lane;
+          float s = -INFINITY;
+          if (v < c.V) {
+            if (CACHE) {
+              s = ord2f(keys[(long long)r * c.V + v]);
+            } else {
+              const float lg = c.logits[(long long)(c.row0 + r) * c.ld + v];
+              s = cr + (c.rowinfo ? ((lg - ri.x) - ri.y) : lg);
+            }
+          }
+          const bool take = v < c.V && sbin(s) <= (unsigned)wb;
+          const unsigned m = __ballot_sync(0xffffffffu, take);
+          if (m) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(&s_gt_pos, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (take) {
+              const unsigned fi = (unsigned)((long long)r * c.V + v);
+              sbuf[base + __popc(m & ((1u << lane) - 1u))] =
+                  ((unsigned long long)f2ord(s) << 32) | (0xFFFFFFFFu - fi);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- (b) exact radix fallback ---------------------------------------------
   uint32_t T = 0, pmask = 0;
   unsigned need = (unsigned)k;
   unsigned eq_total = 0;
-  if (k > 0) {
+  if (k > 0 && !window) {
     const int shifts[3] = {21, 10, 0};
     const int widths[3] = {11, 11, 10};
     for (int pass = 0; pass < 3; ++pass) {
@@ -401,15 +491,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
   // need = number of keys == T to keep (lowest flat indices); eq_total = all keys == T
   const bool all_eq = (need == eq_total);
   const unsigned n_gt = (unsigned)k - need;
-  int wid = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_gt_pos = 0;
+  if (tid == 0 && !window) s_gt_pos = 0;
   // per-row ordered tie ranks: rows are visited in order r = wid, wid+32, ...;
   // pass A counts ties per row (only when some ties must be dropped).
   // Row counts are kept in the sort buffer tail region (cleared below).
   unsigned *row_eq = hist;  // reused: per-row tie counts, 2048 rows per chunk
-  const bool ordered = !all_eq && k > 0;
+  const bool ordered = !all_eq && k > 0 && !window;
   __syncthreads();
-  if (k > 0) {
+  if (k > 0 && !window) {
     if (!ordered) {
       for (int r = wid; r < c.n_rows; r += kSelWarps) {
         float cr = 0.f;
@@ -514,8 +603,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
   __syncthreads();
   // bitonic sort of sbuf[0..n2) descending
   int n2 = 1;
-  while (n2 < k) n2 <<= 1;
-  for (int i = k + tid; i < n2; i += kSelThreads) sbuf[i] = 0ull;
+  while (n2 < n_sort) n2 <<= 1;
+  for (int i = n_sort + tid; i < n2; i += kSelThreads) sbuf[i] = 0ull;
   __syncthreads();
   for (int size = 2; size <= n2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
