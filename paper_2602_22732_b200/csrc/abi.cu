@@ -83,7 +83,7 @@ struct Plan {
   // tensor-core layered path
   bool tc = false;
   long long sc_ld = 0, vt_ld = 0;
-  size_t o_VT = 0, o_WT = 0, o_XT = 0;
+  size_t o_VT = 0, o_WT = 0, o_XT = 0, o_VTlo = 0, o_KVlo = 0;
   long long wt_floats = 0;
   // fused small-model path
   bool fused = false;
@@ -326,6 +326,8 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   p.o_hist = take(Fl * p.H * 3 * d * (size_t)(p.L - p.K));
   if (p.tc) {
     p.o_VT = take(Fl * (size_t)(p.L - p.K) * d * p.vt_ld);
+    p.o_VTlo = take(Fl * (size_t)(p.L - p.K) * d * p.vt_ld);
+    p.o_KVlo = take(Fl * p.S_tot * 2 * (p.L - p.K) * d);
     p.o_XT = take(Fl * (size_t)d * p.vt_ld);
     p.o_WT = take(Fl * (size_t)p.wt_floats * 2);  // tf32 hi parts, then lo parts
   }
@@ -508,6 +510,8 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   if (p.tc && tc_eligible(qk.lda, qk.ldb, d, qk.A, qk.B)) {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = qk;
+    if (!trunk)  // head-layer K arrives pre-split from the encoder epilogue
+      t.b_lo = at<float>(ws, p.o_KVlo) + (size_t)(2 * (i - p.K)) * d;
     GR_TRY(gemm_tc(t, R, d, p.S_tot, d, EPI_STORE, st));
   } else {
     GR_TRY(gemm(qk, true, EPI_STORE, st));
@@ -522,6 +526,7 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
     TcArgs t{};
     static_cast<GemmArgs &>(t) = pv;
     t.B = trunk ? at<float>(ws, p.o_XT) : VT + (size_t)(i - p.K) * d * p.vt_ld;
+    if (!trunk) t.b_lo = at<float>(ws, p.o_VTlo) + (size_t)(i - p.K) * d * p.vt_ld;
     t.ldb = p.vt_ld;
     GR_TRY(gemm_tc(t, R, p.sc_ld, d, p.vt_ld, EPI_STORE, st));
   } else {
@@ -650,6 +655,8 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       t.vt = VT;
       t.vt_ld = p.vt_ld;
       t.kv_d = d;
+      t.c_lo = at<float>(ws, p.o_KVlo);
+      t.vt_lo = at<float>(ws, p.o_VTlo);
       GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * nh * d, d, EPI_KV_SPLIT, st));
       if (K > 0) GR_TRY(transpose(X, d, at<float>(ws, p.o_XT), p.vt_ld, (int)p.S_tot, d, st));
     } else {

@@ -328,10 +328,21 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             else if (EPI == EPI_BIAS_RESID) x = a.R[grow * a.ldr + col] + (x + a.bias[col]);
             else if (EPI == EPI_MULVEC) x = a.vec[(long long)a.row_req[grow] * a.vec_ld + col] * x;
             if (EPI == EPI_KV_SPLIT) {
-              // [2i d, 2i d + d) -> K_i; [2i d + d, 2(i+1) d) -> also V_i^T (coalesced over rows)
+              // [2i d, 2i d + d) -> K_i; [2i d + d, 2(i+1) d) -> also V_i^T (coalesced
+              // over rows); with c_lo set both are stored pre-split for the
+              // attention GEMMs (hi here, lo in c_lo / vt_lo)
               const int layer = col / (2 * a.kv_d), w = col - layer * 2 * a.kv_d;
-              if (w >= a.kv_d)
-                a.vt[((long long)layer * a.kv_d + (w - a.kv_d)) * a.vt_ld + grow] = x;
+              float hi = x, lo = 0.f;
+              if (a.c_lo) {
+                split_tf32(x, hi, lo);
+                a.c_lo[grow * a.ldc + col] = lo;
+              }
+              if (w >= a.kv_d) {
+                const long long o = ((long long)layer * a.kv_d + (w - a.kv_d)) * a.vt_ld + grow;
+                a.vt[o] = hi;
+                if (a.vt_lo) a.vt_lo[o] = lo;
+              }
+              x = hi;
             }
           }
           v[jj] = x;

@@ -7,6 +7,7 @@ namespace gr {
 struct TcArgs : GemmArgs {
   const float *b_lo;  // optional: B pre-split, B holds tf32 hi parts and b_lo the rests
   float *vt;         // EPI_KV_SPLIT: V^T destination (L*d rows, vt_ld columns)
+  float *c_lo, *vt_lo;  // EPI_KV_SPLIT: when set, C / V^T get tf32 hi parts, these the rests
   long long vt_ld;
   int kv_d;
 };
