@@ -171,6 +171,24 @@ int gr4ad_encoder_kv(const gr4ad_dims *dims, const gr4ad_weights *w,
                      const float *x, int rows, int lo, int hi, float *kv,
                      void *stream);
 
+/* Teacher-forced scoring of fixed token sequences (lazy_forward +
+ * sequence_log_prob, decoder.py:162-219): sequence s
+ * belongs to request req[s] (HOST array) of `batch` (whose widths are
+ * ignored) and has tokens[s*T .. s*T+T-1] (device).  Writes the per-level
+ * log-probabilities logp[s*T + t]; when non-NULL also the head logits
+ * head_logits[s*sum(V) + offset_t + v] and, with batch->value_rerank set
+ * (value step at position T), the value-bucket logits
+ * value_logits[s*n_value_buckets + j].  Layered kernels (tcgen05 for
+ * d >= 64), trunk once per request, causal head layers per sequence. */
+int gr4ad_score_sequences(const gr4ad_dims *dims, const gr4ad_weights *w,
+                          const gr4ad_batch *batch, const float *features,
+                          const float *context, int n_seq, const int *req,
+                          const int *tokens, float *logp, float *value_logits,
+                          float *head_logits, void *workspace, size_t workspace_bytes,
+                          void *stream);
+int gr4ad_score_workspace_bytes(const gr4ad_dims *dims, const gr4ad_batch *batch,
+                                int n_seq, size_t *bytes);
+
 /* C = A . BT^T in fp32 (A: (M, K), BT: (N, K), row-major with the given
  * leading dimensions) -- the GEMM the decode uses internally, exposed for
  * numerics tests.  backend 0: CUDA-core fp32; 1: tcgen05 3xTF32 (fp32

@@ -29,7 +29,8 @@ EXPORTS = (
     "gr4ad_workspace_bytes", "gr4ad_beam_search", "gr4ad_prepare",
     "gr4ad_beam_search_run", "gr4ad_context_process", "gr4ad_encoder_kv",
     "gr4ad_topk_precut", "gr4ad_topk_workspace_bytes", "gr4ad_project_topk",
-    "gr4ad_project_topk_workspace_bytes", "gr4ad_gemm",
+    "gr4ad_project_topk_workspace_bytes", "gr4ad_gemm", "gr4ad_score_sequences",
+    "gr4ad_score_workspace_bytes",
 )
 
 _P = C.c_void_p
@@ -102,6 +103,11 @@ def _load():
     lib.gr4ad_project_topk_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
     lib.gr4ad_gemm.argtypes = [_P, C.c_longlong, _P, C.c_longlong, _P, C.c_longlong, C.c_int,
                                C.c_int, C.c_int, C.c_int, _P]
+    lib.gr4ad_score_sequences.argtypes = [C.POINTER(Dims), C.POINTER(Weights), C.POINTER(Batch),
+                                          _P, _P, C.c_int, C.POINTER(C.c_int), _P, _P, _P, _P,
+                                          _P, C.c_size_t, _P]
+    lib.gr4ad_score_workspace_bytes.argtypes = [C.POINTER(Dims), C.POINTER(Batch), C.c_int,
+                                                C.POINTER(C.c_size_t)]
     if lib.gr4ad_abi_version() != 1:
         raise ImportError("libgr4ad ABI version mismatch")
     return lib

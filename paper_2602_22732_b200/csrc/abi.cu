@@ -56,7 +56,7 @@ static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Plan {
   int B = 0, T = 0, L = 0, K = 0, n_pos = 0, d = 0, dff = 0, F = 0, nb = 0, stride = 0;
   int V[GR4AD_MAX_LEVELS] = {};
-  int Vmax = 0;
+  int Vmax = 0, Vsum = 0;
   long long S_tot = 0;
   int S_max = 0;
   bool rerank = false;
@@ -154,7 +154,8 @@ static bool plan_fused(Plan &p) {
   return true;
 }
 
-static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
+static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
+                     long long min_work_rows = 0) {
   if (!dm || !bt) return set_err(GR4AD_ERR_VALUE, "null dims/batch");
   if (dm->n_levels < 1 || dm->n_levels > GR4AD_MAX_LEVELS)
     return set_err(GR4AD_ERR_UNSUPPORTED, "n_levels=%d (max %d)", dm->n_levels, GR4AD_MAX_LEVELS);
@@ -181,6 +182,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
     p.V[t] = dm->vocab[t];
     if (p.V[t] < 1) return set_err(GR4AD_ERR_VALUE, "level_vocab_sizes must be positive");
     p.Vmax = std::max(p.Vmax, p.V[t]);
+    p.Vsum += p.V[t];
   }
   const int B = p.B, T = p.T;
   // each request's context rows start at a 32-row boundary in the layered
@@ -241,7 +243,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p) {
   long long rw = (long long)B * p.n_pos;
   for (int t = 0; t < T; ++t) rw = std::max(rw, p.R[t]);
   if (p.rerank) rw = std::max(rw, p.R[T]);
-  p.Rw = std::max(rw, 1LL);
+  p.Rw = std::max(std::max(rw, min_work_rows), 1LL);
   if (p.H >= (1LL << 31) || p.S_tot >= (1LL << 31))
     return set_err(GR4AD_ERR_UNSUPPORTED, "batch too large");
   bool masked = false;
@@ -391,7 +393,9 @@ __global__ void tile_rows_kernel(const float *src, int n_src, int d, float *dst,
 // one pre-LN decoder layer over a row set (layers.py:66-119)
 struct RowSet {
   int rows;           // rows in the set
-  int max_group_rows; // max rows of one request
+  int max_group_rows; // max rows of one group
+  int groups = 0;     // attention groups (0: one per request)
+  const int *g_ctx_off = nullptr, *g_ctx_len = nullptr;  // per-group context block
   const int *g_row_off, *g_rows, *row_req;
   float *qkv;         // (*, 3d) q/k/v buffer (self-attention history)
   long long hist_row0;
@@ -476,7 +480,9 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   const LayerT *LT = wt ? &wt->layer[i] : nullptr;
   float *N = at<float>(ws, p.o_N), *Q = at<float>(ws, p.o_Q), *A = at<float>(ws, p.o_A);
   float *SC = at<float>(ws, p.o_SC), *Fb = at<float>(ws, p.o_Fb);
-  const int *ctx_off = at<int>(ws, p.o_ctx_off), *ctx_len = at<int>(ws, p.o_ctx_len);
+  const int *ctx_off = rs.g_ctx_off ? rs.g_ctx_off : at<int>(ws, p.o_ctx_off);
+  const int *ctx_len = rs.g_ctx_len ? rs.g_ctx_len : at<int>(ws, p.o_ctx_len);
+  const int n_groups = rs.groups > 0 ? rs.groups : p.B;
   const int nh = p.L - p.K;  // layers whose context K/V are materialised
   const long long ldkv = 2LL * nh * d;
   const bool trunk = i < p.K;
@@ -504,7 +510,7 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   qk.C = SC; qk.ldc = p.sc_ld;
   qk.M = rs.max_group_rows; qk.N = p.S_max; qk.K = d;
   qk.alpha = 1.0f / sqrtf((float)d);
-  qk.groups = p.B; qk.mode = GM_QK;
+  qk.groups = n_groups; qk.mode = GM_QK;
   qk.g_row_off = rs.g_row_off; qk.g_rows = rs.g_rows;
   qk.g_ctx_off = ctx_off; qk.g_ctx_len = ctx_len;
   if (p.tc && tc_eligible(qk.lda, qk.ldb, d, qk.A, qk.B)) {
@@ -567,6 +573,82 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   return GR4AD_OK;
 }
 
+// context projection, head-layer K/V and the trunk (beam.py:159-169): the
+// request-level work every decode of the batch shares
+static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *features,
+                            const float *context, void *ws, WeightsT &wt_store,
+                            const WeightsT *&wt, float *&VT, cudaStream_t st) {
+  const int B = p.B, d = p.d, K = p.K;
+  float *KV = at<float>(ws, p.o_KV), *Ht = at<float>(ws, p.o_Ht);
+  if (p.tc) {
+    GR_TRY(prep_weights_t(p, w, ws, wt_store, st));
+    wt = &wt_store;
+    VT = at<float>(ws, p.o_VT);
+  }
+
+  // context projection (decoder.py:134-140) on 32-row-aligned request blocks
+  if (!features && !context) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
+  const int *in_off = at<int>(ws, p.o_in_off), *ctx_off_d = at<int>(ws, p.o_ctx_off);
+  const int *ctx_len_d = at<int>(ws, p.o_ctx_len);
+  const float *X = at<float>(ws, p.o_X);
+  if (!features) {
+    GR_TRY(pad_rows(context, in_off, ctx_off_d, ctx_len_d, B, d, at<float>(ws, p.o_X), st));
+  } else {
+    float *Fin = at<float>(ws, p.o_Fin);
+    GR_TRY(pad_rows(features, in_off, ctx_off_d, ctx_len_d, B, p.F, Fin, st));
+    features = Fin;
+    float *Xw = at<float>(ws, p.o_X);
+    GemmArgs g = plain_gemm(features, p.F, w->ctx_W, d, Xw, d, (int)p.S_tot, d, p.F);
+    g.bias = w->ctx_b;
+    GR_TRY(dense(p, g, wt ? wt->ctx : nullptr, p.S_tot, EPI_BIAS, st));
+  }
+  // encoder K/V of the head layers, once per request and shared by every beam
+  // (beam.py:98-109); on the tensor-core path the epilogue also writes V^T
+  // for the P.V GEMMs, and X^T serves the trunk's (P X) products
+  {
+    const int nh = p.L - K;
+    GemmArgs g = plain_gemm(X, d, w->cross_kv_W + (size_t)2 * K * d, 2LL * p.L * d, KV,
+                            2LL * nh * d, (int)p.S_tot, 2 * nh * d, d);
+    if (p.tc && tc_eligible(g.lda, d, d, X, wt->kv)) {
+      TcArgs t{};
+      static_cast<GemmArgs &>(t) = g;
+      t.B = wt->kv + (size_t)2 * K * d * d;
+      t.b_lo = t.B + p.wt_floats;
+      t.ldb = d;
+      t.vt = VT;
+      t.vt_ld = p.vt_ld;
+      t.kv_d = d;
+      t.c_lo = at<float>(ws, p.o_KVlo);
+      t.vt_lo = at<float>(ws, p.o_VTlo);
+      GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * nh * d, d, EPI_KV_SPLIT, st));
+      if (K > 0) GR_TRY(transpose(X, d, at<float>(ws, p.o_XT), p.vt_ld, (int)p.S_tot, d, st));
+    } else {
+      if (p.tc) return set_err(GR4AD_ERR_UNSUPPORTED, "tensor-core path: unaligned context");
+      GR_TRY(gemm(g, false, EPI_STORE, st));
+    }
+  }
+
+  // trunk: K layers over the n_pos position rows, shared by all beams (beam.py:159-163)
+  if (K > 0) {
+    long long rows = (long long)B * p.n_pos;
+    GR_LAUNCH(KC_SMALL, st, tile_rows_kernel<<<ceil_div(rows * d, 256), 256, 0, st>>>(w->pos, p.n_pos, d, Ht, rows));
+    RowSet rs{};
+    rs.rows = (int)rows;
+    rs.max_group_rows = p.n_pos;
+    rs.g_row_off = at<int>(ws, p.o_trow_off);
+    rs.g_rows = at<int>(ws, p.o_trows);
+    rs.row_req = at<int>(ws, p.o_trow_req);
+    rs.qkv = at<float>(ws, p.o_QKVt);
+    rs.hist_row0 = 0;
+    rs.anc = at<int>(ws, p.o_tanc);
+    rs.anc_stride = p.n_pos;
+    rs.npos_row = at<int>(ws, p.o_tnpos);
+    for (int i = 0; i < K; ++i) GR_TRY(layer_forward(p, w, wt, i, Ht, rs, ws, KV, VT, st));
+  }
+
+  return GR4AD_OK;
+}
+
 static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
                     const gr4ad_batch *bt, const float *features, const float *context,
                     gr4ad_results *out, void *ws, cudaStream_t st) {
@@ -617,72 +699,8 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
   WeightsT wt_store;
   const WeightsT *wt = nullptr;
   float *VT = nullptr;
-  if (p.tc) {
-    GR_TRY(prep_weights_t(p, w, ws, wt_store, st));
-    wt = &wt_store;
-    VT = at<float>(ws, p.o_VT);
-  }
-
-  // context projection (decoder.py:134-140) on 32-row-aligned request blocks
-  if (!features && !context) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
-  const int *in_off = at<int>(ws, p.o_in_off), *ctx_off_d = at<int>(ws, p.o_ctx_off);
-  const int *ctx_len_d = at<int>(ws, p.o_ctx_len);
-  const float *X = at<float>(ws, p.o_X);
-  if (!features) {
-    GR_TRY(pad_rows(context, in_off, ctx_off_d, ctx_len_d, B, d, at<float>(ws, p.o_X), st));
-  } else {
-    float *Fin = at<float>(ws, p.o_Fin);
-    GR_TRY(pad_rows(features, in_off, ctx_off_d, ctx_len_d, B, p.F, Fin, st));
-    features = Fin;
-    float *Xw = at<float>(ws, p.o_X);
-    GemmArgs g = plain_gemm(features, p.F, w->ctx_W, d, Xw, d, (int)p.S_tot, d, p.F);
-    g.bias = w->ctx_b;
-    GR_TRY(dense(p, g, wt ? wt->ctx : nullptr, p.S_tot, EPI_BIAS, st));
-  }
-  // encoder K/V of the head layers, once per request and shared by every beam
-  // (beam.py:98-109); on the tensor-core path the epilogue also writes V^T
-  // for the P.V GEMMs, and X^T serves the trunk's (P X) products
-  {
-    const int nh = p.L - K;
-    GemmArgs g = plain_gemm(X, d, w->cross_kv_W + (size_t)2 * K * d, 2LL * p.L * d, KV,
-                            2LL * nh * d, (int)p.S_tot, 2 * nh * d, d);
-    if (p.tc && tc_eligible(g.lda, d, d, X, wt->kv)) {
-      TcArgs t{};
-      static_cast<GemmArgs &>(t) = g;
-      t.B = wt->kv + (size_t)2 * K * d * d;
-      t.b_lo = t.B + p.wt_floats;
-      t.ldb = d;
-      t.vt = VT;
-      t.vt_ld = p.vt_ld;
-      t.kv_d = d;
-      t.c_lo = at<float>(ws, p.o_KVlo);
-      t.vt_lo = at<float>(ws, p.o_VTlo);
-      GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * nh * d, d, EPI_KV_SPLIT, st));
-      if (K > 0) GR_TRY(transpose(X, d, at<float>(ws, p.o_XT), p.vt_ld, (int)p.S_tot, d, st));
-    } else {
-      if (p.tc) return set_err(GR4AD_ERR_UNSUPPORTED, "tensor-core path: unaligned context");
-      GR_TRY(gemm(g, false, EPI_STORE, st));
-    }
-  }
+  GR_TRY(encode_and_trunk(p, w, features, context, ws, wt_store, wt, VT, st));
   GR_TRY(init_level0(B, live, cum, prefix, anc, p.stride, tok, st));
-
-  // trunk: K layers over the n_pos position rows, shared by all beams (beam.py:159-163)
-  if (K > 0) {
-    long long rows = (long long)B * p.n_pos;
-    GR_LAUNCH(KC_SMALL, st, tile_rows_kernel<<<ceil_div(rows * d, 256), 256, 0, st>>>(w->pos, p.n_pos, d, Ht, rows));
-    RowSet rs{};
-    rs.rows = (int)rows;
-    rs.max_group_rows = p.n_pos;
-    rs.g_row_off = at<int>(ws, p.o_trow_off);
-    rs.g_rows = at<int>(ws, p.o_trows);
-    rs.row_req = at<int>(ws, p.o_trow_req);
-    rs.qkv = at<float>(ws, p.o_QKVt);
-    rs.hist_row0 = 0;
-    rs.anc = at<int>(ws, p.o_tanc);
-    rs.anc_stride = p.n_pos;
-    rs.npos_row = at<int>(ws, p.o_tnpos);
-    for (int i = 0; i < K; ++i) GR_TRY(layer_forward(p, w, wt, i, Ht, rs, ws, KV, VT, st));
-  }
 
   const int last = p.rerank ? T : T - 1;
   for (int t = 0; t <= last; ++t) {
@@ -855,6 +873,158 @@ int gr4ad_beam_search(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4a
   GR_TRY(gr4ad_prepare(dims, batch, workspace, workspace_bytes, stream));
   return gr4ad_beam_search_run(dims, w, batch, features, context, out, workspace,
                                workspace_bytes, stream);
+}
+
+
+// ---------------------------------------------------------------------------
+// teacher-forced sequence scoring (decoder.py:162-219)
+// ---------------------------------------------------------------------------
+struct ScoreLayout {
+  size_t o_tab, o_qkv, tab_bytes, total;
+  int n_seq, n_pos, rows;
+};
+
+static int score_plan(const gr4ad_dims *dims, const gr4ad_batch *batch, int n_seq, Plan &p,
+                      ScoreLayout &sl) {
+  if (n_seq < 0) return set_err(GR4AD_ERR_VALUE, "n_seq < 0");
+  gr4ad_batch b = *batch;
+  b.decode_path = batch->decode_path == 3 ? 3 : (batch->decode_path == 1 ? 1 : 0);
+  if (b.decode_path == 0) b.decode_path = (dims->d >= 64) ? 3 : 1;  // layered paths only
+  if (b.decode_path == 3) {  // tensor path needs alignment; fall back to CUDA cores
+    bool ok = dims->d % 4 == 0 && dims->d_ff % 4 == 0 && dims->feat_dim % 4 == 0;
+    for (int t = 0; t < dims->n_levels; ++t) ok &= dims->vocab[t] % 4 == 0;
+    if (!ok) b.decode_path = batch->decode_path == 3 ? 3 : 1;
+  }
+  const int n_pos = dims->n_levels + (batch->value_rerank ? 1 : 0);
+  GR_TRY(make_plan(dims, &b, p, (long long)n_seq * n_pos));
+  sl.n_seq = n_seq;
+  sl.n_pos = n_pos;
+  sl.rows = n_seq * n_pos;
+  size_t o = p.total;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = align_up(o + bytes);
+    return r;
+  };
+  const size_t I = sizeof(int);
+  sl.o_tab = take(I * ((size_t)6 * n_seq + (size_t)sl.rows * (3 + n_pos)));
+  sl.tab_bytes = I * ((size_t)6 * n_seq + (size_t)sl.rows * (3 + n_pos));
+  sl.o_qkv = take(sizeof(float) * (size_t)sl.rows * 3 * p.d);
+  sl.total = o;
+  return GR4AD_OK;
+}
+
+int gr4ad_score_workspace_bytes(const gr4ad_dims *dims, const gr4ad_batch *batch, int n_seq,
+                                size_t *bytes) {
+  Plan p;
+  ScoreLayout sl;
+  GR_TRY(score_plan(dims, batch, n_seq, p, sl));
+  if (bytes) *bytes = sl.total;
+  return GR4AD_OK;
+}
+
+int gr4ad_score_sequences(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4ad_batch *batch,
+                          const float *features, const float *context, int n_seq, const int *req,
+                          const int *tokens, float *logp, float *value_logits, float *head_logits,
+                          void *workspace, size_t workspace_bytes, void *stream) {
+  Plan p;
+  ScoreLayout sl;
+  GR_TRY(score_plan(dims, batch, n_seq, p, sl));
+  if (workspace_bytes < sl.total)
+    return set_err(GR4AD_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, sl.total);
+  if (n_seq == 0 || p.B == 0) return GR4AD_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  void *ws = workspace;
+  const int d = p.d, T = p.T, np = sl.n_pos, Rs = sl.rows;
+  // per-sequence tables: attention group = sequence (its request's context),
+  // causal ancestors = earlier positions of the same sequence
+  std::vector<int> tab(sl.tab_bytes / sizeof(int), 0);
+  int *g_row_off = tab.data(), *g_rows = g_row_off + n_seq, *g_ctx_off = g_rows + n_seq;
+  int *g_ctx_len = g_ctx_off + n_seq, *row_grp = g_ctx_len + n_seq + 2 * n_seq;
+  int *vec_row = row_grp + Rs, *npos = vec_row + Rs, *anc = npos + Rs;
+  for (int s = 0; s < n_seq; ++s) {
+    const int r = req[s];
+    if (r < 0 || r >= p.B) return set_err(GR4AD_ERR_VALUE, "sequence %d: request %d out of range", s, r);
+    g_row_off[s] = s * np;
+    g_rows[s] = np;
+    g_ctx_off[s] = p.ctx_off[r];
+    g_ctx_len[s] = p.ctx_len[r];
+    for (int q = 0; q < np; ++q) {
+      const int row = s * np + q;
+      row_grp[row] = s;
+      vec_row[row] = r * np + q;
+      npos[row] = q + 1;
+      for (int tau = 0; tau < np; ++tau) anc[(size_t)row * np + tau] = s * np + std::min(tau, q);
+    }
+  }
+  GR_TRY(upload_tables(p, ws, st));
+  GR_CUDA(cudaMemcpyAsync(at<int>(ws, sl.o_tab), tab.data(), sl.tab_bytes, cudaMemcpyHostToDevice, st));
+  const int *d_tab = at<int>(ws, sl.o_tab);
+  const int *d_row_off = d_tab, *d_rows = d_row_off + n_seq, *d_ctx_off = d_rows + n_seq;
+  const int *d_ctx_len = d_ctx_off + n_seq, *d_row_grp = d_ctx_len + n_seq + 2 * n_seq;
+  const int *d_vec_row = d_row_grp + Rs, *d_npos = d_vec_row + Rs, *d_anc = d_npos + Rs;
+
+  WeightsT wt_store;
+  const WeightsT *wt = nullptr;
+  float *VT = nullptr;
+  GR_TRY(encode_and_trunk(p, w, features, context, ws, wt_store, wt, VT, st));
+  float *KV = at<float>(ws, p.o_KV), *Ht = at<float>(ws, p.o_Ht);
+  float *Hs = at<float>(ws, p.o_Hs), *U = at<float>(ws, p.o_U), *LG = at<float>(ws, p.o_LG);
+  float2 *rinfo = at<float2>(ws, p.o_rinfo);
+  // fused inputs (decoder.py:178-185)
+  SeqInputArgs si{};
+  si.rows = Rs; si.d = d; si.n_pos = np; si.T = T; si.tokens = tokens;
+  si.bos = w->bos; si.pos = w->pos;
+  for (int t = 0; t < T; ++t) si.emb[t] = w->emb[t];
+  if (p.K > 0) {
+    si.U = U;
+    GR_TRY(seq_input(si, st));
+    GemmArgs gg = plain_gemm(U + d, 2LL * d, w->fuse_Wg, d, U, 2LL * d, Rs, d, d);
+    gg.vec = Ht;  // trunk state of (request, position)
+    gg.vec_ld = d;
+    gg.row_req = d_vec_row;
+    GR_TRY(dense(p, gg, wt ? wt->wg : nullptr, Rs, EPI_MULVEC, st));
+    GR_TRY(dense(p, plain_gemm(U, 2LL * d, w->fuse_Wf, d, Hs, d, Rs, d, 2 * d),
+                 wt ? wt->wf : nullptr, Rs, EPI_STORE, st));
+  } else {
+    si.H = Hs;
+    GR_TRY(seq_input(si, st));
+  }
+  // head layers K..L-1 in causal 2-D mode over each sequence (decoder.py:186)
+  RowSet rs{};
+  rs.rows = Rs;
+  rs.max_group_rows = np;
+  rs.groups = n_seq;
+  rs.g_row_off = d_row_off;
+  rs.g_rows = d_rows;
+  rs.g_ctx_off = d_ctx_off;
+  rs.g_ctx_len = d_ctx_len;
+  rs.row_req = d_row_grp;
+  rs.qkv = at<float>(ws, sl.o_qkv);
+  rs.hist_row0 = 0;
+  rs.anc = d_anc;
+  rs.anc_stride = np;
+  rs.npos_row = d_npos;
+  for (int i = p.K; i < p.L; ++i) GR_TRY(layer_forward(p, w, wt, i, Hs, rs, ws, KV, VT, st));
+  // per-level logits of position t (decoder.py:189-194) and log-probabilities
+  long long hoff = 0;
+  for (int t = 0; t < T; ++t) {
+    const int V = p.V[t];
+    GemmArgs g = plain_gemm(Hs + (size_t)t * d, (long long)np * d, w->head[t], V, LG, V, n_seq, V, d);
+    GR_TRY(dense(p, g, wt ? wt->head[t] : nullptr, (long long)n_seq, EPI_STORE, st));
+    GR_TRY(row_lse(LG, V, n_seq, V, rinfo, st));
+    GR_TRY(gather_logp(LG, V, n_seq, rinfo, tokens, T, t, logp, st));
+    if (head_logits)
+      GR_CUDA(cudaMemcpy2DAsync(head_logits + hoff, sizeof(float) * p.Vsum, LG, sizeof(float) * V,
+                                sizeof(float) * V, n_seq, cudaMemcpyDeviceToDevice, st));
+    hoff += V;
+  }
+  if (value_logits && np > T) {  // value-bucket logits at position T (decoder.py:196-197)
+    GemmArgs g = plain_gemm(Hs + (size_t)T * d, (long long)np * d, w->head_value, p.nb,
+                            value_logits, p.nb, n_seq, p.nb, d);
+    GR_TRY(dense(p, g, wt ? wt->hv : nullptr, (long long)n_seq, EPI_STORE, st));
+  }
+  return GR4AD_OK;
 }
 
 int gr4ad_context_process(const gr4ad_dims *dims, const gr4ad_weights *w, const float *features,

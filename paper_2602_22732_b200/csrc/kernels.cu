@@ -750,6 +750,47 @@ int pad_rows(const float *src, const int *in_off, const int *out_off, const int 
 }
 
 // ---------------------------------------------------------------------------
+// teacher-forced inputs (decoder.py:143-152, 180-185): row (s, q) gets BOS at
+// q = 0, else emb_{q-1}[tokens[s][q-1]]; K>0 writes it into U[:, d:2d],
+// K==0 writes H = token + pos[q]
+// ---------------------------------------------------------------------------
+__global__ void seq_input_kernel(SeqInputArgs a) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)a.rows * a.d) return;
+  const int r = (int)(i / a.d), j = (int)(i - (long long)r * a.d);
+  const int s = r / a.n_pos, q = r - s * a.n_pos;
+  const float e = (q == 0) ? a.bos[j]
+                           : a.emb[q - 1][(long long)a.tokens[(long long)s * a.T + q - 1] * a.d + j];
+  if (a.U) a.U[(long long)r * 2 * a.d + a.d + j] = e;
+  else a.H[(long long)r * a.d + j] = e + a.pos[(long long)q * a.d + j];
+}
+
+int seq_input(const SeqInputArgs &a, cudaStream_t st) {
+  long long n = (long long)a.rows * a.d;
+  if (n <= 0) return GR4AD_OK;
+  GR_LAUNCH(KC_SMALL, st, seq_input_kernel<<<ceil_div(n, 256), 256, 0, st>>>(a));
+  return GR4AD_OK;
+}
+
+// logp of the given token from a logits row and its (max, log-sum) (beam.py:92-95)
+__global__ void gather_logp_kernel(const float *__restrict__ logits, long long ld, int rows,
+                                   const float2 *__restrict__ info, const int *__restrict__ tokens,
+                                   int T, int t, float *logp) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= rows) return;
+  const int tok = tokens[(long long)s * T + t];
+  const float2 ri = info[s];
+  logp[(long long)s * T + t] = (logits[(long long)s * ld + tok] - ri.x) - ri.y;
+}
+
+int gather_logp(const float *logits, long long ld, int rows, const float2 *info,
+                const int *tokens, int T, int t, float *logp, cudaStream_t st) {
+  if (rows <= 0) return GR4AD_OK;
+  GR_LAUNCH(KC_SMALL, st, gather_logp_kernel<<<ceil_div(rows, 256), 256, 0, st>>>(logits, ld, rows, info, tokens, T, t, logp));
+  return GR4AD_OK;
+}
+
+// ---------------------------------------------------------------------------
 // level-0 rows
 // ---------------------------------------------------------------------------
 __global__ void init_level0_kernel(int B, int *live0, float *cum, long long *prefix, int *anc,

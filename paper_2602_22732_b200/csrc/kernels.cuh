@@ -77,6 +77,17 @@ int topk_select(const SelectArgs &a, int n_requests, int u_rows, int u_k,
 int pad_rows(const float *src, const int *in_off, const int *out_off, const int *len, int B,
              int width, float *dst, cudaStream_t st);
 
+struct SeqInputArgs {
+  int rows, d, n_pos, T;
+  const int *tokens;  // [n_seq][T]
+  const float *bos, *pos;
+  const float *emb[GR4AD_MAX_LEVELS];
+  float *U, *H;
+};
+int seq_input(const SeqInputArgs &a, cudaStream_t st);
+int gather_logp(const float *logits, long long ld, int rows, const float2 *info,
+                const int *tokens, int T, int t, float *logp, cudaStream_t st);
+
 // level-0 rows: live=1, cum=0, prefix=0, anc[g][0]=g
 int init_level0(int n_requests, int *live0, float *cum, long long *prefix, int *anc,
                 int anc_stride, int *tok, cudaStream_t st);

@@ -151,3 +151,75 @@ class BeamDecoder:
         score = self.score.cpu().numpy().reshape(-1, self.max_out)
         return [[(tuple(int(v) for v in toks[b, j]), float(score[b, j]))
                  for j in range(int(count[b]))] for b in range(self.n_requests)]
+
+
+def score_sequences(model, seq_requests, tokens, features=None, contexts=None,
+                    include_value_step=False, trunk_depth=None, return_logits=False,
+                    device=None, path="auto"):
+    """Teacher-forced scoring on the GPU (lazy_forward + sequence_log_prob,
+    decoder.py:162-219; the RL-log / oracle scoring path).
+
+    ``features`` (or projected ``contexts``) hold one matrix per request;
+    sequence s belongs to request ``seq_requests[s]`` and has ``tokens[s]``
+    (one token per level).  Returns ``logp`` (n_seq, T) float64, plus the
+    value-bucket logits (n_seq, n_value_buckets) with ``include_value_step``
+    and the per-level head logits (list of (n_seq, V_t)) with
+    ``return_logits``."""
+    dev = require_cuda(device)
+    cfg = model.config
+    T = cfg.n_levels
+    items = features if features is not None else contexts
+    if items is None or (features is not None and contexts is not None):
+        raise ValueError("pass exactly one of features / contexts")
+    arrs = [np.atleast_2d(np.asarray(getattr(a, "data", a), dtype=np.float64)) for a in items]
+    toks = np.asarray(tokens, dtype=np.int64).reshape(-1, T)
+    for t in range(T):
+        col = toks[:, t]
+        if col.size and (col.min() < 0 or col.max() >= cfg.level_vocab_sizes[t]):
+            bad = int(col[(col < 0) | (col >= cfg.level_vocab_sizes[t])][0])
+            raise ValueError(f"token {bad} out of range at level {t}")
+    reqs = np.asarray(seq_requests, dtype=np.int32).ravel()
+    n_seq = reqs.size
+    weights = device_weights(model, dev)
+    dims = dims_of(cfg)
+    lens = [a.shape[0] for a in arrs]
+    ctx = (C.c_int * max(len(lens), 1))(*lens)
+    w_arr = (C.c_int * max(len(lens) * T, 1))(*([1] * (len(lens) * T)))
+    bt = N.Batch()
+    bt.n_requests = len(lens)
+    bt.ctx_len = ctx
+    bt.widths = w_arr
+    bt.trunk_depth = -1 if trunk_depth is None else int(trunk_depth)
+    bt.value_rerank = 1 if include_value_step else 0
+    vc = (C.c_int * N.MAX_LEVELS)()
+    bt.valid_prefix_count = vc
+    bt.decode_path = {"auto": 0, "layered": 1, "tensor": 3}[path]
+    nbytes = C.c_size_t()
+    N.check(N.lib.gr4ad_score_workspace_bytes(C.byref(dims), C.byref(bt), n_seq, C.byref(nbytes)))
+    ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=dev)
+    if features is not None:
+        inp = torch.from_numpy(np.concatenate(arrs, 0).astype(np.float32)).to(dev)
+        f, x = C.c_void_p(inp.data_ptr()), None
+    else:
+        inp = torch.from_numpy(np.concatenate(arrs, 0).astype(np.float32)).to(dev)
+        f, x = None, C.c_void_p(inp.data_ptr())
+    tok_d = torch.from_numpy(toks.astype(np.int32)).to(dev)
+    logp = torch.zeros((max(n_seq, 1), T), dtype=torch.float32, device=dev)
+    vl = torch.zeros((max(n_seq, 1), cfg.n_value_buckets), dtype=torch.float32, device=dev)
+    vsum = int(sum(cfg.level_vocab_sizes))
+    hl = torch.zeros((max(n_seq, 1), vsum), dtype=torch.float32, device=dev) if return_logits else None
+    req_c = (C.c_int * max(n_seq, 1))(*reqs.tolist())
+    N.check(N.lib.gr4ad_score_sequences(
+        C.byref(dims), C.byref(weights.struct), C.byref(bt), f, x, n_seq, req_c,
+        C.c_void_p(tok_d.data_ptr()), C.c_void_p(logp.data_ptr()),
+        C.c_void_p(vl.data_ptr()) if include_value_step else None,
+        C.c_void_p(hl.data_ptr()) if return_logits else None,
+        C.c_void_p(ws.data_ptr()), nbytes.value, _stream_handle(dev)))
+    out = [logp.double().cpu().numpy()[:n_seq]]
+    if include_value_step:
+        out.append(vl.double().cpu().numpy()[:n_seq])
+    if return_logits:
+        h = hl.double().cpu().numpy()[:n_seq]
+        offs = np.cumsum([0] + list(cfg.level_vocab_sizes))
+        out.append([h[:, offs[t]:offs[t + 1]] for t in range(T)])
+    return out[0] if len(out) == 1 else tuple(out)

@@ -1,6 +1,7 @@
-from .decoder import (DecoderConfig, DecoderModel, Param, context_process,
-                      load_checkpoint, save_checkpoint)
+from .decoder import (DecoderConfig, DecoderModel, ForwardTrace, Param, context_process,
+                      lazy_forward, load_checkpoint, save_checkpoint, sequence_log_prob)
 from .layers import LN_EPS, LayerCallCounter
 
-__all__ = ["DecoderConfig", "DecoderModel", "Param", "context_process",
+__all__ = ["DecoderConfig", "DecoderModel", "ForwardTrace", "Param", "context_process",
+           "lazy_forward", "sequence_log_prob",
            "load_checkpoint", "save_checkpoint", "LayerCallCounter", "LN_EPS"]

@@ -134,6 +134,55 @@ def context_process(features, params):
     return context_process_gpu(features, params)
 
 
+@dataclass
+class ForwardTrace:
+    """decoder.py:126-131.  Trunk logits feed training losses only and are
+    not computed on the serving path (None)."""
+
+    head_logits: list
+    trunk_logits: object = None
+    value_logits: object = None
+    states: object = None
+
+
+def lazy_forward(model, context, tokens, trunk_depth=None, include_value_step=True,
+                 counter=None):
+    """Teacher-forced forward of one token sequence on the GPU
+    (decoder.py:162-198): per-level head logits and the value-bucket logits."""
+    from paper_2602_22732_b200.decode import score_sequences
+    cfg = model.config
+    k = cfg.trunk_depth if trunk_depth is None else trunk_depth
+    if not 0 <= k < cfg.n_layers:
+        raise ValueError("trunk_depth must satisfy 0 <= K < n_layers")
+    if len(tokens) != cfg.n_levels:
+        raise ValueError(f"expected {cfg.n_levels} tokens, got {len(tokens)}")
+    ctx = getattr(context, "tensor", None)
+    ctx = ctx.double().cpu().numpy() if ctx is not None else getattr(context, "data", context)
+    res = score_sequences(model, [0], [list(tokens)], contexts=[ctx], trunk_depth=k,
+                          include_value_step=include_value_step, return_logits=True)
+    n_pos = cfg.n_levels + (1 if include_value_step else 0)
+    if counter is not None:  # layers.py:79-80 via decoder.py:184-186
+        for _ in range(cfg.n_layers):
+            counter.add_layer_calls(n_pos)
+    if include_value_step:
+        _, vl, heads = res
+        value = Param(vl[0])
+    else:
+        _, heads = res
+        value = None
+    return ForwardTrace([Param(h[0]) for h in heads], None, value)
+
+
+def sequence_log_prob(trace, tokens):
+    """Total log-probability of the sequence under the trace (decoder.py:213-219)."""
+    total = 0.0
+    for t, tok in enumerate(tokens):
+        lg = param_array(trace.head_logits[t])
+        mx = lg.max()
+        total += float((lg[int(tok)] - mx) - np.log(np.exp(lg - mx).sum()))
+    return total
+
+
 def save_checkpoint(model, path, step=0, extra_arrays=None, meta=None):
     """Reference-compatible npz + JSON header (decoder.py:222-247)."""
     c = model.config
