@@ -119,6 +119,16 @@ class BeamDecoder:
         self.graph = None
         self._graph_inputs = None
 
+    def rebind(self, model):
+        """Decode with another snapshot of the same config (hot swap).  The
+        plan and workspace stay; a captured graph is dropped because it
+        holds the previous snapshot's weight pointers."""
+        if model.config != self.cfg:
+            raise ValueError("rebind needs a snapshot with the same DecoderConfig")
+        self.weights = device_weights(model, self.device)
+        self.graph = None
+        self._graph_inputs = None
+
     # -- launch ----------------------------------------------------------
     def run(self, features=None, context=None):
         """features: (sum S, feat_dim) fp32 CUDA tensor, or context: (sum S, d)."""

@@ -51,9 +51,15 @@ def dims_of(cfg, trunk_depth=None):
 
 class DeviceWeights:
     """fp32 copy of ``DecoderModel.params`` on one device + the C struct of
-    pointers into it (gr4ad_weights)."""
+    pointers into it (gr4ad_weights).
 
-    def __init__(self, model, device=None):
+    With ``stream`` the upload is asynchronous: the packed host image is
+    pinned, copied on ``stream`` and ``ready`` records its completion, so a
+    snapshot can be published while decodes keep running on the previous
+    one (consumers order themselves after ``ready`` on the GPU via
+    :func:`device_weights`, never by blocking the host)."""
+
+    def __init__(self, model, device=None, stream=None):
         device = require_cuda(device)
         cfg = model.config
         P = {k: param_array(v) for k, v in model.params.items()}
@@ -81,7 +87,18 @@ class DeviceWeights:
         host = np.zeros(total, dtype=np.float32)
         for k, a in pieces.items():
             host[offs[k]:offs[k] + a.size] = a.astype(np.float32).ravel()
-        self.buffer = torch.from_numpy(host).to(device)
+        self._pinned = None
+        if stream is None:
+            self.buffer = torch.from_numpy(host).to(device)
+            self.ready = None
+        else:
+            pinned = torch.from_numpy(host).pin_memory()
+            with torch.cuda.stream(stream):
+                self.buffer = torch.empty(host.size, dtype=torch.float32, device=device)
+                self.buffer.copy_(pinned, non_blocking=True)
+                self.ready = torch.cuda.Event()
+                self.ready.record(stream)
+            self._pinned = pinned  # alive until the copy has run
         self.device = device
         self.config = cfg
         self.nbytes = host.nbytes
@@ -105,6 +122,18 @@ class DeviceWeights:
             lw.ffn_W1, lw.ffn_b1 = ptr(pre + "ffn.W1"), ptr(pre + "ffn.b1")
             lw.ffn_W2, lw.ffn_b2 = ptr(pre + "ffn.W2"), ptr(pre + "ffn.b2")
         self.struct = w
+
+    def use_on(self, stream=None):
+        """Order ``stream`` (default: current) after the upload and tell the
+        allocator the buffer is in use there, so a replaced snapshot's memory
+        is recycled only after the decodes reading it have finished."""
+        stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if self.ready is not None:
+            stream.wait_event(self.ready)
+            self.buffer.record_stream(stream)
+            if self._pinned is not None and self.ready.query():
+                self._pinned = None
+        return self
 
 
 _CACHE_LOCK = threading.Lock()
@@ -134,14 +163,21 @@ def device_weights(model, device=None):
         hit = _CACHE.get(key)
         if hit is not None and hit[0] == fp:
             _CACHE.move_to_end(key)
-            return hit[2]
+            return hit[2].use_on()
     dw = DeviceWeights(model, device)
+    register(model, dw)
+    return dw
+
+
+def register(model, dw):
+    """Make ``dw`` the resident copy of ``model`` (used by snapshot publish
+    to pre-stage weights before the first decode asks for them)."""
+    key = (id(model.params), str(dw.device))
     with _CACHE_LOCK:
-        _CACHE[key] = (fp, model.params, dw)
+        _CACHE[key] = (_fingerprint(model.params), model.params, dw)
         _CACHE.move_to_end(key)
         while len(_CACHE) > _CACHE_MAX:
             _CACHE.popitem(last=False)
-    return dw
 
 
 def invalidate(model=None):

@@ -12,9 +12,11 @@ compaction all on the device.
 from __future__ import annotations
 
 import threading
+from concurrent.futures import Future
 from dataclasses import dataclass
 
 import numpy as np
+import torch
 
 from ..model.layers import LayerCallCounter
 from .beam import beam_search_batch
@@ -23,21 +25,60 @@ from .schedule import TrafficSignal, scale_schedule, tabs_adjust
 
 
 class SnapshotStore:
-    """Copy-on-publish model snapshots (engine.py:17-36)."""
+    """Copy-on-publish model snapshots (engine.py:17-36), double-buffered on
+    the GPU.
 
-    def __init__(self, model=None):
+    ``publish`` clones the model (the reference contract), packs it and
+    uploads it on a side stream from pinned memory, then swaps the current
+    version atomically: decodes already enqueued keep reading the previous
+    device copy (kept alive by the allocator's stream tracking until they
+    finish), later decodes order themselves after the upload on the GPU.
+    ``publish_async`` runs the clone/pack/upload on a worker thread so the
+    serving thread never stalls on a publish.  Without a CUDA device it is
+    the reference's host-only store.
+    """
+
+    def __init__(self, model=None, device=None, preload=None):
         self._lock = threading.Lock()
+        self._publish_lock = threading.Lock()
         self._version = 0
         self._model = None
+        self._preload = torch.cuda.is_available() if preload is None else preload
+        self._device = device
+        self._stream = None
         if model is not None:
             self.publish(model)
 
+    def _stage(self, snapshot):
+        if not self._preload:
+            return
+        from ..device import DeviceWeights, register, require_cuda
+        dev = require_cuda(self._device)
+        if self._stream is None:
+            self._stream = torch.cuda.Stream(dev)
+        register(snapshot, DeviceWeights(snapshot, dev, stream=self._stream))
+
     def publish(self, model):
         snapshot = model.clone()
-        with self._lock:
-            self._version += 1
-            self._model = snapshot
-            return self._version
+        with self._publish_lock:  # versions are issued in publish order
+            self._stage(snapshot)
+            with self._lock:
+                self._version += 1
+                self._model = snapshot
+                return self._version
+
+    def publish_async(self, model):
+        """Publish from a worker thread; returns a Future of the version."""
+        fut = Future()
+
+        def work():
+            try:
+                fut.set_result(self.publish(model))
+            except BaseException as exc:  # pragma: no cover - surfaced via the future
+                fut.set_exception(exc)
+
+        threading.Thread(target=work, daemon=True).start()
+        return fut
 
     def current(self):
         with self._lock:

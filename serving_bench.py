@@ -1,0 +1,147 @@
+"""Load-adaptive dynamic beam serving on one B200 (BASELINE config 4,
+SURVEY §8d C4).
+
+Real-time Poisson arrivals at 0.1x-1.5x of measured capacity; a batch former
+takes every arrived request (up to --max-batch); each batch's per-level
+widths come from the reference's DBS logic, ``scale_schedule(base,
+tabs_adjust(TrafficSignal(qps, q_threshold=capacity, slack)))`` with
+``slack = clamp(1 - load/capacity, 0, 1)`` (schedule.py:54-70,
+engine.py:100-103): off-peak traffic gets up to 1.6x wider beams, peak
+traffic the base widths.  Request features are synthetic and device
+resident (a pool gathered per batch); latency is arrival -> results on the
+host.  Prints one JSON line per offered load.
+
+    python serving_bench.py [--model c5|c2] [--duration 3] [--loads 0.1,...]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from collections import OrderedDict
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+MODELS = {
+    # (feat_dim, d, d_ff, L, K, vocab, n_buckets), S, base widths
+    "c5": ((16, 1024, 2048, 8, 5, (4096, 4096, 4096), 4), 1024, (64, 128, 256)),
+    "c2": ((16, 16, 32, 2, 1, (256, 256, 256), 4), 256, (64, 128, 256)),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="c5", choices=sorted(MODELS))
+    ap.add_argument("--duration", type=float, default=3.0)
+    ap.add_argument("--loads", default="0.1,0.25,0.5,0.75,1.0,1.25,1.5")
+    ap.add_argument("--max-batch", type=int, default=128)
+    ap.add_argument("--boost", type=float, default=0.6)
+    ap.add_argument("--p99-bound-ms", type=float, default=None)
+    args = ap.parse_args()
+
+    import torch
+
+    from paper_2602_22732_b200.decode import BeamDecoder
+    from paper_2602_22732_b200.model import DecoderConfig, DecoderModel
+    from paper_2602_22732_b200.serving.schedule import (BeamSchedule, TrafficSignal,
+                                                       capacity_slack, scale_schedule,
+                                                       tabs_adjust)
+
+    dev = torch.device("cuda")
+    mcfg, S, base = MODELS[args.model]
+    F, d, dff, L, K, V, nb = mcfg
+    model = DecoderModel(DecoderConfig(F, d, dff, L, K, V, nb, seed=2))
+    base_sched = BeamSchedule(base, base[-1])
+    pool_n = 4 * args.max_batch
+    gen = torch.Generator(device=dev).manual_seed(1000)
+    pool = torch.randn((pool_n, S, F), generator=gen, device=dev)
+
+    buckets = [b for b in (8, 16, 32, 64, 128, 256, 512) if b <= args.max_batch]
+    if buckets[-1] != args.max_batch:
+        buckets.append(args.max_batch)
+    cache = OrderedDict()
+
+    def decoder(nreq, widths):
+        bucket = next(b for b in buckets if b >= nreq)
+        key = (bucket, tuple(widths))
+        dec = cache.get(key)
+        if dec is None:
+            while len(cache) >= len(buckets):
+                cache.popitem(last=False)
+            dec = (BeamDecoder(model, [S] * bucket, [widths] * bucket, device=dev),
+                   torch.empty((bucket * S, F), device=dev))
+            cache[key] = dec
+        cache.move_to_end(key)
+        return dec
+
+    def run_batch(idx, widths):
+        dec, feats = decoder(len(idx), widths)
+        bucket = feats.shape[0] // S
+        rows = torch.as_tensor(np.resize(idx, bucket) % pool_n, device=dev)
+        feats.view(bucket, S, F).copy_(pool.index_select(0, rows))
+        dec.run(features=feats)
+        cnt = dec.count.cpu()  # results on the host (sync)
+        return int(cnt[: len(idx)].sum())
+
+    # capacity at base widths, full batches
+    for _ in range(2):
+        run_batch(np.arange(args.max_batch), base)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps = 5
+    for _ in range(reps):
+        run_batch(np.arange(args.max_batch), base)
+    cap = reps * args.max_batch / (time.perf_counter() - t0)
+    print(json.dumps({"model": args.model, "capacity_req_s": cap, "base_widths": list(base),
+                      "max_batch": args.max_batch}), flush=True)
+
+    rng = np.random.default_rng(7)
+    for rho in [float(x) for x in args.loads.split(",")]:
+        lam = rho * cap
+        n = max(1, int(lam * args.duration))
+        arrivals = np.cumsum(rng.exponential(1.0 / lam, size=n))
+        slack = capacity_slack(lam, cap)
+        active = tabs_adjust(TrafficSignal(lam, cap, slack), base_sched.base_width, args.boost)
+        widths = scale_schedule(base_sched, active).widths
+        for b in buckets:  # plans + workspaces built before the clock starts
+            run_batch(np.arange(b), widths)
+        torch.cuda.synchronize()
+        lat = np.zeros(n)
+        done = 0
+        batches = 0
+        served_results = 0
+        start = time.perf_counter()
+        while done < n:
+            now = time.perf_counter() - start
+            if arrivals[done] > now:
+                time.sleep(min(0.0005, arrivals[done] - now))
+                continue
+            hi = done
+            while hi < n and hi - done < args.max_batch and arrivals[hi] <= now:
+                hi += 1
+            served_results += run_batch(np.arange(done, hi), widths)
+            t_done = time.perf_counter() - start
+            lat[done:hi] = t_done - arrivals[done:hi]
+            batches += 1
+            done = hi
+        wall = time.perf_counter() - start
+        line = {"model": args.model, "offered_load": rho, "offered_req_s": lam,
+                "achieved_req_s": n / wall, "requests": n, "batches": batches,
+                "mean_batch": n / batches, "tabs_active_width": active, "widths": list(widths),
+                "slack": slack, "latency_ms": {"p50": 1e3 * float(np.percentile(lat, 50)),
+                                               "p99": 1e3 * float(np.percentile(lat, 99))},
+                "results": served_results}
+        if args.p99_bound_ms is not None:
+            line["p99_within_bound"] = line["latency_ms"]["p99"] <= args.p99_bound_ms
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
