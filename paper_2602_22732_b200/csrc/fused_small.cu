@@ -58,33 +58,68 @@ __device__ __forceinline__ void publish(const float (&v)[E], float *slot) {
   __syncwarp();
 }
 
-// acc[e] = sum_i slot[i][row] * W[i][cb + e]   (W row-major, row stride ldw)
+// acc[e] = sum_i slot[i][row] * W[i][cb + e]   (W row-major, row stride ldw);
+// two partial sums (even / odd i) halve the dependent FMA chain
 template <int E>
 __device__ __forceinline__ void proj(const float *slot, int din, const float *__restrict__ W,
                                      int ldw, float (&acc)[E]) {
   const int lane = threadIdx.x & 31, rl = lane >> 3, cb = (lane & 7) * E;
+  float a2[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+  for (int e = 0; e < E; ++e) acc[e] = a2[e] = 0.f;
   const float *w = W + cb;
 #pragma unroll 4
-  for (int i = 0; i < din; ++i) {
-    const float x = slot[i * 4 + rl];
+  for (int i = 0; i < din; i += 2) {
+    const float x0 = slot[i * 4 + rl], x1 = slot[(i + 1) * 4 + rl];
     if (E % 4 == 0) {
 #pragma unroll
       for (int e = 0; e < E; e += 4) {
-        float4 w4 = __ldg(reinterpret_cast<const float4 *>(w + (size_t)i * ldw + e));
-        acc[e] = fmaf(x, w4.x, acc[e]);
-        acc[e + 1] = fmaf(x, w4.y, acc[e + 1]);
-        acc[e + 2] = fmaf(x, w4.z, acc[e + 2]);
-        acc[e + 3] = fmaf(x, w4.w, acc[e + 3]);
+        const float4 u = __ldg(reinterpret_cast<const float4 *>(w + (size_t)i * ldw + e));
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(w + (size_t)(i + 1) * ldw + e));
+        acc[e] = fmaf(x0, u.x, acc[e]);
+        acc[e + 1] = fmaf(x0, u.y, acc[e + 1]);
+        acc[e + 2] = fmaf(x0, u.z, acc[e + 2]);
+        acc[e + 3] = fmaf(x0, u.w, acc[e + 3]);
+        a2[e] = fmaf(x1, v.x, a2[e]);
+        a2[e + 1] = fmaf(x1, v.y, a2[e + 1]);
+        a2[e + 2] = fmaf(x1, v.z, a2[e + 2]);
+        a2[e + 3] = fmaf(x1, v.w, a2[e + 3]);
       }
     } else {
 #pragma unroll
       for (int e = 0; e < E; e += 2) {
-        float2 w2 = __ldg(reinterpret_cast<const float2 *>(w + (size_t)i * ldw + e));
-        acc[e] = fmaf(x, w2.x, acc[e]);
-        acc[e + 1] = fmaf(x, w2.y, acc[e + 1]);
+        const float2 u = __ldg(reinterpret_cast<const float2 *>(w + (size_t)i * ldw + e));
+        const float2 v = __ldg(reinterpret_cast<const float2 *>(w + (size_t)(i + 1) * ldw + e));
+        acc[e] = fmaf(x0, u.x, acc[e]);
+        acc[e + 1] = fmaf(x0, u.y, acc[e + 1]);
+        a2[e] = fmaf(x1, v.x, a2[e]);
+        a2[e + 1] = fmaf(x1, v.y, a2[e + 1]);
       }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] += a2[e];
+}
+
+// acc[e] = sum_j slot[j][row] * W[cb + e][j]   (the transposed product, for
+// the trunk's reassociated attention u = q Wk^T)
+template <int E>
+__device__ __forceinline__ void proj_t(const float *slot, int din, const float *__restrict__ W,
+                                       int ldw, float (&acc)[E]) {
+  const int lane = threadIdx.x & 31, rl = lane >> 3, cb = (lane & 7) * E;
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+#pragma unroll 2
+  for (int j = 0; j < din; j += 4) {
+    const float x0 = slot[j * 4 + rl], x1 = slot[(j + 1) * 4 + rl];
+    const float x2 = slot[(j + 2) * 4 + rl], x3 = slot[(j + 3) * 4 + rl];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const float4 w4 = __ldg(reinterpret_cast<const float4 *>(W + (size_t)(cb + e) * ldw + j));
+      acc[e] = fmaf(x0, w4.x, acc[e]);
+      acc[e] = fmaf(x1, w4.y, acc[e]);
+      acc[e] = fmaf(x2, w4.z, acc[e]);
+      acc[e] = fmaf(x3, w4.w, acc[e]);
     }
   }
 }
@@ -270,6 +305,65 @@ __device__ __forceinline__ void hist_add(unsigned *hist, int &cur, unsigned &cnt
   }
 }
 
+// Descending bitonic sort of buf[0, n2) (n2 a power of two >= 64, sorted by
+// the whole 64-bit key).  Stages with stride >= 64 run block-wide through
+// shared memory; the stride <= 32 tail of every merge runs in registers:
+// warp w owns 64-entry chunks (lane holds entries lane and lane + 32) and
+// exchanges with __shfl_xor -- ~log2(n2) block barriers instead of
+// log2(n2)^2 / 2.
+__device__ __forceinline__ unsigned long long cmpx(unsigned long long mine,
+                                                   unsigned long long other, bool take_max) {
+  return take_max ? (mine > other ? mine : other) : (mine < other ? mine : other);
+}
+
+__device__ void warp_merge_tail(unsigned long long *buf, int n2, int size, int st_hi) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = wid * 64; base < n2; base += kWarps * 64) {
+    unsigned long long e0 = buf[base + lane], e1 = buf[base + lane + 32];
+    const int i0 = base + lane, i1 = i0 + 32;
+    for (int sz = (size > 0 ? size : 2); sz <= (size > 0 ? size : 64); sz <<= 1) {
+      for (int st = (size > 0 ? st_hi : sz >> 1); st > 0; st >>= 1) {
+        if (st == 32) {
+          const bool desc = (i0 & sz) == 0;  // i0 is the low side of (i0, i1)
+          const unsigned long long hi = e0 > e1 ? e0 : e1, lo = e0 > e1 ? e1 : e0;
+          e0 = desc ? hi : lo;
+          e1 = desc ? lo : hi;
+        } else {
+          const unsigned long long o0 = __shfl_xor_sync(kFull, e0, st);
+          const unsigned long long o1 = __shfl_xor_sync(kFull, e1, st);
+          const bool low0 = (i0 & st) == 0, low1 = (i1 & st) == 0;
+          const bool d0 = (i0 & sz) == 0, d1 = (i1 & sz) == 0;
+          e0 = cmpx(e0, o0, low0 == d0);
+          e1 = cmpx(e1, o1, low1 == d1);
+        }
+      }
+    }
+    buf[base + lane] = e0;
+    buf[base + lane + 32] = e1;
+  }
+}
+
+__device__ void sort_desc(unsigned long long *buf, int n2) {
+  warp_merge_tail(buf, n2, 0, 0);  // sizes 2..64 entirely in registers
+  __syncthreads();
+  for (int size = 128; size <= n2; size <<= 1) {
+    for (int st = size >> 1; st >= 64; st >>= 1) {
+      for (int i = threadIdx.x; i < n2 / 2; i += kThreads) {
+        const int lo = 2 * i - (i & (st - 1)), hi = lo + st;
+        const bool desc = (lo & size) == 0;
+        const unsigned long long x = buf[lo], y = buf[hi];
+        if ((x < y) == desc) {
+          buf[lo] = y;
+          buf[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+    warp_merge_tail(buf, n2, size, 32);
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 #ifdef GR_FUSED_TIMING
@@ -316,48 +410,86 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
   GR_STAMP(0);
 
   // ---- context projection X = F W_c + b_c (decoder.py:134-140) -------------
-  for (int e = tid; e < S * D; e += kThreads) {
-    int s = e / D, j = e - s * D;
-    float x;
-    if (a.features) {
-      const float *f = a.features + (coff + s) * a.F;
-      float acc = 0.f;
-      for (int i = 0; i < a.F; ++i) acc = fmaf(__ldg(f + i), __ldg(W.ctx_W + (size_t)i * D + j), acc);
-      x = acc + __ldg(W.ctx_b + j);
-    } else {
-      x = __ldg(a.context + (coff + s) * D + j);
+  // thread s owns key s: its feature row in registers, W_c rows broadcast
+  for (int s = tid; s < SP; s += kThreads) {
+    float x[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) x[j] = 0.f;
+    if (s < S) {
+      if (a.features) {
+        const float *f = a.features + (coff + s) * a.F;
+        for (int i = 0; i < a.F; ++i) {
+          const float fi = __ldg(f + i);
+#pragma unroll
+          for (int j = 0; j < D; j += 4) {
+            const float4 w4 = __ldg(reinterpret_cast<const float4 *>(W.ctx_W + (size_t)i * D + j));
+            x[j] = fmaf(fi, w4.x, x[j]);
+            x[j + 1] = fmaf(fi, w4.y, x[j + 1]);
+            x[j + 2] = fmaf(fi, w4.z, x[j + 2]);
+            x[j + 3] = fmaf(fi, w4.w, x[j + 3]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] += __ldg(W.ctx_b + j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] = __ldg(a.context + (coff + s) * D + j);
+      }
     }
-    Xs[j * SP + s] = x;
+#pragma unroll
+    for (int j = 0; j < D; ++j) Xs[j * SP + s] = x[j];
   }
   __syncthreads();
   GR_STAMP(1);
 
-  // K^T / V^T of `layer` into `slot` (keys >= S are zero)
-  auto build_kv = [&](int layer, int slot) {
+  // K^T / V^T of head layer `layer` into `slot` (keys >= S are zero); thread
+  // tid - t0 owns keys s, s + nt, ...: X column in registers, weight rows as
+  // broadcast float4 loads, 8 output columns per pass
+  auto build_kv = [&](int layer, int slot, int t0, int nt) {
     float *Kt = KV + (size_t)slot * 2 * KVS;
     const int ldw = 2 * L * D;
     const float *Wl = W.cross_kv_W + (size_t)(2 * layer) * D;
-    for (int e = tid; e < 2 * D * SP; e += kThreads) {
-      int c = e / SP, s = e - c * SP;  // c < D: K column c, else V column c - D
-      float acc = 0.f;
-      if (s < S) {  // lanes walk consecutive keys: conflict-free X^T reads
+    for (int s = tid - t0; s < SP; s += nt) {
+      float x[D];
 #pragma unroll
-        for (int i = 0; i < D; ++i) acc = fmaf(Xs[i * SP + s], __ldg(Wl + (size_t)i * ldw + c), acc);
+      for (int i = 0; i < D; ++i) x[i] = Xs[i * SP + s];
+#pragma unroll 1
+      for (int c0 = 0; c0 < 2 * D; c0 += 8) {
+        float acc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          const float4 wa = __ldg(reinterpret_cast<const float4 *>(Wl + (size_t)i * ldw + c0));
+          const float4 wb = __ldg(reinterpret_cast<const float4 *>(Wl + (size_t)i * ldw + c0 + 4));
+          acc[0] = fmaf(x[i], wa.x, acc[0]);
+          acc[1] = fmaf(x[i], wa.y, acc[1]);
+          acc[2] = fmaf(x[i], wa.z, acc[2]);
+          acc[3] = fmaf(x[i], wa.w, acc[3]);
+          acc[4] = fmaf(x[i], wb.x, acc[4]);
+          acc[5] = fmaf(x[i], wb.y, acc[5]);
+          acc[6] = fmaf(x[i], wb.z, acc[6]);
+          acc[7] = fmaf(x[i], wb.w, acc[7]);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) Kt[(c0 + c) * SP + s] = s < S ? acc[c] : 0.f;
       }
-      Kt[c * SP + s] = acc;
     }
   };
 
   const int np = a.n_pos;
   // ---- trunk: K layers over the n_pos position rows (beam.py:159-163) -------
-  if (K > 0) {
-    for (int e = tid; e < np * D; e += kThreads) TR[e] = __ldg(W.pos + e);
+  // Warp 0 alone (n_pos <= 9 rows), reassociated so the trunk layers' K/V are
+  // never built: scores (q Wk^T) X^T, output (P X) Wv.  Warps 1-7 build the
+  // head layers' K/V meanwhile.
+  if (K > 0 && wid == 0) {
+    for (int e = lane; e < np * D; e += 32) TR[e] = __ldg(W.pos + e);
+    __syncwarp();
+    const int ldw = 2 * L * D;
     for (int i = 0; i < K; ++i) {
-      __syncthreads();
-      build_kv(i, 0);
-      __syncthreads();
       const gr4ad_layer &Lw = W.layer[i];
-      for (int p0 = wid * RW; p0 < np; p0 += kWarps * RW) {
+      const float *Wk = W.cross_kv_W + (size_t)(2 * i) * D, *Wv = Wk + D;
+      for (int p0 = 0; p0 < np; p0 += RW) {
         const int p = p0 + rl, pp = min(p, np - 1);
         const bool ok = p < np;
         float h[E], n[E], t[E];
@@ -367,7 +499,11 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
         publish<E>(n, slot0);
         proj<E>(slot0, D, Lw.cross_Wq, D, t);
         publish<E>(t, slot1);
-        cross_attn<D>(slot1, KV, KV + KVS, S, slot2, t);
+        proj_t<E>(slot1, D, Wk, ldw, t);  // u = q Wk^T, u . x_s == q . k_s
+        publish<E>(t, slot0);
+        cross_attn<D>(slot0, Xs, Xs, S, slot2, t);  // t = P X
+        publish<E>(t, slot1);
+        proj<E>(slot1, D, Wv, ldw, t);  // (P X) Wv == P V
         publish<E>(t, slot0);
         proj<E>(slot0, D, Lw.cross_Wo, D, t);
 #pragma unroll
@@ -384,8 +520,8 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
 #pragma unroll
           for (int e = 0; e < E; ++e) TR[p * D + cb + e] = h[e];
       }
-      __syncthreads();
-      for (int p0 = wid * RW; p0 < np; p0 += kWarps * RW) {
+      __syncwarp();
+      for (int p0 = 0; p0 < np; p0 += RW) {
         const int p = p0 + rl, pp = min(p, np - 1);
         const bool ok = p < np;
         const int rmax_w = min(p0 + RW, np) - 1;  // warp-uniform loop bound
@@ -428,18 +564,20 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
 #pragma unroll
           for (int e = 0; e < E; ++e) TR[p * D + cb + e] = h[e];
       }
+      __syncwarp();
     }
+  } else {
+    // head-layer K/V, built once and shared by every beam (beam.py:165-169)
+    const int t0 = K > 0 ? 32 : 0;
+    for (int i = K; i < L; ++i) build_kv(i, i - K, t0, kThreads - t0);
   }
-  __syncthreads();
-  GR_STAMP(2);
-  // head-layer K/V, built once and shared by every beam (beam.py:165-169)
-  for (int i = K; i < L; ++i) build_kv(i, i - K);
   if (tid == 0) {
     par[0] = 0;
     tokm[0] = 0;
     cum[0] = 0.f;
   }
   __syncthreads();
+  GR_STAMP(2);
   GR_STAMP(3);
 
   const int last = a.rerank ? T : T - 1;
@@ -452,11 +590,14 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
     // (logp <= 0).  Candidates are binned by min((Rs - s) * scale, 2047), a
     // monotone map of the score, with 2048 bins over ln V + 4 score units,
     // so the k-th best usually lands in a bin holding a handful of keys.
-    if (tid == 0) {
+    if (wid == 0) {
       float mc = -INFINITY;
-      for (int j = 0; j < live; ++j) mc = fmaxf(mc, cum[mo + j]);
-      scr[48] = __float_as_uint(mc);
-      scr[49] = __float_as_uint(2048.0f / (logf((float)max(V, 2)) + 4.0f));
+      for (int j = lane; j < live; j += 32) mc = fmaxf(mc, cum[mo + j]);
+      mc = warp_max(mc);
+      if (lane == 0) {
+        scr[48] = __float_as_uint(mc);
+        scr[49] = __float_as_uint(2048.0f / (logf((float)max(V, 2)) + 4.0f));
+      }
     }
     __syncthreads();
     const float Rs = __uint_as_float(scr[48]);
@@ -702,14 +843,25 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
         __syncthreads();
         const uint4 *keys4 = reinterpret_cast<const uint4 *>(keys);
         const int n4 = n_cand / 4;
-        for (int i4 = tid; i4 < n4; i4 += kThreads) {
-          const uint4 u4 = keys4[i4];
-          const uint32_t us[4] = {u4.x, u4.y, u4.z, u4.w};
+        // 8 independent L2 loads in flight per thread, then filter
+        constexpr int U = 8;
+        for (int i0 = tid; i0 < n4; i0 += U * kThreads) {
+          uint4 u4[U];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (sbin(ord2f(us[q])) <= (unsigned)wb) {
-              unsigned pos = atomicAdd(&scr[40], 1u);
-              sbuf[pos] = ((unsigned long long)us[q] << 32) | (0xFFFFFFFFu - (unsigned)(i4 * 4 + q));
+          for (int j = 0; j < U; ++j) {
+            const int i4 = i0 + j * kThreads;
+            u4[j] = i4 < n4 ? keys4[i4] : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            const int i4 = i0 + j * kThreads;
+            const uint32_t us[4] = {u4[j].x, u4[j].y, u4[j].z, u4[j].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (i4 < n4 && sbin(ord2f(us[q])) <= (unsigned)wb) {
+                unsigned pos = atomicAdd(&scr[40], 1u);
+                sbuf[pos] = ((unsigned long long)us[q] << 32) | (0xFFFFFFFFu - (unsigned)(i4 * 4 + q));
+              }
             }
           }
         }
@@ -794,23 +946,11 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
       }
     }
     __syncthreads();
-    int n2 = 1;
+    int n2 = 64;
     while (n2 < n_sort) n2 <<= 1;
     for (int i = n_sort + tid; i < n2; i += kThreads) sbuf[i] = 0ull;
     __syncthreads();
-    for (int size = 2; size <= n2; size <<= 1)
-      for (int st = size >> 1; st > 0; st >>= 1) {
-        for (int i = tid; i < n2 / 2; i += kThreads) {
-          int lo = 2 * i - (i & (st - 1)), hi = lo + st;
-          bool desc = (lo & size) == 0;
-          unsigned long long x = sbuf[lo], y = sbuf[hi];
-          if ((x < y) == desc) {
-            sbuf[lo] = y;
-            sbuf[hi] = x;
-          }
-        }
-        __syncthreads();
-      }
+    sort_desc(sbuf, n2);
     // compaction: next-level rows in selection order (beam.py:202-210)
     const int mo1 = a.moff[t + 1];
     for (int j = tid; j < k; j += kThreads) {
