@@ -102,8 +102,10 @@ typedef struct {
    * fits on chip (d in {16,32}, d_ff in {d,2d}, S <= 32d, widths <= 2048,
    * no masking), else the layered batch path, with tcgen05 3xTF32 GEMMs
    * when d >= 64 (and d, d_ff, F, V multiples of 4); 1: layered with
-   * CUDA-core GEMMs; 2: fused; 3: layered with tcgen05 GEMMs.  Forcing an
-   * ineligible path returns GR4AD_ERR_UNSUPPORTED. */
+   * CUDA-core GEMMs; 2: fused (its warp-level tensor-core variant -- mma.sync
+   * 3xTF32 -- when d = 16, else CUDA cores); 3: layered with tcgen05 GEMMs;
+   * 4: fused on CUDA cores only.  Forcing an ineligible path returns
+   * GR4AD_ERR_UNSUPPORTED. */
   int decode_path;
 } gr4ad_batch;
 

@@ -87,13 +87,100 @@ struct Plan {
   long long wt_floats = 0;
   // fused small-model path
   bool fused = false;
-  int f_Hrows = 0, f_sort_cap = 0;
+  int f_Hrows = 0, f_sort_cap = 0, f_Hrows_mma = 0;
   int f_hoff[GR4AD_MAX_LEVELS + 2] = {}, f_moff[GR4AD_MAX_LEVELS + 2] = {};
+  int f_hoff4[GR4AD_MAX_LEVELS + 2] = {};
   int f_s[12] = {};  // smem offsets (floats): X KV TR TQ hist par tok cum bins scr sort ws
   size_t f_smem = 0;
   long long f_keys_per_req = 0;
   size_t o_keys = 0, o_wT = 0;
+  // warp-MMA variant of the fused kernel (d = 16)
+  bool f_mma = false;
+  int f_s4[14] = {};  // as f_s, plus [12] = X^T, [13] = tile-group merge scratch
+  size_t f_smem4 = 0;
+  long long frag_f4 = 0;  // fragment-ordered weights (float4 count)
+  size_t o_frag = 0;
 };
+
+// Fragment-ordered weight jobs of the warp-MMA fused kernel; with w == NULL
+// only the offsets / total are computed (planning).
+static long long frag_layout(const Plan &p, const gr4ad_weights *w, FragJobs *jobs,
+                             FragIndex *fi) {
+  const int d = p.d;
+  long long off = 0;
+  if (jobs) jobs->n = 0;
+  auto add = [&](const float *src, long long sk, long long sn, int kin, int nout,
+                 int nreal) -> long long {
+    if (jobs) jobs->job[jobs->n++] = FragJob{src, sk, sn, off, kin, nout, nreal};
+    const long long r = off;
+    off += (long long)(kin / 8) * (nout / 8) * 32;
+    return r;
+  };
+  const gr4ad_weights z{};
+  const gr4ad_weights &W = w ? *w : z;
+  fi->wg = add(W.fuse_Wg, d, 1, d, d, d);
+  fi->wf_m = add(W.fuse_Wf, d, 1, d, d, d);
+  fi->wf_s = add(W.fuse_Wf ? W.fuse_Wf + (size_t)d * d : nullptr, d, 1, d, d, d);
+  fi->value = add(W.head_value, p.nb, 1, d, 8, p.nb);
+  for (int i = p.K; i < p.L; ++i) {
+    const int li = i - p.K;
+    const gr4ad_layer &Lw = W.layer[i];
+    auto sh = [&](const float *q, size_t o) { return q ? q + o : nullptr; };
+    fi->cq[li] = add(Lw.cross_Wq, d, 1, d, d, d);
+    fi->co[li] = add(Lw.cross_Wo, d, 1, d, d, d);
+    fi->sq[li] = add(Lw.self_Wqkv, 3LL * d, 1, d, d, d);
+    fi->sk[li] = add(sh(Lw.self_Wqkv, d), 3LL * d, 1, d, d, d);
+    fi->sv[li] = add(sh(Lw.self_Wqkv, 2 * (size_t)d), 3LL * d, 1, d, d, d);
+    fi->so[li] = add(Lw.self_Wo, d, 1, d, d, d);
+    fi->w1[li] = add(Lw.ffn_W1, p.dff, 1, d, p.dff, p.dff);
+    fi->w2[li] = add(Lw.ffn_W2, d, 1, p.dff, d, d);
+  }
+  for (int t = 0; t < p.T; ++t) fi->head[t] = add(W.head[t], p.V[t], 1, d, p.V[t], p.V[t]);
+  return off;
+}
+
+// Shared-memory plan of the warp-MMA fused kernel (run after plan_fused).
+static bool plan_fused_mma(Plan &p) {
+  const int D = p.d;
+  if (D != 16 || p.L - p.K > kMaxHeadLayersMma) return false;
+  const int SPn = 256, VS = SPn + 8, HS = 2 * D + 8;
+  const int last = p.rerank ? p.T : p.T - 1;
+  long long hrows = 0, mrows = 0;
+  for (int t = 0; t <= p.T; ++t) {
+    mrows += p.maxcap[t];
+    p.f_hoff4[t] = (int)hrows;
+    if (t < last) hrows += p.maxcap[t];  // the last level's history is never read
+  }
+  long long o = 0;
+  auto take = [&](long long floats) {
+    long long r = o;
+    o += (floats + 3) / 4 * 4;
+    return (int)r;
+  };
+  const long long xt = (long long)D * VS, kvl = (long long)SPn * D + xt;
+  const long long hist_floats = (long long)(p.L - p.K) * std::max(hrows, 1LL) * HS;
+  p.f_s4[0] = take(std::max(xt, hist_floats));  // X^T, later the history
+  p.f_s4[12] = p.f_s4[0];
+  p.f_s4[4] = p.f_s4[0];
+  p.f_s4[1] = take((long long)(p.L - p.K) * kvl);  // K [S][D] (swizzled) + V^T [D][S+8]
+  p.f_s4[2] = take((long long)p.n_pos * D);
+  p.f_s4[3] = take((long long)p.n_pos * 3 * D);
+  p.f_s4[5] = take(mrows);
+  p.f_s4[6] = take(mrows);
+  p.f_s4[7] = take(mrows);
+  p.f_s4[8] = take(2048);
+  p.f_s4[9] = take(64);
+  p.f_s4[10] = take(2LL * p.f_sort_cap);
+  p.f_s4[11] = take(4LL * 4 * D);  // warp 0's trunk slots
+  p.f_s4[13] = take(8LL * 16 * (D + 2));  // 8 warps x 16 rows x (D + 2)
+  const size_t bytes = (size_t)o * sizeof(float);
+  if (bytes > 110 * 1024) return false;  // two CTAs per SM
+  p.f_smem4 = bytes;
+  p.f_Hrows_mma = (int)std::max(hrows, 1LL);
+  FragIndex fi;
+  p.frag_f4 = frag_layout(p, nullptr, nullptr, &fi);
+  return true;
+}
 
 
 // Shared-memory plan of the fused per-request kernel; false if it does not fit.
@@ -248,8 +335,9 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     return set_err(GR4AD_ERR_UNSUPPORTED, "batch too large");
   bool masked = false;
   for (int t = 0; t < T; ++t) masked |= bt->valid_prefix[t] != nullptr;
-  if (bt->decode_path != 1 && !masked && B > 0) p.fused = plan_fused(p);
-  if (bt->decode_path == 2 && !p.fused)
+  if (bt->decode_path != 1 && bt->decode_path != 3 && !masked && B > 0) p.fused = plan_fused(p);
+  if (p.fused && bt->decode_path != 4) p.f_mma = plan_fused_mma(p);
+  if ((bt->decode_path == 2 || bt->decode_path == 4) && !p.fused)
     return set_err(GR4AD_ERR_UNSUPPORTED, "fused decode path not eligible for this batch");
   if (!p.fused) {
     bool ok = p.d % 4 == 0 && p.dff % 4 == 0 && p.F % 4 == 0;
@@ -298,6 +386,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.o_tnpos = take(I * (size_t)B * p.n_pos);
   p.table_bytes = o;
   if (p.fused) {
+    if (p.f_mma) p.o_frag = take(16 * (size_t)p.frag_f4);
     p.o_keys = take(sizeof(uint32_t) * (size_t)B * p.f_keys_per_req);
     take(sizeof(long long) * 16 * (size_t)B);  // per-request phase stamps (timing builds)
     p.total = o;
@@ -682,6 +771,22 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     f.out_count = out->count; f.out_tokens = out->tokens; f.out_score = out->score;
     f.dbg = reinterpret_cast<long long *>(static_cast<char *>(ws) + p.total -
                                           (size_t)B * 16 * sizeof(long long));
+    if (p.f_mma) {
+      f.s_X = p.f_s4[0]; f.s_KV = p.f_s4[1]; f.s_TR = p.f_s4[2]; f.s_TQ = p.f_s4[3];
+      f.s_hist = p.f_s4[4]; f.s_par = p.f_s4[5]; f.s_tok = p.f_s4[6]; f.s_cum = p.f_s4[7];
+      f.s_bins = p.f_s4[8]; f.s_scr = p.f_s4[9]; f.s_sort = p.f_s4[10]; f.s_ws = p.f_s4[11];
+      f.s_XT = p.f_s4[12];
+      f.s_mrg = p.f_s4[13];
+      f.tile_split = 1;
+      f.Hrows = p.f_Hrows_mma;
+      for (int t = 0; t < GR4AD_MAX_LEVELS + 2; ++t) f.hoff[t] = p.f_hoff4[t];
+      static thread_local FragJobs jobs;  // ~6 KB: kept off the stack
+      float4 *frag = at<float4>(ws, p.o_frag);
+      frag_layout(p, w, &jobs, &f.fi);
+      f.frag = frag;
+      GR_TRY(frag_prep_launch(jobs, frag, st));
+      return fused_mma_launch(f, B, p.f_smem4, st);
+    }
     return fused_small_launch(f, B, p.f_smem, st);
   }
   int *eff = at<int>(ws, p.o_eff), *cap = at<int>(ws, p.o_cap);

@@ -39,6 +39,11 @@ __device__ __forceinline__ float rmax(float v) {
 }
 
 // tanh-GELU (autodiff.py:301-306) via 0.5*a*(1+tanh z) == a / (1 + exp(-2z))
+__device__ __forceinline__ float gelu_fast(float a) {
+  const float c = 0.7978845608028654f;
+  float z = (a + 0.044715f * a * a * a) * c;
+  return __fdividef(a, 1.0f + __expf(-2.0f * z));
+}
 __device__ __forceinline__ float gelu_exp(float a) {
   const float c = 0.7978845608028654f;
   float z = (a + 0.044715f * a * a * a) * c;
@@ -147,7 +152,7 @@ __device__ __forceinline__ void layer_norm(const float (&h)[E], const float *g, 
 // K^T / V^T (D x SP each): q in a slot; result in the row-lane layout.
 template <int D>
 __device__ __forceinline__ void cross_attn(const float *qslot, const float *KT, const float *VT,
-                                           int S, float *oslot, float (&out)[D / 8]) {
+                                           int S, int ld, float *oslot, float (&out)[D / 8]) {
   const int lane = threadIdx.x & 31;
   const float scale = 1.0f / sqrtf((float)D);
   float sc[RW][8];
@@ -158,8 +163,8 @@ __device__ __forceinline__ void cross_attn(const float *qslot, const float *KT, 
 #pragma unroll 4
   for (int i = 0; i < D; ++i) {
     const float4 q4 = *reinterpret_cast<const float4 *>(qslot + i * 4);
-    const float4 ka = *reinterpret_cast<const float4 *>(KT + i * SP + lane * 8);
-    const float4 kb = *reinterpret_cast<const float4 *>(KT + i * SP + lane * 8 + 4);
+    const float4 ka = *reinterpret_cast<const float4 *>(KT + i * ld + lane * 8);
+    const float4 kb = *reinterpret_cast<const float4 *>(KT + i * ld + lane * 8 + 4);
     const float qq[4] = {q4.x, q4.y, q4.z, q4.w};
     const float kk[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
 #pragma unroll
@@ -196,7 +201,7 @@ __device__ __forceinline__ void cross_attn(const float *qslot, const float *KT, 
     for (int k = 0; k < 32; ++k) acc[k] = 0.f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float *vrow = VT + (h * 8 + j) * SP + lane * 8;
+      const float *vrow = VT + (h * 8 + j) * ld + lane * 8;
       const float4 va = *reinterpret_cast<const float4 *>(vrow);
       const float4 vb = *reinterpret_cast<const float4 *>(vrow + 4);
       const float vv[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
@@ -321,7 +326,9 @@ __device__ void warp_merge_tail(unsigned long long *buf, int n2, int size, int s
   for (int base = wid * 64; base < n2; base += kWarps * 64) {
     unsigned long long e0 = buf[base + lane], e1 = buf[base + lane + 32];
     const int i0 = base + lane, i1 = i0 + 32;
+#pragma unroll 1
     for (int sz = (size > 0 ? size : 2); sz <= (size > 0 ? size : 64); sz <<= 1) {
+#pragma unroll 1
       for (int st = (size > 0 ? st_hi : sz >> 1); st > 0; st >>= 1) {
         if (st == 32) {
           const bool desc = (i0 & sz) == 0;  // i0 is the low side of (i0, i1)
@@ -364,6 +371,103 @@ __device__ void sort_desc(unsigned long long *buf, int n2) {
   }
 }
 
+// Trunk: K layers over the n_pos position rows (beam.py:159-163), run by
+// warp 0 alone and reassociated so the trunk layers' K/V are never built:
+// scores (q Wk^T) X^T, output (P X) Wv.  Xs is X^T with row stride xld.
+template <int D>
+__device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S, float *TR,
+                            float *TQ, float *wsl) {
+  constexpr int E = D / 8;
+  const int lane = threadIdx.x & 31, rl = lane >> 3, cb = (lane & 7) * E;
+  const gr4ad_weights &W = a.w;
+  const int L = a.L, K = a.K, dff = a.dff, np = a.n_pos;
+  const float scale = 1.0f / sqrtf((float)D);
+  float *slot0 = wsl, *slot1 = wsl + 4 * D, *slot2 = wsl + 8 * D, *slot3 = wsl + 12 * D;
+  for (int e = lane; e < np * D; e += 32) TR[e] = __ldg(W.pos + e);
+  __syncwarp();
+  const int ldw = 2 * L * D;
+  for (int i = 0; i < K; ++i) {
+    const gr4ad_layer &Lw = W.layer[i];
+    const float *Wk = W.cross_kv_W + (size_t)(2 * i) * D, *Wv = Wk + D;
+    for (int p0 = 0; p0 < np; p0 += RW) {
+      const int p = p0 + rl, pp = min(p, np - 1);
+      const bool ok = p < np;
+      float h[E], n[E], t[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) h[e] = TR[pp * D + cb + e];
+      layer_norm<E>(h, Lw.ln1_g, Lw.ln1_b, n);
+      publish<E>(n, slot0);
+      proj<E>(slot0, D, Lw.cross_Wq, D, t);
+      publish<E>(t, slot1);
+      proj_t<E>(slot1, D, Wk, ldw, t);  // u = q Wk^T, u . x_s == q . k_s
+      publish<E>(t, slot0);
+      cross_attn<D>(slot0, Xs, Xs, S, xld, slot2, t);  // t = P X
+      publish<E>(t, slot1);
+      proj<E>(slot1, D, Wv, ldw, t);  // (P X) Wv == P V
+      publish<E>(t, slot0);
+      proj<E>(slot0, D, Lw.cross_Wo, D, t);
+#pragma unroll
+      for (int e = 0; e < E; ++e) h[e] += t[e];
+      layer_norm<E>(h, Lw.ln2_g, Lw.ln2_b, n);
+      publish<E>(n, slot0);
+      for (int c = 0; c < 3; ++c) {
+        proj<E>(slot0, D, Lw.self_Wqkv + c * D, 3 * D, t);
+        if (ok)
+#pragma unroll
+          for (int e = 0; e < E; ++e) TQ[(p * 3 + c) * D + cb + e] = t[e];
+      }
+      if (ok)
+#pragma unroll
+        for (int e = 0; e < E; ++e) TR[p * D + cb + e] = h[e];
+    }
+    __syncwarp();
+    for (int p0 = 0; p0 < np; p0 += RW) {
+      const int p = p0 + rl, pp = min(p, np - 1);
+      const bool ok = p < np;
+      const int rmax_w = min(p0 + RW, np) - 1;  // warp-uniform loop bound
+      float h[E], n[E], t[E], q[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        h[e] = TR[pp * D + cb + e];
+        q[e] = TQ[(pp * 3) * D + cb + e];
+      }
+      // causal self-attention over positions 0..p (layers.py:94-100), online
+      float mx = -INFINITY, se = 0.f, so[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) so[e] = 0.f;
+      for (int r = 0; r <= rmax_w; ++r) {
+        float dot = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) dot = fmaf(q[e], TQ[(r * 3 + 1) * D + cb + e], dot);
+        const float sc = rsum(dot) * scale;
+        if (r <= pp) {
+          const float nm = fmaxf(mx, sc), f = expf(mx - nm), w = expf(sc - nm);
+          se = se * f + w;
+#pragma unroll
+          for (int e = 0; e < E; ++e) so[e] = so[e] * f + w * TQ[(r * 3 + 2) * D + cb + e];
+          mx = nm;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) so[e] /= se;
+      publish<E>(so, slot0);
+      proj<E>(slot0, D, Lw.self_Wo, D, t);
+#pragma unroll
+      for (int e = 0; e < E; ++e) h[e] += t[e];
+      layer_norm<E>(h, Lw.ln3_g, Lw.ln3_b, n);
+      publish<E>(n, slot0);
+      ffn<D>(slot0, slot3, Lw, dff, t);
+#pragma unroll
+      for (int e = 0; e < E; ++e) h[e] += t[e] + __ldg(Lw.ffn_b2 + cb + e);
+      __syncwarp();
+      if (ok)
+#pragma unroll
+        for (int e = 0; e < E; ++e) TR[p * D + cb + e] = h[e];
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 #ifdef GR_FUSED_TIMING
@@ -375,9 +479,225 @@ __device__ void sort_desc(unsigned long long *buf, int n2) {
       a.dbg[blockIdx.x * 16 + (i)] = _t;                                        \
     }                                                                           \
   } while (0)
+#define GR_SUB(i)                                                               \
+  do {                                                                          \
+    if (t == 0 && threadIdx.x == 0) {                                           \
+      long long _t;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                   \
+      a.dbg[blockIdx.x * 16 + 10 + (i)] = _t;                                   \
+    }                                                                           \
+  } while (0)
 #else
 #define GR_STAMP(i) do {} while (0)
+#define GR_SUB(i) do {} while (0)
 #endif
+
+
+// Beam selection of level t over the `live` rows' keys (or, at t == T, the
+// value re-rank output) and in-place compaction; returns the next level's
+// live rows (-1 once the re-rank output is written).  Shared by both fused
+// kernels (beam.py:30-89, 202-210, 258-288).
+__device__ int select_level(const FusedArgs &a, int b, int t, int live, int V,
+                            const uint32_t *keys, unsigned *hist, unsigned *scr,
+                            unsigned long long *sbuf, int *par, int *tokm, float *cum, float Rs,
+                            float bscale) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int T = a.T;
+  auto sbin = [&](float sc) -> unsigned {
+    return (unsigned)fminf((Rs - sc) * bscale, 2047.0f);  // NaN-free: sc <= Rs
+  };
+  if (t == T) {  // re-rank output: sort rows by (rank desc, row asc)
+    double *key = reinterpret_cast<double *>(sbuf);
+    int *idx = reinterpret_cast<int *>(hist);
+    int n2 = 1;
+    while (n2 < live) n2 <<= 1;
+    for (int j = tid; j < n2; j += kThreads) {
+      idx[j] = j < live ? j : 0x7fffffff;
+      if (j >= live) key[j] = -INFINITY;
+    }
+    __syncthreads();
+    for (int size = 2; size <= n2; size <<= 1)
+      for (int st = size >> 1; st > 0; st >>= 1) {
+        for (int i = tid; i < n2 / 2; i += kThreads) {
+          int lo = 2 * i - (i & (st - 1)), hi = lo + st;
+          bool desc = (lo & size) == 0;
+          double kx = key[lo], ky = key[hi];
+          int ix = idx[lo], iy = idx[hi];
+          bool xb = (kx > ky) || (kx == ky && ix < iy);
+          if (xb != desc) {
+            key[lo] = ky; key[hi] = kx;
+            idx[lo] = iy; idx[hi] = ix;
+          }
+        }
+        __syncthreads();
+      }
+    for (int j = tid; j < live; j += kThreads) {
+      int ar = idx[j];
+      for (int tau = T - 1; tau >= 0; --tau) {
+        a.out_tokens[((size_t)b * a.max_out + j) * T + tau] = tokm[a.moff[tau + 1] + ar];
+        ar = par[a.moff[tau + 1] + ar];
+      }
+      a.out_score[(size_t)b * a.max_out + j] = key[j];
+    }
+    if (tid == 0) a.out_count[b] = live;
+    GR_STAMP(15);
+    return -1;
+  }
+
+  // ---- exact top-k under (-score, row, token) (beam.py:30-89) --------------
+  const int n_cand = live * V;
+  const int k = min(a.eff[t * a.B + b], n_cand);
+  int n_sort = k;  // entries in sbuf to sort (>= k)
+  {
+    // (a) window: every key in a bin below the k-th key's bin is in the
+    // top-k; the k-th bin is collected whole and the exact sort breaks it
+    unsigned cnt_le = 0;
+    int wb = 2047;
+    {
+      // k-th smallest bin index == (2048 - 1 - bin of the k-th largest in
+      // reversed order): find_bin scans from the top bin, so mirror
+      unsigned above;
+      for (int i = tid; i < 1024; i += kThreads) {
+        unsigned x = hist[i], y = hist[2047 - i];
+        hist[i] = y;
+        hist[2047 - i] = x;
+      }
+      __syncthreads();
+      int rb = find_bin(hist, 2048, (unsigned)k, &above, scr);  // mirrored bin
+      wb = 2047 - rb;
+      cnt_le = above + hist[rb];
+    }
+    const bool window_ok = wb < 2047 && cnt_le <= (unsigned)a.sort_cap;
+#ifdef GR_FUSED_TIMING_WINDOW
+    if (tid == 0 && t < 3) {
+      a.dbg[blockIdx.x * 16 + 10 + t] = ((long long)cnt_le << 32) | (unsigned)wb;
+      a.dbg[blockIdx.x * 16 + 13 + (t == 2)] = (long long)(bscale * 1000);
+    }
+#endif
+    if (window_ok) {
+      if (tid == 0) scr[40] = 0;
+      __syncthreads();
+      const uint4 *keys4 = reinterpret_cast<const uint4 *>(keys);
+      const int n4 = n_cand / 4;
+      // 8 independent L2 loads in flight per thread, then filter
+      constexpr int U = 8;
+      for (int i0 = tid; i0 < n4; i0 += U * kThreads) {
+        uint4 u4[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int i4 = i0 + j * kThreads;
+          u4[j] = i4 < n4 ? keys4[i4] : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int i4 = i0 + j * kThreads;
+          const uint32_t us[4] = {u4[j].x, u4[j].y, u4[j].z, u4[j].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (i4 < n4 && sbin(ord2f(us[q])) <= (unsigned)wb) {
+              unsigned pos = atomicAdd(&scr[40], 1u);
+              sbuf[pos] = ((unsigned long long)us[q] << 32) | (0xFFFFFFFFu - (unsigned)(i4 * 4 + q));
+            }
+          }
+        }
+      }
+      n_sort = (int)cnt_le;
+    } else {
+      // (b) exact radix fallback (11/11/10-bit passes over the keys)
+      unsigned need = (unsigned)k, above;
+      for (int i = tid; i < 2048; i += kThreads) hist[i] = 0u;
+      __syncthreads();
+      uint32_t T32 = 0, pmask = 0;
+      unsigned eq_total = 0;
+      const uint4 *keys4 = reinterpret_cast<const uint4 *>(keys);
+      const int n4 = n_cand / 4;
+      for (int pass = 0; pass < 3; ++pass) {
+        const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
+        const int nb = pass == 2 ? 1024 : 2048;
+        __syncthreads();
+        for (int i = tid; i < nb; i += kThreads) hist[i] = 0u;
+        __syncthreads();
+        int cur = -1;
+        unsigned cnt = 0;
+        for (int i4 = tid; i4 < n4; i4 += kThreads) {
+          const uint4 u4 = keys4[i4];
+          const uint32_t us[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if ((us[q] & pmask) == T32) hist_add(hist, cur, cnt, (int)((us[q] >> shift) & (nb - 1)));
+        }
+        if (cnt) atomicAdd(&hist[cur], cnt);
+        __syncthreads();
+        int bin = find_bin(hist, nb, need, &above, scr);
+        eq_total = hist[bin];
+        need -= above;
+        T32 |= (uint32_t)bin << shift;
+        pmask |= (uint32_t)(nb - 1) << shift;
+      }
+      const unsigned n_gt = (unsigned)k - need;
+      if (tid == 0) scr[40] = 0;
+      __syncthreads();
+      if (need == eq_total) {
+        for (int i0 = wid * 32; i0 < n_cand; i0 += kThreads) {
+          int i = i0 + lane;
+          uint32_t u = i < n_cand ? keys[i] : 0u;
+          bool take = i < n_cand && u >= T32;
+          unsigned m = __ballot_sync(kFull, take);
+          unsigned base = 0;
+          if (m && lane == 0) base = atomicAdd(&scr[40], __popc(m));
+          base = __shfl_sync(kFull, base, 0);
+          if (take) sbuf[base + __popc(m & ((1u << lane) - 1u))] =
+              ((unsigned long long)u << 32) | (0xFFFFFFFFu - (unsigned)i);
+        }
+      } else {
+        // ordered ties: contiguous index chunks per warp, warp tie counts scanned
+        const int chunk = ((n_cand + kWarps - 1) / kWarps + 31) / 32 * 32;
+        const int c0 = wid * chunk, c1 = min(n_cand, c0 + chunk);
+        unsigned neq = 0;
+        for (int i0 = c0; i0 < c1; i0 += 32) {
+          int i = i0 + lane;
+          neq += __popc(__ballot_sync(kFull, i < c1 && keys[i] == T32));
+        }
+        if (lane == 0) scr[8 + wid] = neq;
+        __syncthreads();
+        unsigned rank = 0;
+        for (int w2 = 0; w2 < wid; ++w2) rank += scr[8 + w2];
+        for (int i0 = c0; i0 < c1; i0 += 32) {
+          int i = i0 + lane;
+          uint32_t u = i < c1 ? keys[i] : 0u;
+          bool gt = i < c1 && u > T32;
+          bool eq = i < c1 && u == T32;
+          unsigned me = __ballot_sync(kFull, eq);
+          unsigned myr = rank + __popc(me & ((1u << lane) - 1u));
+          unsigned mg = __ballot_sync(kFull, gt);
+          unsigned base = 0;
+          if (mg && lane == 0) base = atomicAdd(&scr[40], __popc(mg));
+          base = __shfl_sync(kFull, base, 0);
+          unsigned long long e = ((unsigned long long)u << 32) | (0xFFFFFFFFu - (unsigned)i);
+          if (gt) sbuf[base + __popc(mg & ((1u << lane) - 1u))] = e;
+          if (eq && myr < need) sbuf[n_gt + myr] = e;
+          rank += __popc(me);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  int n2 = 64;
+  while (n2 < n_sort) n2 <<= 1;
+  for (int i = n_sort + tid; i < n2; i += kThreads) sbuf[i] = 0ull;
+  __syncthreads();
+  sort_desc(sbuf, n2);
+  // compaction: next-level rows in selection order (beam.py:202-210)
+  const int mo1 = a.moff[t + 1];
+  for (int j = tid; j < k; j += kThreads) {
+    unsigned long long e = sbuf[j];
+    unsigned fi = 0xFFFFFFFFu - (unsigned)(e & 0xFFFFFFFFull);
+    par[mo1 + j] = (int)(fi / (unsigned)V);
+    tokm[mo1 + j] = (int)(fi % (unsigned)V);
+    cum[mo1 + j] = ord2f((uint32_t)(e >> 32));
+  }
+  return k;
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
@@ -477,95 +797,12 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
     }
   };
 
-  const int np = a.n_pos;
   // ---- trunk: K layers over the n_pos position rows (beam.py:159-163) -------
   // Warp 0 alone (n_pos <= 9 rows), reassociated so the trunk layers' K/V are
   // never built: scores (q Wk^T) X^T, output (P X) Wv.  Warps 1-7 build the
   // head layers' K/V meanwhile.
   if (K > 0 && wid == 0) {
-    for (int e = lane; e < np * D; e += 32) TR[e] = __ldg(W.pos + e);
-    __syncwarp();
-    const int ldw = 2 * L * D;
-    for (int i = 0; i < K; ++i) {
-      const gr4ad_layer &Lw = W.layer[i];
-      const float *Wk = W.cross_kv_W + (size_t)(2 * i) * D, *Wv = Wk + D;
-      for (int p0 = 0; p0 < np; p0 += RW) {
-        const int p = p0 + rl, pp = min(p, np - 1);
-        const bool ok = p < np;
-        float h[E], n[E], t[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) h[e] = TR[pp * D + cb + e];
-        layer_norm<E>(h, Lw.ln1_g, Lw.ln1_b, n);
-        publish<E>(n, slot0);
-        proj<E>(slot0, D, Lw.cross_Wq, D, t);
-        publish<E>(t, slot1);
-        proj_t<E>(slot1, D, Wk, ldw, t);  // u = q Wk^T, u . x_s == q . k_s
-        publish<E>(t, slot0);
-        cross_attn<D>(slot0, Xs, Xs, S, slot2, t);  // t = P X
-        publish<E>(t, slot1);
-        proj<E>(slot1, D, Wv, ldw, t);  // (P X) Wv == P V
-        publish<E>(t, slot0);
-        proj<E>(slot0, D, Lw.cross_Wo, D, t);
-#pragma unroll
-        for (int e = 0; e < E; ++e) h[e] += t[e];
-        layer_norm<E>(h, Lw.ln2_g, Lw.ln2_b, n);
-        publish<E>(n, slot0);
-        for (int c = 0; c < 3; ++c) {
-          proj<E>(slot0, D, Lw.self_Wqkv + c * D, 3 * D, t);
-          if (ok)
-#pragma unroll
-            for (int e = 0; e < E; ++e) TQ[(p * 3 + c) * D + cb + e] = t[e];
-        }
-        if (ok)
-#pragma unroll
-          for (int e = 0; e < E; ++e) TR[p * D + cb + e] = h[e];
-      }
-      __syncwarp();
-      for (int p0 = 0; p0 < np; p0 += RW) {
-        const int p = p0 + rl, pp = min(p, np - 1);
-        const bool ok = p < np;
-        const int rmax_w = min(p0 + RW, np) - 1;  // warp-uniform loop bound
-        float h[E], n[E], t[E], q[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          h[e] = TR[pp * D + cb + e];
-          q[e] = TQ[(pp * 3) * D + cb + e];
-        }
-        // causal self-attention over positions 0..p (layers.py:94-100), online
-        float mx = -INFINITY, se = 0.f, so[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) so[e] = 0.f;
-        for (int r = 0; r <= rmax_w; ++r) {
-          float dot = 0.f;
-#pragma unroll
-          for (int e = 0; e < E; ++e) dot = fmaf(q[e], TQ[(r * 3 + 1) * D + cb + e], dot);
-          const float sc = rsum(dot) * scale;
-          if (r <= pp) {
-            const float nm = fmaxf(mx, sc), f = expf(mx - nm), w = expf(sc - nm);
-            se = se * f + w;
-#pragma unroll
-            for (int e = 0; e < E; ++e) so[e] = so[e] * f + w * TQ[(r * 3 + 2) * D + cb + e];
-            mx = nm;
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < E; ++e) so[e] /= se;
-        publish<E>(so, slot0);
-        proj<E>(slot0, D, Lw.self_Wo, D, t);
-#pragma unroll
-        for (int e = 0; e < E; ++e) h[e] += t[e];
-        layer_norm<E>(h, Lw.ln3_g, Lw.ln3_b, n);
-        publish<E>(n, slot0);
-        ffn<D>(slot0, slot3, Lw, dff, t);
-#pragma unroll
-        for (int e = 0; e < E; ++e) h[e] += t[e] + __ldg(Lw.ffn_b2 + cb + e);
-        __syncwarp();
-        if (ok)
-#pragma unroll
-          for (int e = 0; e < E; ++e) TR[p * D + cb + e] = h[e];
-      }
-      __syncwarp();
-    }
+    trunk_warp0<D>(a, Xs, SP, S, TR, TQ, wsl);
   } else {
     // head-layer K/V, built once and shared by every beam (beam.py:165-169)
     const int t0 = K > 0 ? 32 : 0;
@@ -639,7 +876,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
         publish<E>(n, slot0);
         proj<E>(slot0, D, Lw.cross_Wq, D, tt);
         publish<E>(tt, slot1);
-        cross_attn<D>(slot1, Kt, Kt + KVS, S, slot2, tt);
+        cross_attn<D>(slot1, Kt, Kt + KVS, S, SP, slot2, tt);
         publish<E>(tt, slot0);
         proj<E>(slot0, D, Lw.cross_Wo, D, tt);
 #pragma unroll
@@ -770,197 +1007,8 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
     __syncthreads();
     GR_STAMP(4 + 2 * t);
 
-    if (t == T) {  // re-rank output: sort rows by (rank desc, row asc)
-      double *key = reinterpret_cast<double *>(sbuf);
-      int *idx = reinterpret_cast<int *>(hist);
-      int n2 = 1;
-      while (n2 < live) n2 <<= 1;
-      for (int j = tid; j < n2; j += kThreads) {
-        idx[j] = j < live ? j : 0x7fffffff;
-        if (j >= live) key[j] = -INFINITY;
-      }
-      __syncthreads();
-      for (int size = 2; size <= n2; size <<= 1)
-        for (int st = size >> 1; st > 0; st >>= 1) {
-          for (int i = tid; i < n2 / 2; i += kThreads) {
-            int lo = 2 * i - (i & (st - 1)), hi = lo + st;
-            bool desc = (lo & size) == 0;
-            double kx = key[lo], ky = key[hi];
-            int ix = idx[lo], iy = idx[hi];
-            bool xb = (kx > ky) || (kx == ky && ix < iy);
-            if (xb != desc) {
-              key[lo] = ky; key[hi] = kx;
-              idx[lo] = iy; idx[hi] = ix;
-            }
-          }
-          __syncthreads();
-        }
-      for (int j = tid; j < live; j += kThreads) {
-        int ar = idx[j];
-        for (int tau = T - 1; tau >= 0; --tau) {
-          a.out_tokens[((size_t)b * a.max_out + j) * T + tau] = tokm[a.moff[tau + 1] + ar];
-          ar = par[a.moff[tau + 1] + ar];
-        }
-        a.out_score[(size_t)b * a.max_out + j] = key[j];
-      }
-      if (tid == 0) a.out_count[b] = live;
-      GR_STAMP(15);
-      return;
-    }
-
-    // ---- exact top-k under (-score, row, token) (beam.py:30-89) --------------
-    const int n_cand = live * V;
-    const int k = min(a.eff[t * a.B + b], n_cand);
-    int n_sort = k;  // entries in sbuf to sort (>= k)
-    {
-      // (a) window: every key in a bin below the k-th key's bin is in the
-      // top-k; the k-th bin is collected whole and the exact sort breaks it
-      unsigned cnt_le = 0;
-      int wb = 2047;
-      {
-        // k-th smallest bin index == (2048 - 1 - bin of the k-th largest in
-        // reversed order): find_bin scans from the top bin, so mirror
-        unsigned above;
-        for (int i = tid; i < 1024; i += kThreads) {
-          unsigned x = hist[i], y = hist[2047 - i];
-          hist[i] = y;
-          hist[2047 - i] = x;
-        }
-        __syncthreads();
-        int rb = find_bin(hist, 2048, (unsigned)k, &above, scr);  // mirrored bin
-        wb = 2047 - rb;
-        cnt_le = above + hist[rb];
-      }
-      const bool window_ok = wb < 2047 && cnt_le <= (unsigned)a.sort_cap;
-#ifdef GR_FUSED_TIMING
-      if (tid == 0 && t < 3) {
-        a.dbg[blockIdx.x * 16 + 10 + t] = ((long long)cnt_le << 32) | (unsigned)wb;
-        a.dbg[blockIdx.x * 16 + 13 + (t == 2)] = (long long)(bscale * 1000);
-      }
-#endif
-      if (window_ok) {
-        if (tid == 0) scr[40] = 0;
-        __syncthreads();
-        const uint4 *keys4 = reinterpret_cast<const uint4 *>(keys);
-        const int n4 = n_cand / 4;
-        // 8 independent L2 loads in flight per thread, then filter
-        constexpr int U = 8;
-        for (int i0 = tid; i0 < n4; i0 += U * kThreads) {
-          uint4 u4[U];
-#pragma unroll
-          for (int j = 0; j < U; ++j) {
-            const int i4 = i0 + j * kThreads;
-            u4[j] = i4 < n4 ? keys4[i4] : make_uint4(0u, 0u, 0u, 0u);
-          }
-#pragma unroll
-          for (int j = 0; j < U; ++j) {
-            const int i4 = i0 + j * kThreads;
-            const uint32_t us[4] = {u4[j].x, u4[j].y, u4[j].z, u4[j].w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (i4 < n4 && sbin(ord2f(us[q])) <= (unsigned)wb) {
-                unsigned pos = atomicAdd(&scr[40], 1u);
-                sbuf[pos] = ((unsigned long long)us[q] << 32) | (0xFFFFFFFFu - (unsigned)(i4 * 4 + q));
-              }
-            }
-          }
-        }
-        n_sort = (int)cnt_le;
-      } else {
-        // (b) exact radix fallback (11/11/10-bit passes over the keys)
-        unsigned need = (unsigned)k, above;
-        for (int i = tid; i < 2048; i += kThreads) hist[i] = 0u;
-        __syncthreads();
-        uint32_t T32 = 0, pmask = 0;
-        unsigned eq_total = 0;
-        const uint4 *keys4 = reinterpret_cast<const uint4 *>(keys);
-        const int n4 = n_cand / 4;
-        for (int pass = 0; pass < 3; ++pass) {
-          const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
-          const int nb = pass == 2 ? 1024 : 2048;
-          __syncthreads();
-          for (int i = tid; i < nb; i += kThreads) hist[i] = 0u;
-          __syncthreads();
-          int cur = -1;
-          unsigned cnt = 0;
-          for (int i4 = tid; i4 < n4; i4 += kThreads) {
-            const uint4 u4 = keys4[i4];
-            const uint32_t us[4] = {u4.x, u4.y, u4.z, u4.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if ((us[q] & pmask) == T32) hist_add(hist, cur, cnt, (int)((us[q] >> shift) & (nb - 1)));
-          }
-          if (cnt) atomicAdd(&hist[cur], cnt);
-          __syncthreads();
-          int bin = find_bin(hist, nb, need, &above, scr);
-          eq_total = hist[bin];
-          need -= above;
-          T32 |= (uint32_t)bin << shift;
-          pmask |= (uint32_t)(nb - 1) << shift;
-        }
-        const unsigned n_gt = (unsigned)k - need;
-        if (tid == 0) scr[40] = 0;
-        __syncthreads();
-        if (need == eq_total) {
-          for (int i0 = wid * 32; i0 < n_cand; i0 += kThreads) {
-            int i = i0 + lane;
-            uint32_t u = i < n_cand ? keys[i] : 0u;
-            bool take = i < n_cand && u >= T32;
-            unsigned m = __ballot_sync(kFull, take);
-            unsigned base = 0;
-            if (m && lane == 0) base = atomicAdd(&scr[40], __popc(m));
-            base = __shfl_sync(kFull, base, 0);
-            if (take) sbuf[base + __popc(m & ((1u << lane) - 1u))] =
-                ((unsigned long long)u << 32) | (0xFFFFFFFFu - (unsigned)i);
-          }
-        } else {
-          // ordered ties: contiguous index chunks per warp, warp tie counts scanned
-          const int chunk = ((n_cand + kWarps - 1) / kWarps + 31) / 32 * 32;
-          const int c0 = wid * chunk, c1 = min(n_cand, c0 + chunk);
-          unsigned neq = 0;
-          for (int i0 = c0; i0 < c1; i0 += 32) {
-            int i = i0 + lane;
-            neq += __popc(__ballot_sync(kFull, i < c1 && keys[i] == T32));
-          }
-          if (lane == 0) scr[8 + wid] = neq;
-          __syncthreads();
-          unsigned rank = 0;
-          for (int w2 = 0; w2 < wid; ++w2) rank += scr[8 + w2];
-          for (int i0 = c0; i0 < c1; i0 += 32) {
-            int i = i0 + lane;
-            uint32_t u = i < c1 ? keys[i] : 0u;
-            bool gt = i < c1 && u > T32;
-            bool eq = i < c1 && u == T32;
-            unsigned me = __ballot_sync(kFull, eq);
-            unsigned myr = rank + __popc(me & ((1u << lane) - 1u));
-            unsigned mg = __ballot_sync(kFull, gt);
-            unsigned base = 0;
-            if (mg && lane == 0) base = atomicAdd(&scr[40], __popc(mg));
-            base = __shfl_sync(kFull, base, 0);
-            unsigned long long e = ((unsigned long long)u << 32) | (0xFFFFFFFFu - (unsigned)i);
-            if (gt) sbuf[base + __popc(mg & ((1u << lane) - 1u))] = e;
-            if (eq && myr < need) sbuf[n_gt + myr] = e;
-            rank += __popc(me);
-          }
-        }
-      }
-    }
-    __syncthreads();
-    int n2 = 64;
-    while (n2 < n_sort) n2 <<= 1;
-    for (int i = n_sort + tid; i < n2; i += kThreads) sbuf[i] = 0ull;
-    __syncthreads();
-    sort_desc(sbuf, n2);
-    // compaction: next-level rows in selection order (beam.py:202-210)
-    const int mo1 = a.moff[t + 1];
-    for (int j = tid; j < k; j += kThreads) {
-      unsigned long long e = sbuf[j];
-      unsigned fi = 0xFFFFFFFFu - (unsigned)(e & 0xFFFFFFFFull);
-      par[mo1 + j] = (int)(fi / (unsigned)V);
-      tokm[mo1 + j] = (int)(fi % (unsigned)V);
-      cum[mo1 + j] = ord2f((uint32_t)(e >> 32));
-    }
-    live = k;
+    live = select_level(a, b, t, live, V, keys, hist, scr, sbuf, par, tokm, cum, Rs, bscale);
+    if (live < 0) return;
     __syncthreads();
     GR_STAMP(5 + 2 * t);
   }
@@ -975,6 +1023,807 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
   }
   if (tid == 0) a.out_count[b] = live;
   GR_STAMP(15);
+}
+
+// ===========================================================================
+// Warp-MMA variant (d = 16): every per-level product -- fused gate, head-layer
+// projections, cross-attention Q.K^T and P.V, FFN, codebook logits -- runs on
+// the tensor cores through mma.sync.m16n8k8 in 3xTF32 (hi.lo + lo.hi + hi.hi,
+// fp32 accumulate), with a warp owning a 16-row tile.  The per-row state
+// stays in C fragments: under the k-permutation (k = t <-> column 2t,
+// k = t + 4 <-> column 2t + 1, B rows permuted alike) a C fragment is
+// directly the A fragment of the next product, so no shuffles or shared-
+// memory round trips between products.  Cross-attention is flash-style
+// (online softmax over 64-key chunks) over K [S][D+8] and V^T [D][S+8] in
+// shared memory (padded strides: conflict-free LDS.64 fragment loads).
+// Trunk, selection and compaction are the CUDA-core code above.
+// ===========================================================================
+// pull [p, p + bytes) toward this SM's L1 (128-B lines split over the CTA)
+static __device__ __forceinline__ void prefetch_l1(const void *p, size_t bytes) {
+  const char *c = static_cast<const char *>(p);
+  for (size_t o = (size_t)threadIdx.x * 128; o < bytes; o += (size_t)kThreads * 128)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(c + o));
+}
+
+static __device__ __forceinline__ uint32_t tf32_hi(float x) {
+  return __float_as_uint(x) & 0xFFFFE000u;
+}
+
+// C fragment (c0 (g,2t) c1 (g,2t+1) c2 (g+8,2t) c3 (g+8,2t+1)) -> A fragment
+// (a0 (g,k=t) a1 (g+8,t) a2 (g,t+4) a3 (g+8,t+4)) split into tf32 hi / lo
+static __device__ __forceinline__ void split_a(const float (&c)[4], uint32_t (&h)[4],
+                                               uint32_t (&l)[4]) {
+  const float v[4] = {c[0], c[2], c[1], c[3]};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    h[q] = tf32_hi(v[q]);
+    l[q] = __float_as_uint(v[q] - __uint_as_float(h[q]));
+  }
+}
+
+static __device__ __forceinline__ float4 split_b(float2 v) {
+  const float h0 = __uint_as_float(tf32_hi(v.x)), h1 = __uint_as_float(tf32_hi(v.y));
+  return make_float4(h0, h1, v.x - h0, v.y - h1);
+}
+
+static __device__ __forceinline__ void mma8(float (&d)[4], const uint32_t (&a)[4], float b0,
+                                            float b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(__float_as_uint(b0)),
+        "r"(__float_as_uint(b1)));
+}
+
+// d += a . b in 3xTF32; b = {hi0, hi1, lo0, lo1}
+static __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4],
+                                            const uint32_t (&al)[4], float4 b) {
+  mma8(d, al, b.x, b.y);
+  mma8(d, ah, b.z, b.w);
+  mma8(d, ah, b.x, b.y);
+}
+
+// dm += ah.bh, dx += al.bh + ah.bl: two independent accumulator chains
+static __device__ __forceinline__ void mma3s(float (&dm)[4], float (&dx)[4],
+                                             const uint32_t (&ah)[4], const uint32_t (&al)[4],
+                                             float4 b) {
+  mma8(dx, al, b.x, b.y);
+  mma8(dx, ah, b.z, b.w);
+  mma8(dm, ah, b.x, b.y);
+}
+
+static __device__ __forceinline__ float quad_sum(float v) {
+  v += __shfl_xor_sync(kFull, v, 1);
+  v += __shfl_xor_sync(kFull, v, 2);
+  return v;
+}
+static __device__ __forceinline__ float quad_max(float v) {
+  v = fmaxf(v, __shfl_xor_sync(kFull, v, 1));
+  v = fmaxf(v, __shfl_xor_sync(kFull, v, 2));
+  return v;
+}
+static __device__ __forceinline__ double quad_sum_d(double v) {
+  v += __shfl_xor_sync(kFull, v, 1);
+  v += __shfl_xor_sync(kFull, v, 2);
+  return v;
+}
+
+// y (16 x 8NT) (+)= x (16 x 8KT) . W, W fragment-ordered
+template <int KT, int NT, bool ACC = false>
+static __device__ __forceinline__ void mm(const float (&x)[KT][4], const float4 *__restrict__ W,
+                                          float (&y)[NT][4]) {
+  uint32_t h[KT][4], l[KT][4];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) split_a(x[k], h[k], l[k]);
+  const int lane = threadIdx.x & 31;
+  float4 w[KT][NT];
+#pragma unroll
+  for (int k = 0; k < KT; ++k)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) w[k][n] = __ldg(W + (k * NT + n) * 32 + lane);
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    float cx[4] = {0.f, 0.f, 0.f, 0.f};
+    if (!ACC) y[n][0] = y[n][1] = y[n][2] = y[n][3] = 0.f;
+#pragma unroll
+    for (int k = 0; k < KT; ++k) mma3s(y[n], cx, h[k], l[k], w[k][n]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) y[n][c] += cx[c];
+  }
+}
+
+// LayerNorm of the tile's rows (layers.py:38-51); row g in c0/c1, g + 8 in c2/c3
+template <int NT>
+static __device__ __forceinline__ void ln_frag(const float (&x)[NT][4], const float *g,
+                                               const float *b, float (&y)[NT][4]) {
+  const int t = threadIdx.x & 3;
+  float sA = 0.f, sB = 0.f;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    sA += x[n][0] + x[n][1];
+    sB += x[n][2] + x[n][3];
+  }
+  const float mA = quad_sum(sA) / (float)(8 * NT), mB = quad_sum(sB) / (float)(8 * NT);
+  float vA = 0.f, vB = 0.f;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const float d0 = x[n][0] - mA, d1 = x[n][1] - mA, d2 = x[n][2] - mB, d3 = x[n][3] - mB;
+    vA += d0 * d0 + d1 * d1;
+    vB += d2 * d2 + d3 * d3;
+  }
+  const float iA = 1.0f / sqrtf(quad_sum(vA) / (float)(8 * NT) + 1e-5f);
+  const float iB = 1.0f / sqrtf(quad_sum(vB) / (float)(8 * NT) + 1e-5f);
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const float2 gg = __ldg(reinterpret_cast<const float2 *>(g + 8 * n + 2 * t));
+    const float2 bb = __ldg(reinterpret_cast<const float2 *>(b + 8 * n + 2 * t));
+    y[n][0] = (x[n][0] - mA) * iA * gg.x + bb.x;
+    y[n][1] = (x[n][1] - mA) * iA * gg.y + bb.y;
+    y[n][2] = (x[n][2] - mB) * iB * gg.x + bb.x;
+    y[n][3] = (x[n][3] - mB) * iB * gg.y + bb.y;
+  }
+}
+
+// k_lo must be a multiple of 64 (chunks never cross SP; keys in [kend, c0+64)
+// are masked, their K rows zero or finite).
+// Cross-attention of the tile's 16 query rows against one request's shared
+// K [SP][D+8] / V^T [D][SP+8]: online softmax over 64-key chunks
+// (autodiff.py:362-368 up to the rescaling order).
+template <int D>
+static __device__ __forceinline__ void attn_mma(const float (&q)[D / 8][4], const float *Ks,
+                                                const float *VTs, int S, int k_lo, int k_hi,
+                                                float (&o)[D / 8][4], float (&ml)[4]) {
+  constexpr int KT = D / 8, VS = SP + 8;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const float scale = 1.0f / sqrtf((float)D);
+  uint32_t qh[KT][4], ql[KT][4];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) split_a(q[k], qh[k], ql[k]);
+  float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
+  // P.V accumulators: hi.hi terms and cross terms
+  float ox[KT][4];
+#pragma unroll
+  for (int n = 0; n < KT; ++n)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[n][c] = ox[n][c] = 0.f;
+  const int kend = min(S, k_hi);
+  for (int c0 = k_lo; c0 < kend; c0 += 64) {
+    float sc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+      const float *kr = Ks + (c0 + j * 8 + g) * D;
+      const int sw = ((g >> 1) & 1) << 3;  // k_swz: row bit 1 flips the 8-column half
+#pragma unroll
+      for (int k = 0; k < KT; ++k)
+        mma3(sc[j], qh[k], ql[k],
+             split_b(*reinterpret_cast<const float2 *>(kr + ((8 * k + 2 * t) ^ sw))));
+    }
+    float cA = -INFINITY, cB = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int key = c0 + j * 8 + 2 * t;
+      const bool v0 = key < kend, v1 = key + 1 < kend;
+      sc[j][0] = v0 ? sc[j][0] * scale : -INFINITY;
+      sc[j][1] = v1 ? sc[j][1] * scale : -INFINITY;
+      sc[j][2] = v0 ? sc[j][2] * scale : -INFINITY;
+      sc[j][3] = v1 ? sc[j][3] * scale : -INFINITY;
+      cA = fmaxf(cA, fmaxf(sc[j][0], sc[j][1]));
+      cB = fmaxf(cB, fmaxf(sc[j][2], sc[j][3]));
+    }
+    const float nA = fmaxf(mA, quad_max(cA)), nB = fmaxf(mB, quad_max(cB));
+    const float fA = __expf(mA - nA), fB = __expf(mB - nB);  // 0 on the first chunk
+    lA *= fA;
+    lB *= fB;
+#pragma unroll
+    for (int n = 0; n < KT; ++n) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float f = c < 2 ? fA : fB;
+        o[n][c] *= f;
+        ox[n][c] *= f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sc[j][0] = __expf(sc[j][0] - nA);  // arguments <= 0
+      sc[j][1] = __expf(sc[j][1] - nA);
+      sc[j][2] = __expf(sc[j][2] - nB);
+      sc[j][3] = __expf(sc[j][3] - nB);
+      lA += sc[j][0] + sc[j][1];
+      lB += sc[j][2] + sc[j][3];
+    }
+    mA = nA;
+    mB = nB;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t ph[4], pl[4];
+      split_a(sc[j], ph, pl);
+#pragma unroll
+      for (int n = 0; n < KT; ++n) {
+        const float *vr = VTs + (n * 8 + g) * VS + c0 + j * 8 + 2 * t;
+        mma3s(o[n], ox[n], ph, pl, split_b(*reinterpret_cast<const float2 *>(vr)));
+      }
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < KT; ++n)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[n][c] += ox[n][c];
+  ml[0] = mA;  // row g: running max, row g + 8; then the row sums
+  ml[1] = mB;
+  ml[2] = quad_sum(lA);
+  ml[3] = quad_sum(lB);
+}
+
+// o / l of a single-warp attention
+template <int KT>
+static __device__ __forceinline__ void attn_normalize(float (&o)[KT][4], const float (&ml)[4]) {
+  const float iA = 1.0f / ml[2], iB = 1.0f / ml[3];
+#pragma unroll
+  for (int n = 0; n < KT; ++n) {
+    o[n][0] *= iA;
+    o[n][1] *= iA;
+    o[n][2] *= iB;
+    o[n][3] *= iB;
+  }
+}
+
+// Group of `wpt` warps sharing one 16-row tile (named barrier `bar_id`):
+// combine the per-warp partial attentions (flash-style rescale) through the
+// per-warp scratch (16 x (D + 2) floats each); every warp of the group ends
+// with the same normalised o.
+template <int D>
+static __device__ __forceinline__ void attn_merge(float (&o)[D / 8][4], const float (&ml)[4],
+                                                 float *scr_all, int part, int wpt, int bar_id) {
+  constexpr int KT = D / 8, RS = D + 2;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  float *mine = scr_all + part * 16 * RS;
+#pragma unroll
+  for (int n = 0; n < KT; ++n) {
+    *reinterpret_cast<float2 *>(mine + g * RS + 8 * n + 2 * t) = make_float2(o[n][0], o[n][1]);
+    *reinterpret_cast<float2 *>(mine + (g + 8) * RS + 8 * n + 2 * t) = make_float2(o[n][2], o[n][3]);
+  }
+  if (t == 0) {
+    mine[g * RS + D] = ml[0];
+    mine[g * RS + D + 1] = ml[2];
+    mine[(g + 8) * RS + D] = ml[1];
+    mine[(g + 8) * RS + D + 1] = ml[3];
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * wpt) : "memory");
+  float MA = -INFINITY, MB = -INFINITY;
+  for (int p = 0; p < wpt; ++p) {
+    MA = fmaxf(MA, scr_all[p * 16 * RS + g * RS + D]);
+    MB = fmaxf(MB, scr_all[p * 16 * RS + (g + 8) * RS + D]);
+  }
+  float lA = 0.f, lB = 0.f;
+#pragma unroll
+  for (int n = 0; n < KT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  for (int p = 0; p < wpt; ++p) {
+    const float *pp = scr_all + p * 16 * RS;
+    const float fA = __expf(pp[g * RS + D] - MA), fB = __expf(pp[(g + 8) * RS + D] - MB);
+    lA += pp[g * RS + D + 1] * fA;
+    lB += pp[(g + 8) * RS + D + 1] * fB;
+#pragma unroll
+    for (int n = 0; n < KT; ++n) {
+      const float2 a2 = *reinterpret_cast<const float2 *>(pp + g * RS + 8 * n + 2 * t);
+      const float2 b2 = *reinterpret_cast<const float2 *>(pp + (g + 8) * RS + 8 * n + 2 * t);
+      o[n][0] += a2.x * fA;
+      o[n][1] += a2.y * fA;
+      o[n][2] += b2.x * fB;
+      o[n][3] += b2.y * fB;
+    }
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * wpt) : "memory");  // scratch reuse
+  const float iA = 1.0f / lA, iB = 1.0f / lB;
+#pragma unroll
+  for (int n = 0; n < KT; ++n) {
+    o[n][0] *= iA;
+    o[n][1] *= iA;
+    o[n][2] *= iB;
+    o[n][3] *= iB;
+  }
+}
+
+template <int D, int DFF>
+static __device__ __forceinline__ void ffn_mma(const float (&n)[D / 8][4], const gr4ad_layer &Lw,
+                                               const float4 *W1, const float4 *W2,
+                                               float (&h)[D / 8][4]) {
+  constexpr int KT = D / 8, FT = DFF / 8;
+  const int t = threadIdx.x & 3;
+  float f[FT][4];
+  mm<KT, FT>(n, W1, f);
+#pragma unroll
+  for (int j = 0; j < FT; ++j) {
+    const float2 bb = __ldg(reinterpret_cast<const float2 *>(Lw.ffn_b1 + 8 * j + 2 * t));
+    f[j][0] = gelu_fast(f[j][0] + bb.x);
+    f[j][1] = gelu_fast(f[j][1] + bb.y);
+    f[j][2] = gelu_fast(f[j][2] + bb.x);
+    f[j][3] = gelu_fast(f[j][3] + bb.y);
+  }
+  float o[KT][4];
+  mm<FT, KT>(f, W2, o);
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    const float2 bb = __ldg(reinterpret_cast<const float2 *>(Lw.ffn_b2 + 8 * j + 2 * t));
+    h[j][0] += o[j][0] + bb.x;
+    h[j][1] += o[j][1] + bb.y;
+    h[j][2] += o[j][2] + bb.x;
+    h[j][3] += o[j][3] + bb.y;
+  }
+}
+
+// logits of the tile's rows for codebook tiles [n0, n0 + 8) (clamped to NTV)
+constexpr int kLG = 4;  // codebook tiles per logits group
+template <int KT>
+static __device__ __forceinline__ void logits8(const uint32_t (&hh)[KT][4],
+                                               const uint32_t (&hl)[KT][4],
+                                               const float4 *__restrict__ Hf, int NTV, int n0,
+                                               int nend, float (&z)[kLG][4]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < kLG; ++j) {
+    z[j][0] = z[j][1] = z[j][2] = z[j][3] = 0.f;
+    if (n0 + j < nend) {
+#pragma unroll
+      for (int k = 0; k < KT; ++k) mma3(z[j], hh[k], hl[k], __ldg(Hf + (k * NTV + n0 + j) * 32 + lane));
+    } else {
+      z[j][0] = z[j][1] = z[j][2] = z[j][3] = -INFINITY;
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  constexpr int KT = D / 8, VS = SP + 8, HS = 2 * D + 8;
+  constexpr int KVL = SP * D + D * VS;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int T = a.T, L = a.L, K = a.K;
+  const int S = a.ctx_len[b];
+  const long long coff = a.ctx_off[b];
+  const gr4ad_weights &W = a.w;
+  const float scale = 1.0f / sqrtf((float)D);
+
+  float *XT = sm + a.s_XT;  // X^T [D][VS] (dead after the K/V build: aliases HI)
+  float *KV = sm + a.s_KV;  // per head layer: K [SP][D] (k_swz), V^T [D][VS]
+  float *TR = sm + a.s_TR;
+  float *TQ = sm + a.s_TQ;
+  float *HI = sm + a.s_hist;  // self-KV history rows [k | v | pad] (HS floats)
+  int *par = reinterpret_cast<int *>(sm + a.s_par);
+  int *tokm = reinterpret_cast<int *>(sm + a.s_tok);
+  float *cum = sm + a.s_cum;
+  unsigned *hist = reinterpret_cast<unsigned *>(sm + a.s_bins);
+  unsigned *scr = reinterpret_cast<unsigned *>(sm + a.s_scr);
+  unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(sm + a.s_sort);
+  float *wsl = sm + a.s_ws;  // warp 0's trunk slots
+  float *mrg = sm + a.s_mrg;  // per-warp partials of tile groups: 16 x (D + 2) each
+  uint32_t *keys = a.keys + (size_t)b * a.keys_per_req;
+  GR_STAMP(0);
+
+  // ---- context projection X = F W_c + b_c (decoder.py:134-140) -------------
+  for (int s = tid; s < SP; s += kThreads) {
+    float x[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) x[j] = 0.f;
+    if (s < S) {
+      if (a.features) {
+        const float *f = a.features + (coff + s) * a.F;
+        for (int i = 0; i < a.F; ++i) {
+          const float fi = __ldg(f + i);
+#pragma unroll
+          for (int j = 0; j < D; j += 4) {
+            const float4 w4 = __ldg(reinterpret_cast<const float4 *>(W.ctx_W + (size_t)i * D + j));
+            x[j] = fmaf(fi, w4.x, x[j]);
+            x[j + 1] = fmaf(fi, w4.y, x[j + 1]);
+            x[j + 2] = fmaf(fi, w4.z, x[j + 2]);
+            x[j + 3] = fmaf(fi, w4.w, x[j + 3]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] += __ldg(W.ctx_b + j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] = __ldg(a.context + (coff + s) * D + j);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) XT[j * VS + s] = x[j];
+  }
+  __syncthreads();
+  GR_STAMP(1);
+
+  // ---- head-layer K / V^T (beam.py:165-169) by warps 1-7 while warp 0 runs
+  // the trunk; thread owns keys, X column in registers
+  if (K > 0 && wid == 0) {
+    trunk_warp0<D>(a, XT, VS, S, TR, TQ, wsl);
+  } else {
+    const int t0 = K > 0 ? 32 : 0, nt = kThreads - t0;
+    const int ldw = 2 * L * D;
+    for (int i = K; i < L; ++i) {
+      float *Kl = KV + (size_t)(i - K) * KVL, *VTl = Kl + SP * D;
+      const float *Wl = W.cross_kv_W + (size_t)(2 * i) * D;
+      for (int s = tid - t0; s < SP; s += nt) {
+        float x[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] = XT[j * VS + s];
+#pragma unroll 1
+        for (int c0 = 0; c0 < 2 * D; c0 += 8) {
+          float acc[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const float4 wa = __ldg(reinterpret_cast<const float4 *>(Wl + (size_t)j * ldw + c0));
+            const float4 wb = __ldg(reinterpret_cast<const float4 *>(Wl + (size_t)j * ldw + c0 + 4));
+            acc[0] = fmaf(x[j], wa.x, acc[0]);
+            acc[1] = fmaf(x[j], wa.y, acc[1]);
+            acc[2] = fmaf(x[j], wa.z, acc[2]);
+            acc[3] = fmaf(x[j], wa.w, acc[3]);
+            acc[4] = fmaf(x[j], wb.x, acc[4]);
+            acc[5] = fmaf(x[j], wb.y, acc[5]);
+            acc[6] = fmaf(x[j], wb.z, acc[6]);
+            acc[7] = fmaf(x[j], wb.w, acc[7]);
+          }
+          if (s >= S)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+          if (c0 < D) {
+            float4 *kr = reinterpret_cast<float4 *>(Kl + s * D + (c0 ^ (((s >> 1) & 1) << 3)));
+            kr[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            kr[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) VTl[(c0 - D + c) * VS + s] = acc[c];
+          }
+        }
+      }
+    }
+  }
+  if (tid == 0) {
+    par[0] = 0;
+    tokm[0] = 0;
+    cum[0] = 0.f;
+  }
+  __syncthreads();
+  GR_STAMP(2);
+  GR_STAMP(3);
+
+  const int last = a.rerank ? T : T - 1;
+  int live = 1;
+  for (int t = 0; t <= last; ++t) {
+    const int mo = a.moff[t];
+    const int V = t < T ? a.V[t] : 0;
+    for (int i = tid; i < 2048; i += kThreads) hist[i] = 0u;
+    if (wid == 0) {
+      float mc = -INFINITY;
+      for (int j = lane; j < live; j += 32) mc = fmaxf(mc, cum[mo + j]);
+      mc = warp_max(mc);
+      if (lane == 0) {
+        scr[48] = __float_as_uint(mc);
+        scr[49] = __float_as_uint(2048.0f / (logf((float)max(V, 2)) + 4.0f));
+      }
+    }
+    __syncthreads();
+    const float Rs = __uint_as_float(scr[48]);
+    const float bscale = __uint_as_float(scr[49]);
+    auto sbin = [&](float sc) -> unsigned {
+      return (unsigned)fminf((Rs - sc) * bscale, 2047.0f);
+    };
+    int hcur = -1;
+    unsigned hcnt = 0;
+    // 16-row tiles; with fewer than 8 tiles a group of wpt warps shares a
+    // tile (keys and codebook tiles split, per-row work duplicated)
+    const int n_tiles = (live + 15) / 16;
+    int wpt = 1;
+    while (a.tile_split && n_tiles * wpt * 2 <= kWarps) wpt *= 2;
+    const int part = wid % wpt, bar_id = 1 + wid / wpt;
+    float *gscr = mrg + (wid / wpt) * wpt * 16 * (D + 2);
+    for (int tile = wid / wpt; tile < n_tiles; tile += kWarps / wpt) {
+      const int r0 = tile * 16;
+      const int rA = r0 + g, rB = rA + 8;
+      const bool okA = rA < live, okB = rB < live;
+      const int cA = min(rA, live - 1), cB = min(rB, live - 1);
+      // ---- token input + gated fusion (beam.py:180-191; layers.py:129-133)
+      float s[KT][4], h[KT][4];
+#pragma unroll
+      for (int n = 0; n < KT; ++n) {
+        const int col = 8 * n + 2 * t4;
+        float2 xa, xb;
+        if (t == 0) {
+          xa = xb = __ldg(reinterpret_cast<const float2 *>(W.bos + col));
+        } else {
+          xa = __ldg(reinterpret_cast<const float2 *>(W.emb[t - 1] + (size_t)tokm[mo + cA] * D + col));
+          xb = __ldg(reinterpret_cast<const float2 *>(W.emb[t - 1] + (size_t)tokm[mo + cB] * D + col));
+        }
+        s[n][0] = xa.x;
+        s[n][1] = xa.y;
+        s[n][2] = xb.x;
+        s[n][3] = xb.y;
+      }
+      if (K > 0) {
+        float m[KT][4];
+        mm<KT, KT>(s, a.frag + a.fi.wg, m);
+#pragma unroll
+        for (int n = 0; n < KT; ++n) {
+          const float2 tr = *reinterpret_cast<const float2 *>(TR + t * D + 8 * n + 2 * t4);
+          m[n][0] *= tr.x;  // m_t * (s W_g)
+          m[n][1] *= tr.y;
+          m[n][2] *= tr.x;
+          m[n][3] *= tr.y;
+        }
+        mm<KT, KT>(m, a.frag + a.fi.wf_m, h);
+        mm<KT, KT, true>(s, a.frag + a.fi.wf_s, h);
+      } else {
+#pragma unroll
+        for (int n = 0; n < KT; ++n) {
+          const float2 pp = __ldg(reinterpret_cast<const float2 *>(W.pos + (size_t)t * D + 8 * n + 2 * t4));
+          h[n][0] = s[n][0] + pp.x;
+          h[n][1] = s[n][1] + pp.y;
+          h[n][2] = s[n][2] + pp.x;
+          h[n][3] = s[n][3] + pp.y;
+        }
+      }
+      GR_SUB(0);
+      // ---- head layers (layers.py:66-119, incremental) ------------------------
+      for (int i = K; i < L; ++i) {
+        const int li = i - K;
+        const gr4ad_layer &Lw = W.layer[i];
+        const float *Kl = KV + (size_t)li * KVL;
+        float n[KT][4], q[KT][4], o[KT][4];
+        ln_frag<KT>(h, Lw.ln1_g, Lw.ln1_b, n);
+        mm<KT, KT>(n, a.frag + a.fi.cq[li], q);
+        GR_SUB(1);
+        {
+          float ml[4];
+          if (wpt == 1) {
+            attn_mma<D>(q, Kl, Kl + SP * D, S, 0, SP, o, ml);
+            attn_normalize<KT>(o, ml);
+          } else {
+            // whole 64-key chunks per warp (keys >= S are zero rows, masked)
+            const int span = ((S + wpt - 1) / wpt + 63) / 64 * 64;
+            attn_mma<D>(q, Kl, Kl + SP * D, S, part * span, (part + 1) * span, o, ml);
+            attn_merge<D>(o, ml, gscr, part, wpt, bar_id);
+          }
+        }
+        GR_SUB(2);
+        mm<KT, KT, true>(o, a.frag + a.fi.co[li], h);
+        ln_frag<KT>(h, Lw.ln2_g, Lw.ln2_b, n);
+        float ks[KT][4], vs[KT][4];
+        mm<KT, KT>(n, a.frag + a.fi.sq[li], q);
+        mm<KT, KT>(n, a.frag + a.fi.sk[li], ks);
+        mm<KT, KT>(n, a.frag + a.fi.sv[li], vs);
+        // self-attention over the ancestor chain (history by parent pointer):
+        // own position first, then ancestors; online softmax (layers.py:101-113)
+        float dA = 0.f, dB = 0.f;
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+          dA = fmaf(q[j][0], ks[j][0], fmaf(q[j][1], ks[j][1], dA));
+          dB = fmaf(q[j][2], ks[j][2], fmaf(q[j][3], ks[j][3], dB));
+        }
+        float mxA = quad_sum(dA) * scale, mxB = quad_sum(dB) * scale, seA = 1.f, seB = 1.f;
+#pragma unroll
+        for (int j = 0; j < KT; ++j)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) o[j][c] = vs[j][c];
+        int arA = cA, arB = cB;
+        for (int tau = t - 1; tau >= 0; --tau) {
+          arA = par[a.moff[tau + 1] + arA];
+          arB = par[a.moff[tau + 1] + arB];
+          const float *hA = HI + ((size_t)li * a.Hrows + a.hoff[tau] + arA) * HS + 2 * t4;
+          const float *hB = HI + ((size_t)li * a.Hrows + a.hoff[tau] + arB) * HS + 2 * t4;
+          float eA = 0.f, eB = 0.f;
+#pragma unroll
+          for (int j = 0; j < KT; ++j) {
+            const float2 ka = *reinterpret_cast<const float2 *>(hA + 8 * j);
+            const float2 kb = *reinterpret_cast<const float2 *>(hB + 8 * j);
+            eA = fmaf(q[j][0], ka.x, fmaf(q[j][1], ka.y, eA));
+            eB = fmaf(q[j][2], kb.x, fmaf(q[j][3], kb.y, eB));
+          }
+          const float scA = quad_sum(eA) * scale, scB = quad_sum(eB) * scale;
+          const float nA = fmaxf(mxA, scA), fA = expf(mxA - nA), wA = expf(scA - nA);
+          const float nB = fmaxf(mxB, scB), fB = expf(mxB - nB), wB = expf(scB - nB);
+          seA = seA * fA + wA;
+          seB = seB * fB + wB;
+#pragma unroll
+          for (int j = 0; j < KT; ++j) {
+            const float2 va = *reinterpret_cast<const float2 *>(hA + D + 8 * j);
+            const float2 vb = *reinterpret_cast<const float2 *>(hB + D + 8 * j);
+            o[j][0] = o[j][0] * fA + wA * va.x;
+            o[j][1] = o[j][1] * fA + wA * va.y;
+            o[j][2] = o[j][2] * fB + wB * vb.x;
+            o[j][3] = o[j][3] * fB + wB * vb.y;
+          }
+          mxA = nA;
+          mxB = nB;
+        }
+        if (t < last && part == 0) {  // the last level's history is never read
+          float *wA = HI + ((size_t)li * a.Hrows + a.hoff[t] + rA) * HS + 2 * t4;
+          float *wB = HI + ((size_t)li * a.Hrows + a.hoff[t] + rB) * HS + 2 * t4;
+#pragma unroll
+          for (int j = 0; j < KT; ++j) {
+            if (okA) {
+              *reinterpret_cast<float2 *>(wA + 8 * j) = make_float2(ks[j][0], ks[j][1]);
+              *reinterpret_cast<float2 *>(wA + D + 8 * j) = make_float2(vs[j][0], vs[j][1]);
+            }
+            if (okB) {
+              *reinterpret_cast<float2 *>(wB + 8 * j) = make_float2(ks[j][2], ks[j][3]);
+              *reinterpret_cast<float2 *>(wB + D + 8 * j) = make_float2(vs[j][2], vs[j][3]);
+            }
+          }
+        }
+        const float iA = 1.0f / seA, iB = 1.0f / seB;
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+          o[j][0] *= iA;
+          o[j][1] *= iA;
+          o[j][2] *= iB;
+          o[j][3] *= iB;
+        }
+        mm<KT, KT, true>(o, a.frag + a.fi.so[li], h);
+        ln_frag<KT>(h, Lw.ln3_g, Lw.ln3_b, n);
+        if (a.dff == 2 * D)
+          ffn_mma<D, 2 * D>(n, Lw, a.frag + a.fi.w1[li], a.frag + a.fi.w2[li], h);
+        else
+          ffn_mma<D, D>(n, Lw, a.frag + a.fi.w1[li], a.frag + a.fi.w2[li], h);
+      }
+      if (t == T) {  // value re-rank step (beam.py:258-288): rank in double
+        float vl[1][4];
+        mm<KT, 1>(h, a.frag + a.fi.value, vl);
+        const int c0 = 2 * t4, c1 = c0 + 1;
+        const bool u0 = c0 < a.nb, u1 = c1 < a.nb;
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          const float v0 = vl[0][2 * side], v1 = vl[0][2 * side + 1];
+          const float mv = quad_max(fmaxf(u0 ? v0 : -INFINITY, u1 ? v1 : -INFINITY));
+          const double se = quad_sum_d((u0 ? exp((double)v0 - (double)mv) : 0.0) +
+                                       (u1 ? exp((double)v1 - (double)mv) : 0.0));
+          const double ls = log(se);
+          double ev = (u0 ? exp(((double)v0 - (double)mv) - ls) * (double)__ldg(a.value_reps + c0) : 0.0) +
+                      (u1 ? exp(((double)v1 - (double)mv) - ls) * (double)__ldg(a.value_reps + c1) : 0.0);
+          ev = quad_sum_d(ev);
+          const int r = side ? rB : rA;
+          if ((side ? okB : okA) && t4 == 0 && part == 0)
+            reinterpret_cast<double *>(sbuf)[r] = ev * exp((double)cum[mo + r]);
+        }
+        continue;
+      }
+      GR_SUB(3);
+      // ---- codebook logits + log-softmax keys (beam.py:198-200) ---------------
+      const float4 *Hf = a.frag + a.fi.head[t];
+      const int NTV = V / 8;
+      uint32_t hh[KT][4], hl[KT][4];
+#pragma unroll
+      for (int k = 0; k < KT; ++k) split_a(h[k], hh[k], hl[k]);
+      const int per = (NTV + wpt - 1) / wpt;
+      const int nb0 = min(NTV, part * per), nb1 = min(NTV, nb0 + per);
+      float mA = -INFINITY, mB = -INFINITY, sA = 0.f, sB = 0.f;
+      for (int n0 = nb0; n0 < nb1; n0 += kLG) {
+        float z[kLG][4];
+        logits8<KT>(hh, hl, Hf, NTV, n0, nb1, z);
+        float gA = -INFINITY, gB = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < kLG; ++j) {
+          gA = fmaxf(gA, fmaxf(z[j][0], z[j][1]));
+          gB = fmaxf(gB, fmaxf(z[j][2], z[j][3]));
+        }
+        const float nA = fmaxf(mA, gA), nB = fmaxf(mB, gB);
+        sA *= __expf(mA - nA);
+        sB *= __expf(mB - nB);
+#pragma unroll
+        for (int j = 0; j < kLG; ++j) {
+          sA += __expf(z[j][0] - nA) + __expf(z[j][1] - nA);
+          sB += __expf(z[j][2] - nB) + __expf(z[j][3] - nB);
+        }
+        mA = nA;
+        mB = nB;
+      }
+      float MA = quad_max(mA), MB = quad_max(mB);
+      float SA = quad_sum(mA == -INFINITY ? 0.f : sA * __expf(mA - MA));
+      float SB = quad_sum(mB == -INFINITY ? 0.f : sB * __expf(mB - MB));
+      if (wpt > 1) {  // combine (max, sum) over the group's codebook slices
+        if (t4 == 0) {
+          gscr[(part * 16 + g) * 2] = MA;
+          gscr[(part * 16 + g) * 2 + 1] = SA;
+          gscr[(part * 16 + g + 8) * 2] = MB;
+          gscr[(part * 16 + g + 8) * 2 + 1] = SB;
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * wpt) : "memory");
+        float XA = -INFINITY, XB = -INFINITY;
+        for (int p2 = 0; p2 < wpt; ++p2) {
+          XA = fmaxf(XA, gscr[(p2 * 16 + g) * 2]);
+          XB = fmaxf(XB, gscr[(p2 * 16 + g + 8) * 2]);
+        }
+        float YA = 0.f, YB = 0.f;
+        for (int p2 = 0; p2 < wpt; ++p2) {
+          const float ma = gscr[(p2 * 16 + g) * 2], mb = gscr[(p2 * 16 + g + 8) * 2];
+          if (ma != -INFINITY) YA += gscr[(p2 * 16 + g) * 2 + 1] * __expf(ma - XA);
+          if (mb != -INFINITY) YB += gscr[(p2 * 16 + g + 8) * 2 + 1] * __expf(mb - XB);
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * wpt) : "memory");
+        MA = XA;
+        MB = XB;
+        SA = YA;
+        SB = YB;
+      }
+      const float lsA = logf(SA), lsB = logf(SB);
+      GR_SUB(4);
+      const float crA = cum[mo + cA], crB = cum[mo + cB];
+      for (int n0 = nb0; n0 < nb1; n0 += kLG) {
+        float z[kLG][4];
+        logits8<KT>(hh, hl, Hf, NTV, n0, nb1, z);
+#pragma unroll
+        for (int j = 0; j < kLG; ++j) {
+          if (n0 + j < nb1) {
+            const int col = (n0 + j) * 8 + 2 * t4;
+            if (okA) {
+              const float s0 = crA + ((z[j][0] - MA) - lsA), s1 = crA + ((z[j][1] - MA) - lsA);
+              *reinterpret_cast<uint2 *>(keys + (size_t)rA * V + col) = make_uint2(f2ord(s0), f2ord(s1));
+              hist_add(hist, hcur, hcnt, (int)sbin(s0));
+              hist_add(hist, hcur, hcnt, (int)sbin(s1));
+            }
+            if (okB) {
+              const float s0 = crB + ((z[j][2] - MB) - lsB), s1 = crB + ((z[j][3] - MB) - lsB);
+              *reinterpret_cast<uint2 *>(keys + (size_t)rB * V + col) = make_uint2(f2ord(s0), f2ord(s1));
+              hist_add(hist, hcur, hcnt, (int)sbin(s0));
+              hist_add(hist, hcur, hcnt, (int)sbin(s1));
+            }
+          }
+        }
+      }
+    }
+    if (hcnt) atomicAdd(&hist[hcur], hcnt);
+    __syncthreads();
+    GR_STAMP(4 + 2 * t);
+    live = select_level(a, b, t, live, V, keys, hist, scr, sbuf, par, tokm, cum, Rs, bscale);
+    if (live < 0) return;
+    __syncthreads();
+    GR_STAMP(5 + 2 * t);
+  }
+  // results (beam.py:212-213)
+  for (int j = tid; j < live; j += kThreads) {
+    int ar = j;
+    for (int tau = T - 1; tau >= 0; --tau) {
+      a.out_tokens[((size_t)b * a.max_out + j) * T + tau] = tokm[a.moff[tau + 1] + ar];
+      ar = par[a.moff[tau + 1] + ar];
+    }
+    a.out_score[(size_t)b * a.max_out + j] = (double)cum[a.moff[T] + j];
+  }
+  if (tid == 0) a.out_count[b] = live;
+  GR_STAMP(15);
+}
+
+__global__ void frag_prep_kernel(const __grid_constant__ FragJobs jobs, float4 *frag) {
+  const FragJob &jb = jobs.job[blockIdx.y];
+  const int NT = jb.nout / 8, total = (jb.kin / 8) * NT * 32;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int lane = i & 31, tile = i >> 5, nn = tile % NT, kk = tile / NT;
+    const int k0 = kk * 8 + 2 * (lane & 3), n = nn * 8 + (lane >> 2);
+    float x0 = 0.f, x1 = 0.f;
+    if (n < jb.nreal) {
+      x0 = jb.src[k0 * jb.sk + n * jb.sn];
+      x1 = jb.src[(k0 + 1) * jb.sk + n * jb.sn];
+    }
+    frag[jb.dst + i] = split_b(make_float2(x0, x1));
+  }
+}
+
+int frag_prep_launch(const FragJobs &jobs, float4 *frag, cudaStream_t st) {
+  if (jobs.n <= 0) return GR4AD_OK;
+  GR_LAUNCH(KC_SMALL, st, frag_prep_kernel<<<dim3(8, jobs.n), 256, 0, st>>>(jobs, frag));
+  return GR4AD_OK;
+}
+
+int fused_mma_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st) {
+  if (n_requests <= 0) return GR4AD_OK;
+  if (a.D != 16) return set_err(GR4AD_ERR_UNSUPPORTED, "warp-MMA fused decode: d=%d", a.D);
+  GR_CUDA(cudaFuncSetAttribute(fused_mma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  GR_LAUNCH(KC_FUSED, st, fused_mma_kernel<16><<<n_requests, kThreads, smem, st>>>(a));
+  return GR4AD_OK;
 }
 
 int fused_small_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st) {

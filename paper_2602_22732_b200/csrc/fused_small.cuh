@@ -4,6 +4,31 @@
 
 namespace gr {
 
+// Fragment-ordered weights of the warp-MMA fused kernel: for a (Kin x Nout)
+// matrix, float4 [Kin/8][Nout/8][32 lanes] = {hi(W[k0][n]), hi(W[k0+1][n]),
+// lo(W[k0][n]), lo(W[k0+1][n])} with k0 = 8kk + 2(lane & 3), n = 8nn + lane/4
+// (tf32 hi = 13 low mantissa bits cleared, lo = W - hi): the B fragment of
+// mma.m16n8k8 under the k-permutation that lets a C fragment feed the next
+// product as its A fragment.  Offsets are in float4 units.
+constexpr int kMaxHeadLayersMma = 16;
+struct FragIndex {
+  long long wg, wf_m, wf_s, value;
+  long long head[GR4AD_MAX_LEVELS];
+  long long cq[kMaxHeadLayersMma], co[kMaxHeadLayersMma], sq[kMaxHeadLayersMma],
+      sk[kMaxHeadLayersMma], sv[kMaxHeadLayersMma], so[kMaxHeadLayersMma],
+      w1[kMaxHeadLayersMma], w2[kMaxHeadLayersMma];
+};
+struct FragJob {
+  const float *src;  // element (k, n) at src[k * sk + n * sn]
+  long long sk, sn, dst;
+  int kin, nout, nreal;  // nout padded to 8; columns >= nreal are zero
+};
+constexpr int kMaxFragJobs = 4 + GR4AD_MAX_LEVELS + 8 * kMaxHeadLayersMma;
+struct FragJobs {
+  int n;
+  FragJob job[kMaxFragJobs];
+};
+
 struct FusedArgs {
   gr4ad_weights w;
   const float *features;  // (rows, F) caller layout, or NULL
@@ -18,6 +43,11 @@ struct FusedArgs {
   int moff[GR4AD_MAX_LEVELS + 2];  // level-row metadata offset of each level
   // shared-memory layout (float offsets)
   int s_X, s_KV, s_TR, s_TQ, s_hist, s_par, s_tok, s_cum, s_bins, s_scr, s_sort, s_ws;
+  int s_XT;               // warp-MMA kernel: X^T
+  int s_mrg;              // warp-MMA kernel: tile-group merge scratch
+  int tile_split;         // warp-MMA kernel: warps share tiles on small levels
+  const float4 *frag;     // warp-MMA kernel: fragment-ordered weights
+  FragIndex fi;
   uint32_t *keys;  // candidate keys scratch (L2-resident), keys_per_req per request
   long long keys_per_req;
   int max_out;
@@ -28,5 +58,8 @@ struct FusedArgs {
 };
 
 int fused_small_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st);
+// warp-level tensor-core variant (mma.sync tf32, 3xTF32), d = 16
+int frag_prep_launch(const FragJobs &jobs, float4 *frag, cudaStream_t st);
+int fused_mma_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st);
 
 }  // namespace gr

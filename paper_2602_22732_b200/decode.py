@@ -51,7 +51,7 @@ def prefix_keys(valid_sids, vocab_sizes):
 
 
 class BeamDecoder:
-    PATHS = {"auto": 0, "layered": 1, "fused": 2, "tensor": 3}
+    PATHS = {"auto": 0, "layered": 1, "fused": 2, "tensor": 3, "fused_simt": 4}
 
     def __init__(self, model, ctx_lens, widths, trunk_depth=None, value_rerank=False,
                  representatives=None, valid_sids=None, device=None, path="auto"):

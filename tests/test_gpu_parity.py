@@ -124,19 +124,19 @@ def _batch_parity(widths, n_req, label, path="auto", rerank=False, k_depth=None)
     return max(errs)
 
 
-@pytest.mark.parametrize("path", ["fused", "layered", "tensor"])
+@pytest.mark.parametrize("path", ["fused", "fused_simt", "layered", "tensor"])
 def test_c1_batch_matches_oracle(path):
     err = _batch_parity(C1_WIDTHS, 16, "C1", path)
     print(f"C1 ({path}) max abs score error {err:.3e}")
 
 
-@pytest.mark.parametrize("path", ["fused", "layered", "tensor"])
+@pytest.mark.parametrize("path", ["fused", "fused_simt", "layered", "tensor"])
 def test_c2_batch_matches_oracle(path):
     err = _batch_parity(C2_WIDTHS, 8, "C2", path)
     print(f"C2 ({path}) max abs score error {err:.3e}")
 
 
-@pytest.mark.parametrize("path", ["fused", "layered", "tensor"])
+@pytest.mark.parametrize("path", ["fused", "fused_simt", "layered", "tensor"])
 @pytest.mark.parametrize("k_depth", [0, 1])
 def test_c2_rerank_and_vanilla(path, k_depth):
     _batch_parity((16, 48, 96), 4, "C2rr", path, rerank=True, k_depth=k_depth)
@@ -153,7 +153,7 @@ def test_fused_ragged_and_d32():
     feats = [rng.normal(size=(int(rng.integers(1, 200)), 8)) for _ in range(12)]
     widths = [(int(rng.integers(1, 40)), int(rng.integers(1, 200)), int(rng.integers(1, 300)))
               for _ in range(12)]
-    for path in ("fused", "layered", "tensor"):
+    for path in ("fused", "fused_simt", "layered", "tensor"):
         got = S.beam_search_batch(model, features=feats, schedules=widths, path=path)
         for i in range(12):
             want = orc.beam_search(params, ocfg, orc.context_process(feats[i], params), widths[i])
