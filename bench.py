@@ -256,7 +256,29 @@ def class_work(cfgd):
             "fused_decode": ("flop", B * _flops_per_request(cfgd["model"], S, widths))}
 
 
-def roofline_for(dec, feats, cfgd, dev):
+# kernel class -> kernel names in the ncu launch lists (profiles/traffic.json)
+_CLASS_KERNELS = {"fused_decode": ("gr::fused_mma_kernel", "gr::fused_small_kernel"),
+                  "gemm": ("gr::gemm_tc_kernel", "gr::gemm_f32_kernel"),
+                  "attn_gemm": ("gr::gemm_tc_kernel", "gr::gemm_f32_kernel"),
+                  "topk_select": ("gr::topk_select_kernel",)}
+
+
+def _traffic(config, cls):
+    """Mean DRAM bytes per launch of the dominant kernel from the committed ncu
+    launch list (dram__bytes_read.sum + dram__bytes_write.sum), or None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            data = json.load(fh).get(config, {})
+    except (OSError, ValueError):
+        return None
+    for name in _CLASS_KERNELS.get(cls, ()):
+        if name in data:
+            return data[name]["dram_bytes_per_launch"]
+    return None
+
+
+def roofline_for(dec, feats, cfgd, dev, config=None):
     import ctypes as C
 
     import torch
@@ -301,12 +323,12 @@ def roofline_for(dec, feats, cfgd, dev):
         achieved = per_launch / per_launch_s / 1e9
         peak, unit, bound = hbm, "GB/s", "hbm"
     out = {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-           "frac": achieved / peak, "traffic": None, "peak_source": src,
+           "frac": achieved / peak, "traffic": _traffic(config, dom), "peak_source": src,
            "algorithmic_per_launch": per_launch, "launch_ms": per_launch_s * 1e3,
            "classes": classes,
            "note": "per-class times are CUDA events on the launching stream; peak is the "
                    "measured bf16 dense figure although the path computes fp32-faithful "
-                   "(3xTF32 on tcgen05, or fp32 FFMA on CUDA cores)"}
+                   "(3xTF32 on tcgen05 or mma.sync tensor cores, or fp32 FFMA on CUDA cores)"}
     if kind == "flop" and dom in ("gemm", "attn_gemm"):
         # fp32-faithful tensor-core bound: 3 TF32 products per MAC (3xTF32)
         torch.backends.cuda.matmul.allow_tf32 = True
@@ -479,7 +501,7 @@ def main():
 
     line = None
     if rank == 0:
-        roof = roofline_for(dec, feats, cfgd, dev)
+        roof = roofline_for(dec, feats, cfgd, dev, args.config)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1

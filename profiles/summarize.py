@@ -30,13 +30,43 @@ def report(path):
                 print(f"  {k:70s} {v[i]:>16s} {u[i]}")
 
 
+def _scale(v, unit):
+    unit = unit.lower()
+    mult = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}
+    return v * mult.get(unit, 1)
+
+
+def launch_traffic(path):
+    """{kernel: (launches, mean dram bytes per launch)} from a launch list
+    captured with dram__bytes_{read,write}.sum (ncu --csv, one row per metric)."""
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    h = rows[hi]
+    ii, ki = h.index("ID"), h.index("Kernel Name")
+    mi, vi, ui = h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+    per = collections.defaultdict(float)
+    name_of = {}
+    for r in rows[hi + 1:]:
+        if r[mi].startswith("dram__bytes"):
+            per[r[ii]] += _scale(float(r[vi].replace(",", "")), r[ui])
+            name_of[r[ii]] = r[ki].split("(")[0].replace("void ", "").split("<")[0]
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for k, b in per.items():
+        agg[name_of[k]][0] += 1
+        agg[name_of[k]][1] += b
+    return {k: (n, b / n) for k, (n, b) in agg.items()}
+
+
 def launches(path):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[hi + 1:]:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
         name = r[ki].split("(")[0].replace("void ", "")
         name = name.split("<")[0]
         v = float(r[vi].replace(",", ""))
@@ -50,7 +80,22 @@ def launches(path):
     print(f"total {sum(x[0] for x in agg.values())} launches, {tot:.1f} us (cold, serialised)")
 
 
+def write_traffic(out, **lists):
+    """profiles/traffic.json: per config, the mean DRAM bytes per launch of
+    each kernel (bench.py reports it as roofline.traffic)."""
+    import json
+    data = {}
+    for cfg, path in lists.items():
+        data[cfg] = {k: {"launches": n, "dram_bytes_per_launch": b, "source": path}
+                     for k, (n, b) in launch_traffic(path).items()}
+    with open(out, "w") as fh:
+        json.dump(data, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "--traffic":
+        write_traffic(sys.argv[2], **dict(a.split("=", 1) for a in sys.argv[3:]))
+        sys.exit(0)
     for p in sys.argv[1:]:
         print(f"# {p}")
         (report if p.endswith(".ncu-rep") else launches)(p)
