@@ -12,7 +12,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgr4ad.so")
+# GR4AD_LIB: an instrumented build (e.g. GR_FUSED_TIMING, profiles/fused_phases.py)
+LIB_PATH = os.environ.get("GR4AD_LIB") or os.path.join(_HERE, "libgr4ad.so")
 
 MAX_LEVELS = 8
 MAX_LAYERS = 32

@@ -96,7 +96,8 @@ struct Plan {
   size_t o_keys = 0, o_wT = 0;
   // warp-MMA variant of the fused kernel (d = 16)
   bool f_mma = false;
-  int f_s4[14] = {};  // as f_s, plus [12] = X^T, [13] = tile-group merge scratch
+  int f_s4[17] = {};  // as f_s, plus [12] X^T, [13] tile-group merge scratch, [14] codebook, [15] mbarrier, [16] pass-2 row state
+  int f_hst_rows = 0, f_head_floats = 0;
   size_t f_smem4 = 0;
   long long frag_f4 = 0;  // fragment-ordered weights (float4 count)
   size_t o_frag = 0;
@@ -110,10 +111,10 @@ static long long frag_layout(const Plan &p, const gr4ad_weights *w, FragJobs *jo
   long long off = 0;
   if (jobs) jobs->n = 0;
   auto add = [&](const float *src, long long sk, long long sn, int kin, int nout,
-                 int nreal) -> long long {
-    if (jobs) jobs->job[jobs->n++] = FragJob{src, sk, sn, off, kin, nout, nreal};
+                 int nreal, int raw = 0) -> long long {
+    if (jobs) jobs->job[jobs->n++] = FragJob{src, sk, sn, off, kin, nout, nreal, raw};
     const long long r = off;
-    off += (long long)(kin / 8) * (nout / 8) * 32;
+    off += (long long)(kin / 8) * (nout / 8) * (raw ? 16 : 32);  // float4 units
     return r;
   };
   const gr4ad_weights z{};
@@ -136,6 +137,8 @@ static long long frag_layout(const Plan &p, const gr4ad_weights *w, FragJobs *jo
     fi->w2[li] = add(Lw.ffn_W2, d, 1, p.dff, d, d);
   }
   for (int t = 0; t < p.T; ++t) fi->head[t] = add(W.head[t], p.V[t], 1, d, p.V[t], p.V[t]);
+  for (int t = 0; t < p.T; ++t)
+    fi->head_raw[t] = add(W.head[t], p.V[t], 1, d, p.V[t], p.V[t], 1);
   return off;
 }
 
@@ -173,8 +176,24 @@ static bool plan_fused_mma(Plan &p) {
   p.f_s4[10] = take(2LL * p.f_sort_cap);
   p.f_s4[11] = take(4LL * 4 * D);  // warp 0's trunk slots
   p.f_s4[13] = take(8LL * 16 * (D + 2));  // 8 warps x 16 rows x (D + 2)
+  int vmax = 8;
+  for (int t = 0; t < p.T; ++t) vmax = std::max(vmax, p.V[t]);
+  p.f_s4[14] = take((long long)D * vmax);  // one level's codebook, raw fragment order
+  p.f_head_floats = D * vmax;
+  p.f_s4[15] = take(4);                    // two mbarriers (16-B aligned)
+  // two CTAs per SM: 2 x (smem + 1 KB reserved) <= 228 KB
+  constexpr size_t kMaxSmem = 113 * 1024;
+  if ((size_t)o * sizeof(float) > kMaxSmem) return false;
+  // per-row pass-2 state of the proxy-window selection, when it fits
+  long long srows = 1;
+  for (int t = 0; t < p.T; ++t) srows = std::max(srows, (long long)p.maxcap[t]);
+  p.f_hst_rows = 0;
+  p.f_s4[16] = 0;
+  if ((size_t)(o + srows * (D + 2) + 4) * sizeof(float) <= kMaxSmem) {
+    p.f_s4[16] = take(srows * (D + 2));
+    p.f_hst_rows = (int)srows;
+  }
   const size_t bytes = (size_t)o * sizeof(float);
-  if (bytes > 110 * 1024) return false;  // two CTAs per SM
   p.f_smem4 = bytes;
   p.f_Hrows_mma = (int)std::max(hrows, 1LL);
   FragIndex fi;
@@ -388,7 +407,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   if (p.fused) {
     if (p.f_mma) p.o_frag = take(16 * (size_t)p.frag_f4);
     p.o_keys = take(sizeof(uint32_t) * (size_t)B * p.f_keys_per_req);
-    take(sizeof(long long) * 16 * (size_t)B);  // per-request phase stamps (timing builds)
+    take(sizeof(long long) * kDbgSlots * (size_t)B);  // per-request phase stamps (timing builds)
     p.total = o;
     return GR4AD_OK;
   }
@@ -770,13 +789,18 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     f.sort_cap = p.f_sort_cap;
     f.out_count = out->count; f.out_tokens = out->tokens; f.out_score = out->score;
     f.dbg = reinterpret_cast<long long *>(static_cast<char *>(ws) + p.total -
-                                          (size_t)B * 16 * sizeof(long long));
+                                          (size_t)B * kDbgSlots * sizeof(long long));
     if (p.f_mma) {
       f.s_X = p.f_s4[0]; f.s_KV = p.f_s4[1]; f.s_TR = p.f_s4[2]; f.s_TQ = p.f_s4[3];
       f.s_hist = p.f_s4[4]; f.s_par = p.f_s4[5]; f.s_tok = p.f_s4[6]; f.s_cum = p.f_s4[7];
       f.s_bins = p.f_s4[8]; f.s_scr = p.f_s4[9]; f.s_sort = p.f_s4[10]; f.s_ws = p.f_s4[11];
       f.s_XT = p.f_s4[12];
       f.s_mrg = p.f_s4[13];
+      f.s_head = p.f_s4[14];
+      f.s_mbar = p.f_s4[15];
+      f.head_floats = p.f_head_floats;
+      f.s_hst = p.f_s4[16];
+      f.hst_rows = p.f_hst_rows;
       f.tile_split = 1;
       f.Hrows = p.f_Hrows_mma;
       for (int t = 0; t < GR4AD_MAX_LEVELS + 2; ++t) f.hoff[t] = p.f_hoff4[t];

@@ -476,20 +476,30 @@ __device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S,
     if (threadIdx.x == 0) {                                                     \
       long long _t;                                                             \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                   \
-      a.dbg[blockIdx.x * 16 + (i)] = _t;                                        \
+      a.dbg[blockIdx.x * kDbgSlots + (i)] = _t;                                        \
     }                                                                           \
   } while (0)
 #define GR_SUB(i)                                                               \
   do {                                                                          \
-    if (t == 0 && threadIdx.x == 0) {                                           \
+    if (t < 3 && threadIdx.x == 0) {                                            \
       long long _t;                                                             \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                   \
-      a.dbg[blockIdx.x * 16 + 10 + (i)] = _t;                                   \
+      a.dbg[blockIdx.x * kDbgSlots + 18 + 8 * t + (i)] = _t;                    \
+    }                                                                           \
+  } while (0)
+// lane 0 of the calling warp stamps slot i (16 <= i < kDbgSlots)
+#define GR_WSTAMP(i)                                                            \
+  do {                                                                          \
+    if ((threadIdx.x & 31) == 0) {                                              \
+      long long _t;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                   \
+      a.dbg[blockIdx.x * kDbgSlots + (i)] = _t;                                 \
     }                                                                           \
   } while (0)
 #else
 #define GR_STAMP(i) do {} while (0)
 #define GR_SUB(i) do {} while (0)
+#define GR_WSTAMP(i) do {} while (0)
 #endif
 
 
@@ -497,10 +507,13 @@ __device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S,
 // value re-rank output) and in-place compaction; returns the next level's
 // live rows (-1 once the re-rank output is written).  Shared by both fused
 // kernels (beam.py:30-89, 202-210, 258-288).
+// collected >= 0: sbuf already holds that many entries (key << 32 | ~flat
+// index) including every candidate of the top k (the warp-MMA kernel's
+// proxy window); they are only sorted and compacted.
 __device__ int select_level(const FusedArgs &a, int b, int t, int live, int V,
                             const uint32_t *keys, unsigned *hist, unsigned *scr,
                             unsigned long long *sbuf, int *par, int *tokm, float *cum, float Rs,
-                            float bscale) {
+                            float bscale, int collected = -1) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int T = a.T;
   auto sbin = [&](float sc) -> unsigned {
@@ -548,7 +561,9 @@ __device__ int select_level(const FusedArgs &a, int b, int t, int live, int V,
   const int n_cand = live * V;
   const int k = min(a.eff[t * a.B + b], n_cand);
   int n_sort = k;  // entries in sbuf to sort (>= k)
-  {
+  if (collected >= 0) {
+    n_sort = collected;
+  } else {
     // (a) window: every key in a bin below the k-th key's bin is in the
     // top-k; the k-th bin is collected whole and the exact sort breaks it
     unsigned cnt_le = 0;
@@ -570,8 +585,8 @@ __device__ int select_level(const FusedArgs &a, int b, int t, int live, int V,
     const bool window_ok = wb < 2047 && cnt_le <= (unsigned)a.sort_cap;
 #ifdef GR_FUSED_TIMING_WINDOW
     if (tid == 0 && t < 3) {
-      a.dbg[blockIdx.x * 16 + 10 + t] = ((long long)cnt_le << 32) | (unsigned)wb;
-      a.dbg[blockIdx.x * 16 + 13 + (t == 2)] = (long long)(bscale * 1000);
+      a.dbg[blockIdx.x * kDbgSlots + 10 + t] = ((long long)cnt_le << 32) | (unsigned)wb;
+      a.dbg[blockIdx.x * kDbgSlots + 13 + (t == 2)] = (long long)(bscale * 1000);
     }
 #endif
     if (window_ok) {
@@ -1045,6 +1060,40 @@ static __device__ __forceinline__ void prefetch_l1(const void *p, size_t bytes) 
     asm volatile("prefetch.global.L1 [%0];" ::"l"(c + o));
 }
 
+// ---- bulk async copy global -> shared (TMA engine) completing on an mbarrier
+static __device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+static __device__ __forceinline__ void bar_init(uint64_t *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one thread: order earlier generic-proxy reads of dst before the async
+// write, then copy `bytes` (multiple of 16) and arm the barrier
+static __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes,
+                                                 uint64_t *bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+static __device__ __forceinline__ void bar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t"
+      "}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 static __device__ __forceinline__ uint32_t tf32_hi(float x) {
   return __float_as_uint(x) & 0xFFFFE000u;
 }
@@ -1354,8 +1403,27 @@ static __device__ __forceinline__ void ffn_mma(const float (&n)[D / 8][4], const
   }
 }
 
-// logits of the tile's rows for codebook tiles [n0, n0 + 8) (clamped to NTV)
+// logits of the tile's rows for codebook tiles [n0, n0 + kLG) (clamped to nend)
+// from the level's codebook staged in shared memory (raw fragment order)
 constexpr int kLG = 4;  // codebook tiles per logits group
+template <int KT>
+static __device__ __forceinline__ void logits_s(const uint32_t (&hh)[KT][4],
+                                                const uint32_t (&hl)[KT][4],
+                                                const float2 *__restrict__ Hs, int NTV, int n0,
+                                                int nend, float (&z)[kLG][4]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < kLG; ++j) {
+    z[j][0] = z[j][1] = z[j][2] = z[j][3] = 0.f;
+    if (n0 + j < nend) {
+#pragma unroll
+      for (int k = 0; k < KT; ++k) mma3(z[j], hh[k], hl[k], split_b(Hs[(k * NTV + n0 + j) * 32 + lane]));
+    } else {
+      z[j][0] = z[j][1] = z[j][2] = z[j][3] = -INFINITY;
+    }
+  }
+}
+
 template <int KT>
 static __device__ __forceinline__ void logits8(const uint32_t (&hh)[KT][4],
                                                const uint32_t (&hl)[KT][4],
@@ -1370,6 +1438,109 @@ static __device__ __forceinline__ void logits8(const uint32_t (&hh)[KT][4],
       for (int k = 0; k < KT; ++k) mma3(z[j], hh[k], hl[k], __ldg(Hf + (k * NTV + n0 + j) * 32 + lane));
     } else {
       z[j][0] = z[j][1] = z[j][2] = z[j][3] = -INFINITY;
+    }
+  }
+}
+
+// A fragments (tf32 hi / lo) of rows cA (g) and cB (g + 8) of a row-major
+// [rows][ld] state (C-fragment column order, as split_a)
+template <int KT>
+static __device__ __forceinline__ void load_split(const float *st, int ld, int cA, int cB,
+                                                  uint32_t (&hh)[KT][4], uint32_t (&hl)[KT][4]) {
+  const int t4 = threadIdx.x & 3;
+#pragma unroll
+  for (int n = 0; n < KT; ++n) {
+    const float2 a2 = *reinterpret_cast<const float2 *>(st + cA * ld + 8 * n + 2 * t4);
+    const float2 b2 = *reinterpret_cast<const float2 *>(st + cB * ld + 8 * n + 2 * t4);
+    const float c[4] = {a2.x, a2.y, b2.x, b2.y};
+    split_a(c, hh[n], hl[n]);
+  }
+}
+
+// Second logits pass of a tile (beam.py:198-200): recompute the logits, form
+// the candidate scores cum_r + (z - M_r) - lse_r.  !COLLECT: store every key
+// for the selection kernel path and histogram its bin.  COLLECT: append only
+// the candidates whose bin is <= wb (the proxy window) to sbuf, counting in
+// *cnt (entries past cap are counted, not written: the caller falls back).
+struct RowScore {
+  bool ok;
+  int r;
+  float cr, M, ls;
+};
+template <int KT, bool COLLECT>
+static __device__ __forceinline__ void logits_pass2(
+    const uint32_t (&hh)[KT][4], const uint32_t (&hl)[KT][4], const float2 *Hf, int NTV, int nb0,
+    int nb1, const RowScore &A, const RowScore &B, int V, uint32_t *keys, unsigned *hist,
+    int &hcur, unsigned &hcnt, float Rs, float bscale, int wb, unsigned long long *sbuf,
+    unsigned *cnt, int cap) {
+  const int lane = threadIdx.x & 31, t4 = lane & 3;
+  auto sbin = [&](float sc) -> unsigned { return (unsigned)fminf((Rs - sc) * bscale, 2047.0f); };
+  // COLLECT pre-filter: bin <= wb needs s > Rs - (wb + 1) / bscale; the z bound
+  // is loosened by 1e-3 and every pre-pass is checked exactly with sbin
+  const float slo = Rs - (float)(wb + 1) / bscale - 1e-3f;
+  const float zA = A.ok ? slo - A.cr + A.M + A.ls : INFINITY;
+  const float zB = B.ok ? slo - B.cr + B.M + B.ls : INFINITY;
+  for (int n0 = nb0; n0 < nb1; n0 += kLG) {
+    float z[kLG][4];
+    logits_s<KT>(hh, hl, Hf, NTV, n0, nb1, z);
+    if (!COLLECT) {
+#pragma unroll
+      for (int j = 0; j < kLG; ++j) {
+        const int col = (n0 + j) * 8 + 2 * t4;
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          const RowScore &R = side ? B : A;
+          if (n0 + j < nb1 && R.ok) {
+            const float s0 = R.cr + ((z[j][2 * side] - R.M) - R.ls);
+            const float s1 = R.cr + ((z[j][2 * side + 1] - R.M) - R.ls);
+            *reinterpret_cast<uint2 *>(keys + (size_t)R.r * V + col) = make_uint2(f2ord(s0), f2ord(s1));
+            hist_add(hist, hcur, hcnt, (int)sbin(s0));
+            hist_add(hist, hcur, hcnt, (int)sbin(s1));
+          }
+        }
+      }
+    } else {
+      unsigned pm = 0;  // bit 4j + c: value c of n-tile j passed the exact window test
+#pragma unroll
+      for (int j = 0; j < kLG; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (z[j][c] > (c < 2 ? zA : zB)) {  // padded tiles are -inf
+            const RowScore &R = c < 2 ? A : B;
+            const float sc = R.cr + ((z[j][c] - R.M) - R.ls);
+            if (sbin(sc) <= (unsigned)wb) pm |= 1u << (4 * j + c);
+          }
+      if (__any_sync(kFull, pm != 0)) {
+        const unsigned np = __popc(pm);
+        unsigned incl = np;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += y;
+        }
+        unsigned base = 0;
+        if (lane == 31) base = atomicAdd(cnt, incl);
+        base = __shfl_sync(kFull, base, 31) + incl - np;
+        while (pm) {
+          const int bit = __ffs(pm) - 1;
+          pm &= pm - 1;
+          const int j = bit >> 2, c = bit & 3;
+          const RowScore &R = c < 2 ? A : B;
+          float zz = z[0][0];
+#pragma unroll
+          for (int jj = 0; jj < kLG; ++jj)
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc)
+              if (jj == j && cc == c) zz = z[jj][cc];
+          const float sc = (c < 2 ? A.cr : B.cr) + ((zz - (c < 2 ? A.M : B.M)) - (c < 2 ? A.ls : B.ls));
+          const int row = c < 2 ? A.r : B.r;
+          const int col = (n0 + j) * 8 + 2 * t4 + (c & 1);
+          if (base < (unsigned)cap)
+            sbuf[base] = ((unsigned long long)f2ord(sc) << 32) | (0xFFFFFFFFu - (unsigned)(row * V + col));
+          ++base;
+          (void)R;
+        }
+      }
     }
   }
 }
@@ -1401,8 +1572,27 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
   unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(sm + a.s_sort);
   float *wsl = sm + a.s_ws;  // warp 0's trunk slots
   float *mrg = sm + a.s_mrg;  // per-warp partials of tile groups: 16 x (D + 2) each
+  float2 *HS2 = reinterpret_cast<float2 *>(sm + a.s_head);  // level codebook (bulk copy)
+  constexpr int HSD = D + 2;      // per-row pass-2 state: head input h, M, lse
+  float *hst = sm + a.s_hst;      // [hst_rows][HSD]
+  float *prox = reinterpret_cast<float *>(sm + a.s_sort);  // window proxies (before collection)
+  uint64_t *hbar = reinterpret_cast<uint64_t *>(sm + a.s_mbar);
   uint32_t *keys = a.keys + (size_t)b * a.keys_per_req;
   GR_STAMP(0);
+  uint64_t *fbar = hbar + 1;
+  // the request's features land in HS2 by one bulk copy (HS2 takes the
+  // level-0 codebook after the projection)
+  const bool feat_bulk = a.features && a.F % 4 == 0 && S * a.F <= a.head_floats &&
+                         (coff * a.F) % 4 == 0;
+  if (tid == 0) {
+    bar_init(hbar);
+    bar_init(fbar);
+    if (feat_bulk)
+      bulk_load(HS2, a.features + coff * a.F, (uint32_t)(S * a.F * sizeof(float)), fbar);
+  }
+  __syncthreads();
+  // one bulk copy per level into HS2, issued by thread 0 one level ahead;
+  // phase t of hbar completes when level t's codebook has landed
 
   // ---- context projection X = F W_c + b_c (decoder.py:134-140) -------------
   for (int s = tid; s < SP; s += kThreads) {
@@ -1410,17 +1600,45 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
 #pragma unroll
     for (int j = 0; j < D; ++j) x[j] = 0.f;
     if (s < S) {
-      if (a.features) {
-        const float *f = a.features + (coff + s) * a.F;
-        for (int i = 0; i < a.F; ++i) {
-          const float fi = __ldg(f + i);
+      if (feat_bulk) {
+        bar_wait(fbar, 0);
+        const float4 *f4 = reinterpret_cast<const float4 *>(HS2) + s * (a.F / 4);
+        for (int i0 = 0; i0 < a.F; i0 += 4) {
+          const float4 fv = f4[i0 / 4];
+          const float fa[4] = {fv.x, fv.y, fv.z, fv.w};
 #pragma unroll
-          for (int j = 0; j < D; j += 4) {
-            const float4 w4 = __ldg(reinterpret_cast<const float4 *>(W.ctx_W + (size_t)i * D + j));
-            x[j] = fmaf(fi, w4.x, x[j]);
-            x[j + 1] = fmaf(fi, w4.y, x[j + 1]);
-            x[j + 2] = fmaf(fi, w4.z, x[j + 2]);
-            x[j + 3] = fmaf(fi, w4.w, x[j + 3]);
+          for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int j = 0; j < D; j += 4) {
+              const float4 w4 =
+                  __ldg(reinterpret_cast<const float4 *>(W.ctx_W + (size_t)(i0 + u) * D + j));
+              x[j] = fmaf(fa[u], w4.x, x[j]);
+              x[j + 1] = fmaf(fa[u], w4.y, x[j + 1]);
+              x[j + 2] = fmaf(fa[u], w4.z, x[j + 2]);
+              x[j + 3] = fmaf(fa[u], w4.w, x[j + 3]);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] += __ldg(W.ctx_b + j);
+      } else if (a.features) {
+        const float *f = a.features + (coff + s) * a.F;
+        for (int i0 = 0; i0 < a.F; i0 += 16) {  // 16 independent loads in flight
+          float fv[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) fv[u] = i0 + u < a.F ? __ldg(f + i0 + u) : 0.f;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            if (i0 + u >= a.F) break;
+#pragma unroll
+            for (int j = 0; j < D; j += 4) {
+              const float4 w4 =
+                  __ldg(reinterpret_cast<const float4 *>(W.ctx_W + (size_t)(i0 + u) * D + j));
+              x[j] = fmaf(fv[u], w4.x, x[j]);
+              x[j + 1] = fmaf(fv[u], w4.y, x[j + 1]);
+              x[j + 2] = fmaf(fv[u], w4.z, x[j + 2]);
+              x[j + 3] = fmaf(fv[u], w4.w, x[j + 3]);
+            }
           }
         }
 #pragma unroll
@@ -1434,12 +1652,17 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
     for (int j = 0; j < D; ++j) XT[j * VS + s] = x[j];
   }
   __syncthreads();
+  if (tid == 0 && T > 0) {  // level 0's codebook lands during the K/V + trunk phase
+    if (feat_bulk) bar_wait(fbar, 0);  // (complete: every thread waited on it)
+    bulk_load(HS2, a.frag + a.fi.head_raw[0], (uint32_t)(D * a.V[0] * sizeof(float)), hbar);
+  }
   GR_STAMP(1);
 
   // ---- head-layer K / V^T (beam.py:165-169) by warps 1-7 while warp 0 runs
   // the trunk; thread owns keys, X column in registers
   if (K > 0 && wid == 0) {
     trunk_warp0<D>(a, XT, VS, S, TR, TQ, wsl);
+    GR_WSTAMP(16);
   } else {
     const int t0 = K > 0 ? 32 : 0, nt = kThreads - t0;
     const int ldw = 2 * L * D;
@@ -1482,6 +1705,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
         }
       }
     }
+    if (wid == 1) GR_WSTAMP(17);
   }
   if (tid == 0) {
     par[0] = 0;
@@ -1522,6 +1746,8 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
     while (a.tile_split && n_tiles * wpt * 2 <= kWarps) wpt *= 2;
     const int part = wid % wpt, bar_id = 1 + wid / wpt;
     float *gscr = mrg + (wid / wpt) * wpt * 16 * (D + 2);
+    // proxy-window selection (needs the per-row state and the proxies on chip)
+    const bool theta = t < T && live > 0 && live <= a.hst_rows && n_tiles * wpt * 128 <= 2 * a.sort_cap;
     for (int tile = wid / wpt; tile < n_tiles; tile += kWarps / wpt) {
       const int r0 = tile * 16;
       const int rA = r0 + g, rB = rA + 8;
@@ -1693,7 +1919,8 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
       }
       GR_SUB(3);
       // ---- codebook logits + log-softmax keys (beam.py:198-200) ---------------
-      const float4 *Hf = a.frag + a.fi.head[t];
+      bar_wait(hbar, (uint32_t)(t & 1));
+      const float2 *Hf = HS2;
       const int NTV = V / 8;
       uint32_t hh[KT][4], hl[KT][4];
 #pragma unroll
@@ -1701,14 +1928,24 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
       const int per = (NTV + wpt - 1) / wpt;
       const int nb0 = min(NTV, part * per), nb1 = min(NTV, nb0 + per);
       float mA = -INFINITY, mB = -INFINITY, sA = 0.f, sB = 0.f;
+      float p1A = -INFINITY, p2A = -INFINITY, p1B = -INFINITY, p2B = -INFINITY;  // lane top-2
       for (int n0 = nb0; n0 < nb1; n0 += kLG) {
         float z[kLG][4];
-        logits8<KT>(hh, hl, Hf, NTV, n0, nb1, z);
+        logits_s<KT>(hh, hl, Hf, NTV, n0, nb1, z);
         float gA = -INFINITY, gB = -INFINITY;
 #pragma unroll
         for (int j = 0; j < kLG; ++j) {
           gA = fmaxf(gA, fmaxf(z[j][0], z[j][1]));
           gB = fmaxf(gB, fmaxf(z[j][2], z[j][3]));
+          if (theta) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              p2A = fmaxf(p2A, fminf(p1A, z[j][c]));
+              p1A = fmaxf(p1A, z[j][c]);
+              p2B = fmaxf(p2B, fminf(p1B, z[j][2 + c]));
+              p1B = fmaxf(p1B, z[j][2 + c]);
+            }
+          }
         }
         const float nA = fmaxf(mA, gA), nB = fmaxf(mB, gB);
         sA *= __expf(mA - nA);
@@ -1751,38 +1988,124 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
       }
       const float lsA = logf(SA), lsB = logf(SB);
       GR_SUB(4);
-      const float crA = cum[mo + cA], crB = cum[mo + cB];
-      for (int n0 = nb0; n0 < nb1; n0 += kLG) {
-        float z[kLG][4];
-        logits8<KT>(hh, hl, Hf, NTV, n0, nb1, z);
+      const RowScore RA{okA, rA, cum[mo + cA], MA, lsA}, RB{okB, rB, cum[mo + cB], MB, lsB};
+      if (theta) {
+        // save the tile's head input and (M, lse) for pass 2; emit the
+        // per-lane top-2 candidates of each row as window proxies
+        if (part == 0) {
 #pragma unroll
-        for (int j = 0; j < kLG; ++j) {
-          if (n0 + j < nb1) {
-            const int col = (n0 + j) * 8 + 2 * t4;
-            if (okA) {
-              const float s0 = crA + ((z[j][0] - MA) - lsA), s1 = crA + ((z[j][1] - MA) - lsA);
-              *reinterpret_cast<uint2 *>(keys + (size_t)rA * V + col) = make_uint2(f2ord(s0), f2ord(s1));
-              hist_add(hist, hcur, hcnt, (int)sbin(s0));
-              hist_add(hist, hcur, hcnt, (int)sbin(s1));
-            }
-            if (okB) {
-              const float s0 = crB + ((z[j][2] - MB) - lsB), s1 = crB + ((z[j][3] - MB) - lsB);
-              *reinterpret_cast<uint2 *>(keys + (size_t)rB * V + col) = make_uint2(f2ord(s0), f2ord(s1));
-              hist_add(hist, hcur, hcnt, (int)sbin(s0));
-              hist_add(hist, hcur, hcnt, (int)sbin(s1));
-            }
+          for (int n = 0; n < KT; ++n) {
+            if (okA) *reinterpret_cast<float2 *>(hst + rA * HSD + 8 * n + 2 * t4) = make_float2(h[n][0], h[n][1]);
+            if (okB) *reinterpret_cast<float2 *>(hst + rB * HSD + 8 * n + 2 * t4) = make_float2(h[n][2], h[n][3]);
           }
+          if (t4 == 0) {
+            if (okA) { hst[rA * HSD + D] = MA; hst[rA * HSD + D + 1] = lsA; }
+            if (okB) { hst[rB * HSD + D] = MB; hst[rB * HSD + D + 1] = lsB; }
+          }
+        }
+        float4 px;
+        px.x = okA && p1A > -INFINITY ? RA.cr + ((p1A - MA) - lsA) : -INFINITY;
+        px.y = okA && p2A > -INFINITY ? RA.cr + ((p2A - MA) - lsA) : -INFINITY;
+        px.z = okB && p1B > -INFINITY ? RB.cr + ((p1B - MB) - lsB) : -INFINITY;
+        px.w = okB && p2B > -INFINITY ? RB.cr + ((p2B - MB) - lsB) : -INFINITY;
+        reinterpret_cast<float4 *>(prox)[(tile * wpt + part) * 32 + lane] = px;
+      } else {
+        logits_pass2<KT, false>(hh, hl, Hf, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt, Rs,
+                                bscale, 0, sbuf, nullptr, 0);
+      }
+      GR_SUB(5);
+    }
+    int collected = -1;
+    if (theta) {
+      // window from the proxies: >= k real candidates have bin <= wb, so the
+      // whole top k does; collect those in pass 2 and sort them exactly
+      __syncthreads();
+      const int nprox = n_tiles * wpt * 128;
+      const int kk = min(a.eff[t * a.B + b], live * V);
+      const bool all_fit = live * V <= a.sort_cap;  // collect every candidate, no window
+      int hc2 = -1;
+      unsigned hn2 = 0, nfin = 0;
+      if (tid == 0) {
+        scr[40] = 0;
+        scr[41] = 0;
+      }
+      __syncthreads();
+      if (!all_fit) {
+        for (int i = tid; i < nprox; i += kThreads) {
+          const float v = prox[i];
+          if (v > -INFINITY) {
+            hist_add(hist, hc2, hn2, (int)sbin(v));
+            ++nfin;
+          }
+        }
+        if (hn2) atomicAdd(&hist[hc2], hn2);
+        nfin = __reduce_add_sync(kFull, nfin);
+        if (lane == 0 && nfin) atomicAdd(&scr[41], nfin);
+        __syncthreads();
+      }
+      int wb = 2047;  // fewer than k proxies: collect every candidate
+      if (!all_fit && scr[41] >= (unsigned)kk) {
+        for (int i = tid; i < 1024; i += kThreads) {  // mirror: find_bin scans from the top
+          const unsigned x = hist[i], y = hist[2047 - i];
+          hist[i] = y;
+          hist[2047 - i] = x;
+        }
+        __syncthreads();
+        unsigned above;
+        wb = 2047 - find_bin(hist, 2048, (unsigned)kk, &above, scr);
+      }
+      GR_SUB(6);
+      for (int tile = wid / wpt; tile < n_tiles; tile += kWarps / wpt) {
+        const int rA = tile * 16 + g, rB = rA + 8;
+        const bool okA = rA < live, okB = rB < live;
+        const int cA = min(rA, live - 1), cB = min(rB, live - 1);
+        const RowScore RA{okA, rA, cum[mo + cA], hst[cA * HSD + D], hst[cA * HSD + D + 1]};
+        const RowScore RB{okB, rB, cum[mo + cB], hst[cB * HSD + D], hst[cB * HSD + D + 1]};
+        uint32_t hh[KT][4], hl[KT][4];
+        load_split<KT>(hst, HSD, cA, cB, hh, hl);
+        const int NTV = V / 8, per = (NTV + wpt - 1) / wpt;
+        const int nb0 = min(NTV, part * per), nb1 = min(NTV, nb0 + per);
+        logits_pass2<KT, true>(hh, hl, HS2, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt, Rs,
+                               bscale, wb, sbuf, &scr[40], a.sort_cap);
+      }
+      GR_SUB(7);
+      __syncthreads();
+      collected = (int)scr[40];
+      if (collected > a.sort_cap) {
+        // window overflow: exact path -- every key to the scratch + histogram
+        collected = -1;
+        for (int i = tid; i < 2048; i += kThreads) hist[i] = 0u;
+        __syncthreads();
+        for (int tile = wid / wpt; tile < n_tiles; tile += kWarps / wpt) {
+          const int rA = tile * 16 + g, rB = rA + 8;
+          const bool okA = rA < live, okB = rB < live;
+          const int cA = min(rA, live - 1), cB = min(rB, live - 1);
+          const RowScore RA{okA, rA, cum[mo + cA], hst[cA * HSD + D], hst[cA * HSD + D + 1]};
+          const RowScore RB{okB, rB, cum[mo + cB], hst[cB * HSD + D], hst[cB * HSD + D + 1]};
+          uint32_t hh[KT][4], hl[KT][4];
+          load_split<KT>(hst, HSD, cA, cB, hh, hl);
+          const int NTV = V / 8, per = (NTV + wpt - 1) / wpt;
+          const int nb0 = min(NTV, part * per), nb1 = min(NTV, nb0 + per);
+          logits_pass2<KT, false>(hh, hl, HS2, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt,
+                                  Rs, bscale, 0, sbuf, nullptr, 0);
         }
       }
     }
     if (hcnt) atomicAdd(&hist[hcur], hcnt);
     __syncthreads();
     GR_STAMP(4 + 2 * t);
-    live = select_level(a, b, t, live, V, keys, hist, scr, sbuf, par, tokm, cum, Rs, bscale);
+    if (tid == 0 && t + 1 < T) {  // next level's codebook lands during this selection
+      bar_wait(hbar, (uint32_t)(t & 1));  // level t's copy is complete (also with no tiles)
+      bulk_load(HS2, a.frag + a.fi.head_raw[t + 1], (uint32_t)(D * a.V[t + 1] * sizeof(float)),
+                hbar);
+    }
+    live = select_level(a, b, t, live, V, keys, hist, scr, sbuf, par, tokm, cum, Rs, bscale,
+                        collected);
     if (live < 0) return;
     __syncthreads();
     GR_STAMP(5 + 2 * t);
   }
+  if (tid == 0 && T > 0) bar_wait(hbar, (uint32_t)((T - 1) & 1));  // no copy outlives the CTA
   // results (beam.py:212-213)
   for (int j = tid; j < live; j += kThreads) {
     int ar = j;
@@ -1807,7 +2130,10 @@ __global__ void frag_prep_kernel(const __grid_constant__ FragJobs jobs, float4 *
       x0 = jb.src[k0 * jb.sk + n * jb.sn];
       x1 = jb.src[(k0 + 1) * jb.sk + n * jb.sn];
     }
-    frag[jb.dst + i] = split_b(make_float2(x0, x1));
+    if (jb.raw)
+      reinterpret_cast<float2 *>(frag + jb.dst)[i] = make_float2(x0, x1);
+    else
+      frag[jb.dst + i] = split_b(make_float2(x0, x1));
   }
 }
 

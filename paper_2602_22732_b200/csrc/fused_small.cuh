@@ -11,9 +11,11 @@ namespace gr {
 // mma.m16n8k8 under the k-permutation that lets a C fragment feed the next
 // product as its A fragment.  Offsets are in float4 units.
 constexpr int kMaxHeadLayersMma = 16;
+constexpr int kDbgSlots = 48;  // per-request phase stamps (GR_FUSED_TIMING builds)
 struct FragIndex {
   long long wg, wf_m, wf_s, value;
   long long head[GR4AD_MAX_LEVELS];
+  long long head_raw[GR4AD_MAX_LEVELS];  // float2 {W[k0][n], W[k0+1][n]} per lane (staged to smem)
   long long cq[kMaxHeadLayersMma], co[kMaxHeadLayersMma], sq[kMaxHeadLayersMma],
       sk[kMaxHeadLayersMma], sv[kMaxHeadLayersMma], so[kMaxHeadLayersMma],
       w1[kMaxHeadLayersMma], w2[kMaxHeadLayersMma];
@@ -22,8 +24,9 @@ struct FragJob {
   const float *src;  // element (k, n) at src[k * sk + n * sn]
   long long sk, sn, dst;
   int kin, nout, nreal;  // nout padded to 8; columns >= nreal are zero
+  int raw;               // 1: float2 {W[k0][n], W[k0+1][n]} per lane (no hi/lo split)
 };
-constexpr int kMaxFragJobs = 4 + GR4AD_MAX_LEVELS + 8 * kMaxHeadLayersMma;
+constexpr int kMaxFragJobs = 4 + 2 * GR4AD_MAX_LEVELS + 8 * kMaxHeadLayersMma;
 struct FragJobs {
   int n;
   FragJob job[kMaxFragJobs];
@@ -45,6 +48,10 @@ struct FusedArgs {
   int s_X, s_KV, s_TR, s_TQ, s_hist, s_par, s_tok, s_cum, s_bins, s_scr, s_sort, s_ws;
   int s_XT;               // warp-MMA kernel: X^T
   int s_mrg;              // warp-MMA kernel: tile-group merge scratch
+  int s_head;             // warp-MMA kernel: the level's codebook (raw fragment order)
+  int head_floats;        // its capacity (floats); first holds the request's features
+  int s_mbar;             // warp-MMA kernel: mbarrier of the codebook bulk copy
+  int s_hst, hst_rows;    // warp-MMA kernel: per-row pass-2 state [hst_rows][D + 2]
   int tile_split;         // warp-MMA kernel: warps share tiles on small levels
   const float4 *frag;     // warp-MMA kernel: fragment-ordered weights
   FragIndex fi;
@@ -54,7 +61,7 @@ struct FusedArgs {
   int sort_cap;  // entries of the shared sort buffer (>= every width, power of 2)
   int *out_count, *out_tokens;
   double *out_score;
-  long long *dbg;  // GR_FUSED_TIMING builds: [B][16] globaltimer stamps
+  long long *dbg;  // GR_FUSED_TIMING builds: [B][kDbgSlots] globaltimer stamps
 };
 
 int fused_small_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st);
