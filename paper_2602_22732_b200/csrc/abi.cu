@@ -366,7 +366,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
       return set_err(GR4AD_ERR_UNSUPPORTED, "tensor-core path needs d, d_ff, F, V multiples of 4");
   }
   p.sc_ld = (p.S_max + 3) / 4 * 4;
-  p.vt_ld = (p.S_tot + 3) / 4 * 4;
+  p.vt_ld = (p.S_tot + 7) / 8 * 8;  // fp16 rows: 16-B aligned
   if (p.tc) {
     const long long D = p.d;
     p.wt_floats = 0;
@@ -420,7 +420,8 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.o_Fin = take(Fl * p.S_tot * p.F);
   // K/V are materialised for the head layers only: trunk rows (n_pos per
   // request) attend through the reassociated (q Wk^T) X^T / (P X) Wv
-  p.o_KV = take(Fl * p.S_tot * 2 * (p.L - p.K) * d);
+  // (the tensor-core path keeps only the fp16 split K / V^T below)
+  p.o_KV = take(p.tc ? 256 : Fl * p.S_tot * 2 * (p.L - p.K) * d);
   p.o_Ht = take(Fl * (size_t)B * p.n_pos * d);
   p.o_QKVt = take(Fl * (size_t)B * p.n_pos * 3 * d);
   p.o_Hs = take(Fl * p.Rw * d);
@@ -435,11 +436,12 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.o_vlog = take(Fl * std::max(p.R[T], 1LL) * p.nb);
   p.o_hist = take(Fl * p.H * 3 * d * (size_t)(p.L - p.K));
   if (p.tc) {
-    p.o_VT = take(Fl * (size_t)(p.L - p.K) * d * p.vt_ld);
-    p.o_VTlo = take(Fl * (size_t)(p.L - p.K) * d * p.vt_ld);
-    p.o_KVlo = take(Fl * p.S_tot * 2 * (p.L - p.K) * d);
+    const size_t H2 = sizeof(__half);
+    p.o_VT = take(256);  // (unused on this path: V^T lives split below)
+    p.o_VTlo = take(H2 * 2 * (size_t)(p.L - p.K) * d * p.vt_ld);  // V^T fp16 hi, then lo
+    p.o_KVlo = take(H2 * 2 * p.S_tot * (p.L - p.K) * d);           // K fp16 hi, then lo
     p.o_XT = take(Fl * (size_t)d * p.vt_ld);
-    p.o_WT = take(Fl * (size_t)p.wt_floats * 2);  // tf32 hi parts, then lo parts
+    p.o_WT = take(H2 * (size_t)p.wt_floats * 2);  // K-major weights: fp16 hi, then lo
   }
   p.total = o;
   return GR4AD_OK;
@@ -515,24 +517,25 @@ struct RowSet {
 
 // K-major (out, in) copies of the weights for the tensor-core path
 struct LayerT {
-  const float *cq, *co, *sqkv, *so, *w1, *w2;
+  const __half *cq, *co, *sqkv, *so, *w1, *w2;
 };
 struct WeightsT {
-  const float *ctx, *kv, *wg, *wf, *hv;
-  const float *head[GR4AD_MAX_LEVELS];
+  const __half *ctx, *kv, *wg, *wf, *hv;
+  const __half *head[GR4AD_MAX_LEVELS];
   LayerT layer[GR4AD_MAX_LAYERS];
 };
 
 static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, WeightsT &wt,
                           cudaStream_t st) {
-  float *base = at<float>(ws, p.o_WT);
+  __half *base = at<__half>(ws, p.o_WT);
   long long o = 0;
   int rc = GR4AD_OK;
-  // dst (cols x rows) = src (rows x cols)^T
-  auto tr = [&](const float *src, int rows, int cols) -> const float * {
-    float *dst = base + o;
+  // dst (cols x rows) = kWeightScale * src (rows x cols)^T as fp16 hi, lo at + wt_floats
+  auto tr = [&](const float *src, int rows, int cols) -> const __half * {
+    __half *dst = base + o;
     o += ((long long)rows * cols + 63) / 64 * 64;
-    if (rc == GR4AD_OK) rc = transpose_split(src, cols, dst, dst + p.wt_floats, rows, rows, cols, st);
+    if (rc == GR4AD_OK)
+      rc = transpose_split16(src, cols, dst, dst + p.wt_floats, rows, rows, cols, kWeightScale, st);
     return dst;
   };
   const int d = p.d;
@@ -556,14 +559,15 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
 
 // C = epi(A (M x K) . W (K x N)); W in reference layout (ldb = N), WT its
 // K-major copy for the tensor-core path (a_rows = rows covered by A's map)
-static int dense(const Plan &p, const GemmArgs &g, const float *WT, long long a_rows, int epi,
+static int dense(const Plan &p, const GemmArgs &g, const __half *WT, long long a_rows, int epi,
                  cudaStream_t st) {
-  if (p.tc && WT && tc_eligible(g.lda, g.K, g.K, g.A, WT)) {
+  if (p.tc && WT && g.K % 8 == 0 && tc_eligible(g.lda, g.K, g.K, g.A, WT)) {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = g;
-    t.B = WT;
-    t.b_lo = WT + p.wt_floats;  // weights arrive pre-split (prep_weights_t)
+    t.b_hi = WT;  // weights arrive pre-split and scaled (prep_weights_t)
+    t.b_lo = WT + p.wt_floats;
     t.ldb = g.K;
+    t.alpha = g.alpha / kWeightScale;
     return gemm_tc(t, a_rows, g.K, g.N, g.K, epi, st);
   }
   return gemm(g, false, epi, st);
@@ -624,8 +628,13 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   if (p.tc && tc_eligible(qk.lda, qk.ldb, d, qk.A, qk.B)) {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = qk;
-    if (!trunk)  // head-layer K arrives pre-split from the encoder epilogue
-      t.b_lo = at<float>(ws, p.o_KVlo) + (size_t)(2 * (i - p.K)) * d;
+    if (!trunk) {  // head-layer K arrives split (fp16, scaled) from the encoder epilogue
+      const __half *k16 = at<__half>(ws, p.o_KVlo);
+      t.b_hi = k16 + (size_t)(i - p.K) * d;
+      t.b_lo = t.b_hi + (size_t)p.S_tot * nh * d;
+      t.ldb = (long long)nh * d;
+      t.alpha = qk.alpha / kKvScale;
+    }
     GR_TRY(gemm_tc(t, R, d, p.S_tot, d, EPI_STORE, st));
   } else {
     GR_TRY(gemm(qk, true, EPI_STORE, st));
@@ -639,8 +648,13 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   if (p.tc && VT) {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = pv;
-    t.B = trunk ? at<float>(ws, p.o_XT) : VT + (size_t)(i - p.K) * d * p.vt_ld;
-    if (!trunk) t.b_lo = at<float>(ws, p.o_VTlo) + (size_t)(i - p.K) * d * p.vt_ld;
+    t.B = at<float>(ws, p.o_XT);  // trunk: X^T, split on chip
+    if (!trunk) {  // head-layer V^T arrives split (fp16, scaled) from the encoder epilogue
+      const __half *v16 = at<__half>(ws, p.o_VTlo);
+      t.b_hi = v16 + (size_t)(i - p.K) * d * p.vt_ld;
+      t.b_lo = t.b_hi + (size_t)nh * d * p.vt_ld;
+      t.alpha = pv.alpha / kKvScale;
+    }
     t.ldb = p.vt_ld;
     GR_TRY(gemm_tc(t, R, p.sc_ld, d, p.vt_ld, EPI_STORE, st));
   } else {
@@ -720,14 +734,19 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
     if (p.tc && tc_eligible(g.lda, d, d, X, wt->kv)) {
       TcArgs t{};
       static_cast<GemmArgs &>(t) = g;
-      t.B = wt->kv + (size_t)2 * K * d * d;
-      t.b_lo = t.B + p.wt_floats;
+      t.b_hi = wt->kv + (size_t)2 * K * d * d;
+      t.b_lo = t.b_hi + p.wt_floats;
       t.ldb = d;
-      t.vt = VT;
+      t.alpha = g.alpha / kWeightScale;
+      __half *k16 = at<__half>(ws, p.o_KVlo), *v16 = at<__half>(ws, p.o_VTlo);
+      t.k_hi = k16;
+      t.k_lo = k16 + (size_t)p.S_tot * nh * d;
+      t.k_ld = (long long)nh * d;
+      t.vt_hi = v16;
+      t.vt_lo = v16 + (size_t)nh * d * p.vt_ld;
       t.vt_ld = p.vt_ld;
+      t.kv_scale = kKvScale;
       t.kv_d = d;
-      t.c_lo = at<float>(ws, p.o_KVlo);
-      t.vt_lo = at<float>(ws, p.o_VTlo);
       GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * nh * d, d, EPI_KV_SPLIT, st));
       if (K > 0) GR_TRY(transpose(X, d, at<float>(ws, p.o_XT), p.vt_ld, (int)p.S_tot, d, st));
     } else {

@@ -1500,17 +1500,28 @@ static __device__ __forceinline__ void logits_pass2(
         }
       }
     } else {
-      unsigned pm = 0;  // bit 4j + c: value c of n-tile j passed the exact window test
+      unsigned pm = 0;  // bit 4j + c: value c of n-tile j passed the pre-filter
 #pragma unroll
       for (int j = 0; j < kLG; ++j)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (z[j][c] > (c < 2 ? zA : zB)) {  // padded tiles are -inf
-            const RowScore &R = c < 2 ? A : B;
-            const float sc = R.cr + ((z[j][c] - R.M) - R.ls);
-            if (sbin(sc) <= (unsigned)wb) pm |= 1u << (4 * j + c);
-          }
+        for (int c = 0; c < 4; ++c)  // padded tiles are -inf
+          pm |= (z[j][c] > (c < 2 ? zA : zB) ? 1u : 0u) << (4 * j + c);
       if (__any_sync(kFull, pm != 0)) {
+        unsigned pre = pm;  // exact window test of the (rare) pre-passes
+        pm = 0;
+        while (pre) {
+          const int bit = __ffs(pre) - 1;
+          pre &= pre - 1;
+          float zz = z[0][0];
+#pragma unroll
+          for (int jj = 0; jj < kLG; ++jj)
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc)
+              if (4 * jj + cc == bit) zz = z[jj][cc];
+          const bool sb = (bit & 3) >= 2;
+          const float sc = (sb ? B.cr : A.cr) + ((zz - (sb ? B.M : A.M)) - (sb ? B.ls : A.ls));
+          if (sbin(sc) <= (unsigned)wb) pm |= 1u << bit;
+        }
         const unsigned np = __popc(pm);
         unsigned incl = np;
 #pragma unroll

@@ -1,14 +1,26 @@
-// tcgen05 3xTF32 GEMM (see gemm_tc.cu).
+// tcgen05 3xFP16 GEMM (see gemm_tc.cu).
 #pragma once
+#include <cuda_fp16.h>
+
 #include "gemm.cuh"
 
 namespace gr {
 
+// Power-of-two scales of the pre-split fp16 B operands (gemm_tc.cu): weights
+// (|w| < 32) and the encoder's K / V^T (|x| < 256) keep their fp16 lo parts in
+// the normal range; the GEMM's alpha carries the inverse.
+constexpr float kWeightScale = 2048.f;
+constexpr float kKvScale = 256.f;
+
 struct TcArgs : GemmArgs {
-  const float *b_lo;  // optional: B pre-split, B holds tf32 hi parts and b_lo the rests
-  float *vt;         // EPI_KV_SPLIT: V^T destination (L*d rows, vt_ld columns)
-  float *c_lo, *vt_lo;  // EPI_KV_SPLIT: when set, C / V^T get tf32 hi parts, these the rests
-  long long vt_ld;
+  // optional: B pre-split, s.B = b_hi + b_lo (fp16, K-major, ld = ldb);
+  // otherwise B (fp32) is split on chip, unscaled
+  const __half *b_hi, *b_lo;
+  // EPI_KV_SPLIT: the K part of layer i -> k_hi / k_lo [row][k_ld] at column
+  // i d, the V part -> vt_hi / vt_lo [i d + c][vt_ld], all kv_scale * x
+  __half *k_hi, *k_lo, *vt_hi, *vt_lo;
+  long long k_ld, vt_ld;
+  float kv_scale;
   int kv_d;
 };
 
@@ -21,8 +33,8 @@ bool tc_eligible(long long lda, long long ldb, int K, const void *A, const void 
 // dst (cols x rows) = src (rows x cols)^T, both row-major with the given lds
 int transpose(const float *src, long long lds, float *dst, long long ldd, int rows, int cols,
               cudaStream_t st);
-// as transpose, writing the tf32 split of every element: dst_hi + dst_lo == src^T exactly
-int transpose_split(const float *src, long long lds, float *dst_hi, float *dst_lo, long long ldd,
-                    int rows, int cols, cudaStream_t st);
+// as transpose, writing the fp16 split of scale * src^T: dst_hi + dst_lo
+int transpose_split16(const float *src, long long lds, __half *dst_hi, __half *dst_lo,
+                      long long ldd, int rows, int cols, float scale, cudaStream_t st);
 
 }  // namespace gr

@@ -720,11 +720,34 @@ int transpose(const float *src, long long lds, float *dst, long long ldd, int ro
   return GR4AD_OK;
 }
 
-int transpose_split(const float *src, long long lds, float *dst_hi, float *dst_lo, long long ldd,
-                    int rows, int cols, cudaStream_t st) {
+// dst = split of scale * src^T into fp16 hi + lo (the tensor-core B operands)
+__global__ void transpose_split16_kernel(const float *__restrict__ src, long long lds,
+                                         __half *dst_hi, __half *dst_lo, long long ldd, int rows,
+                                         int cols, float scale) {
+  __shared__ float tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    int r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = src[(long long)r * lds + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    int c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) {
+      const float x = tile[threadIdx.x][i] * scale;
+      const __half h = __float2half_rn(x);
+      dst_hi[(long long)c * ldd + r] = h;
+      dst_lo[(long long)c * ldd + r] = __float2half_rn(x - __half2float(h));
+    }
+  }
+}
+
+int transpose_split16(const float *src, long long lds, __half *dst_hi, __half *dst_lo,
+                      long long ldd, int rows, int cols, float scale, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return GR4AD_OK;
   dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32));
-  GR_LAUNCH(KC_SMALL, st, transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, lds, dst_hi, dst_lo, ldd, rows, cols));
+  GR_LAUNCH(KC_SMALL, st, transpose_split16_kernel<<<grid, dim3(32, 8), 0, st>>>(
+                              src, lds, dst_hi, dst_lo, ldd, rows, cols, scale));
   return GR4AD_OK;
 }
 
