@@ -327,8 +327,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else {
-    // ---- epilogue: TMEM -> registers -> global
+    // ---- epilogue: TMEM -> registers -> smem (transpose) -> coalesced global
+    // A lane owns a row after tcgen05.ld; each 32-column chunk is staged
+    // through a padded per-warp buffer so that global traffic (C, R, bias,
+    // gate, K) runs with lanes along columns: one 128-B line per access.
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    float *ebuf = reinterpret_cast<float *>(smem + STAGES * STAGE_BYTES + 256) +
+                  (warp - kEpiWarp0) * 32 * 33;
     int j = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN);
@@ -336,83 +341,86 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int acc = j & 1;
       mbar_wait(&accf[acc], (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int r = ti.m0 + q * 32 + lane;
-      const long long grow = (long long)ti.row_base + r;
+      const int rbase = ti.m0 + q * 32;  // this warp's 32 rows
+      const int nrows = min(32, ti.M - rbase);
       const int N = ti.N;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
         const int col0 = ti.n0 + c * 32;
-        if (r >= ti.M || col0 >= N) continue;
-        if (EPI == EPI_KV_SPLIT && a.kv_d % 32 != 0) {  // general d: element by element
-          for (int jj = 0; jj < 32 && col0 + jj < N; ++jj) {
+        if (nrows <= 0 || col0 >= N) continue;  // warp-uniform
+        if (EPI == EPI_KV_SPLIT) {
+          // [2i d, 2i d + d) -> K_i, [2i d + d, 2(i+1) d) -> V_i^T, both as fp16
+          // hi / lo of kv_scale * x for the attention GEMMs; V^T is written
+          // straight from the row-per-lane registers (coalesced over rows)
+          const long long grow = (long long)ti.row_base + rbase + lane;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
             const int col = col0 + jj, layer = col / (2 * a.kv_d), w = col - layer * 2 * a.kv_d;
-            const float x = v[jj] * a.alpha * a.kv_scale;
-            const __half h = __float2half_rn(x);
-            const __half l = __float2half_rn(x - __half2float(h));
-            if (w < a.kv_d) {
-              const long long o = grow * a.k_ld + (long long)layer * a.kv_d + w;
-              a.k_hi[o] = h;
-              a.k_lo[o] = l;
-            } else {
+            if (col < N && w >= a.kv_d && lane < nrows) {
+              const float x = v[jj] * a.alpha * a.kv_scale;
+              const __half h = __float2half_rn(x);
               const long long o = ((long long)layer * a.kv_d + (w - a.kv_d)) * a.vt_ld + grow;
               a.vt_hi[o] = h;
-              a.vt_lo[o] = l;
+              a.vt_lo[o] = __float2half_rn(x - __half2float(h));
             }
           }
-          continue;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) ebuf[lane * 33 + jj] = v[jj];
+        __syncwarp();
+        const int col = col0 + lane;
+        const bool cok = col < N;
+        float bcol = 0.f;
+        if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID)
+          bcol = cok ? a.bias[col] : 0.f;
+        int kv_layer = 0, kv_w = 0;
+        if (EPI == EPI_KV_SPLIT) {
+          kv_layer = col / (2 * a.kv_d);
+          kv_w = col - kv_layer * 2 * a.kv_d;
         }
         if (EPI == EPI_KV_SPLIT) {
-          // [2i d, 2i d + d) -> K_i, [2i d + d, 2(i+1) d) -> V_i^T: both stored
-          // as fp16 hi / lo of kv_scale * x for the attention GEMMs (a 32-column
-          // chunk never straddles the halves: d % 32 == 0)
-          const int layer = col0 / (2 * a.kv_d), w0 = col0 - layer * 2 * a.kv_d;
-          uint32_t hi[16], lo[16];
-#pragma unroll
-          for (int jj = 0; jj < 32; jj += 2)
-            split_f16x2(v[jj] * a.alpha, v[jj + 1] * a.alpha, a.kv_scale, hi[jj / 2], lo[jj / 2]);
-          if (w0 < a.kv_d) {
-            const long long o = grow * a.k_ld + (long long)layer * a.kv_d + w0;
-            uint4 *kh = reinterpret_cast<uint4 *>(a.k_hi + o), *kl = reinterpret_cast<uint4 *>(a.k_lo + o);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              kh[u] = make_uint4(hi[4 * u], hi[4 * u + 1], hi[4 * u + 2], hi[4 * u + 3]);
-              kl[u] = make_uint4(lo[4 * u], lo[4 * u + 1], lo[4 * u + 2], lo[4 * u + 3]);
-            }
-          } else {
-            const __half *hh = reinterpret_cast<const __half *>(hi);
-            const __half *ll = reinterpret_cast<const __half *>(lo);
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {  // coalesced over rows
-              const long long o = ((long long)layer * a.kv_d + (w0 - a.kv_d) + jj) * a.vt_ld + grow;
-              a.vt_hi[o] = hh[jj];
-              a.vt_lo[o] = ll[jj];
+          if (cok && kv_w < a.kv_d) {
+#pragma unroll 4
+            for (int rr = 0; rr < nrows; ++rr) {
+              const long long grow = (long long)ti.row_base + rbase + rr;
+              const float x = ebuf[rr * 33 + lane] * a.alpha * a.kv_scale;
+              const __half h = __float2half_rn(x);
+              const long long o = grow * a.k_ld + (long long)kv_layer * a.kv_d + kv_w;
+              a.k_hi[o] = h;
+              a.k_lo[o] = __float2half_rn(x - __half2float(h));
             }
           }
-          continue;
-        }
+        } else if (cok) {
+          // operands first (32 independent loads in flight; C may alias R),
+          // then the stores
+          float xv[32];
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          const int col = col0 + jj;
-          float x = v[jj] * a.alpha;
-          if (col < N) {
-            if (EPI == EPI_BIAS) x = x + a.bias[col];
-            else if (EPI == EPI_BIAS_GELU) x = gelu_tanh(x + a.bias[col]);
-            else if (EPI == EPI_RESID) x = a.R[grow * a.ldr + col] + x;
-            else if (EPI == EPI_BIAS_RESID) x = a.R[grow * a.ldr + col] + (x + a.bias[col]);
-            else if (EPI == EPI_MULVEC) x = a.vec[(long long)a.row_req[grow] * a.vec_ld + col] * x;
+          for (int rr = 0; rr < 32; ++rr) {
+            const long long grow = (long long)ti.row_base + rbase + rr;
+            float o = 0.f;
+            if (rr < nrows) {
+              if (EPI == EPI_RESID || EPI == EPI_BIAS_RESID) o = a.R[grow * a.ldr + col];
+              else if (EPI == EPI_MULVEC) o = a.vec[(long long)a.row_req[grow] * a.vec_ld + col];
+            }
+            xv[rr] = o;
           }
-          v[jj] = x;
-        }
-        float *crow = a.C + grow * a.ldc + col0;
-        if (col0 + 32 <= N && (a.ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(crow) % 16) == 0) {
 #pragma unroll
-          for (int jj = 0; jj < 32; jj += 4)
-            *reinterpret_cast<float4 *>(crow + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
-        } else {
-          for (int jj = 0; jj < 32 && col0 + jj < N; ++jj) crow[jj] = v[jj];
+          for (int rr = 0; rr < 32; ++rr) {
+            if (rr < nrows) {
+              const long long grow = (long long)ti.row_base + rbase + rr;
+              float x = ebuf[rr * 33 + lane] * a.alpha;
+              if (EPI == EPI_BIAS) x = x + bcol;
+              else if (EPI == EPI_BIAS_GELU) x = gelu_tanh(x + bcol);
+              else if (EPI == EPI_RESID) x = xv[rr] + x;
+              else if (EPI == EPI_BIAS_RESID) x = xv[rr] + (x + bcol);
+              else if (EPI == EPI_MULVEC) x = xv[rr] * x;
+              a.C[grow * a.ldc + col] = x;
+            }
+          }
         }
+        __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -475,7 +483,7 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
                      const TcArgs &a, int epi, cudaStream_t st) {
   constexpr size_t stage = (size_t)BM * BK * 4 + (BSPLIT ? 0 : (size_t)BN * BK * 4) +
                            2 * (size_t)BM * BK * 2 + 2 * (size_t)BN * BK * 2;
-  constexpr size_t smem = 1024 + STAGES * stage + 256;
+  constexpr size_t smem = 1024 + STAGES * stage + 256 + 4 * 32 * 33 * sizeof(float);
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
   const int n_tiles = tiles_m * tiles_n * a.groups;
