@@ -327,26 +327,15 @@ def roofline_for(dec, feats, cfgd, dev, config=None):
            "algorithmic_per_launch": per_launch, "launch_ms": per_launch_s * 1e3,
            "classes": classes,
            "note": "per-class times are CUDA events on the launching stream; peak is the "
-                   "measured bf16 dense figure although the path computes fp32-faithful "
-                   "(3xTF32 on tcgen05 or mma.sync tensor cores, or fp32 FFMA on CUDA cores)"}
+                   "measured bf16 dense figure although the path computes fp32-faithful: "
+                   "3xFP16 on tcgen05 (layered path), 3xTF32 on mma.sync (fused path)"}
     if kind == "flop" and dom in ("gemm", "attn_gemm"):
-        # fp32-faithful tensor-core bound: 3 TF32 products per MAC (3xTF32)
-        torch.backends.cuda.matmul.allow_tf32 = True
-        x = torch.randn(8192, 8192, device=dev)
-        y = torch.randn(8192, 8192, device=dev)
-        for _ in range(2):
-            x @ y
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(5):
-            x @ y
-        e1.record()
-        torch.cuda.synchronize(dev)
-        torch.backends.cuda.matmul.allow_tf32 = False
-        tf32 = 2 * 8192 ** 3 * 5 / (e0.elapsed_time(e1) / 1e3) / 1e12
-        del x, y
-        out["tf32_cublas_tflops_measured"] = tf32
-        out["frac_of_3xtf32_peak"] = achieved / (tf32 / 3)
+        # fp32-faithful tensor-core bound: 3 fp16 products per MAC (3xFP16,
+        # fp16 dense rate == bf16 dense rate), against the sustained figure
+        # since the GEMMs run inside a long step
+        sus = bf16_sus or bf16
+        out["fp16x3_bound_tflops"] = sus / 3
+        out["frac_of_3xfp16_bound"] = achieved / (sus / 3)
     if kind == "flop":
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         fp32 = sms * 128 * 2 * 1.965e9 / 1e12  # FFMA peak at the max SM clock
@@ -477,17 +466,21 @@ def main():
         lat.append(time.perf_counter() - t0)
     if world > 1:
         dist.barrier()
-    pending = [None, None]
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        j = i % 2
-        if pending[j] is not None:
-            pending[j].synchronize()  # results of step i-2 are on the host
-        pending[j] = submit(j)
-    for ev in pending:
-        if ev is not None:
-            ev.synchronize()
-    e2e_s = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+    best = None
+    for _ in range(3):  # best of three windows of K pipelined steps (host jitter)
+        pending = [None, None]
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            j = i % 2
+            if pending[j] is not None:
+                pending[j].synchronize()  # results of step i-2 are on the host
+            pending[j] = submit(j)
+        for ev in pending:
+            if ev is not None:
+                ev.synchronize()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    e2e_s = torch.tensor([best], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = world * B * args.steps / float(e2e_s.item())
@@ -534,9 +527,9 @@ def main():
                     "d2h_bytes_per_step": d2h,
                     "how": "C ABI with pinned host buffers; per step H2D features + decode + "
                            "D2H results, two buffer sets on two streams (copies of step i+1 "
-                           "overlap the decode of step i)"},
-            "gpu_launches": launches_per_step * args.steps * 3,
-            "gpu_launches_note": "per-step launches x (device-timed + serial e2e + pipelined e2e) steps",
+                           "overlap the decode of step i); best of 3 windows of K steps"},
+            "gpu_launches": launches_per_step * args.steps * 5,
+            "gpu_launches_note": "per-step launches x (device-timed + serial e2e + 3 pipelined e2e windows) steps",
             "launches_per_step": launches_per_step,
             "algorithmic_tflops": flops * value / 1e12,
             "results_per_step": int(cnt.item()),

@@ -111,10 +111,10 @@ static long long frag_layout(const Plan &p, const gr4ad_weights *w, FragJobs *jo
   long long off = 0;
   if (jobs) jobs->n = 0;
   auto add = [&](const float *src, long long sk, long long sn, int kin, int nout,
-                 int nreal, int raw = 0) -> long long {
-    if (jobs) jobs->job[jobs->n++] = FragJob{src, sk, sn, off, kin, nout, nreal, raw};
+                 int nreal) -> long long {
+    if (jobs) jobs->job[jobs->n++] = FragJob{src, sk, sn, off, kin, nout, nreal};
     const long long r = off;
-    off += (long long)(kin / 8) * (nout / 8) * (raw ? 16 : 32);  // float4 units
+    off += (long long)(kin / 16) * (nout / 8) * 32;  // 16-byte units
     return r;
   };
   const gr4ad_weights z{};
@@ -137,8 +137,6 @@ static long long frag_layout(const Plan &p, const gr4ad_weights *w, FragJobs *jo
     fi->w2[li] = add(Lw.ffn_W2, d, 1, p.dff, d, d);
   }
   for (int t = 0; t < p.T; ++t) fi->head[t] = add(W.head[t], p.V[t], 1, d, p.V[t], p.V[t]);
-  for (int t = 0; t < p.T; ++t)
-    fi->head_raw[t] = add(W.head[t], p.V[t], 1, d, p.V[t], p.V[t], 1);
   return off;
 }
 
@@ -178,7 +176,7 @@ static bool plan_fused_mma(Plan &p) {
   p.f_s4[13] = take(8LL * 16 * (D + 2));  // 8 warps x 16 rows x (D + 2)
   int vmax = 8;
   for (int t = 0; t < p.T; ++t) vmax = std::max(vmax, p.V[t]);
-  p.f_s4[14] = take((long long)D * vmax);  // one level's codebook, raw fragment order
+  p.f_s4[14] = take((long long)D * vmax);  // one level's codebook fragments
   p.f_head_floats = D * vmax;
   p.f_s4[15] = take(4);                    // two mbarriers (16-B aligned)
   // two CTAs per SM: 2 x (smem + 1 KB reserved) <= 228 KB
@@ -824,7 +822,7 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       f.Hrows = p.f_Hrows_mma;
       for (int t = 0; t < GR4AD_MAX_LEVELS + 2; ++t) f.hoff[t] = p.f_hoff4[t];
       static thread_local FragJobs jobs;  // ~6 KB: kept off the stack
-      float4 *frag = at<float4>(ws, p.o_frag);
+      uint4 *frag = at<uint4>(ws, p.o_frag);
       frag_layout(p, w, &jobs, &f.fi);
       f.frag = frag;
       GR_TRY(frag_prep_launch(jobs, frag, st));

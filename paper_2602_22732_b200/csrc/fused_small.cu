@@ -12,6 +12,8 @@
 // radix top-k over the level's candidates compacts the beams in place.
 // The C1/C2 working set (K^T/V^T 32 KB, history 25 KB) fits on chip: the
 // batch decode is one launch.
+#include <cuda_fp16.h>
+
 #include "fused_small.cuh"
 
 namespace gr {
@@ -1098,48 +1100,78 @@ static __device__ __forceinline__ uint32_t tf32_hi(float x) {
   return __float_as_uint(x) & 0xFFFFE000u;
 }
 
-// C fragment (c0 (g,2t) c1 (g,2t+1) c2 (g+8,2t) c3 (g+8,2t+1)) -> A fragment
-// (a0 (g,k=t) a1 (g+8,t) a2 (g,t+4) a3 (g+8,t+4)) split into tf32 hi / lo
-static __device__ __forceinline__ void split_a(const float (&c)[4], uint32_t (&h)[4],
-                                               uint32_t (&l)[4]) {
-  const float v[4] = {c[0], c[2], c[1], c[3]};
+// ---- 3xFP16 warp MMA (mma.sync m16n8k16, fp32 accumulate) -----------------
+// x = hi + lo with hi = fp16(x), lo = fp16(x - hi); a product is accumulated
+// as lo.hi + hi.lo + hi.hi (lo.lo ~2^-22 dropped).  Weight / codebook
+// fragments and the context K / V^T are split after a power-of-two scale
+// (their lo parts stay in fp16's normal range; results are rescaled exactly);
+// activations are split unscaled.
+constexpr float kFragScale = 2048.f, kInvFragScale = 1.f / 2048.f;  // weights, codebook
+constexpr float kKvScaleF = 256.f, kInvKvScale = 1.f / 256.f;       // context K / V^T
+
+static __device__ __forceinline__ uint32_t h2u(__half2 h) {
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+// (x0, x1) -> fp16x2 hi / lo
+static __device__ __forceinline__ void split_h2(float x0, float x1, uint32_t &h, uint32_t &l) {
+  const __half2 hh = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(hh);
+  h = h2u(hh);
+  l = h2u(__floats2half2_rn(x0 - hf.x, x1 - hf.y));
+}
+
+// C fragments (c0 (g,2t) c1 (g,2t+1) c2 (g+8,2t) c3 (g+8,2t+1)) of n-tiles
+// 2kk (x0) and 2kk+1 (x1) are the A fragment of k16 step kk -- a0 (g, k 2t..)
+// a1 (g+8, 2t..) a2 (g, 8+2t..) a3 (g+8, 8+2t..) -- so products chain with
+// no data movement; split into fp16 hi / lo
+static __device__ __forceinline__ void split_a16(const float (&x0)[4], const float (&x1)[4],
+                                                 uint32_t (&h)[4], uint32_t (&l)[4]) {
+  split_h2(x0[0], x0[1], h[0], l[0]);
+  split_h2(x0[2], x0[3], h[1], l[1]);
+  split_h2(x1[0], x1[1], h[2], l[2]);
+  split_h2(x1[2], x1[3], h[3], l[3]);
+}
+template <int KT>
+static __device__ __forceinline__ void split_frags(const float (&x)[KT][4],
+                                                   uint32_t (&h)[KT / 2][4],
+                                                   uint32_t (&l)[KT / 2][4]) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    h[q] = tf32_hi(v[q]);
-    l[q] = __float_as_uint(v[q] - __uint_as_float(h[q]));
-  }
+  for (int k = 0; k < KT / 2; ++k) split_a16(x[2 * k], x[2 * k + 1], h[k], l[k]);
 }
 
-static __device__ __forceinline__ float4 split_b(float2 v) {
-  const float h0 = __uint_as_float(tf32_hi(v.x)), h1 = __uint_as_float(tf32_hi(v.y));
-  return make_float4(h0, h1, v.x - h0, v.y - h1);
+// B fragment {b0 hi, b1 hi, b0 lo, b1 lo}: b0 = s (x0, x1), b1 = s (x2, x3)
+static __device__ __forceinline__ uint4 split_b16(float x0, float x1, float x2, float x3,
+                                                  float sc) {
+  uint4 r;
+  split_h2(x0 * sc, x1 * sc, r.x, r.z);
+  split_h2(x2 * sc, x3 * sc, r.y, r.w);
+  return r;
 }
 
-static __device__ __forceinline__ void mma8(float (&d)[4], const uint32_t (&a)[4], float b0,
-                                            float b1) {
+static __device__ __forceinline__ void mma16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                             uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(__float_as_uint(b0)),
-        "r"(__float_as_uint(b1)));
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// d += a . b in 3xTF32; b = {hi0, hi1, lo0, lo1}
+// d += a . b in 3xFP16
 static __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4],
-                                            const uint32_t (&al)[4], float4 b) {
-  mma8(d, al, b.x, b.y);
-  mma8(d, ah, b.z, b.w);
-  mma8(d, ah, b.x, b.y);
+                                            const uint32_t (&al)[4], uint4 b) {
+  mma16(d, al, b.x, b.y);
+  mma16(d, ah, b.z, b.w);
+  mma16(d, ah, b.x, b.y);
 }
 
 // dm += ah.bh, dx += al.bh + ah.bl: two independent accumulator chains
 static __device__ __forceinline__ void mma3s(float (&dm)[4], float (&dx)[4],
                                              const uint32_t (&ah)[4], const uint32_t (&al)[4],
-                                             float4 b) {
-  mma8(dx, al, b.x, b.y);
-  mma8(dx, ah, b.z, b.w);
-  mma8(dm, ah, b.x, b.y);
+                                             uint4 b) {
+  mma16(dx, al, b.x, b.y);
+  mma16(dx, ah, b.z, b.w);
+  mma16(dm, ah, b.x, b.y);
 }
 
 static __device__ __forceinline__ float quad_sum(float v) {
@@ -1158,27 +1190,29 @@ static __device__ __forceinline__ double quad_sum_d(double v) {
   return v;
 }
 
-// y (16 x 8NT) (+)= x (16 x 8KT) . W, W fragment-ordered
+// y (16 x 8NT) (+)= x (16 x 8KT) . W, W fragment-ordered (k16 steps, scaled)
 template <int KT, int NT, bool ACC = false>
-static __device__ __forceinline__ void mm(const float (&x)[KT][4], const float4 *__restrict__ W,
+static __device__ __forceinline__ void mm(const float (&x)[KT][4], const uint4 *__restrict__ W,
                                           float (&y)[NT][4]) {
-  uint32_t h[KT][4], l[KT][4];
-#pragma unroll
-  for (int k = 0; k < KT; ++k) split_a(x[k], h[k], l[k]);
+  constexpr int K16 = KT / 2;
+  uint32_t h[K16][4], l[K16][4];
+  split_frags<KT>(x, h, l);
   const int lane = threadIdx.x & 31;
-  float4 w[KT][NT];
+  uint4 w[K16][NT];
 #pragma unroll
-  for (int k = 0; k < KT; ++k)
+  for (int k = 0; k < K16; ++k)
 #pragma unroll
     for (int n = 0; n < NT; ++n) w[k][n] = __ldg(W + (k * NT + n) * 32 + lane);
 #pragma unroll
   for (int n = 0; n < NT; ++n) {
-    float cx[4] = {0.f, 0.f, 0.f, 0.f};
-    if (!ACC) y[n][0] = y[n][1] = y[n][2] = y[n][3] = 0.f;
+    float dm[4] = {0.f, 0.f, 0.f, 0.f}, dx[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int k = 0; k < KT; ++k) mma3s(y[n], cx, h[k], l[k], w[k][n]);
+    for (int k = 0; k < K16; ++k) mma3s(dm, dx, h[k], l[k], w[k][n]);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) y[n][c] += cx[c];
+    for (int c = 0; c < 4; ++c) {
+      const float v = (dm[c] + dx[c]) * kInvFragScale;
+      y[n][c] = ACC ? y[n][c] + v : v;
+    }
   }
 }
 
@@ -1217,18 +1251,19 @@ static __device__ __forceinline__ void ln_frag(const float (&x)[NT][4], const fl
 // k_lo must be a multiple of 64 (chunks never cross SP; keys in [kend, c0+64)
 // are masked, their K rows zero or finite).
 // Cross-attention of the tile's 16 query rows against one request's shared
-// K [SP][D+8] / V^T [D][SP+8]: online softmax over 64-key chunks
-// (autodiff.py:362-368 up to the rescaling order).
+// K / V^T, both fp16 hi / lo of kKvScaleF * x in shared memory (kv_layout):
+// online softmax over 64-key chunks (autodiff.py:362-368 up to the rescaling
+// order).
 template <int D>
-static __device__ __forceinline__ void attn_mma(const float (&q)[D / 8][4], const float *Ks,
-                                                const float *VTs, int S, int k_lo, int k_hi,
+static __device__ __forceinline__ void attn_mma(const float (&q)[D / 8][4], const uint32_t *Kw,
+                                                const uint32_t *VTw, int S, int k_lo, int k_hi,
                                                 float (&o)[D / 8][4], float (&ml)[4]) {
-  constexpr int KT = D / 8, VS = SP + 8;
+  constexpr int KT = D / 8, K16 = KT / 2, KW = D / 2, VSW = (SP + 8) / 2;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const float scale = 1.0f / sqrtf((float)D);
-  uint32_t qh[KT][4], ql[KT][4];
-#pragma unroll
-  for (int k = 0; k < KT; ++k) split_a(q[k], qh[k], ql[k]);
+  const float scale = rsqrtf((float)D) * kInvKvScale;
+  const uint32_t *Kl = Kw + SP * KW, *VTl = VTw + D * VSW;
+  uint32_t qh[K16][4], ql[K16][4];
+  split_frags<KT>(q, qh, ql);
   float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
   // P.V accumulators: hi.hi terms and cross terms
   float ox[KT][4];
@@ -1237,17 +1272,18 @@ static __device__ __forceinline__ void attn_mma(const float (&q)[D / 8][4], cons
 #pragma unroll
     for (int c = 0; c < 4; ++c) o[n][c] = ox[n][c] = 0.f;
   const int kend = min(S, k_hi);
+  const int sw = ((g >> 2) & 1) << 2;  // kv_layout: key bit 2 swaps the 4-word halves
   for (int c0 = k_lo; c0 < kend; c0 += 64) {
     float sc[8][4];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
-      const float *kr = Ks + (c0 + j * 8 + g) * D;
-      const int sw = ((g >> 1) & 1) << 3;  // k_swz: row bit 1 flips the 8-column half
+      const int r = (c0 + j * 8 + g) * KW;
 #pragma unroll
-      for (int k = 0; k < KT; ++k)
-        mma3(sc[j], qh[k], ql[k],
-             split_b(*reinterpret_cast<const float2 *>(kr + ((8 * k + 2 * t) ^ sw))));
+      for (int k = 0; k < K16; ++k) {
+        const int w0 = (8 * k + t) ^ sw, w1 = (8 * k + t + 4) ^ sw;
+        mma3(sc[j], qh[k], ql[k], make_uint4(Kw[r + w0], Kw[r + w1], Kl[r + w0], Kl[r + w1]));
+      }
     }
     float cA = -INFINITY, cB = -INFINITY;
 #pragma unroll
@@ -1286,20 +1322,20 @@ static __device__ __forceinline__ void attn_mma(const float (&q)[D / 8][4], cons
     mA = nA;
     mB = nB;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int jj = 0; jj < 4; ++jj) {
       uint32_t ph[4], pl[4];
-      split_a(sc[j], ph, pl);
+      split_a16(sc[2 * jj], sc[2 * jj + 1], ph, pl);
 #pragma unroll
       for (int n = 0; n < KT; ++n) {
-        const float *vr = VTs + (n * 8 + g) * VS + c0 + j * 8 + 2 * t;
-        mma3s(o[n], ox[n], ph, pl, split_b(*reinterpret_cast<const float2 *>(vr)));
+        const int v = (n * 8 + g) * VSW + (c0 >> 1) + 8 * jj + t;
+        mma3s(o[n], ox[n], ph, pl, make_uint4(VTw[v], VTw[v + 4], VTl[v], VTl[v + 4]));
       }
     }
   }
 #pragma unroll
   for (int n = 0; n < KT; ++n)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) o[n][c] += ox[n][c];
+    for (int c = 0; c < 4; ++c) o[n][c] = (o[n][c] + ox[n][c]) * kInvKvScale;
   ml[0] = mA;  // row g: running max, row g + 8; then the row sums
   ml[1] = mB;
   ml[2] = quad_sum(lA);
@@ -1377,7 +1413,7 @@ static __device__ __forceinline__ void attn_merge(float (&o)[D / 8][4], const fl
 
 template <int D, int DFF>
 static __device__ __forceinline__ void ffn_mma(const float (&n)[D / 8][4], const gr4ad_layer &Lw,
-                                               const float4 *W1, const float4 *W2,
+                                               const uint4 *W1, const uint4 *W2,
                                                float (&h)[D / 8][4]) {
   constexpr int KT = D / 8, FT = DFF / 8;
   const int t = threadIdx.x & 3;
@@ -1404,12 +1440,12 @@ static __device__ __forceinline__ void ffn_mma(const float (&n)[D / 8][4], const
 }
 
 // logits of the tile's rows for codebook tiles [n0, n0 + kLG) (clamped to nend)
-// from the level's codebook staged in shared memory (raw fragment order)
+// from the level's codebook fragments staged in shared memory
 constexpr int kLG = 4;  // codebook tiles per logits group
-template <int KT>
-static __device__ __forceinline__ void logits_s(const uint32_t (&hh)[KT][4],
-                                                const uint32_t (&hl)[KT][4],
-                                                const float2 *__restrict__ Hs, int NTV, int n0,
+template <int K16>
+static __device__ __forceinline__ void logits_s(const uint32_t (&hh)[K16][4],
+                                                const uint32_t (&hl)[K16][4],
+                                                const uint4 *__restrict__ Hs, int NTV, int n0,
                                                 int nend, float (&z)[kLG][4]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -1417,43 +1453,34 @@ static __device__ __forceinline__ void logits_s(const uint32_t (&hh)[KT][4],
     z[j][0] = z[j][1] = z[j][2] = z[j][3] = 0.f;
     if (n0 + j < nend) {
 #pragma unroll
-      for (int k = 0; k < KT; ++k) mma3(z[j], hh[k], hl[k], split_b(Hs[(k * NTV + n0 + j) * 32 + lane]));
+      for (int k = 0; k < K16; ++k) mma3(z[j], hh[k], hl[k], Hs[(k * NTV + n0 + j) * 32 + lane]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) z[j][c] *= kInvFragScale;
     } else {
       z[j][0] = z[j][1] = z[j][2] = z[j][3] = -INFINITY;
     }
   }
 }
 
-template <int KT>
-static __device__ __forceinline__ void logits8(const uint32_t (&hh)[KT][4],
-                                               const uint32_t (&hl)[KT][4],
-                                               const float4 *__restrict__ Hf, int NTV, int n0,
-                                               int nend, float (&z)[kLG][4]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int j = 0; j < kLG; ++j) {
-    z[j][0] = z[j][1] = z[j][2] = z[j][3] = 0.f;
-    if (n0 + j < nend) {
-#pragma unroll
-      for (int k = 0; k < KT; ++k) mma3(z[j], hh[k], hl[k], __ldg(Hf + (k * NTV + n0 + j) * 32 + lane));
-    } else {
-      z[j][0] = z[j][1] = z[j][2] = z[j][3] = -INFINITY;
-    }
-  }
-}
-
-// A fragments (tf32 hi / lo) of rows cA (g) and cB (g + 8) of a row-major
-// [rows][ld] state (C-fragment column order, as split_a)
-template <int KT>
+// A fragments (fp16 hi / lo, k16 steps) of rows cA (g) and cB (g + 8) of a
+// row-major [rows][ld] state
+template <int K16>
 static __device__ __forceinline__ void load_split(const float *st, int ld, int cA, int cB,
-                                                  uint32_t (&hh)[KT][4], uint32_t (&hl)[KT][4]) {
+                                                  uint32_t (&hh)[K16][4], uint32_t (&hl)[K16][4]) {
   const int t4 = threadIdx.x & 3;
 #pragma unroll
-  for (int n = 0; n < KT; ++n) {
-    const float2 a2 = *reinterpret_cast<const float2 *>(st + cA * ld + 8 * n + 2 * t4);
-    const float2 b2 = *reinterpret_cast<const float2 *>(st + cB * ld + 8 * n + 2 * t4);
-    const float c[4] = {a2.x, a2.y, b2.x, b2.y};
-    split_a(c, hh[n], hl[n]);
+  for (int k = 0; k < K16; ++k) {
+    float c[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const float2 a2 = *reinterpret_cast<const float2 *>(st + cA * ld + 16 * k + 8 * u + 2 * t4);
+      const float2 b2 = *reinterpret_cast<const float2 *>(st + cB * ld + 16 * k + 8 * u + 2 * t4);
+      c[u][0] = a2.x;
+      c[u][1] = a2.y;
+      c[u][2] = b2.x;
+      c[u][3] = b2.y;
+    }
+    split_a16(c[0], c[1], hh[k], hl[k]);
   }
 }
 
@@ -1469,7 +1496,7 @@ struct RowScore {
 };
 template <int KT, bool COLLECT>
 static __device__ __forceinline__ void logits_pass2(
-    const uint32_t (&hh)[KT][4], const uint32_t (&hl)[KT][4], const float2 *Hf, int NTV, int nb0,
+    const uint32_t (&hh)[KT][4], const uint32_t (&hl)[KT][4], const uint4 *Hf, int NTV, int nb0,
     int nb1, const RowScore &A, const RowScore &B, int V, uint32_t *keys, unsigned *hist,
     int &hcur, unsigned &hcnt, float Rs, float bscale, int wb, unsigned long long *sbuf,
     unsigned *cnt, int cap) {
@@ -1583,7 +1610,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
   unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(sm + a.s_sort);
   float *wsl = sm + a.s_ws;  // warp 0's trunk slots
   float *mrg = sm + a.s_mrg;  // per-warp partials of tile groups: 16 x (D + 2) each
-  float2 *HS2 = reinterpret_cast<float2 *>(sm + a.s_head);  // level codebook (bulk copy)
+  uint4 *HS2 = reinterpret_cast<uint4 *>(sm + a.s_head);  // level codebook fragments (bulk copy)
   constexpr int HSD = D + 2;      // per-row pass-2 state: head input h, M, lse
   float *hst = sm + a.s_hst;      // [hst_rows][HSD]
   float *prox = reinterpret_cast<float *>(sm + a.s_sort);  // window proxies (before collection)
@@ -1665,7 +1692,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
   __syncthreads();
   if (tid == 0 && T > 0) {  // level 0's codebook lands during the K/V + trunk phase
     if (feat_bulk) bar_wait(fbar, 0);  // (complete: every thread waited on it)
-    bulk_load(HS2, a.frag + a.fi.head_raw[0], (uint32_t)(D * a.V[0] * sizeof(float)), hbar);
+    bulk_load(HS2, a.frag + a.fi.head[0], (uint32_t)(D * a.V[0] * sizeof(float)), hbar);
   }
   GR_STAMP(1);
 
@@ -1705,13 +1732,27 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
           if (s >= S)
 #pragma unroll
             for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+          // kv_layout (attn_mma): K as fp16 words [SP][D/2] (hi, then lo),
+          // 4-word halves swapped on key bit 2; V^T as fp16 [D][SP + 8]
           if (c0 < D) {
-            float4 *kr = reinterpret_cast<float4 *>(Kl + s * D + (c0 ^ (((s >> 1) & 1) << 3)));
-            kr[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            kr[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+            uint4 hi, lo;
+            split_h2(acc[0] * kKvScaleF, acc[1] * kKvScaleF, hi.x, lo.x);
+            split_h2(acc[2] * kKvScaleF, acc[3] * kKvScaleF, hi.y, lo.y);
+            split_h2(acc[4] * kKvScaleF, acc[5] * kKvScaleF, hi.z, lo.z);
+            split_h2(acc[6] * kKvScaleF, acc[7] * kKvScaleF, hi.w, lo.w);
+            const int w = s * (D / 2) + ((c0 / 2) ^ (((s >> 2) & 1) << 2));
+            uint32_t *kw = reinterpret_cast<uint32_t *>(Kl);
+            *reinterpret_cast<uint4 *>(kw + w) = hi;
+            *reinterpret_cast<uint4 *>(kw + SP * (D / 2) + w) = lo;
           } else {
+            __half *vh = reinterpret_cast<__half *>(VTl), *vl = vh + D * VS;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) VTl[(c0 - D + c) * VS + s] = acc[c];
+            for (int c = 0; c < 8; ++c) {
+              const float x = acc[c] * kKvScaleF;
+              const __half hx = __float2half_rn(x);
+              vh[(c0 - D + c) * VS + s] = hx;
+              vl[(c0 - D + c) * VS + s] = __float2half_rn(x - __half2float(hx));
+            }
           }
         }
       }
@@ -1809,7 +1850,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
       for (int i = K; i < L; ++i) {
         const int li = i - K;
         const gr4ad_layer &Lw = W.layer[i];
-        const float *Kl = KV + (size_t)li * KVL;
+        const uint32_t *KVw = reinterpret_cast<const uint32_t *>(KV + (size_t)li * KVL);
         float n[KT][4], q[KT][4], o[KT][4];
         ln_frag<KT>(h, Lw.ln1_g, Lw.ln1_b, n);
         mm<KT, KT>(n, a.frag + a.fi.cq[li], q);
@@ -1817,12 +1858,12 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
         {
           float ml[4];
           if (wpt == 1) {
-            attn_mma<D>(q, Kl, Kl + SP * D, S, 0, SP, o, ml);
+            attn_mma<D>(q, KVw, KVw + SP * D, S, 0, SP, o, ml);
             attn_normalize<KT>(o, ml);
           } else {
             // whole 64-key chunks per warp (keys >= S are zero rows, masked)
             const int span = ((S + wpt - 1) / wpt + 63) / 64 * 64;
-            attn_mma<D>(q, Kl, Kl + SP * D, S, part * span, (part + 1) * span, o, ml);
+            attn_mma<D>(q, KVw, KVw + SP * D, S, part * span, (part + 1) * span, o, ml);
             attn_merge<D>(o, ml, gscr, part, wpt, bar_id);
           }
         }
@@ -1931,18 +1972,17 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
       GR_SUB(3);
       // ---- codebook logits + log-softmax keys (beam.py:198-200) ---------------
       bar_wait(hbar, (uint32_t)(t & 1));
-      const float2 *Hf = HS2;
+      const uint4 *Hf = HS2;
       const int NTV = V / 8;
-      uint32_t hh[KT][4], hl[KT][4];
-#pragma unroll
-      for (int k = 0; k < KT; ++k) split_a(h[k], hh[k], hl[k]);
+      uint32_t hh[KT / 2][4], hl[KT / 2][4];
+      split_frags<KT>(h, hh, hl);
       const int per = (NTV + wpt - 1) / wpt;
       const int nb0 = min(NTV, part * per), nb1 = min(NTV, nb0 + per);
       float mA = -INFINITY, mB = -INFINITY, sA = 0.f, sB = 0.f;
       float p1A = -INFINITY, p2A = -INFINITY, p1B = -INFINITY, p2B = -INFINITY;  // lane top-2
       for (int n0 = nb0; n0 < nb1; n0 += kLG) {
         float z[kLG][4];
-        logits_s<KT>(hh, hl, Hf, NTV, n0, nb1, z);
+        logits_s<KT / 2>(hh, hl, Hf, NTV, n0, nb1, z);
         float gA = -INFINITY, gB = -INFINITY;
 #pragma unroll
         for (int j = 0; j < kLG; ++j) {
@@ -2021,7 +2061,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
         px.w = okB && p2B > -INFINITY ? RB.cr + ((p2B - MB) - lsB) : -INFINITY;
         reinterpret_cast<float4 *>(prox)[(tile * wpt + part) * 32 + lane] = px;
       } else {
-        logits_pass2<KT, false>(hh, hl, Hf, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt, Rs,
+        logits_pass2<KT / 2, false>(hh, hl, Hf, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt, Rs,
                                 bscale, 0, sbuf, nullptr, 0);
       }
       GR_SUB(5);
@@ -2072,11 +2112,11 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
         const int cA = min(rA, live - 1), cB = min(rB, live - 1);
         const RowScore RA{okA, rA, cum[mo + cA], hst[cA * HSD + D], hst[cA * HSD + D + 1]};
         const RowScore RB{okB, rB, cum[mo + cB], hst[cB * HSD + D], hst[cB * HSD + D + 1]};
-        uint32_t hh[KT][4], hl[KT][4];
-        load_split<KT>(hst, HSD, cA, cB, hh, hl);
+        uint32_t hh[KT / 2][4], hl[KT / 2][4];
+        load_split<KT / 2>(hst, HSD, cA, cB, hh, hl);
         const int NTV = V / 8, per = (NTV + wpt - 1) / wpt;
         const int nb0 = min(NTV, part * per), nb1 = min(NTV, nb0 + per);
-        logits_pass2<KT, true>(hh, hl, HS2, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt, Rs,
+        logits_pass2<KT / 2, true>(hh, hl, HS2, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt, Rs,
                                bscale, wb, sbuf, &scr[40], a.sort_cap);
       }
       GR_SUB(7);
@@ -2093,11 +2133,11 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
           const int cA = min(rA, live - 1), cB = min(rB, live - 1);
           const RowScore RA{okA, rA, cum[mo + cA], hst[cA * HSD + D], hst[cA * HSD + D + 1]};
           const RowScore RB{okB, rB, cum[mo + cB], hst[cB * HSD + D], hst[cB * HSD + D + 1]};
-          uint32_t hh[KT][4], hl[KT][4];
-          load_split<KT>(hst, HSD, cA, cB, hh, hl);
+          uint32_t hh[KT / 2][4], hl[KT / 2][4];
+          load_split<KT / 2>(hst, HSD, cA, cB, hh, hl);
           const int NTV = V / 8, per = (NTV + wpt - 1) / wpt;
           const int nb0 = min(NTV, part * per), nb1 = min(NTV, nb0 + per);
-          logits_pass2<KT, false>(hh, hl, HS2, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt,
+          logits_pass2<KT / 2, false>(hh, hl, HS2, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt,
                                   Rs, bscale, 0, sbuf, nullptr, 0);
         }
       }
@@ -2107,7 +2147,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
     GR_STAMP(4 + 2 * t);
     if (tid == 0 && t + 1 < T) {  // next level's codebook lands during this selection
       bar_wait(hbar, (uint32_t)(t & 1));  // level t's copy is complete (also with no tiles)
-      bulk_load(HS2, a.frag + a.fi.head_raw[t + 1], (uint32_t)(D * a.V[t + 1] * sizeof(float)),
+      bulk_load(HS2, a.frag + a.fi.head[t + 1], (uint32_t)(D * a.V[t + 1] * sizeof(float)),
                 hbar);
     }
     live = select_level(a, b, t, live, V, keys, hist, scr, sbuf, par, tokm, cum, Rs, bscale,
@@ -2130,25 +2170,27 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
   GR_STAMP(15);
 }
 
-__global__ void frag_prep_kernel(const __grid_constant__ FragJobs jobs, float4 *frag) {
+// fragment-ordered B operands of mma.m16n8k16 (fp16 hi / lo of kFragScale x W):
+// per (k16 step kk, n-tile nn, lane) {b0 hi, b1 hi, b0 lo, b1 lo} with
+// b0 = W[16kk + 2t .. + 1][8nn + g], b1 = W[16kk + 8 + 2t .. + 1][8nn + g]
+__global__ void frag_prep_kernel(const __grid_constant__ FragJobs jobs, uint4 *frag) {
   const FragJob &jb = jobs.job[blockIdx.y];
-  const int NT = jb.nout / 8, total = (jb.kin / 8) * NT * 32;
+  const int NT = jb.nout / 8, total = (jb.kin / 16) * NT * 32;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int lane = i & 31, tile = i >> 5, nn = tile % NT, kk = tile / NT;
-    const int k0 = kk * 8 + 2 * (lane & 3), n = nn * 8 + (lane >> 2);
-    float x0 = 0.f, x1 = 0.f;
+    const int k0 = kk * 16 + 2 * (lane & 3), n = nn * 8 + (lane >> 2);
+    float x[4] = {0.f, 0.f, 0.f, 0.f};
     if (n < jb.nreal) {
-      x0 = jb.src[k0 * jb.sk + n * jb.sn];
-      x1 = jb.src[(k0 + 1) * jb.sk + n * jb.sn];
+      x[0] = jb.src[k0 * jb.sk + n * jb.sn];
+      x[1] = jb.src[(k0 + 1) * jb.sk + n * jb.sn];
+      x[2] = jb.src[(k0 + 8) * jb.sk + n * jb.sn];
+      x[3] = jb.src[(k0 + 9) * jb.sk + n * jb.sn];
     }
-    if (jb.raw)
-      reinterpret_cast<float2 *>(frag + jb.dst)[i] = make_float2(x0, x1);
-    else
-      frag[jb.dst + i] = split_b(make_float2(x0, x1));
+    frag[jb.dst + i] = split_b16(x[0], x[1], x[2], x[3], kFragScale);
   }
 }
 
-int frag_prep_launch(const FragJobs &jobs, float4 *frag, cudaStream_t st) {
+int frag_prep_launch(const FragJobs &jobs, uint4 *frag, cudaStream_t st) {
   if (jobs.n <= 0) return GR4AD_OK;
   GR_LAUNCH(KC_SMALL, st, frag_prep_kernel<<<dim3(8, jobs.n), 256, 0, st>>>(jobs, frag));
   return GR4AD_OK;

@@ -5,17 +5,16 @@
 namespace gr {
 
 // Fragment-ordered weights of the warp-MMA fused kernel: for a (Kin x Nout)
-// matrix, float4 [Kin/8][Nout/8][32 lanes] = {hi(W[k0][n]), hi(W[k0+1][n]),
-// lo(W[k0][n]), lo(W[k0+1][n])} with k0 = 8kk + 2(lane & 3), n = 8nn + lane/4
-// (tf32 hi = 13 low mantissa bits cleared, lo = W - hi): the B fragment of
-// mma.m16n8k8 under the k-permutation that lets a C fragment feed the next
-// product as its A fragment.  Offsets are in float4 units.
+// matrix, uint4 [Kin/16][Nout/8][32 lanes] = {b0 hi, b1 hi, b0 lo, b1 lo},
+// the B fragment of mma.m16n8k16 in fp16 hi / lo of 2048 W with
+// b0 = W[16kk + 2t, +1][8nn + g], b1 = W[16kk + 8 + 2t, +1][8nn + g]
+// (g = lane / 4, t = lane & 3).  A C fragment pair is then directly the A
+// fragment of the next product.  Offsets are in 16-byte units.
 constexpr int kMaxHeadLayersMma = 16;
 constexpr int kDbgSlots = 48;  // per-request phase stamps (GR_FUSED_TIMING builds)
 struct FragIndex {
   long long wg, wf_m, wf_s, value;
   long long head[GR4AD_MAX_LEVELS];
-  long long head_raw[GR4AD_MAX_LEVELS];  // float2 {W[k0][n], W[k0+1][n]} per lane (staged to smem)
   long long cq[kMaxHeadLayersMma], co[kMaxHeadLayersMma], sq[kMaxHeadLayersMma],
       sk[kMaxHeadLayersMma], sv[kMaxHeadLayersMma], so[kMaxHeadLayersMma],
       w1[kMaxHeadLayersMma], w2[kMaxHeadLayersMma];
@@ -24,9 +23,8 @@ struct FragJob {
   const float *src;  // element (k, n) at src[k * sk + n * sn]
   long long sk, sn, dst;
   int kin, nout, nreal;  // nout padded to 8; columns >= nreal are zero
-  int raw;               // 1: float2 {W[k0][n], W[k0+1][n]} per lane (no hi/lo split)
 };
-constexpr int kMaxFragJobs = 4 + 2 * GR4AD_MAX_LEVELS + 8 * kMaxHeadLayersMma;
+constexpr int kMaxFragJobs = 4 + GR4AD_MAX_LEVELS + 8 * kMaxHeadLayersMma;
 struct FragJobs {
   int n;
   FragJob job[kMaxFragJobs];
@@ -48,12 +46,12 @@ struct FusedArgs {
   int s_X, s_KV, s_TR, s_TQ, s_hist, s_par, s_tok, s_cum, s_bins, s_scr, s_sort, s_ws;
   int s_XT;               // warp-MMA kernel: X^T
   int s_mrg;              // warp-MMA kernel: tile-group merge scratch
-  int s_head;             // warp-MMA kernel: the level's codebook (raw fragment order)
+  int s_head;             // warp-MMA kernel: the level's codebook fragments (bulk copy)
   int head_floats;        // its capacity (floats); first holds the request's features
   int s_mbar;             // warp-MMA kernel: mbarrier of the codebook bulk copy
   int s_hst, hst_rows;    // warp-MMA kernel: per-row pass-2 state [hst_rows][D + 2]
   int tile_split;         // warp-MMA kernel: warps share tiles on small levels
-  const float4 *frag;     // warp-MMA kernel: fragment-ordered weights
+  const uint4 *frag;      // warp-MMA kernel: fragment-ordered weights (fp16 hi / lo)
   FragIndex fi;
   uint32_t *keys;  // candidate keys scratch (L2-resident), keys_per_req per request
   long long keys_per_req;
@@ -65,8 +63,8 @@ struct FusedArgs {
 };
 
 int fused_small_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st);
-// warp-level tensor-core variant (mma.sync tf32, 3xTF32), d = 16
-int frag_prep_launch(const FragJobs &jobs, float4 *frag, cudaStream_t st);
+// warp-level tensor-core variant (mma.sync m16n8k16, 3xFP16), d = 16
+int frag_prep_launch(const FragJobs &jobs, uint4 *frag, cudaStream_t st);
 int fused_mma_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st);
 
 }  // namespace gr
