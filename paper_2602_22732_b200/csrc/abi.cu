@@ -100,7 +100,7 @@ struct Plan {
   int f_hst_rows = 0, f_head_floats = 0;
   size_t f_smem4 = 0;
   long long frag_f4 = 0;  // fragment-ordered weights (float4 count)
-  size_t o_frag = 0;
+  size_t o_frag = 0, o_tu = 0;
 };
 
 // Fragment-ordered weight jobs of the warp-MMA fused kernel; with w == NULL
@@ -403,7 +403,10 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.o_tnpos = take(I * (size_t)B * p.n_pos);
   p.table_bytes = o;
   if (p.fused) {
-    if (p.f_mma) p.o_frag = take(16 * (size_t)p.frag_f4);
+    if (p.f_mma) {
+      p.o_frag = take(16 * (size_t)p.frag_f4);
+      p.o_tu = take(sizeof(float) * (size_t)std::max(p.n_pos, 1) * p.d);
+    }
     p.o_keys = take(sizeof(uint32_t) * (size_t)B * p.f_keys_per_req);
     take(sizeof(long long) * kDbgSlots * (size_t)B);  // per-request phase stamps (timing builds)
     p.total = o;
@@ -826,6 +829,10 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       frag_layout(p, w, &jobs, &f.fi);
       f.frag = frag;
       GR_TRY(frag_prep_launch(jobs, frag, st));
+      if (K > 0) {
+        f.trunk_u = at<float>(ws, p.o_tu);
+        GR_TRY(trunk_u_launch(*w, d, p.L, p.n_pos, at<float>(ws, p.o_tu), st));
+      }
       return fused_mma_launch(f, B, p.f_smem4, st);
     }
     return fused_small_launch(f, B, p.f_smem, st);

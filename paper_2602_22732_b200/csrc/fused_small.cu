@@ -373,12 +373,25 @@ __device__ void sort_desc(unsigned long long *buf, int n2) {
   }
 }
 
+#ifdef GR_FUSED_TIMING
+#define GR_TSTAMP(i)                                                            \
+  do {                                                                          \
+    if ((threadIdx.x & 31) == 0) {                                              \
+      long long _t;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                   \
+      a.dbg[blockIdx.x * kDbgSlots + (i)] = _t;                                 \
+    }                                                                           \
+  } while (0)
+#else
+#define GR_TSTAMP(i) do {} while (0)
+#endif
+
 // Trunk: K layers over the n_pos position rows (beam.py:159-163), run by
 // warp 0 alone and reassociated so the trunk layers' K/V are never built:
 // scores (q Wk^T) X^T, output (P X) Wv.  Xs is X^T with row stride xld.
 template <int D>
 __device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S, float *TR,
-                            float *TQ, float *wsl) {
+                            float *TQ, float *wsl, const float *u0 = nullptr) {
   constexpr int E = D / 8;
   const int lane = threadIdx.x & 31, rl = lane >> 3, cb = (lane & 7) * E;
   const gr4ad_weights &W = a.w;
@@ -397,13 +410,21 @@ __device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S,
       float h[E], n[E], t[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) h[e] = TR[pp * D + cb + e];
-      layer_norm<E>(h, Lw.ln1_g, Lw.ln1_b, n);
-      publish<E>(n, slot0);
-      proj<E>(slot0, D, Lw.cross_Wq, D, t);
-      publish<E>(t, slot1);
-      proj_t<E>(slot1, D, Wk, ldw, t);  // u = q Wk^T, u . x_s == q . k_s
+      if (i == 0 && u0) {  // layer 0's query side depends on the weights only
+#pragma unroll
+        for (int e = 0; e < E; ++e) t[e] = u0[pp * D + cb + e];
+      } else {
+        layer_norm<E>(h, Lw.ln1_g, Lw.ln1_b, n);
+        publish<E>(n, slot0);
+        proj<E>(slot0, D, Lw.cross_Wq, D, t);
+        GR_TSTAMP(42);
+        publish<E>(t, slot1);
+        proj_t<E>(slot1, D, Wk, ldw, t);  // u = q Wk^T, u . x_s == q . k_s
+      }
+      GR_TSTAMP(43);
       publish<E>(t, slot0);
       cross_attn<D>(slot0, Xs, Xs, S, xld, slot2, t);  // t = P X
+      GR_TSTAMP(44);
       publish<E>(t, slot1);
       proj<E>(slot1, D, Wv, ldw, t);  // (P X) Wv == P V
       publish<E>(t, slot0);
@@ -412,6 +433,7 @@ __device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S,
       for (int e = 0; e < E; ++e) h[e] += t[e];
       layer_norm<E>(h, Lw.ln2_g, Lw.ln2_b, n);
       publish<E>(n, slot0);
+      GR_TSTAMP(45);
       for (int c = 0; c < 3; ++c) {
         proj<E>(slot0, D, Lw.self_Wqkv + c * D, 3 * D, t);
         if (ok)
@@ -452,12 +474,14 @@ __device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S,
       }
 #pragma unroll
       for (int e = 0; e < E; ++e) so[e] /= se;
+      GR_TSTAMP(46);
       publish<E>(so, slot0);
       proj<E>(slot0, D, Lw.self_Wo, D, t);
 #pragma unroll
       for (int e = 0; e < E; ++e) h[e] += t[e];
       layer_norm<E>(h, Lw.ln3_g, Lw.ln3_b, n);
       publish<E>(n, slot0);
+      GR_TSTAMP(47);
       ffn<D>(slot0, slot3, Lw, dff, t);
 #pragma unroll
       for (int e = 0; e < E; ++e) h[e] += t[e] + __ldg(Lw.ffn_b2 + cb + e);
@@ -498,7 +522,16 @@ __device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S,
       a.dbg[blockIdx.x * kDbgSlots + (i)] = _t;                                 \
     }                                                                           \
   } while (0)
+#define GR_XSTAMP(w, i)                                                         \
+  do {                                                                          \
+    if (t == 2 && threadIdx.x == 32 * (w)) {                                    \
+      long long _t;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                   \
+      a.dbg[blockIdx.x * kDbgSlots + (i)] = _t;                                 \
+    }                                                                           \
+  } while (0)
 #else
+#define GR_XSTAMP(w, i) do {} while (0)
 #define GR_STAMP(i) do {} while (0)
 #define GR_SUB(i) do {} while (0)
 #define GR_WSTAMP(i) do {} while (0)
@@ -1527,28 +1560,19 @@ static __device__ __forceinline__ void logits_pass2(
         }
       }
     } else {
-      unsigned pm = 0;  // bit 4j + c: value c of n-tile j passed the pre-filter
+      // exact window test of every value (branch-free), then one warp-wide
+      // scan and one shared atomic per group; entries stored predicated
+      unsigned pm = 0;  // bit 4j + c: value c of n-tile j is in the window
 #pragma unroll
       for (int j = 0; j < kLG; ++j)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)  // padded tiles are -inf
-          pm |= (z[j][c] > (c < 2 ? zA : zB) ? 1u : 0u) << (4 * j + c);
-      if (__any_sync(kFull, pm != 0)) {
-        unsigned pre = pm;  // exact window test of the (rare) pre-passes
-        pm = 0;
-        while (pre) {
-          const int bit = __ffs(pre) - 1;
-          pre &= pre - 1;
-          float zz = z[0][0];
-#pragma unroll
-          for (int jj = 0; jj < kLG; ++jj)
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc)
-              if (4 * jj + cc == bit) zz = z[jj][cc];
-          const bool sb = (bit & 3) >= 2;
-          const float sc = (sb ? B.cr : A.cr) + ((zz - (sb ? B.M : A.M)) - (sb ? B.ls : A.ls));
-          if (sbin(sc) <= (unsigned)wb) pm |= 1u << bit;
+        for (int c = 0; c < 4; ++c) {  // padded tiles are -inf: never pass zA / zB
+          const RowScore &R = c < 2 ? A : B;
+          const float sc = R.cr + ((z[j][c] - R.M) - R.ls);
+          const bool in = z[j][c] > (c < 2 ? zA : zB) && sbin(sc) <= (unsigned)wb;
+          pm |= (in ? 1u : 0u) << (4 * j + c);
         }
+      if (__any_sync(kFull, pm != 0)) {
         const unsigned np = __popc(pm);
         unsigned incl = np;
 #pragma unroll
@@ -1559,25 +1583,18 @@ static __device__ __forceinline__ void logits_pass2(
         unsigned base = 0;
         if (lane == 31) base = atomicAdd(cnt, incl);
         base = __shfl_sync(kFull, base, 31) + incl - np;
-        while (pm) {
-          const int bit = __ffs(pm) - 1;
-          pm &= pm - 1;
-          const int j = bit >> 2, c = bit & 3;
-          const RowScore &R = c < 2 ? A : B;
-          float zz = z[0][0];
 #pragma unroll
-          for (int jj = 0; jj < kLG; ++jj)
+        for (int j = 0; j < kLG; ++j)
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc)
-              if (jj == j && cc == c) zz = z[jj][cc];
-          const float sc = (c < 2 ? A.cr : B.cr) + ((zz - (c < 2 ? A.M : B.M)) - (c < 2 ? A.ls : B.ls));
-          const int row = c < 2 ? A.r : B.r;
-          const int col = (n0 + j) * 8 + 2 * t4 + (c & 1);
-          if (base < (unsigned)cap)
-            sbuf[base] = ((unsigned long long)f2ord(sc) << 32) | (0xFFFFFFFFu - (unsigned)(row * V + col));
-          ++base;
-          (void)R;
-        }
+          for (int c = 0; c < 4; ++c)
+            if ((pm >> (4 * j + c)) & 1u) {
+              const RowScore &R = c < 2 ? A : B;
+              const float sc = R.cr + ((z[j][c] - R.M) - R.ls);
+              if (base < (unsigned)cap)
+                sbuf[base] = ((unsigned long long)f2ord(sc) << 32) |
+                             (0xFFFFFFFFu - (unsigned)(R.r * V + (n0 + j) * 8 + 2 * t4 + (c & 1)));
+              ++base;
+            }
       }
     }
   }
@@ -1699,7 +1716,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
   // ---- head-layer K / V^T (beam.py:165-169) by warps 1-7 while warp 0 runs
   // the trunk; thread owns keys, X column in registers
   if (K > 0 && wid == 0) {
-    trunk_warp0<D>(a, XT, VS, S, TR, TQ, wsl);
+    trunk_warp0<D>(a, XT, VS, S, TR, TQ, wsl, a.trunk_u);
     GR_WSTAMP(16);
   } else {
     const int t0 = K > 0 ? 32 : 0, nt = kThreads - t0;
@@ -2168,6 +2185,47 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
   }
   if (tid == 0) a.out_count[b] = live;
   GR_STAMP(15);
+}
+
+// The request-independent head of trunk layer 0 (beam.py:159-163 with the
+// reassociated attention): u_p = (LN1(pos_p) Wq) Wk^T for every position p,
+// once per batch; the fused kernel's trunk starts at u_p . x_s.
+__global__ void trunk_u_kernel(const __grid_constant__ gr4ad_weights w, int d, int L, int n_pos,
+                               float *u) {
+  extern __shared__ float tsm[];
+  float *nrm = tsm, *q = tsm + n_pos * d;
+  const gr4ad_layer &Lw = w.layer[0];
+  for (int p = threadIdx.x; p < n_pos; p += blockDim.x) {  // layers.py:38-43
+    const float *x = w.pos + (size_t)p * d;
+    float mean = 0.f;
+    for (int i = 0; i < d; ++i) mean += x[i];
+    mean /= (float)d;
+    float var = 0.f;
+    for (int i = 0; i < d; ++i) var += (x[i] - mean) * (x[i] - mean);
+    const float inv = 1.0f / sqrtf(var / (float)d + 1e-5f);
+    for (int i = 0; i < d; ++i) nrm[p * d + i] = (x[i] - mean) * inv * Lw.ln1_g[i] + Lw.ln1_b[i];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n_pos * d; e += blockDim.x) {
+    const int p = e / d, j = e - p * d;
+    float acc = 0.f;
+    for (int i = 0; i < d; ++i) acc = fmaf(nrm[p * d + i], Lw.cross_Wq[(size_t)i * d + j], acc);
+    q[e] = acc;
+  }
+  __syncthreads();
+  const int ldw = 2 * L * d;  // Wk of layer 0: columns [0, d) of cross_kv_W
+  for (int e = threadIdx.x; e < n_pos * d; e += blockDim.x) {
+    const int p = e / d, i = e - p * d;
+    float acc = 0.f;
+    for (int j = 0; j < d; ++j) acc = fmaf(q[p * d + j], w.cross_kv_W[(size_t)i * ldw + j], acc);
+    u[e] = acc;
+  }
+}
+
+int trunk_u_launch(const gr4ad_weights &w, int d, int L, int n_pos, float *u, cudaStream_t st) {
+  const size_t smem = 2 * (size_t)n_pos * d * sizeof(float);
+  GR_LAUNCH(KC_SMALL, st, trunk_u_kernel<<<1, 256, smem, st>>>(w, d, L, n_pos, u));
+  return GR4AD_OK;
 }
 
 // fragment-ordered B operands of mma.m16n8k16 (fp16 hi / lo of kFragScale x W):

@@ -51,6 +51,7 @@ struct FusedArgs {
   int s_mbar;             // warp-MMA kernel: mbarrier of the codebook bulk copy
   int s_hst, hst_rows;    // warp-MMA kernel: per-row pass-2 state [hst_rows][D + 2]
   int tile_split;         // warp-MMA kernel: warps share tiles on small levels
+  const float *trunk_u;   // warp-MMA kernel: [n_pos][D] layer-0 trunk queries (trunk_u_launch)
   const uint4 *frag;      // warp-MMA kernel: fragment-ordered weights (fp16 hi / lo)
   FragIndex fi;
   uint32_t *keys;  // candidate keys scratch (L2-resident), keys_per_req per request
@@ -66,5 +67,6 @@ int fused_small_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStre
 // warp-level tensor-core variant (mma.sync m16n8k16, 3xFP16), d = 16
 int frag_prep_launch(const FragJobs &jobs, uint4 *frag, cudaStream_t st);
 int fused_mma_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st);
+int trunk_u_launch(const gr4ad_weights &w, int d, int L, int n_pos, float *u, cudaStream_t st);
 
 }  // namespace gr
