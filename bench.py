@@ -328,7 +328,7 @@ def roofline_for(dec, feats, cfgd, dev, config=None):
            "classes": classes,
            "note": "per-class times are CUDA events on the launching stream; peak is the "
                    "measured bf16 dense figure although the path computes fp32-faithful: "
-                   "3xFP16 on tcgen05 (layered path), 3xTF32 on mma.sync (fused path)"}
+                   "3xFP16 on tcgen05 (layered path) and on mma.sync m16n8k16 (fused path)"}
     if kind == "flop" and dom in ("gemm", "attn_gemm"):
         # fp32-faithful tensor-core bound: 3 fp16 products per MAC (3xFP16,
         # fp16 dense rate == bf16 dense rate), against the sustained figure
@@ -435,24 +435,30 @@ def main():
     # would; per-request latency is measured on the serial path.
     host_f = [feats.cpu().pin_memory(), feats.cpu().pin_memory()]
     dec2 = BeamDecoder(model, [S] * B, [widths] * B, device=dev)
-    feats2 = torch.empty_like(feats)
-    if not args.no_graph:
-        dec2.capture(features=feats2)
-    decs = [(dec, feats, step), (dec2, feats2, dec2.replay if not args.no_graph
-                                 else (lambda: dec2.run(features=feats2)))]
-    h_out = [[torch.empty_like(t, device="cpu").pin_memory() for t in (d.count, d.tokens, d.score)]
-             for d, _, _ in decs]
+    decs = [dec, dec2]
     h2d = host_f[0].numel() * host_f[0].element_size()
-    d2h = sum(t.numel() * t.element_size() for t in h_out[0])
+    d2h = sum(t.numel() * t.element_size() for t in (dec.count, dec.tokens, dec.score))
     streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    if not args.no_graph:
+        # one graph per buffer set: H2D features -> decode -> D2H results
+        for j in (0, 1):
+            decs[j].capture_host(host_f[j])
+    else:
+        fbufs = [torch.empty_like(feats), torch.empty_like(feats)]
+        for d_ in decs:
+            d_.host_out = [torch.empty_like(t, device="cpu").pin_memory()
+                           for t in (d_.count, d_.tokens, d_.score)]
 
     def submit(j):
-        d, fbuf, run = decs[j]
+        d_ = decs[j]
         with torch.cuda.stream(streams[j]):
-            fbuf.copy_(host_f[j], non_blocking=True)
-            run()
-            for h, t in zip(h_out[j], (d.count, d.tokens, d.score)):
-                h.copy_(t, non_blocking=True)
+            if not args.no_graph:
+                d_.replay_host()
+            else:
+                fbufs[j].copy_(host_f[j], non_blocking=True)
+                d_.run(features=fbufs[j])
+                for h, t in zip(d_.host_out, (d_.count, d_.tokens, d_.score)):
+                    h.copy_(t, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
         return ev
@@ -526,7 +532,8 @@ def main():
             "e2e": {"value": e2e_value, "unit": "req/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "how": "C ABI with pinned host buffers; per step H2D features + decode + "
-                           "D2H results, two buffer sets on two streams (copies of step i+1 "
+                           "D2H results (one CUDA graph per buffer set, BeamDecoder."
+                           "capture_host), two buffer sets on two streams (copies of step i+1 "
                            "overlap the decode of step i); best of 3 windows of K steps"},
             "gpu_launches": launches_per_step * args.steps * 5,
             "gpu_launches_note": "per-step launches x (device-timed + serial e2e + 3 pipelined e2e windows) steps",

@@ -163,6 +163,15 @@ int gr4ad_beam_search_run(const gr4ad_dims *dims, const gr4ad_weights *w,
                           const float *context, gr4ad_results *out, void *workspace,
                           size_t workspace_bytes, void *stream);
 
+/* fp16 split range of the last decode in `workspace` (synchronises `stream`).
+ * The tensor-core paths split weights (x 2048) and the context K / V (x 256)
+ * into fp16 hi + lo; a value outside the fp16 range after that scale sets a
+ * flag in the workspace, reported here as GR4AD_ERR_UNSUPPORTED (decode
+ * with a CUDA-core path instead).  No reference counterpart: the reference
+ * computes in float64 (autodiff.py:55). */
+int gr4ad_range_status(const gr4ad_dims *dims, const gr4ad_batch *batch, const void *workspace,
+                       void *stream);
+
 /* Context projection X = F W_c + b_c (decoder.py:134-140): (rows, F) -> (rows, d). */
 int gr4ad_context_process(const gr4ad_dims *dims, const gr4ad_weights *w,
                           const float *features, int rows, float *x, void *stream);

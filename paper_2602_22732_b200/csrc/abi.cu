@@ -77,7 +77,7 @@ struct Plan {
   size_t o_trow_off, o_trows, o_trow_req, o_tanc, o_tnpos;
   size_t o_tok, o_anc, o_cum, o_prefix;
   size_t o_X, o_KV, o_Ht, o_QKVt, o_Fin = 0;
-  size_t o_Hs, o_N, o_Q, o_A, o_U, o_Fb, o_SC, o_LG, o_rinfo, o_vlog;
+  size_t o_Hs, o_N, o_Q, o_A, o_U, o_Fb, o_SC, o_LG, o_rinfo, o_lsep, o_vlog;
   size_t o_hist;  // (L-K) consecutive (H, 3d) buffers
   size_t table_bytes, total;
   // tensor-core layered path
@@ -101,6 +101,7 @@ struct Plan {
   size_t f_smem4 = 0;
   long long frag_f4 = 0;  // fragment-ordered weights (float4 count)
   size_t o_frag = 0, o_tu = 0;
+  size_t o_flag = 0;  // fp16 range flag (set by the operand splits, read by gr4ad_range_status)
 };
 
 // Fragment-ordered weight jobs of the warp-MMA fused kernel; with w == NULL
@@ -402,6 +403,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.o_tanc = take(I * (size_t)B * p.n_pos * p.n_pos);
   p.o_tnpos = take(I * (size_t)B * p.n_pos);
   p.table_bytes = o;
+  p.o_flag = take(256);
   if (p.fused) {
     if (p.f_mma) {
       p.o_frag = take(16 * (size_t)p.frag_f4);
@@ -434,6 +436,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.o_SC = take(Fl * p.Rw * p.sc_ld);
   p.o_LG = take(Fl * p.Rw * std::max(p.Vmax, p.nb));
   p.o_rinfo = take(sizeof(float2) * p.Rw);
+  p.o_lsep = take(p.tc ? sizeof(float2) * p.Rw * ((p.Vmax + 127) / 128) : 16);
   p.o_vlog = take(Fl * std::max(p.R[T], 1LL) * p.nb);
   p.o_hist = take(Fl * p.H * 3 * d * (size_t)(p.L - p.K));
   if (p.tc) {
@@ -536,7 +539,8 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
     __half *dst = base + o;
     o += ((long long)rows * cols + 63) / 64 * 64;
     if (rc == GR4AD_OK)
-      rc = transpose_split16(src, cols, dst, dst + p.wt_floats, rows, rows, cols, kWeightScale, st);
+      rc = transpose_split16(src, cols, dst, dst + p.wt_floats, rows, rows, cols, kWeightScale,
+                             at<int>(ws, p.o_flag), st);
     return dst;
   };
   const int d = p.d;
@@ -748,6 +752,7 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
       t.vt_ld = p.vt_ld;
       t.kv_scale = kKvScale;
       t.kv_d = d;
+      t.range_flag = at<int>(ws, p.o_flag);
       GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * nh * d, d, EPI_KV_SPLIT, st));
       if (K > 0) GR_TRY(transpose(X, d, at<float>(ws, p.o_XT), p.vt_ld, (int)p.S_tot, d, st));
     } else {
@@ -782,8 +787,11 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
                     gr4ad_results *out, void *ws, cudaStream_t st) {
   const int B = p.B, T = p.T, d = p.d, K = p.K;
   if (B == 0) return GR4AD_OK;
+  int *range_flag = at<int>(ws, p.o_flag);
+  GR_CUDA(cudaMemsetAsync(range_flag, 0, sizeof(int), st));
   if (p.fused) {
     FusedArgs f{};
+    f.range_flag = range_flag;
     f.w = *w;
     if (!features && !context) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
     f.features = features;
@@ -828,11 +836,14 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       uint4 *frag = at<uint4>(ws, p.o_frag);
       frag_layout(p, w, &jobs, &f.fi);
       f.frag = frag;
-      GR_TRY(frag_prep_launch(jobs, frag, st));
-      if (K > 0) {
-        f.trunk_u = at<float>(ws, p.o_tu);
-        GR_TRY(trunk_u_launch(*w, d, p.L, p.n_pos, at<float>(ws, p.o_tu), st));
+      jobs.tu = TrunkUJob{};
+      if (K > 0 && d <= 32) {
+        const gr4ad_layer &L0 = w->layer[0];
+        jobs.tu = TrunkUJob{w->pos, L0.ln1_g, L0.ln1_b, L0.cross_Wq, w->cross_kv_W,
+                            at<float>(ws, p.o_tu), d, 2 * p.L * d, p.n_pos};
+        f.trunk_u = jobs.tu.u;
       }
+      GR_TRY(frag_prep_launch(jobs, frag, range_flag, st));
       return fused_mma_launch(f, B, p.f_smem4, st);
     }
     return fused_small_launch(f, B, p.f_smem, st);
@@ -898,9 +909,23 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     }
     // codebook projection + log-softmax + score accumulation + top-k (beam.py:198-210)
     const int V = p.V[t];
-    GR_TRY(dense(p, plain_gemm(Hs, d, w->head[t], V, LG, V, R, V, d),
-                 wt ? wt->head[t] : nullptr, R, EPI_STORE, st));
-    GR_TRY(row_lse(LG, V, R, V, rinfo, st));
+    const GemmArgs lg = plain_gemm(Hs, d, w->head[t], V, LG, V, R, V, d);
+    if (p.tc && wt && d % 8 == 0 && tc_eligible(d, d, d, Hs, wt->head[t])) {
+      // log-sum-exp partials from the GEMM epilogue (no second pass over the logits)
+      TcArgs tl{};
+      static_cast<GemmArgs &>(tl) = lg;
+      tl.b_hi = wt->head[t];
+      tl.b_lo = wt->head[t] + p.wt_floats;
+      tl.ldb = d;
+      tl.alpha = lg.alpha / kWeightScale;
+      tl.lse_part = at<float2>(ws, p.o_lsep);
+      tl.lse_ld = (V + 127) / 128;
+      GR_TRY(gemm_tc(tl, R, d, V, d, EPI_STORE_LSE, st));
+      GR_TRY(lse_merge(tl.lse_part, tl.lse_ld, R, rinfo, st));
+    } else {
+      GR_TRY(dense(p, lg, wt ? wt->head[t] : nullptr, R, EPI_STORE, st));
+      GR_TRY(row_lse(LG, V, R, V, rinfo, st));
+    }
     if (bt->valid_prefix[t]) {
       GR_TRY(mask_rows(LG, V, R, V, prefix + h0,
                        reinterpret_cast<const long long *>(bt->valid_prefix[t]),
@@ -1020,6 +1045,23 @@ int gr4ad_beam_search_run(const gr4ad_dims *dims, const gr4ad_weights *w,
   return run_plan(p, dims, w, batch, features, context, out, workspace, (cudaStream_t)stream);
 }
 
+int gr4ad_range_status(const gr4ad_dims *dims, const gr4ad_batch *batch, const void *workspace,
+                       void *stream) {
+  Plan p;
+  GR_TRY(make_plan(dims, batch, p));
+  if (p.B == 0) return GR4AD_OK;
+  int flag = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  GR_CUDA(cudaMemcpyAsync(&flag, static_cast<const char *>(workspace) + p.o_flag, sizeof(int),
+                          cudaMemcpyDeviceToHost, st));
+  GR_CUDA(cudaStreamSynchronize(st));
+  if (flag)
+    return set_err(GR4AD_ERR_UNSUPPORTED,
+                   "an operand exceeded the fp16 split range (|weight| < 32, |context K/V| < 256): "
+                   "decode with the CUDA-core path (decode_path layered / fused_simt)");
+  return GR4AD_OK;
+}
+
 int gr4ad_beam_search(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4ad_batch *batch,
                       const float *features, const float *context, gr4ad_results *out,
                       void *workspace, size_t workspace_bytes, void *stream) {
@@ -1088,6 +1130,7 @@ int gr4ad_score_sequences(const gr4ad_dims *dims, const gr4ad_weights *w, const 
   if (n_seq == 0 || p.B == 0) return GR4AD_OK;
   cudaStream_t st = (cudaStream_t)stream;
   void *ws = workspace;
+  GR_CUDA(cudaMemsetAsync(at<int>(ws, p.o_flag), 0, sizeof(int), st));
   const int d = p.d, T = p.T, np = sl.n_pos, Rs = sl.rows;
   // per-sequence tables: attention group = sequence (its request's context),
   // causal ancestors = earlier positions of the same sequence
@@ -1176,6 +1219,15 @@ int gr4ad_score_sequences(const gr4ad_dims *dims, const gr4ad_weights *w, const 
     GemmArgs g = plain_gemm(Hs + (size_t)T * d, (long long)np * d, w->head_value, p.nb,
                             value_logits, p.nb, n_seq, p.nb, d);
     GR_TRY(dense(p, g, wt ? wt->hv : nullptr, (long long)n_seq, EPI_STORE, st));
+  }
+  if (p.tc) {  // fp16 operand range (the scoring API is synchronous for its caller)
+    int flag = 0;
+    GR_CUDA(cudaMemcpyAsync(&flag, at<int>(ws, p.o_flag), sizeof(int), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+    if (flag)
+      return set_err(GR4AD_ERR_UNSUPPORTED,
+                     "an operand exceeded the fp16 split range (|weight| < 32, |context K/V| < "
+                     "256): score with the CUDA-core path");
   }
   return GR4AD_OK;
 }

@@ -9,6 +9,12 @@
 
 namespace gr {
 
+// fp16 operand splits: flag values a saturating conversion would clip
+// (|x| > 65504 after the power-of-two scale, or NaN)
+__device__ __forceinline__ void range_check(float scaled, int *flag) {
+  if (flag && !(fabsf(scaled) <= 65504.f)) atomicOr(flag, 1);
+}
+
 // thread-local error text (the C side keeps no other state)
 int set_err(int code, const char *fmt, ...);
 

@@ -741,7 +741,9 @@ __device__ int select_level(const FusedArgs &a, int b, int t, int live, int V,
   const int mo1 = a.moff[t + 1];
   for (int j = tid; j < k; j += kThreads) {
     unsigned long long e = sbuf[j];
-    unsigned fi = 0xFFFFFFFFu - (unsigned)(e & 0xFFFFFFFFull);
+    // (clamped: non-finite scores from out-of-range inputs -- reported by
+    // gr4ad_range_status -- must not turn into out-of-bounds rows)
+    unsigned fi = min(0xFFFFFFFFu - (unsigned)(e & 0xFFFFFFFFull), (unsigned)(n_cand - 1));
     par[mo1 + j] = (int)(fi / (unsigned)V);
     tokm[mo1 + j] = (int)(fi % (unsigned)V);
     cum[mo1 + j] = ord2f((uint32_t)(e >> 32));
@@ -1751,6 +1753,8 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
             for (int c = 0; c < 8; ++c) acc[c] = 0.f;
           // kv_layout (attn_mma): K as fp16 words [SP][D/2] (hi, then lo),
           // 4-word halves swapped on key bit 2; V^T as fp16 [D][SP + 8]
+#pragma unroll
+          for (int c = 0; c < 8; ++c) range_check(acc[c] * kKvScaleF, a.range_flag);
           if (c0 < D) {
             uint4 hi, lo;
             split_h2(acc[0] * kKvScaleF, acc[1] * kKvScaleF, hi.x, lo.x);
@@ -2189,49 +2193,45 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
 
 // The request-independent head of trunk layer 0 (beam.py:159-163 with the
 // reassociated attention): u_p = (LN1(pos_p) Wq) Wk^T for every position p,
-// once per batch; the fused kernel's trunk starts at u_p . x_s.
-__global__ void trunk_u_kernel(const __grid_constant__ gr4ad_weights w, int d, int L, int n_pos,
-                               float *u) {
-  extern __shared__ float tsm[];
-  float *nrm = tsm, *q = tsm + n_pos * d;
-  const gr4ad_layer &Lw = w.layer[0];
-  for (int p = threadIdx.x; p < n_pos; p += blockDim.x) {  // layers.py:38-43
-    const float *x = w.pos + (size_t)p * d;
+// once per batch (one extra frag_prep block); the fused kernel's trunk
+// starts at u_p . x_s.
+__device__ void trunk_u_block(const TrunkUJob &j) {
+  __shared__ float nrm[(GR4AD_MAX_LEVELS + 2) * 32], q[(GR4AD_MAX_LEVELS + 2) * 32];
+  const int d = j.d, np = j.n_pos;
+  for (int p = threadIdx.x; p < np; p += blockDim.x) {  // layers.py:38-43
+    const float *x = j.pos + (size_t)p * d;
     float mean = 0.f;
     for (int i = 0; i < d; ++i) mean += x[i];
     mean /= (float)d;
     float var = 0.f;
     for (int i = 0; i < d; ++i) var += (x[i] - mean) * (x[i] - mean);
     const float inv = 1.0f / sqrtf(var / (float)d + 1e-5f);
-    for (int i = 0; i < d; ++i) nrm[p * d + i] = (x[i] - mean) * inv * Lw.ln1_g[i] + Lw.ln1_b[i];
+    for (int i = 0; i < d; ++i) nrm[p * d + i] = (x[i] - mean) * inv * j.ln1_g[i] + j.ln1_b[i];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < n_pos * d; e += blockDim.x) {
-    const int p = e / d, j = e - p * d;
+  for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
+    const int p = e / d, c = e - p * d;
     float acc = 0.f;
-    for (int i = 0; i < d; ++i) acc = fmaf(nrm[p * d + i], Lw.cross_Wq[(size_t)i * d + j], acc);
+    for (int i = 0; i < d; ++i) acc = fmaf(nrm[p * d + i], j.wq[(size_t)i * d + c], acc);
     q[e] = acc;
   }
   __syncthreads();
-  const int ldw = 2 * L * d;  // Wk of layer 0: columns [0, d) of cross_kv_W
-  for (int e = threadIdx.x; e < n_pos * d; e += blockDim.x) {
+  for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
     const int p = e / d, i = e - p * d;
     float acc = 0.f;
-    for (int j = 0; j < d; ++j) acc = fmaf(q[p * d + j], w.cross_kv_W[(size_t)i * ldw + j], acc);
-    u[e] = acc;
+    for (int c = 0; c < d; ++c) acc = fmaf(q[p * d + c], j.kv[(size_t)i * j.ldw + c], acc);
+    j.u[e] = acc;
   }
-}
-
-int trunk_u_launch(const gr4ad_weights &w, int d, int L, int n_pos, float *u, cudaStream_t st) {
-  const size_t smem = 2 * (size_t)n_pos * d * sizeof(float);
-  GR_LAUNCH(KC_SMALL, st, trunk_u_kernel<<<1, 256, smem, st>>>(w, d, L, n_pos, u));
-  return GR4AD_OK;
 }
 
 // fragment-ordered B operands of mma.m16n8k16 (fp16 hi / lo of kFragScale x W):
 // per (k16 step kk, n-tile nn, lane) {b0 hi, b1 hi, b0 lo, b1 lo} with
 // b0 = W[16kk + 2t .. + 1][8nn + g], b1 = W[16kk + 8 + 2t .. + 1][8nn + g]
-__global__ void frag_prep_kernel(const __grid_constant__ FragJobs jobs, uint4 *frag) {
+__global__ void frag_prep_kernel(const __grid_constant__ FragJobs jobs, uint4 *frag, int *flag) {
+  if (blockIdx.y == jobs.n) {  // the extra block row: trunk queries
+    if (blockIdx.x == 0 && jobs.tu.u) trunk_u_block(jobs.tu);
+    return;
+  }
   const FragJob &jb = jobs.job[blockIdx.y];
   const int NT = jb.nout / 8, total = (jb.kin / 16) * NT * 32;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -2244,13 +2244,15 @@ __global__ void frag_prep_kernel(const __grid_constant__ FragJobs jobs, uint4 *f
       x[2] = jb.src[(k0 + 8) * jb.sk + n * jb.sn];
       x[3] = jb.src[(k0 + 9) * jb.sk + n * jb.sn];
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) range_check(x[q] * kFragScale, flag);
     frag[jb.dst + i] = split_b16(x[0], x[1], x[2], x[3], kFragScale);
   }
 }
 
-int frag_prep_launch(const FragJobs &jobs, uint4 *frag, cudaStream_t st) {
+int frag_prep_launch(const FragJobs &jobs, uint4 *frag, int *range_flag, cudaStream_t st) {
   if (jobs.n <= 0) return GR4AD_OK;
-  GR_LAUNCH(KC_SMALL, st, frag_prep_kernel<<<dim3(8, jobs.n), 256, 0, st>>>(jobs, frag));
+  GR_LAUNCH(KC_SMALL, st, frag_prep_kernel<<<dim3(8, jobs.n + 1), 256, 0, st>>>(jobs, frag, range_flag));
   return GR4AD_OK;
 }
 

@@ -25,9 +25,17 @@ struct FragJob {
   int kin, nout, nreal;  // nout padded to 8; columns >= nreal are zero
 };
 constexpr int kMaxFragJobs = 4 + GR4AD_MAX_LEVELS + 8 * kMaxHeadLayersMma;
+// frag_prep's extra block: trunk layer 0's position-only queries
+// u_p = (LN1(pos_p) Wq) Wk^T (d <= 32), the fused trunk's starting point
+struct TrunkUJob {
+  const float *pos, *ln1_g, *ln1_b, *wq, *kv;  // kv: cross_kv_W (Wk of layer 0 = columns [0, d))
+  float *u;                                    // [n_pos][d]; NULL: no trunk
+  int d, ldw, n_pos;
+};
 struct FragJobs {
   int n;
   FragJob job[kMaxFragJobs];
+  TrunkUJob tu;
 };
 
 struct FusedArgs {
@@ -51,7 +59,8 @@ struct FusedArgs {
   int s_mbar;             // warp-MMA kernel: mbarrier of the codebook bulk copy
   int s_hst, hst_rows;    // warp-MMA kernel: per-row pass-2 state [hst_rows][D + 2]
   int tile_split;         // warp-MMA kernel: warps share tiles on small levels
-  const float *trunk_u;   // warp-MMA kernel: [n_pos][D] layer-0 trunk queries (trunk_u_launch)
+  const float *trunk_u;   // warp-MMA kernel: [n_pos][D] layer-0 trunk queries (FragJobs.tu)
+  int *range_flag;        // warp-MMA kernel: set when a scaled K / V leaves the fp16 range
   const uint4 *frag;      // warp-MMA kernel: fragment-ordered weights (fp16 hi / lo)
   FragIndex fi;
   uint32_t *keys;  // candidate keys scratch (L2-resident), keys_per_req per request
@@ -65,8 +74,7 @@ struct FusedArgs {
 
 int fused_small_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st);
 // warp-level tensor-core variant (mma.sync m16n8k16, 3xFP16), d = 16
-int frag_prep_launch(const FragJobs &jobs, uint4 *frag, cudaStream_t st);
+int frag_prep_launch(const FragJobs &jobs, uint4 *frag, int *range_flag, cudaStream_t st);
 int fused_mma_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st);
-int trunk_u_launch(const gr4ad_weights &w, int d, int L, int n_pos, float *u, cudaStream_t st);
 
 }  // namespace gr

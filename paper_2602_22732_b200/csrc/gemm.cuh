@@ -19,7 +19,8 @@ enum GemmEpi {
   EPI_RESID = 3,      // C = R + acc
   EPI_BIAS_RESID = 4, // C = R + (acc + bias[n])
   EPI_MULVEC = 5,     // C = vec[req(r)][n] * acc   (fuse gate m * (s W_g))
-  EPI_KV_SPLIT = 6    // C = acc, and the V half of each layer also written transposed
+  EPI_KV_SPLIT = 6,   // C = acc, and the V half of each layer also written transposed
+  EPI_STORE_LSE = 7   // C = alpha*acc, plus per-row (max, sum exp) of every 128 columns
 };
 
 struct GemmArgs {

@@ -344,12 +344,33 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int rbase = ti.m0 + q * 32;  // this warp's 32 rows
       const int nrows = min(32, ti.M - rbase);
       const int N = ti.N;
+      float pm = -INFINITY, ps = 0.f;  // EPI_STORE_LSE: this lane's row, current 128 columns
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
         const int col0 = ti.n0 + c * 32;
         if (nrows <= 0 || col0 >= N) continue;  // warp-uniform
+        if (EPI == EPI_STORE_LSE) {  // online (max, sum exp) over the row-per-lane registers
+          float cm = -INFINITY;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            if (col0 + jj < N) cm = fmaxf(cm, v[jj] * a.alpha);
+          const float nm = fmaxf(pm, cm);
+          float cs = 0.f;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            if (col0 + jj < N) cs += expf(v[jj] * a.alpha - nm);
+          ps = (pm == -INFINITY ? 0.f : ps * expf(pm - nm)) + cs;
+          pm = nm;
+          if ((c & 3) == 3 || col0 + 32 >= N) {
+            if (lane < nrows)
+              a.lse_part[((long long)ti.row_base + rbase + lane) * a.lse_ld + col0 / 128] =
+                  make_float2(pm, ps);
+            pm = -INFINITY;
+            ps = 0.f;
+          }
+        }
         if (EPI == EPI_KV_SPLIT) {
           // [2i d, 2i d + d) -> K_i, [2i d + d, 2(i+1) d) -> V_i^T, both as fp16
           // hi / lo of kv_scale * x for the attention GEMMs; V^T is written
@@ -360,6 +381,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const int col = col0 + jj, layer = col / (2 * a.kv_d), w = col - layer * 2 * a.kv_d;
             if (col < N && w >= a.kv_d && lane < nrows) {
               const float x = v[jj] * a.alpha * a.kv_scale;
+              range_check(x, a.range_flag);
               const __half h = __float2half_rn(x);
               const long long o = ((long long)layer * a.kv_d + (w - a.kv_d)) * a.vt_ld + grow;
               a.vt_hi[o] = h;
@@ -386,6 +408,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             for (int rr = 0; rr < nrows; ++rr) {
               const long long grow = (long long)ti.row_base + rbase + rr;
               const float x = ebuf[rr * 33 + lane] * a.alpha * a.kv_scale;
+              range_check(x, a.range_flag);
               const __half h = __float2half_rn(x);
               const long long o = grow * a.k_ld + (long long)kv_layer * a.kv_d + kv_w;
               a.k_hi[o] = h;
@@ -505,6 +528,7 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
     GR_TC_EPI(EPI_BIAS_RESID)
     GR_TC_EPI(EPI_MULVEC)
     GR_TC_EPI(EPI_KV_SPLIT)
+    GR_TC_EPI(EPI_STORE_LSE)
     default: return set_err(GR4AD_ERR_UNSUPPORTED, "tc epilogue %d", epi);
   }
 #undef GR_TC_EPI

@@ -22,6 +22,11 @@ struct TcArgs : GemmArgs {
   long long k_ld, vt_ld;
   float kv_scale;
   int kv_d;
+  int *range_flag;  // EPI_KV_SPLIT: set when a scaled value leaves the fp16 range
+  // EPI_STORE_LSE: lse_part[row * lse_ld + col / 128] = (max, sum exp(x - max))
+  // over the row's columns [128 j, 128 j + 128) (merged by lse_merge)
+  float2 *lse_part;
+  int lse_ld;
 };
 
 // A is (a_rows, a_cols) with ld lda, B is (b_rows, b_cols) K-major with ld ldb;
@@ -35,6 +40,6 @@ int transpose(const float *src, long long lds, float *dst, long long ldd, int ro
               cudaStream_t st);
 // as transpose, writing the fp16 split of scale * src^T: dst_hi + dst_lo
 int transpose_split16(const float *src, long long lds, __half *dst_hi, __half *dst_lo,
-                      long long ldd, int rows, int cols, float scale, cudaStream_t st);
+                      long long ldd, int rows, int cols, float scale, int *flag, cudaStream_t st);
 
 }  // namespace gr

@@ -84,11 +84,24 @@ self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
   float acc[kMaxPos];
 #pragma unroll
   for (int t = 0; t < kMaxPos; ++t) acc[t] = 0.f;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    float qj = q[j];
+  const bool vec = (d % 4 == 0) && (ld3 % 4 == 0);  // 16-B rows: float4 gathers
+  if (vec) {
+    for (int j = threadIdx.x * 4; j < d; j += blockDim.x * 4) {
+      const float4 q4 = *reinterpret_cast<const float4 *>(q + j);
 #pragma unroll
-    for (int t = 0; t < kMaxPos; ++t)
-      if (t < np) acc[t] = fmaf(qj, qkv[(long long)arow[t] * ld3 + d + j], acc[t]);
+      for (int t = 0; t < kMaxPos; ++t)
+        if (t < np) {
+          const float4 k4 = *reinterpret_cast<const float4 *>(qkv + (long long)arow[t] * ld3 + d + j);
+          acc[t] = fmaf(q4.x, k4.x, fmaf(q4.y, k4.y, fmaf(q4.z, k4.z, fmaf(q4.w, k4.w, acc[t]))));
+        }
+    }
+  } else {
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      float qj = q[j];
+#pragma unroll
+      for (int t = 0; t < kMaxPos; ++t)
+        if (t < np) acc[t] = fmaf(qj, qkv[(long long)arow[t] * ld3 + d + j], acc[t]);
+    }
   }
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
@@ -110,6 +123,23 @@ self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
     for (int t = 0; t < np; ++t) p[t] = expf(sc[t] - lse);
   }
   __syncthreads();
+  if (vec && ldo % 4 == 0) {
+    for (int j = threadIdx.x * 4; j < d; j += blockDim.x * 4) {
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < kMaxPos; ++t)
+        if (t < np) {
+          const float4 v4 =
+              *reinterpret_cast<const float4 *>(qkv + (long long)arow[t] * ld3 + 2 * d + j);
+          o.x = fmaf(p[t], v4.x, o.x);
+          o.y = fmaf(p[t], v4.y, o.y);
+          o.z = fmaf(p[t], v4.z, o.z);
+          o.w = fmaf(p[t], v4.w, o.w);
+        }
+      *reinterpret_cast<float4 *>(out + (long long)r * ldo + j) = o;
+    }
+    return;
+  }
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     float o = 0.f;
     for (int t = 0; t < np; ++t) o = fmaf(p[t], qkv[(long long)arow[t] * ld3 + 2 * d + j], o);
@@ -176,6 +206,30 @@ row_lse_kernel(const float *__restrict__ logits, long long ld, int rows, int V,
   if (lane == 0) red[wid] = s;
   __syncthreads();
   if (threadIdx.x == 0) info[r] = make_float2(mx, logf(red[0] + red[1] + red[2] + red[3]));
+}
+
+// (max, log sum exp) per row from the logits GEMM's per-128-column partials
+// (EPI_STORE_LSE): warp per row
+__global__ void lse_merge_kernel(const float2 *__restrict__ part, int n_part, int rows,
+                                 float2 *info) {
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  float m = -INFINITY;
+  for (int j = lane; j < n_part; j += 32) m = fmaxf(m, part[(long long)r * n_part + j].x);
+  m = warp_max(m);
+  float s = 0.f;
+  for (int j = lane; j < n_part; j += 32) {
+    const float2 p2 = part[(long long)r * n_part + j];
+    if (p2.x != -INFINITY) s += p2.y * expf(p2.x - m);
+  }
+  s = warp_sum(s);
+  if (lane == 0) info[r] = make_float2(m, logf(s));
+}
+
+int lse_merge(const float2 *part, int n_part, int rows, float2 *info, cudaStream_t st) {
+  if (rows <= 0) return GR4AD_OK;
+  GR_LAUNCH(KC_ROW_LSE, st, lse_merge_kernel<<<(rows + 7) / 8, 256, 0, st>>>(part, n_part, rows, info));
+  return GR4AD_OK;
 }
 
 int row_lse(const float *logits, long long ld, int rows, int V, float2 *info,
@@ -400,9 +454,32 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
     auto sbin = [&](float s) -> unsigned { return (unsigned)fminf((Rs - s) * scale, 2047.0f); };
     int cur = -1;
     unsigned cnt = 0;
+    // 16-B rows: float4 loads, four candidates per lane and load
+    const bool vec4 = !CACHE && c.V % 4 == 0 && c.ld % 4 == 0;
     for (int r = wid; r < c.n_rows; r += kSelWarps) {
       const float cr = c.cum[c.hist0 + c.row0 + r];
       const float2 ri = c.rowinfo ? c.rowinfo[c.row0 + r] : make_float2(0.f, 0.f);
+      if (vec4) {
+        const float4 *row4 = reinterpret_cast<const float4 *>(c.logits + (long long)(c.row0 + r) * c.ld);
+#pragma unroll 4
+        for (int v4 = lane; v4 < c.V / 4; v4 += 32) {
+          const float4 l4 = row4[v4];
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float s = cr + (c.rowinfo ? ((lv[q] - ri.x) - ri.y) : lv[q]);
+            const int bin = (int)sbin(s);
+            if (bin == cur) {
+              ++cnt;
+            } else {
+              if (cnt) atomicAdd(&hist[cur], cnt);
+              cur = bin;
+              cnt = 1;
+            }
+          }
+        }
+        continue;
+      }
       for (int v = lane; v < c.V; v += 32) {
         const float lg = c.logits[(long long)(c.row0 + r) * c.ld + v];
         const float s = cr + (c.rowinfo ? ((lg - ri.x) - ri.y) : lg);
@@ -437,6 +514,43 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
       for (int r = wid; r < c.n_rows; r += kSelWarps) {
         const float cr = c.cum[c.hist0 + c.row0 + r];
         const float2 ri = c.rowinfo ? c.rowinfo[c.row0 + r] : make_float2(0.f, 0.f);
+        if (vec4) {
+          const float4 *row4 =
+              reinterpret_cast<const float4 *>(c.logits + (long long)(c.row0 + r) * c.ld);
+#pragma unroll 4
+          for (int v40 = 0; v40 < c.V / 4; v40 += 32) {
+            const int v4 = v40 + lane;
+            float4 l4 = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            if (v4 < c.V / 4) l4 = row4[v4];
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+            unsigned pm = 0;
+            float sv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              sv[q] = cr + (c.rowinfo ? ((lv[q] - ri.x) - ri.y) : lv[q]);
+              if (v4 < c.V / 4 && sbin(sv[q]) <= (unsigned)wb) pm |= 1u << q;
+            }
+            if (__any_sync(0xffffffffu, pm != 0)) {
+              const unsigned np = __popc(pm);
+              unsigned incl = np;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+              }
+              unsigned base = 0;
+              if (lane == 31) base = atomicAdd(&s_gt_pos, incl);
+              base = __shfl_sync(0xffffffffu, base, 31) + incl - np;
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if ((pm >> q) & 1u) {
+                  const unsigned fi = (unsigned)((long long)r * c.V + 4 * v4 + q);
+                  sbuf[base++] = ((unsigned long long)f2ord(sv[q]) << 32) | (0xFFFFFFFFu - fi);
+                }
+            }
+          }
+          continue;
+        }
         for (int v0 = 0; v0 < c.V; v0 += 32) {
           const int v = v0 + lane;
           float s = -INFINITY;
@@ -723,7 +837,7 @@ int transpose(const float *src, long long lds, float *dst, long long ldd, int ro
 // dst = split of scale * src^T into fp16 hi + lo (the tensor-core B operands)
 __global__ void transpose_split16_kernel(const float *__restrict__ src, long long lds,
                                          __half *dst_hi, __half *dst_lo, long long ldd, int rows,
-                                         int cols, float scale) {
+                                         int cols, float scale, int *flag) {
   __shared__ float tile[32][33];
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
@@ -735,6 +849,7 @@ __global__ void transpose_split16_kernel(const float *__restrict__ src, long lon
     int c = c0 + i, r = r0 + threadIdx.x;
     if (r < rows && c < cols) {
       const float x = tile[threadIdx.x][i] * scale;
+      range_check(x, flag);
       const __half h = __float2half_rn(x);
       dst_hi[(long long)c * ldd + r] = h;
       dst_lo[(long long)c * ldd + r] = __float2half_rn(x - __half2float(h));
@@ -743,11 +858,11 @@ __global__ void transpose_split16_kernel(const float *__restrict__ src, long lon
 }
 
 int transpose_split16(const float *src, long long lds, __half *dst_hi, __half *dst_lo,
-                      long long ldd, int rows, int cols, float scale, cudaStream_t st) {
+                      long long ldd, int rows, int cols, float scale, int *flag, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return GR4AD_OK;
   dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32));
   GR_LAUNCH(KC_SMALL, st, transpose_split16_kernel<<<grid, dim3(32, 8), 0, st>>>(
-                              src, lds, dst_hi, dst_lo, ldd, rows, cols, scale));
+                              src, lds, dst_hi, dst_lo, ldd, rows, cols, scale, flag));
   return GR4AD_OK;
 }
 

@@ -27,6 +27,7 @@ int level_input(int t, int rows, int d, const float *bos, const float *emb_prev,
                 cudaStream_t st);
 
 // per-row (max, log sum exp(x - max)) (beam.py:92-95)
+int lse_merge(const float2 *part, int n_part, int rows, float2 *info, cudaStream_t st);
 int row_lse(const float *logits, long long ld, int rows, int V, float2 *info,
             cudaStream_t st);
 

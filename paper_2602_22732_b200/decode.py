@@ -154,8 +154,49 @@ class BeamDecoder:
     def replay(self):
         self.graph.replay()
 
+    def capture_host(self, host_features, warmup=1):
+        """Capture one CUDA graph from pinned host features to pinned host
+        results: the features' H2D copy, the decode, and the D2H copies of
+        count / tokens / score (``self.host_out``).  ``replay_host`` then
+        serves a batch with a single launch on the current stream."""
+        if not host_features.is_pinned():
+            raise ValueError("capture_host needs pinned host features")
+        self._host_in = host_features
+        self._dev_in = torch.empty(host_features.shape, dtype=torch.float32, device=self.device)
+        self.host_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                         for t in (self.count, self.tokens, self.score)]
+
+        def body():
+            self._dev_in.copy_(self._host_in, non_blocking=True)
+            self.run(features=self._dev_in)
+            for h, t in zip(self.host_out, (self.count, self.tokens, self.score)):
+                h.copy_(t, non_blocking=True)
+
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                body()
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            body()
+        self.host_graph = g
+        return g
+
+    def replay_host(self):
+        self.host_graph.replay()
+
     # -- results -----------------------------------------------------------
+    def check_range(self):
+        """Raise if the last decode's fp16 operand splits left their range
+        (tensor-core paths only; gr4ad_range_status)."""
+        N.check(N.lib.gr4ad_range_status(C.byref(self.dims), C.byref(self.batch),
+                                         C.c_void_p(self.workspace.data_ptr()),
+                                         _stream_handle(self.device)))
+
     def host_results(self):
+        self.check_range()
         count = self.count.cpu().numpy()[: self.n_requests]
         toks = self.tokens.cpu().numpy().reshape(-1, self.max_out, self.T)
         score = self.score.cpu().numpy().reshape(-1, self.max_out)

@@ -137,7 +137,7 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
 
     ``path`` picks the decode kernels: "auto" (the fused per-request kernel
     when the working set fits on chip, else the layered batch path with
-    tcgen05 3xTF32 GEMMs for d >= 64, else CUDA-core GEMMs), "fused",
+    tcgen05 3xFP16 GEMMs for d >= 64, else CUDA-core GEMMs), "fused",
     "tensor" (layered + tcgen05) or "layered" (layered + CUDA-core).
 
     ``contexts`` are projected X matrices, or ``features`` raw (S, F)

@@ -1,5 +1,5 @@
 """Numerics of the decode's GEMMs through the C ABI (gr4ad_gemm) against a
-float64 torch reference: the CUDA-core fp32 path and the tcgen05 3xTF32
+float64 torch reference: the CUDA-core fp32 path and the tcgen05 3xFP16
 path must both be fp32-faithful (relative error ~1e-6, far below TF32's
 ~1e-3), since beam lists depend on it (SURVEY §7 hard part 1)."""
 
@@ -38,5 +38,5 @@ def test_gemm_fp32_faithful(shape, backend):
     scale = (A.double().abs() @ BT.double().abs().T)  # error bound scale per entry
     rel = ((got - ref).abs() / scale.clamp_min(1e-30)).max().item()
     print(f"backend {backend} shape {shape}: max scaled error {rel:.3e}")
-    # fp32 accumulation over K: ~K^0.5 * 2^-24 typical; 3xTF32 drops lo.lo (~2^-22)
+    # fp32 accumulation over K: ~K^0.5 * 2^-24 typical; 3xFP16 drops lo.lo (~2^-22)
     assert rel < 1e-5, f"backend {backend} shape {shape}: max scaled error {rel:.3e}"

@@ -174,7 +174,7 @@ def test_c2_golden_reference(golden_small):
 @pytest.mark.parametrize("path", ["tensor", "layered"])
 def test_c3_golden_reference(golden_c3, path):
     """Full C3 shape: d=1024, L=8, K=5, S=1024, V=4096^3, widths 512^3, on
-    the tcgen05 3xTF32 path (auto for d >= 64) and the CUDA-core path."""
+    the tcgen05 3xFP16 path (auto for d >= 64) and the CUDA-core path."""
     M, S = _pkg()
     c = golden_c3["config"]
     cfg = M.DecoderConfig(c["feat_dim"], c["d"], c["d_ff"], c["n_layers"], c["trunk_depth"],
@@ -299,3 +299,18 @@ def test_tensor_path_mid_model():
                                    trunk_depth=k_depth, value_rerank=rerank,
                                    representatives=reps)
             check_parity(want, [(sid.tokens, s) for sid, s in got[i]], f"d64 K={k_depth}[{i}]")
+
+
+@pytest.mark.parametrize("path", ["fused", "tensor"])
+def test_fp16_split_range_is_reported(path):
+    """Context K/V far outside the fp16 split range (|K| >= 256 after the
+    x256 scale) must raise instead of returning saturated scores; the
+    CUDA-core path decodes the same input (gr4ad_range_status)."""
+    M, S = _pkg()
+    model = _model(M, C1_MODEL)
+    feats = [c_features(0, 256) * 1e5]
+    sched = S.BeamSchedule(C1_WIDTHS, C1_WIDTHS[-1])
+    with pytest.raises(RuntimeError, match="fp16"):
+        S.beam_search_batch(model, features=feats, schedules=sched, path=path)
+    got = S.beam_search_batch(model, features=feats, schedules=sched, path="layered")
+    assert len(got[0]) >= 1
