@@ -89,12 +89,13 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
 }
 
 // K-major SWIZZLE_64B smem matrix descriptor (rows of 64 B = 32 fp16, 8-row
-// atoms of 512 B): start>>4 | LBO=1 (16 B) | SBO=512>>4 | version 1 | layout 4
-__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+// core-matrix atoms of 512 B, consecutive atoms sbo bytes apart):
+// start>>4 | LBO=1 (16 B) | SBO | version 1 | layout 4
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)4 << 61;
   return d;
@@ -179,24 +180,28 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, int tile, int til
   return ti;
 }
 
-// fp32 tile [rows][32] in SWIZZLE_128B (as TMA lands it) -> fp16 hi / lo
-// tiles [rows][32] in SWIZZLE_64B (the UMMA operand layout); a task is 8
-// consecutive k of one row (two 16-B fp32 chunks -> one 16-B chunk each)
-__device__ __forceinline__ void convert_tile(const unsigned char *src, unsigned char *hi,
-                                             unsigned char *lo, int rows, int t, int nt) {
-  for (int task = t; task < rows * 4; task += nt) {
-    const int r = task >> 2, c8 = task & 3;
-    const float4 x0 = *reinterpret_cast<const float4 *>(src + r * 128 + (((2 * c8) ^ (r & 7)) << 4));
-    const float4 x1 =
-        *reinterpret_cast<const float4 *>(src + r * 128 + (((2 * c8 + 1) ^ (r & 7)) << 4));
+// In-place split of a landed fp32 tile [rows][32] (SWIZZLE_128B, as TMA
+// writes it) into the fp16 hi / lo UMMA operand tiles (SWIZZLE_64B): the
+// 1024 B of every 8-row group become its 512-B hi atom followed by its 512-B
+// lo atom, so each group converts locally (one warp, no block barrier) and
+// the operand descriptors step 1024 B between atoms.  A lane handles 8
+// consecutive k of one row (two 16-B fp32 chunks -> one 16-B hi + one lo).
+__device__ __forceinline__ void convert_groups(unsigned char *tile, int rows, int warp_idx,
+                                               int n_warps) {
+  const int lane = threadIdx.x & 31, rr = lane >> 2, c8 = lane & 3;
+  for (int grp = warp_idx; grp < rows / 8; grp += n_warps) {
+    unsigned char *g = tile + grp * 1024;
+    const float4 x0 = *reinterpret_cast<const float4 *>(g + rr * 128 + (((2 * c8) ^ rr) << 4));
+    const float4 x1 = *reinterpret_cast<const float4 *>(g + rr * 128 + (((2 * c8 + 1) ^ rr) << 4));
     uint4 h, l;
     split_f16x2(x0.x, x0.y, 1.f, h.x, l.x);
     split_f16x2(x0.z, x0.w, 1.f, h.y, l.y);
     split_f16x2(x1.x, x1.y, 1.f, h.z, l.z);
     split_f16x2(x1.z, x1.w, 1.f, h.w, l.w);
-    const int o = r * 64 + ((c8 ^ ((r >> 1) & 3)) << 4);
-    *reinterpret_cast<uint4 *>(hi + o) = h;
-    *reinterpret_cast<uint4 *>(lo + o) = l;
+    __syncwarp();  // the group's fp32 is in registers before it is overwritten
+    const int o = rr * 64 + ((c8 ^ (rr >> 1)) << 4);
+    *reinterpret_cast<uint4 *>(g + o) = h;
+    *reinterpret_cast<uint4 *>(g + 512 + o) = l;
   }
 }
 
@@ -211,12 +216,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  constexpr int A32 = BM * BK * 4;   // fp32 landing tile
-  constexpr int A16 = BM * BK * 2;   // fp16 hi (or lo) tile
-  constexpr int B16 = BN * BK * 2;
-  constexpr int B32 = BSPLIT ? 0 : BN * BK * 4;
-  // stage: [A32][B32][Ahi][Alo][Bhi][Blo]
-  constexpr int STAGE_BYTES = A32 + B32 + 2 * A16 + 2 * B16;
+  constexpr int A32 = BM * BK * 4;   // fp32 landing tile, split in place (hi / lo atoms)
+  constexpr int B16 = BN * BK * 2;   // pre-split B: fp16 hi tile, then lo tile
+  constexpr int B32 = BN * BK * 4;   // fp32 B landing tile, split in place
+  // stage: [A][B]; A (and an fp32 B) hold interleaved 512-B hi / lo atoms
+  constexpr int STAGE_BYTES = A32 + (BSPLIT ? 2 * B16 : B32);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
   uint64_t *conv = full + STAGES;
   uint64_t *empty = conv + STAGES;
@@ -262,7 +266,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           mbar_expect_tx(&full[s], A32 + (BSPLIT ? 2 * B16 : B32));
           tma_load_2d(st, &tmA, &full[s], kt * BK, ti.row_base + ti.m0);
           if (BSPLIT) {
-            unsigned char *bh = st + A32 + 2 * A16;
+            unsigned char *bh = st + A32;
             tma_load_2d(bh, &tmB, &full[s], ti.b_k_base + kt * BK, ti.b_row_base + ti.n0);
             tma_load_2d(bh + B16, &tmBlo, &full[s], ti.b_k_base + kt * BK, ti.b_row_base + ti.n0);
           } else {
@@ -289,16 +293,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const int s = kg % STAGES;
           mbar_wait(&conv[s], (kg / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t st = smem_u32(smem + s * STAGE_BYTES) + A32 + B32;
-          const uint32_t a_hi = st, a_lo = st + A16;
-          const uint32_t b_hi = st + 2 * A16, b_lo = b_hi + B16;
+          const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t a_hi = st, a_lo = st + 512;  // interleaved atoms, 1024 B apart
+          const uint32_t b_hi = st + A32, b_lo = BSPLIT ? b_hi + B16 : b_hi + 512;
+          constexpr uint32_t b_sbo = BSPLIT ? 512 : 1024;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint32_t off = k * 32;  // 16 fp16 = 32 B along the swizzled row
             const uint32_t acc0 = (kt > 0 || k > 0) ? 1u : 0u;
-            mma_f16(d_tmem, sw64_desc(a_lo + off), sw64_desc(b_hi + off), idesc, acc0);
-            mma_f16(d_tmem, sw64_desc(a_hi + off), sw64_desc(b_lo + off), idesc, 1u);
-            mma_f16(d_tmem, sw64_desc(a_hi + off), sw64_desc(b_hi + off), idesc, 1u);
+            mma_f16(d_tmem, sw64_desc(a_lo + off, 1024), sw64_desc(b_hi + off, b_sbo), idesc, acc0);
+            mma_f16(d_tmem, sw64_desc(a_hi + off, 1024), sw64_desc(b_lo + off, b_sbo), idesc, 1u);
+            mma_f16(d_tmem, sw64_desc(a_hi + off, 1024), sw64_desc(b_hi + off, b_sbo), idesc, 1u);
           }
           mma_commit(&empty[s]);  // frees the stage when these MMAs complete
         }
@@ -308,7 +313,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
   } else if (warp < kEpiWarp0) {
     // ---- converters: landed fp32 tiles -> fp16 hi / lo operand tiles
-    const int ct = threadIdx.x - 64, nct = 32 * kConvWarps;
+    const int cw = warp - 2;  // converter warp index
     int kg = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN);
@@ -318,9 +323,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int s = kg % STAGES;
         mbar_wait(&full[s], (kg / STAGES) & 1);
         unsigned char *st = smem + s * STAGE_BYTES;
-        unsigned char *h16 = st + A32 + B32;
-        convert_tile(st, h16, h16 + A16, BM, ct, nct);
-        if (!BSPLIT) convert_tile(st + A32, h16 + 2 * A16, h16 + 2 * A16 + B16, BN, ct, nct);
+        convert_groups(st, BM, cw, kConvWarps);
+        if (!BSPLIT) convert_groups(st + A32, BN, cw, kConvWarps);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[s]);
@@ -504,8 +508,7 @@ static int num_sms() {
 template <int BN, int STAGES, bool BSPLIT>
 static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl,
                      const TcArgs &a, int epi, cudaStream_t st) {
-  constexpr size_t stage = (size_t)BM * BK * 4 + (BSPLIT ? 0 : (size_t)BN * BK * 4) +
-                           2 * (size_t)BM * BK * 2 + 2 * (size_t)BN * BK * 2;
+  constexpr size_t stage = (size_t)BM * BK * 4 + (size_t)BN * BK * 4;  // (in-place splits)
   constexpr size_t smem = 1024 + STAGES * stage + 256 + 4 * 32 * 33 * sizeof(float);
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
@@ -558,12 +561,12 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
     if (a.ldb % 8 != 0) return set_err(GR4AD_ERR_UNSUPPORTED, "fp16 B rows need ldb %% 8 == 0");
     GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, box_n));
     GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, box_n));
-    return wide ? launch_tc<256, 3, true>(ma, mb, mbl, a, epi, st)
-                : launch_tc<128, 4, true>(ma, mb, mbl, a, epi, st);
+    return wide ? launch_tc<256, 4, true>(ma, mb, mbl, a, epi, st)
+                : launch_tc<128, 6, true>(ma, mb, mbl, a, epi, st);
   }
   GR_TRY(make_map(&mb, a.B, false, b_rows, b_cols, a.ldb, box_n));
-  return wide ? launch_tc<256, 2, false>(ma, mb, mb, a, epi, st)
-              : launch_tc<128, 3, false>(ma, mb, mb, a, epi, st);
+  return wide ? launch_tc<256, 4, false>(ma, mb, mb, a, epi, st)
+              : launch_tc<128, 6, false>(ma, mb, mb, a, epi, st);
 }
 
 }  // namespace gr
