@@ -396,55 +396,93 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) ebuf[lane * 33 + jj] = v[jj];
         __syncwarp();
-        const int col = col0 + lane;
-        const bool cok = col < N;
-        float bcol = 0.f;
-        if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID)
-          bcol = cok ? a.bias[col] : 0.f;
-        int kv_layer = 0, kv_w = 0;
-        if (EPI == EPI_KV_SPLIT) {
-          kv_layer = col / (2 * a.kv_d);
-          kv_w = col - kv_layer * 2 * a.kv_d;
+        // lane -> (row lr of every 4, columns c4..c4+3): float4 global traffic,
+        // 8 row groups per 32-column chunk
+        const int lr = lane >> 3, c4 = (lane & 7) * 4;
+        const int col = col0 + c4;
+        const bool vec = col + 4 <= N && (a.ldc % 4) == 0 &&
+                         (EPI != EPI_RESID && EPI != EPI_BIAS_RESID || (a.ldr % 4) == 0) &&
+                         (EPI != EPI_MULVEC || (a.vec_ld % 4) == 0) &&
+                         (EPI != EPI_KV_SPLIT || (a.k_ld % 4) == 0);
+        float4 bcol = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID) {
+          bcol.x = col < N ? a.bias[col] : 0.f;
+          bcol.y = col + 1 < N ? a.bias[col + 1] : 0.f;
+          bcol.z = col + 2 < N ? a.bias[col + 2] : 0.f;
+          bcol.w = col + 3 < N ? a.bias[col + 3] : 0.f;
         }
-        if (EPI == EPI_KV_SPLIT) {
-          if (cok && kv_w < a.kv_d) {
-#pragma unroll 4
-            for (int rr = 0; rr < nrows; ++rr) {
-              const long long grow = (long long)ti.row_base + rbase + rr;
-              const float x = ebuf[rr * 33 + lane] * a.alpha * a.kv_scale;
-              range_check(x, a.range_flag);
-              const __half h = __float2half_rn(x);
-              const long long o = grow * a.k_ld + (long long)kv_layer * a.kv_d + kv_w;
-              a.k_hi[o] = h;
-              a.k_lo[o] = __float2half_rn(x - __half2float(h));
+        // operands first (all loads in flight; C may alias R), then the stores
+        float4 xo[8];
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = it * 4 + lr;
+          const long long grow = (long long)ti.row_base + rbase + rr;
+          float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (rr < nrows && col < N) {
+            const float *src = nullptr;
+            if (EPI == EPI_RESID || EPI == EPI_BIAS_RESID) src = a.R + grow * a.ldr + col;
+            else if (EPI == EPI_MULVEC) src = a.vec + (long long)a.row_req[grow] * a.vec_ld + col;
+            if (src) {
+              if (vec) {
+                o = *reinterpret_cast<const float4 *>(src);
+              } else {
+                o.x = src[0];
+                if (col + 1 < N) o.y = src[1];
+                if (col + 2 < N) o.z = src[2];
+                if (col + 3 < N) o.w = src[3];
+              }
             }
           }
-        } else if (cok) {
-          // operands first (32 independent loads in flight; C may alias R),
-          // then the stores
-          float xv[32];
+          xo[it] = o;
+        }
 #pragma unroll
-          for (int rr = 0; rr < 32; ++rr) {
-            const long long grow = (long long)ti.row_base + rbase + rr;
-            float o = 0.f;
-            if (rr < nrows) {
-              if (EPI == EPI_RESID || EPI == EPI_BIAS_RESID) o = a.R[grow * a.ldr + col];
-              else if (EPI == EPI_MULVEC) o = a.vec[(long long)a.row_req[grow] * a.vec_ld + col];
-            }
-            xv[rr] = o;
+        for (int it = 0; it < 8; ++it) {
+          const int rr = it * 4 + lr;
+          if (rr >= nrows || col >= N) continue;
+          const long long grow = (long long)ti.row_base + rbase + rr;
+          float x[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = ebuf[rr * 33 + c4 + q] * a.alpha;
+          const float ob[4] = {bcol.x, bcol.y, bcol.z, bcol.w};
+          const float oo[4] = {xo[it].x, xo[it].y, xo[it].z, xo[it].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (EPI == EPI_BIAS) x[q] = x[q] + ob[q];
+            else if (EPI == EPI_BIAS_GELU) x[q] = gelu_tanh(x[q] + ob[q]);
+            else if (EPI == EPI_RESID) x[q] = oo[q] + x[q];
+            else if (EPI == EPI_BIAS_RESID) x[q] = oo[q] + (x[q] + ob[q]);
+            else if (EPI == EPI_MULVEC) x[q] = oo[q] * x[q];
           }
+          if (EPI == EPI_KV_SPLIT) {
+            // K part of the layer (columns never straddle K / V for d % 4 == 0)
+            const int layer = col / (2 * a.kv_d), w = col - layer * 2 * a.kv_d;
+            if (w < a.kv_d) {
+              const long long o = grow * a.k_ld + (long long)layer * a.kv_d + w;
+              __half hq[4], lq[4];
 #pragma unroll
-          for (int rr = 0; rr < 32; ++rr) {
-            if (rr < nrows) {
-              const long long grow = (long long)ti.row_base + rbase + rr;
-              float x = ebuf[rr * 33 + lane] * a.alpha;
-              if (EPI == EPI_BIAS) x = x + bcol;
-              else if (EPI == EPI_BIAS_GELU) x = gelu_tanh(x + bcol);
-              else if (EPI == EPI_RESID) x = xv[rr] + x;
-              else if (EPI == EPI_BIAS_RESID) x = xv[rr] + (x + bcol);
-              else if (EPI == EPI_MULVEC) x = xv[rr] * x;
-              a.C[grow * a.ldc + col] = x;
+              for (int q = 0; q < 4; ++q) {
+                const float xs = x[q] * a.kv_scale;
+                range_check(xs, a.range_flag);
+                hq[q] = __float2half_rn(xs);
+                lq[q] = __float2half_rn(xs - __half2float(hq[q]));
+              }
+              if (vec) {
+                *reinterpret_cast<uint2 *>(a.k_hi + o) = *reinterpret_cast<const uint2 *>(hq);
+                *reinterpret_cast<uint2 *>(a.k_lo + o) = *reinterpret_cast<const uint2 *>(lq);
+              } else {
+                for (int q = 0; q < 4 && col + q < N; ++q) {
+                  a.k_hi[o + q] = hq[q];
+                  a.k_lo[o + q] = lq[q];
+                }
+              }
             }
+            continue;
+          }
+          float *dst = a.C + grow * a.ldc + col;
+          if (vec) {
+            *reinterpret_cast<float4 *>(dst) = make_float4(x[0], x[1], x[2], x[3]);
+          } else {
+            for (int q = 0; q < 4 && col + q < N; ++q) dst[q] = x[q];
           }
         }
         __syncwarp();
