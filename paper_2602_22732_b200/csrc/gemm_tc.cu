@@ -448,7 +448,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             if (EPI == EPI_BIAS) x[q] = x[q] + ob[q];
-            else if (EPI == EPI_BIAS_GELU) x[q] = gelu_tanh(x[q] + ob[q]);
+            else if (EPI == EPI_BIAS_GELU) x[q] = gelu_tanh_fast(x[q] + ob[q]);
             else if (EPI == EPI_RESID) x[q] = oo[q] + x[q];
             else if (EPI == EPI_BIAS_RESID) x[q] = oo[q] + (x[q] + ob[q]);
             else if (EPI == EPI_MULVEC) x[q] = oo[q] * x[q];
