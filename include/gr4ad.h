@@ -100,13 +100,17 @@ typedef struct {
   const int *valid_prefix_count; /* host [n_levels] */
   /* 0: auto -- the fused per-request kernel when a request's working set
    * fits on chip (d in {16,32}, d_ff in {d,2d}, S <= 32d, widths <= 2048,
-   * no masking), else the layered batch path, with tcgen05 3xTF32 GEMMs
+   * no masking), else the layered batch path, with tcgen05 3xFP16 GEMMs
    * when d >= 64 (and d, d_ff, F, V multiples of 4); 1: layered with
    * CUDA-core GEMMs; 2: fused (its warp-level tensor-core variant -- mma.sync
-   * 3xTF32 -- when d = 16, else CUDA cores); 3: layered with tcgen05 GEMMs;
+   * 3xFP16 -- when d = 16, else CUDA cores); 3: layered with tcgen05 GEMMs;
    * 4: fused on CUDA cores only.  Forcing an ineligible path returns
    * GR4AD_ERR_UNSUPPORTED. */
   int decode_path;
+  /* 1: the workspace already holds this snapshot's derived weight copies
+   * (gr4ad_prepare_weights: fragment-ordered / K-major fp16 hi+lo splits);
+   * the decode then skips rebuilding them.  0: rebuilt every call. */
+  int weights_prepared;
 } gr4ad_batch;
 
 /* Results: for request b, count[b] entries in selection order (or value
@@ -162,6 +166,16 @@ int gr4ad_beam_search_run(const gr4ad_dims *dims, const gr4ad_weights *w,
                           const gr4ad_batch *batch, const float *features,
                           const float *context, gr4ad_results *out, void *workspace,
                           size_t workspace_bytes, void *stream);
+
+/* Build the snapshot-derived weight copies a decode of this batch shape uses
+ * (fused path: mma fragments + trunk queries; tensor-core path: K-major fp16
+ * hi/lo splits) into `workspace`, once per snapshot (the SnapshotStore
+ * contract, engine.py:17-36); then set batch->weights_prepared.  Synchronises
+ * `stream`; returns GR4AD_ERR_UNSUPPORTED if a weight leaves the fp16 split
+ * range. */
+int gr4ad_prepare_weights(const gr4ad_dims *dims, const gr4ad_weights *w,
+                          const gr4ad_batch *batch, void *workspace, size_t workspace_bytes,
+                          void *stream);
 
 /* fp16 split range of the last decode in `workspace` (synchronises `stream`).
  * The tensor-core paths split weights (x 2048) and the context K / V (x 256)

@@ -31,7 +31,7 @@ EXPORTS = (
     "gr4ad_beam_search_run", "gr4ad_context_process", "gr4ad_encoder_kv",
     "gr4ad_topk_precut", "gr4ad_topk_workspace_bytes", "gr4ad_project_topk",
     "gr4ad_project_topk_workspace_bytes", "gr4ad_gemm", "gr4ad_score_sequences",
-    "gr4ad_score_workspace_bytes", "gr4ad_range_status",
+    "gr4ad_score_workspace_bytes", "gr4ad_range_status", "gr4ad_prepare_weights",
 )
 
 _P = C.c_void_p
@@ -61,7 +61,8 @@ class Batch(C.Structure):
                 ("widths", C.POINTER(C.c_int)), ("trunk_depth", C.c_int),
                 ("value_rerank", C.c_int), ("value_reps", _P),
                 ("valid_prefix", _P * MAX_LEVELS),
-                ("valid_prefix_count", C.POINTER(C.c_int)), ("decode_path", C.c_int)]
+                ("valid_prefix_count", C.POINTER(C.c_int)), ("decode_path", C.c_int),
+                ("weights_prepared", C.c_int)]
 
 PATH_AUTO, PATH_LAYERED, PATH_FUSED = 0, 1, 2
 
@@ -91,6 +92,8 @@ def _load():
     lib.gr4ad_beam_search_run.argtypes = run_args
     lib.gr4ad_prepare.argtypes = [C.POINTER(Dims), C.POINTER(Batch), _P, C.c_size_t, _P]
     lib.gr4ad_range_status.argtypes = [C.POINTER(Dims), C.POINTER(Batch), _P, _P]
+    lib.gr4ad_prepare_weights.argtypes = [C.POINTER(Dims), C.POINTER(Weights), C.POINTER(Batch),
+                                          _P, C.c_size_t, _P]
     lib.gr4ad_context_process.argtypes = [C.POINTER(Dims), C.POINTER(Weights), _P, C.c_int,
                                           _P, _P]
     lib.gr4ad_encoder_kv.argtypes = [C.POINTER(Dims), C.POINTER(Weights), _P, C.c_int,

@@ -101,6 +101,7 @@ struct Plan {
   size_t f_smem4 = 0;
   long long frag_f4 = 0;  // fragment-ordered weights (float4 count)
   size_t o_frag = 0, o_tu = 0;
+  bool weights_prepared = false;  // batch->weights_prepared
   size_t o_flag = 0;  // fp16 range flag (set by the operand splits, read by gr4ad_range_status)
 };
 
@@ -280,6 +281,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.F = dm->feat_dim;
   p.nb = dm->n_value_buckets;
   p.rerank = bt->value_rerank != 0;
+  p.weights_prepared = bt->weights_prepared != 0;
   p.n_pos = p.T + (p.rerank ? 1 : 0);
   p.stride = p.T + 1;
   p.n_lv = p.T + 1;
@@ -530,7 +532,7 @@ struct WeightsT {
 };
 
 static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, WeightsT &wt,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool launch = true) {
   __half *base = at<__half>(ws, p.o_WT);
   long long o = 0;
   int rc = GR4AD_OK;
@@ -538,7 +540,7 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
   auto tr = [&](const float *src, int rows, int cols) -> const __half * {
     __half *dst = base + o;
     o += ((long long)rows * cols + 63) / 64 * 64;
-    if (rc == GR4AD_OK)
+    if (rc == GR4AD_OK && launch)
       rc = transpose_split16(src, cols, dst, dst + p.wt_floats, rows, rows, cols, kWeightScale,
                              at<int>(ws, p.o_flag), st);
     return dst;
@@ -708,7 +710,7 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
   const int B = p.B, d = p.d, K = p.K;
   float *KV = at<float>(ws, p.o_KV), *Ht = at<float>(ws, p.o_Ht);
   if (p.tc) {
-    GR_TRY(prep_weights_t(p, w, ws, wt_store, st));
+    GR_TRY(prep_weights_t(p, w, ws, wt_store, st, !p.weights_prepared));
     wt = &wt_store;
     VT = at<float>(ws, p.o_VT);
   }
@@ -843,7 +845,7 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
                             at<float>(ws, p.o_tu), d, 2 * p.L * d, p.n_pos};
         f.trunk_u = jobs.tu.u;
       }
-      GR_TRY(frag_prep_launch(jobs, frag, range_flag, st));
+      if (!p.weights_prepared) GR_TRY(frag_prep_launch(jobs, frag, range_flag, st));
       return fused_mma_launch(f, B, p.f_smem4, st);
     }
     return fused_small_launch(f, B, p.f_smem, st);
@@ -1043,6 +1045,43 @@ int gr4ad_beam_search_run(const gr4ad_dims *dims, const gr4ad_weights *w,
   if (p.rerank && !batch->value_reps)
     return set_err(GR4AD_ERR_VALUE, "value_rerank requires bucket representatives");
   return run_plan(p, dims, w, batch, features, context, out, workspace, (cudaStream_t)stream);
+}
+
+int gr4ad_prepare_weights(const gr4ad_dims *dims, const gr4ad_weights *w,
+                          const gr4ad_batch *batch, void *workspace, size_t workspace_bytes,
+                          void *stream) {
+  Plan p;
+  GR_TRY(make_plan(dims, batch, p));
+  if (workspace_bytes < p.total)
+    return set_err(GR4AD_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, p.total);
+  if (p.B == 0) return GR4AD_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  void *ws = workspace;
+  int *flag = at<int>(ws, p.o_flag);
+  GR_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  if (p.fused && p.f_mma) {
+    static thread_local FragJobs jobs;  // ~7 KB: kept off the stack
+    FragIndex fi;
+    frag_layout(p, w, &jobs, &fi);
+    jobs.tu = TrunkUJob{};
+    if (p.K > 0 && p.d <= 32) {
+      const gr4ad_layer &L0 = w->layer[0];
+      jobs.tu = TrunkUJob{w->pos, L0.ln1_g, L0.ln1_b, L0.cross_Wq, w->cross_kv_W,
+                          at<float>(ws, p.o_tu), p.d, 2 * p.L * p.d, p.n_pos};
+    }
+    GR_TRY(frag_prep_launch(jobs, at<uint4>(ws, p.o_frag), flag, st));
+  } else if (p.tc) {
+    WeightsT wt;
+    GR_TRY(prep_weights_t(p, w, ws, wt, st, true));
+  }
+  int h = 0;
+  GR_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GR_CUDA(cudaStreamSynchronize(st));
+  if (h)
+    return set_err(GR4AD_ERR_UNSUPPORTED,
+                   "a weight exceeded the fp16 split range (|weight| < 32): decode with the "
+                   "CUDA-core path (decode_path layered / fused_simt)");
+  return GR4AD_OK;
 }
 
 int gr4ad_range_status(const gr4ad_dims *dims, const gr4ad_batch *batch, const void *workspace,

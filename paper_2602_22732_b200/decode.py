@@ -116,8 +116,19 @@ class BeamDecoder:
         N.check(N.lib.gr4ad_prepare(C.byref(self.dims), C.byref(bt),
                                     C.c_void_p(self.workspace.data_ptr()),
                                     self.workspace_bytes, _stream_handle(self.device)))
+        self._prepare_weights()
         self.graph = None
         self._graph_inputs = None
+
+    def _prepare_weights(self):
+        """Derived weight copies (mma fragments / K-major fp16 splits) built
+        once per bound snapshot; decodes then skip them (weights_prepared)."""
+        self.batch.weights_prepared = 0
+        N.check(N.lib.gr4ad_prepare_weights(C.byref(self.dims), C.byref(self.weights.struct),
+                                            C.byref(self.batch),
+                                            C.c_void_p(self.workspace.data_ptr()),
+                                            self.workspace_bytes, _stream_handle(self.device)))
+        self.batch.weights_prepared = 1
 
     def rebind(self, model):
         """Decode with another snapshot of the same config (hot swap).  The
@@ -126,6 +137,7 @@ class BeamDecoder:
         if model.config != self.cfg:
             raise ValueError("rebind needs a snapshot with the same DecoderConfig")
         self.weights = device_weights(model, self.device)
+        self._prepare_weights()
         self.graph = None
         self._graph_inputs = None
 
