@@ -378,18 +378,38 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (EPI == EPI_KV_SPLIT) {
           // [2i d, 2i d + d) -> K_i, [2i d + d, 2(i+1) d) -> V_i^T, both as fp16
           // hi / lo of kv_scale * x for the attention GEMMs; V^T is written
-          // straight from the row-per-lane registers (coalesced over rows)
+          // straight from the row-per-lane registers (coalesced over rows).
+          // With d % 32 == 0 a chunk lies wholly in one K or V block.
           const long long grow = (long long)ti.row_base + rbase + lane;
+          const int layer = col0 / (2 * a.kv_d), w0 = col0 - layer * 2 * a.kv_d;
+          if (a.kv_d % 32 == 0) {
+            if (w0 >= a.kv_d) {
+              if (lane < nrows) {
+                __half *vh = a.vt_hi + ((long long)layer * a.kv_d + (w0 - a.kv_d)) * a.vt_ld + grow;
+                __half *vl = a.vt_lo + ((long long)layer * a.kv_d + (w0 - a.kv_d)) * a.vt_ld + grow;
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            const int col = col0 + jj, layer = col / (2 * a.kv_d), w = col - layer * 2 * a.kv_d;
-            if (col < N && w >= a.kv_d && lane < nrows) {
-              const float x = v[jj] * a.alpha * a.kv_scale;
-              range_check(x, a.range_flag);
-              const __half h = __float2half_rn(x);
-              const long long o = ((long long)layer * a.kv_d + (w - a.kv_d)) * a.vt_ld + grow;
-              a.vt_hi[o] = h;
-              a.vt_lo[o] = __float2half_rn(x - __half2float(h));
+                for (int jj = 0; jj < 32; ++jj) {
+                  const float x = v[jj] * a.alpha * a.kv_scale;
+                  range_check(x, a.range_flag);
+                  const __half h = __float2half_rn(x);
+                  vh[(long long)jj * a.vt_ld] = h;
+                  vl[(long long)jj * a.vt_ld] = __float2half_rn(x - __half2float(h));
+                }
+              }
+              continue;  // no K columns in this chunk
+            }
+          } else {
+#pragma unroll 1
+            for (int jj = 0; jj < 32; ++jj) {
+              const int col = col0 + jj, ly = col / (2 * a.kv_d), w = col - ly * 2 * a.kv_d;
+              if (col < N && w >= a.kv_d && lane < nrows) {
+                const float x = v[jj] * a.alpha * a.kv_scale;
+                range_check(x, a.range_flag);
+                const __half h = __float2half_rn(x);
+                const long long o = ((long long)ly * a.kv_d + (w - a.kv_d)) * a.vt_ld + grow;
+                a.vt_hi[o] = h;
+                a.vt_lo[o] = __float2half_rn(x - __half2float(h));
+              }
             }
           }
         }

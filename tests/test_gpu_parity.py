@@ -314,3 +314,48 @@ def test_fp16_split_range_is_reported(path):
         S.beam_search_batch(model, features=feats, schedules=sched, path=path)
     got = S.beam_search_batch(model, features=feats, schedules=sched, path="layered")
     assert len(got[0]) >= 1
+
+
+def test_host_graph_matches_device_path():
+    """BeamDecoder.capture_host (H2D features -> decode -> D2H results in one
+    CUDA graph, the e2e bench path) returns the device path's results."""
+    _need_gpu()
+    from paper_2602_22732_b200.decode import BeamDecoder
+    M, S = _pkg()
+    model = _model(M, C1_MODEL)
+    feats = [c_features(i, 256) for i in range(4)]
+    host = torch.from_numpy(np.concatenate(feats, 0).astype(np.float32)).pin_memory()
+    dec = BeamDecoder(model, [256] * 4, [C2_WIDTHS] * 4)
+    dec.run(features=host.cuda())
+    want = dec.host_results()
+    dec2 = BeamDecoder(model, [256] * 4, [C2_WIDTHS] * 4)
+    dec2.capture_host(host)
+    dec2.replay_host()
+    torch.cuda.synchronize()
+    count, toks, score = (t.numpy() for t in dec2.host_out)
+    toks = toks.reshape(-1, dec2.max_out, dec2.T)
+    score = score.reshape(-1, dec2.max_out)
+    for b in range(4):
+        got = [(tuple(int(v) for v in toks[b, j]), float(score[b, j])) for j in range(int(count[b]))]
+        assert got == want[b]
+
+
+@pytest.mark.parametrize("path", ["fused", "fused_simt", "layered", "tensor"])
+def test_exact_ties_follow_reference_order(path):
+    """Zero codebooks make every candidate of a level tie exactly
+    (logp = -ln V for all tokens): the kept beams must be the reference's
+    (-score, row, token) order bit for bit.  At C2 widths the level-1 window
+    holds every one of the 64 x 256 tied candidates, more than the fused
+    kernel's sort buffer, so this also drives its exact overflow fallback."""
+    M, S = _pkg()
+    model = _model(M, C1_MODEL)
+    for t in range(C1_MODEL.n_levels):
+        model.params[f"head.{t}"].data[:] = 0.0
+    params = {k: v.data for k, v in model.params.items()}
+    feats = [c_features(i, 256) for i in range(2)]
+    got = S.beam_search_batch(model, features=feats,
+                              schedules=S.BeamSchedule(C2_WIDTHS, C2_WIDTHS[-1]), path=path)
+    for i in range(2):
+        want = orc.beam_search(params, C1_MODEL, orc.context_process(feats[i], params), C2_WIDTHS)
+        assert [sid.tokens for sid, _ in got[i]] == [tuple(t) for t, _ in want]
+        np.testing.assert_allclose([s for _, s in got[i]], [s for _, s in want], rtol=1e-6)
