@@ -632,7 +632,28 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   qk.groups = n_groups; qk.mode = GM_QK;
   qk.g_row_off = rs.g_row_off; qk.g_rows = rs.g_rows;
   qk.g_ctx_off = ctx_off; qk.g_ctx_len = ctx_len;
-  if (p.tc && tc_eligible(qk.lda, qk.ldb, d, qk.A, qk.B)) {
+  // few beam rows per request: swap A / B so tiles are not padded to 128 rows
+  const bool swap = p.tc && rs.max_group_rows <= 64 && d % 8 == 0;
+  if (swap) {
+    TcArgs t{};
+    static_cast<GemmArgs &>(t) = qk;
+    t.mode = GM_QK_T;
+    t.M = qk.N;  // tile M = keys (S_max), N = beam rows
+    t.N = qk.M;
+    t.B = qsrc;  // the query rows, split on chip
+    t.ldb = d;
+    if (trunk) {
+      t.A = X;  // keys = the context rows themselves (reassociated trunk)
+      t.lda = d;
+    } else {
+      const __half *k16 = at<__half>(ws, p.o_KVlo);
+      t.a_hi = k16 + (size_t)(i - p.K) * d;
+      t.a_lo = t.a_hi + (size_t)p.S_tot * nh * d;
+      t.lda = (long long)nh * d;
+      t.alpha = qk.alpha / kKvScale;
+    }
+    GR_TRY(gemm_tc_swapped(t, p.S_tot, d, R, d, st));
+  } else if (p.tc && tc_eligible(qk.lda, qk.ldb, d, qk.A, qk.B)) {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = qk;
     if (!trunk) {  // head-layer K arrives split (fp16, scaled) from the encoder epilogue
@@ -652,7 +673,26 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   pv.C = A; pv.ldc = d;
   pv.M = rs.max_group_rows; pv.N = d; pv.K = p.S_max;
   pv.alpha = 1.f; pv.mode = GM_PV;
-  if (p.tc && VT) {
+  if (swap && VT) {
+    TcArgs t{};
+    static_cast<GemmArgs &>(t) = pv;
+    t.mode = GM_PV_T;
+    t.N = pv.M;    // tile N = beam rows
+    t.M = d;       // tile M = output dims
+    t.B = SC;      // P, split on chip (zero past each request's S)
+    t.ldb = p.sc_ld;
+    if (trunk) {
+      t.A = at<float>(ws, p.o_XT);  // (P X): values = the context rows
+      t.lda = p.vt_ld;
+    } else {
+      const __half *v16 = at<__half>(ws, p.o_VTlo);
+      t.a_hi = v16 + (size_t)(i - p.K) * d * p.vt_ld;
+      t.a_lo = t.a_hi + (size_t)nh * d * p.vt_ld;
+      t.lda = p.vt_ld;
+      t.alpha = pv.alpha / kKvScale;
+    }
+    GR_TRY(gemm_tc_swapped(t, d, p.vt_ld, R, p.sc_ld, st));
+  } else if (p.tc && VT) {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = pv;
     t.B = at<float>(ws, p.o_XT);  // trunk: X^T, split on chip

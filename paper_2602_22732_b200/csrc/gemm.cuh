@@ -11,7 +11,11 @@
 
 namespace gr {
 
-enum GemmMode { GM_PLAIN = 0, GM_QK = 1, GM_PV = 2 };
+// GM_QK_T / GM_PV_T (tcgen05 only): the per-request attention products with
+// A and B swapped for small beam counts -- M = keys (QK) or dims (PV) of the
+// request, N = its beam rows -- and the result stored transposed, so tiles
+// are not padded to 128 rows
+enum GemmMode { GM_PLAIN = 0, GM_QK = 1, GM_PV = 2, GM_QK_T = 3, GM_PV_T = 4 };
 enum GemmEpi {
   EPI_STORE = 0,      // C = alpha*acc
   EPI_BIAS = 1,       // C = acc + bias[n]
@@ -20,7 +24,8 @@ enum GemmEpi {
   EPI_BIAS_RESID = 4, // C = R + (acc + bias[n])
   EPI_MULVEC = 5,     // C = vec[req(r)][n] * acc   (fuse gate m * (s W_g))
   EPI_KV_SPLIT = 6,   // C = acc, and the V half of each layer also written transposed
-  EPI_STORE_LSE = 7   // C = alpha*acc, plus per-row (max, sum exp) of every 128 columns
+  EPI_STORE_LSE = 7,  // C = alpha*acc, plus per-row (max, sum exp) of every 128 columns
+  EPI_STORE_T = 8     // C^T = alpha*acc (GM_QK_T / GM_PV_T)
 };
 
 struct GemmArgs {

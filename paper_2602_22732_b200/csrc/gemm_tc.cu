@@ -150,7 +150,9 @@ __device__ __forceinline__ void split_f16x2(float x0, float x1, float s, uint32_
 }
 
 struct TileInfo {
-  int m0, n0, M, N, K, row_base, b_row_base, b_k_base;
+  int m0, n0, M, N, K;
+  int a_row, a_k, b_row, b_k;  // operand bases (rows, k) of the tile's group
+  int c_row;                   // C row of tile row 0 (of tile column 0 when transposed)
   bool valid;
 };
 
@@ -162,16 +164,31 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, int tile, int til
   const int g = tile / per_g, r = tile - g * per_g;
   const int tm = r / tiles_n, tn = r - tm * tiles_n;
   ti.M = a.M; ti.N = a.N; ti.K = a.K;
-  ti.row_base = 0; ti.b_row_base = 0; ti.b_k_base = 0;
+  ti.a_row = 0; ti.a_k = 0; ti.b_row = 0; ti.b_k = 0; ti.c_row = 0;
   if (a.g_rows) {
-    ti.row_base = a.g_row_off[g];
-    ti.M = a.g_rows[g];
-    if (a.mode == GM_QK) {
-      ti.N = a.g_ctx_len[g];
-      ti.b_row_base = a.g_ctx_off[g];
-    } else if (a.mode == GM_PV) {
+    if (a.mode == GM_QK_T) {  // M = the request's keys, N = its rows
+      ti.M = a.g_ctx_len[g];
+      ti.a_row = a.g_ctx_off[g];
+      ti.N = a.g_rows[g];
+      ti.b_row = a.g_row_off[g];
+      ti.c_row = a.g_row_off[g];
+    } else if (a.mode == GM_PV_T) {  // M = dims, N = rows, K = the request's keys
+      ti.a_k = a.g_ctx_off[g];
+      ti.N = a.g_rows[g];
+      ti.b_row = a.g_row_off[g];
       ti.K = a.g_ctx_len[g];
-      ti.b_k_base = a.g_ctx_off[g];
+      ti.c_row = a.g_row_off[g];
+    } else {
+      ti.a_row = a.g_row_off[g];
+      ti.c_row = a.g_row_off[g];
+      ti.M = a.g_rows[g];
+      if (a.mode == GM_QK) {
+        ti.N = a.g_ctx_len[g];
+        ti.b_row = a.g_ctx_off[g];
+      } else if (a.mode == GM_PV) {
+        ti.K = a.g_ctx_len[g];
+        ti.b_k = a.g_ctx_off[g];
+      }
     }
   }
   ti.m0 = tm * BM;
@@ -208,15 +225,17 @@ __device__ __forceinline__ void convert_groups(unsigned char *tile, int rows, in
 // Persistent, warp-specialised: each CTA walks tiles blockIdx.x, +gridDim.x, ...
 // Two TMEM accumulators (2 x BN columns) let the epilogue of tile j overlap
 // the MMAs of tile j+1.  BSPLIT: B arrives as pre-split fp16 hi / lo.
-template <int BN, int STAGES, int EPI, bool BSPLIT>
+template <int BN, int STAGES, int EPI, bool BSPLIT, bool ASPLIT>
 __global__ void __launch_bounds__(kTcThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmBlo, TcArgs a, int tiles_m, int tiles_n,
-               int n_tiles) {
+               const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmAlo,
+               TcArgs a, int tiles_m, int tiles_n, int n_tiles) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  constexpr int A32 = BM * BK * 4;   // fp32 landing tile, split in place (hi / lo atoms)
+  constexpr int A32 = BM * BK * 4;   // fp32 landing tile split in place (hi / lo atoms),
+                                     // or (ASPLIT) the fp16 hi tile then the lo tile
+  constexpr int A16 = BM * BK * 2;
   constexpr int B16 = BN * BK * 2;   // pre-split B: fp16 hi tile, then lo tile
   constexpr int B32 = BN * BK * 4;   // fp32 B landing tile, split in place
   // stage: [A][B]; A (and an fp32 B) hold interleaved 512-B hi / lo atoms
@@ -264,13 +283,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (kg >= STAGES) mbar_wait(&empty[s], ((kg / STAGES) - 1) & 1);
           unsigned char *st = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full[s], A32 + (BSPLIT ? 2 * B16 : B32));
-          tma_load_2d(st, &tmA, &full[s], kt * BK, ti.row_base + ti.m0);
+          tma_load_2d(st, &tmA, &full[s], ti.a_k + kt * BK, ti.a_row + ti.m0);
+          if (ASPLIT) tma_load_2d(st + A16, &tmAlo, &full[s], ti.a_k + kt * BK, ti.a_row + ti.m0);
           if (BSPLIT) {
             unsigned char *bh = st + A32;
-            tma_load_2d(bh, &tmB, &full[s], ti.b_k_base + kt * BK, ti.b_row_base + ti.n0);
-            tma_load_2d(bh + B16, &tmBlo, &full[s], ti.b_k_base + kt * BK, ti.b_row_base + ti.n0);
+            tma_load_2d(bh, &tmB, &full[s], ti.b_k + kt * BK, ti.b_row + ti.n0);
+            tma_load_2d(bh + B16, &tmBlo, &full[s], ti.b_k + kt * BK, ti.b_row + ti.n0);
           } else {
-            tma_load_2d(st + A32, &tmB, &full[s], ti.b_k_base + kt * BK, ti.b_row_base + ti.n0);
+            tma_load_2d(st + A32, &tmB, &full[s], ti.b_k + kt * BK, ti.b_row + ti.n0);
           }
         }
       }
@@ -294,16 +314,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           mbar_wait(&conv[s], (kg / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-          const uint32_t a_hi = st, a_lo = st + 512;  // interleaved atoms, 1024 B apart
+          // in-place split: interleaved hi / lo atoms 1024 B apart; ASPLIT: two tiles
+          const uint32_t a_hi = st, a_lo = ASPLIT ? st + A16 : st + 512;
+          constexpr uint32_t a_sbo = ASPLIT ? 512 : 1024;
           const uint32_t b_hi = st + A32, b_lo = BSPLIT ? b_hi + B16 : b_hi + 512;
           constexpr uint32_t b_sbo = BSPLIT ? 512 : 1024;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint32_t off = k * 32;  // 16 fp16 = 32 B along the swizzled row
             const uint32_t acc0 = (kt > 0 || k > 0) ? 1u : 0u;
-            mma_f16(d_tmem, sw64_desc(a_lo + off, 1024), sw64_desc(b_hi + off, b_sbo), idesc, acc0);
-            mma_f16(d_tmem, sw64_desc(a_hi + off, 1024), sw64_desc(b_lo + off, b_sbo), idesc, 1u);
-            mma_f16(d_tmem, sw64_desc(a_hi + off, 1024), sw64_desc(b_hi + off, b_sbo), idesc, 1u);
+            mma_f16(d_tmem, sw64_desc(a_lo + off, a_sbo), sw64_desc(b_hi + off, b_sbo), idesc, acc0);
+            mma_f16(d_tmem, sw64_desc(a_hi + off, a_sbo), sw64_desc(b_lo + off, b_sbo), idesc, 1u);
+            mma_f16(d_tmem, sw64_desc(a_hi + off, a_sbo), sw64_desc(b_hi + off, b_sbo), idesc, 1u);
           }
           mma_commit(&empty[s]);  // frees the stage when these MMAs complete
         }
@@ -323,7 +345,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int s = kg % STAGES;
         mbar_wait(&full[s], (kg / STAGES) & 1);
         unsigned char *st = smem + s * STAGE_BYTES;
-        convert_groups(st, BM, cw, kConvWarps);
+        if (!ASPLIT) convert_groups(st, BM, cw, kConvWarps);
         if (!BSPLIT) convert_groups(st + A32, BN, cw, kConvWarps);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -345,7 +367,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int acc = j & 1;
       mbar_wait(&accf[acc], (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int rbase = ti.m0 + q * 32;  // this warp's 32 rows
+      const int rbase = ti.m0 + q * 32;  // this warp's 32 rows (tile M side)
       const int nrows = min(32, ti.M - rbase);
       const int N = ti.N;
       float pm = -INFINITY, ps = 0.f;  // EPI_STORE_LSE: this lane's row, current 128 columns
@@ -369,18 +391,29 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           pm = nm;
           if ((c & 3) == 3 || col0 + 32 >= N) {
             if (lane < nrows)
-              a.lse_part[((long long)ti.row_base + rbase + lane) * a.lse_ld + col0 / 128] =
+              a.lse_part[((long long)ti.c_row + rbase + lane) * a.lse_ld + col0 / 128] =
                   make_float2(pm, ps);
             pm = -INFINITY;
             ps = 0.f;
           }
+        }
+        if (EPI == EPI_STORE_T) {
+          // C[c_row + n][m]: lanes (m) are contiguous in every stored row
+          const int m = rbase + lane;
+          if (lane < nrows) {
+            float *dst = a.C + (long long)ti.c_row * a.ldc + m;
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj)
+              if (col0 + jj < N) dst[(long long)(col0 + jj) * a.ldc] = v[jj] * a.alpha;
+          }
+          continue;
         }
         if (EPI == EPI_KV_SPLIT) {
           // [2i d, 2i d + d) -> K_i, [2i d + d, 2(i+1) d) -> V_i^T, both as fp16
           // hi / lo of kv_scale * x for the attention GEMMs; V^T is written
           // straight from the row-per-lane registers (coalesced over rows).
           // With d % 32 == 0 a chunk lies wholly in one K or V block.
-          const long long grow = (long long)ti.row_base + rbase + lane;
+          const long long grow = (long long)ti.c_row + rbase + lane;
           const int layer = col0 / (2 * a.kv_d), w0 = col0 - layer * 2 * a.kv_d;
           if (a.kv_d % 32 == 0) {
             if (w0 >= a.kv_d) {
@@ -436,7 +469,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
           const int rr = it * 4 + lr;
-          const long long grow = (long long)ti.row_base + rbase + rr;
+          const long long grow = (long long)ti.c_row + rbase + rr;
           float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
           if (rr < nrows && col < N) {
             const float *src = nullptr;
@@ -459,7 +492,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int it = 0; it < 8; ++it) {
           const int rr = it * 4 + lr;
           if (rr >= nrows || col >= N) continue;
-          const long long grow = (long long)ti.row_base + rbase + rr;
+          const long long grow = (long long)ti.c_row + rbase + rr;
           float x[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) x[q] = ebuf[rr * 33 + c4 + q] * a.alpha;
@@ -563,9 +596,9 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, bool BSPLIT>
+template <int BN, int STAGES, bool BSPLIT, bool ASPLIT = false>
 static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl,
-                     const TcArgs &a, int epi, cudaStream_t st) {
+                     const CUtensorMap &mal, const TcArgs &a, int epi, cudaStream_t st) {
   constexpr size_t stage = (size_t)BM * BK * 4 + (size_t)BN * BK * 4;  // (in-place splits)
   constexpr size_t smem = 1024 + STAGES * stage + 256 + 4 * 32 * 33 * sizeof(float);
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
@@ -575,11 +608,18 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
   const int cls = (a.mode == GM_PLAIN) ? KC_GEMM : KC_ATTN_GEMM;
 #define GR_TC_EPI(E)                                                                          \
   case E: {                                                                                   \
-    GR_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E, BSPLIT>,                       \
+    GR_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E, BSPLIT, ASPLIT>,               \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
-    GR_LAUNCH(cls, st, gemm_tc_kernel<BN, STAGES, E, BSPLIT><<<grid, kTcThreads, smem, st>>>(   \
-                           ma, mb, mbl, a, tiles_m, tiles_n, n_tiles));                       \
+    GR_LAUNCH(cls, st, gemm_tc_kernel<BN, STAGES, E, BSPLIT, ASPLIT>                           \
+                       <<<grid, kTcThreads, smem, st>>>(ma, mb, mbl, mal, a, tiles_m, tiles_n,  \
+                                                        n_tiles));                            \
     return GR4AD_OK;                                                                          \
+  }
+  if (ASPLIT || epi == EPI_STORE_T) {
+    switch (epi) {
+      GR_TC_EPI(EPI_STORE_T)
+      default: return set_err(GR4AD_ERR_UNSUPPORTED, "swapped tc epilogue %d", epi);
+    }
   }
   switch (epi) {
     GR_TC_EPI(EPI_STORE)
@@ -619,12 +659,35 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
     if (a.ldb % 8 != 0) return set_err(GR4AD_ERR_UNSUPPORTED, "fp16 B rows need ldb %% 8 == 0");
     GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, box_n));
     GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, box_n));
-    return wide ? launch_tc<256, 4, true>(ma, mb, mbl, a, epi, st)
-                : launch_tc<128, 6, true>(ma, mb, mbl, a, epi, st);
+    return wide ? launch_tc<256, 4, true>(ma, mb, mbl, ma, a, epi, st)
+                : launch_tc<128, 6, true>(ma, mb, mbl, ma, a, epi, st);
   }
   GR_TRY(make_map(&mb, a.B, false, b_rows, b_cols, a.ldb, box_n));
-  return wide ? launch_tc<256, 4, false>(ma, mb, mb, a, epi, st)
-              : launch_tc<128, 6, false>(ma, mb, mb, a, epi, st);
+  return wide ? launch_tc<256, 4, false>(ma, mb, mb, ma, a, epi, st)
+              : launch_tc<128, 6, false>(ma, mb, mb, ma, a, epi, st);
+}
+
+int gemm_tc_swapped(const TcArgs &a, long long a_rows, long long a_cols, long long b_rows,
+                    long long b_cols, cudaStream_t st) {
+  if (a.M <= 0 || a.N <= 0 || a.groups <= 0) return GR4AD_OK;
+  if (a.mode != GM_QK_T && a.mode != GM_PV_T)
+    return set_err(GR4AD_ERR_UNSUPPORTED, "swapped tc gemm: mode %d", a.mode);
+  CUtensorMap ma, mal, mb;
+  // N = beam rows per request: the smallest tile that holds them
+  const int bn = a.N <= 32 ? 32 : (a.N <= 64 ? 64 : 128);
+  GR_TRY(make_map(&mb, a.B, false, b_rows, b_cols, a.ldb, bn));
+  if (a.a_hi) {
+    if (a.lda % 8 != 0) return set_err(GR4AD_ERR_UNSUPPORTED, "fp16 A rows need lda %% 8 == 0");
+    GR_TRY(make_map(&ma, a.a_hi, true, a_rows, a_cols, a.lda, BM));
+    GR_TRY(make_map(&mal, a.a_lo, true, a_rows, a_cols, a.lda, BM));
+    if (bn == 32) return launch_tc<32, 8, false, true>(ma, mb, mb, mal, a, EPI_STORE_T, st);
+    if (bn == 64) return launch_tc<64, 8, false, true>(ma, mb, mb, mal, a, EPI_STORE_T, st);
+    return launch_tc<128, 6, false, true>(ma, mb, mb, mal, a, EPI_STORE_T, st);
+  }
+  GR_TRY(make_map(&ma, a.A, false, a_rows, a_cols, a.lda, BM));
+  if (bn == 32) return launch_tc<32, 8, false, false>(ma, mb, mb, ma, a, EPI_STORE_T, st);
+  if (bn == 64) return launch_tc<64, 8, false, false>(ma, mb, mb, ma, a, EPI_STORE_T, st);
+  return launch_tc<128, 6, false, false>(ma, mb, mb, ma, a, EPI_STORE_T, st);
 }
 
 }  // namespace gr

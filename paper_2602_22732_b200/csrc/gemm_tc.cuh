@@ -16,6 +16,8 @@ struct TcArgs : GemmArgs {
   // optional: B pre-split, s.B = b_hi + b_lo (fp16, K-major, ld = ldb);
   // otherwise B (fp32) is split on chip, unscaled
   const __half *b_hi, *b_lo;
+  // optional: A pre-split likewise (a_hi / a_lo, ld = lda), scale folded into alpha
+  const __half *a_hi, *a_lo;
   // EPI_KV_SPLIT: the K part of layer i -> k_hi / k_lo [row][k_ld] at column
   // i d, the V part -> vt_hi / vt_lo [i d + c][vt_ld], all kv_scale * x
   __half *k_hi, *k_lo, *vt_hi, *vt_lo;
@@ -34,6 +36,11 @@ struct TcArgs : GemmArgs {
 int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_rows,
             long long b_cols, int epi, cudaStream_t st);
 bool tc_eligible(long long lda, long long ldb, int K, const void *A, const void *B);
+// GM_QK_T / GM_PV_T attention products (EPI_STORE_T): A (a_hi/a_lo fp16, or
+// A fp32) is (a_rows, a_cols), B fp32 (b_rows, b_cols); tile N sized to the
+// beam rows per request (32 / 64 / 128)
+int gemm_tc_swapped(const TcArgs &a, long long a_rows, long long a_cols, long long b_rows,
+                    long long b_cols, cudaStream_t st);
 
 // dst (cols x rows) = src (rows x cols)^T, both row-major with the given lds
 int transpose(const float *src, long long lds, float *dst, long long ldd, int rows, int cols,
