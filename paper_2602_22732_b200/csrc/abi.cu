@@ -591,6 +591,24 @@ static int dense_nk(const Plan &p, const GemmArgs &g, long long a_rows, long lon
   return gemm(g, true, epi, st);
 }
 
+// C = epi(A . W) with A already split into fp16 hi / lo (written so by the
+// producing LayerNorm / epilogue / self-attention): no on-chip conversion
+static int dense_split(const Plan &p, const GemmArgs &g, const __half *WT, const __half *a_hi,
+                       const __half *a_lo, long long a_rows, int epi, cudaStream_t st,
+                       __half *c_hi = nullptr, __half *c_lo = nullptr) {
+  TcArgs t{};
+  static_cast<GemmArgs &>(t) = g;
+  t.b_hi = WT;
+  t.b_lo = WT + p.wt_floats;
+  t.ldb = g.K;
+  t.a_hi = a_hi;
+  t.a_lo = a_lo;
+  t.alpha = g.alpha / kWeightScale;
+  t.c_hi = c_hi;
+  t.c_lo = c_lo;
+  return gemm_tc(t, a_rows, g.K, g.N, g.K, epi, st);
+}
+
 static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *wt, int i,
                          float *Hs, const RowSet &rs, void *ws, const float *KV,
                          const float *VT, cudaStream_t st) {
@@ -607,10 +625,25 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   const bool trunk = i < p.K;
   const float *X = at<float>(ws, p.o_X);
   const long long ldw = 2LL * p.L * d;
+  // head layers on the tensor-core path: every dense product's activation
+  // operand is produced already split into fp16 hi / lo (LayerNorm, P.V and
+  // GELU epilogues, self-attention), so the GEMMs only move and multiply
+  const bool spl = p.tc && LT && !trunk && d % 128 == 0 && d <= 1024 && p.dff % 8 == 0;
+  __half *Nh = reinterpret_cast<__half *>(N), *Nl = Nh + (size_t)p.Rw * d;
+  __half *Ah = reinterpret_cast<__half *>(A), *Al = Ah + (size_t)p.Rw * d;
+  __half *Fh = reinterpret_cast<__half *>(Fb), *Fl = Fh + (size_t)p.Rw * p.dff;
+  auto layer_norm = [&](const float *g_, const float *b_) -> int {
+    return spl ? ln_rows_split(Hs, d, Nh, Nl, d, g_, b_, R, d, st)
+               : ln_rows(Hs, d, N, d, g_, b_, R, d, st);
+  };
   // cross-attention into the beam-shared context KV (layers.py:82-90)
-  GR_TRY(ln_rows(Hs, d, N, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
-  GR_TRY(dense(p, plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), LT ? LT->cq : nullptr, R,
-               EPI_STORE, st));
+  GR_TRY(layer_norm(Lw.ln1_g, Lw.ln1_b));
+  if (spl)
+    GR_TRY(dense_split(p, plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), LT->cq, Nh, Nl, R,
+                       EPI_STORE, st));
+  else
+    GR_TRY(dense(p, plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), LT ? LT->cq : nullptr, R,
+                 EPI_STORE, st));
   const float *qsrc = Q;
   if (trunk) {
     // trunk rows: q (X Wk)^T = (q Wk^T) X^T -- the trunk layers' K is never built
@@ -691,7 +724,11 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
       t.lda = p.vt_ld;
       t.alpha = pv.alpha / kKvScale;
     }
-    GR_TRY(gemm_tc_swapped(t, d, p.vt_ld, R, p.sc_ld, st));
+    if (spl) {
+      t.c_hi = Ah;
+      t.c_lo = Al;
+    }
+    GR_TRY(gemm_tc_swapped(t, d, p.vt_ld, R, p.sc_ld, st, spl ? EPI_STORE_T_SPLIT : EPI_STORE_T));
   } else if (p.tc && VT) {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = pv;
@@ -703,7 +740,11 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
       t.alpha = pv.alpha / kKvScale;
     }
     t.ldb = p.vt_ld;
-    GR_TRY(gemm_tc(t, R, p.sc_ld, d, p.vt_ld, EPI_STORE, st));
+    if (spl) {
+      t.c_hi = Ah;
+      t.c_lo = Al;
+    }
+    GR_TRY(gemm_tc(t, R, p.sc_ld, d, p.vt_ld, spl ? EPI_STORE_SPLIT : EPI_STORE, st));
   } else {
     if (trunk) {
       pv.B = X; pv.ldb = d;
@@ -720,25 +761,40 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   }
   GemmArgs o = plain_gemm(attn, d, Lw.cross_Wo, d, Hs, d, R, d, d);
   o.R = Hs; o.ldr = d;
-  GR_TRY(dense(p, o, LT ? LT->co : nullptr, R, EPI_RESID, st));
+  if (spl)
+    GR_TRY(dense_split(p, o, LT->co, Ah, Al, R, EPI_RESID, st));
+  else
+    GR_TRY(dense(p, o, LT ? LT->co : nullptr, R, EPI_RESID, st));
   // self-attention over decoded positions (layers.py:92-113)
-  GR_TRY(ln_rows(Hs, d, N, d, Lw.ln2_g, Lw.ln2_b, R, d, st));
+  GR_TRY(layer_norm(Lw.ln2_g, Lw.ln2_b));
   float *qkv_rows = rs.qkv + rs.hist_row0 * 3 * d;
-  GR_TRY(dense(p, plain_gemm(N, d, Lw.self_Wqkv, 3 * d, qkv_rows, 3 * d, R, 3 * d, d),
-               LT ? LT->sqkv : nullptr, R, EPI_STORE, st));
+  const GemmArgs qkv = plain_gemm(N, d, Lw.self_Wqkv, 3 * d, qkv_rows, 3 * d, R, 3 * d, d);
+  if (spl)
+    GR_TRY(dense_split(p, qkv, LT->sqkv, Nh, Nl, R, EPI_STORE, st));
+  else
+    GR_TRY(dense(p, qkv, LT ? LT->sqkv : nullptr, R, EPI_STORE, st));
   GR_TRY(self_attn(rs.qkv, 3LL * d, d, rs.anc, rs.anc_stride, (int)rs.hist_row0, R,
-                   rs.npos_u, rs.npos_row, A, d, st));
+                   rs.npos_u, rs.npos_row, A, d, st, spl ? Ah : nullptr, spl ? Al : nullptr));
   GemmArgs so = plain_gemm(A, d, Lw.self_Wo, d, Hs, d, R, d, d);
   so.R = Hs; so.ldr = d;
-  GR_TRY(dense(p, so, LT ? LT->so : nullptr, R, EPI_RESID, st));
+  if (spl)
+    GR_TRY(dense_split(p, so, LT->so, Ah, Al, R, EPI_RESID, st));
+  else
+    GR_TRY(dense(p, so, LT ? LT->so : nullptr, R, EPI_RESID, st));
   // position-wise FFN (layers.py:115-118)
-  GR_TRY(ln_rows(Hs, d, N, d, Lw.ln3_g, Lw.ln3_b, R, d, st));
+  GR_TRY(layer_norm(Lw.ln3_g, Lw.ln3_b));
   GemmArgs f1 = plain_gemm(N, d, Lw.ffn_W1, p.dff, Fb, p.dff, R, p.dff, d);
   f1.bias = Lw.ffn_b1;
-  GR_TRY(dense(p, f1, LT ? LT->w1 : nullptr, R, EPI_BIAS_GELU, st));
+  if (spl)
+    GR_TRY(dense_split(p, f1, LT->w1, Nh, Nl, R, EPI_BIAS_GELU_SPLIT, st, Fh, Fl));
+  else
+    GR_TRY(dense(p, f1, LT ? LT->w1 : nullptr, R, EPI_BIAS_GELU, st));
   GemmArgs f2 = plain_gemm(Fb, p.dff, Lw.ffn_W2, d, Hs, d, R, d, p.dff);
   f2.bias = Lw.ffn_b2; f2.R = Hs; f2.ldr = d;
-  GR_TRY(dense(p, f2, LT ? LT->w2 : nullptr, R, EPI_BIAS_RESID, st));
+  if (spl)
+    GR_TRY(dense_split(p, f2, LT->w2, Fh, Fl, R, EPI_BIAS_RESID, st));
+  else
+    GR_TRY(dense(p, f2, LT ? LT->w2 : nullptr, R, EPI_BIAS_RESID, st));
   return GR4AD_OK;
 }
 

@@ -25,7 +25,12 @@ enum GemmEpi {
   EPI_MULVEC = 5,     // C = vec[req(r)][n] * acc   (fuse gate m * (s W_g))
   EPI_KV_SPLIT = 6,   // C = acc, and the V half of each layer also written transposed
   EPI_STORE_LSE = 7,  // C = alpha*acc, plus per-row (max, sum exp) of every 128 columns
-  EPI_STORE_T = 8     // C^T = alpha*acc (GM_QK_T / GM_PV_T)
+  EPI_STORE_T = 8,    // C^T = alpha*acc (GM_QK_T / GM_PV_T)
+  // tcgen05 only: the result as fp16 hi / lo (c_hi / c_lo, ld = ldc), the
+  // next GEMM's pre-split A operand
+  EPI_STORE_SPLIT = 9,
+  EPI_BIAS_GELU_SPLIT = 10,
+  EPI_STORE_T_SPLIT = 11
 };
 
 struct GemmArgs {

@@ -397,14 +397,24 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             ps = 0.f;
           }
         }
-        if (EPI == EPI_STORE_T) {
+        if (EPI == EPI_STORE_T || EPI == EPI_STORE_T_SPLIT) {
           // C[c_row + n][m]: lanes (m) are contiguous in every stored row
           const int m = rbase + lane;
           if (lane < nrows) {
-            float *dst = a.C + (long long)ti.c_row * a.ldc + m;
+            const long long o0 = (long long)ti.c_row * a.ldc + m;
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj)
-              if (col0 + jj < N) dst[(long long)(col0 + jj) * a.ldc] = v[jj] * a.alpha;
+              if (col0 + jj < N) {
+                const float x = v[jj] * a.alpha;
+                const long long o = o0 + (long long)(col0 + jj) * a.ldc;
+                if (EPI == EPI_STORE_T) {
+                  a.C[o] = x;
+                } else {
+                  const __half h = __float2half_rn(x);
+                  a.c_hi[o] = h;
+                  a.c_lo[o] = __float2half_rn(x - __half2float(h));
+                }
+              }
           }
           continue;
         }
@@ -458,7 +468,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                          (EPI != EPI_MULVEC || (a.vec_ld % 4) == 0) &&
                          (EPI != EPI_KV_SPLIT || (a.k_ld % 4) == 0);
         float4 bcol = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID) {
+        if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID ||
+            EPI == EPI_BIAS_GELU_SPLIT) {
           bcol.x = col < N ? a.bias[col] : 0.f;
           bcol.y = col + 1 < N ? a.bias[col + 1] : 0.f;
           bcol.z = col + 2 < N ? a.bias[col + 2] : 0.f;
@@ -501,7 +512,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             if (EPI == EPI_BIAS) x[q] = x[q] + ob[q];
-            else if (EPI == EPI_BIAS_GELU) x[q] = gelu_tanh_fast(x[q] + ob[q]);
+            else if (EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_GELU_SPLIT)
+              x[q] = gelu_tanh_fast(x[q] + ob[q]);
             else if (EPI == EPI_RESID) x[q] = oo[q] + x[q];
             else if (EPI == EPI_BIAS_RESID) x[q] = oo[q] + (x[q] + ob[q]);
             else if (EPI == EPI_MULVEC) x[q] = oo[q] * x[q];
@@ -527,6 +539,25 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                   a.k_hi[o + q] = hq[q];
                   a.k_lo[o + q] = lq[q];
                 }
+              }
+            }
+            continue;
+          }
+          if (EPI == EPI_STORE_SPLIT || EPI == EPI_BIAS_GELU_SPLIT) {
+            __half hq[4], lq[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              hq[q] = __float2half_rn(x[q]);
+              lq[q] = __float2half_rn(x[q] - __half2float(hq[q]));
+            }
+            const long long o = grow * a.ldc + col;
+            if (vec) {
+              *reinterpret_cast<uint2 *>(a.c_hi + o) = *reinterpret_cast<const uint2 *>(hq);
+              *reinterpret_cast<uint2 *>(a.c_lo + o) = *reinterpret_cast<const uint2 *>(lq);
+            } else {
+              for (int q = 0; q < 4 && col + q < N; ++q) {
+                a.c_hi[o + q] = hq[q];
+                a.c_lo[o + q] = lq[q];
               }
             }
             continue;
@@ -615,12 +646,24 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
                                                         n_tiles));                            \
     return GR4AD_OK;                                                                          \
   }
-  if (ASPLIT || epi == EPI_STORE_T) {
+  if (epi == EPI_STORE_T || epi == EPI_STORE_T_SPLIT) {
     switch (epi) {
       GR_TC_EPI(EPI_STORE_T)
-      default: return set_err(GR4AD_ERR_UNSUPPORTED, "swapped tc epilogue %d", epi);
+      GR_TC_EPI(EPI_STORE_T_SPLIT)
+      default: break;
     }
   }
+  if constexpr (BN < 128) {
+    return set_err(GR4AD_ERR_UNSUPPORTED, "tc epilogue %d at BN=%d", epi, BN);
+  } else if constexpr (ASPLIT) {  // the head layers' dense products on pre-split activations
+    switch (epi) {
+      GR_TC_EPI(EPI_STORE)
+      GR_TC_EPI(EPI_RESID)
+      GR_TC_EPI(EPI_BIAS_RESID)
+      GR_TC_EPI(EPI_BIAS_GELU_SPLIT)
+      default: return set_err(GR4AD_ERR_UNSUPPORTED, "pre-split-A tc epilogue %d", epi);
+    }
+  } else {
   switch (epi) {
     GR_TC_EPI(EPI_STORE)
     GR_TC_EPI(EPI_BIAS)
@@ -630,7 +673,9 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
     GR_TC_EPI(EPI_MULVEC)
     GR_TC_EPI(EPI_KV_SPLIT)
     GR_TC_EPI(EPI_STORE_LSE)
+    GR_TC_EPI(EPI_STORE_SPLIT)
     default: return set_err(GR4AD_ERR_UNSUPPORTED, "tc epilogue %d", epi);
+  }
   }
 #undef GR_TC_EPI
 }
@@ -654,6 +699,17 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
   const bool wide = a.N >= 256;
   const int box_n = wide ? 256 : 128;
   CUtensorMap ma, mb, mbl;
+  if (a.a_hi) {  // both operands pre-split: TMA only, no on-chip conversion
+    if (!a.b_hi || a.lda % 8 != 0 || a.ldb % 8 != 0)
+      return set_err(GR4AD_ERR_UNSUPPORTED, "pre-split A needs pre-split B and 16-B fp16 rows");
+    CUtensorMap mal;
+    GR_TRY(make_map(&ma, a.a_hi, true, a_rows, a_cols, a.lda, BM));
+    GR_TRY(make_map(&mal, a.a_lo, true, a_rows, a_cols, a.lda, BM));
+    GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, box_n));
+    GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, box_n));
+    return wide ? launch_tc<256, 4, true, true>(ma, mb, mbl, mal, a, epi, st)
+                : launch_tc<128, 6, true, true>(ma, mb, mbl, mal, a, epi, st);
+  }
   GR_TRY(make_map(&ma, a.A, false, a_rows, a_cols, a.lda, BM));
   if (a.b_hi) {
     if (a.ldb % 8 != 0) return set_err(GR4AD_ERR_UNSUPPORTED, "fp16 B rows need ldb %% 8 == 0");
@@ -668,7 +724,9 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
 }
 
 int gemm_tc_swapped(const TcArgs &a, long long a_rows, long long a_cols, long long b_rows,
-                    long long b_cols, cudaStream_t st) {
+                    long long b_cols, cudaStream_t st, int epi) {
+  if (epi != EPI_STORE_T && epi != EPI_STORE_T_SPLIT)
+    return set_err(GR4AD_ERR_UNSUPPORTED, "swapped tc gemm: epilogue %d", epi);
   if (a.M <= 0 || a.N <= 0 || a.groups <= 0) return GR4AD_OK;
   if (a.mode != GM_QK_T && a.mode != GM_PV_T)
     return set_err(GR4AD_ERR_UNSUPPORTED, "swapped tc gemm: mode %d", a.mode);
@@ -680,14 +738,14 @@ int gemm_tc_swapped(const TcArgs &a, long long a_rows, long long a_cols, long lo
     if (a.lda % 8 != 0) return set_err(GR4AD_ERR_UNSUPPORTED, "fp16 A rows need lda %% 8 == 0");
     GR_TRY(make_map(&ma, a.a_hi, true, a_rows, a_cols, a.lda, BM));
     GR_TRY(make_map(&mal, a.a_lo, true, a_rows, a_cols, a.lda, BM));
-    if (bn == 32) return launch_tc<32, 8, false, true>(ma, mb, mb, mal, a, EPI_STORE_T, st);
-    if (bn == 64) return launch_tc<64, 8, false, true>(ma, mb, mb, mal, a, EPI_STORE_T, st);
-    return launch_tc<128, 6, false, true>(ma, mb, mb, mal, a, EPI_STORE_T, st);
+    if (bn == 32) return launch_tc<32, 8, false, true>(ma, mb, mb, mal, a, epi, st);
+    if (bn == 64) return launch_tc<64, 8, false, true>(ma, mb, mb, mal, a, epi, st);
+    return launch_tc<128, 6, false, true>(ma, mb, mb, mal, a, epi, st);
   }
   GR_TRY(make_map(&ma, a.A, false, a_rows, a_cols, a.lda, BM));
-  if (bn == 32) return launch_tc<32, 8, false, false>(ma, mb, mb, ma, a, EPI_STORE_T, st);
-  if (bn == 64) return launch_tc<64, 8, false, false>(ma, mb, mb, ma, a, EPI_STORE_T, st);
-  return launch_tc<128, 6, false, false>(ma, mb, mb, ma, a, EPI_STORE_T, st);
+  if (bn == 32) return launch_tc<32, 8, false, false>(ma, mb, mb, ma, a, epi, st);
+  if (bn == 64) return launch_tc<64, 8, false, false>(ma, mb, mb, ma, a, epi, st);
+  return launch_tc<128, 6, false, false>(ma, mb, mb, ma, a, epi, st);
 }
 
 }  // namespace gr

@@ -18,6 +18,8 @@ struct TcArgs : GemmArgs {
   const __half *b_hi, *b_lo;
   // optional: A pre-split likewise (a_hi / a_lo, ld = lda), scale folded into alpha
   const __half *a_hi, *a_lo;
+  // EPI_*_SPLIT: fp16 hi / lo destinations (ld = ldc)
+  __half *c_hi, *c_lo;
   // EPI_KV_SPLIT: the K part of layer i -> k_hi / k_lo [row][k_ld] at column
   // i d, the V part -> vt_hi / vt_lo [i d + c][vt_ld], all kv_scale * x
   __half *k_hi, *k_lo, *vt_hi, *vt_lo;
@@ -40,7 +42,7 @@ bool tc_eligible(long long lda, long long ldb, int K, const void *A, const void 
 // A fp32) is (a_rows, a_cols), B fp32 (b_rows, b_cols); tile N sized to the
 // beam rows per request (32 / 64 / 128)
 int gemm_tc_swapped(const TcArgs &a, long long a_rows, long long a_cols, long long b_rows,
-                    long long b_cols, cudaStream_t st);
+                    long long b_cols, cudaStream_t st, int epi = EPI_STORE_T);
 
 // dst (cols x rows) = src (rows x cols)^T, both row-major with the given lds
 int transpose(const float *src, long long lds, float *dst, long long ldd, int rows, int cols,

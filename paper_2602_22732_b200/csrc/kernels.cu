@@ -27,6 +27,67 @@ __global__ void ln_rows_kernel(const float *__restrict__ x, long long ldx, float
   for (int j = lane; j < d; j += 32) yr[j] = (xr[j] - mean) * inv * g[j] + b[j];
 }
 
+// LayerNorm writing the fp16 hi / lo split of its output (the next GEMM's A
+// operand, loaded by TMA with no on-chip conversion): warp per row, the row
+// in registers (d % 128 == 0, d <= 1024), float4 loads
+template <int NV>
+__global__ void ln_rows_split_kernel(const float *__restrict__ x, long long ldx, __half *y_hi,
+                                     __half *y_lo, long long ldy, const float *__restrict__ g,
+                                     const float *__restrict__ b, int rows, int d) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const float4 *xr = reinterpret_cast<const float4 *>(x + (long long)w * ldx);
+  float4 v[NV];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    v[i] = xr[lane + 32 * i];
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+  const float mean = warp_sum(s) / (float)d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float a0 = v[i].x - mean, a1 = v[i].y - mean, a2 = v[i].z - mean, a3 = v[i].w - mean;
+    q += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+  }
+  const float inv = 1.0f / sqrtf(warp_sum(q) / (float)d + 1e-5f);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int j = 4 * (lane + 32 * i);
+    const float4 gg = *reinterpret_cast<const float4 *>(g + j);
+    const float4 bb = *reinterpret_cast<const float4 *>(b + j);
+    const float o[4] = {(v[i].x - mean) * inv * gg.x + bb.x, (v[i].y - mean) * inv * gg.y + bb.y,
+                        (v[i].z - mean) * inv * gg.z + bb.z, (v[i].w - mean) * inv * gg.w + bb.w};
+    __half h[4], l[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      h[c] = __float2half_rn(o[c]);
+      l[c] = __float2half_rn(o[c] - __half2float(h[c]));
+    }
+    *reinterpret_cast<uint2 *>(y_hi + (long long)w * ldy + j) = *reinterpret_cast<const uint2 *>(h);
+    *reinterpret_cast<uint2 *>(y_lo + (long long)w * ldy + j) = *reinterpret_cast<const uint2 *>(l);
+  }
+}
+
+int ln_rows_split(const float *x, long long ldx, __half *y_hi, __half *y_lo, long long ldy,
+                  const float *g, const float *b, int rows, int d, cudaStream_t st) {
+  if (rows <= 0) return GR4AD_OK;
+  if (d % 128 != 0 || d > 1024 || ldx % 4 != 0 || ldy % 4 != 0)
+    return set_err(GR4AD_ERR_UNSUPPORTED, "split LayerNorm: d %d", d);
+  const int nv = d / 128;
+#define GR_LNS(NV)                                                                           \
+  case NV:                                                                                   \
+    GR_LAUNCH(KC_LAYERNORM, st, ln_rows_split_kernel<NV><<<ceil_div(rows, 8), 256, 0, st>>>(  \
+                                    x, ldx, y_hi, y_lo, ldy, g, b, rows, d));                \
+    return GR4AD_OK;
+  switch (nv) {
+    GR_LNS(1) GR_LNS(2) GR_LNS(3) GR_LNS(4) GR_LNS(5) GR_LNS(6) GR_LNS(7) GR_LNS(8)
+  }
+#undef GR_LNS
+  return set_err(GR4AD_ERR_UNSUPPORTED, "split LayerNorm: d %d", d);
+}
+
 int ln_rows(const float *x, long long ldx, float *y, long long ldy, const float *g,
             const float *b, int rows, int d, cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;
@@ -70,7 +131,7 @@ __global__ void __launch_bounds__(128)
 self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
                  const int *__restrict__ anc, int stride, int hist_row0, int rows,
                  int npos_u, const int *__restrict__ npos_row, float *out,
-                 long long ldo, float scale) {
+                 long long ldo, float scale, __half *out_hi, __half *out_lo) {
   int r = blockIdx.x;
   if (r >= rows) return;
   int g = hist_row0 + r;
@@ -136,7 +197,19 @@ self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
           o.z = fmaf(p[t], v4.z, o.z);
           o.w = fmaf(p[t], v4.w, o.w);
         }
-      *reinterpret_cast<float4 *>(out + (long long)r * ldo + j) = o;
+      if (out_hi) {  // fp16 hi / lo split for the next GEMM's A operand
+        const float oo[4] = {o.x, o.y, o.z, o.w};
+        __half h[4], l[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          h[c] = __float2half_rn(oo[c]);
+          l[c] = __float2half_rn(oo[c] - __half2float(h[c]));
+        }
+        *reinterpret_cast<uint2 *>(out_hi + (long long)r * ldo + j) = *reinterpret_cast<const uint2 *>(h);
+        *reinterpret_cast<uint2 *>(out_lo + (long long)r * ldo + j) = *reinterpret_cast<const uint2 *>(l);
+      } else {
+        *reinterpret_cast<float4 *>(out + (long long)r * ldo + j) = o;
+      }
     }
     return;
   }
@@ -149,11 +222,13 @@ self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
 
 int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_stride,
               int hist_row0, int rows, int npos_uniform, const int *npos_row,
-              float *out, long long ldo, cudaStream_t st) {
+              float *out, long long ldo, cudaStream_t st, __half *out_hi, __half *out_lo) {
   if (rows <= 0) return GR4AD_OK;
+  if (out_hi && (d % 4 != 0 || ld3 % 4 != 0 || ldo % 4 != 0))
+    return set_err(GR4AD_ERR_UNSUPPORTED, "split self-attention output: d %d", d);
   GR_LAUNCH(KC_SELF_ATTN, st, self_attn_kernel<<<rows, 128, 0, st>>>(qkv, ld3, d, anc, anc_stride, hist_row0, rows,
                                          npos_uniform, npos_row, out, ldo,
-                                         1.0f / sqrtf((float)d)));
+                                         1.0f / sqrtf((float)d), out_hi, out_lo));
   return GR4AD_OK;
 }
 

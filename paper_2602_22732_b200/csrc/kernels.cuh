@@ -1,10 +1,15 @@
 // Row-wise and selection kernels of the beam step (declarations).
 #pragma once
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace gr {
 
 // LN over rows (layers.py:38-43): y = (x - mean) * (var + 1e-5)^-1/2 * g + b
+// LayerNorm with the output as fp16 hi / lo (d % 128 == 0, d <= 1024)
+int ln_rows_split(const float *x, long long ldx, __half *y_hi, __half *y_lo, long long ldy,
+                  const float *g, const float *b, int rows, int d, cudaStream_t st);
 int ln_rows(const float *x, long long ldx, float *y, long long ldy, const float *g,
             const float *b, int rows, int d, cudaStream_t st);
 
@@ -18,7 +23,8 @@ int softmax_rows(float *s, long long ld, int rows, const int *row_req,
 // tau < npos (npos_row[r] or npos_uniform); q/k/v in a (*, 3d) buffer.
 int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_stride,
               int hist_row0, int rows, int npos_uniform, const int *npos_row,
-              float *out, long long ldo, cudaStream_t st);
+              float *out, long long ldo, cudaStream_t st, __half *out_hi = nullptr,
+              __half *out_lo = nullptr);
 
 // level input (beam.py:180-191): s = bos (t==0) or emb_{t-1}[tok]; K>0 writes
 // s into U[:, d:2d]; K==0 writes H = s + pos[t].
