@@ -77,7 +77,7 @@ struct Plan {
   size_t o_trow_off, o_trows, o_trow_req, o_tanc, o_tnpos;
   size_t o_tok, o_anc, o_cum, o_prefix;
   size_t o_X, o_KV, o_Ht, o_QKVt, o_Fin = 0;
-  size_t o_Hs, o_N, o_Q, o_A, o_U, o_Fb, o_SC, o_LG, o_rinfo, o_lsep, o_vlog;
+  size_t o_Hs, o_N, o_Q, o_A, o_U, o_Fb, o_SC, o_SCs, o_LG, o_rinfo, o_lsep, o_vlog;
   size_t o_hist;  // (L-K) consecutive (H, 3d) buffers
   size_t table_bytes, total;
   // tensor-core layered path
@@ -366,7 +366,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     if (bt->decode_path == 3 && !ok)
       return set_err(GR4AD_ERR_UNSUPPORTED, "tensor-core path needs d, d_ff, F, V multiples of 4");
   }
-  p.sc_ld = (p.S_max + 3) / 4 * 4;
+  p.sc_ld = (p.S_max + 7) / 8 * 8;  // (fp16 P rows: 16-B aligned)
   p.vt_ld = (p.S_tot + 7) / 8 * 8;  // fp16 rows: 16-B aligned
   if (p.tc) {
     const long long D = p.d;
@@ -436,6 +436,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.o_U = take(Fl * p.Rw * 2 * d);
   p.o_Fb = take(Fl * p.Rw * p.dff);
   p.o_SC = take(Fl * p.Rw * p.sc_ld);
+  p.o_SCs = take(p.tc ? sizeof(__half) * 2 * p.Rw * p.sc_ld : 16);  // P as fp16 hi, lo
   p.o_LG = take(Fl * p.Rw * std::max(p.Vmax, p.nb));
   p.o_rinfo = take(sizeof(float2) * p.Rw);
   p.o_lsep = take(p.tc ? sizeof(float2) * p.Rw * ((p.Vmax + 127) / 128) : 16);
@@ -638,9 +639,14 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   };
   // cross-attention into the beam-shared context KV (layers.py:82-90)
   GR_TRY(layer_norm(Lw.ln1_g, Lw.ln1_b));
+  // attention on many rows per request (no A/B swap): q and P split too
+  const bool swap = p.tc && rs.max_group_rows <= 64 && d % 8 == 0;
+  const bool spl_att = spl && !swap;
+  __half *Qh = reinterpret_cast<__half *>(Q), *Ql = Qh + (size_t)p.Rw * d;
+  __half *Ph = at<__half>(ws, p.o_SCs), *Pl = Ph + (size_t)p.Rw * p.sc_ld;
   if (spl)
     GR_TRY(dense_split(p, plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), LT->cq, Nh, Nl, R,
-                       EPI_STORE, st));
+                       spl_att ? EPI_STORE_SPLIT : EPI_STORE, st, Qh, Ql));
   else
     GR_TRY(dense(p, plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), LT ? LT->cq : nullptr, R,
                  EPI_STORE, st));
@@ -666,7 +672,6 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
   qk.g_row_off = rs.g_row_off; qk.g_rows = rs.g_rows;
   qk.g_ctx_off = ctx_off; qk.g_ctx_len = ctx_len;
   // few beam rows per request: swap A / B so tiles are not padded to 128 rows
-  const bool swap = p.tc && rs.max_group_rows <= 64 && d % 8 == 0;
   if (swap) {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = qk;
@@ -696,11 +701,18 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
       t.ldb = (long long)nh * d;
       t.alpha = qk.alpha / kKvScale;
     }
+    if (spl_att) {  // q arrives split from the Wq epilogue
+      t.a_hi = Qh;
+      t.a_lo = Ql;
+    }
     GR_TRY(gemm_tc(t, R, d, p.S_tot, d, EPI_STORE, st));
   } else {
     GR_TRY(gemm(qk, true, EPI_STORE, st));
   }
-  GR_TRY(softmax_rows(SC, p.sc_ld, R, rs.row_req, ctx_len, st));
+  if (spl_att)
+    GR_TRY(softmax_rows_split(SC, p.sc_ld, Ph, Pl, R, rs.row_req, ctx_len, st));
+  else
+    GR_TRY(softmax_rows(SC, p.sc_ld, R, rs.row_req, ctx_len, st));
   GemmArgs pv = qk;
   pv.A = SC; pv.lda = p.sc_ld;
   pv.C = A; pv.ldc = d;
@@ -743,6 +755,10 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
     if (spl) {
       t.c_hi = Ah;
       t.c_lo = Al;
+    }
+    if (spl_att) {  // P arrives split from the softmax
+      t.a_hi = Ph;
+      t.a_lo = Pl;
     }
     GR_TRY(gemm_tc(t, R, p.sc_ld, d, p.vt_ld, spl ? EPI_STORE_SPLIT : EPI_STORE, st));
   } else {

@@ -661,6 +661,7 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
       GR_TC_EPI(EPI_RESID)
       GR_TC_EPI(EPI_BIAS_RESID)
       GR_TC_EPI(EPI_BIAS_GELU_SPLIT)
+      GR_TC_EPI(EPI_STORE_SPLIT)
       default: return set_err(GR4AD_ERR_UNSUPPORTED, "pre-split-A tc epilogue %d", epi);
     }
   } else {

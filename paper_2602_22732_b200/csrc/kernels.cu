@@ -115,6 +115,43 @@ __global__ void softmax_rows_kernel(float *s, long long ld, int rows,
   for (int j = n + lane; j < ld; j += 32) r[j] = 0.f;  // keeps P.V exact past S_b
 }
 
+// the same, writing P as fp16 hi / lo (the P.V GEMM's pre-split A operand)
+__global__ void softmax_rows_split_kernel(const float *__restrict__ s, long long ld, __half *p_hi,
+                                          __half *p_lo, int rows,
+                                          const int *__restrict__ row_req,
+                                          const int *__restrict__ len) {
+  int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  int n = len[row_req[w]];
+  const float *r = s + (long long)w * ld;
+  float mx = -INFINITY;
+  for (int j = lane; j < n; j += 32) mx = fmaxf(mx, r[j]);
+  mx = warp_max(mx);
+  float sum = 0.f;
+  for (int j = lane; j < n; j += 32) sum += expf(r[j] - mx);
+  float lse = logf(warp_sum(sum)) + mx;
+  __half *ph = p_hi + (long long)w * ld, *pl = p_lo + (long long)w * ld;
+  for (int j = lane; j < n; j += 32) {
+    const float x = expf(r[j] - lse);
+    const __half h = __float2half_rn(x);
+    ph[j] = h;
+    pl[j] = __float2half_rn(x - __half2float(h));
+  }
+  const __half z = __float2half_rn(0.f);
+  for (int j = n + lane; j < ld; j += 32) {  // keeps P.V exact past S_b
+    ph[j] = z;
+    pl[j] = z;
+  }
+}
+
+int softmax_rows_split(const float *s, long long ld, __half *p_hi, __half *p_lo, int rows,
+                       const int *row_req, const int *len, cudaStream_t st) {
+  if (rows <= 0) return GR4AD_OK;
+  GR_LAUNCH(KC_SOFTMAX, st, softmax_rows_split_kernel<<<ceil_div(rows, 8), 256, 0, st>>>(
+                                s, ld, p_hi, p_lo, rows, row_req, len));
+  return GR4AD_OK;
+}
+
 int softmax_rows(float *s, long long ld, int rows, const int *row_req, const int *len,
                  cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;

@@ -15,6 +15,9 @@ int ln_rows(const float *x, long long ldx, float *y, long long ldy, const float 
 
 // in-place softmax (autodiff.py:362-368) of row r over its first len[req(r)]
 // columns; row_req maps rows to groups.
+// softmax writing P as fp16 hi / lo (ld halves per row, zero past each S)
+int softmax_rows_split(const float *s, long long ld, __half *p_hi, __half *p_lo, int rows,
+                       const int *row_req, const int *len, cudaStream_t st);
 int softmax_rows(float *s, long long ld, int rows, const int *row_req,
                  const int *len, cudaStream_t st);
 
