@@ -610,9 +610,11 @@ static int dense_split(const Plan &p, const GemmArgs &g, const __half *WT, const
   return gemm_tc(t, a_rows, g.K, g.N, g.K, epi, st);
 }
 
+// split_out: also leave the layer's output rows as fp16 hi / lo in the N
+// buffer (the codebook GEMM's pre-split A); returns whether it did
 static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *wt, int i,
                          float *Hs, const RowSet &rs, void *ws, const float *KV,
-                         const float *VT, cudaStream_t st) {
+                         const float *VT, cudaStream_t st, bool *split_out = nullptr) {
   const int d = p.d, R = rs.rows;
   const gr4ad_layer &Lw = w->layer[i];
   const LayerT *LT = wt ? &wt->layer[i] : nullptr;
@@ -807,10 +809,13 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
     GR_TRY(dense(p, f1, LT ? LT->w1 : nullptr, R, EPI_BIAS_GELU, st));
   GemmArgs f2 = plain_gemm(Fb, p.dff, Lw.ffn_W2, d, Hs, d, R, d, p.dff);
   f2.bias = Lw.ffn_b2; f2.R = Hs; f2.ldr = d;
+  const bool dual = spl && split_out;
   if (spl)
-    GR_TRY(dense_split(p, f2, LT->w2, Fh, Fl, R, EPI_BIAS_RESID, st));
+    GR_TRY(dense_split(p, f2, LT->w2, Fh, Fl, R, dual ? EPI_BIAS_RESID_DUAL : EPI_BIAS_RESID, st,
+                       dual ? Nh : nullptr, dual ? Nl : nullptr));
   else
     GR_TRY(dense(p, f2, LT ? LT->w2 : nullptr, R, EPI_BIAS_RESID, st));
+  if (split_out) *split_out = dual;
   return GR4AD_OK;
 }
 
@@ -1011,9 +1016,11 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     rs.anc_stride = p.stride;
     rs.npos_u = t + 1;
     rs.npos_row = nullptr;
+    bool h_split = false;  // the last layer left Hs as fp16 hi / lo in N
     for (int i = K; i < p.L; ++i) {
       rs.qkv = hist + (size_t)(i - K) * hist_layer;
-      GR_TRY(layer_forward(p, w, wt, i, Hs, rs, ws, KV, VT, st));
+      GR_TRY(layer_forward(p, w, wt, i, Hs, rs, ws, KV, VT, st,
+                           (i == p.L - 1 && t < T) ? &h_split : nullptr));
     }
     if (t == T) {  // value re-rank step (beam.py:258-288)
       float *vlog = at<float>(ws, p.o_vlog);
@@ -1034,6 +1041,10 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       tl.alpha = lg.alpha / kWeightScale;
       tl.lse_part = at<float2>(ws, p.o_lsep);
       tl.lse_ld = (V + 127) / 128;
+      if (h_split) {
+        tl.a_hi = at<__half>(ws, p.o_N);
+        tl.a_lo = tl.a_hi + (size_t)p.Rw * d;
+      }
       GR_TRY(gemm_tc(tl, R, d, V, d, EPI_STORE_LSE, st));
       GR_TRY(lse_merge(tl.lse_part, tl.lse_ld, R, rinfo, st));
     } else {

@@ -30,7 +30,8 @@ enum GemmEpi {
   // next GEMM's pre-split A operand
   EPI_STORE_SPLIT = 9,
   EPI_BIAS_GELU_SPLIT = 10,
-  EPI_STORE_T_SPLIT = 11
+  EPI_STORE_T_SPLIT = 11,
+  EPI_BIAS_RESID_DUAL = 12  // EPI_BIAS_RESID, and the result also as fp16 hi / lo
 };
 
 struct GemmArgs {

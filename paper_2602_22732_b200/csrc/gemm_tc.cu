@@ -464,12 +464,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int lr = lane >> 3, c4 = (lane & 7) * 4;
         const int col = col0 + c4;
         const bool vec = col + 4 <= N && (a.ldc % 4) == 0 &&
-                         (EPI != EPI_RESID && EPI != EPI_BIAS_RESID || (a.ldr % 4) == 0) &&
+                         (EPI != EPI_RESID && EPI != EPI_BIAS_RESID && EPI != EPI_BIAS_RESID_DUAL ||
+         (a.ldr % 4) == 0) &&
                          (EPI != EPI_MULVEC || (a.vec_ld % 4) == 0) &&
                          (EPI != EPI_KV_SPLIT || (a.k_ld % 4) == 0);
         float4 bcol = make_float4(0.f, 0.f, 0.f, 0.f);
         if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID ||
-            EPI == EPI_BIAS_GELU_SPLIT) {
+            EPI == EPI_BIAS_GELU_SPLIT || EPI == EPI_BIAS_RESID_DUAL) {
           bcol.x = col < N ? a.bias[col] : 0.f;
           bcol.y = col + 1 < N ? a.bias[col + 1] : 0.f;
           bcol.z = col + 2 < N ? a.bias[col + 2] : 0.f;
@@ -484,7 +485,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
           if (rr < nrows && col < N) {
             const float *src = nullptr;
-            if (EPI == EPI_RESID || EPI == EPI_BIAS_RESID) src = a.R + grow * a.ldr + col;
+            if (EPI == EPI_RESID || EPI == EPI_BIAS_RESID || EPI == EPI_BIAS_RESID_DUAL)
+              src = a.R + grow * a.ldr + col;
             else if (EPI == EPI_MULVEC) src = a.vec + (long long)a.row_req[grow] * a.vec_ld + col;
             if (src) {
               if (vec) {
@@ -515,7 +517,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             else if (EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_GELU_SPLIT)
               x[q] = gelu_tanh_fast(x[q] + ob[q]);
             else if (EPI == EPI_RESID) x[q] = oo[q] + x[q];
-            else if (EPI == EPI_BIAS_RESID) x[q] = oo[q] + (x[q] + ob[q]);
+            else if (EPI == EPI_BIAS_RESID || EPI == EPI_BIAS_RESID_DUAL)
+              x[q] = oo[q] + (x[q] + ob[q]);
             else if (EPI == EPI_MULVEC) x[q] = oo[q] * x[q];
           }
           if (EPI == EPI_KV_SPLIT) {
@@ -543,7 +546,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
             continue;
           }
-          if (EPI == EPI_STORE_SPLIT || EPI == EPI_BIAS_GELU_SPLIT) {
+          if (EPI == EPI_STORE_SPLIT || EPI == EPI_BIAS_GELU_SPLIT || EPI == EPI_BIAS_RESID_DUAL) {
             __half hq[4], lq[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -560,7 +563,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 a.c_lo[o + q] = lq[q];
               }
             }
-            continue;
+            if (EPI != EPI_BIAS_RESID_DUAL) continue;
           }
           float *dst = a.C + grow * a.ldc + col;
           if (vec) {
@@ -662,6 +665,8 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
       GR_TC_EPI(EPI_BIAS_RESID)
       GR_TC_EPI(EPI_BIAS_GELU_SPLIT)
       GR_TC_EPI(EPI_STORE_SPLIT)
+      GR_TC_EPI(EPI_BIAS_RESID_DUAL)
+      GR_TC_EPI(EPI_STORE_LSE)
       default: return set_err(GR4AD_ERR_UNSUPPORTED, "pre-split-A tc epilogue %d", epi);
     }
   } else {
