@@ -2141,8 +2141,16 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
                                bscale, wb, sbuf, &scr[40], a.sort_cap);
       }
       GR_SUB(7);
+      GR_XSTAMP(1, 42);
+      GR_XSTAMP(2, 43);
+      GR_XSTAMP(3, 44);
+      GR_XSTAMP(5, 45);
+      GR_XSTAMP(7, 46);
       __syncthreads();
       collected = (int)scr[40];
+#ifdef GR_FUSED_TIMING
+      if (t == 2 && tid == 0) a.dbg[blockIdx.x * kDbgSlots + 47] = collected;
+#endif
       if (collected > a.sort_cap) {
         // window overflow: exact path -- every key to the scratch + histogram
         collected = -1;

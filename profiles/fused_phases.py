@@ -69,8 +69,8 @@ for t in range(3):
         s2 = (sub - tail[:, [level_start[t]]]) / 1e3
         print(f"  level-{t} warp-0 tile (fuse, ln+q, cross-attn, self+ffn, pass 1, [pass 2], window, collect)"
               f" cumulative us:", np.round(np.median(s2, 0), 2))
-x = tail[:, [42, 43, 44, 45, 46, 47, 16]]
+x = tail[:, 42:47]
 if (x > 0).all():
-    r = np.median((x - tail[:, [1]]) / 1e3, 0)
-    print("  trunk (LN1+q, u=qWk^T, cross-attn, PX Wv Wo + LN2, qkv + self-attn, so + LN3, FFN) "
-          "cumulative us from ctx proj end:", np.round(r, 2))
+    r = np.median((x - tail[:, [7]]) / 1e3, 0)
+    print("  level-2 loop-B end (us from level start) warps 1,2,3,5,7:", np.round(r, 2),
+          " window entries collected: median", np.median(tail[:, 47]), "max", tail[:, 47].max())
