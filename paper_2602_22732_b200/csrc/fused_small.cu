@@ -1476,7 +1476,10 @@ static __device__ __forceinline__ void ffn_mma(const float (&n)[D / 8][4], const
 
 // logits of the tile's rows for codebook tiles [n0, n0 + kLG) (clamped to nend)
 // from the level's codebook fragments staged in shared memory
-constexpr int kLG = 4;  // codebook tiles per logits group
+#ifndef GR_KLG
+#define GR_KLG 4
+#endif
+constexpr int kLG = GR_KLG;  // codebook tiles per logits group
 template <int K16>
 static __device__ __forceinline__ void logits_s(const uint32_t (&hh)[K16][4],
                                                 const uint32_t (&hl)[K16][4],
