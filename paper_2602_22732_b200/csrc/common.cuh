@@ -90,10 +90,10 @@ __device__ __forceinline__ float gelu_tanh(float a) {
 }
 
 // the same via 0.5 a (1 + tanh z) == a / (1 + exp(-2z)) with the hardware
-// exp2 (relative error ~1e-7; exp overflow -> a / inf = -0 for a << 0)
+// exp2 and divide (relative error ~2e-7; exp overflow -> 0 for a << 0)
 __device__ __forceinline__ float gelu_tanh_fast(float a) {
   const float c = 0.7978845608028654f;
-  return a / (1.0f + __expf(-2.0f * c * (a + 0.044715f * a * a * a)));
+  return __fdividef(a, 1.0f + __expf(-2.0f * c * (a + 0.044715f * a * a * a)));
 }
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
