@@ -96,12 +96,14 @@ struct Plan {
   size_t o_keys = 0, o_wT = 0;
   // warp-MMA variant of the fused kernel (d = 16)
   bool f_mma = false;
-  int f_s4[17] = {};  // as f_s, plus [12] X^T, [13] tile-group merge scratch, [14] codebook, [15] mbarrier, [16] pass-2 row state
+  int f_s4[18] = {};  // as f_s, plus [12] X^T, [13] tile-group merge scratch, [14] codebook, [15] mbarrier, [16] pass-2 row state
   int f_hst_rows = 0, f_head_floats = 0;
   size_t f_smem4 = 0;
   long long frag_f4 = 0;  // fragment-ordered weights (float4 count)
   size_t o_frag = 0, o_tu = 0;
   bool weights_prepared = false;  // batch->weights_prepared
+  size_t o_vprp[GR4AD_MAX_LEVELS] = {};  // masking: CSR row pointers per level
+  long long vp_np[GR4AD_MAX_LEVELS] = {};
   size_t o_flag = 0;  // fp16 range flag (set by the operand splits, read by gr4ad_range_status)
 };
 
@@ -181,6 +183,7 @@ static bool plan_fused_mma(Plan &p) {
   p.f_s4[14] = take((long long)D * vmax);  // one level's codebook fragments
   p.f_head_floats = D * vmax;
   p.f_s4[15] = take(4);                    // two mbarriers (16-B aligned)
+  p.f_s4[17] = take(mrows);                // rows' SID prefix keys (masking)
   // two CTAs per SM: 2 x (smem + 1 KB reserved) <= 228 KB
   constexpr size_t kMaxSmem = 113 * 1024;
   if ((size_t)o * sizeof(float) > kMaxSmem) return false;
@@ -355,8 +358,14 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     return set_err(GR4AD_ERR_UNSUPPORTED, "batch too large");
   bool masked = false;
   for (int t = 0; t < T; ++t) masked |= bt->valid_prefix[t] != nullptr;
-  if (bt->decode_path != 1 && bt->decode_path != 3 && !masked && B > 0) p.fused = plan_fused(p);
+  // masking runs in the warp-MMA kernel (prefix keys as int32 CSR rows)
+  long long n_prefix = 1;
+  for (int t = 0; t + 1 < T; ++t) n_prefix *= p.V[t];
+  const bool mask_fused = !masked || (bt->decode_path != 4 && n_prefix * p.V[T - 1] < (1LL << 31) &&
+                                      n_prefix <= (1LL << 24));
+  if (bt->decode_path != 1 && bt->decode_path != 3 && mask_fused && B > 0) p.fused = plan_fused(p);
   if (p.fused && bt->decode_path != 4) p.f_mma = plan_fused_mma(p);
+  if (p.fused && masked && !p.f_mma) p.fused = false;
   if ((bt->decode_path == 2 || bt->decode_path == 4) && !p.fused)
     return set_err(GR4AD_ERR_UNSUPPORTED, "fused decode path not eligible for this batch");
   if (!p.fused) {
@@ -412,6 +421,13 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
       p.o_tu = take(sizeof(float) * (size_t)std::max(p.n_pos, 1) * p.d);
     }
     p.o_keys = take(sizeof(uint32_t) * (size_t)B * p.f_keys_per_req);
+    // valid-SID masking: per level, CSR row pointers over the prefix key
+    long long np_t = 1;
+    for (int t = 0; t < T; ++t) {
+      p.o_vprp[t] = bt->valid_prefix[t] ? take(sizeof(int) * (size_t)(np_t + 1)) : 0;
+      p.vp_np[t] = np_t;
+      np_t *= p.V[t];
+    }
     take(sizeof(long long) * kDbgSlots * (size_t)B);  // per-request phase stamps (timing builds)
     p.total = o;
     return GR4AD_OK;
@@ -947,6 +963,11 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       f.s_mbar = p.f_s4[15];
       f.head_floats = p.f_head_floats;
       f.s_hst = p.f_s4[16];
+      f.s_pfx = p.f_s4[17];
+      for (int t = 0; t < T; ++t) {
+        f.vp_rp[t] = bt->valid_prefix[t] ? at<int>(ws, p.o_vprp[t]) : nullptr;
+        f.vp_keys[t] = reinterpret_cast<const long long *>(bt->valid_prefix[t]);
+      }
       f.hst_rows = p.f_hst_rows;
       f.tile_split = 1;
       f.Hrows = p.f_Hrows_mma;
@@ -1152,7 +1173,14 @@ int gr4ad_prepare(const gr4ad_dims *dims, const gr4ad_batch *batch, void *worksp
   GR_TRY(make_plan(dims, batch, p));
   if (workspace_bytes < p.total)
     return set_err(GR4AD_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, p.total);
-  return upload_tables(p, workspace, (cudaStream_t)stream);
+  GR_TRY(upload_tables(p, workspace, (cudaStream_t)stream));
+  if (p.fused)  // masking tables of the warp-MMA kernel
+    for (int t = 0; t < p.T; ++t)
+      if (batch->valid_prefix[t])
+        GR_TRY(csr_rows(reinterpret_cast<const long long *>(batch->valid_prefix[t]),
+                        batch->valid_prefix_count[t], p.V[t], p.vp_np[t],
+                        at<int>(workspace, p.o_vprp[t]), (cudaStream_t)stream));
+  return GR4AD_OK;
 }
 
 int gr4ad_beam_search_run(const gr4ad_dims *dims, const gr4ad_weights *w,

@@ -548,7 +548,7 @@ __device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S,
 __device__ int select_level(const FusedArgs &a, int b, int t, int live, int V,
                             const uint32_t *keys, unsigned *hist, unsigned *scr,
                             unsigned long long *sbuf, int *par, int *tokm, float *cum, float Rs,
-                            float bscale, int collected = -1) {
+                            float bscale, int collected = -1, int *pfx = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int T = a.T;
   auto sbin = [&](float sc) -> unsigned {
@@ -737,9 +737,22 @@ __device__ int select_level(const FusedArgs &a, int b, int t, int live, int V,
   for (int i = n_sort + tid; i < n2; i += kThreads) sbuf[i] = 0ull;
   __syncthreads();
   sort_desc(sbuf, n2);
+  // alive filter (beam.py:202-203): with masking, -inf candidates sort last;
+  // keep the finite prefix of the selection
+  int kk = k;
+  if (a.vp_rp[t]) {
+    if (tid == 0) scr[42] = (unsigned)k;
+    __syncthreads();
+    const uint32_t ninf = f2ord(-INFINITY);
+    for (int j = tid; j < k; j += kThreads)
+      if ((uint32_t)(sbuf[j] >> 32) <= ninf) atomicMin(&scr[42], (unsigned)j);
+    __syncthreads();
+    kk = (int)scr[42];
+  }
   // compaction: next-level rows in selection order (beam.py:202-210)
   const int mo1 = a.moff[t + 1];
-  for (int j = tid; j < k; j += kThreads) {
+  const int mo0 = a.moff[t];
+  for (int j = tid; j < kk; j += kThreads) {
     unsigned long long e = sbuf[j];
     // (clamped: non-finite scores from out-of-range inputs -- reported by
     // gr4ad_range_status -- must not turn into out-of-bounds rows)
@@ -747,8 +760,9 @@ __device__ int select_level(const FusedArgs &a, int b, int t, int live, int V,
     par[mo1 + j] = (int)(fi / (unsigned)V);
     tokm[mo1 + j] = (int)(fi % (unsigned)V);
     cum[mo1 + j] = ord2f((uint32_t)(e >> 32));
+    if (pfx) pfx[mo1 + j] = pfx[mo0 + fi / (unsigned)V] * V + (int)(fi % (unsigned)V);
   }
-  return k;
+  return kk;
 }
 
 template <int D>
@@ -1531,8 +1545,37 @@ struct RowScore {
   bool ok;
   int r;
   float cr, M, ls;
+  uint32_t vb0, vb1;  // valid-SID masking: bit 2n + c <-> token 8n + 2 t4 + c (all set: no mask)
 };
-template <int KT, bool COLLECT>
+
+// Valid-SID prefix masking (oracle prefix_mask): this
+// lane's valid-token bits of a row with prefix key P at level t, from the
+// level's CSR table (rows of sorted valid (t+1)-prefix keys grouped by P)
+static __device__ __forceinline__ void row_valid_bits(const FusedArgs &a, int t, int P, bool ok,
+                                                      RowScore &R) {
+  R.vb0 = R.vb1 = 0xFFFFFFFFu;
+  if (!a.vp_rp[t]) return;
+  R.vb0 = R.vb1 = 0u;
+  if (!ok) return;
+  const int V = a.V[t], t4 = threadIdx.x & 3;
+  const int lo = __ldg(a.vp_rp[t] + P), hi = __ldg(a.vp_rp[t] + P + 1);
+  const long long base = (long long)P * V;
+  for (int i = lo; i < hi; ++i) {
+    const int tok = (int)(__ldg(a.vp_keys[t] + i) - base);
+    if (((tok & 7) >> 1) == t4) {
+      const int bit = ((tok >> 3) << 1) | (tok & 1);
+      if (bit < 32)
+        R.vb0 |= 1u << bit;
+      else
+        R.vb1 |= 1u << (bit - 32);
+    }
+  }
+}
+static __device__ __forceinline__ bool tok_valid(const RowScore &R, int n, int c) {
+  const int bit = (n << 1) | (c & 1);
+  return ((bit < 32 ? R.vb0 : R.vb1) >> (bit & 31)) & 1u;
+}
+template <int KT, bool COLLECT, bool MASK>
 static __device__ __forceinline__ void logits_pass2(
     const uint32_t (&hh)[KT][4], const uint32_t (&hl)[KT][4], const uint4 *Hf, int NTV, int nb0,
     int nb1, const RowScore &A, const RowScore &B, int V, uint32_t *keys, unsigned *hist,
@@ -1556,8 +1599,12 @@ static __device__ __forceinline__ void logits_pass2(
         for (int side = 0; side < 2; ++side) {
           const RowScore &R = side ? B : A;
           if (n0 + j < nb1 && R.ok) {
-            const float s0 = R.cr + ((z[j][2 * side] - R.M) - R.ls);
-            const float s1 = R.cr + ((z[j][2 * side + 1] - R.M) - R.ls);
+            // masked tokens: logp = -inf after the log-softmax (oracle prefix_mask)
+            const float s0 = !MASK || tok_valid(R, n0 + j, 0) ? R.cr + ((z[j][2 * side] - R.M) - R.ls)
+                                                     : -INFINITY;
+            const float s1 = !MASK || tok_valid(R, n0 + j, 1)
+                                 ? R.cr + ((z[j][2 * side + 1] - R.M) - R.ls)
+                                 : -INFINITY;
             *reinterpret_cast<uint2 *>(keys + (size_t)R.r * V + col) = make_uint2(f2ord(s0), f2ord(s1));
             hist_add(hist, hcur, hcnt, (int)sbin(s0));
             hist_add(hist, hcur, hcnt, (int)sbin(s1));
@@ -1574,7 +1621,8 @@ static __device__ __forceinline__ void logits_pass2(
         for (int c = 0; c < 4; ++c) {  // padded tiles are -inf: never pass zA / zB
           const RowScore &R = c < 2 ? A : B;
           const float sc = R.cr + ((z[j][c] - R.M) - R.ls);
-          const bool in = z[j][c] > (c < 2 ? zA : zB) && sbin(sc) <= (unsigned)wb;
+          const bool in = z[j][c] > (c < 2 ? zA : zB) && sbin(sc) <= (unsigned)wb &&
+                          (!MASK || tok_valid(R, n0 + j, c));
           pm |= (in ? 1u : 0u) << (4 * j + c);
         }
       if (__any_sync(kFull, pm != 0)) {
@@ -1605,7 +1653,9 @@ static __device__ __forceinline__ void logits_pass2(
   }
 }
 
-template <int D>
+// MASK: valid-SID prefix masking compiled in (a separate instantiation, so
+// the unmasked decode carries none of its checks)
+template <int D, bool MASK>
 __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
   extern __shared__ __align__(16) float sm[];
   constexpr int KT = D / 8, VS = SP + 8, HS = 2 * D + 8;
@@ -1626,6 +1676,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
   float *HI = sm + a.s_hist;  // self-KV history rows [k | v | pad] (HS floats)
   int *par = reinterpret_cast<int *>(sm + a.s_par);
   int *tokm = reinterpret_cast<int *>(sm + a.s_tok);
+  int *pfx = reinterpret_cast<int *>(sm + a.s_pfx);  // rows' SID prefix keys (masking)
   float *cum = sm + a.s_cum;
   unsigned *hist = reinterpret_cast<unsigned *>(sm + a.s_bins);
   unsigned *scr = reinterpret_cast<unsigned *>(sm + a.s_scr);
@@ -1787,6 +1838,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
     par[0] = 0;
     tokm[0] = 0;
     cum[0] = 0.f;
+    pfx[0] = 0;
   }
   __syncthreads();
   GR_STAMP(2);
@@ -2003,6 +2055,11 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
       const int per = (NTV + wpt - 1) / wpt;
       const int nb0 = min(NTV, part * per), nb1 = min(NTV, nb0 + per);
       float mA = -INFINITY, mB = -INFINITY, sA = 0.f, sB = 0.f;
+      RowScore RA{okA, rA, 0.f, 0.f, 0.f, 0u, 0u}, RB{okB, rB, 0.f, 0.f, 0.f, 0u, 0u};
+      if (MASK) {
+        row_valid_bits(a, t, pfx[mo + cA], okA, RA);
+        row_valid_bits(a, t, pfx[mo + cB], okB, RB);
+      }
       float p1A = -INFINITY, p2A = -INFINITY, p1B = -INFINITY, p2B = -INFINITY;  // lane top-2
       for (int n0 = nb0; n0 < nb1; n0 += kLG) {
         float z[kLG][4];
@@ -2014,11 +2071,13 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
           gB = fmaxf(gB, fmaxf(z[j][2], z[j][3]));
           if (theta) {
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              p2A = fmaxf(p2A, fminf(p1A, z[j][c]));
-              p1A = fmaxf(p1A, z[j][c]);
-              p2B = fmaxf(p2B, fminf(p1B, z[j][2 + c]));
-              p1B = fmaxf(p1B, z[j][2 + c]);
+            for (int c = 0; c < 2; ++c) {  // proxies: valid candidates only
+              const float za = !MASK || tok_valid(RA, n0 + j, c) ? z[j][c] : -INFINITY;
+              const float zb = !MASK || tok_valid(RB, n0 + j, c) ? z[j][2 + c] : -INFINITY;
+              p2A = fmaxf(p2A, fminf(p1A, za));
+              p1A = fmaxf(p1A, za);
+              p2B = fmaxf(p2B, fminf(p1B, zb));
+              p1B = fmaxf(p1B, zb);
             }
           }
         }
@@ -2063,7 +2122,12 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
       }
       const float lsA = logf(SA), lsB = logf(SB);
       GR_SUB(4);
-      const RowScore RA{okA, rA, cum[mo + cA], MA, lsA}, RB{okB, rB, cum[mo + cB], MB, lsB};
+      RA.cr = cum[mo + cA];
+      RA.M = MA;
+      RA.ls = lsA;
+      RB.cr = cum[mo + cB];
+      RB.M = MB;
+      RB.ls = lsB;
       if (theta) {
         // save the tile's head input and (M, lse) for pass 2; emit the
         // per-lane top-2 candidates of each row as window proxies
@@ -2085,7 +2149,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
         px.w = okB && p2B > -INFINITY ? RB.cr + ((p2B - MB) - lsB) : -INFINITY;
         reinterpret_cast<float4 *>(prox)[(tile * wpt + part) * 32 + lane] = px;
       } else {
-        logits_pass2<KT / 2, false>(hh, hl, Hf, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt, Rs,
+        logits_pass2<KT / 2, false, MASK>(hh, hl, Hf, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt, Rs,
                                 bscale, 0, sbuf, nullptr, 0);
       }
       GR_SUB(5);
@@ -2134,13 +2198,17 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
         const int rA = tile * 16 + g, rB = rA + 8;
         const bool okA = rA < live, okB = rB < live;
         const int cA = min(rA, live - 1), cB = min(rB, live - 1);
-        const RowScore RA{okA, rA, cum[mo + cA], hst[cA * HSD + D], hst[cA * HSD + D + 1]};
-        const RowScore RB{okB, rB, cum[mo + cB], hst[cB * HSD + D], hst[cB * HSD + D + 1]};
+        RowScore RA{okA, rA, cum[mo + cA], hst[cA * HSD + D], hst[cA * HSD + D + 1], 0u, 0u};
+        RowScore RB{okB, rB, cum[mo + cB], hst[cB * HSD + D], hst[cB * HSD + D + 1], 0u, 0u};
+        if (MASK) {
+          row_valid_bits(a, t, pfx[mo + cA], okA, RA);
+          row_valid_bits(a, t, pfx[mo + cB], okB, RB);
+        }
         uint32_t hh[KT / 2][4], hl[KT / 2][4];
         load_split<KT / 2>(hst, HSD, cA, cB, hh, hl);
         const int NTV = V / 8, per = (NTV + wpt - 1) / wpt;
         const int nb0 = min(NTV, part * per), nb1 = min(NTV, nb0 + per);
-        logits_pass2<KT / 2, true>(hh, hl, HS2, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt, Rs,
+        logits_pass2<KT / 2, true, MASK>(hh, hl, HS2, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt, Rs,
                                bscale, wb, sbuf, &scr[40], a.sort_cap);
       }
       GR_SUB(7);
@@ -2163,13 +2231,17 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
           const int rA = tile * 16 + g, rB = rA + 8;
           const bool okA = rA < live, okB = rB < live;
           const int cA = min(rA, live - 1), cB = min(rB, live - 1);
-          const RowScore RA{okA, rA, cum[mo + cA], hst[cA * HSD + D], hst[cA * HSD + D + 1]};
-          const RowScore RB{okB, rB, cum[mo + cB], hst[cB * HSD + D], hst[cB * HSD + D + 1]};
+          RowScore RA{okA, rA, cum[mo + cA], hst[cA * HSD + D], hst[cA * HSD + D + 1], 0u, 0u};
+          RowScore RB{okB, rB, cum[mo + cB], hst[cB * HSD + D], hst[cB * HSD + D + 1], 0u, 0u};
+          if (MASK) {
+            row_valid_bits(a, t, pfx[mo + cA], okA, RA);
+            row_valid_bits(a, t, pfx[mo + cB], okB, RB);
+          }
           uint32_t hh[KT / 2][4], hl[KT / 2][4];
           load_split<KT / 2>(hst, HSD, cA, cB, hh, hl);
           const int NTV = V / 8, per = (NTV + wpt - 1) / wpt;
           const int nb0 = min(NTV, part * per), nb1 = min(NTV, nb0 + per);
-          logits_pass2<KT / 2, false>(hh, hl, HS2, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt,
+          logits_pass2<KT / 2, false, MASK>(hh, hl, HS2, NTV, nb0, nb1, RA, RB, V, keys, hist, hcur, hcnt,
                                   Rs, bscale, 0, sbuf, nullptr, 0);
         }
       }
@@ -2183,7 +2255,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
                 hbar);
     }
     live = select_level(a, b, t, live, V, keys, hist, scr, sbuf, par, tokm, cum, Rs, bscale,
-                        collected);
+                        collected, MASK ? pfx : nullptr);
     if (live < 0) return;
     __syncthreads();
     GR_STAMP(5 + 2 * t);
@@ -2270,9 +2342,17 @@ int frag_prep_launch(const FragJobs &jobs, uint4 *frag, int *range_flag, cudaStr
 int fused_mma_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream_t st) {
   if (n_requests <= 0) return GR4AD_OK;
   if (a.D != 16) return set_err(GR4AD_ERR_UNSUPPORTED, "warp-MMA fused decode: d=%d", a.D);
-  GR_CUDA(cudaFuncSetAttribute(fused_mma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
-  GR_LAUNCH(KC_FUSED, st, fused_mma_kernel<16><<<n_requests, kThreads, smem, st>>>(a));
+  bool masked = false;
+  for (int t = 0; t < a.T; ++t) masked |= a.vp_rp[t] != nullptr;
+  if (masked) {
+    GR_CUDA(cudaFuncSetAttribute(fused_mma_kernel<16, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GR_LAUNCH(KC_FUSED, st, fused_mma_kernel<16, true><<<n_requests, kThreads, smem, st>>>(a));
+  } else {
+    GR_CUDA(cudaFuncSetAttribute(fused_mma_kernel<16, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GR_LAUNCH(KC_FUSED, st, fused_mma_kernel<16, false><<<n_requests, kThreads, smem, st>>>(a));
+  }
   return GR4AD_OK;
 }
 

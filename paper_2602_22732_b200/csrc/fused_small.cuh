@@ -61,6 +61,11 @@ struct FusedArgs {
   int tile_split;         // warp-MMA kernel: warps share tiles on small levels
   const float *trunk_u;   // warp-MMA kernel: [n_pos][D] layer-0 trunk queries (FragJobs.tu)
   int *range_flag;        // warp-MMA kernel: set when a scaled K / V leaves the fp16 range
+  // warp-MMA kernel, valid-SID prefix masking: per level, CSR rows over the
+  // prefix key P (vp_rp[t][P] .. vp_rp[t][P+1] index vp_keys[t]); NULL: no mask
+  const int *vp_rp[GR4AD_MAX_LEVELS];
+  const long long *vp_keys[GR4AD_MAX_LEVELS];
+  int s_pfx;              // warp-MMA kernel: rows' prefix keys (int)
   const uint4 *frag;      // warp-MMA kernel: fragment-ordered weights (fp16 hi / lo)
   FragIndex fi;
   uint32_t *keys;  // candidate keys scratch (L2-resident), keys_per_req per request

@@ -389,6 +389,23 @@ __global__ void mask_rows_kernel(float *logits, long long ld, int rows, int V,
     if (!((bits[v >> 5] >> (v & 31)) & 1u)) x[v] = -INFINITY;
 }
 
+// CSR row pointers of sorted (t+1)-prefix keys grouped by their t-prefix P =
+// key / V: rp[P] = lower_bound(keys, P V) for P in [0, n_prefix]
+__global__ void csr_rows_kernel(const long long *__restrict__ keys, int n, int V,
+                                long long n_prefix, int *rp) {
+  const long long P = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (P > n_prefix) return;
+  rp[P] = lower_bound64(keys, n, P * V);
+}
+
+int csr_rows(const long long *keys, int n, int V, long long n_prefix, int *rp,
+             cudaStream_t st) {
+  const long long m = n_prefix + 1;
+  GR_LAUNCH(KC_SMALL, st, csr_rows_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(
+                              keys, n, V, n_prefix, rp));
+  return GR4AD_OK;
+}
+
 int mask_rows(float *logits, long long ld, int rows, int V, const long long *prefix,
               const long long *valid, int n_valid, cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;

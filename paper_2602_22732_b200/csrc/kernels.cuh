@@ -42,6 +42,9 @@ int row_lse(const float *logits, long long ld, int rows, int V, float2 *info,
 
 // valid-SID prefix mask: logits[r][v] = -inf unless prefix[r]*V + v is a
 // valid key (sorted array). SURVEY §8f row 2 (no reference counterpart).
+// CSR row pointers (over the t-prefix key) of sorted valid (t+1)-prefix keys
+int csr_rows(const long long *keys, int n, int V, long long n_prefix, int *rp,
+             cudaStream_t st);
 int mask_rows(float *logits, long long ld, int rows, int V, const long long *prefix,
               const long long *valid, int n_valid, cudaStream_t st);
 

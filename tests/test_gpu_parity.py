@@ -359,3 +359,26 @@ def test_exact_ties_follow_reference_order(path):
         want = orc.beam_search(params, C1_MODEL, orc.context_process(feats[i], params), C2_WIDTHS)
         assert [sid.tokens for sid, _ in got[i]] == [tuple(t) for t, _ in want]
         np.testing.assert_allclose([s for _, s in got[i]], [s for _, s in want], rtol=1e-6)
+
+
+@pytest.mark.parametrize("path", ["fused", "layered", "tensor"])
+@pytest.mark.parametrize("n_valid", [300, 20000])
+def test_prefix_masking_c1_model(path, n_valid):
+    """Valid-SID prefix masking on the C1 model (the fused warp-MMA kernel
+    masks inside its window selection): sparse and dense valid sets against
+    the oracle restatement; beams that run out of valid continuations drop
+    (alive filter)."""
+    M, S = _pkg()
+    model = _model(M, C1_MODEL)
+    params = {k: v.data for k, v in model.params.items()}
+    rng = np.random.default_rng(n_valid)
+    valid = sorted({tuple(int(x) for x in rng.integers(0, 256, size=3)) for _ in range(n_valid)})
+    feats = [c_features(i, 256) for i in range(3)]
+    got = S.beam_search_batch(model, features=feats, schedules=S.BeamSchedule(C2_WIDTHS, 256),
+                              valid_sids=valid, path=path)
+    vset = set(valid)
+    for i in range(3):
+        want = orc.beam_search(params, C1_MODEL, orc.context_process(feats[i], params), C2_WIDTHS,
+                               valid_sids=valid)
+        assert all(sid.tokens in vset for sid, _ in got[i])
+        check_parity(want, [(sid.tokens, s) for sid, s in got[i]], f"mask{n_valid}[{i}]")
