@@ -257,12 +257,103 @@ self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
   }
 }
 
+// Warp per row for d % 128 == 0, d <= 1024 (NV = d / 128 float4 per lane):
+// q in registers, every ancestor's k / v row gathered with NV independent
+// 16-B loads per lane, scores and softmax in registers -- no block barrier
+template <int NV>
+__global__ void __launch_bounds__(256)
+self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
+                      const int *__restrict__ anc, int stride, int hist_row0, int rows,
+                      int npos_u, const int *__restrict__ npos_row, float *out, long long ldo,
+                      float scale, __half *out_hi, __half *out_lo) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int g = hist_row0 + r;
+  const int np = npos_row ? npos_row[r] : npos_u;
+  const float4 *q4 = reinterpret_cast<const float4 *>(qkv + (long long)g * ld3);
+  float4 q[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) q[i] = q4[lane + 32 * i];
+  float sc[kMaxPos];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int t = 0; t < kMaxPos; ++t) {
+    sc[t] = -INFINITY;
+    if (t < np) {
+      const float4 *k4 =
+          reinterpret_cast<const float4 *>(qkv + (long long)anc[(long long)g * stride + t] * ld3 + d);
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const float4 k = k4[lane + 32 * i];
+        acc = fmaf(q[i].x, k.x, fmaf(q[i].y, k.y, fmaf(q[i].z, k.z, fmaf(q[i].w, k.w, acc))));
+      }
+      sc[t] = warp_sum(acc) * scale;
+      mx = fmaxf(mx, sc[t]);
+    }
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int t = 0; t < kMaxPos; ++t)
+    if (t < np) sum += expf(sc[t] - mx);
+  const float lse = logf(sum) + mx;
+  float4 o[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int t = 0; t < kMaxPos; ++t) {
+    if (t < np) {
+      const float pt = expf(sc[t] - lse);
+      const float4 *v4 = reinterpret_cast<const float4 *>(
+          qkv + (long long)anc[(long long)g * stride + t] * ld3 + 2 * d);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const float4 v = v4[lane + 32 * i];
+        o[i].x = fmaf(pt, v.x, o[i].x);
+        o[i].y = fmaf(pt, v.y, o[i].y);
+        o[i].z = fmaf(pt, v.z, o[i].z);
+        o[i].w = fmaf(pt, v.w, o[i].w);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int j = 4 * (lane + 32 * i);
+    if (out_hi) {  // fp16 hi / lo split for the next GEMM's A operand
+      const float oo[4] = {o[i].x, o[i].y, o[i].z, o[i].w};
+      __half h[4], l[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        h[c] = __float2half_rn(oo[c]);
+        l[c] = __float2half_rn(oo[c] - __half2float(h[c]));
+      }
+      *reinterpret_cast<uint2 *>(out_hi + (long long)r * ldo + j) = *reinterpret_cast<const uint2 *>(h);
+      *reinterpret_cast<uint2 *>(out_lo + (long long)r * ldo + j) = *reinterpret_cast<const uint2 *>(l);
+    } else {
+      *reinterpret_cast<float4 *>(out + (long long)r * ldo + j) = o[i];
+    }
+  }
+}
+
 int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_stride,
               int hist_row0, int rows, int npos_uniform, const int *npos_row,
               float *out, long long ldo, cudaStream_t st, __half *out_hi, __half *out_lo) {
   if (rows <= 0) return GR4AD_OK;
   if (out_hi && (d % 4 != 0 || ld3 % 4 != 0 || ldo % 4 != 0))
     return set_err(GR4AD_ERR_UNSUPPORTED, "split self-attention output: d %d", d);
+  const float scale = 1.0f / sqrtf((float)d);
+  if (d % 128 == 0 && d <= 1024 && ld3 % 4 == 0 && ldo % 4 == 0) {
+#define GR_SAW(NV)                                                                           \
+  case NV:                                                                                   \
+    GR_LAUNCH(KC_SELF_ATTN, st, self_attn_warp_kernel<NV><<<ceil_div(rows, 8), 256, 0, st>>>( \
+                                    qkv, ld3, d, anc, anc_stride, hist_row0, rows,           \
+                                    npos_uniform, npos_row, out, ldo, scale, out_hi, out_lo)); \
+    return GR4AD_OK;
+    switch (d / 128) {
+      GR_SAW(1) GR_SAW(2) GR_SAW(3) GR_SAW(4) GR_SAW(5) GR_SAW(6) GR_SAW(7) GR_SAW(8)
+    }
+#undef GR_SAW
+  }
   GR_LAUNCH(KC_SELF_ATTN, st, self_attn_kernel<<<rows, 128, 0, st>>>(qkv, ld3, d, anc, anc_stride, hist_row0, rows,
                                          npos_uniform, npos_row, out, ldo,
                                          1.0f / sqrtf((float)d), out_hi, out_lo));
