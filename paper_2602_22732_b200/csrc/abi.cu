@@ -455,7 +455,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.o_SCs = take(p.tc ? sizeof(__half) * 2 * p.Rw * p.sc_ld : 16);  // P as fp16 hi, lo
   p.o_LG = take(Fl * p.Rw * std::max(p.Vmax, p.nb));
   p.o_rinfo = take(sizeof(float2) * p.Rw);
-  p.o_lsep = take(p.tc ? sizeof(float2) * p.Rw * ((p.Vmax + 127) / 128) : 16);
+  p.o_lsep = take(p.tc ? sizeof(float4) * p.Rw * ((p.Vmax + 127) / 128) : 16);
   p.o_vlog = take(Fl * std::max(p.R[T], 1LL) * p.nb);
   p.o_hist = take(Fl * p.H * 3 * d * (size_t)(p.L - p.K));
   if (p.tc) {
@@ -917,6 +917,12 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
   return GR4AD_OK;
 }
 
+// debug / A-B aid: GR4AD_NO_PROXY=1 selects with the histogram pass only
+static bool no_proxy_window() {
+  static const bool off = getenv("GR4AD_NO_PROXY") != nullptr;
+  return off;
+}
+
 static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
                     const gr4ad_batch *bt, const float *features, const float *context,
                     gr4ad_results *out, void *ws, cudaStream_t st) {
@@ -1052,6 +1058,7 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     // codebook projection + log-softmax + score accumulation + top-k (beam.py:198-210)
     const int V = p.V[t];
     const GemmArgs lg = plain_gemm(Hs, d, w->head[t], V, LG, V, R, V, d);
+    const float4 *proxies = nullptr;
     if (p.tc && wt && d % 8 == 0 && tc_eligible(d, d, d, Hs, wt->head[t])) {
       // log-sum-exp partials from the GEMM epilogue (no second pass over the logits)
       TcArgs tl{};
@@ -1060,7 +1067,7 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       tl.b_lo = wt->head[t] + p.wt_floats;
       tl.ldb = d;
       tl.alpha = lg.alpha / kWeightScale;
-      tl.lse_part = at<float2>(ws, p.o_lsep);
+      tl.lse_part = at<float4>(ws, p.o_lsep);
       tl.lse_ld = (V + 127) / 128;
       if (h_split) {
         tl.a_hi = at<__half>(ws, p.o_N);
@@ -1068,6 +1075,7 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       }
       GR_TRY(gemm_tc(tl, R, d, V, d, EPI_STORE_LSE, st));
       GR_TRY(lse_merge(tl.lse_part, tl.lse_ld, R, rinfo, st));
+      if (!bt->valid_prefix[t] && !no_proxy_window()) proxies = tl.lse_part;
     } else {
       GR_TRY(dense(p, lg, wt ? wt->head[t] : nullptr, R, EPI_STORE, st));
       GR_TRY(row_lse(LG, V, R, V, rinfo, st));
@@ -1080,6 +1088,7 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     SelectArgs sa{};
     sa.logits = LG; sa.ld = V; sa.V = V; sa.level = t;
     sa.rowinfo = rinfo; sa.cum = cum;
+    sa.proxies = proxies; sa.proxy_ld = (V + 127) / 128;
     sa.row_off = row_off + (size_t)t * B;
     sa.live = live + (size_t)t * B;
     sa.eff = eff + (size_t)t * B;

@@ -370,7 +370,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int rbase = ti.m0 + q * 32;  // this warp's 32 rows (tile M side)
       const int nrows = min(32, ti.M - rbase);
       const int N = ti.N;
-      float pm = -INFINITY, ps = 0.f;  // EPI_STORE_LSE: this lane's row, current 128 columns
+      // EPI_STORE_LSE: this lane's row, current 128 columns: max, sum, top-2
+      float pm = -INFINITY, ps = 0.f, pt1 = -INFINITY, pt2 = -INFINITY;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         float v[32];
@@ -381,7 +382,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           float cm = -INFINITY;
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj)
-            if (col0 + jj < N) cm = fmaxf(cm, v[jj] * a.alpha);
+            if (col0 + jj < N) {
+              const float x = v[jj] * a.alpha;
+              cm = fmaxf(cm, x);
+              pt2 = fmaxf(pt2, fminf(pt1, x));
+              pt1 = fmaxf(pt1, x);
+            }
           const float nm = fmaxf(pm, cm);
           float cs = 0.f;
 #pragma unroll
@@ -392,9 +398,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if ((c & 3) == 3 || col0 + 32 >= N) {
             if (lane < nrows)
               a.lse_part[((long long)ti.c_row + rbase + lane) * a.lse_ld + col0 / 128] =
-                  make_float2(pm, ps);
+                  make_float4(pm, ps, pt1, pt2);
             pm = -INFINITY;
             ps = 0.f;
+            pt1 = pt2 = -INFINITY;
           }
         }
         if (EPI == EPI_STORE_T || EPI == EPI_STORE_T_SPLIT) {

@@ -27,9 +27,10 @@ struct TcArgs : GemmArgs {
   float kv_scale;
   int kv_d;
   int *range_flag;  // EPI_KV_SPLIT: set when a scaled value leaves the fp16 range
-  // EPI_STORE_LSE: lse_part[row * lse_ld + col / 128] = (max, sum exp(x - max))
-  // over the row's columns [128 j, 128 j + 128) (merged by lse_merge)
-  float2 *lse_part;
+  // EPI_STORE_LSE: lse_part[row * lse_ld + col / 128] = (max, sum exp(x - max),
+  // top-1, top-2) over the row's columns [128 j, 128 j + 128) (merged by
+  // lse_merge; top-1 / top-2 are the selection's window proxies)
+  float4 *lse_part;
   int lse_ld;
 };
 

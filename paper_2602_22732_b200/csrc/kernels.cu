@@ -144,9 +144,67 @@ __global__ void softmax_rows_split_kernel(const float *__restrict__ s, long long
   }
 }
 
+// the same with the row in registers (ld % 128 == 0, ld <= 2048): float4 loads,
+// one read of the scores
+template <int NV>
+__global__ void softmax_rows_split_reg_kernel(const float *__restrict__ s, long long ld,
+                                              __half *p_hi, __half *p_lo, int rows,
+                                              const int *__restrict__ row_req,
+                                              const int *__restrict__ len) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const int n = len[row_req[w]];
+  const float4 *r4 = reinterpret_cast<const float4 *>(s + (long long)w * ld);
+  float x[NV][4];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int j = 4 * (lane + 32 * i);
+    const float4 v = r4[lane + 32 * i];
+    x[i][0] = j < n ? v.x : -INFINITY;
+    x[i][1] = j + 1 < n ? v.y : -INFINITY;
+    x[i][2] = j + 2 < n ? v.z : -INFINITY;
+    x[i][3] = j + 3 < n ? v.w : -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) mx = fmaxf(mx, x[i][c]);
+  }
+  mx = warp_max(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sum += x[i][c] == -INFINITY ? 0.f : expf(x[i][c] - mx);
+  const float lse = logf(warp_sum(sum)) + mx;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int j = 4 * (lane + 32 * i);
+    __half h[4], l[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float pv = x[i][c] == -INFINITY ? 0.f : expf(x[i][c] - lse);  // 0 past S_b
+      h[c] = __float2half_rn(pv);
+      l[c] = __float2half_rn(pv - __half2float(h[c]));
+    }
+    *reinterpret_cast<uint2 *>(p_hi + (long long)w * ld + j) = *reinterpret_cast<const uint2 *>(h);
+    *reinterpret_cast<uint2 *>(p_lo + (long long)w * ld + j) = *reinterpret_cast<const uint2 *>(l);
+  }
+}
+
 int softmax_rows_split(const float *s, long long ld, __half *p_hi, __half *p_lo, int rows,
                        const int *row_req, const int *len, cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;
+  if (ld % 128 == 0 && ld <= 2048) {
+#define GR_SMS(NV)                                                                           \
+  case NV:                                                                                   \
+    GR_LAUNCH(KC_SOFTMAX, st, softmax_rows_split_reg_kernel<NV><<<ceil_div(rows, 8), 256, 0, st>>>( \
+                                  s, ld, p_hi, p_lo, rows, row_req, len));                   \
+    return GR4AD_OK;
+    switch (ld / 128) {
+      GR_SMS(1) GR_SMS(2) GR_SMS(3) GR_SMS(4) GR_SMS(5) GR_SMS(6) GR_SMS(7) GR_SMS(8)
+      GR_SMS(9) GR_SMS(10) GR_SMS(11) GR_SMS(12) GR_SMS(13) GR_SMS(14) GR_SMS(15) GR_SMS(16)
+    }
+#undef GR_SMS
+  }
   GR_LAUNCH(KC_SOFTMAX, st, softmax_rows_split_kernel<<<ceil_div(rows, 8), 256, 0, st>>>(
                                 s, ld, p_hi, p_lo, rows, row_req, len));
   return GR4AD_OK;
@@ -413,7 +471,7 @@ row_lse_kernel(const float *__restrict__ logits, long long ld, int rows, int V,
 
 // (max, log sum exp) per row from the logits GEMM's per-128-column partials
 // (EPI_STORE_LSE): warp per row
-__global__ void lse_merge_kernel(const float2 *__restrict__ part, int n_part, int rows,
+__global__ void lse_merge_kernel(const float4 *__restrict__ part, int n_part, int rows,
                                  float2 *info) {
   const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -422,14 +480,14 @@ __global__ void lse_merge_kernel(const float2 *__restrict__ part, int n_part, in
   m = warp_max(m);
   float s = 0.f;
   for (int j = lane; j < n_part; j += 32) {
-    const float2 p2 = part[(long long)r * n_part + j];
+    const float4 p2 = part[(long long)r * n_part + j];
     if (p2.x != -INFINITY) s += p2.y * expf(p2.x - m);
   }
   s = warp_sum(s);
   if (lane == 0) info[r] = make_float2(m, logf(s));
 }
 
-int lse_merge(const float2 *part, int n_part, int rows, float2 *info, cudaStream_t st) {
+int lse_merge(const float4 *part, int n_part, int rows, float2 *info, cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;
   GR_LAUNCH(KC_ROW_LSE, st, lse_merge_kernel<<<(rows + 7) / 8, 256, 0, st>>>(part, n_part, rows, info));
   return GR4AD_OK;
@@ -517,6 +575,12 @@ int mask_rows(float *logits, long long ld, int rows, int V, const long long *pre
 // candidate set fits in shared memory the keys are cached there after the
 // first pass.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 constexpr int kSelThreads = 1024;
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kCacheKeys = 28 * 1024;  // 112 KB of cached keys
@@ -672,22 +736,73 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
     for (int w = 0; w < kSelWarps; ++w) Rs = fmaxf(Rs, s_red[w]);
     const float scale = 2048.0f / (logf((float)max(c.V, 2)) + 4.0f);
     auto sbin = [&](float s) -> unsigned { return (unsigned)fminf((Rs - s) * scale, 2047.0f); };
-    int cur = -1;
-    unsigned cnt = 0;
     // 16-B rows: float4 loads, four candidates per lane and load
     const bool vec4 = !CACHE && c.V % 4 == 0 && c.ld % 4 == 0;
-    for (int r = wid; r < c.n_rows; r += kSelWarps) {
-      const float cr = c.cum[c.hist0 + c.row0 + r];
-      const float2 ri = c.rowinfo ? c.rowinfo[c.row0 + r] : make_float2(0.f, 0.f);
-      if (vec4) {
-        const float4 *row4 = reinterpret_cast<const float4 *>(c.logits + (long long)(c.row0 + r) * c.ld);
-#pragma unroll 4
-        for (int v4 = lane; v4 < c.V / 4; v4 += 32) {
-          const float4 l4 = row4[v4];
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+    // attempt 0: window bin from the logits GEMM epilogue's per-row top-2
+    // proxies (every proxy is a real candidate with the identical score
+    // expression, so the k-th best proxy's bin bounds the k-th best
+    // candidate's): no histogram pass over the logits.  Attempt 1: the
+    // histogram pass.  A window wider than the sort buffer falls through.
+    for (int attempt = (a.proxies && !CACHE) ? 0 : 1; attempt < 2 && !window; ++attempt) {
+      int cur = -1;
+      unsigned cnt = 0;
+      if (attempt == 0) {
+        if (tid == 0) s_nfin = 0;
+        __syncthreads();
+        unsigned nprox = 0;
+        for (int r = wid; r < c.n_rows; r += kSelWarps) {
+          const float cr = c.cum[c.hist0 + c.row0 + r];
+          const float2 ri = c.rowinfo[c.row0 + r];
+          for (int j = lane; j < a.proxy_ld; j += 32) {
+            const float4 pr = a.proxies[(long long)(c.row0 + r) * a.proxy_ld + j];
+            const float pv[2] = {pr.z, pr.w};
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float s = cr + (c.rowinfo ? ((lv[q] - ri.x) - ri.y) : lv[q]);
+            for (int q = 0; q < 2; ++q)
+              if (pv[q] > -INFINITY) {
+                const int bin = (int)sbin(cr + ((pv[q] - ri.x) - ri.y));
+                ++nprox;
+                if (bin == cur) {
+                  ++cnt;
+                } else {
+                  if (cnt) atomicAdd(&hist[cur], cnt);
+                  cur = bin;
+                  cnt = 1;
+                }
+              }
+          }
+        }
+        nprox = warp_sum_u(nprox);
+        if (lane == 0 && nprox) atomicAdd(&s_nfin, nprox);
+      } else {
+        for (int r = wid; r < c.n_rows; r += kSelWarps) {
+          const float cr = c.cum[c.hist0 + c.row0 + r];
+          const float2 ri = c.rowinfo ? c.rowinfo[c.row0 + r] : make_float2(0.f, 0.f);
+          if (vec4) {
+            const float4 *row4 =
+                reinterpret_cast<const float4 *>(c.logits + (long long)(c.row0 + r) * c.ld);
+#pragma unroll 4
+            for (int v4 = lane; v4 < c.V / 4; v4 += 32) {
+              const float4 l4 = row4[v4];
+              const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float s = cr + (c.rowinfo ? ((lv[q] - ri.x) - ri.y) : lv[q]);
+                const int bin = (int)sbin(s);
+                if (bin == cur) {
+                  ++cnt;
+                } else {
+                  if (cnt) atomicAdd(&hist[cur], cnt);
+                  cur = bin;
+                  cnt = 1;
+                }
+              }
+            }
+            continue;
+          }
+          for (int v = lane; v < c.V; v += 32) {
+            const float lg = c.logits[(long long)(c.row0 + r) * c.ld + v];
+            const float s = cr + (c.rowinfo ? ((lg - ri.x) - ri.y) : lg);
+            if (CACHE) keys[(long long)r * c.V + v] = f2ord(s);
             const int bin = (int)sbin(s);
             if (bin == cur) {
               ++cnt;
@@ -698,39 +813,29 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
             }
           }
         }
+      }
+      if (cnt) atomicAdd(&hist[cur], cnt);
+      __syncthreads();
+      if (attempt == 0 && s_nfin < (unsigned)k) {  // too few proxies (uniform)
+        for (int i = tid; i < 2048; i += kSelThreads) hist[i] = 0u;
+        __syncthreads();
         continue;
       }
-      for (int v = lane; v < c.V; v += 32) {
-        const float lg = c.logits[(long long)(c.row0 + r) * c.ld + v];
-        const float s = cr + (c.rowinfo ? ((lg - ri.x) - ri.y) : lg);
-        if (CACHE) keys[(long long)r * c.V + v] = f2ord(s);
-        const int bin = (int)sbin(s);
-        if (bin == cur) {
-          ++cnt;
-        } else {
-          if (cnt) atomicAdd(&hist[cur], cnt);
-          cur = bin;
-          cnt = 1;
-        }
+      for (int i = tid; i < 1024; i += kSelThreads) {  // mirror: sel_find_bin scans from the top
+        unsigned x = hist[i], y = hist[2047 - i];
+        hist[i] = y;
+        hist[2047 - i] = x;
       }
-    }
-    if (cnt) atomicAdd(&hist[cur], cnt);
-    __syncthreads();
-    for (int i = tid; i < 1024; i += kSelThreads) {  // mirror: sel_find_bin scans from the top
-      unsigned x = hist[i], y = hist[2047 - i];
-      hist[i] = y;
-      hist[2047 - i] = x;
-    }
-    __syncthreads();
-    unsigned above;
-    const int rb = sel_find_bin(hist, 2048, (unsigned)k, &above, scan);
-    const int wb = 2047 - rb;
-    const unsigned cnt_le = above + hist[rb];
-    if (wb < 2047 && cnt_le <= (unsigned)GR4AD_MAX_BEAM) {
-      window = true;
-      n_sort = (int)cnt_le;
+      __syncthreads();
+      unsigned above;
+      const int rb = sel_find_bin(hist, 2048, (unsigned)k, &above, scan);
+      const int wb = 2047 - rb;
+      const unsigned cnt_le = above + hist[rb];
+      __syncthreads();
+      for (int i = tid; i < 2048; i += kSelThreads) hist[i] = 0u;
       if (tid == 0) s_gt_pos = 0;
       __syncthreads();
+      if (wb == 2047 || (attempt == 1 && cnt_le > (unsigned)GR4AD_MAX_BEAM)) continue;
       for (int r = wid; r < c.n_rows; r += kSelWarps) {
         const float cr = c.cum[c.hist0 + c.row0 + r];
         const float2 ri = c.rowinfo ? c.rowinfo[c.row0 + r] : make_float2(0.f, 0.f);
@@ -765,7 +870,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
               for (int q = 0; q < 4; ++q)
                 if ((pm >> q) & 1u) {
                   const unsigned fi = (unsigned)((long long)r * c.V + 4 * v4 + q);
-                  sbuf[base++] = ((unsigned long long)f2ord(sv[q]) << 32) | (0xFFFFFFFFu - fi);
+                  if (base < (unsigned)GR4AD_MAX_BEAM)  // (proxy window: counted, checked below)
+                    sbuf[base] = ((unsigned long long)f2ord(sv[q]) << 32) | (0xFFFFFFFFu - fi);
+                  ++base;
                 }
             }
           }
@@ -788,13 +895,20 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
             unsigned base = 0;
             if (lane == 0) base = atomicAdd(&s_gt_pos, __popc(m));
             base = __shfl_sync(0xffffffffu, base, 0);
-            if (take) {
+            const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
+            if (take && pos < (unsigned)GR4AD_MAX_BEAM) {
               const unsigned fi = (unsigned)((long long)r * c.V + v);
-              sbuf[base + __popc(m & ((1u << lane) - 1u))] =
-                  ((unsigned long long)f2ord(s) << 32) | (0xFFFFFFFFu - fi);
+              sbuf[pos] = ((unsigned long long)f2ord(s) << 32) | (0xFFFFFFFFu - fi);
             }
           }
         }
+      }
+      __syncthreads();
+      const unsigned n_win = s_gt_pos;  // (the proxy window's size is known only now)
+      __syncthreads();
+      if (n_win <= (unsigned)GR4AD_MAX_BEAM) {
+        window = true;
+        n_sort = (int)n_win;
       }
     }
     __syncthreads();

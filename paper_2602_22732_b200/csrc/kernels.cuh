@@ -36,7 +36,7 @@ int level_input(int t, int rows, int d, const float *bos, const float *emb_prev,
                 cudaStream_t st);
 
 // per-row (max, log sum exp(x - max)) (beam.py:92-95)
-int lse_merge(const float2 *part, int n_part, int rows, float2 *info, cudaStream_t st);
+int lse_merge(const float4 *part, int n_part, int rows, float2 *info, cudaStream_t st);
 int row_lse(const float *logits, long long ld, int rows, int V, float2 *info,
             cudaStream_t st);
 
@@ -55,6 +55,10 @@ struct SelectArgs {
   int V;
   int level;
   const float2 *rowinfo;  // per level row
+  // optional (no masking): per level row, proxy_ld (max, sum, top1, top2)
+  // partials of the logits GEMM epilogue; top1 / top2 are window proxies
+  const float4 *proxies;
+  int proxy_ld;
   const float *cum;       // per history row
   const int *row_off;     // [B] row offset (within level t)
   const int *live;        // [B] live rows of request (level t)
