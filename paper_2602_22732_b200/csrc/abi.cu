@@ -83,7 +83,7 @@ struct Plan {
   // tensor-core layered path
   bool tc = false;
   long long sc_ld = 0, vt_ld = 0;
-  size_t o_VT = 0, o_WT = 0, o_XT = 0, o_VTlo = 0, o_KVlo = 0;
+  size_t o_VT = 0, o_WT = 0, o_XT = 0, o_VTlo = 0, o_KVlo = 0, o_Xs = 0;
   long long wt_floats = 0;
   // fused small-model path
   bool fused = false;
@@ -464,6 +464,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     p.o_VTlo = take(H2 * 2 * (size_t)(p.L - p.K) * d * p.vt_ld);  // V^T fp16 hi, then lo
     p.o_KVlo = take(H2 * 2 * p.S_tot * (p.L - p.K) * d);           // K fp16 hi, then lo
     p.o_XT = take(Fl * (size_t)d * p.vt_ld);
+    p.o_Xs = take(H2 * 2 * p.S_tot * d);  // X as fp16 hi, then lo (the K/V GEMM's A)
     p.o_WT = take(H2 * (size_t)p.wt_floats * 2);  // K-major weights: fp16 hi, then lo
   }
   p.total = o;
@@ -853,6 +854,7 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
   const int *in_off = at<int>(ws, p.o_in_off), *ctx_off_d = at<int>(ws, p.o_ctx_off);
   const int *ctx_len_d = at<int>(ws, p.o_ctx_len);
   const float *X = at<float>(ws, p.o_X);
+  bool x_split = false;  // X also as fp16 hi / lo at o_Xs
   if (!features) {
     GR_TRY(pad_rows(context, in_off, ctx_off_d, ctx_len_d, B, d, at<float>(ws, p.o_X), st));
   } else {
@@ -862,7 +864,21 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
     float *Xw = at<float>(ws, p.o_X);
     GemmArgs g = plain_gemm(features, p.F, w->ctx_W, d, Xw, d, (int)p.S_tot, d, p.F);
     g.bias = w->ctx_b;
-    GR_TRY(dense(p, g, wt ? wt->ctx : nullptr, p.S_tot, EPI_BIAS, st));
+    if (p.tc && p.F % 8 == 0 && d % 8 == 0 && tc_eligible(g.lda, g.K, g.K, g.A, wt->ctx)) {
+      // X in fp32 (trunk) and as fp16 hi / lo: the K/V GEMM's A, TMA-only
+      TcArgs t{};
+      static_cast<GemmArgs &>(t) = g;
+      t.b_hi = wt->ctx;
+      t.b_lo = wt->ctx + p.wt_floats;
+      t.ldb = g.K;
+      t.alpha = g.alpha / kWeightScale;
+      t.c_hi = at<__half>(ws, p.o_Xs);
+      t.c_lo = t.c_hi + (size_t)p.S_tot * d;
+      GR_TRY(gemm_tc(t, p.S_tot, g.K, g.N, g.K, EPI_BIAS_DUAL, st));
+      x_split = true;
+    } else {
+      GR_TRY(dense(p, g, wt ? wt->ctx : nullptr, p.S_tot, EPI_BIAS, st));
+    }
   }
   // encoder K/V of the head layers, once per request and shared by every beam
   // (beam.py:98-109); on the tensor-core path the epilogue also writes V^T
@@ -888,6 +904,10 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
       t.kv_scale = kKvScale;
       t.kv_d = d;
       t.range_flag = at<int>(ws, p.o_flag);
+      if (x_split) {
+        t.a_hi = at<__half>(ws, p.o_Xs);
+        t.a_lo = t.a_hi + (size_t)p.S_tot * d;
+      }
       GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * nh * d, d, EPI_KV_SPLIT, st));
       if (K > 0) GR_TRY(transpose(X, d, at<float>(ws, p.o_XT), p.vt_ld, (int)p.S_tot, d, st));
     } else {

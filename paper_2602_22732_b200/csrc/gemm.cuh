@@ -31,7 +31,8 @@ enum GemmEpi {
   EPI_STORE_SPLIT = 9,
   EPI_BIAS_GELU_SPLIT = 10,
   EPI_STORE_T_SPLIT = 11,
-  EPI_BIAS_RESID_DUAL = 12  // EPI_BIAS_RESID, and the result also as fp16 hi / lo
+  EPI_BIAS_RESID_DUAL = 12,  // EPI_BIAS_RESID, and the result also as fp16 hi / lo
+  EPI_BIAS_DUAL = 13         // EPI_BIAS, and the result also as fp16 hi / lo
 };
 
 struct GemmArgs {

@@ -79,6 +79,60 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t cluster_addr(const void *p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+// arrive on an mbarrier of another CTA of the cluster (shared::cluster address)
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cbar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
+}
+
+// CTA-pair load: lands in this CTA's shared memory, completes on the pair
+// leader's mbarrier (shared::cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *map, uint32_t cbar,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(cbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+// commit to the mbarrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
                                             int c0, int c1) {
   asm volatile(
@@ -157,8 +211,10 @@ struct TileInfo {
 };
 
 // tile -> (group, m-tile, n-tile); identical in every warp role
+// (bm: tile rows -- 2 BM for a CTA pair, whose CTA `moff / BM` owns rows
+// [m0 + moff, m0 + moff + BM) of the pair's tile)
 __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, int tile, int tiles_m, int tiles_n,
-                                              int bn) {
+                                              int bn, int bm = BM, int moff = 0) {
   TileInfo ti;
   const int per_g = tiles_m * tiles_n;
   const int g = tile / per_g, r = tile - g * per_g;
@@ -191,9 +247,9 @@ __device__ __forceinline__ TileInfo tile_info(const TcArgs &a, int tile, int til
       }
     }
   }
-  ti.m0 = tm * BM;
+  ti.m0 = tm * bm + moff;
   ti.n0 = tn * bn;
-  ti.valid = ti.m0 < ti.M && ti.n0 < ti.N;
+  ti.valid = tm * bm < ti.M && ti.n0 < ti.N;
   return ti;
 }
 
@@ -225,7 +281,14 @@ __device__ __forceinline__ void convert_groups(unsigned char *tile, int rows, in
 // Persistent, warp-specialised: each CTA walks tiles blockIdx.x, +gridDim.x, ...
 // Two TMEM accumulators (2 x BN columns) let the epilogue of tile j overlap
 // the MMAs of tile j+1.  BSPLIT: B arrives as pre-split fp16 hi / lo.
-template <int BN, int STAGES, int EPI, bool BSPLIT, bool ASPLIT>
+// PAIR (both operands pre-split): a cluster of two CTAs on one TPC computes
+// 256 x BN tiles with tcgen05.mma.cta_group::2 issued by the leader; each CTA
+// loads its 128 rows of A and half of the B tile (BN / 2 rows), so per SM the
+// shared-memory operand traffic per flop drops by a third.  Stage-full
+// barriers live in the leader (both CTAs' TMA bytes complete there), stage-
+// free and accumulator-ready barriers are multicast commits to both CTAs,
+// and both CTAs' epilogues release the accumulator on the leader's barrier.
+template <int BN, int STAGES, int EPI, bool BSPLIT, bool ASPLIT, bool PAIR = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmAlo,
@@ -236,7 +299,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   constexpr int A32 = BM * BK * 4;   // fp32 landing tile split in place (hi / lo atoms),
                                      // or (ASPLIT) the fp16 hi tile then the lo tile
   constexpr int A16 = BM * BK * 2;
-  constexpr int B16 = BN * BK * 2;   // pre-split B: fp16 hi tile, then lo tile
+  static_assert(!PAIR || (BSPLIT && ASPLIT), "CTA pairs take pre-split operands");
+  constexpr int BNL = PAIR ? BN / 2 : BN;  // B rows loaded by this CTA
+  constexpr int B16 = BNL * BK * 2;  // pre-split B: fp16 hi tile, then lo tile
   constexpr int B32 = BN * BK * 4;   // fp32 B landing tile, split in place
   // stage: [A][B]; A (and an fp32 B) hold interleaved 512-B hi / lo atoms
   constexpr int STAGE_BYTES = A32 + (BSPLIT ? 2 * B16 : B32);
@@ -256,32 +321,56 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int j = 0; j < 2; ++j) {
       mbar_init(&accf[j], 1);
-      mbar_init(&acce[j], 4);
+      mbar_init(&acce[j], PAIR ? 8 : 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(2 * BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // the leader's barriers exist before any peer traffic
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int tstep = PAIR ? gridDim.x / 2 : gridDim.x;  // tiles are per pair
+  const int tfirst = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int moff = (int)rank * BM;
+  constexpr int TBM = PAIR ? 2 * BM : BM;
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
       int kg = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN);
+      for (int tile = tfirst; tile < n_tiles; tile += tstep) {
+        const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN, TBM, moff);
         if (!ti.valid) continue;
         const int nk = (ti.K + BK - 1) / BK;
         for (int kt = 0; kt < nk; ++kt, ++kg) {
           const int s = kg % STAGES;
           if (kg >= STAGES) mbar_wait(&empty[s], ((kg / STAGES) - 1) & 1);
           unsigned char *st = smem + s * STAGE_BYTES;
+          if constexpr (PAIR) {
+            const uint32_t fb = cluster_addr(&full[s], 0);
+            if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);  // both CTAs' bytes
+            const int ak = ti.a_k + kt * BK, bk = ti.b_k + kt * BK;
+            tma_load_2d_pair(st, &tmA, fb, ak, ti.a_row + ti.m0);
+            tma_load_2d_pair(st + A16, &tmAlo, fb, ak, ti.a_row + ti.m0);
+            tma_load_2d_pair(st + A32, &tmB, fb, bk, ti.b_row + ti.n0 + (int)rank * BNL);
+            tma_load_2d_pair(st + A32 + B16, &tmBlo, fb, bk, ti.b_row + ti.n0 + (int)rank * BNL);
+            continue;
+          }
           mbar_expect_tx(&full[s], A32 + (BSPLIT ? 2 * B16 : B32));
           tma_load_2d(st, &tmA, &full[s], ti.a_k + kt * BK, ti.a_row + ti.m0);
           if (ASPLIT) tma_load_2d(st + A16, &tmAlo, &full[s], ti.a_k + kt * BK, ti.a_row + ti.m0);
@@ -296,13 +385,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
+    if (lane == 0 && leader) {  // ---- MMA issuer (the pair's leader)
       // kind::f16: D f32 (bit 4), A / B fp16 (format 0), both K-major, N >> 3, M >> 4
       constexpr uint32_t idesc =
-          (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+          (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TBM >> 4) << 24);
       int kg = 0, j = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN);
+      for (int tile = tfirst; tile < n_tiles; tile += tstep) {
+        const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN, TBM, moff);
         if (!ti.valid) continue;
         const int acc = j & 1;
         if (j >= 2) mbar_wait(&acce[acc], ((j >> 1) - 1) & 1);
@@ -311,7 +400,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int nk = (ti.K + BK - 1) / BK;
         for (int kt = 0; kt < nk; ++kt, ++kg) {
           const int s = kg % STAGES;
-          mbar_wait(&conv[s], (kg / STAGES) & 1);
+          mbar_wait(PAIR ? &full[s] : &conv[s], (kg / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
           // in-place split: interleaved hi / lo atoms 1024 B apart; ASPLIT: two tiles
@@ -323,13 +412,25 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           for (int k = 0; k < BK / 16; ++k) {
             const uint32_t off = k * 32;  // 16 fp16 = 32 B along the swizzled row
             const uint32_t acc0 = (kt > 0 || k > 0) ? 1u : 0u;
-            mma_f16(d_tmem, sw64_desc(a_lo + off, a_sbo), sw64_desc(b_hi + off, b_sbo), idesc, acc0);
-            mma_f16(d_tmem, sw64_desc(a_hi + off, a_sbo), sw64_desc(b_lo + off, b_sbo), idesc, 1u);
-            mma_f16(d_tmem, sw64_desc(a_hi + off, a_sbo), sw64_desc(b_hi + off, b_sbo), idesc, 1u);
+            if constexpr (PAIR) {
+              mma_f16_pair(d_tmem, sw64_desc(a_lo + off, a_sbo), sw64_desc(b_hi + off, b_sbo), idesc, acc0);
+              mma_f16_pair(d_tmem, sw64_desc(a_hi + off, a_sbo), sw64_desc(b_lo + off, b_sbo), idesc, 1u);
+              mma_f16_pair(d_tmem, sw64_desc(a_hi + off, a_sbo), sw64_desc(b_hi + off, b_sbo), idesc, 1u);
+            } else {
+              mma_f16(d_tmem, sw64_desc(a_lo + off, a_sbo), sw64_desc(b_hi + off, b_sbo), idesc, acc0);
+              mma_f16(d_tmem, sw64_desc(a_hi + off, a_sbo), sw64_desc(b_lo + off, b_sbo), idesc, 1u);
+              mma_f16(d_tmem, sw64_desc(a_hi + off, a_sbo), sw64_desc(b_hi + off, b_sbo), idesc, 1u);
+            }
           }
-          mma_commit(&empty[s]);  // frees the stage when these MMAs complete
+          if (PAIR)
+            mma_commit_pair(&empty[s]);  // frees the stage in both CTAs
+          else
+            mma_commit(&empty[s]);  // frees the stage when these MMAs complete
         }
-        mma_commit(&accf[acc]);
+        if (PAIR)
+          mma_commit_pair(&accf[acc]);
+        else
+          mma_commit(&accf[acc]);
         ++j;
       }
     }
@@ -337,7 +438,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // ---- converters: landed fp32 tiles -> fp16 hi / lo operand tiles
     const int cw = warp - 2;  // converter warp index
     int kg = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (int tile = blockIdx.x; !PAIR && tile < n_tiles; tile += gridDim.x) {
       const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN);
       if (!ti.valid) continue;
       const int nk = (ti.K + BK - 1) / BK;
@@ -361,8 +462,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     float *ebuf = reinterpret_cast<float *>(smem + STAGES * STAGE_BYTES + 256) +
                   (warp - kEpiWarp0) * 32 * 33;
     int j = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN);
+    for (int tile = tfirst; tile < n_tiles; tile += tstep) {
+      const TileInfo ti = tile_info(a, tile, tiles_m, tiles_n, BN, TBM, moff);
       if (!ti.valid) continue;
       const int acc = j & 1;
       mbar_wait(&accf[acc], (j >> 1) & 1);
@@ -477,7 +578,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                          (EPI != EPI_KV_SPLIT || (a.k_ld % 4) == 0);
         float4 bcol = make_float4(0.f, 0.f, 0.f, 0.f);
         if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID ||
-            EPI == EPI_BIAS_GELU_SPLIT || EPI == EPI_BIAS_RESID_DUAL) {
+            EPI == EPI_BIAS_GELU_SPLIT || EPI == EPI_BIAS_RESID_DUAL || EPI == EPI_BIAS_DUAL) {
           bcol.x = col < N ? a.bias[col] : 0.f;
           bcol.y = col + 1 < N ? a.bias[col + 1] : 0.f;
           bcol.z = col + 2 < N ? a.bias[col + 2] : 0.f;
@@ -520,7 +621,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const float oo[4] = {xo[it].x, xo[it].y, xo[it].z, xo[it].w};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            if (EPI == EPI_BIAS) x[q] = x[q] + ob[q];
+            if (EPI == EPI_BIAS || EPI == EPI_BIAS_DUAL) x[q] = x[q] + ob[q];
             else if (EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_GELU_SPLIT)
               x[q] = gelu_tanh_fast(x[q] + ob[q]);
             else if (EPI == EPI_RESID) x[q] = oo[q] + x[q];
@@ -553,7 +654,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
             continue;
           }
-          if (EPI == EPI_STORE_SPLIT || EPI == EPI_BIAS_GELU_SPLIT || EPI == EPI_BIAS_RESID_DUAL) {
+          if (EPI == EPI_STORE_SPLIT || EPI == EPI_BIAS_GELU_SPLIT || EPI == EPI_BIAS_RESID_DUAL ||
+              EPI == EPI_BIAS_DUAL) {
             __half hq[4], lq[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -570,7 +672,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 a.c_lo[o + q] = lq[q];
               }
             }
-            if (EPI != EPI_BIAS_RESID_DUAL) continue;
+            if (EPI != EPI_BIAS_RESID_DUAL && EPI != EPI_BIAS_DUAL) continue;
           }
           float *dst = a.C + grow * a.ldc + col;
           if (vec) {
@@ -583,15 +685,24 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acce[acc]);
+      if (lane == 0) {
+        if (PAIR)
+          mbar_arrive_remote(cluster_addr(&acce[acc], 0));  // the leader's MMA waits on it
+        else
+          mbar_arrive(&acce[acc]);
+      }
       ++j;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // no CTA leaves while its peer's traffic targets it
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
@@ -674,6 +785,7 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
       GR_TC_EPI(EPI_STORE_SPLIT)
       GR_TC_EPI(EPI_BIAS_RESID_DUAL)
       GR_TC_EPI(EPI_STORE_LSE)
+      GR_TC_EPI(EPI_KV_SPLIT)
       default: return set_err(GR4AD_ERR_UNSUPPORTED, "pre-split-A tc epilogue %d", epi);
     }
   } else {
@@ -687,10 +799,64 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
     GR_TC_EPI(EPI_KV_SPLIT)
     GR_TC_EPI(EPI_STORE_LSE)
     GR_TC_EPI(EPI_STORE_SPLIT)
+    GR_TC_EPI(EPI_BIAS_DUAL)
     default: return set_err(GR4AD_ERR_UNSUPPORTED, "tc epilogue %d", epi);
   }
   }
 #undef GR_TC_EPI
+}
+
+// CTA-pair launch (PAIR instantiation): 256 x BN tiles, clusters of two
+template <int BN, int STAGES>
+static int launch_tc_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl,
+                          const CUtensorMap &mal, const TcArgs &a, int epi, cudaStream_t st) {
+  constexpr size_t stage = (size_t)BM * BK * 4 + (size_t)BN * BK * 2;  // A hi + lo, half B hi + lo
+  constexpr size_t smem = 1024 + STAGES * stage + 256 + 4 * 32 * 33 * sizeof(float);
+  static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
+  const int tiles_m = (a.M + 2 * BM - 1) / (2 * BM), tiles_n = (a.N + BN - 1) / BN;
+  const int n_tiles = tiles_m * tiles_n;
+  const int grid = 2 * std::min(n_tiles, num_sms() / 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#define GR_TC_PAIR(E)                                                                            \
+  case E: {                                                                                      \
+    auto *k = gemm_tc_kernel<BN, STAGES, E, true, true, true>;                                   \
+    GR_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
+    GR_LAUNCH(KC_GEMM, st, GR_CUDA(cudaLaunchKernelEx(&cfg, k, ma, mb, mbl, mal, a, tiles_m,       \
+                                                      tiles_n, n_tiles)));                       \
+    return GR4AD_OK;                                                                             \
+  }
+  switch (epi) {
+    GR_TC_PAIR(EPI_STORE)
+    GR_TC_PAIR(EPI_RESID)
+    GR_TC_PAIR(EPI_BIAS_RESID)
+    GR_TC_PAIR(EPI_BIAS_GELU_SPLIT)
+    GR_TC_PAIR(EPI_STORE_SPLIT)
+    GR_TC_PAIR(EPI_BIAS_RESID_DUAL)
+    GR_TC_PAIR(EPI_STORE_LSE)
+    GR_TC_PAIR(EPI_KV_SPLIT)
+    default: return set_err(GR4AD_ERR_UNSUPPORTED, "pre-split-A tc epilogue %d", epi);
+  }
+#undef GR_TC_PAIR
+}
+
+// GR4AD_TC_PAIR=0 keeps the single-CTA kernel for every product (A/B aid)
+static bool pair_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("GR4AD_TC_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 bool tc_eligible(long long lda, long long ldb, int K, const void *A, const void *B) {
@@ -718,6 +884,11 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
     CUtensorMap mal;
     GR_TRY(make_map(&ma, a.a_hi, true, a_rows, a_cols, a.lda, BM));
     GR_TRY(make_map(&mal, a.a_lo, true, a_rows, a_cols, a.lda, BM));
+    if (wide && a.mode == GM_PLAIN && !a.g_rows && a.groups == 1 && pair_enabled()) {
+      GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, 128));
+      GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, 128));
+      return launch_tc_pair<256, 6>(ma, mb, mbl, mal, a, epi, st);
+    }
     GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, box_n));
     GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, box_n));
     return wide ? launch_tc<256, 4, true, true>(ma, mb, mbl, mal, a, epi, st)
