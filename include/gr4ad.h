@@ -216,10 +216,18 @@ int gr4ad_score_workspace_bytes(const gr4ad_dims *dims, const gr4ad_batch *batch
 
 /* C = A . BT^T in fp32 (A: (M, K), BT: (N, K), row-major with the given
  * leading dimensions) -- the GEMM the decode uses internally, exposed for
- * numerics tests.  backend 0: CUDA-core fp32; 1: tcgen05 3xTF32 (fp32
+ * numerics tests.  backend 0: CUDA-core fp32; 1: tcgen05 3xFP16 (fp32
  * accumulation in TMEM; needs 16-B aligned rows). */
 int gr4ad_gemm(const float *A, long long lda, const float *BT, long long ldb, float *C,
                long long ldc, int M, int N, int K, int backend, void *stream);
+
+/* C = alpha (a_hi + a_lo) . (b_hi + b_lo)^T with both operands already split
+ * into fp16 hi / lo (K-major rows, lda / ldb and K multiples of 8) -- the
+ * TMA-only tcgen05 path the decode's head-layer and encoder K/V products take
+ * (CTA pairs, 256 x 256 tiles, when N >= 256), exposed for numerics tests. */
+int gr4ad_gemm_presplit(const void *a_hi, const void *a_lo, long long lda, const void *b_hi,
+                        const void *b_lo, long long ldb, float *C, long long ldc, int M, int N,
+                        int K, float alpha, void *stream);
 
 /* Batched pre-cut selection (beam.py:50-89 topk_precut/_precut_arrays and
  * beam.py:37-47 topk_global -- identical results): for problem p,

@@ -32,6 +32,7 @@ EXPORTS = (
     "gr4ad_topk_precut", "gr4ad_topk_workspace_bytes", "gr4ad_project_topk",
     "gr4ad_project_topk_workspace_bytes", "gr4ad_gemm", "gr4ad_score_sequences",
     "gr4ad_score_workspace_bytes", "gr4ad_range_status", "gr4ad_prepare_weights",
+    "gr4ad_gemm_presplit",
 )
 
 _P = C.c_void_p
@@ -108,6 +109,8 @@ def _load():
     lib.gr4ad_project_topk_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
     lib.gr4ad_gemm.argtypes = [_P, C.c_longlong, _P, C.c_longlong, _P, C.c_longlong, C.c_int,
                                C.c_int, C.c_int, C.c_int, _P]
+    lib.gr4ad_gemm_presplit.argtypes = [_P, _P, C.c_longlong, _P, _P, C.c_longlong, _P,
+                                        C.c_longlong, C.c_int, C.c_int, C.c_int, C.c_float, _P]
     lib.gr4ad_score_sequences.argtypes = [C.POINTER(Dims), C.POINTER(Weights), C.POINTER(Batch),
                                           _P, _P, C.c_int, C.POINTER(C.c_int), _P, _P, _P, _P,
                                           _P, C.c_size_t, _P]

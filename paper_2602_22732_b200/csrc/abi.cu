@@ -1485,6 +1485,22 @@ int gr4ad_gemm(const float *A, long long lda, const float *BT, long long ldb, fl
   return gemm(plain_gemm(A, lda, BT, ldb, C, ldc, M, N, K), true, EPI_STORE, st);
 }
 
+int gr4ad_gemm_presplit(const void *a_hi, const void *a_lo, long long lda, const void *b_hi,
+                        const void *b_lo, long long ldb, float *C, long long ldc, int M, int N,
+                        int K, float alpha, void *stream) {
+  if (M < 0 || N < 0 || K < 1) return set_err(GR4AD_ERR_VALUE, "bad gemm shape");
+  if (lda % 8 || ldb % 8 || K % 8)
+    return set_err(GR4AD_ERR_UNSUPPORTED, "pre-split gemm needs 16-B aligned fp16 rows");
+  TcArgs t{};
+  static_cast<GemmArgs &>(t) = plain_gemm(nullptr, lda, nullptr, ldb, C, ldc, M, N, K);
+  t.alpha = alpha;
+  t.a_hi = static_cast<const __half *>(a_hi);
+  t.a_lo = static_cast<const __half *>(a_lo);
+  t.b_hi = static_cast<const __half *>(b_hi);
+  t.b_lo = static_cast<const __half *>(b_lo);
+  return gemm_tc(t, M, K, N, K, EPI_STORE, (cudaStream_t)stream);
+}
+
 size_t gr4ad_topk_workspace_bytes(int n_problems, int b, int v) { return 256; }
 
 int gr4ad_topk_precut(const float *prev_scores, const float *logprobs, int n_problems, int b,
