@@ -814,8 +814,9 @@ static int launch_tc_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CU
   constexpr size_t smem = 1024 + STAGES * stage + 256 + 4 * 32 * 33 * sizeof(float);
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
   const int tiles_m = (a.M + 2 * BM - 1) / (2 * BM), tiles_n = (a.N + BN - 1) / BN;
-  const int n_tiles = tiles_m * tiles_n;
+  const int n_tiles = tiles_m * tiles_n * a.groups;  // (per-request groups: GM_QK / GM_PV)
   const int grid = 2 * std::min(n_tiles, num_sms() / 2);
+  const int cls = (a.mode == GM_PLAIN) ? KC_GEMM : KC_ATTN_GEMM;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kTcThreads);
@@ -832,7 +833,7 @@ static int launch_tc_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CU
   case E: {                                                                                      \
     auto *k = gemm_tc_kernel<BN, STAGES, E, true, true, true>;                                   \
     GR_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
-    GR_LAUNCH(KC_GEMM, st, GR_CUDA(cudaLaunchKernelEx(&cfg, k, ma, mb, mbl, mal, a, tiles_m,       \
+    GR_LAUNCH(cls, st, GR_CUDA(cudaLaunchKernelEx(&cfg, k, ma, mb, mbl, mal, a, tiles_m,           \
                                                       tiles_n, n_tiles)));                       \
     return GR4AD_OK;                                                                             \
   }
@@ -870,9 +871,9 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
   static const bool trace = getenv("GR4AD_TRACE") != nullptr;  // debug aid (read-only)
   if (trace)
     fprintf(stderr, "gemm_tc M=%d N=%d K=%d groups=%d mode=%d epi=%d lda=%lld ldb=%lld ldc=%lld "
-                    "A=(%lld,%lld) B=(%lld,%lld) presplit=%d\n",
+                    "A=(%lld,%lld) B=(%lld,%lld) presplit=%d asplit=%d\n",
             a.M, a.N, a.K, a.groups, a.mode, epi, a.lda, a.ldb, a.ldc, a_rows, a_cols, b_rows,
-            b_cols, a.b_hi != nullptr);
+            b_cols, a.b_hi != nullptr, a.a_hi != nullptr);
   if (epi == EPI_KV_SPLIT && (!a.k_hi || !a.vt_hi))
     return set_err(GR4AD_ERR_UNSUPPORTED, "K|V^T split epilogue needs its fp16 outputs");
   const bool wide = a.N >= 256;
@@ -884,7 +885,7 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
     CUtensorMap mal;
     GR_TRY(make_map(&ma, a.a_hi, true, a_rows, a_cols, a.lda, BM));
     GR_TRY(make_map(&mal, a.a_lo, true, a_rows, a_cols, a.lda, BM));
-    if (wide && a.mode == GM_PLAIN && !a.g_rows && a.groups == 1 && pair_enabled()) {
+    if (wide && (a.mode == GM_PLAIN || a.mode == GM_QK || a.mode == GM_PV) && pair_enabled()) {
       GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, 128));
       GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, 128));
       return launch_tc_pair<256, 6>(ma, mb, mbl, mal, a, epi, st);
