@@ -83,7 +83,7 @@ struct Plan {
   // tensor-core layered path
   bool tc = false;
   long long sc_ld = 0, vt_ld = 0;
-  size_t o_VT = 0, o_WT = 0, o_XT = 0, o_VTlo = 0, o_KVlo = 0, o_Xs = 0;
+  size_t o_VT = 0, o_WT = 0, o_XT = 0, o_VTlo = 0, o_KVlo = 0, o_Xs = 0, o_U16 = 0;
   long long wt_floats = 0;
   // fused small-model path
   bool fused = false;
@@ -465,6 +465,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     p.o_KVlo = take(H2 * 2 * p.S_tot * (p.L - p.K) * d);           // K fp16 hi, then lo
     p.o_XT = take(Fl * (size_t)d * p.vt_ld);
     p.o_Xs = take(H2 * 2 * p.S_tot * d);  // X as fp16 hi, then lo (the K/V GEMM's A)
+    p.o_U16 = take(H2 * 2 * p.Rw * 2 * d);  // the fuse input [g | s] as fp16 hi, then lo
     p.o_WT = take(H2 * (size_t)p.wt_floats * 2);  // K-major weights: fp16 hi, then lo
   }
   p.total = o;
@@ -1038,7 +1039,20 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     const long long h0 = p.hist_off[t];
     // token input + gated fusion (beam.py:180-191; layers.py:129-133)
     const float *emb_prev = t > 0 ? w->emb[t - 1] : nullptr;
-    if (K > 0) {
+    if (K > 0 && p.tc && wt && d % 8 == 0) {
+      // the fuse on pre-split operands: s (and the gate product g) as fp16
+      // hi / lo, so both GEMMs run TMA-only (CTA pairs)
+      __half *Uh = at<__half>(ws, p.o_U16), *Ul = Uh + (size_t)p.Rw * 2 * d;
+      GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, nullptr, nullptr, nullptr, st, Uh,
+                         Ul));
+      GemmArgs gg = plain_gemm(nullptr, 2LL * d, w->fuse_Wg, d, nullptr, 2LL * d, R, d, d);
+      gg.vec = Ht + (size_t)t * d;
+      gg.vec_ld = (long long)p.n_pos * d;
+      gg.row_req = row_req + h0;
+      GR_TRY(dense_split(p, gg, wt->wg, Uh + d, Ul + d, R, EPI_MULVEC_SPLIT, st, Uh, Ul));
+      GR_TRY(dense_split(p, plain_gemm(nullptr, 2LL * d, w->fuse_Wf, d, Hs, d, R, d, 2 * d), wt->wf,
+                         Uh, Ul, R, EPI_STORE, st));
+    } else if (K > 0) {
       GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, nullptr, U, nullptr, st));
       GemmArgs gg = plain_gemm(U + d, 2LL * d, w->fuse_Wg, d, U, 2LL * d, R, d, d);
       gg.vec = Ht + (size_t)t * d;

@@ -32,7 +32,8 @@ enum GemmEpi {
   EPI_BIAS_GELU_SPLIT = 10,
   EPI_STORE_T_SPLIT = 11,
   EPI_BIAS_RESID_DUAL = 12,  // EPI_BIAS_RESID, and the result also as fp16 hi / lo
-  EPI_BIAS_DUAL = 13         // EPI_BIAS, and the result also as fp16 hi / lo
+  EPI_BIAS_DUAL = 13,        // EPI_BIAS, and the result also as fp16 hi / lo
+  EPI_MULVEC_SPLIT = 14      // EPI_MULVEC, the result only as fp16 hi / lo
 };
 
 struct GemmArgs {

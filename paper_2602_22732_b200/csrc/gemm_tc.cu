@@ -574,7 +574,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const bool vec = col + 4 <= N && (a.ldc % 4) == 0 &&
                          (EPI != EPI_RESID && EPI != EPI_BIAS_RESID && EPI != EPI_BIAS_RESID_DUAL ||
          (a.ldr % 4) == 0) &&
-                         (EPI != EPI_MULVEC || (a.vec_ld % 4) == 0) &&
+                         (EPI != EPI_MULVEC && EPI != EPI_MULVEC_SPLIT || (a.vec_ld % 4) == 0) &&
                          (EPI != EPI_KV_SPLIT || (a.k_ld % 4) == 0);
         float4 bcol = make_float4(0.f, 0.f, 0.f, 0.f);
         if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID ||
@@ -595,7 +595,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const float *src = nullptr;
             if (EPI == EPI_RESID || EPI == EPI_BIAS_RESID || EPI == EPI_BIAS_RESID_DUAL)
               src = a.R + grow * a.ldr + col;
-            else if (EPI == EPI_MULVEC) src = a.vec + (long long)a.row_req[grow] * a.vec_ld + col;
+            else if (EPI == EPI_MULVEC || EPI == EPI_MULVEC_SPLIT)
+              src = a.vec + (long long)a.row_req[grow] * a.vec_ld + col;
             if (src) {
               if (vec) {
                 o = *reinterpret_cast<const float4 *>(src);
@@ -627,7 +628,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             else if (EPI == EPI_RESID) x[q] = oo[q] + x[q];
             else if (EPI == EPI_BIAS_RESID || EPI == EPI_BIAS_RESID_DUAL)
               x[q] = oo[q] + (x[q] + ob[q]);
-            else if (EPI == EPI_MULVEC) x[q] = oo[q] * x[q];
+            else if (EPI == EPI_MULVEC || EPI == EPI_MULVEC_SPLIT) x[q] = oo[q] * x[q];
           }
           if (EPI == EPI_KV_SPLIT) {
             // K part of the layer (columns never straddle K / V for d % 4 == 0)
@@ -655,7 +656,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             continue;
           }
           if (EPI == EPI_STORE_SPLIT || EPI == EPI_BIAS_GELU_SPLIT || EPI == EPI_BIAS_RESID_DUAL ||
-              EPI == EPI_BIAS_DUAL) {
+              EPI == EPI_BIAS_DUAL || EPI == EPI_MULVEC_SPLIT) {
             __half hq[4], lq[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -786,6 +787,7 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
       GR_TC_EPI(EPI_BIAS_RESID_DUAL)
       GR_TC_EPI(EPI_STORE_LSE)
       GR_TC_EPI(EPI_KV_SPLIT)
+      GR_TC_EPI(EPI_MULVEC_SPLIT)
       default: return set_err(GR4AD_ERR_UNSUPPORTED, "pre-split-A tc epilogue %d", epi);
     }
   } else {
@@ -846,6 +848,7 @@ static int launch_tc_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CU
     GR_TC_PAIR(EPI_BIAS_RESID_DUAL)
     GR_TC_PAIR(EPI_STORE_LSE)
     GR_TC_PAIR(EPI_KV_SPLIT)
+    GR_TC_PAIR(EPI_MULVEC_SPLIT)
     default: return set_err(GR4AD_ERR_UNSUPPORTED, "pre-split-A tc epilogue %d", epi);
   }
 #undef GR_TC_PAIR

@@ -424,22 +424,28 @@ int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_st
 __global__ void level_input_kernel(int t, int rows, int d, const float *__restrict__ bos,
                                    const float *__restrict__ emb_prev,
                                    const int *__restrict__ tok,
-                                   const float *__restrict__ pos_t, float *U, float *H) {
+                                   const float *__restrict__ pos_t, float *U, float *H,
+                                   __half *Uh, __half *Ul) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)rows * d) return;
   int r = (int)(i / d), j = (int)(i - (long long)r * d);
   float s = (t == 0) ? bos[j] : emb_prev[(long long)tok[r] * d + j];
   if (U) U[(long long)r * 2 * d + d + j] = s;
+  if (Uh) {  // the fuse GEMMs' pre-split A (same split as on chip)
+    const __half h = __float2half_rn(s);
+    Uh[(long long)r * 2 * d + d + j] = h;
+    Ul[(long long)r * 2 * d + d + j] = __float2half_rn(s - __half2float(h));
+  }
   if (H) H[(long long)r * d + j] = s + pos_t[j];
 }
 
 int level_input(int t, int rows, int d, const float *bos, const float *emb_prev,
                 const int *tok, const float *pos_t, float *U, float *H,
-                cudaStream_t st) {
+                cudaStream_t st, __half *Uh, __half *Ul) {
   long long n = (long long)rows * d;
   if (n <= 0) return GR4AD_OK;
   GR_LAUNCH(KC_SMALL, st, level_input_kernel<<<ceil_div(n, 256), 256, 0, st>>>(t, rows, d, bos, emb_prev, tok,
-                                                       pos_t, U, H));
+                                                       pos_t, U, H, Uh, Ul));
   return GR4AD_OK;
 }
 

@@ -33,7 +33,7 @@ int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_st
 // s into U[:, d:2d]; K==0 writes H = s + pos[t].
 int level_input(int t, int rows, int d, const float *bos, const float *emb_prev,
                 const int *tok, const float *pos_t, float *U, float *H,
-                cudaStream_t st);
+                cudaStream_t st, __half *Uh = nullptr, __half *Ul = nullptr);
 
 // per-row (max, log sum exp(x - max)) (beam.py:92-95)
 int lse_merge(const float4 *part, int n_part, int rows, float2 *info, cudaStream_t st);
