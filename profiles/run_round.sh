@@ -20,6 +20,8 @@ timeout -s KILL 300 ncu --metrics $M --clock-control none -c 400 --csv \
   --log-file $O/launches_c2.csv $B > /dev/null 2>&1
 timeout -s KILL 900 ncu --metrics $M --clock-control none -c 1200 --csv \
   --log-file $O/launches_c3.csv $B --config c3 > /dev/null 2>&1
+timeout -s KILL 900 ncu --metrics $M --clock-control none -c 1200 --csv \
+  --log-file $O/launches_c5.csv $B --config c5 > /dev/null 2>&1
 timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k regex:fused_mma \
   -s 1 -c 1 -o $O/prof_fused_c2 $B > /dev/null 2>&1
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc \
@@ -30,4 +32,5 @@ if [ -f profiles/libgr4ad_timing.so ]; then
   GR4AD_LIB=profiles/libgr4ad_timing.so timeout 300 python profiles/fused_phases.py --batch 296 \
     > $O/fused_phases_c2.txt 2>&1
 fi
+timeout 120 python profiles/h2d_probe.py > $O/h2d.txt 2>&1
 ls -la $O
