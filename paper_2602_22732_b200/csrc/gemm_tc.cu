@@ -480,22 +480,30 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int col0 = ti.n0 + c * 32;
         if (nrows <= 0 || col0 >= N) continue;  // warp-uniform
         if (EPI == EPI_STORE_LSE) {  // online (max, sum exp) over the row-per-lane registers
-          float cm = -INFINITY;
+          // four independent accumulators (no 32-long dependency chains);
+          // exp as ex2.approx of a pre-scaled argument (rel. error ~2^-22)
+          constexpr float kL2e = 1.4426950408889634f;
+          float x[32];
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj)
-            if (col0 + jj < N) {
-              const float x = v[jj] * a.alpha;
-              cm = fmaxf(cm, x);
-              pt2 = fmaxf(pt2, fminf(pt1, x));
-              pt1 = fmaxf(pt1, x);
-            }
-          const float nm = fmaxf(pm, cm);
-          float cs = 0.f;
+          for (int jj = 0; jj < 32; ++jj) x[jj] = col0 + jj < N ? v[jj] * a.alpha : -INFINITY;
+          float m4[4] = {x[0], x[1], x[2], x[3]};
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj)
-            if (col0 + jj < N) cs += expf(v[jj] * a.alpha - nm);
-          ps = (pm == -INFINITY ? 0.f : ps * expf(pm - nm)) + cs;
+          for (int jj = 4; jj < 32; ++jj) m4[jj & 3] = fmaxf(m4[jj & 3], x[jj]);
+          const float cm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+          const float nm = fmaxf(pm, cm);  // finite: col0 < N
+          const float nl = nm * kL2e;
+          float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) s4[jj & 3] += exp2f(fmaf(x[jj], kL2e, -nl));
+          const float cs = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+          ps = (pm == -INFINITY ? 0.f : ps * exp2f((pm - nm) * kL2e)) + cs;
           pm = nm;
+          // window proxies: the maxima of the part's two 64-column halves
+          // (each a real candidate value, as the selection requires)
+          if ((c & 3) < 2)
+            pt1 = fmaxf(pt1, cm);
+          else
+            pt2 = fmaxf(pt2, cm);
           if ((c & 3) == 3 || col0 + 32 >= N) {
             if (lane < nrows)
               a.lse_part[((long long)ti.c_row + rbase + lane) * a.lse_ld + col0 / 128] =

@@ -28,8 +28,9 @@ struct TcArgs : GemmArgs {
   int kv_d;
   int *range_flag;  // EPI_KV_SPLIT: set when a scaled value leaves the fp16 range
   // EPI_STORE_LSE: lse_part[row * lse_ld + col / 128] = (max, sum exp(x - max),
-  // top-1, top-2) over the row's columns [128 j, 128 j + 128) (merged by
-  // lse_merge; top-1 / top-2 are the selection's window proxies)
+  // max of the first 64 columns, max of the last 64) over the row's columns
+  // [128 j, 128 j + 128) (merged by lse_merge; the half maxima are the
+  // selection's window proxies)
   float4 *lse_part;
   int lse_ld;
 };

@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
     auto sbin = [&](float s) -> unsigned { return (unsigned)fminf((Rs - s) * scale, 2047.0f); };
     // 16-B rows: float4 loads, four candidates per lane and load
     const bool vec4 = !CACHE && c.V % 4 == 0 && c.ld % 4 == 0;
-    // attempt 0: window bin from the logits GEMM epilogue's per-row top-2
+    // attempt 0: window bin from the logits GEMM epilogue's per-64-column maxima
     // proxies (every proxy is a real candidate with the identical score
     // expression, so the k-th best proxy's bin bounds the k-th best
     // candidate's): no histogram pass over the logits.  Attempt 1: the

@@ -55,8 +55,9 @@ struct SelectArgs {
   int V;
   int level;
   const float2 *rowinfo;  // per level row
-  // optional (no masking): per level row, proxy_ld (max, sum, top1, top2)
-  // partials of the logits GEMM epilogue; top1 / top2 are window proxies
+  // optional (no masking): per level row, proxy_ld (max, sum, p1, p2)
+  // partials of the logits GEMM epilogue; p1 / p2 (64-column maxima) are
+  // window proxies
   const float4 *proxies;
   int proxy_ld;
   const float *cum;       // per history row
