@@ -1636,17 +1636,20 @@ static __device__ __forceinline__ void logits_pass2(
         unsigned base = 0;
         if (lane == 31) base = atomicAdd(cnt, incl);
         base = __shfl_sync(kFull, base, 31) + incl - np;
+        // branch-free: every value's entry is formed, the store predicated
+        // (a per-entry branch costs two warp reconvergence points)
 #pragma unroll
         for (int j = 0; j < kLG; ++j)
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if ((pm >> (4 * j + c)) & 1u) {
-              const RowScore &R = c < 2 ? A : B;
-              const float sc = R.cr + ((z[j][c] - R.M) - R.ls);
-              if (base < (unsigned)cap)
-                sbuf[base] = ((unsigned long long)f2ord(sc) << 32) |
-                             (0xFFFFFFFFu - (unsigned)(R.r * V + (n0 + j) * 8 + 2 * t4 + (c & 1)));
-              ++base;
+          for (int c = 0; c < 4; ++c) {
+            const RowScore &R = c < 2 ? A : B;
+            const bool take = (pm >> (4 * j + c)) & 1u;
+            const float sc = R.cr + ((z[j][c] - R.M) - R.ls);
+            const unsigned long long e =
+                ((unsigned long long)f2ord(sc) << 32) |
+                (0xFFFFFFFFu - (unsigned)(R.r * V + (n0 + j) * 8 + 2 * t4 + (c & 1)));
+            if (take && base < (unsigned)cap) sbuf[base] = e;
+            base += take ? 1u : 0u;
             }
       }
     }
