@@ -873,13 +873,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs 
               if (lane == 31) base = atomicAdd(&s_gt_pos, incl);
               base = __shfl_sync(0xffffffffu, base, 31) + incl - np;
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                if ((pm >> q) & 1u) {
-                  const unsigned fi = (unsigned)((long long)r * c.V + 4 * v4 + q);
-                  if (base < (unsigned)GR4AD_MAX_BEAM)  // (proxy window: counted, checked below)
-                    sbuf[base] = ((unsigned long long)f2ord(sv[q]) << 32) | (0xFFFFFFFFu - fi);
-                  ++base;
-                }
+              for (int q = 0; q < 4; ++q) {  // branch-free: predicated stores
+                const bool take = (pm >> q) & 1u;
+                const unsigned fi = (unsigned)((long long)r * c.V + 4 * v4 + q);
+                const unsigned long long e =
+                    ((unsigned long long)f2ord(sv[q]) << 32) | (0xFFFFFFFFu - fi);
+                if (take && base < (unsigned)GR4AD_MAX_BEAM) sbuf[base] = e;  // (overflow: counted)
+                base += take ? 1u : 0u;
+              }
             }
           }
           continue;
