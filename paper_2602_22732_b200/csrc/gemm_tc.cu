@@ -45,7 +45,14 @@ constexpr int BM = 128;
 constexpr int BK = 32;           // k per stage: one 128-B fp32 row, two 16-deep MMA k-steps
 constexpr int kConvWarps = 4;    // warps 2 .. 2 + kConvWarps - 1
 constexpr int kEpiWarp0 = 2 + kConvWarps;
-constexpr int kTcThreads = 32 * (kEpiWarp0 + 4);
+// two epilogue warps per TMEM lane quarter: with BN = 256 they drain the
+// accumulator's column halves in parallel (one warp per SMSP was latency-bound
+// on the heavier epilogues)
+#ifndef GR_TC_EPI_WARPS
+#define GR_TC_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = GR_TC_EPI_WARPS;
+constexpr int kTcThreads = 32 * (kEpiWarp0 + kEpiWarps);
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -321,7 +328,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int j = 0; j < 2; ++j) {
       mbar_init(&accf[j], 1);
-      mbar_init(&acce[j], PAIR ? 8 : 4);
+      mbar_init(&acce[j], PAIR ? 2 * kEpiWarps : kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -473,8 +480,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int N = ti.N;
       // EPI_STORE_LSE: this lane's row, current 128 columns: max, sum, top-2
       float pm = -INFINITY, ps = 0.f, pt1 = -INFINITY, pt2 = -INFINITY;
+      // this warp's chunks: with two warps per lane quarter and BN = 256 each
+      // drains one 128-column half (whole log-sum-exp parts); narrower tiles
+      // leave the second warp idle
+      constexpr int NC = BN / 32;
+      constexpr bool halves = kEpiWarps == 8 && NC >= 8;
+      const int eh = (warp - kEpiWarp0) >> 2;
+      const int c_begin = halves ? eh * (NC / 2) : 0;
+      const int c_end = halves ? c_begin + NC / 2 : (eh == 0 ? NC : 0);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = c_begin; c < c_end; ++c) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
         const int col0 = ti.n0 + c * 32;
@@ -761,7 +776,7 @@ template <int BN, int STAGES, bool BSPLIT, bool ASPLIT = false>
 static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl,
                      const CUtensorMap &mal, const TcArgs &a, int epi, cudaStream_t st) {
   constexpr size_t stage = (size_t)BM * BK * 4 + (size_t)BN * BK * 4;  // (in-place splits)
-  constexpr size_t smem = 1024 + STAGES * stage + 256 + 4 * 32 * 33 * sizeof(float);
+  constexpr size_t smem = 1024 + STAGES * stage + 256 + kEpiWarps * 32 * 33 * sizeof(float);
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
   const int n_tiles = tiles_m * tiles_n * a.groups;
@@ -821,7 +836,7 @@ template <int BN, int STAGES>
 static int launch_tc_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl,
                           const CUtensorMap &mal, const TcArgs &a, int epi, cudaStream_t st) {
   constexpr size_t stage = (size_t)BM * BK * 4 + (size_t)BN * BK * 2;  // A hi + lo, half B hi + lo
-  constexpr size_t smem = 1024 + STAGES * stage + 256 + 4 * 32 * 33 * sizeof(float);
+  constexpr size_t smem = 1024 + STAGES * stage + 256 + kEpiWarps * 32 * 33 * sizeof(float);
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
   const int tiles_m = (a.M + 2 * BM - 1) / (2 * BM), tiles_n = (a.N + BN - 1) / BN;
   const int n_tiles = tiles_m * tiles_n * a.groups;  // (per-request groups: GM_QK / GM_PV)
