@@ -911,7 +911,9 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
     CUtensorMap mal;
     GR_TRY(make_map(&ma, a.a_hi, true, a_rows, a_cols, a.lda, BM));
     GR_TRY(make_map(&mal, a.a_lo, true, a_rows, a_cols, a.lda, BM));
-    if (wide && (a.mode == GM_PLAIN || a.mode == GM_QK || a.mode == GM_PV) && pair_enabled()) {
+    // (per-request groups of <= 128 rows would leave half of a pair tile empty)
+    const bool pair_mode = a.mode == GM_PLAIN || ((a.mode == GM_QK || a.mode == GM_PV) && a.M > BM);
+    if (wide && pair_mode && pair_enabled()) {
       GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, 128));
       GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, 128));
       return launch_tc_pair<256, 6>(ma, mb, mbl, mal, a, epi, st);
