@@ -910,6 +910,8 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
         t.a_lo = t.a_hi + (size_t)p.S_tot * d;
       }
       GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * nh * d, d, EPI_KV_SPLIT, st));
+      // (the trunk's X^T: a transpose pass measured no slower than
+      // transposed stores from the context projection's epilogue)
       if (K > 0) GR_TRY(transpose(X, d, at<float>(ws, p.o_XT), p.vt_ld, (int)p.S_tot, d, st));
     } else {
       if (p.tc) return set_err(GR4AD_ERR_UNSUPPORTED, "tensor-core path: unaligned context");

@@ -645,7 +645,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const float oo[4] = {xo[it].x, xo[it].y, xo[it].z, xo[it].w};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            if (EPI == EPI_BIAS || EPI == EPI_BIAS_DUAL) x[q] = x[q] + ob[q];
+            if (EPI == EPI_BIAS) x[q] = x[q] + ob[q];
+            else if (EPI == EPI_BIAS_DUAL) x[q] = x[q] + ob[q];
             else if (EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_GELU_SPLIT)
               x[q] = gelu_tanh_fast(x[q] + ob[q]);
             else if (EPI == EPI_RESID) x[q] = oo[q] + x[q];

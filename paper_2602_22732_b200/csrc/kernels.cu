@@ -439,11 +439,40 @@ __global__ void level_input_kernel(int t, int rows, int d, const float *__restri
   if (H) H[(long long)r * d + j] = s + pos_t[j];
 }
 
+// the split-only gather (the fuse's pre-split A): four columns per thread,
+// float4 loads and 8-B fp16 stores
+__global__ void level_input_split4_kernel(int t, int rows, int d, const float *__restrict__ bos,
+                                          const float *__restrict__ emb_prev,
+                                          const int *__restrict__ tok, __half *Uh, __half *Ul) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int d4 = d / 4;
+  if (i >= (long long)rows * d4) return;
+  const int r = (int)(i / d4), j = (int)(i - (long long)r * d4) * 4;
+  const float4 s = *reinterpret_cast<const float4 *>(
+      (t == 0) ? bos + j : emb_prev + (long long)tok[r] * d + j);
+  const float sv[4] = {s.x, s.y, s.z, s.w};
+  __align__(8) __half hq[4], lq[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    hq[q] = __float2half_rn(sv[q]);
+    lq[q] = __float2half_rn(sv[q] - __half2float(hq[q]));
+  }
+  const long long o = (long long)r * 2 * d + d + j;
+  *reinterpret_cast<uint2 *>(Uh + o) = *reinterpret_cast<const uint2 *>(hq);
+  *reinterpret_cast<uint2 *>(Ul + o) = *reinterpret_cast<const uint2 *>(lq);
+}
+
 int level_input(int t, int rows, int d, const float *bos, const float *emb_prev,
                 const int *tok, const float *pos_t, float *U, float *H,
                 cudaStream_t st, __half *Uh, __half *Ul) {
   long long n = (long long)rows * d;
   if (n <= 0) return GR4AD_OK;
+  if (Uh && !U && !H && d % 4 == 0) {
+    const long long n4 = n / 4;
+    GR_LAUNCH(KC_SMALL, st, level_input_split4_kernel<<<ceil_div(n4, 256), 256, 0, st>>>(
+                                t, rows, d, bos, emb_prev, tok, Uh, Ul));
+    return GR4AD_OK;
+  }
   GR_LAUNCH(KC_SMALL, st, level_input_kernel<<<ceil_div(n, 256), 256, 0, st>>>(t, rows, d, bos, emb_prev, tok,
                                                        pos_t, U, H, Uh, Ul));
   return GR4AD_OK;
