@@ -352,9 +352,53 @@ __device__ void warp_merge_tail(unsigned long long *buf, int n2, int size, int s
   }
 }
 
-__device__ void sort_desc(unsigned long long *buf, int n2) {
+// buf[0 .. k) = the k largest of buf[0 .. n2) in descending order (keys
+// unique, or zero padding that never ranks below n_real <= n2).
+// n2 <= 256: every warp sorts one 64-entry chunk in registers, then
+// each entry's rank is its position in its own chunk plus, for every other
+// chunk, the count of larger entries (a branch-free 64-way binary search);
+// one scatter.  No block-wide merge stages.  Larger n2: full bitonic sort
+// (measured faster from 512 on: the searches grow with the chunk count).
+__device__ void sort_desc(unsigned long long *buf, int n2, int k) {
   warp_merge_tail(buf, n2, 0, 0);  // sizes 2..64 entirely in registers
   __syncthreads();
+  if (n2 == 64) return;  // one chunk: sorted already
+  if (n2 <= 256) {
+    const int nc = n2 / 64;  // chunk c is descending for even c, ascending for odd
+    unsigned long long x[2];
+    int rk[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = threadIdx.x + u * kThreads;
+      rk[u] = 0x7fffffff;
+      x[u] = 0ull;
+      if (i < n2) {
+        x[u] = buf[i];
+        const int c = i >> 6, o = i & 63;
+        int r = (c & 1) ? 63 - o : o;
+        for (int c2 = 0; c2 < nc; ++c2) {
+          if (c2 == c) continue;
+          const unsigned long long *b = buf + c2 * 64;
+          const bool asc = c2 & 1;
+          int pos = 0;  // count of entries > x in chunk c2
+#pragma unroll
+          for (int st = 32; st >= 1; st >>= 1) {
+            const int j = pos + st - 1;
+            pos += b[asc ? 63 - j : j] > x[u] ? st : 0;
+          }
+          pos += (pos == 63 && b[asc ? 0 : 63] > x[u]) ? 1 : 0;
+          r += pos;
+        }
+        rk[u] = r;
+      }
+    }
+    __syncthreads();  // every read done before the scatter
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (rk[u] < k) buf[rk[u]] = x[u];
+    __syncthreads();
+    return;
+  }
   for (int size = 128; size <= n2; size <<= 1) {
     for (int st = size >> 1; st >= 64; st >>= 1) {
       for (int i = threadIdx.x; i < n2 / 2; i += kThreads) {
@@ -736,7 +780,7 @@ __device__ int select_level(const FusedArgs &a, int b, int t, int live, int V,
   while (n2 < n_sort) n2 <<= 1;
   for (int i = n_sort + tid; i < n2; i += kThreads) sbuf[i] = 0ull;
   __syncthreads();
-  sort_desc(sbuf, n2);
+  sort_desc(sbuf, n2, k);
   // alive filter (beam.py:202-203): with masking, -inf candidates sort last;
   // keep the finite prefix of the selection
   int kk = k;
