@@ -566,6 +566,9 @@ __device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S,
       a.dbg[blockIdx.x * kDbgSlots + (i)] = _t;                                 \
     }                                                                           \
   } while (0)
+#ifdef GR_NO_XSTAMP
+#define GR_XSTAMP(w, i) do {} while (0)
+#else
 #define GR_XSTAMP(w, i)                                                         \
   do {                                                                          \
     if (t == 2 && threadIdx.x == 32 * (w)) {                                    \
@@ -574,6 +577,7 @@ __device__ void trunk_warp0(const FusedArgs &a, const float *Xs, int xld, int S,
       a.dbg[blockIdx.x * kDbgSlots + (i)] = _t;                                 \
     }                                                                           \
   } while (0)
+#endif
 #else
 #define GR_XSTAMP(w, i) do {} while (0)
 #define GR_STAMP(i) do {} while (0)
@@ -2266,7 +2270,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
       GR_XSTAMP(7, 46);
       __syncthreads();
       collected = (int)scr[40];
-#ifdef GR_FUSED_TIMING
+#if defined(GR_FUSED_TIMING) && !defined(GR_NO_XSTAMP)
       if (t == 2 && tid == 0) a.dbg[blockIdx.x * kDbgSlots + 47] = collected;
 #endif
       if (collected > a.sort_cap) {

@@ -74,3 +74,6 @@ if (x > 0).all():
     r = np.median((x - tail[:, [7]]) / 1e3, 0)
     print("  level-2 loop-B end (us from level start) warps 1,2,3,5,7:", np.round(r, 2),
           " window entries collected: median", np.median(tail[:, 47]), "max", tail[:, 47].max())
+if os.environ.get("GR_TRUNK_STAMPS"):  # build with -DGR_NO_XSTAMP: slots 42-47 = trunk stamps
+    r = np.median((tail[:, 42:48] - tail[:, [1]]) / 1e3, 0)
+    print("  trunk stamps 42..47 (us after ctx proj):", np.round(r, 2))
