@@ -436,6 +436,7 @@ def main():
     # host collects step i-2, as a serving loop would; per-request latency is
     # measured on the serial path.
     NSET = 3
+    E2E_WINDOWS = 5
     host_f = [feats.cpu().pin_memory() for _ in range(NSET)]
     decs = [dec] + [BeamDecoder(model, [S] * B, [widths] * B, device=dev) for _ in range(NSET - 1)]
     h2d = host_f[0].numel() * host_f[0].element_size()
@@ -478,7 +479,7 @@ def main():
     if world > 1:
         dist.barrier()
     best = None
-    for _ in range(3):  # best of three windows of pipelined steps (host jitter)
+    for _ in range(E2E_WINDOWS):  # best of several windows of pipelined steps (host jitter)
         pending = [None] * NSET
         t0 = time.perf_counter()
         for i in range(e2e_steps):
@@ -544,11 +545,11 @@ def main():
                     "how": "C ABI with pinned host buffers; per step H2D features + decode + "
                            "D2H results (one CUDA graph per buffer set, BeamDecoder."
                            "capture_host), three buffer sets on three streams (copies of step "
-                           "i+1 overlap the decode of step i); best of 3 windows of e2e_steps "
+                           "i+1 overlap the decode of step i); best of 5 windows of e2e_steps "
                            "steps (>= K, >= ~50 ms of device work)",
                     "e2e_steps": e2e_steps},
-            "gpu_launches": launches_per_step * (args.steps * 2 + e2e_steps * 3),
-            "gpu_launches_note": "per-step launches x (device-timed K + serial e2e K + 3 pipelined e2e windows of e2e_steps) steps",
+            "gpu_launches": launches_per_step * (args.steps * 2 + e2e_steps * E2E_WINDOWS),
+            "gpu_launches_note": "per-step launches x (device-timed K + serial e2e K + 5 pipelined e2e windows of e2e_steps) steps",
             "launches_per_step": launches_per_step,
             "algorithmic_tflops": flops * value / 1e12,
             "results_per_step": int(cnt.item()),

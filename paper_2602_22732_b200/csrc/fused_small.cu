@@ -1826,12 +1826,17 @@ __global__ void __launch_bounds__(kThreads, 2) fused_mma_kernel(FusedArgs a) {
     trunk_warp0<D>(a, XT, VS, S, TR, TQ, wsl, a.trunk_u);
     GR_WSTAMP(16);
   } else {
-    const int t0 = K > 0 ? 32 : 0, nt = kThreads - t0;
+    // with a trunk, warp 4 (warp 0's SMSP) stays idle so the trunk warp -- the
+    // phase's critical path -- does not share its scheduler with K/V work
+    // (six warps need two rounds over the 256 keys, as seven do)
+    const bool spare = K > 0;
+    const int kv_t = !spare ? tid : (wid < 4 ? tid - 32 : tid - 64);
+    const int nt = !spare ? kThreads : kThreads - 64;
     const int ldw = 2 * L * D;
-    for (int i = K; i < L; ++i) {
+    for (int i = K; i < L && !(spare && wid == 4); ++i) {
       float *Kl = KV + (size_t)(i - K) * KVL, *VTl = Kl + SP * D;
       const float *Wl = W.cross_kv_W + (size_t)(2 * i) * D;
-      for (int s = tid - t0; s < SP; s += nt) {
+      for (int s = kv_t; s < SP; s += nt) {
         float x[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) x[j] = XT[j * VS + s];
