@@ -485,7 +485,10 @@ def main():
         for i in range(e2e_steps):
             j = i % NSET
             if pending[j] is not None:
-                pending[j].synchronize()  # results of step i-2 are on the host
+                # results of step i-NSET are on the host (spin on the event,
+                # as a latency-sensitive serving loop would: no wake-up jitter)
+                while not pending[j].query():
+                    pass
             pending[j] = submit(j)
         for ev in pending:
             if ev is not None:
