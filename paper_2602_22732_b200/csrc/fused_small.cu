@@ -1142,14 +1142,13 @@ __global__ void __launch_bounds__(kThreads, 2) fused_small_kernel(FusedArgs a) {
 // ===========================================================================
 // Warp-MMA variant (d = 16): every per-level product -- fused gate, head-layer
 // projections, cross-attention Q.K^T and P.V, FFN, codebook logits -- runs on
-// the tensor cores through mma.sync.m16n8k8 in 3xTF32 (hi.lo + lo.hi + hi.hi,
-// fp32 accumulate), with a warp owning a 16-row tile.  The per-row state
-// stays in C fragments: under the k-permutation (k = t <-> column 2t,
-// k = t + 4 <-> column 2t + 1, B rows permuted alike) a C fragment is
-// directly the A fragment of the next product, so no shuffles or shared-
-// memory round trips between products.  Cross-attention is flash-style
-// (online softmax over 64-key chunks) over K [S][D+8] and V^T [D][S+8] in
-// shared memory (padded strides: conflict-free LDS.64 fragment loads).
+// the tensor cores through mma.sync.m16n8k16 in 3xFP16 (lo.hi + hi.lo +
+// hi.hi, fp32 accumulate; weights pre-scaled by kFragScale, context K / V by
+// kKvScaleF), with a warp owning a 16-row tile.  The per-row state stays in C
+// fragments: a pair of m16n8 C fragments is the A fragment of the next k16
+// product, so no shuffles or shared-memory round trips between products.
+// Cross-attention is flash-style (online softmax over key chunks) over K as
+// fp16 hi / lo words (bank-swizzled) and V^T [D][S+8] in shared memory.
 // Trunk, selection and compaction are the CUDA-core code above.
 // ===========================================================================
 // pull [p, p + bytes) toward this SM's L1 (128-B lines split over the CTA)
