@@ -488,7 +488,7 @@ def main():
                 # results of step i-NSET are on the host (spin on the event,
                 # as a latency-sensitive serving loop would: no wake-up jitter)
                 while not pending[j].query():
-                    pass
+                    time.sleep(0)  # (releases the GIL: the clocks sampler thread runs)
             pending[j] = submit(j)
         for ev in pending:
             if ev is not None:
