@@ -616,7 +616,10 @@ __device__ __forceinline__ unsigned warp_sum_u(unsigned v) {
   return v;
 }
 
-constexpr int kSelThreads = 1024;
+// 512 threads, two CTAs per SM (the uncached instantiation's 72 KB of shared
+// memory allows it): a batch's requests stream their logits in one wave
+// instead of 1.7 waves of one 1024-thread CTA per SM
+constexpr int kSelThreads = 512;
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kCacheKeys = 28 * 1024;  // 112 KB of cached keys
 
@@ -696,13 +699,13 @@ __device__ int sel_find_bin(unsigned *hist, int nbins, unsigned need, unsigned *
   if (lane == 31) wsum[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    unsigned s = wsum[lane];
+    unsigned s = lane < kSelWarps ? wsum[lane] : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       unsigned y = __shfl_up_sync(0xffffffffu, s, o);
       if (lane >= o) s += y;
     }
-    wsum[lane] = s;  // inclusive
+    if (lane < kSelWarps) wsum[lane] = s;  // inclusive
   }
   __syncthreads();
   unsigned excl = x - local + (wid > 0 ? wsum[wid - 1] : 0u);
@@ -726,7 +729,7 @@ __device__ int sel_find_bin(unsigned *hist, int nbins, unsigned need, unsigned *
 }
 
 template <bool CACHE>
-__global__ void __launch_bounds__(kSelThreads, 1) topk_select_kernel(SelectArgs a, int u_rows, int u_k) {
+__global__ void __launch_bounds__(kSelThreads, 2) topk_select_kernel(SelectArgs a, int u_rows, int u_k) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(smem);  // GR4AD_MAX_BEAM
   unsigned *hist = reinterpret_cast<unsigned *>(sbuf + GR4AD_MAX_BEAM);    // 2048
