@@ -944,6 +944,12 @@ int gemm_tc_swapped(const TcArgs &a, long long a_rows, long long a_cols, long lo
   if (a.M <= 0 || a.N <= 0 || a.groups <= 0) return GR4AD_OK;
   if (a.mode != GM_QK_T && a.mode != GM_PV_T)
     return set_err(GR4AD_ERR_UNSUPPORTED, "swapped tc gemm: mode %d", a.mode);
+  static const bool trace = getenv("GR4AD_TRACE") != nullptr;  // debug aid (read-only)
+  if (trace)
+    fprintf(stderr, "gemm_tc M=%d N=%d K=%d groups=%d mode=%d epi=%d lda=%lld ldb=%lld ldc=%lld "
+                    "A=(%lld,%lld) B=(%lld,%lld) presplit=%d asplit=%d swapped=1\n",
+            a.M, a.N, a.K, a.groups, a.mode, epi, a.lda, a.ldb, a.ldc, a_rows, a_cols, b_rows,
+            b_cols, a.b_hi != nullptr, a.a_hi != nullptr);
   CUtensorMap ma, mal, mb;
   // N = beam rows per request: the smallest tile that holds them
   const int bn = a.N <= 32 ? 32 : (a.N <= 64 ? 64 : 128);

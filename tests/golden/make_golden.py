@@ -4,6 +4,7 @@ Run in the build container (the only place /root/reference exists):
 
     python tests/golden/make_golden.py            # small fixtures (~1 min)
     python tests/golden/make_golden.py --c3       # + one C3 request (~5-10 min)
+    python tests/golden/make_golden.py --big      # C3 x8, C5 x8, C4-width x2 (~10 min)
 
 Outputs (committed, read by tests/test_oracle_golden.py and the GPU parity
 tests; nothing at test time reads /root/reference):
@@ -11,6 +12,13 @@ tests; nothing at test time reads /root/reference):
 * golden_small.json  -- pre-cut instances, init checksums, beam-search
   outputs + counters on random/tiny/C1/C2 models, teacher-forced logits.
 * golden_c3.json     -- one request at the C3 shape (widths 512^3).
+* golden_big.json    -- the C3 model decoded at the benched shapes:
+  requests 0..7 at C3 widths 512^3, requests 0..7 at the C5 schedule
+  64/128/256, and requests 0..1 at the C4 off-peak TABS widths 99/197/394
+  (scale_schedule(64/128/256, 394)), each with the reference's per-level
+  cut gaps (k-th minus (k+1)-th best candidate, recorded by wrapping
+  beam._select) so a divergence at an intermediate level can be excused
+  only where the reference's own cut was closer than tau.
 
 Reference entry points used: adrec.serving.beam.{beam_search, topk_precut,
 topk_global} (beam.py:37-143), adrec.model.decoder.{DecoderConfig,
@@ -57,6 +65,8 @@ def c_features(i, s_ctx, feat_dim=16):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3", action="store_true")
+    ap.add_argument("--big", action="store_true")
+    ap.add_argument("--big-only", action="store_true")
     args = ap.parse_args()
     sys.path.insert(0, REF)
     from adrec.losses.supervised import fit_ecpm_buckets
@@ -74,6 +84,12 @@ def main():
                                    counter=counter, **kw)
         return ([list(sid.tokens) for sid, _ in res], [float(s) for _, s in res],
                 [counter.layer_calls, counter.kv_builds, counter.kv_floats])
+
+    if args.big or args.big_only:
+        make_big(DecoderConfig, DecoderModel, context_process, ref_beam, BeamSchedule,
+                 resolve_dbw, scale_schedule, run)
+        if args.big_only:
+            return
 
     out = {"generator": "tests/golden/make_golden.py", "reference": REF}
 
@@ -227,6 +243,53 @@ def main():
         with open(os.path.join(HERE, "golden_c3.json"), "w") as fh:
             json.dump(c3, fh)
         print("wrote golden_c3.json in", c3["seconds"], "s")
+
+
+def make_big(DecoderConfig, DecoderModel, context_process, ref_beam, BeamSchedule,
+             resolve_dbw, scale_schedule, run):
+    """C3-model requests at the C3 / C5 / C4 widths, with per-level cut gaps."""
+    cfg = DecoderConfig(16, 1024, 2048, 8, 5, (4096, 4096, 4096), 4, seed=2)
+    model = DecoderModel(cfg)
+    gaps = []
+    orig = ref_beam._select
+
+    def select(beam_scores, logprobs, k, precut):
+        res = orig(beam_scores, logprobs, k, precut)
+        nxt = orig(beam_scores, logprobs, k + 1, precut)[2]
+        sel = res[2]
+        if len(nxt) > len(sel) and len(sel) and np.isfinite(nxt[len(sel)]):
+            gaps.append(float(sel[-1] - nxt[len(sel)]))
+        else:
+            gaps.append(None)
+        return res
+
+    ref_beam._select = select
+    c4 = list(scale_schedule(resolve_dbw([64, 128, 256], 3), 394).widths)
+    plan = ([("C3", i, [512, 512, 512]) for i in range(8)]
+            + [("C5", i, [64, 128, 256]) for i in range(8)]
+            + [("C4", i, c4) for i in range(2)])
+    cases = []
+    t_all = time.time()
+    try:
+        for name, i, widths in plan:
+            t0 = time.time()
+            x = context_process(c_features(i, 1024), model.params)
+            del gaps[:]
+            toks, scores, counter = run(model, x, widths)
+            cases.append({"name": f"{name}_req{i}", "request": i, "s_ctx": 1024,
+                          "widths": widths, "tokens": toks, "scores": scores,
+                          "counter": counter, "level_cut_gaps": list(gaps),
+                          "seconds": time.time() - t0})
+            print(name, i, widths, f"{time.time() - t0:.1f}s", flush=True)
+    finally:
+        ref_beam._select = orig
+    big = {"generator": "tests/golden/make_golden.py --big", "reference": REF,
+           "config": _cfg_dict(cfg), "init_sha256": params_digest(model.params),
+           "c4_widths_from": "scale_schedule(resolve_dbw([64,128,256],3), 394)",
+           "cases": cases, "seconds": time.time() - t_all}
+    with open(os.path.join(HERE, "golden_big.json"), "w") as fh:
+        json.dump(big, fh)
+    print("wrote golden_big.json in", big["seconds"], "s")
 
 
 if __name__ == "__main__":

@@ -39,7 +39,8 @@ def _common(d):
 def test_reference_arm_contract():
     """`bench.py --impl reference`: the oracle port on the host cores, same
     metric / unit / config as our arm, e2e = the line's own value."""
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1"], timeout=600)
+    d = _run(["--impl", "reference", "--config", "c2", "--steps", "1", "--warmup", "1"],
+             timeout=600)
     _common(d)
     assert d["impl"] == "reference"
     cb = d["cpu_baseline"]
@@ -56,7 +57,8 @@ def test_our_arm_contract():
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    d = _run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline"], timeout=600)
+    d = _run(["--config", "c2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"],
+             timeout=600)
     _common(d)
     r = d["roofline"]
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
