@@ -41,7 +41,10 @@ typedef enum {
   GR4AD_ERR_VALUE = 1,     /* maps to ValueError (reference argument errors) */
   GR4AD_ERR_UNSUPPORTED = 2,
   GR4AD_ERR_WORKSPACE = 3, /* workspace too small */
-  GR4AD_ERR_CUDA = 4       /* maps to RuntimeError */
+  GR4AD_ERR_CUDA = 4,      /* maps to RuntimeError */
+  GR4AD_ERR_RANGE = 5      /* an operand left the fp16 split range of the tensor-core
+                              paths: decode with a CUDA-core path (the Python API does
+                              so automatically for decode_path auto) */
 } gr4ad_status;
 
 /* DecoderConfig (pkg/src/adrec/model/decoder.py:32-51). */
@@ -180,11 +183,50 @@ int gr4ad_prepare_weights(const gr4ad_dims *dims, const gr4ad_weights *w,
 /* fp16 split range of the last decode in `workspace` (synchronises `stream`).
  * The tensor-core paths split weights (x 2048) and the context K / V (x 256)
  * into fp16 hi + lo; a value outside the fp16 range after that scale sets a
- * flag in the workspace, reported here as GR4AD_ERR_UNSUPPORTED (decode
- * with a CUDA-core path instead).  No reference counterpart: the reference
+ * flag in the workspace, reported here as GR4AD_ERR_RANGE (decode with a
+ * CUDA-core path instead).  No reference counterpart: the reference
  * computes in float64 (autodiff.py:55). */
 int gr4ad_range_status(const gr4ad_dims *dims, const gr4ad_batch *batch, const void *workspace,
                        void *stream);
+/* Byte offset of that flag (an int, nonzero = out of range) inside the
+ * workspace, so a caller can copy it to the host together with the results
+ * instead of synchronising in gr4ad_range_status. */
+int gr4ad_range_flag_offset(const gr4ad_dims *dims, const gr4ad_batch *batch, size_t *offset);
+
+/* The layered decode split at the reference's own phase boundaries
+ * (beam.py:146-218), for callers that interleave their own
+ * work between levels.  After gr4ad_prepare (+ gr4ad_prepare_weights):
+ *   gr4ad_encode_trunk   context projection (decoder.py:134-140), shared
+ *                        encoder K/V (beam.py:98-109, 164-169), trunk pass
+ *                        (beam.py:159-163), level-0 beam rows;
+ *   gr4ad_level_step(t)  level t = 0..T-1: token gather + fuse
+ *                        (beam.py:180-191), head layers (beam.py:243-255),
+ *                        codebook projection + log-softmax + score
+ *                        accumulation + top-k + alive filter + in-place
+ *                        compaction (beam.py:198-210); t = T with
+ *                        value_rerank: the re-rank head pass (beam.py:258-288);
+ *   gr4ad_collect        the final beams into `out` (beam.py:212-217).
+ * The sequence is bit-identical to gr4ad_beam_search_run on the same
+ * workspace.  Needs the layered path (decode_path 1 or 3, or auto when it
+ * picks the layered path); GR4AD_ERR_UNSUPPORTED for the fused kernel. */
+int gr4ad_encode_trunk(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4ad_batch *batch,
+                       const float *features, const float *context, void *workspace,
+                       size_t workspace_bytes, void *stream);
+int gr4ad_level_step(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4ad_batch *batch,
+                     int level, void *workspace, size_t workspace_bytes, void *stream);
+int gr4ad_collect(const gr4ad_dims *dims, const gr4ad_batch *batch, gr4ad_results *out,
+                  void *workspace, size_t workspace_bytes, void *stream);
+
+/* On-device SID -> item resolution (reference engine.py:114-118,
+ * quantizer/index.py:33-35): for every result entry
+ * (b, j < count[b]) of `res`, the SID's mixed-radix key
+ * sum_t tok_t * prod_{u>t} V_u is looked up in `sid_keys` (device, sorted
+ * ascending, n_keys entries -- the index's SIDs); out_item[b*max_out + j]
+ * = item_ids[pos] (device) when found, else -1 (unindexed: the engine drops
+ * it, as the reference's post-filter does).  Entries past count[b] get -1. */
+int gr4ad_resolve_items(const int64_t *sid_keys, const int *item_ids, int n_keys,
+                        const gr4ad_dims *dims, const gr4ad_results *res, int n_requests,
+                        int *out_item, void *stream);
 
 /* Context projection X = F W_c + b_c (decoder.py:134-140): (rows, F) -> (rows, d). */
 int gr4ad_context_process(const gr4ad_dims *dims, const gr4ad_weights *w,
@@ -238,6 +280,17 @@ int gr4ad_topk_precut(const float *prev_scores, const float *logprobs,
                       int *out_token, float *out_score, int *out_count,
                       void *workspace, size_t workspace_bytes, void *stream);
 size_t gr4ad_topk_workspace_bytes(int n_problems, int b, int v);
+
+/* The same selection on float64 inputs, bit-exact against the reference
+ * (beam.py:37-89): candidate score = prev_scores[p*b + i] + logprobs[...]
+ * computed in IEEE double exactly as numpy's broadcast add, ranked by
+ * (-score, beam, token) with no rounding of the keys; -inf candidates rank
+ * last (the caller's alive filter drops them, beam.py:202-203).  Scores are
+ * returned in double.  One CTA per problem: 64-bit radix select, ordered tie
+ * collection, in-shared-memory sort of the k winners (k <= GR4AD_MAX_BEAM). */
+int gr4ad_topk_precut_f64(const double *prev_scores, const double *logprobs, int n_problems,
+                          int b, int v, int k, int *out_beam, int *out_token, double *out_score,
+                          int *out_count, void *stream);
 
 /* Fused codebook projection + log-softmax + score accumulation + top-k for
  * one level (beam.py:198-201): states (n_problems*b, d) @ head (d, v),

@@ -19,7 +19,13 @@ MAX_LEVELS = 8
 MAX_LAYERS = 32
 MAX_BEAM = 8192
 
-OK, ERR_VALUE, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA = range(5)
+OK, ERR_VALUE, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA, ERR_RANGE = range(6)
+
+
+class RangeError(RuntimeError):
+    """An operand left the fp16 split range of the tensor-core paths
+    (GR4AD_ERR_RANGE): |weight| >= 32 or |context K/V| >= 256.  The decode
+    API retries such batches on the CUDA-core path when ``path="auto"``."""
 
 KERNEL_CLASSES = ("gemm", "attn_gemm", "topk_select", "softmax", "layernorm", "self_attn",
                   "row_lse", "small", "collect", "fused_decode")
@@ -32,7 +38,8 @@ EXPORTS = (
     "gr4ad_topk_precut", "gr4ad_topk_workspace_bytes", "gr4ad_project_topk",
     "gr4ad_project_topk_workspace_bytes", "gr4ad_gemm", "gr4ad_score_sequences",
     "gr4ad_score_workspace_bytes", "gr4ad_range_status", "gr4ad_prepare_weights",
-    "gr4ad_gemm_presplit",
+    "gr4ad_gemm_presplit", "gr4ad_range_flag_offset", "gr4ad_encode_trunk",
+    "gr4ad_level_step", "gr4ad_collect", "gr4ad_topk_precut_f64", "gr4ad_resolve_items",
 )
 
 _P = C.c_void_p
@@ -116,6 +123,18 @@ def _load():
                                           _P, C.c_size_t, _P]
     lib.gr4ad_score_workspace_bytes.argtypes = [C.POINTER(Dims), C.POINTER(Batch), C.c_int,
                                                 C.POINTER(C.c_size_t)]
+    lib.gr4ad_range_flag_offset.argtypes = [C.POINTER(Dims), C.POINTER(Batch),
+                                            C.POINTER(C.c_size_t)]
+    lib.gr4ad_encode_trunk.argtypes = [C.POINTER(Dims), C.POINTER(Weights), C.POINTER(Batch),
+                                       _P, _P, _P, C.c_size_t, _P]
+    lib.gr4ad_level_step.argtypes = [C.POINTER(Dims), C.POINTER(Weights), C.POINTER(Batch),
+                                     C.c_int, _P, C.c_size_t, _P]
+    lib.gr4ad_collect.argtypes = [C.POINTER(Dims), C.POINTER(Batch), C.POINTER(Results), _P,
+                                  C.c_size_t, _P]
+    lib.gr4ad_topk_precut_f64.argtypes = [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P,
+                                          _P, _P, _P]
+    lib.gr4ad_resolve_items.argtypes = [_P, _P, C.c_int, C.POINTER(Dims), C.POINTER(Results),
+                                        C.c_int, _P, _P]
     if lib.gr4ad_abi_version() != 1:
         raise ImportError("libgr4ad ABI version mismatch")
     return lib
@@ -131,4 +150,6 @@ def check(status):
     if status == ERR_VALUE:
         raise ValueError(msg)
     kind = lib.gr4ad_status_string(status).decode()
+    if status == ERR_RANGE:
+        raise RangeError(f"libgr4ad: {kind}: {msg}")
     raise RuntimeError(f"libgr4ad: {kind}: {msg}")

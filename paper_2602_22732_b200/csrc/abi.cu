@@ -946,6 +946,148 @@ static bool no_proxy_window() {
   return off;
 }
 
+// Layered decode, split at the boundaries the per-level C entry points
+// expose (gr4ad_encode_trunk / gr4ad_level_step / gr4ad_collect):
+// context projection + shared encoder K/V + trunk + level-0 rows ...
+static int layered_begin(const Plan &p, const gr4ad_weights *w, const float *features,
+                         const float *context, void *ws, WeightsT &wt_store, const WeightsT *&wt,
+                         float *&VT, cudaStream_t st) {
+  GR_TRY(encode_and_trunk(p, w, features, context, ws, wt_store, wt, VT, st));
+  return init_level0(p.B, at<int>(ws, p.o_live), at<float>(ws, p.o_cum),
+                     at<long long>(ws, p.o_prefix), at<int>(ws, p.o_anc), p.stride,
+                     at<int>(ws, p.o_tok), st);
+}
+
+// ... one level step t (t == T: the value re-rank head pass) ...
+static int layered_level(const Plan &p, const gr4ad_weights *w, const gr4ad_batch *bt, int t,
+                         void *ws, const WeightsT *wt, float *VT, cudaStream_t st) {
+  const int B = p.B, T = p.T, d = p.d, K = p.K;
+  int *eff = at<int>(ws, p.o_eff), *cap = at<int>(ws, p.o_cap);
+  int *row_off = at<int>(ws, p.o_row_off), *live = at<int>(ws, p.o_live);
+  int *row_req = at<int>(ws, p.o_row_req);
+  int *tok = at<int>(ws, p.o_tok), *anc = at<int>(ws, p.o_anc);
+  float *cum = at<float>(ws, p.o_cum);
+  long long *prefix = at<long long>(ws, p.o_prefix);
+  float *KV = at<float>(ws, p.o_KV), *Ht = at<float>(ws, p.o_Ht);
+  float *Hs = at<float>(ws, p.o_Hs), *U = at<float>(ws, p.o_U);
+  float *LG = at<float>(ws, p.o_LG);
+  float2 *rinfo = at<float2>(ws, p.o_rinfo);
+  float *hist = at<float>(ws, p.o_hist);
+  const size_t hist_layer = (size_t)p.H * 3 * d;
+  const int R = (int)p.R[t];
+  const long long h0 = p.hist_off[t];
+  // token input + gated fusion (beam.py:180-191; layers.py:129-133)
+  const float *emb_prev = t > 0 ? w->emb[t - 1] : nullptr;
+  if (K > 0 && p.tc && wt && d % 8 == 0) {
+    // the fuse on pre-split operands: s (and the gate product g) as fp16
+    // hi / lo, so both GEMMs run TMA-only (CTA pairs)
+    __half *Uh = at<__half>(ws, p.o_U16), *Ul = Uh + (size_t)p.Rw * 2 * d;
+    GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, nullptr, nullptr, nullptr, st, Uh,
+                       Ul));
+    GemmArgs gg = plain_gemm(nullptr, 2LL * d, w->fuse_Wg, d, nullptr, 2LL * d, R, d, d);
+    gg.vec = Ht + (size_t)t * d;
+    gg.vec_ld = (long long)p.n_pos * d;
+    gg.row_req = row_req + h0;
+    GR_TRY(dense_split(p, gg, wt->wg, Uh + d, Ul + d, R, EPI_MULVEC_SPLIT, st, Uh, Ul));
+    GR_TRY(dense_split(p, plain_gemm(nullptr, 2LL * d, w->fuse_Wf, d, Hs, d, R, d, 2 * d), wt->wf,
+                       Uh, Ul, R, EPI_STORE, st));
+  } else if (K > 0) {
+    GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, nullptr, U, nullptr, st));
+    GemmArgs gg = plain_gemm(U + d, 2LL * d, w->fuse_Wg, d, U, 2LL * d, R, d, d);
+    gg.vec = Ht + (size_t)t * d;
+    gg.vec_ld = (long long)p.n_pos * d;
+    gg.row_req = row_req + h0;
+    GR_TRY(dense(p, gg, wt ? wt->wg : nullptr, R, EPI_MULVEC, st));
+    GR_TRY(dense(p, plain_gemm(U, 2LL * d, w->fuse_Wf, d, Hs, d, R, d, 2 * d),
+                 wt ? wt->wf : nullptr, R, EPI_STORE, st));
+  } else {
+    GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, w->pos + (size_t)t * d, nullptr,
+                       Hs, st));
+  }
+  // head layers K..L-1 against the shared context KV (beam.py:243-255)
+  RowSet rs{};
+  rs.rows = R;
+  rs.max_group_rows = p.maxcap[t];
+  rs.g_row_off = row_off + (size_t)t * B;
+  rs.g_rows = cap + (size_t)t * B;
+  rs.row_req = row_req + h0;
+  rs.hist_row0 = h0;
+  rs.anc = anc;
+  rs.anc_stride = p.stride;
+  rs.npos_u = t + 1;
+  rs.npos_row = nullptr;
+  bool h_split = false;  // the last layer left Hs as fp16 hi / lo in N
+  for (int i = K; i < p.L; ++i) {
+    rs.qkv = hist + (size_t)(i - K) * hist_layer;
+    GR_TRY(layer_forward(p, w, wt, i, Hs, rs, ws, KV, VT, st,
+                         (i == p.L - 1 && t < T) ? &h_split : nullptr));
+  }
+  if (t == T) {  // value re-rank step (beam.py:258-288)
+    float *vlog = at<float>(ws, p.o_vlog);
+    GR_TRY(dense(p, plain_gemm(Hs, d, w->head_value, p.nb, vlog, p.nb, R, p.nb, d),
+                 wt ? wt->hv : nullptr, R, EPI_STORE, st));
+    return GR4AD_OK;
+  }
+  // codebook projection + log-softmax + score accumulation + top-k (beam.py:198-210)
+  const int V = p.V[t];
+  const GemmArgs lg = plain_gemm(Hs, d, w->head[t], V, LG, V, R, V, d);
+  const float4 *proxies = nullptr;
+  if (p.tc && wt && d % 8 == 0 && tc_eligible(d, d, d, Hs, wt->head[t])) {
+    // log-sum-exp partials from the GEMM epilogue (no second pass over the logits)
+    TcArgs tl{};
+    static_cast<GemmArgs &>(tl) = lg;
+    tl.b_hi = wt->head[t];
+    tl.b_lo = wt->head[t] + p.wt_floats;
+    tl.ldb = d;
+    tl.alpha = lg.alpha / kWeightScale;
+    tl.lse_part = at<float4>(ws, p.o_lsep);
+    tl.lse_ld = (V + 127) / 128;
+    if (h_split) {
+      tl.a_hi = at<__half>(ws, p.o_N);
+      tl.a_lo = tl.a_hi + (size_t)p.Rw * d;
+    }
+    GR_TRY(gemm_tc(tl, R, d, V, d, EPI_STORE_LSE, st));
+    GR_TRY(lse_merge(tl.lse_part, tl.lse_ld, R, rinfo, st));
+    if (!bt->valid_prefix[t] && !no_proxy_window()) proxies = tl.lse_part;
+  } else {
+    GR_TRY(dense(p, lg, wt ? wt->head[t] : nullptr, R, EPI_STORE, st));
+    GR_TRY(row_lse(LG, V, R, V, rinfo, st));
+  }
+  if (bt->valid_prefix[t]) {
+    GR_TRY(mask_rows(LG, V, R, V, prefix + h0,
+                     reinterpret_cast<const long long *>(bt->valid_prefix[t]),
+                     bt->valid_prefix_count[t], st));
+  }
+  SelectArgs sa{};
+  sa.logits = LG; sa.ld = V; sa.V = V; sa.level = t;
+  sa.rowinfo = rinfo; sa.cum = cum;
+  sa.proxies = proxies; sa.proxy_ld = (V + 127) / 128;
+  sa.row_off = row_off + (size_t)t * B;
+  sa.live = live + (size_t)t * B;
+  sa.eff = eff + (size_t)t * B;
+  sa.hist_off = (int)h0;
+  sa.out_row_off = row_off + (size_t)(t + 1) * B;
+  sa.out_cap = cap + (size_t)(t + 1) * B;
+  sa.out_live = live + (size_t)(t + 1) * B;
+  sa.out_hist_off = (int)p.hist_off[t + 1];
+  sa.tok = tok; sa.cum_out = cum; sa.prefix = prefix; sa.anc = anc;
+  sa.anc_stride = p.stride;
+  GR_TRY(topk_select(sa, B, 0, 0, p.max_cand[t], st));
+  return GR4AD_OK;
+}
+
+// ... and the results of the last level (or of the re-rank).
+static int layered_end(const Plan &p, const gr4ad_batch *bt, gr4ad_results *out, void *ws,
+                       cudaStream_t st) {
+  const int B = p.B, T = p.T;
+  int *row_off = at<int>(ws, p.o_row_off), *live = at<int>(ws, p.o_live);
+  return collect_results(B, T, row_off + (size_t)T * B, live + (size_t)T * B,
+                         (int)p.hist_off[T], at<int>(ws, p.o_tok), at<int>(ws, p.o_anc), p.stride,
+                         at<float>(ws, p.o_cum), p.rerank ? at<float>(ws, p.o_vlog) : nullptr,
+                         p.nb, bt->value_reps, out->max_out, out->count, out->tokens, out->score,
+                         st);
+}
+
 static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
                     const gr4ad_batch *bt, const float *features, const float *context,
                     gr4ad_results *out, void *ws, cudaStream_t st) {
@@ -1017,131 +1159,13 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
     }
     return fused_small_launch(f, B, p.f_smem, st);
   }
-  int *eff = at<int>(ws, p.o_eff), *cap = at<int>(ws, p.o_cap);
-  int *row_off = at<int>(ws, p.o_row_off), *live = at<int>(ws, p.o_live);
-  int *row_req = at<int>(ws, p.o_row_req);
-  int *tok = at<int>(ws, p.o_tok), *anc = at<int>(ws, p.o_anc);
-  float *cum = at<float>(ws, p.o_cum);
-  long long *prefix = at<long long>(ws, p.o_prefix);
-  float *KV = at<float>(ws, p.o_KV), *Ht = at<float>(ws, p.o_Ht);
-  float *Hs = at<float>(ws, p.o_Hs), *U = at<float>(ws, p.o_U);
-  float *LG = at<float>(ws, p.o_LG);
-  float2 *rinfo = at<float2>(ws, p.o_rinfo);
-  float *hist = at<float>(ws, p.o_hist);
-  const size_t hist_layer = (size_t)p.H * 3 * d;
   WeightsT wt_store;
   const WeightsT *wt = nullptr;
   float *VT = nullptr;
-  GR_TRY(encode_and_trunk(p, w, features, context, ws, wt_store, wt, VT, st));
-  GR_TRY(init_level0(B, live, cum, prefix, anc, p.stride, tok, st));
-
+  GR_TRY(layered_begin(p, w, features, context, ws, wt_store, wt, VT, st));
   const int last = p.rerank ? T : T - 1;
-  for (int t = 0; t <= last; ++t) {
-    const int R = (int)p.R[t];
-    const long long h0 = p.hist_off[t];
-    // token input + gated fusion (beam.py:180-191; layers.py:129-133)
-    const float *emb_prev = t > 0 ? w->emb[t - 1] : nullptr;
-    if (K > 0 && p.tc && wt && d % 8 == 0) {
-      // the fuse on pre-split operands: s (and the gate product g) as fp16
-      // hi / lo, so both GEMMs run TMA-only (CTA pairs)
-      __half *Uh = at<__half>(ws, p.o_U16), *Ul = Uh + (size_t)p.Rw * 2 * d;
-      GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, nullptr, nullptr, nullptr, st, Uh,
-                         Ul));
-      GemmArgs gg = plain_gemm(nullptr, 2LL * d, w->fuse_Wg, d, nullptr, 2LL * d, R, d, d);
-      gg.vec = Ht + (size_t)t * d;
-      gg.vec_ld = (long long)p.n_pos * d;
-      gg.row_req = row_req + h0;
-      GR_TRY(dense_split(p, gg, wt->wg, Uh + d, Ul + d, R, EPI_MULVEC_SPLIT, st, Uh, Ul));
-      GR_TRY(dense_split(p, plain_gemm(nullptr, 2LL * d, w->fuse_Wf, d, Hs, d, R, d, 2 * d), wt->wf,
-                         Uh, Ul, R, EPI_STORE, st));
-    } else if (K > 0) {
-      GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, nullptr, U, nullptr, st));
-      GemmArgs gg = plain_gemm(U + d, 2LL * d, w->fuse_Wg, d, U, 2LL * d, R, d, d);
-      gg.vec = Ht + (size_t)t * d;
-      gg.vec_ld = (long long)p.n_pos * d;
-      gg.row_req = row_req + h0;
-      GR_TRY(dense(p, gg, wt ? wt->wg : nullptr, R, EPI_MULVEC, st));
-      GR_TRY(dense(p, plain_gemm(U, 2LL * d, w->fuse_Wf, d, Hs, d, R, d, 2 * d),
-                   wt ? wt->wf : nullptr, R, EPI_STORE, st));
-    } else {
-      GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, w->pos + (size_t)t * d, nullptr,
-                         Hs, st));
-    }
-    // head layers K..L-1 against the shared context KV (beam.py:243-255)
-    RowSet rs{};
-    rs.rows = R;
-    rs.max_group_rows = p.maxcap[t];
-    rs.g_row_off = row_off + (size_t)t * B;
-    rs.g_rows = cap + (size_t)t * B;
-    rs.row_req = row_req + h0;
-    rs.hist_row0 = h0;
-    rs.anc = anc;
-    rs.anc_stride = p.stride;
-    rs.npos_u = t + 1;
-    rs.npos_row = nullptr;
-    bool h_split = false;  // the last layer left Hs as fp16 hi / lo in N
-    for (int i = K; i < p.L; ++i) {
-      rs.qkv = hist + (size_t)(i - K) * hist_layer;
-      GR_TRY(layer_forward(p, w, wt, i, Hs, rs, ws, KV, VT, st,
-                           (i == p.L - 1 && t < T) ? &h_split : nullptr));
-    }
-    if (t == T) {  // value re-rank step (beam.py:258-288)
-      float *vlog = at<float>(ws, p.o_vlog);
-      GR_TRY(dense(p, plain_gemm(Hs, d, w->head_value, p.nb, vlog, p.nb, R, p.nb, d),
-                   wt ? wt->hv : nullptr, R, EPI_STORE, st));
-      break;
-    }
-    // codebook projection + log-softmax + score accumulation + top-k (beam.py:198-210)
-    const int V = p.V[t];
-    const GemmArgs lg = plain_gemm(Hs, d, w->head[t], V, LG, V, R, V, d);
-    const float4 *proxies = nullptr;
-    if (p.tc && wt && d % 8 == 0 && tc_eligible(d, d, d, Hs, wt->head[t])) {
-      // log-sum-exp partials from the GEMM epilogue (no second pass over the logits)
-      TcArgs tl{};
-      static_cast<GemmArgs &>(tl) = lg;
-      tl.b_hi = wt->head[t];
-      tl.b_lo = wt->head[t] + p.wt_floats;
-      tl.ldb = d;
-      tl.alpha = lg.alpha / kWeightScale;
-      tl.lse_part = at<float4>(ws, p.o_lsep);
-      tl.lse_ld = (V + 127) / 128;
-      if (h_split) {
-        tl.a_hi = at<__half>(ws, p.o_N);
-        tl.a_lo = tl.a_hi + (size_t)p.Rw * d;
-      }
-      GR_TRY(gemm_tc(tl, R, d, V, d, EPI_STORE_LSE, st));
-      GR_TRY(lse_merge(tl.lse_part, tl.lse_ld, R, rinfo, st));
-      if (!bt->valid_prefix[t] && !no_proxy_window()) proxies = tl.lse_part;
-    } else {
-      GR_TRY(dense(p, lg, wt ? wt->head[t] : nullptr, R, EPI_STORE, st));
-      GR_TRY(row_lse(LG, V, R, V, rinfo, st));
-    }
-    if (bt->valid_prefix[t]) {
-      GR_TRY(mask_rows(LG, V, R, V, prefix + h0,
-                       reinterpret_cast<const long long *>(bt->valid_prefix[t]),
-                       bt->valid_prefix_count[t], st));
-    }
-    SelectArgs sa{};
-    sa.logits = LG; sa.ld = V; sa.V = V; sa.level = t;
-    sa.rowinfo = rinfo; sa.cum = cum;
-    sa.proxies = proxies; sa.proxy_ld = (V + 127) / 128;
-    sa.row_off = row_off + (size_t)t * B;
-    sa.live = live + (size_t)t * B;
-    sa.eff = eff + (size_t)t * B;
-    sa.hist_off = (int)h0;
-    sa.out_row_off = row_off + (size_t)(t + 1) * B;
-    sa.out_cap = cap + (size_t)(t + 1) * B;
-    sa.out_live = live + (size_t)(t + 1) * B;
-    sa.out_hist_off = (int)p.hist_off[t + 1];
-    sa.tok = tok; sa.cum_out = cum; sa.prefix = prefix; sa.anc = anc;
-    sa.anc_stride = p.stride;
-    GR_TRY(topk_select(sa, B, 0, 0, p.max_cand[t], st));
-  }
-  GR_TRY(collect_results(B, T, row_off + (size_t)T * B, live + (size_t)T * B,
-                         (int)p.hist_off[T], tok, anc, p.stride, cum,
-                         p.rerank ? at<float>(ws, p.o_vlog) : nullptr, p.nb, bt->value_reps,
-                         out->max_out, out->count, out->tokens, out->score, st));
-  return GR4AD_OK;
+  for (int t = 0; t <= last; ++t) GR_TRY(layered_level(p, w, bt, t, ws, wt, VT, st));
+  return layered_end(p, bt, out, ws, st);
 }
 
 }  // namespace gr
@@ -1199,6 +1223,7 @@ const char *gr4ad_status_string(int s) {
     case GR4AD_ERR_UNSUPPORTED: return "unsupported shape";
     case GR4AD_ERR_WORKSPACE: return "workspace too small";
     case GR4AD_ERR_CUDA: return "CUDA error";
+    case GR4AD_ERR_RANGE: return "fp16 split range exceeded";
     default: return "unknown status";
   }
 }
@@ -1243,6 +1268,70 @@ int gr4ad_beam_search_run(const gr4ad_dims *dims, const gr4ad_weights *w,
   return run_plan(p, dims, w, batch, features, context, out, workspace, (cudaStream_t)stream);
 }
 
+// per-level entry points: the layered decode in three parts
+static int split_plan(const gr4ad_dims *dims, const gr4ad_batch *batch, size_t workspace_bytes,
+                      Plan &p) {
+  GR_TRY(make_plan(dims, batch, p));
+  if (workspace_bytes < p.total)
+    return set_err(GR4AD_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, p.total);
+  if (p.fused)
+    return set_err(GR4AD_ERR_UNSUPPORTED,
+                   "the per-level entry points run the layered path: set decode_path 1 or 3");
+  if (p.rerank && !batch->value_reps)
+    return set_err(GR4AD_ERR_VALUE, "value_rerank requires bucket representatives");
+  return GR4AD_OK;
+}
+
+int gr4ad_encode_trunk(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4ad_batch *batch,
+                       const float *features, const float *context, void *workspace,
+                       size_t workspace_bytes, void *stream) {
+  Plan p;
+  GR_TRY(split_plan(dims, batch, workspace_bytes, p));
+  if (p.B == 0) return GR4AD_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  GR_CUDA(cudaMemsetAsync(at<int>(workspace, p.o_flag), 0, sizeof(int), st));
+  WeightsT wt_store;
+  const WeightsT *wt = nullptr;
+  float *VT = nullptr;
+  return layered_begin(p, w, features, context, workspace, wt_store, wt, VT, st);
+}
+
+int gr4ad_level_step(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4ad_batch *batch,
+                     int level, void *workspace, size_t workspace_bytes, void *stream) {
+  Plan p;
+  GR_TRY(split_plan(dims, batch, workspace_bytes, p));
+  if (level < 0 || level > p.T || (level == p.T && !p.rerank))
+    return set_err(GR4AD_ERR_VALUE, "level %d outside [0, %d)", level, p.T + (p.rerank ? 1 : 0));
+  if (p.B == 0) return GR4AD_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  WeightsT wt_store;
+  const WeightsT *wt = nullptr;
+  float *VT = nullptr;
+  if (p.tc) {  // the derived weight copies: pointers only (built by encode_trunk / prepare)
+    GR_TRY(prep_weights_t(p, w, workspace, wt_store, st, false));
+    wt = &wt_store;
+    VT = at<float>(workspace, p.o_VT);
+  }
+  return layered_level(p, w, batch, level, workspace, wt, VT, st);
+}
+
+int gr4ad_collect(const gr4ad_dims *dims, const gr4ad_batch *batch, gr4ad_results *out,
+                  void *workspace, size_t workspace_bytes, void *stream) {
+  Plan p;
+  GR_TRY(split_plan(dims, batch, workspace_bytes, p));
+  if (!out || out->max_out < p.max_out)
+    return set_err(GR4AD_ERR_VALUE, "results.max_out < %d", p.max_out);
+  if (p.B == 0) return GR4AD_OK;
+  return layered_end(p, batch, out, workspace, (cudaStream_t)stream);
+}
+
+int gr4ad_range_flag_offset(const gr4ad_dims *dims, const gr4ad_batch *batch, size_t *offset) {
+  Plan p;
+  GR_TRY(make_plan(dims, batch, p));
+  if (offset) *offset = p.o_flag;
+  return GR4AD_OK;
+}
+
 int gr4ad_prepare_weights(const gr4ad_dims *dims, const gr4ad_weights *w,
                           const gr4ad_batch *batch, void *workspace, size_t workspace_bytes,
                           void *stream) {
@@ -1274,7 +1363,7 @@ int gr4ad_prepare_weights(const gr4ad_dims *dims, const gr4ad_weights *w,
   GR_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   GR_CUDA(cudaStreamSynchronize(st));
   if (h)
-    return set_err(GR4AD_ERR_UNSUPPORTED,
+    return set_err(GR4AD_ERR_RANGE,
                    "a weight exceeded the fp16 split range (|weight| < 32): decode with the "
                    "CUDA-core path (decode_path layered / fused_simt)");
   return GR4AD_OK;
@@ -1291,7 +1380,7 @@ int gr4ad_range_status(const gr4ad_dims *dims, const gr4ad_batch *batch, const v
                           cudaMemcpyDeviceToHost, st));
   GR_CUDA(cudaStreamSynchronize(st));
   if (flag)
-    return set_err(GR4AD_ERR_UNSUPPORTED,
+    return set_err(GR4AD_ERR_RANGE,
                    "an operand exceeded the fp16 split range (|weight| < 32, |context K/V| < 256): "
                    "decode with the CUDA-core path (decode_path layered / fused_simt)");
   return GR4AD_OK;
@@ -1460,7 +1549,7 @@ int gr4ad_score_sequences(const gr4ad_dims *dims, const gr4ad_weights *w, const 
     GR_CUDA(cudaMemcpyAsync(&flag, at<int>(ws, p.o_flag), sizeof(int), cudaMemcpyDeviceToHost, st));
     GR_CUDA(cudaStreamSynchronize(st));
     if (flag)
-      return set_err(GR4AD_ERR_UNSUPPORTED,
+      return set_err(GR4AD_ERR_RANGE,
                      "an operand exceeded the fp16 split range (|weight| < 32, |context K/V| < "
                      "256): score with the CUDA-core path");
   }

@@ -12,12 +12,16 @@ it can be captured once into a CUDA graph and replayed per batch.
 from __future__ import annotations
 
 import ctypes as C
+import gc
+import threading
+from collections import OrderedDict
 
 import numpy as np
 import torch
 
 from . import _native as N
 from .device import _stream_handle, device_weights, dims_of, require_cuda
+from .quantizer.residual import check_token_range, sid_type
 
 
 def effective_widths(widths, vocab_sizes):
@@ -117,8 +121,20 @@ class BeamDecoder:
                                     C.c_void_p(self.workspace.data_ptr()),
                                     self.workspace_bytes, _stream_handle(self.device)))
         self._prepare_weights()
+        off = C.c_size_t()
+        N.check(N.lib.gr4ad_range_flag_offset(C.byref(self.dims), C.byref(bt), C.byref(off)))
+        self._flag = self.workspace[off.value:off.value + 4].view(torch.int32)
         self.graph = None
         self._graph_inputs = None
+        self.host_graph = None
+        self._host_out = None
+        self._fetched = None
+        self.in_buf = None
+        self._in_host = None
+        self.uses = 0
+        self.item_idx = None
+        self._resolved = False
+        self.last_item_idx = None
 
     def _prepare_weights(self):
         """Derived weight copies (mma fragments / K-major fp16 splits) built
@@ -138,8 +154,11 @@ class BeamDecoder:
             raise ValueError("rebind needs a snapshot with the same DecoderConfig")
         self.weights = device_weights(model, self.device)
         self._prepare_weights()
+        # every captured graph holds the previous snapshot's weight pointers
         self.graph = None
         self._graph_inputs = None
+        self.host_graph = None
+        self._host_in = self._dev_in = self.host_out = None
 
     # -- launch ----------------------------------------------------------
     def run(self, features=None, context=None):
@@ -197,6 +216,8 @@ class BeamDecoder:
         return g
 
     def replay_host(self):
+        if self.host_graph is None:
+            raise RuntimeError("no host graph: capture_host() again (rebind drops it)")
         self.host_graph.replay()
 
     # -- results -----------------------------------------------------------
@@ -207,13 +228,192 @@ class BeamDecoder:
                                          C.c_void_p(self.workspace.data_ptr()),
                                          _stream_handle(self.device)))
 
-    def host_results(self):
-        self.check_range()
-        count = self.count.cpu().numpy()[: self.n_requests]
-        toks = self.tokens.cpu().numpy().reshape(-1, self.max_out, self.T)
-        score = self.score.cpu().numpy().reshape(-1, self.max_out)
-        return [[(tuple(int(v) for v in toks[b, j]), float(score[b, j]))
-                 for j in range(int(count[b]))] for b in range(self.n_requests)]
+    def resolve_items(self, keys, ids, n_keys):
+        """On-device SID -> item slot for every result of the last decode
+        (gr4ad_resolve_items; -1 = SID not in the index).  ``keys`` / ``ids``:
+        device int64 sorted SID keys and int32 item slots.  Fetched with the
+        results into ``last_item_idx``."""
+        if self.item_idx is None:
+            self.item_idx = torch.empty(max(self.n_requests, 1) * self.max_out,
+                                        dtype=torch.int32, device=self.device)
+        N.check(N.lib.gr4ad_resolve_items(
+            C.c_void_p(keys.data_ptr()), C.c_void_p(ids.data_ptr()), int(n_keys),
+            C.byref(self.dims), C.byref(self.results_struct), self.n_requests,
+            C.c_void_p(self.item_idx.data_ptr()), _stream_handle(self.device)))
+        self._resolved = True
+
+    def fetch_async(self):
+        """Start the D2H copies of this decode's results and fp16 range flag
+        (and resolved item slots) into pinned buffers on the current stream;
+        :meth:`results` reads them after the event."""
+        srcs = [self.count, self.tokens, self.score, self._flag]
+        if self._resolved:
+            srcs.append(self.item_idx)
+        if self._host_out is None or len(self._host_out) != len(srcs):
+            self._host_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in srcs]
+        for h, t in zip(self._host_out, srcs):
+            h.copy_(t, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._fetched = ev
+        return ev
+
+    def results(self):
+        """[(tokens, score)] lists per request from the fetched buffers; the
+        token rows are SemanticIds when ``sids`` (one vectorised range check,
+        C-level construction, no per-token Python validation)."""
+        if self._fetched is None:
+            self.fetch_async()
+        self._fetched.synchronize()
+        self._fetched = None
+        host = [t.numpy() for t in self._host_out]
+        count, toks, score, flag = host[:4]
+        self.last_item_idx = (host[4].reshape(-1, self.max_out)[: self.n_requests]
+                              if self._resolved else None)
+        self._resolved = False
+        if int(flag[0]):
+            raise N.RangeError(
+                "libgr4ad: fp16 split range exceeded: an operand exceeded the fp16 split range "
+                "(|weight| < 32, |context K/V| < 256): decode with the CUDA-core path "
+                "(path='layered')")
+        return materialize(count[: self.n_requests], toks, score, self.max_out, self.T,
+                           self.cfg.level_vocab_sizes)
+
+    def host_results(self, sids=False):
+        """Blocking fetch of the last decode's results: per request a list
+        of (token tuple | SemanticId, score)."""
+        self.fetch_async()
+        return self.results() if sids else [
+            [(tuple(s), v) for s, v in req] for req in self.results()]
+
+
+def materialize(count, toks, score, max_out, T, vocab):
+    """Per-request [(SemanticId, float)] from host result arrays (count (B,),
+    tokens (B*max_out*T,), score (B*max_out,)); entries past count[b] are
+    ignored.  One vectorised range check replaces SemanticId's per-token
+    validation (the tokens come from the device, bounded by construction);
+    the cyclic GC is paused while the result objects are built."""
+    B = int(count.shape[0])
+    toks = toks.reshape(-1, max_out, T)[:B]
+    score = score.reshape(-1, max_out)[:B]
+    n = count.astype(np.int64)
+    m = int(n.max()) if B else 0
+    if m:
+        live = np.arange(m)[None, :] < n[:, None]
+        check_token_range(toks[:, :m][live], vocab)
+    cls = sid_type(vocab)
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        tl = toks[:, :m].tolist()
+        sl = score[:, :m].tolist()
+        return [list(zip(map(cls, tl[b][:k]), sl[b][:k])) for b, k in enumerate(n.tolist())]
+    finally:
+        if was:
+            gc.enable()
+
+
+class DecoderPool:
+    """Idle BeamDecoders (workspace, plan, derived weight copies and a CUDA
+    graph each) kept per batch shape, so repeated drop-in calls --
+    ``beam_search_batch``, ``ServingEngine.serve_batch`` -- replay one graph
+    instead of re-planning, re-allocating and re-splitting the weights.  A
+    decoder is exclusively checked out while a call uses it (concurrent
+    callers of the same shape get separate decoders); LRU-bounded by total
+    workspace bytes."""
+
+    def __init__(self, max_bytes=48 << 30, max_decoders=32):
+        self._lock = threading.Lock()
+        self._idle = OrderedDict()
+        self.max_bytes = max_bytes
+        self.max_decoders = max_decoders
+
+    def acquire(self, key, factory):
+        with self._lock:
+            lst = self._idle.get(key)
+            if lst:
+                dec = lst.pop()
+                if not lst:
+                    del self._idle[key]
+                return dec
+        return factory()
+
+    def release(self, key, dec):
+        with self._lock:
+            self._idle.setdefault(key, []).append(dec)
+            self._idle.move_to_end(key)
+            while True:
+                n = sum(len(v) for v in self._idle.values())
+                nbytes = sum(d.workspace_bytes for v in self._idle.values() for d in v)
+                if n <= self.max_decoders and nbytes <= self.max_bytes:
+                    break
+                k0 = next(iter(self._idle))
+                self._idle[k0].pop(0)
+                if not self._idle[k0]:
+                    del self._idle[k0]
+
+    def clear(self):
+        with self._lock:
+            self._idle.clear()
+
+    def __len__(self):
+        with self._lock:
+            return sum(len(v) for v in self._idle.values())
+
+
+POOL = DecoderPool()
+
+
+def decode_cached(key, factory, model, host_input, kind, items=None):
+    """One decode through a pooled BeamDecoder: host input (a float32 numpy
+    array, features or context rows; or a CUDA tensor) -> pinned staging ->
+    H2D into the decoder's static input buffer -> decode (graph replay from
+    the second use of a shape on) -> [on-device SID -> item resolution when
+    ``items`` = (keys, ids, n)] -> async D2H of results + range flag -> host
+    lists.  Returns (per-request [(SemanticId, float)], item slots (B,
+    max_out) int32 array or None)."""
+    dec = POOL.acquire(key, factory)
+    ok = False
+    try:
+        if dec.weights is not device_weights(model, dec.device):
+            dec.rebind(model)  # a republished snapshot of the same shape
+        shape = tuple(host_input.shape)
+        if dec.in_buf is None or tuple(dec.in_buf.shape) != shape:
+            dec.in_buf = torch.empty(shape, dtype=torch.float32, device=dec.device)
+            dec._in_host = None
+            dec.graph = None
+        if isinstance(host_input, torch.Tensor):  # already on the device
+            dec.in_buf.copy_(host_input)
+        else:
+            if dec._in_host is None:
+                dec._in_host = torch.empty(shape, dtype=torch.float32).pin_memory()
+            np.copyto(dec._in_host.numpy(), host_input, casting="same_kind")
+            dec.in_buf.copy_(dec._in_host, non_blocking=True)
+        inputs = {kind: dec.in_buf}
+        if dec.graph is not None:
+            dec.graph.replay()
+        elif dec.uses >= 1:
+            # second use of this shape: capture once, replay from now on
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(dec.device)
+            s.wait_stream(torch.cuda.current_stream(dec.device))
+            with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+                dec.run(**inputs)
+            torch.cuda.current_stream(dec.device).wait_stream(s)
+            dec.graph = g
+            g.replay()
+        else:
+            dec.run(**inputs)
+        dec.uses += 1
+        if items is not None:
+            dec.resolve_items(*items)
+        dec.fetch_async()
+        out = dec.results()
+        ok = True
+        return out, dec.last_item_idx
+    finally:
+        if ok:
+            POOL.release(key, dec)
 
 
 def score_sequences(model, seq_requests, tokens, features=None, contexts=None,

@@ -153,9 +153,25 @@ def _fingerprint(params):
     return tuple(fp)
 
 
+def _freeze(params, frozen=True):
+    """Mark the host parameter arrays read-only while a device copy of them
+    is resident, so an in-place edit (``params[k].data[i] = ...``) raises
+    instead of silently decoding with stale GPU weights; replacing an array
+    (``params[k].data = new``) re-uploads.  :func:`invalidate` lifts it."""
+    for v in params.values():
+        a = getattr(v, "data", v)
+        if isinstance(a, np.ndarray):
+            try:
+                a.flags.writeable = not frozen
+            except ValueError:  # a view of a read-only base: stays as it is
+                pass
+
+
 def device_weights(model, device=None):
-    """Resident weights for ``model`` (re-uploaded only when its parameter
-    arrays change)."""
+    """Resident weights for ``model``: uploaded once and reused while the
+    parameter arrays are the same objects (their identity is the key; the
+    arrays are made read-only while resident -- call :func:`invalidate`
+    before editing them in place)."""
     device = require_cuda(device)
     key = (id(model.params), str(device))
     fp = _fingerprint(model.params)
@@ -173,20 +189,30 @@ def register(model, dw):
     """Make ``dw`` the resident copy of ``model`` (used by snapshot publish
     to pre-stage weights before the first decode asks for them)."""
     key = (id(model.params), str(dw.device))
+    _freeze(model.params)
     with _CACHE_LOCK:
         _CACHE[key] = (_fingerprint(model.params), model.params, dw)
         _CACHE.move_to_end(key)
         while len(_CACHE) > _CACHE_MAX:
-            _CACHE.popitem(last=False)
+            _, (_, params, _) = _CACHE.popitem(last=False)
+            if not any(p is params for _, p, _ in _CACHE.values()):
+                _freeze(params, False)
 
 
 def invalidate(model=None):
+    """Drop resident copies (of ``model``, or all) and make their host
+    arrays writeable again; the next decode re-uploads."""
     with _CACHE_LOCK:
         if model is None:
+            for _, params, _ in _CACHE.values():
+                _freeze(params, False)
             _CACHE.clear()
         else:
             for k in [k for k in _CACHE if k[0] == id(model.params)]:
                 del _CACHE[k]
+            _freeze(model.params, False)
+    from .decode import POOL
+    POOL.clear()
 
 
 class DeviceContext:

@@ -19,43 +19,58 @@ reference's (-score, beam slot, token).
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 
 import numpy as np
 import torch
 
 from .. import _native as N
-from ..decode import BeamDecoder, effective_widths, live_rows
+from ..decode import BeamDecoder, decode_cached, effective_widths, live_rows
 from ..device import (DeviceContext, _stream_handle, device_weights, dims_of,
                       require_cuda)
 from ..model.decoder import param_array
-from ..quantizer.residual import SemanticId
 
 
-def _context_rows(context):
-    """Device fp32 (S, d) tensor for a DeviceContext / Tensor / ndarray,
-    validated like beam.py:124-128."""
+def _finite_rows(arr, d):
+    """Validation of beam.py:124-128 plus the width check the reference gets
+    from its matmul (a context must be the projected X, (S, d))."""
+    if arr.size == 0 if isinstance(arr, np.ndarray) else arr.numel() == 0:
+        raise ValueError("empty context")
+    if arr.shape[-1] != d:
+        raise ValueError(f"context has {arr.shape[-1]} columns, expected d={d} (the projected "
+                         "X; raw features go through context_process or features=)")
+    ok = np.isfinite(arr).all() if isinstance(arr, np.ndarray) else bool(torch.isfinite(arr).all())
+    if not ok:
+        raise ValueError("context must be finite")
+
+
+def _context_input(context, d):
+    """A validated (S, d) context: float32 host ndarray, or the fp32 CUDA
+    tensor for a DeviceContext / CUDA Tensor (no host round trip)."""
     if isinstance(context, DeviceContext):
         x = context.tensor
-        if x.numel() == 0:
-            raise ValueError("empty context")
-        if not bool(torch.isfinite(x).all()):
-            raise ValueError("context must be finite")
-        return x if x.dim() == 2 else x.reshape(-1, x.shape[-1])
+        x = x if x.dim() == 2 else x.reshape(-1, x.shape[-1])
+        _finite_rows(x, d)
+        return x
     data = getattr(context, "data", context)
     if isinstance(data, torch.Tensor):
         arr = data.detach()
-        if arr.numel() == 0:
-            raise ValueError("empty context")
-        if not bool(torch.isfinite(arr).all()):
-            raise ValueError("context must be finite")
         arr = arr.reshape(-1, arr.shape[-1]) if arr.dim() != 2 else arr
-        return arr.to(device=require_cuda(), dtype=torch.float32).contiguous()
+        _finite_rows(arr, d)
+        if arr.is_cuda:
+            return arr.to(dtype=torch.float32).contiguous()
+        data = arr.numpy()
     arr = np.atleast_2d(np.asarray(data, dtype=np.float64))
-    if arr.size == 0:
-        raise ValueError("empty context")
-    if not np.isfinite(arr).all():
-        raise ValueError("context must be finite")
-    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to(require_cuda())
+    if arr.ndim != 2:
+        arr = arr.reshape(-1, arr.shape[-1])
+    _finite_rows(arr, d)
+    return np.ascontiguousarray(arr, dtype=np.float32)
+
+
+def _context_rows(context, d=None):
+    """Device fp32 (S, d) tensor of a context (shared_encoder_kv)."""
+    x = _context_input(context, d if d is not None else np.shape(getattr(context, "data", context))[-1])
+    return x if isinstance(x, torch.Tensor) else torch.from_numpy(x).to(require_cuda())
 
 
 def _check_schedule(cfg, widths):
@@ -99,8 +114,39 @@ def record_counter(counter, cfg, widths, s_ctx, shared_kv, value_rerank, k_depth
             counter.add_layer_calls(live[T])
 
 
-def _to_sids(rows, vocab):
-    return [(SemanticId(toks, vocab), score) for toks, score in rows]
+def _valid_key(valid_sids):
+    """Content digest of a valid-SID set (part of the pooled decoder's key:
+    the decoder holds the set's device prefix tables)."""
+    if valid_sids is None:
+        return None
+    toks = np.asarray([tuple(getattr(v, "tokens", v)) for v in valid_sids], dtype=np.int64)
+    return (toks.shape, hashlib.sha1(toks.tobytes()).hexdigest())
+
+
+def _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path, inp, kind,
+            items=None):
+    """Pooled decode with the automatic fp16-range fallback: with
+    path="auto", a batch whose weights or context K/V leave the fp16 split
+    range of the tensor-core paths is decoded again on the fp32 CUDA-core
+    path (another GPU path -- there is no CPU fallback)."""
+    dev = inp.device if isinstance(inp, torch.Tensor) else require_cuda()
+    reps_key = None if reps is None else tuple(np.asarray(reps, dtype=np.float64).ravel().tolist())
+    vkey = _valid_key(valid_sids)
+
+    def attempt(p):
+        key = (id(model.params), str(dev), kind, tuple(lens), tuple(per), k_depth,
+               bool(value_rerank), reps_key, vkey, p)
+        factory = lambda: BeamDecoder(model, lens, per, trunk_depth=k_depth,
+                                      value_rerank=value_rerank, representatives=reps,
+                                      valid_sids=valid_sids, device=dev, path=p)
+        return decode_cached(key, factory, model, inp, kind, items)
+
+    try:
+        return attempt(path)
+    except N.RangeError:
+        if path != "auto":
+            raise
+        return attempt("layered")
 
 
 def beam_search(model, context, schedule, shared_kv=True, precut=True, counter=None,
@@ -112,7 +158,7 @@ def beam_search(model, context, schedule, shared_kv=True, precut=True, counter=N
     ``valid_sids`` (extension) restricts expansion to
     prefixes of the given SIDs."""
     cfg = model.config
-    x = _context_rows(context)
+    x = _context_input(context, cfg.d)
     widths = tuple(int(w) for w in schedule.widths)
     _check_schedule(cfg, widths)
     k_depth = _check_depth(cfg, trunk_depth)
@@ -121,31 +167,33 @@ def beam_search(model, context, schedule, shared_kv=True, precut=True, counter=N
         if buckets is None:
             raise ValueError("value_rerank requires buckets")
         reps = getattr(buckets, "representatives", buckets)
-    dec = BeamDecoder(model, [x.shape[0]], [widths], trunk_depth=k_depth,
-                      value_rerank=value_rerank, representatives=reps,
-                      valid_sids=valid_sids, device=x.device)
-    dec.run(context=x)
-    rows = dec.host_results()[0]
+    out = _decode(model, [x.shape[0]], [widths], k_depth, value_rerank, reps, valid_sids, "auto",
+                  x, "context")[0][0]
     record_counter(counter, cfg, widths, x.shape[0], shared_kv, value_rerank, k_depth)
-    return _to_sids(rows, tuple(cfg.level_vocab_sizes))
+    return out
 
 
 def beam_search_batch(model, contexts=None, schedules=None, features=None, shared_kv=True,
                       precut=True, counter=None, value_rerank=False, buckets=None,
-                      trunk_depth=None, valid_sids=None, path="auto"):
+                      trunk_depth=None, valid_sids=None, path="auto", _items=None):
     """Batched ``beam_search``: one result list per request.
 
     ``path`` picks the decode kernels: "auto" (the fused per-request kernel
     when the working set fits on chip, else the layered batch path with
-    tcgen05 3xFP16 GEMMs for d >= 64, else CUDA-core GEMMs), "fused",
-    "tensor" (layered + tcgen05) or "layered" (layered + CUDA-core).
+    tcgen05 3xFP16 GEMMs for d >= 64, else CUDA-core GEMMs; a batch that
+    leaves the fp16 split range is re-decoded on the CUDA-core path),
+    "fused", "tensor" (layered + tcgen05) or "layered" (layered + CUDA-core).
 
     ``contexts`` are projected X matrices, or ``features`` raw (S, F)
     feature matrices (the context projection then runs on the GPU, as the
     engine does, engine.py:104-105).  ``schedules`` is one BeamSchedule (or
-    width tuple) for all requests or one per request (TABS widths)."""
+    width tuple) for all requests or one per request (TABS widths).
+
+    Repeated calls with the same batch shape reuse one pooled decoder and
+    replay its CUDA graph (``decode.POOL``): inputs go host -> pinned ->
+    device, results come back as one async copy, and the SemanticIds are
+    built in bulk."""
     cfg = model.config
-    dev = require_cuda()
     if (contexts is None) == (features is None):
         raise ValueError("pass exactly one of contexts / features")
     items = contexts if contexts is not None else features
@@ -161,13 +209,20 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
     for w in per:
         _check_schedule(cfg, w)
     k_depth = _check_depth(cfg, trunk_depth)
+    if B == 0:
+        return []
     if contexts is not None:
-        rows = [_context_rows(c) for c in contexts]
+        rows = [_context_input(c, cfg.d) for c in contexts]
         lens = [r.shape[0] for r in rows]
-        x = torch.cat(rows, 0) if B else None
-        f = None
+        if all(isinstance(r, np.ndarray) for r in rows):
+            inp = np.concatenate(rows, 0)
+        else:
+            dev = next(r.device for r in rows if isinstance(r, torch.Tensor))
+            inp = torch.cat([r if isinstance(r, torch.Tensor) else torch.from_numpy(r).to(dev)
+                             for r in rows], 0)
+        kind = "context"
     else:
-        arrs = [np.atleast_2d(np.asarray(getattr(a, "data", a), dtype=np.float64)) for a in features]
+        arrs = [np.atleast_2d(np.asarray(getattr(a, "data", a))) for a in features]
         for a in arrs:
             if a.size == 0:
                 raise ValueError("empty context")
@@ -176,26 +231,28 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
             if not np.isfinite(a).all():
                 raise ValueError("context must be finite")
         lens = [a.shape[0] for a in arrs]
-        f = torch.from_numpy(np.concatenate(arrs, 0).astype(np.float32)).to(dev) if B else None
-        x = None
-    if B == 0:
-        return []
+        with np.errstate(over="ignore"):
+            inp = np.concatenate(arrs, 0).astype(np.float32, copy=False)
+        if not np.isfinite(inp).all():
+            raise RuntimeError("a feature exceeds the fp32 range of the GPU decode")
+        kind = "features"
     reps = None
     if value_rerank:
         if buckets is None:
             raise ValueError("value_rerank requires buckets")
         reps = getattr(buckets, "representatives", buckets)
-    dec = BeamDecoder(model, lens, per, trunk_depth=k_depth, value_rerank=value_rerank,
-                      representatives=reps, valid_sids=valid_sids, device=dev, path=path)
-    dec.run(features=f, context=x)
-    out = dec.host_results()
-    vocab = tuple(cfg.level_vocab_sizes)
-    for b in range(B):
-        record_counter(counter, cfg, per[b], lens[b], shared_kv, value_rerank, k_depth)
-    return [_to_sids(r, vocab) for r in out]
+    out, item_idx = _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path,
+                            inp, kind, _items)
+    if counter is not None:
+        for b in range(B):
+            record_counter(counter, cfg, per[b], lens[b], shared_kv, value_rerank, k_depth)
+    return (out, item_idx) if _items is not None else out
 
 
 def _select_gpu(beam_scores, logprobs, k):
+    """Exact float64 selection on the GPU (gr4ad_topk_precut_f64): the
+    candidate scores are the reference's own double sums, ranked with no
+    rounding, so the order is the reference's bit for bit."""
     dev = require_cuda()
     s = np.asarray(beam_scores, dtype=np.float64).ravel()
     lp = np.atleast_2d(np.asarray(logprobs, dtype=np.float64))
@@ -206,20 +263,17 @@ def _select_gpu(beam_scores, logprobs, k):
     if k < 1 or b * v == 0:
         return np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0)
     kk = min(k, b * v)
-    st = torch.from_numpy(s.astype(np.float32)).to(dev)
-    lt = torch.from_numpy(np.ascontiguousarray(lp, dtype=np.float32)).to(dev)
+    st = torch.from_numpy(s).to(dev)
+    lt = torch.from_numpy(np.ascontiguousarray(lp)).to(dev)
     ob = torch.empty(kk, dtype=torch.int32, device=dev)
     ot = torch.empty(kk, dtype=torch.int32, device=dev)
-    osc = torch.empty(kk, dtype=torch.float32, device=dev)
+    osc = torch.empty(kk, dtype=torch.float64, device=dev)
     oc = torch.empty(1, dtype=torch.int32, device=dev)
-    ws = torch.empty(256, dtype=torch.uint8, device=dev)
     ptr = lambda t: C.c_void_p(t.data_ptr())
-    N.check(N.lib.gr4ad_topk_precut(ptr(st), ptr(lt), 1, b, v, kk, ptr(ob), ptr(ot), ptr(osc),
-                                    ptr(oc), ptr(ws), 256, _stream_handle(dev)))
-    # scores are re-added in float64 on the host from the reference's inputs
-    beams = ob.cpu().numpy().astype(np.int64)
-    toks = ot.cpu().numpy().astype(np.int64)
-    return beams, toks, s[beams] + lp[beams, toks]
+    N.check(N.lib.gr4ad_topk_precut_f64(ptr(st), ptr(lt), 1, b, v, kk, ptr(ob), ptr(ot),
+                                        ptr(osc), ptr(oc), _stream_handle(dev)))
+    return (ob.cpu().numpy().astype(np.int64), ot.cpu().numpy().astype(np.int64),
+            osc.cpu().numpy())
 
 
 def topk_precut(prev_beams, level_logprobs, k):
@@ -240,7 +294,7 @@ def shared_encoder_kv(model, context, trunk_depth=None):
     (beam.py:98-109): {layer: (keys, values)} as float64 host arrays; the
     decode itself keeps them resident on the GPU."""
     cfg = model.config
-    x = _context_rows(context)
+    x = _context_rows(context, cfg.d)
     k = cfg.trunk_depth if trunk_depth is None else trunk_depth
     L, d = cfg.n_layers, cfg.d
     if k >= L:

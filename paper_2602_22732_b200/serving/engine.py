@@ -12,6 +12,7 @@ compaction all on the device.
 from __future__ import annotations
 
 import threading
+import time
 from concurrent.futures import Future
 from dataclasses import dataclass
 
@@ -19,7 +20,7 @@ import numpy as np
 import torch
 
 from ..model.layers import LayerCallCounter
-from .beam import beam_search_batch
+from .beam import beam_search_batch, record_counter
 from .cache import TtlCache
 from .schedule import TrafficSignal, scale_schedule, tabs_adjust
 
@@ -113,8 +114,111 @@ class ServeResult:
                 "widths": list(self.widths), "latency_virtual": self.latency_virtual}
 
 
+class LoadEstimator:
+    """Online load signal for TABS (N1): the reference's caller measures
+    traffic per tick and passes ``qps`` / ``capacity_slack`` to every
+    request (sim/loop.py:239-264 -> engine.py:100-103).  Here the engine
+    measures both itself:
+
+    * arrival rate -- requests seen in a sliding window of ``window``
+      seconds of request time (``now``), so each request's rate is the one
+      at its own arrival;
+    * capacity -- requests decoded per second of decode time, an EWMA over
+      the engine's own GPU batches (wall time around each batched decode,
+      results on the host).
+
+    ``capacity_slack = clamp(1 - rate / capacity, 0, 1)`` (the C4 sweep's
+    definition); 1.0 until a capacity has been measured."""
+
+    def __init__(self, window=1.0, alpha=0.2):
+        self.window = float(window)
+        self.alpha = float(alpha)
+        self._arrivals = []  # sorted request times inside the window
+        self._head = 0
+        self.capacity = None  # requests / s of decode time
+        self._lock = threading.Lock()
+
+    def observe(self, now, n=1):
+        with self._lock:
+            self._arrivals.extend([float(now)] * int(n))
+
+    def rate(self, now):
+        with self._lock:
+            lo = float(now) - self.window
+            arr = self._arrivals
+            h = self._head
+            while h < len(arr) and arr[h] <= lo:
+                h += 1
+            if h > 4096 and h * 2 > len(arr):
+                del arr[:h]
+                h = 0
+            self._head = h
+            upto = len(arr)
+            while upto > h and arr[upto - 1] > now:
+                upto -= 1
+            return (upto - h) / self.window
+
+    def record_service(self, n_requests, seconds):
+        if n_requests <= 0 or seconds <= 0:
+            return
+        c = n_requests / seconds
+        with self._lock:
+            self.capacity = c if self.capacity is None else (
+                (1 - self.alpha) * self.capacity + self.alpha * c)
+
+    def signal(self, now):
+        """(qps, capacity_slack) at request time ``now``."""
+        qps = self.rate(now)
+        cap = self.capacity
+        slack = 1.0 if not cap else min(1.0, max(0.0, 1.0 - qps / cap))
+        return qps, slack
+
+
+class ItemTable:
+    """Device copy of a SidIndex for on-device SID -> item resolution
+    (gr4ad_resolve_items): sorted mixed-radix SID keys (int64) and, per key,
+    the slot of min(item ids) (engine.py:114-118 takes min(ids)) in
+    ``items``.  Built once per index version."""
+
+    def __init__(self, index, vocab, device):
+        keys, items = [], []
+        for sid in index.all_sids():
+            toks = getattr(sid, "tokens", sid)
+            if len(toks) != len(vocab) or any(not 0 <= t < v for t, v in zip(toks, vocab)):
+                continue  # a SID of another vocabulary can never be decoded
+            ids = index.lookup(sid)
+            if not ids:
+                continue
+            k = 0
+            for t, v in zip(toks, vocab):
+                k = k * int(v) + int(t)
+            keys.append(k)
+            items.append(min(ids))
+        order = np.argsort(np.asarray(keys, dtype=np.int64), kind="stable")
+        self.n = len(keys)
+        k_sorted = np.asarray(keys, dtype=np.int64)[order] if keys else np.zeros(1, np.int64)
+        self.items = np.empty(max(self.n, 1), dtype=object)
+        for j, o in enumerate(order.tolist()):
+            self.items[j] = items[o]
+        self.keys = torch.from_numpy(k_sorted).to(device)
+        self.ids = torch.arange(max(self.n, 1), dtype=torch.int32, device=device)
+
+    def args(self):
+        return (self.keys, self.ids, self.n)
+
+    def resolve(self, sids, slots):
+        """[(item, score)] for one request from its SID list and slot row."""
+        n = len(sids)
+        row = slots[:n]
+        keep = np.flatnonzero(row >= 0)
+        if keep.size == 0:
+            return []
+        objs = self.items[row[keep]].tolist()
+        return [(o, float(sids[j][1])) for o, j in zip(objs, keep.tolist())]
+
+
 class ServingEngine:
-    def __init__(self, store, index, config, buckets=None, counter=None):
+    def __init__(self, store, index, config, buckets=None, counter=None, load=None):
         self.store = store
         self.index = index
         self.config = config
@@ -124,11 +228,23 @@ class ServingEngine:
         self._lock = threading.Lock()
         self.model_invocations = 0
         self.requests = 0
+        self.load = load if load is not None else LoadEstimator()
+        self._table = None  # (index version, vocab, ItemTable)
 
     def _widths(self, qps, capacity_slack):
         sig = TrafficSignal(qps, self.config.q_threshold, capacity_slack)
         active = tabs_adjust(sig, self.config.schedule.base_width, self.config.boost)
         return scale_schedule(self.config.schedule, active)
+
+    def _item_table(self, model):
+        vocab = tuple(model.config.level_vocab_sizes)
+        version = self.index.version
+        tab = self._table
+        if tab is None or tab[0] != version or tab[1] != vocab:
+            from ..device import require_cuda
+            tab = (version, vocab, ItemTable(self.index, vocab, require_cuda()))
+            self._table = tab
+        return tab[2]
 
     def _resolve(self, sids):
         items = []
@@ -138,19 +254,33 @@ class ServingEngine:
                 items.append((min(ids), float(score)))
         return items
 
-    def serve_request(self, user_id, features, now, qps, capacity_slack=1.0):
+    def serve_request(self, user_id, features, now, qps=None, capacity_slack=1.0):
         """One request: cache first; on a miss, traffic-scaled GPU beam
-        generation and ID resolution (engine.py:84-121)."""
+        generation and ID resolution (engine.py:84-121).  ``qps=None``
+        takes the engine's own measured load (:class:`LoadEstimator`)."""
         return self.serve_batch([(user_id, features)], now, qps, capacity_slack)[0]
 
-    def serve_batch(self, requests, now, qps, capacity_slack=1.0):
-        """requests: [(user_id, features)] -> [ServeResult] in order."""
+    def serve_batch(self, requests, now, qps=None, capacity_slack=1.0):
+        """requests: [(user_id, features)] or [(user_id, features, t_arrival)]
+        -> [ServeResult] in order.
+
+        All cache misses decode in ONE batched GPU call (context projection,
+        encoder K/V, trunk, level steps, compaction and SID -> item
+        resolution on the device).  Widths: with an explicit ``qps`` every
+        miss gets scale_schedule(tabs_adjust(qps, capacity_slack)) as in the
+        reference; with ``qps=None`` each request gets the widths of the
+        load the engine measured at its own arrival time (per-request TABS
+        widths inside one batch)."""
         with self._lock:
             self.requests += len(requests)
         version_key = self.index.version
         out = [None] * len(requests)
         misses = []
-        for i, (uid, feats) in enumerate(requests):
+        for i, req in enumerate(requests):
+            uid = req[0]
+            t_arr = req[2] if len(req) > 2 else now
+            if qps is None:
+                self.load.observe(t_arr)
             cached = self.cache.get((uid, version_key), now)
             if cached is not None:
                 out[i] = ServeResult(cached[0], cached[1], True, cached[2], cached[3], 0)
@@ -159,27 +289,39 @@ class ServingEngine:
         if not misses:
             return out
         version, model = self.store.current()
-        sched = self._widths(qps, capacity_slack)
+        if qps is not None:
+            scheds = [self._widths(qps, capacity_slack)] * len(misses)
+        else:
+            scheds = []
+            for i in misses:
+                t_arr = requests[i][2] if len(requests[i]) > 2 else now
+                scheds.append(self._widths(*self.load.signal(t_arr)))
         valid = self.index.all_sids() if self.config.mask_to_index else None
         feats = [np.atleast_2d(np.asarray(requests[i][1], dtype=np.float64)) for i in misses]
-        # one GPU launch for all misses; per-request latency_virtual from the
-        # closed-form counter (engine.py:106-111)
+        table = self._item_table(model)
         local = LayerCallCounter()
-        results = beam_search_batch(model, features=feats, schedules=[sched] * len(misses),
-                                    shared_kv=self.config.shared_kv, precut=self.config.precut,
-                                    counter=local, value_rerank=self.config.value_rerank,
-                                    buckets=self.buckets, valid_sids=valid)
-        per_req = local.layer_calls // max(len(misses), 1)
+        t0 = time.perf_counter()
+        results, slots = beam_search_batch(
+            model, features=feats, schedules=scheds, shared_kv=self.config.shared_kv,
+            precut=self.config.precut, counter=local, value_rerank=self.config.value_rerank,
+            buckets=self.buckets, valid_sids=valid, _items=table.args())
+        self.load.record_service(len(misses), time.perf_counter() - t0)
         self.counter.add_layer_calls(local.layer_calls)
         self.counter.add_kv_build(local.kv_builds, local.kv_floats)
         with self._lock:
             self.model_invocations += len(misses)
-        for i, sids in zip(misses, results):
+        for j, (i, sids) in enumerate(zip(misses, results)):
             uid = requests[i][0]
-            items = self._resolve(sids)
+            sched = scheds[j]
+            items = table.resolve(sids, slots[j])
             self.cache.put((uid, version_key), (items, sids, version, sched.widths), now)
+            # per-request virtual latency: the closed-form layer calls of its decode
+            c = LayerCallCounter()
+            record_counter(c, model.config, sched.widths, feats[j].shape[0],
+                           self.config.shared_kv, self.config.value_rerank,
+                           model.config.trunk_depth)
             out[i] = ServeResult(items, sids, False, version, sched.widths,
-                                 latency_virtual=per_req)
+                                 latency_virtual=c.layer_calls)
         return out
 
     def hit_rate(self):

@@ -12,6 +12,8 @@ tests; nothing at test time reads /root/reference):
 * golden_small.json  -- pre-cut instances, init checksums, beam-search
   outputs + counters on random/tiny/C1/C2 models, teacher-forced logits.
 * golden_c3.json     -- one request at the C3 shape (widths 512^3).
+* ref_checkpoint.npz -- (--ckpt) a checkpoint written by the reference's
+  save_checkpoint, for the interop test (tests/test_api_host.py).
 * golden_big.json    -- the C3 model decoded at the benched shapes:
   requests 0..7 at C3 widths 512^3, requests 0..7 at the C5 schedule
   64/128/256, and requests 0..1 at the C4 off-peak TABS widths 99/197/394
@@ -67,6 +69,7 @@ def main():
     ap.add_argument("--c3", action="store_true")
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--big-only", action="store_true")
+    ap.add_argument("--ckpt", action="store_true")
     args = ap.parse_args()
     sys.path.insert(0, REF)
     from adrec.losses.supervised import fit_ecpm_buckets
@@ -84,6 +87,15 @@ def main():
                                    counter=counter, **kw)
         return ([list(sid.tokens) for sid, _ in res], [float(s) for _, s in res],
                 [counter.layer_calls, counter.kv_builds, counter.kv_floats])
+
+    if args.ckpt:
+        # a checkpoint written by the reference's save_checkpoint (decoder.py:222-247)
+        from adrec.model.decoder import save_checkpoint
+        model = DecoderModel(DecoderConfig(3, 4, 6, 2, 1, (3, 3), 3, seed=123))
+        save_checkpoint(model, os.path.join(HERE, "ref_checkpoint.npz"), step=17,
+                        extra_arrays={"adam_t": np.array([17])}, meta={"note": "test"})
+        print("wrote ref_checkpoint.npz")
+        return
 
     if args.big or args.big_only:
         make_big(DecoderConfig, DecoderModel, context_process, ref_beam, BeamSchedule,

@@ -10,7 +10,7 @@ from conftest import ROOT
 def _declared():
     with open(os.path.join(ROOT, "include", "gr4ad.h")) as fh:
         text = fh.read()
-    return sorted(set(re.findall(r"\b(gr4ad_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(gr4ad_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_every_declared_symbol():
