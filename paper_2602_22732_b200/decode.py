@@ -12,16 +12,17 @@ it can be captured once into a CUDA graph and replayed per batch.
 from __future__ import annotations
 
 import ctypes as C
-import gc
 import threading
 from collections import OrderedDict
 
 import numpy as np
 import torch
 
+from . import _hostmarshal
 from . import _native as N
-from .device import _stream_handle, device_weights, dims_of, require_cuda
-from .quantizer.residual import check_token_range, sid_type
+from .device import (CAPTURE_GATE, _stream_handle, device_weights, dims_of, gated,
+                     require_cuda)
+from .quantizer.residual import sid_type
 
 
 def effective_widths(widths, vocab_sizes):
@@ -57,6 +58,7 @@ def prefix_keys(valid_sids, vocab_sizes):
 class BeamDecoder:
     PATHS = {"auto": 0, "layered": 1, "fused": 2, "tensor": 3, "fused_simt": 4}
 
+    @gated
     def __init__(self, model, ctx_lens, widths, trunk_depth=None, value_rerank=False,
                  representatives=None, valid_sids=None, device=None, path="auto"):
         self.device = require_cuda(device)
@@ -288,29 +290,17 @@ class BeamDecoder:
 
 
 def materialize(count, toks, score, max_out, T, vocab):
-    """Per-request [(SemanticId, float)] from host result arrays (count (B,),
-    tokens (B*max_out*T,), score (B*max_out,)); entries past count[b] are
-    ignored.  One vectorised range check replaces SemanticId's per-token
-    validation (the tokens come from the device, bounded by construction);
-    the cyclic GC is paused while the result objects are built."""
-    B = int(count.shape[0])
-    toks = toks.reshape(-1, max_out, T)[:B]
-    score = score.reshape(-1, max_out)[:B]
-    n = count.astype(np.int64)
-    m = int(n.max()) if B else 0
-    if m:
-        live = np.arange(m)[None, :] < n[:, None]
-        check_token_range(toks[:, :m][live], vocab)
-    cls = sid_type(vocab)
-    was = gc.isenabled()
-    gc.disable()
-    try:
-        tl = toks[:, :m].tolist()
-        sl = score[:, :m].tolist()
-        return [list(zip(map(cls, tl[b][:k]), sl[b][:k])) for b, k in enumerate(n.tolist())]
-    finally:
-        if was:
-            gc.enable()
+    """Per-request [(SemanticId, float)] from host result arrays (count (B,)
+    int32, tokens (B*max_out*T,) int32, score (B*max_out,) float64); entries
+    past count[b] are ignored.  Built by the native marshaller
+    (csrc/hostmarshal.c): one range check over the live tokens (the same
+    ValueError SemanticId raises), token ints from a prebuilt table,
+    SemanticId tuples allocated directly, cyclic GC paused."""
+    vocab = tuple(int(v) for v in vocab)
+    return _hostmarshal.build(np.ascontiguousarray(count, dtype=np.int32),
+                              np.ascontiguousarray(toks, dtype=np.int32),
+                              np.ascontiguousarray(score, dtype=np.float64),
+                              int(max_out), int(T), vocab, sid_type(vocab))
 
 
 class DecoderPool:
@@ -372,12 +362,36 @@ def decode_cached(key, factory, model, host_input, kind, items=None):
     ``items`` = (keys, ids, n)] -> async D2H of results + range flag -> host
     lists.  Returns (per-request [(SemanticId, float)], item slots (B,
     max_out) int32 array or None)."""
-    dec = POOL.acquire(key, factory)
+    with CAPTURE_GATE.shared():
+        dec = POOL.acquire(key, factory)
+    capture = dec.graph is None and dec.uses >= 1
+    gate = CAPTURE_GATE.exclusive() if capture else CAPTURE_GATE.shared()
     ok = False
-    try:
+    with gate:
+        try:
+            out = _decode_on(dec, model, host_input, kind, items)
+            ok = True
+            return out
+        except InputRangeError:
+            ok = True  # the decoder itself is fine
+            raise
+        finally:
+            if ok:
+                POOL.release(key, dec)
+
+
+class InputRangeError(RuntimeError):
+    """A finite float64 input that does not fit the fp32 decode."""
+
+
+def _decode_on(dec, model, host_input, kind, items):
+    if True:
         if dec.weights is not device_weights(model, dec.device):
             dec.rebind(model)  # a republished snapshot of the same shape
-        shape = tuple(host_input.shape)
+        if isinstance(host_input, (list, tuple)):  # per-request float64 blocks
+            shape = (sum(a.shape[0] for a in host_input), host_input[0].shape[1])
+        else:
+            shape = tuple(host_input.shape)
         if dec.in_buf is None or tuple(dec.in_buf.shape) != shape:
             dec.in_buf = torch.empty(shape, dtype=torch.float32, device=dec.device)
             dec._in_host = None
@@ -387,7 +401,15 @@ def decode_cached(key, factory, model, host_input, kind, items=None):
         else:
             if dec._in_host is None:
                 dec._in_host = torch.empty(shape, dtype=torch.float32).pin_memory()
-            np.copyto(dec._in_host.numpy(), host_input, casting="same_kind")
+            staged = dec._in_host.numpy()
+            with np.errstate(over="ignore"):
+                if isinstance(host_input, (list, tuple)):
+                    # one pass: concatenate + cast straight into pinned memory
+                    np.concatenate(host_input, 0, out=staged, casting="unsafe")
+                else:
+                    np.copyto(staged, host_input, casting="unsafe")
+            if not np.isfinite(staged).all():
+                raise InputRangeError("an input exceeds the fp32 range of the GPU decode")
             dec.in_buf.copy_(dec._in_host, non_blocking=True)
         inputs = {kind: dec.in_buf}
         if dec.graph is not None:
@@ -409,13 +431,10 @@ def decode_cached(key, factory, model, host_input, kind, items=None):
             dec.resolve_items(*items)
         dec.fetch_async()
         out = dec.results()
-        ok = True
         return out, dec.last_item_idx
-    finally:
-        if ok:
-            POOL.release(key, dec)
 
 
+@gated
 def score_sequences(model, seq_requests, tokens, features=None, contexts=None,
                     include_value_step=False, trunk_depth=None, return_logits=False,
                     device=None, path="auto"):

@@ -9,6 +9,7 @@ the encoder pass is a single GEMM over all requests' context rows.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import threading
 from collections import OrderedDict
@@ -20,6 +21,73 @@ from . import _native as N
 from .model.decoder import param_array
 
 _ALIGN = 64  # floats (256 B) between packed tensors
+
+
+class _CaptureGate:
+    """Readers-writer gate between CUDA-graph capture and the package's other
+    device work.  While a stream captures, CUDA rejects work that implicitly
+    synchronises with it from any thread (e.g. a copy on the legacy default
+    stream), so the one-time capture of a pooled decoder's graph runs
+    exclusively; every other device call of the package holds the gate
+    shared (concurrent decodes proceed together)."""
+
+    def __init__(self):
+        self._cv = threading.Condition()
+        self._readers = 0
+        self._writer = False
+        self._local = threading.local()
+
+    def _depth(self):
+        return getattr(self._local, "depth", 0)
+
+    @contextlib.contextmanager
+    def shared(self):
+        if self._depth():  # re-entrant inside either mode
+            yield
+            return
+        with self._cv:
+            while self._writer:
+                self._cv.wait()
+            self._readers += 1
+        self._local.depth = 1
+        try:
+            yield
+        finally:
+            self._local.depth = 0
+            with self._cv:
+                self._readers -= 1
+                self._cv.notify_all()
+
+    @contextlib.contextmanager
+    def exclusive(self):
+        if self._depth():
+            raise RuntimeError("graph capture requested inside a device call")
+        with self._cv:
+            while self._writer or self._readers:
+                self._cv.wait()
+            self._writer = True
+        self._local.depth = 1
+        try:
+            yield
+        finally:
+            self._local.depth = 0
+            with self._cv:
+                self._writer = False
+                self._cv.notify_all()
+
+
+CAPTURE_GATE = _CaptureGate()
+
+
+def gated(fn):
+    """Run ``fn`` holding the capture gate shared (see _CaptureGate)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*a, **kw):
+        with CAPTURE_GATE.shared():
+            return fn(*a, **kw)
+    return wrapper
 
 
 def _stream_handle(device=None):
@@ -175,14 +243,15 @@ def device_weights(model, device=None):
     device = require_cuda(device)
     key = (id(model.params), str(device))
     fp = _fingerprint(model.params)
-    with _CACHE_LOCK:
-        hit = _CACHE.get(key)
-        if hit is not None and hit[0] == fp:
-            _CACHE.move_to_end(key)
-            return hit[2].use_on()
-    dw = DeviceWeights(model, device)
-    register(model, dw)
-    return dw
+    with CAPTURE_GATE.shared():
+        with _CACHE_LOCK:
+            hit = _CACHE.get(key)
+            if hit is not None and hit[0] == fp:
+                _CACHE.move_to_end(key)
+                return hit[2].use_on()
+        dw = DeviceWeights(model, device)
+        register(model, dw)
+        return dw
 
 
 def register(model, dw):
@@ -235,6 +304,7 @@ class DeviceContext:
         return self.tensor.double().cpu().numpy()
 
 
+@gated
 def context_process_gpu(features, params):
     device = require_cuda()
     feats = np.atleast_2d(np.asarray(getattr(features, "data", features), dtype=np.float64))

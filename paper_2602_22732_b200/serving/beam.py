@@ -26,7 +26,7 @@ import torch
 
 from .. import _native as N
 from ..decode import BeamDecoder, decode_cached, effective_widths, live_rows
-from ..device import (DeviceContext, _stream_handle, device_weights, dims_of,
+from ..device import (DeviceContext, _stream_handle, device_weights, dims_of, gated,
                       require_cuda)
 from ..model.decoder import param_array
 
@@ -130,6 +130,8 @@ def _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path, inp
     range of the tensor-core paths is decoded again on the fp32 CUDA-core
     path (another GPU path -- there is no CPU fallback)."""
     dev = inp.device if isinstance(inp, torch.Tensor) else require_cuda()
+    if isinstance(inp, list) and len({a.shape[1] for a in inp}) != 1:
+        raise ValueError("feature blocks must share one width")
     reps_key = None if reps is None else tuple(np.asarray(reps, dtype=np.float64).ravel().tolist())
     vkey = _valid_key(valid_sids)
 
@@ -231,10 +233,7 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
             if not np.isfinite(a).all():
                 raise ValueError("context must be finite")
         lens = [a.shape[0] for a in arrs]
-        with np.errstate(over="ignore"):
-            inp = np.concatenate(arrs, 0).astype(np.float32, copy=False)
-        if not np.isfinite(inp).all():
-            raise RuntimeError("a feature exceeds the fp32 range of the GPU decode")
+        inp = arrs  # concatenated + cast into the decoder's pinned staging buffer
         kind = "features"
     reps = None
     if value_rerank:
@@ -249,6 +248,7 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
     return (out, item_idx) if _items is not None else out
 
 
+@gated
 def _select_gpu(beam_scores, logprobs, k):
     """Exact float64 selection on the GPU (gr4ad_topk_precut_f64): the
     candidate scores are the reference's own double sums, ranked with no
@@ -289,6 +289,7 @@ def topk_global(beam_scores, level_logprobs, k):
     return _select_gpu(beam_scores, level_logprobs, k)
 
 
+@gated
 def shared_encoder_kv(model, context, trunk_depth=None):
     """Per-request cross-attention K/V for the layers above the trunk
     (beam.py:98-109): {layer: (keys, values)} as float64 host arrays; the

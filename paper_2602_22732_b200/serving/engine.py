@@ -53,6 +53,11 @@ class SnapshotStore:
     def _stage(self, snapshot):
         if not self._preload:
             return
+        from ..device import CAPTURE_GATE
+        with CAPTURE_GATE.shared():
+            self._stage_locked(snapshot)
+
+    def _stage_locked(self, snapshot):
         from ..device import DeviceWeights, register, require_cuda
         dev = require_cuda(self._device)
         if self._stream is None:
@@ -241,8 +246,9 @@ class ServingEngine:
         version = self.index.version
         tab = self._table
         if tab is None or tab[0] != version or tab[1] != vocab:
-            from ..device import require_cuda
-            tab = (version, vocab, ItemTable(self.index, vocab, require_cuda()))
+            from ..device import CAPTURE_GATE, require_cuda
+            with CAPTURE_GATE.shared():
+                tab = (version, vocab, ItemTable(self.index, vocab, require_cuda()))
             self._table = tab
         return tab[2]
 
