@@ -136,7 +136,7 @@ def _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path, inp
     vkey = _valid_key(valid_sids)
 
     def attempt(p):
-        key = (id(model.params), str(dev), kind, tuple(lens), tuple(per), k_depth,
+        key = (id(model.params), model.config, str(dev), kind, tuple(lens), tuple(per), k_depth,
                bool(value_rerank), reps_key, vkey, p)
         factory = lambda: BeamDecoder(model, lens, per, trunk_depth=k_depth,
                                       value_rerank=value_rerank, representatives=reps,
