@@ -258,17 +258,19 @@ def class_work(cfgd):
     n_trunk = B * T if K > 0 else 0
     head_rows = sum(R[:T])
     layer_rows = K * n_trunk + (L - K) * head_rows
-    # executed: encoder K/V for the head layers only; trunk rows attend through
-    # (q Wk^T) X^T and (P X) Wv, i.e. 2 extra d x d products per trunk row
-    gemm = B * (2 * S * F * d + 4 * (L - K) * S * d * d) + layer_rows * (12 * d * d + 4 * d * dff)
-    gemm += K * n_trunk * 4 * d * d
+    # executed on the tensor-core path (factored attention, abi.cu
+    # layer_forward_tc): no encoder K/V; per layer row the folded
+    # attention products n (Wq Wk^T), u (Wv Wo) for the cross- and the
+    # self-attention (4 d^2 MAC) plus the FFN (2 d dff MAC)
+    gemm = B * 2 * S * F * d + layer_rows * (8 * d * d + 4 * d * dff)
     gemm += sum(R[t] * ((6 * d * d if K > 0 else 0) + 2 * d * V[t]) for t in range(T))
     attn = layer_rows * 4 * S * d
     topk = sum(R[t] * V[t] * 4 + R[t] * 12 + R[t + 1] * (20 + 8 * (t + 2)) for t in range(T))
     soft = layer_rows * S * 8
     ln = layer_rows * 3 * 8 * d
-    sattn = K * n_trunk * 4 * (2 * d + 2 * d * T) + (L - K) * sum(
-        R[t] * 4 * (2 * d + 2 * d * (t + 1)) for t in range(T))
+    # q' and the normalised history rows n (fp32), the output as fp16 hi / lo
+    sattn = K * n_trunk * 4 * (2 * d + d * T) + (L - K) * sum(
+        R[t] * 4 * (2 * d + d * (t + 1)) for t in range(T))
     lse = sum(R[t] * (V[t] * 4 + 8) for t in range(T))
     return {"gemm": ("flop", gemm), "attn_gemm": ("flop", attn), "topk_select": ("byte", topk),
             "softmax": ("byte", soft), "layernorm": ("byte", ln), "self_attn": ("byte", sattn),

@@ -24,7 +24,7 @@ OK, ERR_VALUE, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA, ERR_RANGE = range(6)
 
 class RangeError(RuntimeError):
     """An operand left the fp16 split range of the tensor-core paths
-    (GR4AD_ERR_RANGE): |weight| >= 32 or |context K/V| >= 256.  The decode
+    (GR4AD_ERR_RANGE): |weight| >= 32 or |context X| >= 256.  The decode
     API retries such batches on the CUDA-core path when ``path="auto"``."""
 
 KERNEL_CLASSES = ("gemm", "attn_gemm", "topk_select", "softmax", "layernorm", "self_attn",

@@ -78,12 +78,13 @@ struct Plan {
   size_t o_tok, o_anc, o_cum, o_prefix;
   size_t o_X, o_KV, o_Ht, o_QKVt, o_Fin = 0;
   size_t o_Hs, o_N, o_Q, o_A, o_U, o_Fb, o_SC, o_SCs, o_LG, o_rinfo, o_lsep, o_vlog;
-  size_t o_hist;  // (L-K) consecutive (H, 3d) buffers
+  size_t o_hist;  // (L-K) consecutive (H, hist_ld) buffers
+  long long hist_ld = 0;  // self-attention history row: [q|k|v] (3d) or factored [q'|n] (2d)
   size_t table_bytes, total;
   // tensor-core layered path
   bool tc = false;
   long long sc_ld = 0, vt_ld = 0;
-  size_t o_VT = 0, o_WT = 0, o_XT = 0, o_VTlo = 0, o_KVlo = 0, o_Xs = 0, o_U16 = 0;
+  size_t o_WT = 0, o_XTs = 0, o_Xs = 0, o_U16 = 0, o_Mf = 0;
   long long wt_floats = 0;
   // fused small-model path
   bool fused = false;
@@ -369,12 +370,14 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   if ((bt->decode_path == 2 || bt->decode_path == 4) && !p.fused)
     return set_err(GR4AD_ERR_UNSUPPORTED, "fused decode path not eligible for this batch");
   if (!p.fused) {
-    bool ok = p.d % 4 == 0 && p.dff % 4 == 0 && p.F % 4 == 0;
+    bool ok = p.d % 8 == 0 && p.dff % 4 == 0 && p.F % 4 == 0;
     for (int t = 0; t < T; ++t) ok &= p.V[t] % 4 == 0;
     p.tc = ok && (bt->decode_path == 3 || (bt->decode_path == 0 && p.d >= 64));
     if (bt->decode_path == 3 && !ok)
-      return set_err(GR4AD_ERR_UNSUPPORTED, "tensor-core path needs d, d_ff, F, V multiples of 4");
+      return set_err(GR4AD_ERR_UNSUPPORTED,
+                     "tensor-core path needs d a multiple of 8 and d_ff, F, V multiples of 4");
   }
+  p.hist_ld = (p.tc ? 2LL : 3LL) * p.d;
   p.sc_ld = (p.S_max + 7) / 8 * 8;  // (fp16 P rows: 16-B aligned)
   p.vt_ld = (p.S_tot + 7) / 8 * 8;  // fp16 rows: 16-B aligned
   if (p.tc) {
@@ -382,13 +385,12 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     p.wt_floats = 0;
     auto add = [&](long long n) { p.wt_floats += (n + 63) / 64 * 64; };
     add(D * p.F);
-    add(2LL * p.L * D * D);
     add(D * D);
     add(2 * D * D);
     for (int t = 0; t < T; ++t) add((long long)p.V[t] * D);
     add((long long)p.nb * D);
-    for (int i = 0; i < p.L; ++i) {
-      add(D * D); add(D * D); add(3 * D * D); add(D * D); add(p.dff * D); add(D * p.dff);
+    for (int i = 0; i < p.L; ++i) {  // qk, vo, self qk, self vo, W1, W2
+      add(D * D); add(D * D); add(D * D); add(D * D); add(p.dff * D); add(D * p.dff);
     }
   }
 
@@ -439,12 +441,12 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   const size_t d = p.d;
   p.o_X = take(Fl * p.S_tot * d);
   p.o_Fin = take(Fl * p.S_tot * p.F);
-  // K/V are materialised for the head layers only: trunk rows (n_pos per
-  // request) attend through the reassociated (q Wk^T) X^T / (P X) Wv
-  // (the tensor-core path keeps only the fp16 split K / V^T below)
+  // CUDA-core path: K/V materialised for the head layers only (trunk rows
+  // attend through the reassociated (q Wk^T) X^T / (P X) Wv); the
+  // tensor-core path attends against X itself (factored attention)
   p.o_KV = take(p.tc ? 256 : Fl * p.S_tot * 2 * (p.L - p.K) * d);
   p.o_Ht = take(Fl * (size_t)B * p.n_pos * d);
-  p.o_QKVt = take(Fl * (size_t)B * p.n_pos * 3 * d);
+  p.o_QKVt = take(Fl * (size_t)B * p.n_pos * p.hist_ld);
   p.o_Hs = take(Fl * p.Rw * d);
   p.o_N = take(Fl * p.Rw * d);
   p.o_Q = take(Fl * p.Rw * d);
@@ -457,14 +459,12 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.o_rinfo = take(sizeof(float2) * p.Rw);
   p.o_lsep = take(p.tc ? sizeof(float4) * p.Rw * ((p.Vmax + 127) / 128) : 16);
   p.o_vlog = take(Fl * std::max(p.R[T], 1LL) * p.nb);
-  p.o_hist = take(Fl * p.H * 3 * d * (size_t)(p.L - p.K));
+  p.o_hist = take(Fl * p.H * p.hist_ld * (size_t)(p.L - p.K));
   if (p.tc) {
     const size_t H2 = sizeof(__half);
-    p.o_VT = take(256);  // (unused on this path: V^T lives split below)
-    p.o_VTlo = take(H2 * 2 * (size_t)(p.L - p.K) * d * p.vt_ld);  // V^T fp16 hi, then lo
-    p.o_KVlo = take(H2 * 2 * p.S_tot * (p.L - p.K) * d);           // K fp16 hi, then lo
-    p.o_XT = take(Fl * (size_t)d * p.vt_ld);
-    p.o_Xs = take(H2 * 2 * p.S_tot * d);  // X as fp16 hi, then lo (the K/V GEMM's A)
+    p.o_XTs = take(H2 * 2 * (size_t)d * p.vt_ld);  // kKvScale X^T as fp16 hi, then lo
+    p.o_Xs = take(H2 * 2 * p.S_tot * d);           // kKvScale X as fp16 hi, then lo
+    p.o_Mf = take(Fl * 4 * (size_t)p.L * d * d);   // factored attention weights (fp32)
     p.o_U16 = take(H2 * 2 * p.Rw * 2 * d);  // the fuse input [g | s] as fp16 hi, then lo
     p.o_WT = take(H2 * (size_t)p.wt_floats * 2);  // K-major weights: fp16 hi, then lo
   }
@@ -532,7 +532,7 @@ struct RowSet {
   int groups = 0;     // attention groups (0: one per request)
   const int *g_ctx_off = nullptr, *g_ctx_len = nullptr;  // per-group context block
   const int *g_row_off, *g_rows, *row_req;
-  float *qkv;         // (*, 3d) q/k/v buffer (self-attention history)
+  float *qkv;         // (*, hist_ld) self-attention history rows
   long long hist_row0;
   const int *anc;
   int anc_stride;
@@ -540,12 +540,17 @@ struct RowSet {
   const int *npos_row;
 };
 
-// K-major (out, in) copies of the weights for the tensor-core path
+// Tensor-core path: K-major (out, in) fp16 hi / lo copies of the weights,
+// with every attention projection pair folded into one matrix (factored
+// attention, see layer_forward_tc): qk = W_q W_k^T and vo = W_v W_o of the
+// cross- and the self-attention.  m* are the fp32 products themselves
+// (rounded once from double; the CUDA-core fallback of `dense` reads them).
 struct LayerT {
-  const __half *cq, *co, *sqkv, *so, *w1, *w2;
+  const __half *qk, *vo, *sqk, *svo, *w1, *w2;
+  const float *mqk, *mvo, *msqk, *msvo;
 };
 struct WeightsT {
-  const __half *ctx, *kv, *wg, *wf, *hv;
+  const __half *ctx, *wg, *wf, *hv;
   const __half *head[GR4AD_MAX_LEVELS];
   LayerT layer[GR4AD_MAX_LAYERS];
 };
@@ -564,21 +569,38 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
                              at<int>(ws, p.o_flag), st);
     return dst;
   };
+  // C (d x d) = A . op(B) in double (weight_product), once per snapshot
+  auto prod = [&](const float *A, long long lda, const float *B, long long ldb, bool tb,
+                  float *C) {
+    if (rc == GR4AD_OK && launch) rc = weight_product(A, lda, B, ldb, tb, C, p.d, p.d, p.d, p.d, st);
+  };
   const int d = p.d;
+  const long long dd = (long long)d * d, ldw = 2LL * p.L * d;
   wt.ctx = tr(w->ctx_W, p.F, d);
-  wt.kv = tr(w->cross_kv_W, d, 2 * p.L * d);
   wt.wg = tr(w->fuse_Wg, d, d);
   wt.wf = tr(w->fuse_Wf, 2 * d, d);
   for (int t = 0; t < p.T; ++t) wt.head[t] = tr(w->head[t], d, p.V[t]);
   wt.hv = tr(w->head_value, d, p.nb);
+  float *Mf = at<float>(ws, p.o_Mf);
   for (int i = 0; i < p.L; ++i) {
     const gr4ad_layer &Lw = w->layer[i];
-    wt.layer[i].cq = tr(Lw.cross_Wq, d, d);
-    wt.layer[i].co = tr(Lw.cross_Wo, d, d);
-    wt.layer[i].sqkv = tr(Lw.self_Wqkv, d, 3 * d);
-    wt.layer[i].so = tr(Lw.self_Wo, d, d);
-    wt.layer[i].w1 = tr(Lw.ffn_W1, d, p.dff);
-    wt.layer[i].w2 = tr(Lw.ffn_W2, p.dff, d);
+    LayerT &lt = wt.layer[i];
+    float *m = Mf + 4 * dd * i;
+    const float *Wk = w->cross_kv_W + (size_t)2 * i * d, *Wv = Wk + d;
+    prod(Lw.cross_Wq, d, Wk, ldw, true, m);                             // W_q W_k^T
+    prod(Wv, ldw, Lw.cross_Wo, d, false, m + dd);                       // W_v W_o
+    prod(Lw.self_Wqkv, 3LL * d, Lw.self_Wqkv + d, 3LL * d, true, m + 2 * dd);   // self W_q W_k^T
+    prod(Lw.self_Wqkv + 2 * d, 3LL * d, Lw.self_Wo, d, false, m + 3 * dd);      // self W_v W_o
+    lt.mqk = m;
+    lt.mvo = m + dd;
+    lt.msqk = m + 2 * dd;
+    lt.msvo = m + 3 * dd;
+    lt.qk = tr(lt.mqk, d, d);
+    lt.vo = tr(lt.mvo, d, d);
+    lt.sqk = tr(lt.msqk, d, d);
+    lt.svo = tr(lt.msvo, d, d);
+    lt.w1 = tr(Lw.ffn_W1, d, p.dff);
+    lt.w2 = tr(Lw.ffn_W2, p.dff, d);
   }
   return rc;
 }
@@ -599,17 +621,6 @@ static int dense(const Plan &p, const GemmArgs &g, const __half *WT, long long a
   return gemm(g, false, epi, st);
 }
 
-// C = epi(A (M x K) . B^T) with B given as an (N x K) row-major matrix
-static int dense_nk(const Plan &p, const GemmArgs &g, long long a_rows, long long b_rows, int epi,
-                    cudaStream_t st) {
-  if (p.tc && tc_eligible(g.lda, g.ldb, g.K, g.A, g.B)) {
-    TcArgs t{};
-    static_cast<GemmArgs &>(t) = g;
-    return gemm_tc(t, a_rows, g.K, b_rows, g.K, epi, st);
-  }
-  return gemm(g, true, epi, st);
-}
-
 // C = epi(A . W) with A already split into fp16 hi / lo (written so by the
 // producing LayerNorm / epilogue / self-attention): no on-chip conversion
 static int dense_split(const Plan &p, const GemmArgs &g, const __half *WT, const __half *a_hi,
@@ -628,149 +639,193 @@ static int dense_split(const Plan &p, const GemmArgs &g, const __half *WT, const
   return gemm_tc(t, a_rows, g.K, g.N, g.K, epi, st);
 }
 
-// split_out: also leave the layer's output rows as fp16 hi / lo in the N
-// buffer (the codebook GEMM's pre-split A); returns whether it did
-static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *wt, int i,
-                         float *Hs, const RowSet &rs, void *ws, const float *KV,
-                         const float *VT, cudaStream_t st, bool *split_out = nullptr) {
+// CUDA-core layered path: the reference's layer as written, with the trunk
+// layers' K / V reassociated -- q (X W_k)^T = (q W_k^T) X^T and P (X W_v) =
+// (P X) W_v -- so only the head layers' K / V are materialised (KV)
+static int layer_forward(const Plan &p, const gr4ad_weights *w, int i, float *Hs,
+                         const RowSet &rs, void *ws, const float *KV, cudaStream_t st) {
   const int d = p.d, R = rs.rows;
   const gr4ad_layer &Lw = w->layer[i];
-  const LayerT *LT = wt ? &wt->layer[i] : nullptr;
   float *N = at<float>(ws, p.o_N), *Q = at<float>(ws, p.o_Q), *A = at<float>(ws, p.o_A);
   float *SC = at<float>(ws, p.o_SC), *Fb = at<float>(ws, p.o_Fb);
   const int *ctx_off = rs.g_ctx_off ? rs.g_ctx_off : at<int>(ws, p.o_ctx_off);
   const int *ctx_len = rs.g_ctx_len ? rs.g_ctx_len : at<int>(ws, p.o_ctx_len);
   const int n_groups = rs.groups > 0 ? rs.groups : p.B;
-  const int nh = p.L - p.K;  // layers whose context K/V are materialised
-  const long long ldkv = 2LL * nh * d;
+  const long long ldkv = 2LL * (p.L - p.K) * d, ldw = 2LL * p.L * d;
   const bool trunk = i < p.K;
   const float *X = at<float>(ws, p.o_X);
-  const long long ldw = 2LL * p.L * d;
-  // head layers on the tensor-core path: every dense product's activation
-  // operand is produced already split into fp16 hi / lo (LayerNorm, P.V and
-  // GELU epilogues, self-attention), so the GEMMs only move and multiply
-  const bool spl = p.tc && LT && !trunk && d % 128 == 0 && d <= 1024 && p.dff % 8 == 0;
-  __half *Nh = reinterpret_cast<__half *>(N), *Nl = Nh + (size_t)p.Rw * d;
-  __half *Ah = reinterpret_cast<__half *>(A), *Al = Ah + (size_t)p.Rw * d;
-  __half *Fh = reinterpret_cast<__half *>(Fb), *Fl = Fh + (size_t)p.Rw * p.dff;
-  auto layer_norm = [&](const float *g_, const float *b_) -> int {
-    return spl ? ln_rows_split(Hs, d, Nh, Nl, d, g_, b_, R, d, st)
-               : ln_rows(Hs, d, N, d, g_, b_, R, d, st);
-  };
   // cross-attention into the beam-shared context KV (layers.py:82-90)
-  GR_TRY(layer_norm(Lw.ln1_g, Lw.ln1_b));
-  // attention on many rows per request (no A/B swap): q and P split too
-  const bool swap = p.tc && rs.max_group_rows <= 64 && d % 8 == 0;
-  const bool spl_att = spl && !swap;
-  __half *Qh = reinterpret_cast<__half *>(Q), *Ql = Qh + (size_t)p.Rw * d;
-  __half *Ph = at<__half>(ws, p.o_SCs), *Pl = Ph + (size_t)p.Rw * p.sc_ld;
-  if (spl)
-    GR_TRY(dense_split(p, plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), LT->cq, Nh, Nl, R,
-                       spl_att ? EPI_STORE_SPLIT : EPI_STORE, st, Qh, Ql));
-  else
-    GR_TRY(dense(p, plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), LT ? LT->cq : nullptr, R,
-                 EPI_STORE, st));
+  GR_TRY(ln_rows(Hs, d, N, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
+  GR_TRY(gemm(plain_gemm(N, d, Lw.cross_Wq, d, Q, d, R, d, d), false, EPI_STORE, st));
   const float *qsrc = Q;
-  if (trunk) {
-    // trunk rows: q (X Wk)^T = (q Wk^T) X^T -- the trunk layers' K is never built
-    float *Q2 = N;
-    GemmArgs g = plain_gemm(Q, d, w->cross_kv_W + (size_t)(2 * i) * d, ldw, Q2, d, R, d, d);
-    GR_TRY(dense_nk(p, g, R, d, EPI_STORE, st));  // B = Wk as (N x K): Q2 = Q Wk^T
-    qsrc = Q2;
+  if (trunk) {  // B = W_k as (N x K): N = Q W_k^T
+    GR_TRY(gemm(plain_gemm(Q, d, w->cross_kv_W + (size_t)(2 * i) * d, ldw, N, d, R, d, d), true,
+                EPI_STORE, st));
+    qsrc = N;
   }
   GemmArgs qk{};
   qk.A = qsrc; qk.lda = d;
-  if (trunk) {
-    qk.B = X; qk.ldb = d;
-  } else {
-    qk.B = KV + (size_t)(2 * (i - p.K)) * d; qk.ldb = ldkv;
-  }
+  qk.B = trunk ? X : KV + (size_t)(2 * (i - p.K)) * d;
+  qk.ldb = trunk ? d : ldkv;
   qk.C = SC; qk.ldc = p.sc_ld;
   qk.M = rs.max_group_rows; qk.N = p.S_max; qk.K = d;
   qk.alpha = 1.0f / sqrtf((float)d);
   qk.groups = n_groups; qk.mode = GM_QK;
   qk.g_row_off = rs.g_row_off; qk.g_rows = rs.g_rows;
   qk.g_ctx_off = ctx_off; qk.g_ctx_len = ctx_len;
+  GR_TRY(gemm(qk, true, EPI_STORE, st));
+  GR_TRY(softmax_rows(SC, p.sc_ld, R, rs.row_req, ctx_len, st));
+  GemmArgs pv = qk;
+  pv.A = SC; pv.lda = p.sc_ld;
+  pv.B = trunk ? X : KV + (size_t)(2 * (i - p.K) + 1) * d;
+  pv.C = A; pv.ldc = d;
+  pv.M = rs.max_group_rows; pv.N = d; pv.K = p.S_max;
+  pv.alpha = 1.f; pv.mode = GM_PV;
+  GR_TRY(gemm(pv, false, EPI_STORE, st));
+  const float *attn = A;
+  if (trunk) {  // (P X) W_v
+    GR_TRY(gemm(plain_gemm(A, d, w->cross_kv_W + (size_t)(2 * i + 1) * d, ldw, Q, d, R, d, d),
+                false, EPI_STORE, st));
+    attn = Q;
+  }
+  GemmArgs o = plain_gemm(attn, d, Lw.cross_Wo, d, Hs, d, R, d, d);
+  o.R = Hs; o.ldr = d;
+  GR_TRY(gemm(o, false, EPI_RESID, st));
+  // self-attention over decoded positions (layers.py:92-113)
+  GR_TRY(ln_rows(Hs, d, N, d, Lw.ln2_g, Lw.ln2_b, R, d, st));
+  float *qkv_rows = rs.qkv + rs.hist_row0 * p.hist_ld;
+  GR_TRY(gemm(plain_gemm(N, d, Lw.self_Wqkv, 3 * d, qkv_rows, p.hist_ld, R, 3 * d, d), false,
+              EPI_STORE, st));
+  GR_TRY(self_attn(rs.qkv, p.hist_ld, d, rs.anc, rs.anc_stride, (int)rs.hist_row0, R, rs.npos_u,
+                   rs.npos_row, A, d, st));
+  GemmArgs so = plain_gemm(A, d, Lw.self_Wo, d, Hs, d, R, d, d);
+  so.R = Hs; so.ldr = d;
+  GR_TRY(gemm(so, false, EPI_RESID, st));
+  // position-wise FFN (layers.py:115-118)
+  GR_TRY(ln_rows(Hs, d, N, d, Lw.ln3_g, Lw.ln3_b, R, d, st));
+  GemmArgs f1 = plain_gemm(N, d, Lw.ffn_W1, p.dff, Fb, p.dff, R, p.dff, d);
+  f1.bias = Lw.ffn_b1;
+  GR_TRY(gemm(f1, false, EPI_BIAS_GELU, st));
+  GemmArgs f2 = plain_gemm(Fb, p.dff, Lw.ffn_W2, d, Hs, d, R, d, p.dff);
+  f2.bias = Lw.ffn_b2; f2.R = Hs; f2.ldr = d;
+  return gemm(f2, false, EPI_BIAS_RESID, st);
+}
+
+// Tensor-core path, factored attention.  The reference attends with
+// q = n W_q, K = X W_k, V = X W_v (layers.py:46-51, 82-90; beam.py:98-109,
+// 221-232) and the self-attention likewise on the LayerNorm'd rows n
+// (layers.py:101-113).  Single head, no projection biases, so
+//   q K^T = (n W_q W_k^T) X^T        P V W_o = (P X)(W_v W_o)
+// exactly: with W_q W_k^T and W_v W_o formed once per snapshot
+// (prep_weights_t), every layer attends straight against the request's
+// context X -- one fp16-split copy of X and of X^T, shared by all beams AND
+// all layers -- and the per-request encoder K / V GEMM (4 (L-K) S d^2 flop)
+// disappears, as do the self-attention's K / V projections (the history
+// keeps n itself).  Per beam row the dense products drop from 10 d^2 to
+// 8 d^2 MACs per layer.
+//
+// split_out: also leave the layer's output rows as fp16 hi / lo in the N
+// buffer (the codebook GEMM's pre-split A); returns whether it did
+static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const WeightsT &wt, int i,
+                            float *Hs, const RowSet &rs, void *ws, cudaStream_t st,
+                            bool *split_out = nullptr) {
+  const int d = p.d, R = rs.rows;
+  const gr4ad_layer &Lw = w->layer[i];
+  const LayerT &LT = wt.layer[i];
+  float *N = at<float>(ws, p.o_N), *Q = at<float>(ws, p.o_Q), *A = at<float>(ws, p.o_A);
+  float *SC = at<float>(ws, p.o_SC), *Fb = at<float>(ws, p.o_Fb);
+  const int *ctx_off = rs.g_ctx_off ? rs.g_ctx_off : at<int>(ws, p.o_ctx_off);
+  const int *ctx_len = rs.g_ctx_len ? rs.g_ctx_len : at<int>(ws, p.o_ctx_len);
+  const int n_groups = rs.groups > 0 ? rs.groups : p.B;
+  // every activation operand produced already split into fp16 hi / lo
+  // (LayerNorm, epilogues, softmax, self-attention): the GEMMs only move and
+  // multiply
+  const bool spl = d % 128 == 0 && d <= 1024 && p.dff % 8 == 0;
+  __half *Nh = reinterpret_cast<__half *>(N), *Nl = Nh + (size_t)p.Rw * d;
+  __half *Ah = reinterpret_cast<__half *>(A), *Al = Ah + (size_t)p.Rw * d;
+  __half *Fh = reinterpret_cast<__half *>(Fb), *Fl = Fh + (size_t)p.Rw * p.dff;
+  __half *Qh = reinterpret_cast<__half *>(Q), *Ql = Qh + (size_t)p.Rw * d;
+  __half *Ph = at<__half>(ws, p.o_SCs), *Pl = Ph + (size_t)p.Rw * p.sc_ld;
+  // the request's context, kKvScale * X as fp16 hi / lo: X (S_tot x d) is
+  // the K-side operand, X^T (d x vt_ld) the V-side one
+  const __half *xs_hi = at<__half>(ws, p.o_Xs), *xs_lo = xs_hi + (size_t)p.S_tot * d;
+  const __half *xt_hi = at<__half>(ws, p.o_XTs), *xt_lo = xt_hi + (size_t)d * p.vt_ld;
+
+  // ---- cross-attention into the beam-shared context (layers.py:82-90) ----
+  if (spl)
+    GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
+  else
+    GR_TRY(ln_rows(Hs, d, N, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
   // few beam rows per request: swap A / B so tiles are not padded to 128 rows
-  if (swap) {
+  const bool swap = rs.max_group_rows <= 64;
+  const bool spl_att = spl && !swap;
+  const GemmArgs gq = plain_gemm(N, d, LT.mqk, d, Q, d, R, d, d);  // q' = n (W_q W_k^T)
+  if (spl)
+    GR_TRY(dense_split(p, gq, LT.qk, Nh, Nl, R, spl_att ? EPI_STORE_SPLIT : EPI_STORE, st, Qh, Ql));
+  else
+    GR_TRY(dense(p, gq, LT.qk, R, EPI_STORE, st));
+  GemmArgs qk{};
+  qk.A = Q; qk.lda = d;
+  qk.C = SC; qk.ldc = p.sc_ld;
+  qk.M = rs.max_group_rows; qk.N = p.S_max; qk.K = d;
+  qk.alpha = 1.0f / sqrtf((float)d) / kKvScale;
+  qk.groups = n_groups; qk.mode = GM_QK;
+  qk.g_row_off = rs.g_row_off; qk.g_rows = rs.g_rows;
+  qk.g_ctx_off = ctx_off; qk.g_ctx_len = ctx_len;
+  if (swap) {  // tile M = keys (S_max), N = beam rows; q split on chip
     TcArgs t{};
     static_cast<GemmArgs &>(t) = qk;
     t.mode = GM_QK_T;
-    t.M = qk.N;  // tile M = keys (S_max), N = beam rows
+    t.M = qk.N;
     t.N = qk.M;
-    t.B = qsrc;  // the query rows, split on chip
+    t.B = Q;
     t.ldb = d;
-    if (trunk) {
-      t.A = X;  // keys = the context rows themselves (reassociated trunk)
-      t.lda = d;
-    } else {
-      const __half *k16 = at<__half>(ws, p.o_KVlo);
-      t.a_hi = k16 + (size_t)(i - p.K) * d;
-      t.a_lo = t.a_hi + (size_t)p.S_tot * nh * d;
-      t.lda = (long long)nh * d;
-      t.alpha = qk.alpha / kKvScale;
-    }
+    t.a_hi = xs_hi;
+    t.a_lo = xs_lo;
+    t.lda = d;
     GR_TRY(gemm_tc_swapped(t, p.S_tot, d, R, d, st));
-  } else if (p.tc && tc_eligible(qk.lda, qk.ldb, d, qk.A, qk.B)) {
+  } else {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = qk;
-    if (!trunk) {  // head-layer K arrives split (fp16, scaled) from the encoder epilogue
-      const __half *k16 = at<__half>(ws, p.o_KVlo);
-      t.b_hi = k16 + (size_t)(i - p.K) * d;
-      t.b_lo = t.b_hi + (size_t)p.S_tot * nh * d;
-      t.ldb = (long long)nh * d;
-      t.alpha = qk.alpha / kKvScale;
-    }
-    if (spl_att) {  // q arrives split from the Wq epilogue
+    t.b_hi = xs_hi;
+    t.b_lo = xs_lo;
+    t.ldb = d;
+    if (spl_att) {  // q' arrives split from its GEMM's epilogue
       t.a_hi = Qh;
       t.a_lo = Ql;
     }
     GR_TRY(gemm_tc(t, R, d, p.S_tot, d, EPI_STORE, st));
-  } else {
-    GR_TRY(gemm(qk, true, EPI_STORE, st));
   }
   if (spl_att)
     GR_TRY(softmax_rows_split(SC, p.sc_ld, Ph, Pl, R, rs.row_req, ctx_len, st));
   else
     GR_TRY(softmax_rows(SC, p.sc_ld, R, rs.row_req, ctx_len, st));
-  GemmArgs pv = qk;
+  GemmArgs pv = qk;  // u = P X
   pv.A = SC; pv.lda = p.sc_ld;
   pv.C = A; pv.ldc = d;
   pv.M = rs.max_group_rows; pv.N = d; pv.K = p.S_max;
-  pv.alpha = 1.f; pv.mode = GM_PV;
-  if (swap && VT) {
+  pv.alpha = 1.f / kKvScale; pv.mode = GM_PV;
+  if (swap) {  // tile M = output dims, N = beam rows; P split on chip
     TcArgs t{};
     static_cast<GemmArgs &>(t) = pv;
     t.mode = GM_PV_T;
-    t.N = pv.M;    // tile N = beam rows
-    t.M = d;       // tile M = output dims
-    t.B = SC;      // P, split on chip (zero past each request's S)
+    t.N = pv.M;
+    t.M = d;
+    t.B = SC;
     t.ldb = p.sc_ld;
-    if (trunk) {
-      t.A = at<float>(ws, p.o_XT);  // (P X): values = the context rows
-      t.lda = p.vt_ld;
-    } else {
-      const __half *v16 = at<__half>(ws, p.o_VTlo);
-      t.a_hi = v16 + (size_t)(i - p.K) * d * p.vt_ld;
-      t.a_lo = t.a_hi + (size_t)nh * d * p.vt_ld;
-      t.lda = p.vt_ld;
-      t.alpha = pv.alpha / kKvScale;
-    }
+    t.a_hi = xt_hi;
+    t.a_lo = xt_lo;
+    t.lda = p.vt_ld;
     if (spl) {
       t.c_hi = Ah;
       t.c_lo = Al;
     }
     GR_TRY(gemm_tc_swapped(t, d, p.vt_ld, R, p.sc_ld, st, spl ? EPI_STORE_T_SPLIT : EPI_STORE_T));
-  } else if (p.tc && VT) {
+  } else {
     TcArgs t{};
     static_cast<GemmArgs &>(t) = pv;
-    t.B = at<float>(ws, p.o_XT);  // trunk: X^T, split on chip
-    if (!trunk) {  // head-layer V^T arrives split (fp16, scaled) from the encoder epilogue
-      const __half *v16 = at<__half>(ws, p.o_VTlo);
-      t.b_hi = v16 + (size_t)(i - p.K) * d * p.vt_ld;
-      t.b_lo = t.b_hi + (size_t)nh * d * p.vt_ld;
-      t.alpha = pv.alpha / kKvScale;
-    }
+    t.b_hi = xt_hi;
+    t.b_lo = xt_lo;
     t.ldb = p.vt_ld;
     if (spl) {
       t.c_hi = Ah;
@@ -781,142 +836,118 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, const WeightsT *
       t.a_lo = Pl;
     }
     GR_TRY(gemm_tc(t, R, p.sc_ld, d, p.vt_ld, spl ? EPI_STORE_SPLIT : EPI_STORE, st));
-  } else {
-    if (trunk) {
-      pv.B = X; pv.ldb = d;
-    } else {
-      pv.B = KV + (size_t)(2 * (i - p.K) + 1) * d; pv.ldb = ldkv;
-    }
-    GR_TRY(gemm(pv, false, EPI_STORE, st));
   }
-  const float *attn = A;
-  if (trunk) {  // (P X) Wv
-    GR_TRY(dense(p, plain_gemm(A, d, w->cross_kv_W + (size_t)(2 * i + 1) * d, ldw, Q, d, R, d, d),
-                 wt ? wt->kv + (size_t)(2 * i + 1) * d * d : nullptr, R, EPI_STORE, st));
-    attn = Q;
-  }
-  GemmArgs o = plain_gemm(attn, d, Lw.cross_Wo, d, Hs, d, R, d, d);
+  GemmArgs o = plain_gemm(A, d, LT.mvo, d, Hs, d, R, d, d);  // h += u (W_v W_o)
   o.R = Hs; o.ldr = d;
   if (spl)
-    GR_TRY(dense_split(p, o, LT->co, Ah, Al, R, EPI_RESID, st));
+    GR_TRY(dense_split(p, o, LT.vo, Ah, Al, R, EPI_RESID, st));
   else
-    GR_TRY(dense(p, o, LT ? LT->co : nullptr, R, EPI_RESID, st));
-  // self-attention over decoded positions (layers.py:92-113)
-  GR_TRY(layer_norm(Lw.ln2_g, Lw.ln2_b));
-  float *qkv_rows = rs.qkv + rs.hist_row0 * 3 * d;
-  const GemmArgs qkv = plain_gemm(N, d, Lw.self_Wqkv, 3 * d, qkv_rows, 3 * d, R, 3 * d, d);
+    GR_TRY(dense(p, o, LT.vo, R, EPI_RESID, st));
+
+  // ---- self-attention over decoded positions (layers.py:92-113) ----------
+  // history row: [q' = n (W_q W_k^T) | n]; keys and values are n itself
+  float *hq = rs.qkv + rs.hist_row0 * p.hist_ld, *hn = hq + d;
   if (spl)
-    GR_TRY(dense_split(p, qkv, LT->sqkv, Nh, Nl, R, EPI_STORE, st));
+    GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln2_g, Lw.ln2_b, R, d, st, hn, p.hist_ld));
   else
-    GR_TRY(dense(p, qkv, LT ? LT->sqkv : nullptr, R, EPI_STORE, st));
-  GR_TRY(self_attn(rs.qkv, 3LL * d, d, rs.anc, rs.anc_stride, (int)rs.hist_row0, R,
-                   rs.npos_u, rs.npos_row, A, d, st, spl ? Ah : nullptr, spl ? Al : nullptr));
-  GemmArgs so = plain_gemm(A, d, Lw.self_Wo, d, Hs, d, R, d, d);
+    GR_TRY(ln_rows(Hs, d, hn, p.hist_ld, Lw.ln2_g, Lw.ln2_b, R, d, st));
+  const GemmArgs sq = spl ? plain_gemm(N, d, LT.msqk, d, hq, p.hist_ld, R, d, d)
+                          : plain_gemm(hn, p.hist_ld, LT.msqk, d, hq, p.hist_ld, R, d, d);
+  if (spl)
+    GR_TRY(dense_split(p, sq, LT.sqk, Nh, Nl, R, EPI_STORE, st));
+  else
+    GR_TRY(dense(p, sq, LT.sqk, R, EPI_STORE, st));
+  GR_TRY(self_attn(rs.qkv, p.hist_ld, d, rs.anc, rs.anc_stride, (int)rs.hist_row0, R, rs.npos_u,
+                   rs.npos_row, A, d, st, spl ? Ah : nullptr, spl ? Al : nullptr, d));
+  GemmArgs so = plain_gemm(A, d, LT.msvo, d, Hs, d, R, d, d);  // h += (P n) (W_v W_o)
   so.R = Hs; so.ldr = d;
   if (spl)
-    GR_TRY(dense_split(p, so, LT->so, Ah, Al, R, EPI_RESID, st));
+    GR_TRY(dense_split(p, so, LT.svo, Ah, Al, R, EPI_RESID, st));
   else
-    GR_TRY(dense(p, so, LT ? LT->so : nullptr, R, EPI_RESID, st));
-  // position-wise FFN (layers.py:115-118)
-  GR_TRY(layer_norm(Lw.ln3_g, Lw.ln3_b));
+    GR_TRY(dense(p, so, LT.svo, R, EPI_RESID, st));
+
+  // ---- position-wise FFN (layers.py:115-118) ------------------------------
+  if (spl)
+    GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln3_g, Lw.ln3_b, R, d, st));
+  else
+    GR_TRY(ln_rows(Hs, d, N, d, Lw.ln3_g, Lw.ln3_b, R, d, st));
   GemmArgs f1 = plain_gemm(N, d, Lw.ffn_W1, p.dff, Fb, p.dff, R, p.dff, d);
   f1.bias = Lw.ffn_b1;
   if (spl)
-    GR_TRY(dense_split(p, f1, LT->w1, Nh, Nl, R, EPI_BIAS_GELU_SPLIT, st, Fh, Fl));
+    GR_TRY(dense_split(p, f1, LT.w1, Nh, Nl, R, EPI_BIAS_GELU_SPLIT, st, Fh, Fl));
   else
-    GR_TRY(dense(p, f1, LT ? LT->w1 : nullptr, R, EPI_BIAS_GELU, st));
+    GR_TRY(dense(p, f1, LT.w1, R, EPI_BIAS_GELU, st));
   GemmArgs f2 = plain_gemm(Fb, p.dff, Lw.ffn_W2, d, Hs, d, R, d, p.dff);
   f2.bias = Lw.ffn_b2; f2.R = Hs; f2.ldr = d;
   const bool dual = spl && split_out;
   if (spl)
-    GR_TRY(dense_split(p, f2, LT->w2, Fh, Fl, R, dual ? EPI_BIAS_RESID_DUAL : EPI_BIAS_RESID, st,
+    GR_TRY(dense_split(p, f2, LT.w2, Fh, Fl, R, dual ? EPI_BIAS_RESID_DUAL : EPI_BIAS_RESID, st,
                        dual ? Nh : nullptr, dual ? Nl : nullptr));
   else
-    GR_TRY(dense(p, f2, LT ? LT->w2 : nullptr, R, EPI_BIAS_RESID, st));
+    GR_TRY(dense(p, f2, LT.w2, R, EPI_BIAS_RESID, st));
   if (split_out) *split_out = dual;
   return GR4AD_OK;
 }
 
-// context projection, head-layer K/V and the trunk (beam.py:159-169): the
-// request-level work every decode of the batch shares
+// context projection, the shared context operands and the trunk
+// (beam.py:159-169): the request-level work every decode of the batch shares
 static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *features,
                             const float *context, void *ws, WeightsT &wt_store,
-                            const WeightsT *&wt, float *&VT, cudaStream_t st) {
+                            const WeightsT *&wt, cudaStream_t st) {
   const int B = p.B, d = p.d, K = p.K;
   float *KV = at<float>(ws, p.o_KV), *Ht = at<float>(ws, p.o_Ht);
+  int *flag = at<int>(ws, p.o_flag);
   if (p.tc) {
     GR_TRY(prep_weights_t(p, w, ws, wt_store, st, !p.weights_prepared));
     wt = &wt_store;
-    VT = at<float>(ws, p.o_VT);
   }
 
   // context projection (decoder.py:134-140) on 32-row-aligned request blocks
   if (!features && !context) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
   const int *in_off = at<int>(ws, p.o_in_off), *ctx_off_d = at<int>(ws, p.o_ctx_off);
   const int *ctx_len_d = at<int>(ws, p.o_ctx_len);
-  const float *X = at<float>(ws, p.o_X);
-  bool x_split = false;  // X also as fp16 hi / lo at o_Xs
+  float *X = at<float>(ws, p.o_X);
+  __half *xs_hi = p.tc ? at<__half>(ws, p.o_Xs) : nullptr;
+  __half *xs_lo = p.tc ? xs_hi + (size_t)p.S_tot * d : nullptr;
+  bool x_split = false;  // kKvScale * X also as fp16 hi / lo at o_Xs
   if (!features) {
-    GR_TRY(pad_rows(context, in_off, ctx_off_d, ctx_len_d, B, d, at<float>(ws, p.o_X), st));
+    GR_TRY(pad_rows(context, in_off, ctx_off_d, ctx_len_d, B, d, X, st));
   } else {
     float *Fin = at<float>(ws, p.o_Fin);
     GR_TRY(pad_rows(features, in_off, ctx_off_d, ctx_len_d, B, p.F, Fin, st));
-    features = Fin;
-    float *Xw = at<float>(ws, p.o_X);
-    GemmArgs g = plain_gemm(features, p.F, w->ctx_W, d, Xw, d, (int)p.S_tot, d, p.F);
+    GemmArgs g = plain_gemm(Fin, p.F, w->ctx_W, d, X, d, (int)p.S_tot, d, p.F);
     g.bias = w->ctx_b;
-    if (p.tc && p.F % 8 == 0 && d % 8 == 0 && tc_eligible(g.lda, g.K, g.K, g.A, wt->ctx)) {
-      // X in fp32 (trunk) and as fp16 hi / lo: the K/V GEMM's A, TMA-only
+    if (p.tc && p.F % 8 == 0 && tc_eligible(g.lda, g.K, g.K, g.A, wt->ctx)) {
       TcArgs t{};
       static_cast<GemmArgs &>(t) = g;
       t.b_hi = wt->ctx;
       t.b_lo = wt->ctx + p.wt_floats;
       t.ldb = g.K;
       t.alpha = g.alpha / kWeightScale;
-      t.c_hi = at<__half>(ws, p.o_Xs);
-      t.c_lo = t.c_hi + (size_t)p.S_tot * d;
+      t.c_hi = xs_hi;
+      t.c_lo = xs_lo;
+      t.c_scale = kKvScale;
+      t.range_flag = flag;
       GR_TRY(gemm_tc(t, p.S_tot, g.K, g.N, g.K, EPI_BIAS_DUAL, st));
       x_split = true;
     } else {
       GR_TRY(dense(p, g, wt ? wt->ctx : nullptr, p.S_tot, EPI_BIAS, st));
     }
   }
-  // encoder K/V of the head layers, once per request and shared by every beam
-  // (beam.py:98-109); on the tensor-core path the epilogue also writes V^T
-  // for the P.V GEMMs, and X^T serves the trunk's (P X) products
-  {
+  if (p.tc) {
+    // the shared context operands of every layer's attention (factored
+    // attention: X stands in for all layers' K and V, beam.py:98-109)
+    if (!x_split) GR_TRY(split16(X, d, xs_hi, xs_lo, d, (int)p.S_tot, d, kKvScale, flag, st));
+    __half *xt_hi = at<__half>(ws, p.o_XTs);
+    GR_TRY(transpose_split16(X, d, xt_hi, xt_hi + (size_t)d * p.vt_ld, p.vt_ld, (int)p.S_tot, d,
+                             kKvScale, flag, st));
+  } else {
+    // encoder K/V of the head layers, once per request and shared by every
+    // beam (beam.py:98-109)
     const int nh = p.L - K;
-    GemmArgs g = plain_gemm(X, d, w->cross_kv_W + (size_t)2 * K * d, 2LL * p.L * d, KV,
-                            2LL * nh * d, (int)p.S_tot, 2 * nh * d, d);
-    if (p.tc && tc_eligible(g.lda, d, d, X, wt->kv)) {
-      TcArgs t{};
-      static_cast<GemmArgs &>(t) = g;
-      t.b_hi = wt->kv + (size_t)2 * K * d * d;
-      t.b_lo = t.b_hi + p.wt_floats;
-      t.ldb = d;
-      t.alpha = g.alpha / kWeightScale;
-      __half *k16 = at<__half>(ws, p.o_KVlo), *v16 = at<__half>(ws, p.o_VTlo);
-      t.k_hi = k16;
-      t.k_lo = k16 + (size_t)p.S_tot * nh * d;
-      t.k_ld = (long long)nh * d;
-      t.vt_hi = v16;
-      t.vt_lo = v16 + (size_t)nh * d * p.vt_ld;
-      t.vt_ld = p.vt_ld;
-      t.kv_scale = kKvScale;
-      t.kv_d = d;
-      t.range_flag = at<int>(ws, p.o_flag);
-      if (x_split) {
-        t.a_hi = at<__half>(ws, p.o_Xs);
-        t.a_lo = t.a_hi + (size_t)p.S_tot * d;
-      }
-      GR_TRY(gemm_tc(t, p.S_tot, d, 2LL * nh * d, d, EPI_KV_SPLIT, st));
-      // (the trunk's X^T: a transpose pass measured no slower than
-      // transposed stores from the context projection's epilogue)
-      if (K > 0) GR_TRY(transpose(X, d, at<float>(ws, p.o_XT), p.vt_ld, (int)p.S_tot, d, st));
-    } else {
-      if (p.tc) return set_err(GR4AD_ERR_UNSUPPORTED, "tensor-core path: unaligned context");
-      GR_TRY(gemm(g, false, EPI_STORE, st));
-    }
+    GR_TRY(gemm(plain_gemm(X, d, w->cross_kv_W + (size_t)2 * K * d, 2LL * p.L * d, KV,
+                           2LL * nh * d, (int)p.S_tot, 2 * nh * d, d),
+                false, EPI_STORE, st));
   }
 
   // trunk: K layers over the n_pos position rows, shared by all beams (beam.py:159-163)
@@ -934,7 +965,9 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
     rs.anc = at<int>(ws, p.o_tanc);
     rs.anc_stride = p.n_pos;
     rs.npos_row = at<int>(ws, p.o_tnpos);
-    for (int i = 0; i < K; ++i) GR_TRY(layer_forward(p, w, wt, i, Ht, rs, ws, KV, VT, st));
+    for (int i = 0; i < K; ++i)
+      GR_TRY(p.tc ? layer_forward_tc(p, w, *wt, i, Ht, rs, ws, st)
+                  : layer_forward(p, w, i, Ht, rs, ws, KV, st));
   }
 
   return GR4AD_OK;
@@ -951,8 +984,8 @@ static bool no_proxy_window() {
 // context projection + shared encoder K/V + trunk + level-0 rows ...
 static int layered_begin(const Plan &p, const gr4ad_weights *w, const float *features,
                          const float *context, void *ws, WeightsT &wt_store, const WeightsT *&wt,
-                         float *&VT, cudaStream_t st) {
-  GR_TRY(encode_and_trunk(p, w, features, context, ws, wt_store, wt, VT, st));
+                         cudaStream_t st) {
+  GR_TRY(encode_and_trunk(p, w, features, context, ws, wt_store, wt, st));
   return init_level0(p.B, at<int>(ws, p.o_live), at<float>(ws, p.o_cum),
                      at<long long>(ws, p.o_prefix), at<int>(ws, p.o_anc), p.stride,
                      at<int>(ws, p.o_tok), st);
@@ -960,7 +993,7 @@ static int layered_begin(const Plan &p, const gr4ad_weights *w, const float *fea
 
 // ... one level step t (t == T: the value re-rank head pass) ...
 static int layered_level(const Plan &p, const gr4ad_weights *w, const gr4ad_batch *bt, int t,
-                         void *ws, const WeightsT *wt, float *VT, cudaStream_t st) {
+                         void *ws, const WeightsT *wt, cudaStream_t st) {
   const int B = p.B, T = p.T, d = p.d, K = p.K;
   int *eff = at<int>(ws, p.o_eff), *cap = at<int>(ws, p.o_cap);
   int *row_off = at<int>(ws, p.o_row_off), *live = at<int>(ws, p.o_live);
@@ -973,7 +1006,7 @@ static int layered_level(const Plan &p, const gr4ad_weights *w, const gr4ad_batc
   float *LG = at<float>(ws, p.o_LG);
   float2 *rinfo = at<float2>(ws, p.o_rinfo);
   float *hist = at<float>(ws, p.o_hist);
-  const size_t hist_layer = (size_t)p.H * 3 * d;
+  const size_t hist_layer = (size_t)p.H * p.hist_ld;
   const int R = (int)p.R[t];
   const long long h0 = p.hist_off[t];
   // token input + gated fusion (beam.py:180-191; layers.py:129-133)
@@ -1019,8 +1052,11 @@ static int layered_level(const Plan &p, const gr4ad_weights *w, const gr4ad_batc
   bool h_split = false;  // the last layer left Hs as fp16 hi / lo in N
   for (int i = K; i < p.L; ++i) {
     rs.qkv = hist + (size_t)(i - K) * hist_layer;
-    GR_TRY(layer_forward(p, w, wt, i, Hs, rs, ws, KV, VT, st,
-                         (i == p.L - 1 && t < T) ? &h_split : nullptr));
+    if (wt)
+      GR_TRY(layer_forward_tc(p, w, *wt, i, Hs, rs, ws, st,
+                              (i == p.L - 1 && t < T) ? &h_split : nullptr));
+    else
+      GR_TRY(layer_forward(p, w, i, Hs, rs, ws, KV, st));
   }
   if (t == T) {  // value re-rank step (beam.py:258-288)
     float *vlog = at<float>(ws, p.o_vlog);
@@ -1161,10 +1197,9 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
   }
   WeightsT wt_store;
   const WeightsT *wt = nullptr;
-  float *VT = nullptr;
-  GR_TRY(layered_begin(p, w, features, context, ws, wt_store, wt, VT, st));
+  GR_TRY(layered_begin(p, w, features, context, ws, wt_store, wt, st));
   const int last = p.rerank ? T : T - 1;
-  for (int t = 0; t <= last; ++t) GR_TRY(layered_level(p, w, bt, t, ws, wt, VT, st));
+  for (int t = 0; t <= last; ++t) GR_TRY(layered_level(p, w, bt, t, ws, wt, st));
   return layered_end(p, bt, out, ws, st);
 }
 
@@ -1292,8 +1327,7 @@ int gr4ad_encode_trunk(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4
   GR_CUDA(cudaMemsetAsync(at<int>(workspace, p.o_flag), 0, sizeof(int), st));
   WeightsT wt_store;
   const WeightsT *wt = nullptr;
-  float *VT = nullptr;
-  return layered_begin(p, w, features, context, workspace, wt_store, wt, VT, st);
+  return layered_begin(p, w, features, context, workspace, wt_store, wt, st);
 }
 
 int gr4ad_level_step(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4ad_batch *batch,
@@ -1306,13 +1340,11 @@ int gr4ad_level_step(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4ad
   cudaStream_t st = (cudaStream_t)stream;
   WeightsT wt_store;
   const WeightsT *wt = nullptr;
-  float *VT = nullptr;
   if (p.tc) {  // the derived weight copies: pointers only (built by encode_trunk / prepare)
     GR_TRY(prep_weights_t(p, w, workspace, wt_store, st, false));
     wt = &wt_store;
-    VT = at<float>(workspace, p.o_VT);
   }
-  return layered_level(p, w, batch, level, workspace, wt, VT, st);
+  return layered_level(p, w, batch, level, workspace, wt, st);
 }
 
 int gr4ad_collect(const gr4ad_dims *dims, const gr4ad_batch *batch, gr4ad_results *out,
@@ -1381,7 +1413,7 @@ int gr4ad_range_status(const gr4ad_dims *dims, const gr4ad_batch *batch, const v
   GR_CUDA(cudaStreamSynchronize(st));
   if (flag)
     return set_err(GR4AD_ERR_RANGE,
-                   "an operand exceeded the fp16 split range (|weight| < 32, |context K/V| < 256): "
+                   "an operand exceeded the fp16 split range (|weight| < 32, |context X| < 256): "
                    "decode with the CUDA-core path (decode_path layered / fused_simt)");
   return GR4AD_OK;
 }
@@ -1428,7 +1460,7 @@ static int score_plan(const gr4ad_dims *dims, const gr4ad_batch *batch, int n_se
   const size_t I = sizeof(int);
   sl.o_tab = take(I * ((size_t)6 * n_seq + (size_t)sl.rows * (3 + n_pos)));
   sl.tab_bytes = I * ((size_t)6 * n_seq + (size_t)sl.rows * (3 + n_pos));
-  sl.o_qkv = take(sizeof(float) * (size_t)sl.rows * 3 * p.d);
+  sl.o_qkv = take(sizeof(float) * (size_t)sl.rows * p.hist_ld);
   sl.total = o;
   return GR4AD_OK;
 }
@@ -1486,8 +1518,7 @@ int gr4ad_score_sequences(const gr4ad_dims *dims, const gr4ad_weights *w, const 
 
   WeightsT wt_store;
   const WeightsT *wt = nullptr;
-  float *VT = nullptr;
-  GR_TRY(encode_and_trunk(p, w, features, context, ws, wt_store, wt, VT, st));
+  GR_TRY(encode_and_trunk(p, w, features, context, ws, wt_store, wt, st));
   float *KV = at<float>(ws, p.o_KV), *Ht = at<float>(ws, p.o_Ht);
   float *Hs = at<float>(ws, p.o_Hs), *U = at<float>(ws, p.o_U), *LG = at<float>(ws, p.o_LG);
   float2 *rinfo = at<float2>(ws, p.o_rinfo);
@@ -1525,7 +1556,9 @@ int gr4ad_score_sequences(const gr4ad_dims *dims, const gr4ad_weights *w, const 
   rs.anc = d_anc;
   rs.anc_stride = np;
   rs.npos_row = d_npos;
-  for (int i = p.K; i < p.L; ++i) GR_TRY(layer_forward(p, w, wt, i, Hs, rs, ws, KV, VT, st));
+  for (int i = p.K; i < p.L; ++i)
+    GR_TRY(wt ? layer_forward_tc(p, w, *wt, i, Hs, rs, ws, st)
+              : layer_forward(p, w, i, Hs, rs, ws, KV, st));
   // per-level logits of position t (decoder.py:189-194) and log-probabilities
   long long hoff = 0;
   for (int t = 0; t < T; ++t) {
@@ -1550,7 +1583,7 @@ int gr4ad_score_sequences(const gr4ad_dims *dims, const gr4ad_weights *w, const 
     GR_CUDA(cudaStreamSynchronize(st));
     if (flag)
       return set_err(GR4AD_ERR_RANGE,
-                     "an operand exceeded the fp16 split range (|weight| < 32, |context K/V| < "
+                     "an operand exceeded the fp16 split range (|weight| < 32, |context X| < "
                      "256): score with the CUDA-core path");
   }
   return GR4AD_OK;

@@ -682,10 +682,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (EPI == EPI_STORE_SPLIT || EPI == EPI_BIAS_GELU_SPLIT || EPI == EPI_BIAS_RESID_DUAL ||
               EPI == EPI_BIAS_DUAL || EPI == EPI_MULVEC_SPLIT) {
             __half hq[4], lq[4];
+            const float cs = a.c_scale != 0.f ? a.c_scale : 1.f;  // (power of two)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              hq[q] = __float2half_rn(x[q]);
-              lq[q] = __float2half_rn(x[q] - __half2float(hq[q]));
+              const float xs = x[q] * cs;
+              if (a.c_scale != 0.f) range_check(xs, a.range_flag);
+              hq[q] = __float2half_rn(xs);
+              lq[q] = __float2half_rn(xs - __half2float(hq[q]));
             }
             const long long o = grow * a.ldc + col;
             if (vec) {

@@ -18,15 +18,17 @@ struct TcArgs : GemmArgs {
   const __half *b_hi, *b_lo;
   // optional: A pre-split likewise (a_hi / a_lo, ld = lda), scale folded into alpha
   const __half *a_hi, *a_lo;
-  // EPI_*_SPLIT: fp16 hi / lo destinations (ld = ldc)
+  // EPI_*_SPLIT: fp16 hi / lo destinations (ld = ldc) of c_scale * C (0: 1);
+  // a nonzero c_scale also range-checks the scaled values into range_flag
   __half *c_hi, *c_lo;
+  float c_scale;
   // EPI_KV_SPLIT: the K part of layer i -> k_hi / k_lo [row][k_ld] at column
   // i d, the V part -> vt_hi / vt_lo [i d + c][vt_ld], all kv_scale * x
   __half *k_hi, *k_lo, *vt_hi, *vt_lo;
   long long k_ld, vt_ld;
   float kv_scale;
   int kv_d;
-  int *range_flag;  // EPI_KV_SPLIT: set when a scaled value leaves the fp16 range
+  int *range_flag;  // EPI_KV_SPLIT / c_scale: set when a scaled value leaves the fp16 range
   // EPI_STORE_LSE: lse_part[row * lse_ld + col / 128] = (max, sum exp(x - max),
   // max of the first 64 columns, max of the last 64) over the row's columns
   // [128 j, 128 j + 128) (merged by lse_merge; the half maxima are the

@@ -1,4 +1,6 @@
 // Row-wise kernels and the exact per-request top-k of the beam step.
+#include <algorithm>
+
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
 
@@ -33,7 +35,8 @@ __global__ void ln_rows_kernel(const float *__restrict__ x, long long ldx, float
 template <int NV>
 __global__ void ln_rows_split_kernel(const float *__restrict__ x, long long ldx, __half *y_hi,
                                      __half *y_lo, long long ldy, const float *__restrict__ g,
-                                     const float *__restrict__ b, int rows, int d) {
+                                     const float *__restrict__ b, int rows, int d, float *y32,
+                                     long long ld32) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= rows) return;
   const float4 *xr = reinterpret_cast<const float4 *>(x + (long long)w * ldx);
@@ -67,19 +70,22 @@ __global__ void ln_rows_split_kernel(const float *__restrict__ x, long long ldx,
     }
     *reinterpret_cast<uint2 *>(y_hi + (long long)w * ldy + j) = *reinterpret_cast<const uint2 *>(h);
     *reinterpret_cast<uint2 *>(y_lo + (long long)w * ldy + j) = *reinterpret_cast<const uint2 *>(l);
+    if (y32)  // the normalised row itself (the factored self-attention's history)
+      *reinterpret_cast<float4 *>(y32 + (long long)w * ld32 + j) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
 int ln_rows_split(const float *x, long long ldx, __half *y_hi, __half *y_lo, long long ldy,
-                  const float *g, const float *b, int rows, int d, cudaStream_t st) {
+                  const float *g, const float *b, int rows, int d, cudaStream_t st, float *y32,
+                  long long ld32) {
   if (rows <= 0) return GR4AD_OK;
-  if (d % 128 != 0 || d > 1024 || ldx % 4 != 0 || ldy % 4 != 0)
+  if (d % 128 != 0 || d > 1024 || ldx % 4 != 0 || ldy % 4 != 0 || (y32 && ld32 % 4 != 0))
     return set_err(GR4AD_ERR_UNSUPPORTED, "split LayerNorm: d %d", d);
   const int nv = d / 128;
 #define GR_LNS(NV)                                                                           \
   case NV:                                                                                   \
     GR_LAUNCH(KC_LAYERNORM, st, ln_rows_split_kernel<NV><<<ceil_div(rows, 8), 256, 0, st>>>(  \
-                                    x, ldx, y_hi, y_lo, ldy, g, b, rows, d));                \
+                                    x, ldx, y_hi, y_lo, ldy, g, b, rows, d, y32, ld32));     \
     return GR4AD_OK;
   switch (nv) {
     GR_LNS(1) GR_LNS(2) GR_LNS(3) GR_LNS(4) GR_LNS(5) GR_LNS(6) GR_LNS(7) GR_LNS(8)
@@ -226,7 +232,7 @@ __global__ void __launch_bounds__(128)
 self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
                  const int *__restrict__ anc, int stride, int hist_row0, int rows,
                  int npos_u, const int *__restrict__ npos_row, float *out,
-                 long long ldo, float scale, __half *out_hi, __half *out_lo) {
+                 long long ldo, float scale, __half *out_hi, __half *out_lo, int v_off) {
   int r = blockIdx.x;
   if (r >= rows) return;
   int g = hist_row0 + r;
@@ -286,7 +292,7 @@ self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
       for (int t = 0; t < kMaxPos; ++t)
         if (t < np) {
           const float4 v4 =
-              *reinterpret_cast<const float4 *>(qkv + (long long)arow[t] * ld3 + 2 * d + j);
+              *reinterpret_cast<const float4 *>(qkv + (long long)arow[t] * ld3 + v_off + j);
           o.x = fmaf(p[t], v4.x, o.x);
           o.y = fmaf(p[t], v4.y, o.y);
           o.z = fmaf(p[t], v4.z, o.z);
@@ -310,7 +316,7 @@ self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
   }
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     float o = 0.f;
-    for (int t = 0; t < np; ++t) o = fmaf(p[t], qkv[(long long)arow[t] * ld3 + 2 * d + j], o);
+    for (int t = 0; t < np; ++t) o = fmaf(p[t], qkv[(long long)arow[t] * ld3 + v_off + j], o);
     out[(long long)r * ldo + j] = o;
   }
 }
@@ -323,7 +329,7 @@ __global__ void __launch_bounds__(256)
 self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
                       const int *__restrict__ anc, int stride, int hist_row0, int rows,
                       int npos_u, const int *__restrict__ npos_row, float *out, long long ldo,
-                      float scale, __half *out_hi, __half *out_lo) {
+                      float scale, __half *out_hi, __half *out_lo, int v_off) {
   const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (r >= rows) return;
   const int g = hist_row0 + r;
@@ -363,7 +369,7 @@ self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
     if (t < np) {
       const float pt = expf(sc[t] - lse);
       const float4 *v4 = reinterpret_cast<const float4 *>(
-          qkv + (long long)anc[(long long)g * stride + t] * ld3 + 2 * d);
+          qkv + (long long)anc[(long long)g * stride + t] * ld3 + v_off);
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
         const float4 v = v4[lane + 32 * i];
@@ -395,8 +401,10 @@ self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
 
 int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_stride,
               int hist_row0, int rows, int npos_uniform, const int *npos_row,
-              float *out, long long ldo, cudaStream_t st, __half *out_hi, __half *out_lo) {
+              float *out, long long ldo, cudaStream_t st, __half *out_hi, __half *out_lo,
+              int v_off) {
   if (rows <= 0) return GR4AD_OK;
+  if (v_off < 0) v_off = 2 * d;
   if (out_hi && (d % 4 != 0 || ld3 % 4 != 0 || ldo % 4 != 0))
     return set_err(GR4AD_ERR_UNSUPPORTED, "split self-attention output: d %d", d);
   const float scale = 1.0f / sqrtf((float)d);
@@ -405,7 +413,8 @@ int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_st
   case NV:                                                                                   \
     GR_LAUNCH(KC_SELF_ATTN, st, self_attn_warp_kernel<NV><<<ceil_div(rows, 8), 256, 0, st>>>( \
                                     qkv, ld3, d, anc, anc_stride, hist_row0, rows,           \
-                                    npos_uniform, npos_row, out, ldo, scale, out_hi, out_lo)); \
+                                    npos_uniform, npos_row, out, ldo, scale, out_hi, out_lo, \
+                                    v_off));                                                 \
     return GR4AD_OK;
     switch (d / 128) {
       GR_SAW(1) GR_SAW(2) GR_SAW(3) GR_SAW(4) GR_SAW(5) GR_SAW(6) GR_SAW(7) GR_SAW(8)
@@ -414,7 +423,7 @@ int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_st
   }
   GR_LAUNCH(KC_SELF_ATTN, st, self_attn_kernel<<<rows, 128, 0, st>>>(qkv, ld3, d, anc, anc_stride, hist_row0, rows,
                                          npos_uniform, npos_row, out, ldo,
-                                         1.0f / sqrtf((float)d), out_hi, out_lo));
+                                         1.0f / sqrtf((float)d), out_hi, out_lo, v_off));
   return GR4AD_OK;
 }
 
@@ -1236,6 +1245,93 @@ int transpose_split16(const float *src, long long lds, __half *dst_hi, __half *d
   dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32));
   GR_LAUNCH(KC_SMALL, st, transpose_split16_kernel<<<grid, dim3(32, 8), 0, st>>>(
                               src, lds, dst_hi, dst_lo, ldd, rows, cols, scale, flag));
+  return GR4AD_OK;
+}
+
+// dst = split of scale * src into fp16 hi + lo (row-major, same shape)
+__global__ void split16_kernel(const float *__restrict__ src, long long lds, __half *dst_hi,
+                               __half *dst_lo, long long ldd, int rows, int cols, float scale,
+                               int *flag) {
+  const long long n = (long long)rows * cols;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cols;
+    const int c = (int)(i - r * cols);
+    const float x = src[r * lds + c] * scale;
+    range_check(x, flag);
+    const __half h = __float2half_rn(x);
+    dst_hi[r * ldd + c] = h;
+    dst_lo[r * ldd + c] = __float2half_rn(x - __half2float(h));
+  }
+}
+
+int split16(const float *src, long long lds, __half *dst_hi, __half *dst_lo, long long ldd,
+            int rows, int cols, float scale, int *flag, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return GR4AD_OK;
+  const long long n = (long long)rows * cols;
+  const int grid = (int)std::min<long long>(ceil_div(n, 256), 148LL * 16);
+  GR_LAUNCH(KC_SMALL, st, split16_kernel<<<grid, 256, 0, st>>>(src, lds, dst_hi, dst_lo, ldd, rows,
+                                                                cols, scale, flag));
+  return GR4AD_OK;
+}
+
+// C (M x N, fp32) = A (M x K) . op(B), op(B) = B (K x N) or B^T (B: N x K),
+// accumulated in double: the snapshot's factored attention weights
+// (W_q W_k^T, W_v W_o) are products of two weight matrices, formed once per
+// snapshot and rounded to fp32 once
+__global__ void __launch_bounds__(256)
+weight_product_kernel(const float *__restrict__ A, long long lda, const float *__restrict__ B,
+                      long long ldb, int trans_b, float *C, long long ldc, int M, int N, int K) {
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int kk = e & 15, mm = e >> 4;  // A: consecutive threads walk k (row-contiguous)
+      const int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < M && k < K) ? (double)A[(long long)m * lda + k] : 0.0;
+      int n, kb;
+      if (trans_b) { kb = kk; n = n0 + mm; }          // B (N x K): walk k
+      else { kb = e >> 6; n = n0 + (e & 63); }        // B (K x N): walk n
+      const int kg = k0 + kb;
+      const double bv = (n < N && kg < K)
+                            ? (double)(trans_b ? B[(long long)n * ldb + kg] : B[(long long)kg * ldb + n])
+                            : 0.0;
+      Bs[kb][trans_b ? mm : (e & 63)] = bv;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = As[kk][ty + 16 * i];
+        b[i] = Bs[kk][tx + 16 * i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+      if (m < M && n < N) C[(long long)m * ldc + n] = (float)acc[i][j];
+    }
+}
+
+int weight_product(const float *A, long long lda, const float *B, long long ldb, bool trans_b,
+                   float *C, long long ldc, int M, int N, int K, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return GR4AD_OK;
+  dim3 grid(ceil_div(N, 64), ceil_div(M, 64));
+  GR_LAUNCH(KC_SMALL, st, weight_product_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, trans_b ? 1 : 0,
+                                                                       C, ldc, M, N, K));
   return GR4AD_OK;
 }
 

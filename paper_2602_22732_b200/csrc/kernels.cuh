@@ -8,8 +8,10 @@ namespace gr {
 
 // LN over rows (layers.py:38-43): y = (x - mean) * (var + 1e-5)^-1/2 * g + b
 // LayerNorm with the output as fp16 hi / lo (d % 128 == 0, d <= 1024)
+// (y32: optionally also the fp32 output, ld ld32)
 int ln_rows_split(const float *x, long long ldx, __half *y_hi, __half *y_lo, long long ldy,
-                  const float *g, const float *b, int rows, int d, cudaStream_t st);
+                  const float *g, const float *b, int rows, int d, cudaStream_t st,
+                  float *y32 = nullptr, long long ld32 = 0);
 int ln_rows(const float *x, long long ldx, float *y, long long ldy, const float *g,
             const float *b, int rows, int d, cudaStream_t st);
 
@@ -23,11 +25,21 @@ int softmax_rows(float *s, long long ld, int rows, const int *row_req,
 
 // self-attention of each row over its ancestor chain (layers.py:101-113 with
 // the history gathered by beam.py:247-248): positions anc[g*stride + tau],
-// tau < npos (npos_row[r] or npos_uniform); q/k/v in a (*, 3d) buffer.
+// tau < npos (npos_row[r] or npos_uniform); per history row (ld ld3) q at
+// column 0, k at column d, v at column v_off (default 2d).  The factored
+// tensor-core path stores [q W_k^T | n] (n = the LayerNorm'd row) and passes
+// v_off = d: k = v = n, the projections folded into its weights.
 int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_stride,
               int hist_row0, int rows, int npos_uniform, const int *npos_row,
               float *out, long long ldo, cudaStream_t st, __half *out_hi = nullptr,
-              __half *out_lo = nullptr);
+              __half *out_lo = nullptr, int v_off = -1);
+
+// dst = fp16 hi / lo split of scale * src (row-major, rows x cols)
+int split16(const float *src, long long lds, __half *dst_hi, __half *dst_lo, long long ldd,
+            int rows, int cols, float scale, int *flag, cudaStream_t st);
+// C = A . op(B) in double, rounded to fp32 (snapshot weight products)
+int weight_product(const float *A, long long lda, const float *B, long long ldb, bool trans_b,
+                   float *C, long long ldc, int M, int N, int K, cudaStream_t st);
 
 // level input (beam.py:180-191): s = bos (t==0) or emb_{t-1}[tok]; K>0 writes
 // s into U[:, d:2d]; K==0 writes H = s + pos[t].

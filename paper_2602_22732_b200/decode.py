@@ -276,7 +276,7 @@ class BeamDecoder:
         if int(flag[0]):
             raise N.RangeError(
                 "libgr4ad: fp16 split range exceeded: an operand exceeded the fp16 split range "
-                "(|weight| < 32, |context K/V| < 256): decode with the CUDA-core path "
+                "(|weight| < 32, |context X| < 256): decode with the CUDA-core path "
                 "(path='layered')")
         return materialize(count[: self.n_requests], toks, score, self.max_out, self.T,
                            self.cfg.level_vocab_sizes)
