@@ -104,11 +104,17 @@ typedef struct {
   /* 0: auto -- the fused per-request kernel when a request's working set
    * fits on chip (d in {16,32}, d_ff in {d,2d}, S <= 32d, widths <= 2048,
    * no masking), else the layered batch path, with tcgen05 3xFP16 GEMMs
-   * when d >= 64 (and d, d_ff, F, V multiples of 4); 1: layered with
-   * CUDA-core GEMMs; 2: fused (its warp-level tensor-core variant -- mma.sync
-   * 3xFP16 -- when d = 16, else CUDA cores); 3: layered with tcgen05 GEMMs;
-   * 4: fused on CUDA cores only.  Forcing an ineligible path returns
-   * GR4AD_ERR_UNSUPPORTED. */
+   * when d >= 64 (d a multiple of 8; d_ff, F, V multiples of 4); 1: layered
+   * with CUDA-core GEMMs; 2: fused (its warp-level tensor-core variant --
+   * mma.sync 3xFP16 -- when d = 16, else CUDA cores); 3: layered with
+   * tcgen05 GEMMs; 4: fused on CUDA cores only; 5: as 3, but the
+   * cross-attention always attends against the projected context X.
+   * On the tcgen05 path (3 / auto), a decode given `features` with
+   * d % 128 == 0, d <= 1024 and F in {4, 8, 16, 32} attends over the
+   * request's F-wide features instead (weight absorption through the linear
+   * context projection, decoder.py:134-140: exact algebra);
+   * given a projected `context` it attends against X.  Forcing an
+   * ineligible path returns GR4AD_ERR_UNSUPPORTED. */
   int decode_path;
   /* 1: the workspace already holds this snapshot's derived weight copies
    * (gr4ad_prepare_weights: fragment-ordered / K-major fp16 hi+lo splits);

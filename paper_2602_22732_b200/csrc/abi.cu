@@ -4,6 +4,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "fused_small.cuh"
@@ -22,13 +23,25 @@ void count_launch() { ++g_launches; }
 struct ProfRec {
   int cls;
   cudaEvent_t a, b;
+  std::string tag;
 };
 static thread_local bool g_prof_on = false;
 static thread_local std::vector<ProfRec> *g_prof = nullptr;
+static thread_local char g_tag[192] = "";
+
+// label of the next launch (shapes), kept with its timing record
+void prof_tag(const char *fmt, ...) {
+  if (!g_prof_on) return;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_tag, sizeof g_tag, fmt, ap);
+  va_end(ap);
+}
 
 void prof_begin(int cls, cudaStream_t st) {
   if (!g_prof_on) return;
-  ProfRec r{cls, nullptr, nullptr};
+  ProfRec r{cls, nullptr, nullptr, std::string(g_tag)};
+  g_tag[0] = 0;
   cudaEventCreate(&r.a);
   cudaEventCreate(&r.b);
   cudaEventRecord(r.a, st);
@@ -85,6 +98,9 @@ struct Plan {
   bool tc = false;
   long long sc_ld = 0, vt_ld = 0;
   size_t o_WT = 0, o_XTs = 0, o_Xs = 0, o_U16 = 0, o_Mf = 0;
+  // latent (weight-absorbed) cross-attention: per layer A^T, B (F x d), c (d)
+  bool lat_ok = false;
+  size_t o_Lat = 0, o_LatTmp = 0;
   long long wt_floats = 0;
   // fused small-model path
   bool fused = false;
@@ -275,6 +291,8 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     return set_err(GR4AD_ERR_VALUE, "bad model dimensions");
   p.B = bt->n_requests;
   if (p.B < 0) return set_err(GR4AD_ERR_VALUE, "n_requests < 0");
+  if (bt->decode_path < 0 || bt->decode_path > 5)
+    return set_err(GR4AD_ERR_VALUE, "decode_path %d outside [0, 5]", bt->decode_path);
   p.T = dm->n_levels;
   p.L = dm->n_layers;
   p.K = bt->trunk_depth >= 0 ? bt->trunk_depth : dm->trunk_depth;
@@ -364,7 +382,8 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   for (int t = 0; t + 1 < T; ++t) n_prefix *= p.V[t];
   const bool mask_fused = !masked || (bt->decode_path != 4 && n_prefix * p.V[T - 1] < (1LL << 31) &&
                                       n_prefix <= (1LL << 24));
-  if (bt->decode_path != 1 && bt->decode_path != 3 && mask_fused && B > 0) p.fused = plan_fused(p);
+  if (bt->decode_path != 1 && bt->decode_path != 3 && bt->decode_path != 5 && mask_fused && B > 0)
+    p.fused = plan_fused(p);
   if (p.fused && bt->decode_path != 4) p.f_mma = plan_fused_mma(p);
   if (p.fused && masked && !p.f_mma) p.fused = false;
   if ((bt->decode_path == 2 || bt->decode_path == 4) && !p.fused)
@@ -372,8 +391,10 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   if (!p.fused) {
     bool ok = p.d % 8 == 0 && p.dff % 4 == 0 && p.F % 4 == 0;
     for (int t = 0; t < T; ++t) ok &= p.V[t] % 4 == 0;
-    p.tc = ok && (bt->decode_path == 3 || (bt->decode_path == 0 && p.d >= 64));
-    if (bt->decode_path == 3 && !ok)
+    const bool forced = bt->decode_path == 3 || bt->decode_path == 5;
+    p.tc = ok && (forced || (bt->decode_path == 0 && p.d >= 64));
+    p.lat_ok = p.tc && bt->decode_path != 5 && latent_supported(p.d, p.F) && p.dff % 8 == 0;
+    if (forced && !ok)
       return set_err(GR4AD_ERR_UNSUPPORTED,
                      "tensor-core path needs d a multiple of 8 and d_ff, F, V multiples of 4");
   }
@@ -465,6 +486,10 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     p.o_XTs = take(H2 * 2 * (size_t)d * p.vt_ld);  // kKvScale X^T as fp16 hi, then lo
     p.o_Xs = take(H2 * 2 * p.S_tot * d);           // kKvScale X as fp16 hi, then lo
     p.o_Mf = take(Fl * 4 * (size_t)p.L * d * d);   // factored attention weights (fp32)
+    if (p.lat_ok) {
+      p.o_Lat = take(Fl * (size_t)p.L * (2 * p.F + 1) * d);
+      p.o_LatTmp = take(Fl * (size_t)(p.F + 1) * d);
+    }
     p.o_U16 = take(H2 * 2 * p.Rw * 2 * d);  // the fuse input [g | s] as fp16 hi, then lo
     p.o_WT = take(H2 * (size_t)p.wt_floats * 2);  // K-major weights: fp16 hi, then lo
   }
@@ -548,11 +573,15 @@ struct RowSet {
 struct LayerT {
   const __half *qk, *vo, *sqk, *svo, *w1, *w2;
   const float *mqk, *mvo, *msqk, *msvo;
+  // latent cross-attention (latent.cu): A^T = (W_q W_k^T W_c^T)^T and
+  // B = W_c W_v W_o (F x d), c = b_c W_v W_o (d)
+  const float *lat_at, *lat_b, *lat_c;
 };
 struct WeightsT {
   const __half *ctx, *wg, *wf, *hv;
   const __half *head[GR4AD_MAX_LEVELS];
   LayerT layer[GR4AD_MAX_LAYERS];
+  bool lat = false;  // this decode attends over the latent (features given)
 };
 
 static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, WeightsT &wt,
@@ -601,6 +630,30 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
     lt.svo = tr(lt.msvo, d, d);
     lt.w1 = tr(Lw.ffn_W1, d, p.dff);
     lt.w2 = tr(Lw.ffn_W2, p.dff, d);
+    lt.lat_at = lt.lat_b = lt.lat_c = nullptr;
+    if (p.lat_ok) {
+      // absorbed through the context projection X = F W_c + b_c, each
+      // product formed in double from the fp32 weights (weight_product)
+      const int F = p.F;
+      float *la = at<float>(ws, p.o_Lat) + (size_t)i * (2 * F + 1) * d;
+      float *tmp = at<float>(ws, p.o_LatTmp), *tv = tmp + (size_t)F * d;
+      lt.lat_at = la;
+      lt.lat_b = la + (size_t)F * d;
+      lt.lat_c = la + (size_t)2 * F * d;
+      if (rc == GR4AD_OK && launch) {
+        rc = weight_product(w->ctx_W, d, Wk, ldw, false, tmp, d, F, d, d, st);  // W_c W_k
+        if (rc == GR4AD_OK)  // A^T = (W_c W_k) W_q^T
+          rc = weight_product(tmp, d, Lw.cross_Wq, d, true, la, d, F, d, d, st);
+        if (rc == GR4AD_OK)  // W_c W_v
+          rc = weight_product(w->ctx_W, d, Wv, ldw, false, tmp, d, F, d, d, st);
+        if (rc == GR4AD_OK)  // B = (W_c W_v) W_o
+          rc = weight_product(tmp, d, Lw.cross_Wo, d, false, la + (size_t)F * d, d, F, d, d, st);
+        if (rc == GR4AD_OK)  // b_c W_v
+          rc = weight_product(w->ctx_b, d, Wv, ldw, false, tv, d, 1, d, d, st);
+        if (rc == GR4AD_OK)  // c = (b_c W_v) W_o
+          rc = weight_product(tv, d, Lw.cross_Wo, d, false, la + (size_t)2 * F * d, d, 1, d, d, st);
+      }
+    }
   }
   return rc;
 }
@@ -751,6 +804,18 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
   const __half *xs_hi = at<__half>(ws, p.o_Xs), *xs_lo = xs_hi + (size_t)p.S_tot * d;
   const __half *xt_hi = at<__half>(ws, p.o_XTs), *xt_lo = xt_hi + (size_t)d * p.vt_ld;
 
+  float *hq = rs.qkv + rs.hist_row0 * p.hist_ld, *hn = hq + d;  // self history [q' | n]
+  if (wt.lat) {
+    // ---- cross-attention over the request's latent (latent.cu) ----------
+    // q_lat = LN1(h) A;  z = softmax(q_lat F^T / sqrt d) F;  h += z B + c;
+    // then LN2 of h (split for the next GEMM, fp32 into the self history)
+    const float *Fin = at<float>(ws, p.o_Fin);
+    GR_TRY(ln_qlat(Hs, d, Lw.ln1_g, Lw.ln1_b, LT.lat_at, R, d, p.F, Q, st));
+    GR_TRY(latent_attn(Q, Fin, p.F, rs.g_row_off, rs.g_rows, ctx_off, ctx_len, n_groups,
+                       rs.max_group_rows, 1.0f / sqrtf((float)d), A, st));
+    GR_TRY(lat_out_ln(Hs, d, A, LT.lat_b, LT.lat_c, Lw.ln2_g, Lw.ln2_b, R, d, p.F, Nh, Nl, d, hn,
+                      p.hist_ld, st));
+  } else {
   // ---- cross-attention into the beam-shared context (layers.py:82-90) ----
   if (spl)
     GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
@@ -846,11 +911,11 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
 
   // ---- self-attention over decoded positions (layers.py:92-113) ----------
   // history row: [q' = n (W_q W_k^T) | n]; keys and values are n itself
-  float *hq = rs.qkv + rs.hist_row0 * p.hist_ld, *hn = hq + d;
   if (spl)
     GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln2_g, Lw.ln2_b, R, d, st, hn, p.hist_ld));
   else
     GR_TRY(ln_rows(Hs, d, hn, p.hist_ld, Lw.ln2_g, Lw.ln2_b, R, d, st));
+  }  // (context-operand cross-attention)
   const GemmArgs sq = spl ? plain_gemm(N, d, LT.msqk, d, hq, p.hist_ld, R, d, d)
                           : plain_gemm(hn, p.hist_ld, LT.msqk, d, hq, p.hist_ld, R, d, d);
   if (spl)
@@ -897,13 +962,20 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
   const int B = p.B, d = p.d, K = p.K;
   float *KV = at<float>(ws, p.o_KV), *Ht = at<float>(ws, p.o_Ht);
   int *flag = at<int>(ws, p.o_flag);
+  if (!features && !context) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
   if (p.tc) {
     GR_TRY(prep_weights_t(p, w, ws, wt_store, st, !p.weights_prepared));
+    wt_store.lat = p.lat_ok && features != nullptr;
     wt = &wt_store;
   }
-
+  if (p.tc && wt_store.lat) {
+    // latent path: the shared context is the request's raw features (32-row
+    // aligned blocks); X = F W_c + b_c is absorbed into the weights and
+    // never formed
+    GR_TRY(pad_rows(features, at<int>(ws, p.o_in_off), at<int>(ws, p.o_ctx_off),
+                    at<int>(ws, p.o_ctx_len), B, p.F, at<float>(ws, p.o_Fin), st));
+  } else {
   // context projection (decoder.py:134-140) on 32-row-aligned request blocks
-  if (!features && !context) return set_err(GR4AD_ERR_VALUE, "either features or context is required");
   const int *in_off = at<int>(ws, p.o_in_off), *ctx_off_d = at<int>(ws, p.o_ctx_off);
   const int *ctx_len_d = at<int>(ws, p.o_ctx_len);
   float *X = at<float>(ws, p.o_X);
@@ -949,6 +1021,7 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
                            2LL * nh * d, (int)p.S_tot, 2 * nh * d, d),
                 false, EPI_STORE, st));
   }
+  }  // (context operands)
 
   // trunk: K layers over the n_pos position rows, shared by all beams (beam.py:159-163)
   if (K > 0) {
@@ -1230,16 +1303,25 @@ int gr4ad_profile_end(double *ms, long long *launches, int n_classes) {
     launches[c] = 0;
   }
   if (!g_prof) return GR4AD_OK;
+  // GR4AD_PROF_DUMP=<path>: append every launch (class, ms, shape tag) -- the
+  // per-launch attribution behind the bench's per-class roofline
+  static const char *dump_path = getenv("GR4AD_PROF_DUMP");
+  FILE *dump = dump_path ? fopen(dump_path, "a") : nullptr;
   for (auto &r : *g_prof) {
     GR_CUDA(cudaEventSynchronize(r.b));
     float t = 0.f;
     GR_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    if (dump) fprintf(dump, "%d\t%.4f\t%s\n", r.cls, t, r.tag.c_str());
     if (r.cls >= 0 && r.cls < n_classes) {
       ms[r.cls] += t;
       launches[r.cls] += 1;
     }
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
+  }
+  if (dump) {
+    fprintf(dump, "--\n");
+    fclose(dump);
   }
   g_prof->clear();
   return GR4AD_OK;
@@ -1324,6 +1406,10 @@ int gr4ad_encode_trunk(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4
   GR_TRY(split_plan(dims, batch, workspace_bytes, p));
   if (p.B == 0) return GR4AD_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  if (p.lat_ok && !features)
+    return set_err(GR4AD_ERR_VALUE,
+                   "per-level decode of this batch attends over the request features: pass "
+                   "features, or decode_path 5 to encode from a projected context");
   GR_CUDA(cudaMemsetAsync(at<int>(workspace, p.o_flag), 0, sizeof(int), st));
   WeightsT wt_store;
   const WeightsT *wt = nullptr;
@@ -1342,6 +1428,7 @@ int gr4ad_level_step(const gr4ad_dims *dims, const gr4ad_weights *w, const gr4ad
   const WeightsT *wt = nullptr;
   if (p.tc) {  // the derived weight copies: pointers only (built by encode_trunk / prepare)
     GR_TRY(prep_weights_t(p, w, workspace, wt_store, st, false));
+    wt_store.lat = p.lat_ok;  // (gr4ad_encode_trunk had the features)
     wt = &wt_store;
   }
   return layered_level(p, w, batch, level, workspace, wt, st);
@@ -1439,12 +1526,13 @@ static int score_plan(const gr4ad_dims *dims, const gr4ad_batch *batch, int n_se
                       ScoreLayout &sl) {
   if (n_seq < 0) return set_err(GR4AD_ERR_VALUE, "n_seq < 0");
   gr4ad_batch b = *batch;
-  b.decode_path = batch->decode_path == 3 ? 3 : (batch->decode_path == 1 ? 1 : 0);
+  const int dp = batch->decode_path;
+  b.decode_path = (dp == 3 || dp == 5) ? dp : (dp == 1 ? 1 : 0);
   if (b.decode_path == 0) b.decode_path = (dims->d >= 64) ? 3 : 1;  // layered paths only
-  if (b.decode_path == 3) {  // tensor path needs alignment; fall back to CUDA cores
-    bool ok = dims->d % 4 == 0 && dims->d_ff % 4 == 0 && dims->feat_dim % 4 == 0;
+  if (b.decode_path == 3 || b.decode_path == 5) {  // tensor path needs alignment
+    bool ok = dims->d % 8 == 0 && dims->d_ff % 4 == 0 && dims->feat_dim % 4 == 0;
     for (int t = 0; t < dims->n_levels; ++t) ok &= dims->vocab[t] % 4 == 0;
-    if (!ok) b.decode_path = batch->decode_path == 3 ? 3 : 1;
+    if (!ok) b.decode_path = (dp == 3 || dp == 5) ? dp : 1;  // (forced: make_plan reports it)
   }
   const int n_pos = dims->n_levels + (batch->value_rerank ? 1 : 0);
   GR_TRY(make_plan(dims, &b, p, (long long)n_seq * n_pos));

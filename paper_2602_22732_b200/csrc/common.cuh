@@ -52,6 +52,7 @@ enum KernelClass {
 // around every launch.
 void count_launch();
 void prof_begin(int cls, cudaStream_t st);
+void prof_tag(const char *fmt, ...);  // label of the next launch (profiling only)
 void prof_end(int cls, cudaStream_t st);
 
 #define GR_LAUNCH(cls, st, ...)          \

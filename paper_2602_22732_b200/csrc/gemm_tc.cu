@@ -904,6 +904,9 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
                     "A=(%lld,%lld) B=(%lld,%lld) presplit=%d asplit=%d\n",
             a.M, a.N, a.K, a.groups, a.mode, epi, a.lda, a.ldb, a.ldc, a_rows, a_cols, b_rows,
             b_cols, a.b_hi != nullptr, a.a_hi != nullptr);
+  prof_tag("tc M=%d N=%d K=%d g=%d mode=%d epi=%d A=%lldx%lld B=%lldx%lld split=%d%d", a.M, a.N,
+           a.K, a.groups, a.mode, epi, a_rows, a_cols, b_rows, b_cols, a.a_hi != nullptr,
+           a.b_hi != nullptr);
   if (epi == EPI_KV_SPLIT && (!a.k_hi || !a.vt_hi))
     return set_err(GR4AD_ERR_UNSUPPORTED, "K|V^T split epilogue needs its fp16 outputs");
   const bool wide = a.N >= 256;
@@ -953,6 +956,8 @@ int gemm_tc_swapped(const TcArgs &a, long long a_rows, long long a_cols, long lo
                     "A=(%lld,%lld) B=(%lld,%lld) presplit=%d asplit=%d swapped=1\n",
             a.M, a.N, a.K, a.groups, a.mode, epi, a.lda, a.ldb, a.ldc, a_rows, a_cols, b_rows,
             b_cols, a.b_hi != nullptr, a.a_hi != nullptr);
+  prof_tag("tcT M=%d N=%d K=%d g=%d mode=%d epi=%d A=%lldx%lld B=%lldx%lld split=%d", a.M, a.N,
+           a.K, a.groups, a.mode, epi, a_rows, a_cols, b_rows, b_cols, a.a_hi != nullptr);
   CUtensorMap ma, mal, mb;
   // N = beam rows per request: the smallest tile that holds them
   const int bn = a.N <= 32 ? 32 : (a.N <= 64 ? 64 : 128);

@@ -56,7 +56,9 @@ def prefix_keys(valid_sids, vocab_sizes):
 
 
 class BeamDecoder:
-    PATHS = {"auto": 0, "layered": 1, "fused": 2, "tensor": 3, "fused_simt": 4}
+    # "tensor_ctx": the tcgen05 path attending against the projected context X
+    # even when features are given (no latent absorption; A/B and parity aid)
+    PATHS = {"auto": 0, "layered": 1, "fused": 2, "tensor": 3, "fused_simt": 4, "tensor_ctx": 5}
 
     @gated
     def __init__(self, model, ctx_lens, widths, trunk_depth=None, value_rerank=False,
@@ -475,7 +477,7 @@ def score_sequences(model, seq_requests, tokens, features=None, contexts=None,
     bt.value_rerank = 1 if include_value_step else 0
     vc = (C.c_int * N.MAX_LEVELS)()
     bt.valid_prefix_count = vc
-    bt.decode_path = {"auto": 0, "layered": 1, "tensor": 3}[path]
+    bt.decode_path = {"auto": 0, "layered": 1, "tensor": 3, "tensor_ctx": 5}[path]
     nbytes = C.c_size_t()
     N.check(N.lib.gr4ad_score_workspace_bytes(C.byref(dims), C.byref(bt), n_seq, C.byref(nbytes)))
     ws = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=dev)

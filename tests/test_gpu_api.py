@@ -66,7 +66,8 @@ def _oracle_of(model):
             {k: v.data for k, v in model.params.items()})
 
 
-@pytest.mark.parametrize("d,path", [(64, "tensor"), (16, "layered")])
+@pytest.mark.parametrize("d,path", [(64, "tensor"), (128, "tensor"), (128, "tensor_ctx"),
+                                    (16, "layered")])
 @pytest.mark.parametrize("rerank", [False, True])
 def test_per_level_entry_points_equal_whole_decode(d, path, rerank):
     """gr4ad_encode_trunk + gr4ad_level_step(t) + gr4ad_collect (SURVEY

@@ -171,10 +171,12 @@ def test_c2_golden_reference(golden_small):
         check_parity(ref, [(sid.tokens, s) for sid, s in got], case["name"])
 
 
-@pytest.mark.parametrize("path", ["tensor", "layered"])
+@pytest.mark.parametrize("path", ["tensor", "tensor_ctx", "layered"])
 def test_c3_golden_reference(golden_c3, path):
     """Full C3 shape: d=1024, L=8, K=5, S=1024, V=4096^3, widths 512^3, on
-    the tcgen05 3xFP16 path (auto for d >= 64) and the CUDA-core path."""
+    the tcgen05 3xFP16 path (auto for d >= 64; latent cross-attention over
+    the features), the same path attending against the projected context
+    X, and the CUDA-core path."""
     M, S = _pkg()
     c = golden_c3["config"]
     cfg = M.DecoderConfig(c["feat_dim"], c["d"], c["d_ff"], c["n_layers"], c["trunk_depth"],
@@ -278,6 +280,37 @@ def test_errors_mirror_reference():
         S.beam_search(model, np.ones((1, 4)), S.BeamSchedule((2,), 2))
     with pytest.raises(ValueError):
         S.beam_search(model, np.ones((1, 4)), S.BeamSchedule((2, 2), 2), trunk_depth=2)
+
+
+@pytest.mark.parametrize("feat_dim", [8, 16, 32])
+def test_latent_and_context_operand_paths(feat_dim):
+    """d=128 (latent-eligible): the tcgen05 path with the cross-attention
+    over the request features (weight absorption), the same batch attending
+    against the projected context X (tensor_ctx), and a projected-context
+    input -- ragged S, per-request widths, value re-rank, K=0 / K=2."""
+    M, S = _pkg()
+    ocfg = orc.OracleConfig(feat_dim, 128, 256, 4, 2, (128, 64, 256), 4, 41 + feat_dim)
+    model = _model(M, ocfg)
+    params = {k: v.data for k, v in model.params.items()}
+    rng = np.random.default_rng(feat_dim)
+    n = 7
+    feats = [rng.normal(size=(int(rng.integers(1, 300)), feat_dim)) for _ in range(n)]
+    widths = [(int(rng.integers(1, 40)), int(rng.integers(1, 100)), int(rng.integers(1, 160)))
+              for _ in range(n)]
+    reps = np.array([0.3, 0.8, 1.6, 2.9])
+    ctx = [orc.context_process(f, params) for f in feats]
+    for k_depth, rerank in ((2, False), (0, True)):
+        want = [orc.beam_search(params, ocfg, ctx[i], widths[i], trunk_depth=k_depth,
+                                value_rerank=rerank, representatives=reps) for i in range(n)]
+        kw = dict(schedules=widths, trunk_depth=k_depth, value_rerank=rerank,
+                  buckets=reps if rerank else None)
+        runs = {"latent": S.beam_search_batch(model, features=feats, path="tensor", **kw),
+                "x_operand": S.beam_search_batch(model, features=feats, path="tensor_ctx", **kw),
+                "context_in": S.beam_search_batch(model, contexts=ctx, path="tensor", **kw)}
+        for name, got in runs.items():
+            for i in range(n):
+                check_parity(want[i], [(sid.tokens, s) for sid, s in got[i]],
+                             f"F={feat_dim} {name} K={k_depth}[{i}]")
 
 
 def test_tensor_path_mid_model():
