@@ -258,16 +258,20 @@ def class_work(cfgd):
     n_trunk = B * T if K > 0 else 0
     head_rows = sum(R[:T])
     layer_rows = K * n_trunk + (L - K) * head_rows
-    # executed on the tensor-core path (factored attention, abi.cu
-    # layer_forward_tc): no encoder K/V; per layer row the folded
-    # attention products n (Wq Wk^T), u (Wv Wo) for the cross- and the
-    # self-attention (4 d^2 MAC) plus the FFN (2 d dff MAC)
-    gemm = B * 2 * S * F * d + layer_rows * (8 * d * d + 4 * d * dff)
+    # executed on the tcgen05 path with features input (abi.cu
+    # layer_forward_tc, latent cross-attention): no context projection and no
+    # encoder K/V; per layer row the self-attention's folded products
+    # n (Wq Wk^T) and u (Wv Wo) (2 d^2 MAC) plus the FFN (2 d dff MAC); the
+    # cross-attention runs on CUDA cores over the F-wide latent
+    # (latent_attn: q.F^T and P.F, 4 S F flop per row, mma.sync) between
+    # its absorbed d x F / F x d projections (two thin GEMMs, 4 d F flop)
+    gemm = layer_rows * (4 * d * d + 4 * d * dff + 4 * d * F)
     gemm += sum(R[t] * ((6 * d * d if K > 0 else 0) + 2 * d * V[t]) for t in range(T))
-    attn = layer_rows * 4 * S * d
+    attn = layer_rows * 4 * S * F
     topk = sum(R[t] * V[t] * 4 + R[t] * 12 + R[t + 1] * (20 + 8 * (t + 2)) for t in range(T))
-    soft = layer_rows * S * 8
-    ln = layer_rows * 3 * 8 * d
+    soft = 0
+    # LN1 / LN3 (h in, fp16 hi / lo out), LN2 (h in, hi / lo + fp32 history out)
+    ln = layer_rows * 28 * d
     # q' and the normalised history rows n (fp32), the output as fp16 hi / lo
     sattn = K * n_trunk * 4 * (2 * d + d * T) + (L - K) * sum(
         R[t] * 4 * (2 * d + d * (t + 1)) for t in range(T))

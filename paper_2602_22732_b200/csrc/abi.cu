@@ -413,6 +413,10 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     for (int i = 0; i < p.L; ++i) {  // qk, vo, self qk, self vo, W1, W2
       add(D * D); add(D * D); add(D * D); add(D * D); add(p.dff * D); add(D * p.dff);
     }
+    if (p.lat_ok)
+      for (int i = 0; i < p.L; ++i) {  // latent A^T, B^T
+        add((long long)p.F * D); add((long long)p.F * D);
+      }
   }
 
   // ---- workspace layout ----
@@ -576,6 +580,9 @@ struct LayerT {
   // latent cross-attention (latent.cu): A^T = (W_q W_k^T W_c^T)^T and
   // B = W_c W_v W_o (F x d), c = b_c W_v W_o (d)
   const float *lat_at, *lat_b, *lat_c;
+  // their K-major fp16 hi / lo copies: q_lat = n A (B operand A^T, F x d)
+  // and h += z B + c (B operand B^T, d x F)
+  const __half *lat_q16, *lat_o16;
 };
 struct WeightsT {
   const __half *ctx, *wg, *wf, *hv;
@@ -631,6 +638,7 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
     lt.w1 = tr(Lw.ffn_W1, d, p.dff);
     lt.w2 = tr(Lw.ffn_W2, p.dff, d);
     lt.lat_at = lt.lat_b = lt.lat_c = nullptr;
+    lt.lat_q16 = lt.lat_o16 = nullptr;
     if (p.lat_ok) {
       // absorbed through the context projection X = F W_c + b_c, each
       // product formed in double from the fp32 weights (weight_product)
@@ -653,6 +661,15 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
         if (rc == GR4AD_OK)  // c = (b_c W_v) W_o
           rc = weight_product(tv, d, Lw.cross_Wo, d, false, la + (size_t)2 * F * d, d, 1, d, d, st);
       }
+      // K-major fp16 splits: the q_lat GEMM's B operand is A^T itself, the
+      // output GEMM's is B^T
+      __half *q16 = base + o;
+      o += ((long long)F * d + 63) / 64 * 64;
+      if (rc == GR4AD_OK && launch)
+        rc = split16(la, d, q16, q16 + p.wt_floats, d, F, d, kWeightScale, at<int>(ws, p.o_flag),
+                     st);
+      lt.lat_q16 = q16;
+      lt.lat_o16 = tr(lt.lat_b, F, d);
     }
   }
   return rc;
@@ -810,11 +827,18 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
     // q_lat = LN1(h) A;  z = softmax(q_lat F^T / sqrt d) F;  h += z B + c;
     // then LN2 of h (split for the next GEMM, fp32 into the self history)
     const float *Fin = at<float>(ws, p.o_Fin);
-    GR_TRY(ln_qlat(Hs, d, Lw.ln1_g, Lw.ln1_b, LT.lat_at, R, d, p.F, Q, st));
-    GR_TRY(latent_attn(Q, Fin, p.F, rs.g_row_off, rs.g_rows, ctx_off, ctx_len, n_groups,
-                       rs.max_group_rows, 1.0f / sqrtf((float)d), A, st));
-    GR_TRY(lat_out_ln(Hs, d, A, LT.lat_b, LT.lat_c, Lw.ln2_g, Lw.ln2_b, R, d, p.F, Nh, Nl, d, hn,
-                      p.hist_ld, st));
+    const int F = p.F;
+    GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
+    GR_TRY(dense_split(p, plain_gemm(N, d, LT.lat_at, d, Q, F, R, F, d), LT.lat_q16, Nh, Nl, R,
+                       EPI_STORE, st));
+    GR_TRY(latent_attn(Q, Fin, F, rs.g_row_off, rs.g_rows, ctx_off, ctx_len, n_groups,
+                       rs.max_group_rows, 1.0f / sqrtf((float)d), A, at<int>(ws, p.o_flag), st));
+    GemmArgs go = plain_gemm(A, F, LT.lat_b, d, Hs, d, R, d, F);  // h += z B + c
+    go.bias = LT.lat_c;
+    go.R = Hs;
+    go.ldr = d;
+    GR_TRY(dense(p, go, LT.lat_o16, R, EPI_BIAS_RESID, st));
+    GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln2_g, Lw.ln2_b, R, d, st, hn, p.hist_ld));
   } else {
   // ---- cross-attention into the beam-shared context (layers.py:82-90) ----
   if (spl)

@@ -82,6 +82,7 @@ int ln_rows_split(const float *x, long long ldx, __half *y_hi, __half *y_lo, lon
   if (d % 128 != 0 || d > 1024 || ldx % 4 != 0 || ldy % 4 != 0 || (y32 && ld32 % 4 != 0))
     return set_err(GR4AD_ERR_UNSUPPORTED, "split LayerNorm: d %d", d);
   const int nv = d / 128;
+  prof_tag("ln_split rows=%d", rows);
 #define GR_LNS(NV)                                                                           \
   case NV:                                                                                   \
     GR_LAUNCH(KC_LAYERNORM, st, ln_rows_split_kernel<NV><<<ceil_div(rows, 8), 256, 0, st>>>(  \
@@ -408,6 +409,7 @@ int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_st
   if (out_hi && (d % 4 != 0 || ld3 % 4 != 0 || ldo % 4 != 0))
     return set_err(GR4AD_ERR_UNSUPPORTED, "split self-attention output: d %d", d);
   const float scale = 1.0f / sqrtf((float)d);
+  prof_tag("self_attn rows=%d", rows);
   if (d % 128 == 0 && d <= 1024 && ld3 % 4 == 0 && ldo % 4 == 0) {
 #define GR_SAW(NV)                                                                           \
   case NV:                                                                                   \

@@ -39,14 +39,9 @@ int split16(const float *src, long long lds, __half *dst_hi, __half *dst_lo, lon
             int rows, int cols, float scale, int *flag, cudaStream_t st);
 // latent (weight-absorbed) cross-attention (latent.cu): F = feature width
 bool latent_supported(int d, int F);
-int ln_qlat(const float *x, long long ldx, const float *g, const float *b, const float *AT,
-            int rows, int d, int F, float *q, cudaStream_t st);
 int latent_attn(const float *q, const float *feats, int F, const int *g_row_off, const int *g_rows,
                 const int *g_ctx_off, const int *g_ctx_len, int n_groups, int max_group_rows,
-                float scale, float *z, cudaStream_t st);
-int lat_out_ln(float *h, long long ldh, const float *z, const float *B, const float *c,
-               const float *g, const float *b, int rows, int d, int F, __half *y_hi,
-               __half *y_lo, long long ldy, float *y32, long long ld32, cudaStream_t st);
+                float scale, float *z, int *flag, cudaStream_t st);
 // C = A . op(B) in double, rounded to fp32 (snapshot weight products)
 int weight_product(const float *A, long long lda, const float *B, long long ldb, bool trans_b,
                    float *C, long long ldc, int M, int N, int K, cudaStream_t st);
