@@ -266,7 +266,8 @@ def class_work(cfgd):
     # (latent_attn: q.F^T and P.F, 4 S F flop per row, mma.sync) between
     # its absorbed d x F / F x d projections (two thin GEMMs, 4 d F flop)
     gemm = layer_rows * (4 * d * d + 4 * d * dff + 4 * d * F)
-    gemm += sum(R[t] * ((6 * d * d if K > 0 else 0) + 2 * d * V[t]) for t in range(T))
+    # the fuse: one d x d GEMM per level row (token-side products tabulated)
+    gemm += sum(R[t] * ((2 * d * d if K > 0 else 0) + 2 * d * V[t]) for t in range(T))
     attn = layer_rows * 4 * S * F
     topk = sum(R[t] * V[t] * 4 + R[t] * 12 + R[t + 1] * (20 + 8 * (t + 2)) for t in range(T))
     soft = 0

@@ -101,6 +101,10 @@ struct Plan {
   // latent (weight-absorbed) cross-attention: per layer A^T, B (F x d), c (d)
   bool lat_ok = false;
   size_t o_Lat = 0, o_LatTmp = 0;
+  // token-side fuse tables per level t (K > 0): s W_g and s W_f[d:2d] for
+  // every possible s (bos at t = 0, emb_{t-1} rows after)
+  size_t o_FuseT[GR4AD_MAX_LEVELS + 1] = {};
+  int fuse_n[GR4AD_MAX_LEVELS + 1] = {};
   long long wt_floats = 0;
   // fused small-model path
   bool fused = false;
@@ -413,6 +417,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     for (int i = 0; i < p.L; ++i) {  // qk, vo, self qk, self vo, W1, W2
       add(D * D); add(D * D); add(D * D); add(D * D); add(p.dff * D); add(D * p.dff);
     }
+    add(D * D);  // W_f[0:d] (the fuse GEMM on the gathered gate)
     if (p.lat_ok)
       for (int i = 0; i < p.L; ++i) {  // latent A^T, B^T
         add((long long)p.F * D); add((long long)p.F * D);
@@ -495,6 +500,11 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
       p.o_LatTmp = take(Fl * (size_t)(p.F + 1) * d);
     }
     p.o_U16 = take(H2 * 2 * p.Rw * 2 * d);  // the fuse input [g | s] as fp16 hi, then lo
+    if (p.K > 0)
+      for (int t = 0; t < p.n_pos; ++t) {
+        p.fuse_n[t] = t == 0 ? 1 : p.V[t - 1];
+        p.o_FuseT[t] = take(Fl * 2 * (size_t)p.fuse_n[t] * d);
+      }
     p.o_WT = take(H2 * (size_t)p.wt_floats * 2);  // K-major weights: fp16 hi, then lo
   }
   p.total = o;
@@ -586,6 +596,9 @@ struct LayerT {
 };
 struct WeightsT {
   const __half *ctx, *wg, *wf, *hv;
+  const __half *wf_top;  // K-major W_f[0:d]
+  // per level t: [s W_g | s W_f[d:2d]] for every token s (fp32, 2 x n_t x d)
+  const float *fuse_tab[GR4AD_MAX_LEVELS + 1];
   const __half *head[GR4AD_MAX_LEVELS];
   LayerT layer[GR4AD_MAX_LAYERS];
   bool lat = false;  // this decode attends over the latent (features given)
@@ -615,6 +628,22 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
   wt.ctx = tr(w->ctx_W, p.F, d);
   wt.wg = tr(w->fuse_Wg, d, d);
   wt.wf = tr(w->fuse_Wf, 2 * d, d);
+  wt.wf_top = tr(w->fuse_Wf, d, d);
+  for (int t = 0; t <= GR4AD_MAX_LEVELS; ++t) wt.fuse_tab[t] = nullptr;
+  if (p.K > 0)
+    for (int t = 0; t < p.n_pos; ++t) {
+      // the token side of the fuse (layers.py:129-133) is a function of the
+      // token alone: s W_g and s W_f[d:2d] tabulated once per snapshot
+      float *tab = at<float>(ws, p.o_FuseT[t]);
+      const int n = p.fuse_n[t];
+      const float *S = t == 0 ? w->bos : w->emb[t - 1];
+      wt.fuse_tab[t] = tab;
+      if (rc == GR4AD_OK && launch)
+        rc = weight_product(S, d, w->fuse_Wg, d, false, tab, d, n, d, d, st);
+      if (rc == GR4AD_OK && launch)
+        rc = weight_product(S, d, w->fuse_Wf + (size_t)d * d, d, false, tab + (size_t)n * d, d, n,
+                            d, d, st);
+    }
   for (int t = 0; t < p.T; ++t) wt.head[t] = tr(w->head[t], d, p.V[t]);
   wt.hv = tr(w->head_value, d, p.nb);
   float *Mf = at<float>(ws, p.o_Mf);
@@ -1109,18 +1138,16 @@ static int layered_level(const Plan &p, const gr4ad_weights *w, const gr4ad_batc
   // token input + gated fusion (beam.py:180-191; layers.py:129-133)
   const float *emb_prev = t > 0 ? w->emb[t - 1] : nullptr;
   if (K > 0 && p.tc && wt && d % 8 == 0) {
-    // the fuse on pre-split operands: s (and the gate product g) as fp16
-    // hi / lo, so both GEMMs run TMA-only (CTA pairs)
+    // h = [m (s W_g) | s] W_f = (m (s W_g)) W_f[0:d] + s W_f[d:2d]: the
+    // token-side products come from the per-snapshot tables (one d x d GEMM
+    // per row instead of three)
     __half *Uh = at<__half>(ws, p.o_U16), *Ul = Uh + (size_t)p.Rw * 2 * d;
-    GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, nullptr, nullptr, nullptr, st, Uh,
-                       Ul));
-    GemmArgs gg = plain_gemm(nullptr, 2LL * d, w->fuse_Wg, d, nullptr, 2LL * d, R, d, d);
-    gg.vec = Ht + (size_t)t * d;
-    gg.vec_ld = (long long)p.n_pos * d;
-    gg.row_req = row_req + h0;
-    GR_TRY(dense_split(p, gg, wt->wg, Uh + d, Ul + d, R, EPI_MULVEC_SPLIT, st, Uh, Ul));
-    GR_TRY(dense_split(p, plain_gemm(nullptr, 2LL * d, w->fuse_Wf, d, Hs, d, R, d, 2 * d), wt->wf,
-                       Uh, Ul, R, EPI_STORE, st));
+    GR_TRY(fuse_gather(t, R, d, tok + h0, wt->fuse_tab[t], p.fuse_n[t], Ht + (size_t)t * d,
+                       (long long)p.n_pos * d, row_req + h0, Hs, Uh, Ul, st));
+    GemmArgs gf = plain_gemm(nullptr, d, w->fuse_Wf, d, Hs, d, R, d, d);
+    gf.R = Hs;
+    gf.ldr = d;
+    GR_TRY(dense_split(p, gf, wt->wf_top, Uh, Ul, R, EPI_RESID, st));
   } else if (K > 0) {
     GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, nullptr, U, nullptr, st));
     GemmArgs gg = plain_gemm(U + d, 2LL * d, w->fuse_Wg, d, U, 2LL * d, R, d, d);

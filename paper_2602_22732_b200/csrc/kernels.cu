@@ -473,6 +473,45 @@ __global__ void level_input_split4_kernel(int t, int rows, int d, const float *_
   *reinterpret_cast<uint2 *>(Ul + o) = *reinterpret_cast<const uint2 *>(lq);
 }
 
+// the fuse's gathered inputs (layers.py:129-133 with the token-side
+// products tabulated): H = (s W_f[d:2d])[tok], (Uh, Ul) = split of
+// m_t[req] * (s W_g)[tok] (ld d); four columns per thread
+__global__ void fuse_gather_kernel(int t, int rows, int d, const int *__restrict__ tok,
+                                   const float *__restrict__ tab, int n_tok,
+                                   const float *__restrict__ m, long long m_ld,
+                                   const int *__restrict__ row_req, float *H, __half *Uh,
+                                   __half *Ul) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int d4 = d / 4;
+  if (i >= (long long)rows * d4) return;
+  const int r = (int)(i / d4), j = (int)(i - (long long)r * d4) * 4;
+  const long long k = t == 0 ? 0 : tok[r];
+  const float4 g = *reinterpret_cast<const float4 *>(tab + k * d + j);
+  const float4 f = *reinterpret_cast<const float4 *>(tab + ((long long)n_tok + k) * d + j);
+  const float4 mm = *reinterpret_cast<const float4 *>(m + (long long)row_req[r] * m_ld + j);
+  *reinterpret_cast<float4 *>(H + (long long)r * d + j) = f;
+  const float gv[4] = {mm.x * g.x, mm.y * g.y, mm.z * g.z, mm.w * g.w};
+  __align__(8) __half hq[4], lq[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    hq[q] = __float2half_rn(gv[q]);
+    lq[q] = __float2half_rn(gv[q] - __half2float(hq[q]));
+  }
+  *reinterpret_cast<uint2 *>(Uh + (long long)r * d + j) = *reinterpret_cast<const uint2 *>(hq);
+  *reinterpret_cast<uint2 *>(Ul + (long long)r * d + j) = *reinterpret_cast<const uint2 *>(lq);
+}
+
+int fuse_gather(int t, int rows, int d, const int *tok, const float *tab, int n_tok,
+                const float *m, long long m_ld, const int *row_req, float *H, __half *Uh,
+                __half *Ul, cudaStream_t st) {
+  const long long n4 = (long long)rows * (d / 4);
+  if (n4 <= 0) return GR4AD_OK;
+  if (d % 4 != 0) return set_err(GR4AD_ERR_UNSUPPORTED, "fuse gather: d %d", d);
+  GR_LAUNCH(KC_SMALL, st, fuse_gather_kernel<<<ceil_div(n4, 256), 256, 0, st>>>(
+                              t, rows, d, tok, tab, n_tok, m, m_ld, row_req, H, Uh, Ul));
+  return GR4AD_OK;
+}
+
 int level_input(int t, int rows, int d, const float *bos, const float *emb_prev,
                 const int *tok, const float *pos_t, float *U, float *H,
                 cudaStream_t st, __half *Uh, __half *Ul) {

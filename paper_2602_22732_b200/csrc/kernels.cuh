@@ -52,6 +52,12 @@ int level_input(int t, int rows, int d, const float *bos, const float *emb_prev,
                 const int *tok, const float *pos_t, float *U, float *H,
                 cudaStream_t st, __half *Uh = nullptr, __half *Ul = nullptr);
 
+// fuse inputs from the per-snapshot token tables (tab: [s W_g | s W_f[d:2d]],
+// 2 x n_tok x d): H = tab_f[tok], (Uh, Ul) = split of m[req] * tab_g[tok]
+int fuse_gather(int t, int rows, int d, const int *tok, const float *tab, int n_tok,
+                const float *m, long long m_ld, const int *row_req, float *H, __half *Uh,
+                __half *Ul, cudaStream_t st);
+
 // per-row (max, log sum exp(x - max)) (beam.py:92-95)
 int lse_merge(const float4 *part, int n_part, int rows, float2 *info, cudaStream_t st);
 int row_lse(const float *logits, long long ld, int rows, int V, float2 *info,
