@@ -387,6 +387,10 @@ def main():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    # user-sharded job size: total synthetic requests routed by
+    # FNV-1a(user id) % world, decoded per rank in batches of --batch; one step
+    # = every rank's whole shard.  Default: one batch per GPU (batch x world users)
+    ap.add_argument("--requests", type=int, default=None)
     args = ap.parse_args()
     cfgd = dict(CONFIGS[args.config])
     if args.batch:
@@ -402,10 +406,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (GR4AD_DIST_BACKEND=gloo lets tests run several ranks on one GPU)
+    backend = os.environ.get("GR4AD_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_2602_22732_b200 import _native as N
     from paper_2602_22732_b200.decode import BeamDecoder
@@ -414,20 +424,43 @@ def main():
     F, d, dff, L, K, V, nb = cfgd["model"]
     cfg = DecoderConfig(F, d, dff, L, K, V, nb, seed=2)
     model = DecoderModel(cfg)
-    B, S, widths = cfgd["batch"], cfgd["S"], cfgd["widths"]
-    dec = BeamDecoder(model, [S] * B, [widths] * B, device=dev)
+    Bcfg, S, widths = cfgd["batch"], cfgd["S"], cfgd["widths"]
+    # ---- user-sharded requests: stable FNV-1a routing ----------
+    from paper_2602_22732_b200 import sharding as SH
+    n_total = args.requests or Bcfg * world
+    users = [f"user{i:06d}" for i in range(n_total)]
+    n_mine = len(SH.partition(users, world)[rank])
+    if args.requests:
+        sizes = [Bcfg] * (n_mine // Bcfg) + ([n_mine % Bcfg] if n_mine % Bcfg else [])
+    else:
+        sizes = [n_mine]  # one (ragged) batch per rank
+    B = max(sizes)  # the main decoder's batch
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
-    feats = torch.randn((B * S, F), generator=gen, device=dev, dtype=torch.float32)
+    decoders = {}
+    for n in sorted(set(sizes)):
+        dn = BeamDecoder(model, [S] * n, [widths] * n, device=dev)
+        fn = torch.randn((n * S, F), generator=gen, device=dev, dtype=torch.float32)
+        decoders[n] = (dn, fn)
+    dec, feats = decoders[B]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     N.lib.gr4ad_take_launch_count()
     dec.run(features=feats)
-    launches_per_step = int(N.lib.gr4ad_take_launch_count())
+    launches_per_batch = int(N.lib.gr4ad_take_launch_count())
+    launches_per_step = launches_per_batch * len(sizes)
     torch.cuda.synchronize(dev)
     if not args.no_graph:
-        dec.capture(features=feats)
-    step = dec.replay if not args.no_graph else (lambda: dec.run(features=feats))
+        for dn, fn in decoders.values():
+            dn.capture(features=fn)
+
+    def step():
+        for n in sizes:
+            dn, fn = decoders[n]
+            if args.no_graph:
+                dn.run(features=fn)
+            else:
+                dn.replay()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -455,7 +488,12 @@ def main():
     if world > 1:
         dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
     ms_per_step = float(tot_ms.item()) / args.steps
-    value = world * B / (ms_per_step / 1000.0)
+    value = n_total / (ms_per_step / 1000.0)
+    # requests of the main batch summed over ranks (the e2e / API legs run it)
+    n_main = torch.tensor([B], device=dev, dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(n_main)
+    n_main = int(n_main.item())
 
     # ---- end to end through the C ABI with host buffers --------------------
     # Every step copies its own features pinned-host -> HBM and its results
@@ -531,7 +569,7 @@ def main():
     e2e_s = torch.tensor([best], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_value = world * B * e2e_steps / float(e2e_s.item())
+    e2e_value = n_main * e2e_steps / float(e2e_s.item())
     clk = clocks.stop()
 
     # ---- end to end through the drop-in Python API ------------------------
@@ -566,7 +604,7 @@ def main():
         api_t = torch.tensor([api_s], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(api_t, op=dist.ReduceOp.MAX)
-        api = {"value": world * B / float(api_t.item()), "unit": "req/s",
+        api = {"value": n_main / float(api_t.item()), "unit": "req/s",
                "ms_per_step": 1e3 * float(api_t.item()),
                "h2d_bytes_per_step": B * S * F * 4,
                "d2h_bytes_per_step": d2h + 4,
@@ -577,10 +615,23 @@ def main():
                       "calls (pooled decoder + CUDA graph replay; host staging, H2D, decode, "
                       "D2H, bulk SemanticId build inside each call)"}
 
-    # ---- results sanity (gathered: NCCL only moves results/stats) ------------
+    # ---- results: gathered to rank 0 (NCCL point-to-point), stats all-reduced
     cnt = dec.count[:B].to(torch.int64).sum().reshape(1)
+    stats = {"requests": n_mine * args.steps, "results": int(cnt.item())}
+    sharding = None
     if world > 1:
-        dist.all_reduce(cnt)
+        got = SH.gather_decoded(dec.count, dec.tokens, dec.score, B)
+        stats = SH.all_reduce_stats(stats, device=dev)
+        if rank == 0:
+            gathered = sum(int(c.to(torch.int64).sum().item()) for c, _, _ in got)
+            if gathered != stats["results"]:
+                raise RuntimeError(f"gathered {gathered} results, all-reduced {stats['results']}")
+            sharding = {"route": "FNV-1a(user id) % world (sharding.shard_of)",
+                        "users": n_total, "per_rank": [int(c.numel()) for c, _, _ in got],
+                        "gathered_results": gathered, "stats": stats,
+                        "collectives": "results: NCCL send/recv to rank 0; counters: one "
+                                       "all-reduce; no data-path collective"}
+    cnt = torch.tensor([stats["results"]], device=dev)
     flops = _flops_per_request(cfgd["model"], S, widths)
 
     line = None
@@ -608,7 +659,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (random-init weights seed 2, N(0,1) features)",
-            "config": {"workload": cfgd["name"], "batch_per_gpu": B, "global_batch": B * world,
+            "config": {"workload": cfgd["name"], "batch_per_gpu": B, "global_batch": n_total,
+                       "requests_per_step": n_total, "batches_per_rank": len(sizes),
                        "ctx_len": S, "widths": list(widths),
                        "parallelism": f"user-sharded x{world} (replicas, no data-path collective)",
                        "l2": "flushed (256 MiB write) between timed steps",
@@ -628,10 +680,11 @@ def main():
                            "steps (>= K, >= ~50 ms of device work)",
                     "e2e_steps": e2e_steps},
             "e2e_api": api,
-            "gpu_launches": launches_per_step * (args.steps * 2 + e2e_steps * E2E_WINDOWS
-                                                 + api_steps),
-            "gpu_launches_note": "per-step launches x (device-timed K + serial e2e K + 5 "
-                                 "pipelined e2e windows of e2e_steps + e2e_api steps) steps",
+            "gpu_launches": launches_per_step * args.steps + launches_per_batch * (
+                args.steps + e2e_steps * E2E_WINDOWS + api_steps),
+            "gpu_launches_note": "per-step launches x device-timed K + per-batch launches x "
+                                 "(serial e2e K + 5 pipelined e2e windows of e2e_steps + "
+                                 "e2e_api steps)",
             "launches_per_step": launches_per_step,
             "algorithmic_tflops": flops * value / 1e12,
             "results_per_step": int(cnt.item()),
@@ -639,6 +692,7 @@ def main():
             "wall_s_timed": wall,
             "roofline": roof,
             "cpu_baseline": cpu,
+            "sharding": sharding,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

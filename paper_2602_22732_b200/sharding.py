@@ -7,8 +7,11 @@ entries (keyed by ``(user_id, index.version)``, engine.py:93) stay on one
 GPU.  The only collectives move results and counters (NCCL over NVLink on
 GPUs, gloo on CPU for tests):
 
-* ``gather_results`` -- one gather of fixed-size result tensors to rank 0
-  (int32 tokens [n, max_out, T], fp64 scores [n, max_out], int32 counts);
+* ``gather_decoded`` -- the decoder's device result tensors (int32 counts,
+  int32 tokens [n, max_out, T], fp64 scores [n, max_out]) of every rank sent
+  point-to-point to rank 0 (NCCL send / recv over NVLink): only rank 0
+  receives, ~(4 T + 8) max_out bytes per request;
+* ``gather_results`` -- the same for host result lists (the engine's);
 * ``all_reduce_stats`` -- one all-reduce of a small int64 counter vector.
 """
 
@@ -91,6 +94,65 @@ def gather_results(local_results, n_levels, max_out, n_local_max, device=None, g
         m = int(metas[r].item())
         out.append(unpack_results(cs[r].cpu().numpy()[:m], ks[r].cpu().numpy()[:m],
                                   ss[r].cpu().numpy()[:m]))
+    return out
+
+
+def gather_decoded(count, tokens, score, n_local, group=None):
+    """Every rank's decode results to rank 0, point to point.
+
+    ``count`` / ``tokens`` / ``score`` are one rank's result tensors in
+    ``BeamDecoder`` layout (request-major: count [>= n], tokens [>= n *
+    max_out * T], score [>= n * max_out]); ranks may hold different request
+    counts and widths.  A 3-int all-gather exchanges the shapes, then each
+    rank sends its first ``n_local`` requests to rank 0 (NCCL send/recv on
+    the device tensors over NVLink; gloo on CPU tensors) -- nothing is
+    broadcast.  Returns on rank 0 a list over ranks of (count [n], tokens
+    [n, max_out * T], score [n, max_out]) tensors; None on the other ranks."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if dist.get_backend(group) != "nccl":  # gloo moves host tensors
+        count, tokens, score = count.cpu(), tokens.cpu(), score.cpu()
+    dev = count.device
+    per_tok = tokens.numel() // max(count.numel(), 1)
+    per_score = score.numel() // max(count.numel(), 1)
+    meta = torch.tensor([n_local, per_tok, per_score], dtype=torch.int64, device=dev)
+    metas = [torch.empty_like(meta) for _ in range(world)]
+    dist.all_gather(metas, meta, group=group)
+    shapes = [tuple(int(x) for x in m.tolist()) for m in metas]
+    mine = (count[:n_local].contiguous(),
+            tokens[:n_local * per_tok].reshape(n_local, per_tok).contiguous(),
+            score[:n_local * per_score].reshape(n_local, per_score).contiguous())
+    if rank != 0:
+        for t in mine:
+            if t.numel():
+                dist.send(t, dst=0, group=group)
+        return None
+    out = [mine]
+    for r in range(1, world):
+        n, pt, ps = shapes[r]
+        bufs = (torch.empty(n, dtype=count.dtype, device=dev),
+                torch.empty((n, pt), dtype=tokens.dtype, device=dev),
+                torch.empty((n, ps), dtype=score.dtype, device=dev))
+        for t in bufs:
+            if t.numel():
+                dist.recv(t, src=r, group=group)
+        out.append(bufs)
+    return out
+
+
+def decoded_to_lists(count, tokens, score, n_levels):
+    """(count, tokens, score) tensors of ``gather_decoded`` -> [(tokens tuple,
+    score)] per request."""
+    c = count.cpu().numpy()
+    t = tokens.cpu().numpy()
+    s = score.cpu().numpy()
+    if t.ndim == 1:  # BeamDecoder's flat request-major buffers
+        t = t[:t.size // max(len(c), 1) * len(c)].reshape(len(c), -1)
+        s = s[:s.size // max(len(c), 1) * len(c)].reshape(len(c), -1)
+    out = []
+    for i in range(len(c)):
+        ti = t[i].reshape(-1, n_levels)
+        out.append([(tuple(int(v) for v in ti[j]), float(s[i, j])) for j in range(int(c[i]))])
     return out
 
 
