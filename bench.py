@@ -261,18 +261,20 @@ def class_work(cfgd):
     # executed on the tcgen05 path with features input (abi.cu
     # layer_forward_tc, latent cross-attention): no context projection and no
     # encoder K/V; per layer row the self-attention's folded products
-    # n (Wq Wk^T) and u (Wv Wo) (2 d^2 MAC) plus the FFN (2 d dff MAC); the
-    # cross-attention runs on CUDA cores over the F-wide latent
-    # (latent_attn: q.F^T and P.F, 4 S F flop per row, mma.sync) between
-    # its absorbed d x F / F x d projections (two thin GEMMs, 4 d F flop)
-    gemm = layer_rows * (4 * d * d + 4 * d * dff + 4 * d * F)
+    # n (Wq Wk^T) and u (Wv Wo) (2 d^2 MAC) plus the FFN (2 d dff MAC) on
+    # tcgen05.  The cross-attention block runs on mma.sync in two kernels
+    # (latent.cu): LN1 + q_lat = LN1(h) A (2 d F flop) + attention over the
+    # F-wide latent (q.F^T and P.F, 4 S F flop) in one ("attn_gemm"), and
+    # h += z B + c (2 d F flop) + LN2 in the other ("layernorm", bytes)
+    gemm = layer_rows * (4 * d * d + 4 * d * dff)
     # the fuse: one d x d GEMM per level row (token-side products tabulated)
     gemm += sum(R[t] * ((2 * d * d if K > 0 else 0) + 2 * d * V[t]) for t in range(T))
-    attn = layer_rows * 4 * S * F
+    attn = layer_rows * (4 * S * F + 2 * d * F)
     topk = sum(R[t] * V[t] * 4 + R[t] * 12 + R[t + 1] * (20 + 8 * (t + 2)) for t in range(T))
     soft = 0
-    # LN1 / LN3 (h in, fp16 hi / lo out), LN2 (h in, hi / lo + fp32 history out)
-    ln = layer_rows * 28 * d
+    # LN3 (h in, fp16 hi / lo out); the latent output + LN2 kernel (h and z
+    # in; h, hi / lo and the fp32 history row out)
+    ln = layer_rows * (24 * d + 4 * F)
     # q' and the normalised history rows n (fp32), the output as fp16 hi / lo
     sattn = K * n_trunk * 4 * (2 * d + d * T) + (L - K) * sum(
         R[t] * 4 * (2 * d + d * (t + 1)) for t in range(T))

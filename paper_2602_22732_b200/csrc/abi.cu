@@ -101,6 +101,10 @@ struct Plan {
   // latent (weight-absorbed) cross-attention: per layer A^T, B (F x d), c (d)
   bool lat_ok = false;
   size_t o_Lat = 0, o_LatTmp = 0;
+  // LN1 folded into the latent query (diag(g1) A^T, 1^T A', b1 A per layer)
+  // and the features pre-split for the fused latent kernel
+  size_t o_LatG = 0, o_FinS = 0;
+  long long fs_rows = 0;
   // token-side fuse tables per level t (K > 0): s W_g and s W_f[d:2d] for
   // every possible s (bos at t = 0, emb_{t-1} rows after)
   size_t o_FuseT[GR4AD_MAX_LEVELS + 1] = {};
@@ -419,8 +423,8 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     }
     add(D * D);  // W_f[0:d] (the fuse GEMM on the gathered gate)
     if (p.lat_ok)
-      for (int i = 0; i < p.L; ++i) {  // latent A^T, B^T
-        add((long long)p.F * D); add((long long)p.F * D);
+      for (int i = 0; i < p.L; ++i) {  // latent A^T, B^T, diag(g1) A^T
+        add((long long)p.F * D); add((long long)p.F * D); add((long long)p.F * D);
       }
   }
 
@@ -498,6 +502,10 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     if (p.lat_ok) {
       p.o_Lat = take(Fl * (size_t)p.L * (2 * p.F + 1) * d);
       p.o_LatTmp = take(Fl * (size_t)(p.F + 1) * d);
+      p.o_LatG = take(Fl * (size_t)p.L * (p.F * d + 2 * p.F));  // diag(g1) A^T, 1^T A', b1 A
+      // pre-split features (fused latent kernel), one spare chunk of rows
+      p.fs_rows = p.S_tot + 256;
+      p.o_FinS = take(H2 * 2 * (size_t)p.fs_rows * latent_feat_kst(p.F));
     }
     p.o_U16 = take(H2 * 2 * p.Rw * 2 * d);  // the fuse input [g | s] as fp16 hi, then lo
     if (p.K > 0)
@@ -593,6 +601,10 @@ struct LayerT {
   // their K-major fp16 hi / lo copies: q_lat = n A (B operand A^T, F x d)
   // and h += z B + c (B operand B^T, d x F)
   const __half *lat_q16, *lat_o16;
+  // LN1 folded into the query projection (latent.cu latent_cross_ln):
+  // kWeightScale diag(g1) A^T as fp16 hi / lo, s = 1^T diag(g1) A, c = b1 A
+  const __half *lat_qg16;
+  const float *lat_s, *lat_c1;
 };
 struct WeightsT {
   const __half *ctx, *wg, *wf, *hv;
@@ -667,7 +679,8 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
     lt.w1 = tr(Lw.ffn_W1, d, p.dff);
     lt.w2 = tr(Lw.ffn_W2, p.dff, d);
     lt.lat_at = lt.lat_b = lt.lat_c = nullptr;
-    lt.lat_q16 = lt.lat_o16 = nullptr;
+    lt.lat_q16 = lt.lat_o16 = lt.lat_qg16 = nullptr;
+    lt.lat_s = lt.lat_c1 = nullptr;
     if (p.lat_ok) {
       // absorbed through the context projection X = F W_c + b_c, each
       // product formed in double from the fp32 weights (weight_product)
@@ -699,6 +712,18 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
                      st);
       lt.lat_q16 = q16;
       lt.lat_o16 = tr(lt.lat_b, F, d);
+      float *ag = at<float>(ws, p.o_LatG) + (size_t)i * (F * d + 2 * F);
+      lt.lat_s = ag + (size_t)F * d;
+      lt.lat_c1 = lt.lat_s + F;
+      if (rc == GR4AD_OK && launch)
+        rc = latent_fold(la, Lw.ln1_g, Lw.ln1_b, d, F, ag, ag + (size_t)F * d,
+                         ag + (size_t)F * d + F, st);
+      __half *qg16 = base + o;
+      o += ((long long)F * d + 63) / 64 * 64;
+      if (rc == GR4AD_OK && launch)
+        rc = split16(ag, d, qg16, qg16 + p.wt_floats, d, F, d, kWeightScale, at<int>(ws, p.o_flag),
+                     st);
+      lt.lat_qg16 = qg16;
     }
   }
   return rc;
@@ -810,6 +835,16 @@ static int layer_forward(const Plan &p, const gr4ad_weights *w, int i, float *Hs
   return gemm(f2, false, EPI_BIAS_RESID, st);
 }
 
+// A/B aid: GR4AD_LAT_FUSED=0 runs the latent block as LN1 / q_lat GEMM /
+// latent_attn / output GEMM / LN2
+static bool lat_fused() {
+  static const bool on = [] {
+    const char *e = getenv("GR4AD_LAT_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Tensor-core path, factored attention.  The reference attends with
 // q = n W_q, K = X W_k, V = X W_v (layers.py:46-51, 82-90; beam.py:98-109,
 // 221-232) and the self-attention likewise on the LayerNorm'd rows n
@@ -857,6 +892,18 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
     // then LN2 of h (split for the next GEMM, fp32 into the self history)
     const float *Fin = at<float>(ws, p.o_Fin);
     const int F = p.F;
+    if (lat_fused()) {
+      // LN1 + q_lat inside the attention kernel, z B + c + residual + LN2 in
+      // one row-tile kernel: LN1's output and q_lat never reach HBM
+      const __half *fs = at<__half>(ws, p.o_FinS);
+      GR_TRY(latent_cross_ln(Hs, d, LT.lat_qg16, LT.lat_qg16 + p.wt_floats, LT.lat_s, LT.lat_c1,
+                             fs, fs + (size_t)p.fs_rows * latent_feat_kst(F), F, rs.g_row_off,
+                             rs.g_rows, ctx_off, ctx_len, n_groups, rs.max_group_rows,
+                             1.0f / sqrtf((float)d), A, at<int>(ws, p.o_flag), st));
+      GR_TRY(latent_out_ln(A, F, LT.lat_o16, LT.lat_o16 + p.wt_floats, 1.0f / kWeightScale,
+                           LT.lat_c, Hs, d, Lw.ln2_g, Lw.ln2_b, Nh, Nl, hn, p.hist_ld, R,
+                           at<int>(ws, p.o_flag), st));
+    } else {
     GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
     GR_TRY(dense_split(p, plain_gemm(N, d, LT.lat_at, d, Q, F, R, F, d), LT.lat_q16, Nh, Nl, R,
                        EPI_STORE, st));
@@ -868,6 +915,7 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
     go.ldr = d;
     GR_TRY(dense(p, go, LT.lat_o16, R, EPI_BIAS_RESID, st));
     GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln2_g, Lw.ln2_b, R, d, st, hn, p.hist_ld));
+    }
   } else {
   // ---- cross-attention into the beam-shared context (layers.py:82-90) ----
   if (spl)
@@ -1027,6 +1075,11 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
     // never formed
     GR_TRY(pad_rows(features, at<int>(ws, p.o_in_off), at<int>(ws, p.o_ctx_off),
                     at<int>(ws, p.o_ctx_len), B, p.F, at<float>(ws, p.o_Fin), st));
+    if (lat_fused()) {
+      __half *fs = at<__half>(ws, p.o_FinS);
+      GR_TRY(latent_feat_split(at<float>(ws, p.o_Fin), p.S_tot, p.fs_rows, p.F, fs,
+                               fs + (size_t)p.fs_rows * latent_feat_kst(p.F), flag, st));
+    }
   } else {
   // context projection (decoder.py:134-140) on 32-row-aligned request blocks
   const int *in_off = at<int>(ws, p.o_in_off), *ctx_off_d = at<int>(ws, p.o_ctx_off);

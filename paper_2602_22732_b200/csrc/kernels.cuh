@@ -42,6 +42,25 @@ bool latent_supported(int d, int F);
 int latent_attn(const float *q, const float *feats, int F, const int *g_row_off, const int *g_rows,
                 const int *g_ctx_off, const int *g_ctx_len, int n_groups, int max_group_rows,
                 float scale, float *z, int *flag, cudaStream_t st);
+// the latent cross-attention block without LN1's output or q_lat in HBM:
+// z = softmax(LN1(h) A F^T scale) F in one kernel (LN1 folded: A'^T =
+// kWeightScale diag(g1) A as fp16 hi / lo, s = 1^T A', c = b1 A; features
+// pre-split by latent_feat_split), then h += alpha z B + c and LN2 of the new
+// rows (n split, hn fp32) in a second
+int latent_cross_ln(const float *h, int d, const __half *aq_hi, const __half *aq_lo,
+                    const float *s1, const float *c1, const __half *fs_hi, const __half *fs_lo,
+                    int F, const int *g_row_off, const int *g_rows, const int *g_ctx_off,
+                    const int *g_ctx_len, int n_groups, int max_group_rows, float scale, float *z,
+                    int *flag, cudaStream_t st);
+int latent_out_ln(const float *z, int F, const __half *bo_hi, const __half *bo_lo, float alpha,
+                  const float *c, float *hs, int d, const float *g2, const float *b2,
+                  __half *n_hi, __half *n_lo, float *hn, long long ld_hn, int rows, int *flag,
+                  cudaStream_t st);
+int latent_fold(const float *at, const float *g1, const float *b1, int d, int F, float *ag,
+                float *sv, float *cv, cudaStream_t st);
+int latent_feat_kst(int F);  // halves per pre-split feature row
+int latent_feat_split(const float *fin, long long rows_used, long long rows_alloc, int F,
+                      __half *hi, __half *lo, int *flag, cudaStream_t st);
 // C = A . op(B) in double, rounded to fp32 (snapshot weight products)
 int weight_product(const float *A, long long lda, const float *B, long long ldb, bool trans_b,
                    float *C, long long ldc, int M, int N, int K, cudaStream_t st);
