@@ -1,0 +1,52 @@
+#!/bin/bash
+# Round-2 evidence pass (1 GPU): parity numbers at the benched shapes, the
+# default (C3) bench line with its CPU baseline, the reference arm, C1 / C2 /
+# C5 lines, the C3 launch list, and ncu --set full of the top kernels
+# (text pages only, so gpurun_out stays small).
+O=${O:-gpurun_out/ev}
+mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $O/gpu.txt
+timeout 900 python -m pytest tests/test_gpu_big.py -m gpu -q -s -p no:cacheprovider > $O/parity_big.txt 2>&1
+tail -4 $O/parity_big.txt
+timeout 900 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err
+timeout 900 python bench.py --impl reference > $O/bench_reference_c3.json 2> $O/bench_ref.err
+for c in c5 c2 c1; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err
+done
+for f in $O/bench_*.json; do echo $f; tail -c 250 $f; echo; done
+B="python bench.py --steps 1 --warmup 1 --no-graph --no-cpu-baseline"
+GR4AD_TRACE=1 timeout 300 $B > /dev/null 2> $O/trace_c3.txt
+python - $O/trace_c3.txt > $O/idx.txt <<'PY'
+import sys
+lines=[l for l in open(sys.argv[1]) if l.startswith("gemm_tc ")]
+def first(*keys):
+    return next((i for i,l in enumerate(lines) if all(k in l for k in keys)), 0)
+print(first("M=131072 ", "N=2048 ", "K=1024 "), first("M=131072 ", "N=4096 "),
+      first("M=131072 ", "N=1024 ", "K=2048 "))
+PY
+read W1 LG W2 < $O/idx.txt
+echo "idx $W1 $LG $W2"
+NF="ncu --set full --clock-control none --import-source on"
+timeout -s KILL 600 $NF -k regex:gemm_tc -s $W1 -c 1 -o $O/prof_gemm_w1 $B > $O/ncu1.log 2>&1
+timeout -s KILL 600 $NF -k regex:gemm_tc -s $LG -c 1 -o $O/prof_gemm_logits $B > $O/ncu2.log 2>&1
+timeout -s KILL 600 $NF -k regex:gemm_tc -s $W2 -c 1 -o $O/prof_gemm_w2 $B > $O/ncu3.log 2>&1
+timeout -s KILL 600 $NF -k regex:topk_select -s 1 -c 1 -o $O/prof_topk $B > $O/ncu4.log 2>&1
+timeout -s KILL 600 $NF -k regex:self_attn -s 20 -c 1 -o $O/prof_self $B > $O/ncu5.log 2>&1
+timeout -s KILL 600 $NF -k regex:ln_rows_split -s 8 -c 1 -o $O/prof_ln3 $B > $O/ncu6.log 2>&1
+timeout -s KILL 600 $NF -k regex:latent_attn -s 8 -c 1 -o $O/prof_lat_x $B > $O/ncu7.log 2>&1
+timeout -s KILL 600 $NF -k regex:latent_out -s 8 -c 1 -o $O/prof_lat_y $B > $O/ncu8.log 2>&1
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+timeout -s KILL 900 ncu --metrics $M --clock-control none -c 1500 --csv \
+  --log-file $O/launches_c3.csv $B > /dev/null 2>&1
+timeout -s KILL 900 ncu --metrics $M --clock-control none -c 1500 --csv \
+  --log-file $O/launches_c5.csv $B --config c5 > /dev/null 2>&1
+for r in $O/*.ncu-rep; do
+  b=${r%.ncu-rep}
+  ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
+  ncu -i $r --page details --csv > $b.details.csv 2>/dev/null
+  ncu -i $r --page source --csv > $b.source.csv 2>/dev/null
+  gzip -f $b.source.csv
+  rm -f $r
+done
+rm -f $O/trace_c3.txt
+du -sh $O
