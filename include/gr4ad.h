@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define GR4AD_ABI_VERSION 1
+#define GR4AD_ABI_VERSION 2
 #define GR4AD_MAX_LEVELS 8
 #define GR4AD_MAX_LAYERS 32
 #define GR4AD_MAX_BEAM 8192 /* per-request selection width handled on chip */
@@ -120,6 +120,15 @@ typedef struct {
    * (gr4ad_prepare_weights: fragment-ordered / K-major fp16 hi+lo splits);
    * the decode then skips rebuilding them.  0: rebuilt every call. */
   int weights_prepared;
+  /* optional: the snapshot's derived weight copies (factored / absorbed
+   * products, fuse tables, K-major fp16 splits, MMA fragments) in a
+   * caller-owned device buffer shared by every decode of that snapshot and
+   * path (gr4ad_derived_layout sizes it and names its layout;
+   * gr4ad_prepare_weights fills it).  NULL: they live at the start of the
+   * workspace.  With a buffer, the workspace shrinks by derived bytes and a
+   * new batch shape costs no weight preparation. */
+  void *derived;
+  size_t derived_bytes;
 } gr4ad_batch;
 
 /* Results: for request b, count[b] entries in selection order (or value
@@ -178,7 +187,8 @@ int gr4ad_beam_search_run(const gr4ad_dims *dims, const gr4ad_weights *w,
 
 /* Build the snapshot-derived weight copies a decode of this batch shape uses
  * (fused path: mma fragments + trunk queries; tensor-core path: K-major fp16
- * hi/lo splits) into `workspace`, once per snapshot (the SnapshotStore
+ * hi/lo splits) into batch->derived when set (workspace may then be NULL),
+ * else into `workspace`, once per snapshot (the SnapshotStore
  * contract, engine.py:17-36); then set batch->weights_prepared.  Synchronises
  * `stream`; returns GR4AD_ERR_UNSUPPORTED if a weight leaves the fp16 split
  * range. */
@@ -194,6 +204,15 @@ int gr4ad_prepare_weights(const gr4ad_dims *dims, const gr4ad_weights *w,
  * computes in float64 (autodiff.py:55). */
 int gr4ad_range_status(const gr4ad_dims *dims, const gr4ad_batch *batch, const void *workspace,
                        void *stream);
+/* Size and layout signature of the derived weight region of this batch's
+ * plan (it depends only on dims, the decode path, the trunk depth and
+ * value re-rank -- not on the batch size or widths): decodes whose plans
+ * report the same signature share one derived buffer (batch->derived).
+ * Replaces the per-call weight re-derivation of the reference's stateless
+ * beam_search (beam.py:112-143) with the SnapshotStore contract
+ * (engine.py:17-36): derive once per published snapshot. */
+int gr4ad_derived_layout(const gr4ad_dims *dims, const gr4ad_batch *batch, size_t *bytes,
+                         unsigned long long *signature);
 /* Byte offset of that flag (an int, nonzero = out of range) inside the
  * workspace, so a caller can copy it to the host together with the results
  * instead of synchronising in gr4ad_range_status. */

@@ -40,6 +40,7 @@ EXPORTS = (
     "gr4ad_score_workspace_bytes", "gr4ad_range_status", "gr4ad_prepare_weights",
     "gr4ad_gemm_presplit", "gr4ad_range_flag_offset", "gr4ad_encode_trunk",
     "gr4ad_level_step", "gr4ad_collect", "gr4ad_topk_precut_f64", "gr4ad_resolve_items",
+    "gr4ad_derived_layout",
 )
 
 _P = C.c_void_p
@@ -70,7 +71,7 @@ class Batch(C.Structure):
                 ("value_rerank", C.c_int), ("value_reps", _P),
                 ("valid_prefix", _P * MAX_LEVELS),
                 ("valid_prefix_count", C.POINTER(C.c_int)), ("decode_path", C.c_int),
-                ("weights_prepared", C.c_int)]
+                ("weights_prepared", C.c_int), ("derived", _P), ("derived_bytes", C.c_size_t)]
 
 PATH_AUTO, PATH_LAYERED, PATH_FUSED = 0, 1, 2
 
@@ -135,7 +136,9 @@ def _load():
                                           _P, _P, _P]
     lib.gr4ad_resolve_items.argtypes = [_P, _P, C.c_int, C.POINTER(Dims), C.POINTER(Results),
                                         C.c_int, _P, _P]
-    if lib.gr4ad_abi_version() != 1:
+    lib.gr4ad_derived_layout.argtypes = [C.POINTER(Dims), C.POINTER(Batch),
+                                         C.POINTER(C.c_size_t), C.POINTER(C.c_ulonglong)]
+    if lib.gr4ad_abi_version() != 2:
         raise ImportError("libgr4ad ABI version mismatch")
     return lib
 

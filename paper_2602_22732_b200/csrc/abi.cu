@@ -93,6 +93,9 @@ struct Plan {
   size_t o_Hs, o_N, o_Q, o_A, o_U, o_Fb, o_SC, o_SCs, o_LG, o_rinfo, o_lsep, o_vlog;
   size_t o_hist;  // (L-K) consecutive (H, hist_ld) buffers
   long long hist_ld = 0;  // self-attention history row: [q|k|v] (3d) or factored [q'|n] (2d)
+  // factored history with n kept as fp16 hi / lo halves ([q' fp32 | n hi | n lo],
+  // the q' GEMM's A operand and the self-attention's keys / values at once)
+  bool hist_split = false;
   size_t table_bytes, total;
   // tensor-core layered path
   bool tc = false;
@@ -127,6 +130,13 @@ struct Plan {
   long long frag_f4 = 0;  // fragment-ordered weights (float4 count)
   size_t o_frag = 0, o_tu = 0;
   bool weights_prepared = false;  // batch->weights_prepared
+  // derived weight copies (per snapshot, dims + path only): at the start of
+  // the workspace, or in the caller's batch->derived buffer (shared by every
+  // decode of the snapshot); offsets o_WT o_Mf o_Lat* o_FuseT o_frag o_tu
+  // o_dflag are relative to that region
+  char *derived = nullptr;
+  size_t derived_total = 0, o_dflag = 0;
+  unsigned long long derived_sig = 0;
   size_t o_vprp[GR4AD_MAX_LEVELS] = {};  // masking: CSR row pointers per level
   long long vp_np[GR4AD_MAX_LEVELS] = {};
   size_t o_flag = 0;  // fp16 range flag (set by the operand splits, read by gr4ad_range_status)
@@ -407,6 +417,7 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
                      "tensor-core path needs d a multiple of 8 and d_ff, F, V multiples of 4");
   }
   p.hist_ld = (p.tc ? 2LL : 3LL) * p.d;
+  p.hist_split = p.tc && p.d % 128 == 0 && p.d <= 1024 && p.dff % 8 == 0;
   p.sc_ld = (p.S_max + 7) / 8 * 8;  // (fp16 P rows: 16-B aligned)
   p.vt_ld = (p.S_tot + 7) / 8 * 8;  // fp16 rows: 16-B aligned
   if (p.tc) {
@@ -428,14 +439,55 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
       }
   }
 
+  const size_t I = sizeof(int), Fl = sizeof(float);
+  // ---- derived weight region (gr4ad_derived_layout) ----
+  size_t od = 0;
+  auto take_d = [&](size_t bytes) {
+    size_t r = od;
+    od = align_up(od + bytes);
+    return r;
+  };
+  p.o_dflag = take_d(256);  // fp16 split range flag of the weight preparation
+  if (p.fused && p.f_mma) {
+    p.o_frag = take_d(16 * (size_t)p.frag_f4);
+    p.o_tu = take_d(sizeof(float) * (size_t)std::max(p.n_pos, 1) * p.d);
+  }
+  if (!p.fused && p.tc) {
+    const size_t d = p.d, H2 = sizeof(__half);
+    p.o_Mf = take_d(Fl * 4 * (size_t)p.L * d * d);  // factored attention weights (fp32)
+    if (p.lat_ok) {
+      p.o_Lat = take_d(Fl * (size_t)p.L * (2 * p.F + 1) * d);
+      p.o_LatTmp = take_d(Fl * (size_t)(p.F + 1) * d);
+      p.o_LatG = take_d(Fl * (size_t)p.L * (p.F * d + 2 * p.F));  // diag(g1) A^T, 1^T A', b1 A
+    }
+    if (p.K > 0)
+      for (int t = 0; t < p.n_pos; ++t) {
+        p.fuse_n[t] = t == 0 ? 1 : p.V[t - 1];
+        p.o_FuseT[t] = take_d(Fl * 2 * (size_t)p.fuse_n[t] * d);
+      }
+    p.o_WT = take_d(H2 * (size_t)p.wt_floats * 2);  // K-major weights: fp16 hi, then lo
+  }
+  p.derived_total = od;
+  // layout signature: everything the region's layout depends on
+  {
+    unsigned long long h = 1469598103934665603ULL;
+    auto mix = [&](unsigned long long v) { h = (h ^ v) * 1099511628211ULL; };
+    mix((unsigned long long)od); mix(p.fused); mix(p.f_mma); mix(p.tc); mix(p.lat_ok);
+    mix((unsigned long long)p.K); mix((unsigned long long)p.n_pos); mix((unsigned long long)p.wt_floats);
+    p.derived_sig = h;
+  }
+  p.derived = static_cast<char *>(bt->derived);
+  if (p.derived && bt->derived_bytes < od)
+    return set_err(GR4AD_ERR_WORKSPACE, "derived weight buffer: %zu bytes < %zu", bt->derived_bytes,
+                   od);
+
   // ---- workspace layout ----
-  size_t o = 0;
+  size_t o = p.derived ? 0 : od;
   auto take = [&](size_t bytes) {
     size_t r = o;
     o = align_up(o + bytes);
     return r;
   };
-  const size_t I = sizeof(int), Fl = sizeof(float);
   p.o_ctx_off = take(I * B);
   p.o_in_off = take(I * B);
   p.o_ctx_len = take(I * B);
@@ -451,11 +503,8 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
   p.o_tnpos = take(I * (size_t)B * p.n_pos);
   p.table_bytes = o;
   p.o_flag = take(256);
+  if (!p.derived) p.o_dflag = p.o_flag;  // one flag when the region is in the workspace
   if (p.fused) {
-    if (p.f_mma) {
-      p.o_frag = take(16 * (size_t)p.frag_f4);
-      p.o_tu = take(sizeof(float) * (size_t)std::max(p.n_pos, 1) * p.d);
-    }
     p.o_keys = take(sizeof(uint32_t) * (size_t)B * p.f_keys_per_req);
     // valid-SID masking: per level, CSR row pointers over the prefix key
     long long np_t = 1;
@@ -498,22 +547,12 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
     const size_t H2 = sizeof(__half);
     p.o_XTs = take(H2 * 2 * (size_t)d * p.vt_ld);  // kKvScale X^T as fp16 hi, then lo
     p.o_Xs = take(H2 * 2 * p.S_tot * d);           // kKvScale X as fp16 hi, then lo
-    p.o_Mf = take(Fl * 4 * (size_t)p.L * d * d);   // factored attention weights (fp32)
     if (p.lat_ok) {
-      p.o_Lat = take(Fl * (size_t)p.L * (2 * p.F + 1) * d);
-      p.o_LatTmp = take(Fl * (size_t)(p.F + 1) * d);
-      p.o_LatG = take(Fl * (size_t)p.L * (p.F * d + 2 * p.F));  // diag(g1) A^T, 1^T A', b1 A
       // pre-split features (fused latent kernel), one spare chunk of rows
       p.fs_rows = p.S_tot + 256;
       p.o_FinS = take(H2 * 2 * (size_t)p.fs_rows * latent_feat_kst(p.F));
     }
     p.o_U16 = take(H2 * 2 * p.Rw * 2 * d);  // the fuse input [g | s] as fp16 hi, then lo
-    if (p.K > 0)
-      for (int t = 0; t < p.n_pos; ++t) {
-        p.fuse_n[t] = t == 0 ? 1 : p.V[t - 1];
-        p.o_FuseT[t] = take(Fl * 2 * (size_t)p.fuse_n[t] * d);
-      }
-    p.o_WT = take(H2 * (size_t)p.wt_floats * 2);  // K-major weights: fp16 hi, then lo
   }
   p.total = o;
   return GR4AD_OK;
@@ -522,6 +561,11 @@ static int make_plan(const gr4ad_dims *dm, const gr4ad_batch *bt, Plan &p,
 template <typename T>
 static T *at(void *ws, size_t off) {
   return reinterpret_cast<T *>(static_cast<char *>(ws) + off);
+}
+// a derived-weight region offset (the caller's shared buffer or the workspace)
+template <typename T>
+static T *atd(const Plan &p, void *ws, size_t off) {
+  return reinterpret_cast<T *>((p.derived ? p.derived : static_cast<char *>(ws)) + off);
 }
 
 static int upload_tables(const Plan &p, void *ws, cudaStream_t st) {
@@ -618,7 +662,7 @@ struct WeightsT {
 
 static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, WeightsT &wt,
                           cudaStream_t st, bool launch = true) {
-  __half *base = at<__half>(ws, p.o_WT);
+  __half *base = atd<__half>(p, ws, p.o_WT);
   long long o = 0;
   int rc = GR4AD_OK;
   // dst (cols x rows) = kWeightScale * src (rows x cols)^T as fp16 hi, lo at + wt_floats
@@ -627,7 +671,7 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
     o += ((long long)rows * cols + 63) / 64 * 64;
     if (rc == GR4AD_OK && launch)
       rc = transpose_split16(src, cols, dst, dst + p.wt_floats, rows, rows, cols, kWeightScale,
-                             at<int>(ws, p.o_flag), st);
+                             atd<int>(p, ws, p.o_dflag), st);
     return dst;
   };
   // C (d x d) = A . op(B) in double (weight_product), once per snapshot
@@ -646,7 +690,7 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
     for (int t = 0; t < p.n_pos; ++t) {
       // the token side of the fuse (layers.py:129-133) is a function of the
       // token alone: s W_g and s W_f[d:2d] tabulated once per snapshot
-      float *tab = at<float>(ws, p.o_FuseT[t]);
+      float *tab = atd<float>(p, ws, p.o_FuseT[t]);
       const int n = p.fuse_n[t];
       const float *S = t == 0 ? w->bos : w->emb[t - 1];
       wt.fuse_tab[t] = tab;
@@ -658,7 +702,7 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
     }
   for (int t = 0; t < p.T; ++t) wt.head[t] = tr(w->head[t], d, p.V[t]);
   wt.hv = tr(w->head_value, d, p.nb);
-  float *Mf = at<float>(ws, p.o_Mf);
+  float *Mf = atd<float>(p, ws, p.o_Mf);
   for (int i = 0; i < p.L; ++i) {
     const gr4ad_layer &Lw = w->layer[i];
     LayerT &lt = wt.layer[i];
@@ -685,8 +729,8 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
       // absorbed through the context projection X = F W_c + b_c, each
       // product formed in double from the fp32 weights (weight_product)
       const int F = p.F;
-      float *la = at<float>(ws, p.o_Lat) + (size_t)i * (2 * F + 1) * d;
-      float *tmp = at<float>(ws, p.o_LatTmp), *tv = tmp + (size_t)F * d;
+      float *la = atd<float>(p, ws, p.o_Lat) + (size_t)i * (2 * F + 1) * d;
+      float *tmp = atd<float>(p, ws, p.o_LatTmp), *tv = tmp + (size_t)F * d;
       lt.lat_at = la;
       lt.lat_b = la + (size_t)F * d;
       lt.lat_c = la + (size_t)2 * F * d;
@@ -708,11 +752,11 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
       __half *q16 = base + o;
       o += ((long long)F * d + 63) / 64 * 64;
       if (rc == GR4AD_OK && launch)
-        rc = split16(la, d, q16, q16 + p.wt_floats, d, F, d, kWeightScale, at<int>(ws, p.o_flag),
+        rc = split16(la, d, q16, q16 + p.wt_floats, d, F, d, kWeightScale, atd<int>(p, ws, p.o_dflag),
                      st);
       lt.lat_q16 = q16;
       lt.lat_o16 = tr(lt.lat_b, F, d);
-      float *ag = at<float>(ws, p.o_LatG) + (size_t)i * (F * d + 2 * F);
+      float *ag = atd<float>(p, ws, p.o_LatG) + (size_t)i * (F * d + 2 * F);
       lt.lat_s = ag + (size_t)F * d;
       lt.lat_c1 = lt.lat_s + F;
       if (rc == GR4AD_OK && launch)
@@ -721,7 +765,7 @@ static int prep_weights_t(const Plan &p, const gr4ad_weights *w, void *ws, Weigh
       __half *qg16 = base + o;
       o += ((long long)F * d + 63) / 64 * 64;
       if (rc == GR4AD_OK && launch)
-        rc = split16(ag, d, qg16, qg16 + p.wt_floats, d, F, d, kWeightScale, at<int>(ws, p.o_flag),
+        rc = split16(ag, d, qg16, qg16 + p.wt_floats, d, F, d, kWeightScale, atd<int>(p, ws, p.o_dflag),
                      st);
       lt.lat_qg16 = qg16;
     }
@@ -886,6 +930,14 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
   const __half *xt_hi = at<__half>(ws, p.o_XTs), *xt_lo = xt_hi + (size_t)d * p.vt_ld;
 
   float *hq = rs.qkv + rs.hist_row0 * p.hist_ld, *hn = hq + d;  // self history [q' | n]
+  // split history: n as fp16 hi / lo halves after q' (row pitch 2 hist_ld halves)
+  const bool hs2 = p.hist_split && spl;
+  __half *nh_hi = reinterpret_cast<__half *>(hq) + 2 * d, *nh_lo = nh_hi + d;
+  const long long ld_nh = 2 * p.hist_ld;
+  // LN2's split output (the q' GEMM's A operand) and its fp32 copy
+  __half *n2h = hs2 ? nh_hi : Nh, *n2l = hs2 ? nh_lo : Nl;
+  const long long ld_n2 = hs2 ? ld_nh : d;
+  float *n2f = hs2 ? nullptr : hn;
   if (wt.lat) {
     // ---- cross-attention over the request's latent (latent.cu) ----------
     // q_lat = LN1(h) A;  z = softmax(q_lat F^T / sqrt d) F;  h += z B + c;
@@ -901,8 +953,8 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
                              rs.g_rows, ctx_off, ctx_len, n_groups, rs.max_group_rows,
                              1.0f / sqrtf((float)d), A, at<int>(ws, p.o_flag), st));
       GR_TRY(latent_out_ln(A, F, LT.lat_o16, LT.lat_o16 + p.wt_floats, 1.0f / kWeightScale,
-                           LT.lat_c, Hs, d, Lw.ln2_g, Lw.ln2_b, Nh, Nl, hn, p.hist_ld, R,
-                           at<int>(ws, p.o_flag), st));
+                           LT.lat_c, Hs, d, Lw.ln2_g, Lw.ln2_b, n2h, n2l, ld_n2, n2f, p.hist_ld,
+                           R, at<int>(ws, p.o_flag), st));
     } else {
     GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln1_g, Lw.ln1_b, R, d, st));
     GR_TRY(dense_split(p, plain_gemm(N, d, LT.lat_at, d, Q, F, R, F, d), LT.lat_q16, Nh, Nl, R,
@@ -914,7 +966,7 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
     go.R = Hs;
     go.ldr = d;
     GR_TRY(dense(p, go, LT.lat_o16, R, EPI_BIAS_RESID, st));
-    GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln2_g, Lw.ln2_b, R, d, st, hn, p.hist_ld));
+    GR_TRY(ln_rows_split(Hs, d, n2h, n2l, ld_n2, Lw.ln2_g, Lw.ln2_b, R, d, st, n2f, p.hist_ld));
     }
   } else {
   // ---- cross-attention into the beam-shared context (layers.py:82-90) ----
@@ -1013,18 +1065,20 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
   // ---- self-attention over decoded positions (layers.py:92-113) ----------
   // history row: [q' = n (W_q W_k^T) | n]; keys and values are n itself
   if (spl)
-    GR_TRY(ln_rows_split(Hs, d, Nh, Nl, d, Lw.ln2_g, Lw.ln2_b, R, d, st, hn, p.hist_ld));
+    GR_TRY(ln_rows_split(Hs, d, n2h, n2l, ld_n2, Lw.ln2_g, Lw.ln2_b, R, d, st, n2f, p.hist_ld));
   else
     GR_TRY(ln_rows(Hs, d, hn, p.hist_ld, Lw.ln2_g, Lw.ln2_b, R, d, st));
   }  // (context-operand cross-attention)
-  const GemmArgs sq = spl ? plain_gemm(N, d, LT.msqk, d, hq, p.hist_ld, R, d, d)
-                          : plain_gemm(hn, p.hist_ld, LT.msqk, d, hq, p.hist_ld, R, d, d);
-  if (spl)
-    GR_TRY(dense_split(p, sq, LT.sqk, Nh, Nl, R, EPI_STORE, st));
-  else
+  GemmArgs sq = spl ? plain_gemm(N, d, LT.msqk, d, hq, p.hist_ld, R, d, d)
+                    : plain_gemm(hn, p.hist_ld, LT.msqk, d, hq, p.hist_ld, R, d, d);
+  if (spl) {
+    sq.lda = ld_n2;  // (in halves: the A operand arrives pre-split)
+    GR_TRY(dense_split(p, sq, LT.sqk, n2h, n2l, R, EPI_STORE, st));
+  } else {
     GR_TRY(dense(p, sq, LT.sqk, R, EPI_STORE, st));
+  }
   GR_TRY(self_attn(rs.qkv, p.hist_ld, d, rs.anc, rs.anc_stride, (int)rs.hist_row0, R, rs.npos_u,
-                   rs.npos_row, A, d, st, spl ? Ah : nullptr, spl ? Al : nullptr, d));
+                   rs.npos_row, A, d, st, spl ? Ah : nullptr, spl ? Al : nullptr, d, hs2));
   GemmArgs so = plain_gemm(A, d, LT.msvo, d, Hs, d, R, d, d);  // h += (P n) (W_v W_o)
   so.R = Hs; so.ldr = d;
   if (spl)
@@ -1357,14 +1411,14 @@ static int run_plan(const Plan &p, const gr4ad_dims *dm, const gr4ad_weights *w,
       f.Hrows = p.f_Hrows_mma;
       for (int t = 0; t < GR4AD_MAX_LEVELS + 2; ++t) f.hoff[t] = p.f_hoff4[t];
       static thread_local FragJobs jobs;  // ~6 KB: kept off the stack
-      uint4 *frag = at<uint4>(ws, p.o_frag);
+      uint4 *frag = atd<uint4>(p, ws, p.o_frag);
       frag_layout(p, w, &jobs, &f.fi);
       f.frag = frag;
       jobs.tu = TrunkUJob{};
       if (K > 0 && d <= 32) {
         const gr4ad_layer &L0 = w->layer[0];
         jobs.tu = TrunkUJob{w->pos, L0.ln1_g, L0.ln1_b, L0.cross_Wq, w->cross_kv_W,
-                            at<float>(ws, p.o_tu), d, 2 * p.L * d, p.n_pos};
+                            atd<float>(p, ws, p.o_tu), d, 2 * p.L * d, p.n_pos};
         f.trunk_u = jobs.tu.u;
       }
       if (!p.weights_prepared) GR_TRY(frag_prep_launch(jobs, frag, range_flag, st));
@@ -1548,6 +1602,18 @@ int gr4ad_collect(const gr4ad_dims *dims, const gr4ad_batch *batch, gr4ad_result
   return layered_end(p, batch, out, workspace, (cudaStream_t)stream);
 }
 
+int gr4ad_derived_layout(const gr4ad_dims *dims, const gr4ad_batch *batch, size_t *bytes,
+                         unsigned long long *signature) {
+  gr4ad_batch b = *batch;
+  b.derived = nullptr;
+  b.derived_bytes = 0;
+  Plan p;
+  GR_TRY(make_plan(dims, &b, p));
+  if (bytes) *bytes = p.derived_total;
+  if (signature) *signature = p.derived_sig;
+  return GR4AD_OK;
+}
+
 int gr4ad_range_flag_offset(const gr4ad_dims *dims, const gr4ad_batch *batch, size_t *offset) {
   Plan p;
   GR_TRY(make_plan(dims, batch, p));
@@ -1560,12 +1626,13 @@ int gr4ad_prepare_weights(const gr4ad_dims *dims, const gr4ad_weights *w,
                           void *stream) {
   Plan p;
   GR_TRY(make_plan(dims, batch, p));
-  if (workspace_bytes < p.total)
+  // into the caller's derived buffer (no workspace needed) or the workspace
+  if (!p.derived && workspace_bytes < p.total)
     return set_err(GR4AD_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, p.total);
   if (p.B == 0) return GR4AD_OK;
   cudaStream_t st = (cudaStream_t)stream;
   void *ws = workspace;
-  int *flag = at<int>(ws, p.o_flag);
+  int *flag = atd<int>(p, ws, p.o_dflag);
   GR_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
   if (p.fused && p.f_mma) {
     static thread_local FragJobs jobs;  // ~7 KB: kept off the stack
@@ -1575,9 +1642,9 @@ int gr4ad_prepare_weights(const gr4ad_dims *dims, const gr4ad_weights *w,
     if (p.K > 0 && p.d <= 32) {
       const gr4ad_layer &L0 = w->layer[0];
       jobs.tu = TrunkUJob{w->pos, L0.ln1_g, L0.ln1_b, L0.cross_Wq, w->cross_kv_W,
-                          at<float>(ws, p.o_tu), p.d, 2 * p.L * p.d, p.n_pos};
+                          atd<float>(p, ws, p.o_tu), p.d, 2 * p.L * p.d, p.n_pos};
     }
-    GR_TRY(frag_prep_launch(jobs, at<uint4>(ws, p.o_frag), flag, st));
+    GR_TRY(frag_prep_launch(jobs, atd<uint4>(p, ws, p.o_frag), flag, st));
   } else if (p.tc) {
     WeightsT wt;
     GR_TRY(prep_weights_t(p, w, ws, wt, st, true));

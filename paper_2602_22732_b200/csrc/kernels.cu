@@ -324,8 +324,11 @@ self_attn_kernel(const float *__restrict__ qkv, long long ld3, int d,
 
 // Warp per row for d % 128 == 0, d <= 1024 (NV = d / 128 float4 per lane):
 // q in registers, every ancestor's k / v row gathered with NV independent
-// 16-B loads per lane, scores and softmax in registers -- no block barrier
-template <int NV>
+// 16-B loads per lane, scores and softmax in registers -- no block barrier.
+// HS: the factored history keeps n (= k = v) as fp16 hi / lo halves after
+// q' ([q' fp32 | n hi | n lo], the next GEMM reads the same halves), and n
+// is rebuilt as hi + lo (~2^-22 relative)
+template <int NV, bool HS>
 __global__ void __launch_bounds__(256)
 self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
                       const int *__restrict__ anc, int stride, int hist_row0, int rows,
@@ -339,18 +342,33 @@ self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
   float4 q[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) q[i] = q4[lane + 32 * i];
+  // element block i of history row `row` at column offset `off` (k: d, v: v_off)
+  auto hrow = [&](long long row, int off, int i) -> float4 {
+    if constexpr (HS) {
+      const __half *hb = reinterpret_cast<const __half *>(qkv + row * ld3) + 2 * d;
+      const int j = 4 * (lane + 32 * i);
+      const uint2 h = *reinterpret_cast<const uint2 *>(hb + j);
+      const uint2 l = *reinterpret_cast<const uint2 *>(hb + d + j);
+      const float2 h0 = __half22float2(*reinterpret_cast<const __half2 *>(&h.x));
+      const float2 h1 = __half22float2(*reinterpret_cast<const __half2 *>(&h.y));
+      const float2 l0 = __half22float2(*reinterpret_cast<const __half2 *>(&l.x));
+      const float2 l1 = __half22float2(*reinterpret_cast<const __half2 *>(&l.y));
+      return make_float4(h0.x + l0.x, h0.y + l0.y, h1.x + l1.x, h1.y + l1.y);
+    } else {
+      return reinterpret_cast<const float4 *>(qkv + row * ld3 + off)[lane + 32 * i];
+    }
+  };
   float sc[kMaxPos];
   float mx = -INFINITY;
 #pragma unroll
   for (int t = 0; t < kMaxPos; ++t) {
     sc[t] = -INFINITY;
     if (t < np) {
-      const float4 *k4 =
-          reinterpret_cast<const float4 *>(qkv + (long long)anc[(long long)g * stride + t] * ld3 + d);
+      const long long row = anc[(long long)g * stride + t];
       float acc = 0.f;
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
-        const float4 k = k4[lane + 32 * i];
+        const float4 k = hrow(row, d, i);
         acc = fmaf(q[i].x, k.x, fmaf(q[i].y, k.y, fmaf(q[i].z, k.z, fmaf(q[i].w, k.w, acc))));
       }
       sc[t] = warp_sum(acc) * scale;
@@ -369,11 +387,10 @@ self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
   for (int t = 0; t < kMaxPos; ++t) {
     if (t < np) {
       const float pt = expf(sc[t] - lse);
-      const float4 *v4 = reinterpret_cast<const float4 *>(
-          qkv + (long long)anc[(long long)g * stride + t] * ld3 + v_off);
+      const long long row = anc[(long long)g * stride + t];
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
-        const float4 v = v4[lane + 32 * i];
+        const float4 v = hrow(row, v_off, i);
         o[i].x = fmaf(pt, v.x, o[i].x);
         o[i].y = fmaf(pt, v.y, o[i].y);
         o[i].z = fmaf(pt, v.z, o[i].z);
@@ -403,20 +420,29 @@ self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
 int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_stride,
               int hist_row0, int rows, int npos_uniform, const int *npos_row,
               float *out, long long ldo, cudaStream_t st, __half *out_hi, __half *out_lo,
-              int v_off) {
+              int v_off, bool hist_split) {
   if (rows <= 0) return GR4AD_OK;
   if (v_off < 0) v_off = 2 * d;
   if (out_hi && (d % 4 != 0 || ld3 % 4 != 0 || ldo % 4 != 0))
     return set_err(GR4AD_ERR_UNSUPPORTED, "split self-attention output: d %d", d);
   const float scale = 1.0f / sqrtf((float)d);
   prof_tag("self_attn rows=%d", rows);
-  if (d % 128 == 0 && d <= 1024 && ld3 % 4 == 0 && ldo % 4 == 0) {
+  const bool warp_ok = d % 128 == 0 && d <= 1024 && ld3 % 4 == 0 && ldo % 4 == 0;
+  if (hist_split && (!warp_ok || v_off != d))
+    return set_err(GR4AD_ERR_UNSUPPORTED, "split self-attention history: d %d", d);
+  if (warp_ok) {
 #define GR_SAW(NV)                                                                           \
   case NV:                                                                                   \
-    GR_LAUNCH(KC_SELF_ATTN, st, self_attn_warp_kernel<NV><<<ceil_div(rows, 8), 256, 0, st>>>( \
-                                    qkv, ld3, d, anc, anc_stride, hist_row0, rows,           \
-                                    npos_uniform, npos_row, out, ldo, scale, out_hi, out_lo, \
-                                    v_off));                                                 \
+    if (hist_split)                                                                          \
+      GR_LAUNCH(KC_SELF_ATTN, st,                                                            \
+                self_attn_warp_kernel<NV, true><<<ceil_div(rows, 8), 256, 0, st>>>(          \
+                    qkv, ld3, d, anc, anc_stride, hist_row0, rows, npos_uniform, npos_row,   \
+                    out, ldo, scale, out_hi, out_lo, v_off));                                \
+    else                                                                                     \
+      GR_LAUNCH(KC_SELF_ATTN, st,                                                            \
+                self_attn_warp_kernel<NV, false><<<ceil_div(rows, 8), 256, 0, st>>>(         \
+                    qkv, ld3, d, anc, anc_stride, hist_row0, rows, npos_uniform, npos_row,   \
+                    out, ldo, scale, out_hi, out_lo, v_off));                                \
     return GR4AD_OK;
     switch (d / 128) {
       GR_SAW(1) GR_SAW(2) GR_SAW(3) GR_SAW(4) GR_SAW(5) GR_SAW(6) GR_SAW(7) GR_SAW(8)
@@ -927,6 +953,67 @@ __global__ void __launch_bounds__(kSelThreads, 2) topk_select_kernel(SelectArgs 
       for (int r = wid; r < c.n_rows; r += kSelWarps) {
         const float cr = c.cum[c.hist0 + c.row0 + r];
         const float2 ri = c.rowinfo ? c.rowinfo[c.row0 + r] : make_float2(0.f, 0.f);
+        if (vec4 && a.proxies) {
+          // block-skipping collect: the proxies are the exact maxima of the
+          // row's 64-column blocks (same fp32 values the logits hold), so a
+          // block whose maximum is outside the window holds no window
+          // candidate and is never read -- only the few blocks around the
+          // cut leave HBM
+          const float *row = c.logits + (long long)(c.row0 + r) * c.ld;
+          for (int j0 = 0; j0 < a.proxy_ld; j0 += 32) {
+            const int j = j0 + lane;
+            bool q1 = false, q2 = false;
+            if (j < a.proxy_ld) {
+              const float4 pr = a.proxies[(long long)(c.row0 + r) * a.proxy_ld + j];
+              q1 = pr.z > -INFINITY && sbin(cr + ((pr.z - ri.x) - ri.y)) <= (unsigned)wb;
+              q2 = pr.w > -INFINITY && sbin(cr + ((pr.w - ri.x) - ri.y)) <= (unsigned)wb;
+            }
+            unsigned m1 = __ballot_sync(0xffffffffu, q1), m2 = __ballot_sync(0xffffffffu, q2);
+            while (m1 | m2) {
+              int blk;  // 64-column block index (2 per proxy entry)
+              if (m1 && (!m2 || __ffs(m1) <= __ffs(m2))) {
+                const int b = __ffs(m1) - 1;
+                m1 &= m1 - 1;
+                blk = 2 * (j0 + b);
+              } else {
+                const int b = __ffs(m2) - 1;
+                m2 &= m2 - 1;
+                blk = 2 * (j0 + b) + 1;
+              }
+              const int v0 = 64 * blk + 2 * lane;
+              float2 l2 = make_float2(-INFINITY, -INFINITY);
+              if (v0 + 1 < c.V) l2 = *reinterpret_cast<const float2 *>(row + v0);
+              else if (v0 < c.V) l2.x = row[v0];
+              const float sv[2] = {cr + ((l2.x - ri.x) - ri.y), cr + ((l2.y - ri.x) - ri.y)};
+              unsigned pm = 0;
+#pragma unroll
+              for (int q = 0; q < 2; ++q)
+                if (v0 + q < c.V && sbin(sv[q]) <= (unsigned)wb) pm |= 1u << q;
+              if (__any_sync(0xffffffffu, pm != 0)) {
+                const unsigned np = __popc(pm);
+                unsigned incl = np;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                  const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                  if (lane >= o) incl += y;
+                }
+                unsigned base = 0;
+                if (lane == 31) base = atomicAdd(&s_gt_pos, incl);
+                base = __shfl_sync(0xffffffffu, base, 31) + incl - np;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                  const bool take = (pm >> q) & 1u;
+                  const unsigned fi = (unsigned)((long long)r * c.V + v0 + q);
+                  const unsigned long long e =
+                      ((unsigned long long)f2ord(sv[q]) << 32) | (0xFFFFFFFFu - fi);
+                  if (take && base < (unsigned)GR4AD_MAX_BEAM) sbuf[base] = e;
+                  base += take ? 1u : 0u;
+                }
+              }
+            }
+          }
+          continue;
+        }
         if (vec4) {
           const float4 *row4 =
               reinterpret_cast<const float4 *>(c.logits + (long long)(c.row0 + r) * c.ld);

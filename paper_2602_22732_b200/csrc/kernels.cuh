@@ -32,7 +32,7 @@ int softmax_rows(float *s, long long ld, int rows, const int *row_req,
 int self_attn(const float *qkv, long long ld3, int d, const int *anc, int anc_stride,
               int hist_row0, int rows, int npos_uniform, const int *npos_row,
               float *out, long long ldo, cudaStream_t st, __half *out_hi = nullptr,
-              __half *out_lo = nullptr, int v_off = -1);
+              __half *out_lo = nullptr, int v_off = -1, bool hist_split = false);
 
 // dst = fp16 hi / lo split of scale * src (row-major, rows x cols)
 int split16(const float *src, long long lds, __half *dst_hi, __half *dst_lo, long long ldd,
@@ -54,8 +54,8 @@ int latent_cross_ln(const float *h, int d, const __half *aq_hi, const __half *aq
                     int *flag, cudaStream_t st);
 int latent_out_ln(const float *z, int F, const __half *bo_hi, const __half *bo_lo, float alpha,
                   const float *c, float *hs, int d, const float *g2, const float *b2,
-                  __half *n_hi, __half *n_lo, float *hn, long long ld_hn, int rows, int *flag,
-                  cudaStream_t st);
+                  __half *n_hi, __half *n_lo, long long ld_n, float *hn, long long ld_hn,
+                  int rows, int *flag, cudaStream_t st);
 int latent_fold(const float *at, const float *g1, const float *b1, int d, int F, float *ag,
                 float *sv, float *cv, cudaStream_t st);
 int latent_feat_kst(int F);  // halves per pre-split feature row

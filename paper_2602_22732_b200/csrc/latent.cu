@@ -205,8 +205,11 @@ latent_attn_kernel(const float *__restrict__ q, const float *__restrict__ feats,
         bl[n] = __ldg(pl[n] + (k0 >> 3));
       }
     };
-    load(0);
-    for (int k0 = 0; k0 < d; k0 += 32) {
+    // warps sharing a row tile (small groups: KSL key slices) split the k
+    // range of q_lat too and add their partials through shared memory
+    const int kspan = d / KSL, kbeg = ks * kspan, kend = kbeg + kspan;
+    load(kbeg);
+    for (int k0 = kbeg; k0 < kend; k0 += 32) {
       float4 ca[2] = {xa[0], xa[1]}, cb[2] = {xb[0], xb[1]};
       uint4 ch[FT], cl[FT];
 #pragma unroll
@@ -215,7 +218,7 @@ latent_attn_kernel(const float *__restrict__ q, const float *__restrict__ feats,
         ch[n] = live ? bh[n] : make_uint4(0, 0, 0, 0);
         cl[n] = live ? bl[n] : make_uint4(0, 0, 0, 0);
       }
-      if (k0 + 32 < d) load(k0 + 32);
+      if (k0 + 32 < kend) load(k0 + 32);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         float4 u = ca[j], v = cb[j];
@@ -241,6 +244,40 @@ latent_attn_kernel(const float *__restrict__ q, const float *__restrict__ feats,
     // row statistics (the quad's four lanes hold a row's partial sums)
     s1A = lat_qsum(s1A); s2A = lat_qsum(s2A);
     s1B = lat_qsum(s1B); s2B = lat_qsum(s2B);
+    if (KSL > 1) {  // sum the k-slice partials of this row tile (block-uniform)
+      constexpr int SL = FP + 2;
+      float *mw = mrg + warp * 16 * SL;
+#pragma unroll
+      for (int n = 0; n < FT; ++n) {
+        const int col = 8 * n + 2 * qq;
+        mw[gq * SL + col] = c[n][0];
+        mw[gq * SL + col + 1] = c[n][1];
+        mw[(gq + 8) * SL + col] = c[n][2];
+        mw[(gq + 8) * SL + col + 1] = c[n][3];
+      }
+      if (qq == 0) {
+        mw[gq * SL + FP] = s1A; mw[gq * SL + FP + 1] = s2A;
+        mw[(gq + 8) * SL + FP] = s1B; mw[(gq + 8) * SL + FP + 1] = s2B;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int n = 0; n < FT; ++n) c[n][0] = c[n][1] = c[n][2] = c[n][3] = 0.f;
+      s1A = s2A = s1B = s2B = 0.f;
+      for (int k2 = 0; k2 < KSL; ++k2) {
+        const float *ow = mrg + (k2 * RT + rt) * 16 * SL;
+#pragma unroll
+        for (int n = 0; n < FT; ++n) {
+          const int col = 8 * n + 2 * qq;
+          c[n][0] += ow[gq * SL + col];
+          c[n][1] += ow[gq * SL + col + 1];
+          c[n][2] += ow[(gq + 8) * SL + col];
+          c[n][3] += ow[(gq + 8) * SL + col + 1];
+        }
+        s1A += ow[gq * SL + FP]; s2A += ow[gq * SL + FP + 1];
+        s1B += ow[(gq + 8) * SL + FP]; s2B += ow[(gq + 8) * SL + FP + 1];
+      }
+      __syncthreads();  // (the merge area is reused at the end)
+    }
     const float invd = 1.f / (float)d;
     const float mA = s1A * invd, mB = s1B * invd;  // mu - k
     const float rA = 1.0f / sqrtf(fmaxf(fmaf(s2A, invd, -mA * mA), 0.f) + 1e-5f);
@@ -473,8 +510,8 @@ __global__ void __launch_bounds__(NW * 32, 2)
 latent_out_ln_kernel(const float *__restrict__ z, const __half *__restrict__ bo_hi,
                      const __half *__restrict__ bo_lo, float alpha, const float *__restrict__ c,
                      float *hs, const float *__restrict__ g2, const float *__restrict__ b2,
-                     __half *__restrict__ n_hi, __half *__restrict__ n_lo, float *__restrict__ hn,
-                     long long ld_hn, int rows, int *flag) {
+                     __half *__restrict__ n_hi, __half *__restrict__ n_lo, long long ld_n,
+                     float *__restrict__ hn, long long ld_hn, int rows, int *flag) {
   constexpr int FP = F < 16 ? 16 : F, KK = FP / 16, D = LatOut<NW>::D, LDT = LatOut<NW>::LDT;
   extern __shared__ float4 sm4[];
   float *tile = reinterpret_cast<float *>(sm4);
@@ -583,8 +620,8 @@ latent_out_ln_kernel(const float *__restrict__ z, const __half *__restrict__ bo_
       uint32_t h0, l0, h1, l1;
       lat_split2(o[0], o[1], h0, l0);
       lat_split2(o[2], o[3], h1, l1);
-      *reinterpret_cast<uint2 *>(n_hi + gr * D + j) = make_uint2(h0, h1);
-      *reinterpret_cast<uint2 *>(n_lo + gr * D + j) = make_uint2(l0, l1);
+      *reinterpret_cast<uint2 *>(n_hi + gr * ld_n + j) = make_uint2(h0, h1);
+      *reinterpret_cast<uint2 *>(n_lo + gr * ld_n + j) = make_uint2(l0, l1);
       if (hn) *reinterpret_cast<float4 *>(hn + gr * ld_hn + j) = make_float4(o[0], o[1], o[2], o[3]);
     }
   }
@@ -592,17 +629,21 @@ latent_out_ln_kernel(const float *__restrict__ z, const __half *__restrict__ bo_
 
 #define GR_LAT_F(M) M(4) M(8) M(16) M(32)
 
-static int rows_per_cta_for(int max_group_rows) {
+static int rows_per_cta_for(int max_group_rows, int n_groups) {
   // one 16-row tile per warp, or fewer row tiles with the keys split
-  // between the warps
-  return max_group_rows <= 16 ? 16 : (max_group_rows <= 32 ? 32 : 64);
+  // between the warps: the widest tile that still gives >= 4 CTAs per SM
+  // (148 SMs), so small groups (DBW early levels, trunk rows) fill the GPU
+  const int cap = max_group_rows <= 16 ? 16 : (max_group_rows <= 32 ? 32 : 64);
+  for (int rpc = cap; rpc > 16; rpc >>= 1)
+    if ((long long)n_groups * ceil_div(max_group_rows, rpc) >= 4 * 148) return rpc;
+  return 16;
 }
 
 int latent_attn(const float *q, const float *feats, int F, const int *g_row_off, const int *g_rows,
                 const int *g_ctx_off, const int *g_ctx_len, int n_groups, int max_group_rows,
                 float scale, float *z, int *flag, cudaStream_t st) {
   if (n_groups <= 0 || max_group_rows <= 0) return GR4AD_OK;
-  const int rpc = rows_per_cta_for(max_group_rows);
+  const int rpc = rows_per_cta_for(max_group_rows, n_groups);
   prof_tag("latent_attn groups=%d max_rows=%d", n_groups, max_group_rows);
 #define GR_LA_F(FF)                                                                          \
   if (F == FF) {                                                                             \
@@ -627,7 +668,7 @@ int latent_cross_ln(const float *h, int d, const __half *aq_hi, const __half *aq
                     int *flag, cudaStream_t st) {
   if (n_groups <= 0 || max_group_rows <= 0) return GR4AD_OK;
   if (!latent_supported(d, F)) return set_err(GR4AD_ERR_UNSUPPORTED, "latent LN1: d %d F %d", d, F);
-  const int rpc = rows_per_cta_for(max_group_rows);
+  const int rpc = rows_per_cta_for(max_group_rows, n_groups);
   const LatLn ln{h, d, aq_hi, aq_lo, s1, c1, fs_hi, fs_lo};
   prof_tag("latent_ln1 groups=%d max_rows=%d", n_groups, max_group_rows);
 #define GR_LA_F(FF)                                                                          \
@@ -735,10 +776,10 @@ int latent_feat_split(const float *fin, long long rows_used, long long rows_allo
 
 int latent_out_ln(const float *z, int F, const __half *bo_hi, const __half *bo_lo, float alpha,
                   const float *c, float *hs, int d, const float *g2, const float *b2,
-                  __half *n_hi, __half *n_lo, float *hn, long long ld_hn, int rows, int *flag,
-                  cudaStream_t st) {
+                  __half *n_hi, __half *n_lo, long long ld_n, float *hn, long long ld_hn,
+                  int rows, int *flag, cudaStream_t st) {
   if (rows <= 0) return GR4AD_OK;
-  if (!latent_supported(d, F) || (hn && ld_hn % 4 != 0))
+  if (!latent_supported(d, F) || (hn && ld_hn % 4 != 0) || ld_n % 4 != 0)
     return set_err(GR4AD_ERR_UNSUPPORTED, "latent output + LN2: d %d F %d", d, F);
   prof_tag("latent_out_ln2 rows=%d", rows);
   const float a = alpha / kLatZs;
@@ -749,8 +790,8 @@ int latent_out_ln(const float *z, int F, const __half *bo_hi, const __half *bo_l
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));     \
     GR_LAUNCH(KC_LAYERNORM, st, latent_out_ln_kernel<FF, NW><<<ceil_div(rows, 16), NW * 32,   \
                                                                sm, st>>>(                    \
-                                    z, bo_hi, bo_lo, a, c, hs, g2, b2, n_hi, n_lo, hn, ld_hn, \
-                                    rows, flag));                                            \
+                                    z, bo_hi, bo_lo, a, c, hs, g2, b2, n_hi, n_lo, ld_n, hn, \
+                                    ld_hn, rows, flag));                                     \
     return GR4AD_OK;                                                                         \
   }
 #define GR_LO_F(FF) GR_LO(FF, 1) GR_LO(FF, 2) GR_LO(FF, 3) GR_LO(FF, 4) GR_LO(FF, 5) \

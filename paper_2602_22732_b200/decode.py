@@ -12,8 +12,10 @@ it can be captured once into a CUDA graph and replayed per batch.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from collections import OrderedDict
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import torch
@@ -103,6 +105,7 @@ class BeamDecoder:
         bt.valid_prefix_count = self._vcount
         bt.decode_path = self.PATHS[path]
         self.batch = bt
+        self._bind_derived()
         nbytes, max_out = C.c_size_t(), C.c_int()
         N.check(N.lib.gr4ad_workspace_bytes(C.byref(self.dims), C.byref(bt), C.byref(nbytes),
                                             C.byref(max_out)))
@@ -124,7 +127,6 @@ class BeamDecoder:
         N.check(N.lib.gr4ad_prepare(C.byref(self.dims), C.byref(bt),
                                     C.c_void_p(self.workspace.data_ptr()),
                                     self.workspace_bytes, _stream_handle(self.device)))
-        self._prepare_weights()
         off = C.c_size_t()
         N.check(N.lib.gr4ad_range_flag_offset(C.byref(self.dims), C.byref(bt), C.byref(off)))
         self._flag = self.workspace[off.value:off.value + 4].view(torch.int32)
@@ -140,15 +142,32 @@ class BeamDecoder:
         self._resolved = False
         self.last_item_idx = None
 
-    def _prepare_weights(self):
-        """Derived weight copies (mma fragments / K-major fp16 splits) built
-        once per bound snapshot; decodes then skip them (weights_prepared)."""
-        self.batch.weights_prepared = 0
-        N.check(N.lib.gr4ad_prepare_weights(C.byref(self.dims), C.byref(self.weights.struct),
-                                            C.byref(self.batch),
-                                            C.c_void_p(self.workspace.data_ptr()),
-                                            self.workspace_bytes, _stream_handle(self.device)))
-        self.batch.weights_prepared = 1
+    def _bind_derived(self):
+        """Point the batch at the snapshot's derived weight copies (factored
+        / absorbed products, fuse tables, K-major fp16 splits, mma fragments):
+        one buffer per (snapshot, plan layout) held by the DeviceWeights and
+        built on first use, so decoders of any batch shape share it and a new
+        shape costs no weight preparation (gr4ad_derived_layout)."""
+        bt = self.batch
+        bt.derived = None
+        bt.derived_bytes = 0
+        nb, sig = C.c_size_t(), C.c_ulonglong()
+        N.check(N.lib.gr4ad_derived_layout(C.byref(self.dims), C.byref(bt), C.byref(nb),
+                                           C.byref(sig)))
+
+        def prepare(buf):
+            bt.derived = C.c_void_p(buf.data_ptr())
+            bt.derived_bytes = nb.value
+            bt.weights_prepared = 0
+            N.check(N.lib.gr4ad_prepare_weights(C.byref(self.dims), C.byref(self.weights.struct),
+                                                C.byref(bt), None, 0,
+                                                _stream_handle(self.device)))
+
+        buf = self.weights.derived_buffer(sig.value, nb.value, prepare)
+        self._derived = buf
+        bt.derived = C.c_void_p(buf.data_ptr())
+        bt.derived_bytes = nb.value
+        bt.weights_prepared = 1
 
     def rebind(self, model):
         """Decode with another snapshot of the same config (hot swap).  The
@@ -157,7 +176,7 @@ class BeamDecoder:
         if model.config != self.cfg:
             raise ValueError("rebind needs a snapshot with the same DecoderConfig")
         self.weights = device_weights(model, self.device)
-        self._prepare_weights()
+        self._bind_derived()
         # every captured graph holds the previous snapshot's weight pointers
         self.graph = None
         self._graph_inputs = None
@@ -386,6 +405,40 @@ class InputRangeError(RuntimeError):
     """A finite float64 input that does not fit the fp32 decode."""
 
 
+_STAGE_WORKERS = max(1, min(8, (os.cpu_count() or 2) // 2))
+_STAGE_POOL = None
+_STAGE_LOCK = threading.Lock()
+
+
+def _stage_pool():
+    global _STAGE_POOL
+    with _STAGE_LOCK:
+        if _STAGE_POOL is None:
+            _STAGE_POOL = ThreadPoolExecutor(_STAGE_WORKERS, thread_name_prefix="gr4ad-stage")
+        return _STAGE_POOL
+
+
+def _stage_blocks(blocks, staged):
+    """Cast + concatenate per-request float64 blocks into the pinned fp32
+    staging rows, split over a few threads (numpy copies release the GIL);
+    returns False if a value leaves the fp32 range."""
+    offs = np.cumsum([0] + [a.shape[0] for a in blocks])
+    n = len(blocks)
+    parts = min(_STAGE_WORKERS, max(1, int(offs[-1]) // 16384), n)
+
+    def work(lo, hi):
+        out = staged[offs[lo]:offs[hi]]
+        with np.errstate(over="ignore"):
+            np.concatenate(blocks[lo:hi], 0, out=out, casting="unsafe")
+        return bool(np.isfinite(out).all())
+
+    if parts <= 1:
+        return work(0, n)
+    cuts = [round(k * n / parts) for k in range(parts + 1)]
+    futs = [_stage_pool().submit(work, cuts[k], cuts[k + 1]) for k in range(parts)]
+    return all(f.result() for f in futs)
+
+
 def _decode_on(dec, model, host_input, kind, items):
     if True:
         if dec.weights is not device_weights(model, dec.device):
@@ -404,13 +457,14 @@ def _decode_on(dec, model, host_input, kind, items):
             if dec._in_host is None:
                 dec._in_host = torch.empty(shape, dtype=torch.float32).pin_memory()
             staged = dec._in_host.numpy()
-            with np.errstate(over="ignore"):
-                if isinstance(host_input, (list, tuple)):
-                    # one pass: concatenate + cast straight into pinned memory
-                    np.concatenate(host_input, 0, out=staged, casting="unsafe")
-                else:
+            if isinstance(host_input, (list, tuple)):
+                # concatenate + cast straight into pinned memory, on a few threads
+                ok = _stage_blocks(host_input, staged)
+            else:
+                with np.errstate(over="ignore"):
                     np.copyto(staged, host_input, casting="unsafe")
-            if not np.isfinite(staged).all():
+                ok = bool(np.isfinite(staged).all())
+            if not ok:
                 raise InputRangeError("an input exceeds the fp32 range of the GPU decode")
             dec.in_buf.copy_(dec._in_host, non_blocking=True)
         inputs = {kind: dec.in_buf}

@@ -190,6 +190,21 @@ class DeviceWeights:
             lw.ffn_W1, lw.ffn_b1 = ptr(pre + "ffn.W1"), ptr(pre + "ffn.b1")
             lw.ffn_W2, lw.ffn_b2 = ptr(pre + "ffn.W2"), ptr(pre + "ffn.b2")
         self.struct = w
+        self._derived = {}  # layout signature -> prepared derived-weight buffer
+        self._derived_lock = threading.Lock()
+
+    def derived_buffer(self, signature, nbytes, prepare):
+        """The snapshot's derived weight copies for one plan layout
+        (gr4ad_derived_layout signature): built once by ``prepare(buf)`` and
+        shared by every decoder of this snapshot with that layout, so a new
+        batch shape or width schedule costs no weight preparation."""
+        with self._derived_lock:
+            buf = self._derived.get(signature)
+            if buf is None:
+                buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=self.device)
+                prepare(buf)  # synchronous; raises (RangeError) before caching
+                self._derived[signature] = buf
+            return buf
 
     def use_on(self, stream=None):
         """Order ``stream`` (default: current) after the upload and tell the

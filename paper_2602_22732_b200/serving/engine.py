@@ -130,7 +130,9 @@ class LoadEstimator:
       at its own arrival;
     * capacity -- requests decoded per second of decode time, an EWMA over
       the engine's own GPU batches (wall time around each batched decode,
-      results on the host).
+      results on the host); only batches of at least half the largest batch
+      seen update it (a small batch is latency-bound and would read as a
+      low capacity).
 
     ``capacity_slack = clamp(1 - rate / capacity, 0, 1)`` (the C4 sweep's
     definition); 1.0 until a capacity has been measured."""
@@ -141,6 +143,7 @@ class LoadEstimator:
         self._arrivals = []  # sorted request times inside the window
         self._head = 0
         self.capacity = None  # requests / s of decode time
+        self._max_batch = 0
         self._lock = threading.Lock()
 
     def observe(self, now, n=1):
@@ -168,6 +171,9 @@ class LoadEstimator:
             return
         c = n_requests / seconds
         with self._lock:
+            self._max_batch = max(self._max_batch, int(n_requests))
+            if 2 * n_requests < self._max_batch:
+                return
             self.capacity = c if self.capacity is None else (
                 (1 - self.alpha) * self.capacity + self.alpha * c)
 

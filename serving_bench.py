@@ -1,16 +1,20 @@
 """Load-adaptive dynamic beam serving on one B200 (BASELINE config 4,
-SURVEY §8d C4).
+SURVEY §8d C4), through the drop-in serving API.
 
-Real-time Poisson arrivals at 0.1x-1.5x of measured capacity; a batch former
-takes every arrived request (up to --max-batch); each batch's per-level
-widths come from the reference's DBS logic, ``scale_schedule(base,
-tabs_adjust(TrafficSignal(qps, q_threshold=capacity, slack)))`` with
-``slack = clamp(1 - load/capacity, 0, 1)`` (schedule.py:54-70,
-engine.py:100-103): off-peak traffic gets up to 1.6x wider beams, peak
-traffic the base widths.  Request features are synthetic and device
-resident (a pool gathered per batch); every (batch bucket, widths) shape is
-captured once as a CUDA graph and replayed per batch; latency is arrival ->
-results on the host.  Prints one JSON line per offered load.
+Real-time Poisson arrivals at 0.1x-1.5x of measured capacity.  A batch
+former hands every arrived request (up to --max-batch) to
+``ServingEngine.serve_batch`` (engine.py:84-121 semantics) with
+``qps=None``: the engine's own ``LoadEstimator`` measures the arrival rate
+(sliding window) and its decode capacity, and each request gets the widths
+of the load at ITS arrival, ``scale_schedule(base, tabs_adjust(
+TrafficSignal(qps, q_threshold, slack)))`` with ``slack = clamp(1 -
+qps / capacity, 0, 1)`` (schedule.py:54-70, engine.py:100-103) -- off-peak
+traffic gets up to 1.6x wider beams, peak traffic the base widths.  Inputs
+are host float64 (S, F) feature matrices (unique users, so no TTL-cache
+hits); every call does the H2D copy, the decode (pooled decoders sharing one
+prepared copy of the snapshot's derived weights), on-device SID -> item
+resolution, the D2H copy and the host SemanticId / item lists.  Latency is
+arrival -> ServeResult on the host.  Prints one JSON line per offered load.
 
     python serving_bench.py [--model c5|c2] [--duration 3] [--loads 0.1,...]
 """
@@ -44,82 +48,67 @@ def main():
     ap.add_argument("--loads", default="0.1,0.25,0.5,0.75,1.0,1.25,1.5")
     ap.add_argument("--max-batch", type=int, default=128)
     ap.add_argument("--boost", type=float, default=0.6)
+    ap.add_argument("--items", type=int, default=100000)
     ap.add_argument("--p99-bound-ms", type=float, default=None)
     args = ap.parse_args()
 
     import torch
 
-    from paper_2602_22732_b200.decode import BeamDecoder
     from paper_2602_22732_b200.model import DecoderConfig, DecoderModel
-    from paper_2602_22732_b200.serving.schedule import (BeamSchedule, TrafficSignal,
-                                                       capacity_slack, scale_schedule,
-                                                       tabs_adjust)
+    from paper_2602_22732_b200.quantizer import SemanticId, SidIndex
+    from paper_2602_22732_b200.serving import (BeamSchedule, ServingConfig, ServingEngine,
+                                               SnapshotStore)
+    from paper_2602_22732_b200.serving.engine import LoadEstimator
 
-    dev = torch.device("cuda")
+    assert torch.cuda.is_available(), "serving_bench needs a CUDA device"
     mcfg, S, base = MODELS[args.model]
     F, d, dff, L, K, V, nb = mcfg
     model = DecoderModel(DecoderConfig(F, d, dff, L, K, V, nb, seed=2))
     base_sched = BeamSchedule(base, base[-1])
+    store = SnapshotStore(model)
+    index = SidIndex()
+    rng = np.random.default_rng(3)
+    toks = np.stack([rng.integers(0, v, size=args.items) for v in V], 1)
+    for i, t in enumerate(toks.tolist()):
+        index.upsert(i, SemanticId(tuple(t), V))
     pool_n = 4 * args.max_batch
-    gen = torch.Generator(device=dev).manual_seed(1000)
-    pool = torch.randn((pool_n, S, F), generator=gen, device=dev)
+    feats = [np.random.default_rng(1000 + i).normal(size=(S, F)) for i in range(pool_n)]
+    uid = [0]
 
-    buckets = [b for b in (8, 16, 32, 64, 128, 256, 512) if b <= args.max_batch]
-    if buckets[-1] != args.max_batch:
-        buckets.append(args.max_batch)
-    cache = OrderedDict()
+    def requests(n, t_arr):
+        out = []
+        for j in range(n):
+            out.append((f"user{uid[0]:08d}", feats[uid[0] % pool_n], float(t_arr[j])))
+            uid[0] += 1
+        return out
 
-    def decoder(nreq, widths):
-        bucket = next(b for b in buckets if b >= nreq)
-        key = (bucket, tuple(widths))
-        dec = cache.get(key)
-        if dec is None:
-            while len(cache) >= len(buckets):
-                cache.popitem(last=False)
-            bd = BeamDecoder(model, [S] * bucket, [widths] * bucket, device=dev)
-            fb = torch.zeros((bucket * S, F), device=dev)
-            bd.capture(features=fb)  # one graph replay per batch (no per-kernel host launches)
-            dec = (bd, fb)
-            cache[key] = dec
-        cache.move_to_end(key)
-        return dec
+    def engine(capacity):
+        cfg = ServingConfig(schedule=base_sched, q_threshold=capacity, boost=args.boost, ttl=60.0)
+        return ServingEngine(store, index, cfg, load=LoadEstimator(window=1.0))
 
-    def run_batch(idx, widths):
-        dec, feats = decoder(len(idx), widths)
-        bucket = feats.shape[0] // S
-        rows = torch.as_tensor(np.resize(idx, bucket) % pool_n, device=dev)
-        feats.view(bucket, S, F).copy_(pool.index_select(0, rows))
-        dec.replay()
-        cnt = dec.count.cpu()  # results on the host (sync)
-        return int(cnt[: len(idx)].sum())
-
-    # capacity at base widths, full batches
-    for _ in range(2):
-        run_batch(np.arange(args.max_batch), base)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    # capacity at base widths: full batches through the same API (explicit
+    # qps above the threshold -> base widths), warm pools first
+    eng = engine(1e12)
+    for _ in range(3):
+        eng.serve_batch(requests(args.max_batch, np.zeros(args.max_batch)), 0.0, qps=1e13)
     reps = 5
+    t0 = time.perf_counter()
     for _ in range(reps):
-        run_batch(np.arange(args.max_batch), base)
+        eng.serve_batch(requests(args.max_batch, np.zeros(args.max_batch)), 0.0, qps=1e13)
     cap = reps * args.max_batch / (time.perf_counter() - t0)
     print(json.dumps({"model": args.model, "capacity_req_s": cap, "base_widths": list(base),
-                      "max_batch": args.max_batch}), flush=True)
+                      "max_batch": args.max_batch, "api": "ServingEngine.serve_batch",
+                      "items_indexed": args.items}), flush=True)
 
-    rng = np.random.default_rng(7)
     for rho in [float(x) for x in args.loads.split(",")]:
         lam = rho * cap
         n = max(1, int(lam * args.duration))
         arrivals = np.cumsum(rng.exponential(1.0 / lam, size=n))
-        slack = capacity_slack(lam, cap)
-        active = tabs_adjust(TrafficSignal(lam, cap, slack), base_sched.base_width, args.boost)
-        widths = scale_schedule(base_sched, active).widths
-        for b in buckets:  # plans + workspaces built before the clock starts
-            run_batch(np.arange(b), widths)
-        torch.cuda.synchronize()
+        eng = engine(cap)
+        eng.load.capacity = cap  # seeded with the calibration; the engine's EWMA refines it
         lat = np.zeros(n)
-        done = 0
-        batches = 0
-        served_results = 0
+        widths_seen = []
+        done = batches = n_items = 0
         start = time.perf_counter()
         while done < n:
             now = time.perf_counter() - start
@@ -129,18 +118,24 @@ def main():
             hi = done
             while hi < n and hi - done < args.max_batch and arrivals[hi] <= now:
                 hi += 1
-            served_results += run_batch(np.arange(done, hi), widths)
+            res = eng.serve_batch(requests(hi - done, arrivals[done:hi]), now)
             t_done = time.perf_counter() - start
             lat[done:hi] = t_done - arrivals[done:hi]
+            widths_seen.extend(r.widths[-1] for r in res)
+            n_items += sum(len(r.items) for r in res)
             batches += 1
             done = hi
         wall = time.perf_counter() - start
+        ws = np.asarray(widths_seen)
         line = {"model": args.model, "offered_load": rho, "offered_req_s": lam,
                 "achieved_req_s": n / wall, "requests": n, "batches": batches,
-                "mean_batch": n / batches, "tabs_active_width": active, "widths": list(widths),
-                "slack": slack, "latency_ms": {"p50": 1e3 * float(np.percentile(lat, 50)),
-                                               "p99": 1e3 * float(np.percentile(lat, 99))},
-                "results": served_results}
+                "mean_batch": n / batches,
+                "last_level_width": {"min": int(ws.min()), "median": float(np.median(ws)),
+                                     "max": int(ws.max())},
+                "engine_capacity_req_s": eng.load.capacity,
+                "latency_ms": {"p50": 1e3 * float(np.percentile(lat, 50)),
+                               "p99": 1e3 * float(np.percentile(lat, 99))},
+                "items_resolved": n_items}
         if args.p99_bound_ms is not None:
             line["p99_within_bound"] = line["latency_ms"]["p99"] <= args.p99_bound_ms
         print(json.dumps(line), flush=True)

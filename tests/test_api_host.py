@@ -160,3 +160,8 @@ def test_load_estimator_rate_and_slack():
     hi = scale_schedule(sched, tabs_adjust(TrafficSignal(qps2, 1000.0, slack2), 256, 0.6))
     assert hi.widths == (64, 128, 256) and lo.widths[-1] > hi.widths[-1]
     assert est.rate(10.0) == 0.0  # the window slides
+    # a small (latency-bound) batch does not read as a capacity drop
+    est.record_service(10, 1.0)
+    assert abs(est.capacity - 400.0) < 1e-9
+    est.record_service(300, 0.5)  # >= half the largest batch: EWMA update
+    assert abs(est.capacity - (0.8 * 400.0 + 0.2 * 600.0)) < 1e-9

@@ -308,6 +308,34 @@ def test_pooled_decoder_and_graph_replay():
             _parity(want, got[i], "pooled")
 
 
+@pytest.mark.parametrize("d,path", [(128, "tensor"), (16, "fused")])
+def test_decoders_share_the_snapshots_derived_weights(d, path):
+    """Decoders of different batch shapes / widths of one snapshot share a
+    single prepared copy of the derived weights (gr4ad_derived_layout /
+    batch->derived): the second decoder prepares nothing, its workspace
+    excludes the region, and both decode like the oracle; a republished
+    snapshot gets its own copy."""
+    M, S = _need()
+    from paper_2602_22732_b200.decode import BeamDecoder
+    F = 16
+    model = M.DecoderModel(M.DecoderConfig(F, d, 2 * d, 3, 2, (256, 256, 256), 4, seed=5))
+    shapes = [([256] * 3, [(8, 16, 32)] * 3), ([256] * 5, [(16, 32, 64)] * 4 + [(4, 8, 16)])]
+    decs = [BeamDecoder(model, lens, widths, path=path) for lens, widths in shapes]
+    assert decs[0]._derived.data_ptr() == decs[1]._derived.data_ptr()
+    ocfg, params = _oracle_of(model)
+    for (lens, widths), dec in zip(shapes, decs):
+        feats = [c_features(100 + i, lens[i]) for i in range(len(lens))]
+        x = torch.from_numpy(np.concatenate(feats).astype(np.float32)).cuda()
+        dec.run(features=x)
+        got = dec.host_results()
+        for i in range(len(lens)):
+            want = orc.beam_search(params, ocfg, orc.context_process(feats[i], params), widths[i])
+            _parity(want, got[i], f"derived {path} shape {len(lens)} request {i}")
+    other = model.clone()
+    dec2 = BeamDecoder(other, *shapes[0], path=path)
+    assert dec2._derived.data_ptr() != decs[0]._derived.data_ptr()
+
+
 def test_rebind_drops_the_host_graph():
     """after a hot swap, replay_host must not run the previous
     snapshot's graph."""

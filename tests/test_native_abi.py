@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     from paper_2602_22732_b200 import _native as N
-    assert N.lib.gr4ad_abi_version() == 1
+    assert N.lib.gr4ad_abi_version() == 2
     assert N.lib.gr4ad_status_string(0) == b"ok"
     assert N.lib.gr4ad_status_string(1) == b"invalid argument"
 
