@@ -101,6 +101,15 @@ class ServingConfig:
     precut: bool = True
     value_rerank: bool = False
     mask_to_index: bool = False  # extension: valid-SID prefix masking
+    # batched engine (no reference counterpart; the reference serves one
+    # request per call): a batch's misses are padded to the next of these
+    # sizes so the pooled decoders (and their CUDA graphs) are reused across
+    # batches; None decodes exactly the misses
+    batch_buckets: tuple = (1, 2, 4, 8, 16, 32, 64, 128, 256, 512)
+    # TABS widths from the engine's own load signal: "batch" measures it once
+    # per batch (the reference's per-tick traffic signal, sim/loop.py:239-264),
+    # "request" at every request's arrival (per-request widths in one batch)
+    load_widths: str = "batch"
 
 
 @dataclass
@@ -303,6 +312,8 @@ class ServingEngine:
         version, model = self.store.current()
         if qps is not None:
             scheds = [self._widths(qps, capacity_slack)] * len(misses)
+        elif self.config.load_widths == "batch":
+            scheds = [self._widths(*self.load.signal(now))] * len(misses)
         else:
             scheds = []
             for i in misses:
@@ -311,30 +322,54 @@ class ServingEngine:
         valid = self.index.all_sids() if self.config.mask_to_index else None
         feats = [np.atleast_2d(np.asarray(requests[i][1], dtype=np.float64)) for i in misses]
         table = self._item_table(model)
-        local = LayerCallCounter()
+        # pad to a batch bucket with copies of the last miss (results dropped)
+        n = len(misses)
+        pad = n
+        for b in self.config.batch_buckets or ():
+            if b >= n:
+                pad = b
+                break
+        dfeats = feats + [feats[-1]] * (pad - n)
+        dscheds = list(scheds) + [scheds[-1]] * (pad - n)
         t0 = time.perf_counter()
         results, slots = beam_search_batch(
-            model, features=feats, schedules=scheds, shared_kv=self.config.shared_kv,
-            precut=self.config.precut, counter=local, value_rerank=self.config.value_rerank,
+            model, features=dfeats, schedules=dscheds, shared_kv=self.config.shared_kv,
+            precut=self.config.precut, value_rerank=self.config.value_rerank,
             buckets=self.buckets, valid_sids=valid, _items=table.args())
-        self.load.record_service(len(misses), time.perf_counter() - t0)
-        self.counter.add_layer_calls(local.layer_calls)
-        self.counter.add_kv_build(local.kv_builds, local.kv_floats)
+        self.load.record_service(n, time.perf_counter() - t0)
         with self._lock:
             self.model_invocations += len(misses)
+        calls = kv_b = kv_f = 0
         for j, (i, sids) in enumerate(zip(misses, results)):
             uid = requests[i][0]
             sched = scheds[j]
             items = table.resolve(sids, slots[j])
             self.cache.put((uid, version_key), (items, sids, version, sched.widths), now)
             # per-request virtual latency: the closed-form layer calls of its decode
-            c = LayerCallCounter()
-            record_counter(c, model.config, sched.widths, feats[j].shape[0],
-                           self.config.shared_kv, self.config.value_rerank,
-                           model.config.trunk_depth)
-            out[i] = ServeResult(items, sids, False, version, sched.widths,
-                                 latency_virtual=c.layer_calls)
+            c = self._closed_form(model.config, sched.widths, feats[j].shape[0])
+            calls += c[0]
+            kv_b += c[1]
+            kv_f = max(kv_f, c[2])
+            out[i] = ServeResult(items, sids, False, version, sched.widths, latency_virtual=c[0])
+        self.counter.add_layer_calls(calls)
+        self.counter.add_kv_build(kv_b, kv_f)
         return out
+
+    def _closed_form(self, cfg, widths, s_ctx):
+        """(layer calls, kv builds, kv floats) of one request's decode
+        (record_counter's closed form), memoised per (config, widths, S)."""
+        key = (cfg, tuple(widths), int(s_ctx), self.config.shared_kv, self.config.value_rerank)
+        memo = self.__dict__.setdefault("_cf_memo", {})
+        hit = memo.get(key)
+        if hit is None:
+            c = LayerCallCounter()
+            record_counter(c, cfg, widths, s_ctx, self.config.shared_kv,
+                           self.config.value_rerank, cfg.trunk_depth)
+            hit = (c.layer_calls, c.kv_builds, c.kv_floats)
+            if len(memo) > 4096:
+                memo.clear()
+            memo[key] = hit
+        return hit
 
     def hit_rate(self):
         total = self.cache.hits + self.cache.misses

@@ -420,7 +420,9 @@ def test_engine_resolves_items_on_device_and_measures_load():
 
     est = Fixed(window=1.0)
     est.capacity = 100.0
-    eng2 = S.ServingEngine(store, index, cfg, load=est)
+    cfg_req = S.ServingConfig(S.BeamSchedule(C2_WIDTHS, 256), q_threshold=1e9,
+                              load_widths="request")
+    eng2 = S.ServingEngine(store, index, cfg_req, load=est)
     quiet = eng2.serve_batch([(f"q{i}", c_features(i, 256), i * 0.5) for i in range(2)],
                              now=0.5)
     burst = eng2.serve_batch([(f"b{i}", c_features(i % 8, 256), 2.0 + i * 1e-4)
@@ -429,3 +431,16 @@ def test_engine_resolves_items_on_device_and_measures_load():
     assert burst[-1].widths == (64, 128, 256)
     assert burst[0].widths[-1] > burst[-1].widths[-1]  # per-request widths, one batch
     assert all(len(r.sids) == r.widths[-1] for r in quiet + burst)
+    # default: one load reading per batch (the reference's per-tick signal),
+    # misses padded to a batch bucket (13 -> 16) with the padding dropped
+    est3 = Fixed(window=1.0)
+    est3.capacity = 100.0
+    eng3 = S.ServingEngine(store, index, cfg, load=est3)
+    tick = eng3.serve_batch([(f"t{i}", c_features(i % 8, 256), 3.0 + i * 1e-4)
+                             for i in range(13)], now=3.01)
+    assert len(tick) == 13 and len({r.widths for r in tick}) == 1
+    assert tick[0].widths[-1] > 256  # 13 req/s against a capacity of 100
+    ocfg, params = _oracle_of(model)
+    want = orc.beam_search(params, ocfg, orc.context_process(c_features(12 % 8, 256), params),
+                           tick[12].widths)
+    _parity(want, tick[12].sids, "bucket-padded engine batch")
