@@ -121,6 +121,13 @@ static PyObject *build(PyObject *self, PyObject *args) {
       }
       PyTuple_SET_ITEM(pair, 0, sid);
       PyTuple_SET_ITEM(pair, 1, f);
+      /* Both hold only ints / a float and are immutable: they can never be
+         part of a reference cycle, so they leave the cyclic GC's lists (as
+         CPython does for such plain tuples).  A serving process keeps
+         millions of them alive in its TTL cache; tracked, every full
+         collection would walk them all (100s of ms pauses). */
+      PyObject_GC_UnTrack(sid);
+      PyObject_GC_UnTrack(pair);
       PyList_SET_ITEM(lst, j, pair);
     }
   }

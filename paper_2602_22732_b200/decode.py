@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import time
 from collections import OrderedDict
 from concurrent.futures import ThreadPoolExecutor
 
@@ -138,6 +139,8 @@ class BeamDecoder:
         self.in_buf = None
         self._in_host = None
         self.uses = 0
+        self._graphs = OrderedDict()  # width plan -> parked CUDA graph (set_widths)
+        self._plan_uses = {}
         self.item_idx = None
         self._resolved = False
         self.last_item_idx = None
@@ -182,6 +185,58 @@ class BeamDecoder:
         self._graph_inputs = None
         self.host_graph = None
         self._host_in = self._dev_in = self.host_out = None
+        self._graphs.clear()
+        self._plan_uses.clear()
+
+    def set_widths(self, widths):
+        """Re-plan for new per-request width schedules (same request count and
+        context lengths) inside this decoder's workspace and result buffers.
+
+        TABS widths follow the load (schedule.py:54-70), so a serving batch
+        shape recurs with many width plans; a re-plan is a host plan plus
+        one table upload (gr4ad_prepare), not a new decoder (workspace,
+        derived-weight binding, graph).  Captured graphs are parked per plan
+        (up to 8): returning to a plan re-uploads its tables and replays its
+        graph.  Returns False, changing nothing, when the plan does not fit
+        the buffers (the caller then needs a decoder of its own)."""
+        w = np.asarray(widths, dtype=np.int32).reshape(self.n_requests, self.T)
+        if np.array_equal(w, self.widths):
+            return True
+        bt = self.batch
+        cw = (C.c_int * max(w.size, 1))(*w.ravel().tolist())
+        old = bt.widths
+        bt.widths = cw
+        nbytes, max_out = C.c_size_t(), C.c_int()
+        N.check(N.lib.gr4ad_workspace_bytes(C.byref(self.dims), C.byref(bt), C.byref(nbytes),
+                                            C.byref(max_out)))
+        if nbytes.value > self.workspace.numel() or max_out.value > self.max_out:
+            bt.widths = old
+            return False
+        okey = self.widths.tobytes()
+        if self.graph is not None:
+            self._graphs[okey] = self.graph
+            self._graphs.move_to_end(okey)
+            while len(self._graphs) > 8:
+                self._graphs.popitem(last=False)
+        if len(self._plan_uses) > 1024:
+            self._plan_uses.clear()
+        self._plan_uses[okey] = self.uses
+        self._w = cw
+        self.widths = w
+        self.workspace_bytes = nbytes.value
+        self.host_graph = None  # captured on the previous plan
+        self._bind_derived()
+        N.check(N.lib.gr4ad_prepare(C.byref(self.dims), C.byref(bt),
+                                    C.c_void_p(self.workspace.data_ptr()),
+                                    self.workspace.numel(), _stream_handle(self.device)))
+        off = C.c_size_t()
+        N.check(N.lib.gr4ad_range_flag_offset(C.byref(self.dims), C.byref(bt), C.byref(off)))
+        self._flag = self.workspace[off.value:off.value + 4].view(torch.int32)
+        nkey = w.tobytes()
+        STATS["replans"] += 1
+        self.graph = self._graphs.pop(nkey, None)
+        self.uses = self._plan_uses.get(nkey, 0)
+        return True
 
     # -- launch ----------------------------------------------------------
     def run(self, features=None, context=None):
@@ -191,7 +246,7 @@ class BeamDecoder:
         N.check(N.lib.gr4ad_beam_search_run(
             C.byref(self.dims), C.byref(self.weights.struct), C.byref(self.batch), f, x,
             C.byref(self.results_struct), C.c_void_p(self.workspace.data_ptr()),
-            self.workspace_bytes, _stream_handle(self.device)))
+            self.workspace.numel(), _stream_handle(self.device)))
 
     def capture(self, features=None, context=None, warmup=1):
         """Capture ``run`` on static input tensors into a CUDA graph."""
@@ -324,6 +379,17 @@ def materialize(count, toks, score, max_out, T, vocab):
                               int(max_out), int(T), vocab, sid_type(vocab))
 
 
+# host-side accounting of the pooled decode path (serving_bench reports it):
+# seconds per phase and event counts; plain adds under the GIL
+STATS = {"stage_s": 0.0, "launch_s": 0.0, "wait_s": 0.0, "marshal_s": 0.0, "calls": 0,
+         "builds": 0, "evictions": 0, "replans": 0, "captures": 0}
+
+
+def reset_stats():
+    for k in STATS:
+        STATS[k] = 0 if isinstance(STATS[k], int) else 0.0
+
+
 class DecoderPool:
     """Idle BeamDecoders (workspace, plan, derived weight copies and a CUDA
     graph each) kept per batch shape, so repeated drop-in calls --
@@ -347,6 +413,7 @@ class DecoderPool:
                 if not lst:
                     del self._idle[key]
                 return dec
+        STATS["builds"] += 1
         return factory()
 
     def release(self, key, dec):
@@ -359,6 +426,7 @@ class DecoderPool:
                 if n <= self.max_decoders and nbytes <= self.max_bytes:
                     break
                 k0 = next(iter(self._idle))
+                STATS["evictions"] += 1
                 self._idle[k0].pop(0)
                 if not self._idle[k0]:
                     del self._idle[k0]
@@ -375,16 +443,24 @@ class DecoderPool:
 POOL = DecoderPool()
 
 
-def decode_cached(key, factory, model, host_input, kind, items=None):
+class PlanMismatch(RuntimeError):
+    """A width plan that does not fit the pooled decoder's buffers."""
+
+
+def decode_cached(key, factory, model, host_input, kind, items=None, widths=None):
     """One decode through a pooled BeamDecoder: host input (a float32 numpy
     array, features or context rows; or a CUDA tensor) -> pinned staging ->
     H2D into the decoder's static input buffer -> decode (graph replay from
     the second use of a shape on) -> [on-device SID -> item resolution when
     ``items`` = (keys, ids, n)] -> async D2H of results + range flag -> host
     lists.  Returns (per-request [(SemanticId, float)], item slots (B,
-    max_out) int32 array or None)."""
+    max_out) int32 array or None).  ``widths`` (B, T) re-plans a decoder
+    pooled under a capacity key (:meth:`BeamDecoder.set_widths`)."""
     with CAPTURE_GATE.shared():
         dec = POOL.acquire(key, factory)
+        if widths is not None and not dec.set_widths(widths):
+            POOL.release(key, dec)
+            raise PlanMismatch("width plan exceeds the pooled decoder's capacity")
     capture = dec.graph is None and dec.uses >= 1
     gate = CAPTURE_GATE.exclusive() if capture else CAPTURE_GATE.shared()
     ok = False
@@ -393,7 +469,7 @@ def decode_cached(key, factory, model, host_input, kind, items=None):
             out = _decode_on(dec, model, host_input, kind, items)
             ok = True
             return out
-        except InputRangeError:
+        except (InputRangeError, ValueError):
             ok = True  # the decoder itself is fine
             raise
         finally:
@@ -440,6 +516,7 @@ def _stage_blocks(blocks, staged):
 
 
 def _decode_on(dec, model, host_input, kind, items):
+    t0 = time.perf_counter()
     if True:
         if dec.weights is not device_weights(model, dec.device):
             dec.rebind(model)  # a republished snapshot of the same shape
@@ -451,6 +528,7 @@ def _decode_on(dec, model, host_input, kind, items):
             dec.in_buf = torch.empty(shape, dtype=torch.float32, device=dec.device)
             dec._in_host = None
             dec.graph = None
+            dec._graphs.clear()  # parked graphs hold the old input pointer
         if isinstance(host_input, torch.Tensor):  # already on the device
             dec.in_buf.copy_(host_input)
         else:
@@ -465,9 +543,13 @@ def _decode_on(dec, model, host_input, kind, items):
                     np.copyto(staged, host_input, casting="unsafe")
                 ok = bool(np.isfinite(staged).all())
             if not ok:
+                blocks = host_input if isinstance(host_input, (list, tuple)) else [host_input]
+                if not all(np.isfinite(np.asarray(a)).all() for a in blocks):
+                    raise ValueError("context must be finite")
                 raise InputRangeError("an input exceeds the fp32 range of the GPU decode")
             dec.in_buf.copy_(dec._in_host, non_blocking=True)
         inputs = {kind: dec.in_buf}
+        t1 = time.perf_counter()
         if dec.graph is not None:
             dec.graph.replay()
         elif dec.uses >= 1:
@@ -479,14 +561,24 @@ def _decode_on(dec, model, host_input, kind, items):
                 dec.run(**inputs)
             torch.cuda.current_stream(dec.device).wait_stream(s)
             dec.graph = g
+            STATS["captures"] += 1
             g.replay()
         else:
             dec.run(**inputs)
         dec.uses += 1
         if items is not None:
             dec.resolve_items(*items)
-        dec.fetch_async()
+        ev = dec.fetch_async()
+        t2 = time.perf_counter()
+        ev.synchronize()
+        t3 = time.perf_counter()
         out = dec.results()
+        t4 = time.perf_counter()
+        STATS["calls"] += 1
+        STATS["stage_s"] += t1 - t0
+        STATS["launch_s"] += t2 - t1
+        STATS["wait_s"] += t3 - t2
+        STATS["marshal_s"] += t4 - t3
         return out, dec.last_item_idx
 
 

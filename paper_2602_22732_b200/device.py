@@ -94,8 +94,14 @@ def _stream_handle(device=None):
     return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+_HAS_CUDA = []
+
+
 def require_cuda(device=None):
-    if not torch.cuda.is_available():
+    # torch.cuda.is_available() re-queries the driver (~0.2 ms a call): once
+    if not _HAS_CUDA:
+        _HAS_CUDA.append(torch.cuda.is_available())
+    if not _HAS_CUDA[0]:
         raise RuntimeError("paper_2602_22732_b200 needs a CUDA device (B200, sm_100a); "
                            "there is no CPU fallback")
     return torch.device(device if device is not None else "cuda")

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from .. import _native as N
-from ..decode import BeamDecoder, decode_cached, effective_widths, live_rows
+from ..decode import BeamDecoder, PlanMismatch, decode_cached, effective_widths, live_rows
 from ..device import (DeviceContext, _stream_handle, device_weights, dims_of, gated,
                       require_cuda)
 from ..model.decoder import param_array
@@ -124,7 +124,7 @@ def _valid_key(valid_sids):
 
 
 def _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path, inp, kind,
-            items=None):
+            items=None, cap=None):
     """Pooled decode with the automatic fp16-range fallback: with
     path="auto", a batch whose weights or context K/V leave the fp16 split
     range of the tensor-core paths is decoded again on the fp32 CUDA-core
@@ -136,6 +136,17 @@ def _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path, inp
     vkey = _valid_key(valid_sids)
 
     def attempt(p):
+        if cap is not None:
+            # one decoder per capacity plan, re-planned for the call's widths
+            key = (id(model.params), model.config, str(dev), kind, tuple(lens), "cap",
+                   tuple(cap), k_depth, bool(value_rerank), reps_key, vkey, p)
+            factory = lambda: BeamDecoder(model, lens, cap, trunk_depth=k_depth,
+                                          value_rerank=value_rerank, representatives=reps,
+                                          valid_sids=valid_sids, device=dev, path=p)
+            try:
+                return decode_cached(key, factory, model, inp, kind, items, widths=per)
+            except PlanMismatch:
+                pass
         key = (id(model.params), model.config, str(dev), kind, tuple(lens), tuple(per), k_depth,
                bool(value_rerank), reps_key, vkey, p)
         factory = lambda: BeamDecoder(model, lens, per, trunk_depth=k_depth,
@@ -177,7 +188,8 @@ def beam_search(model, context, schedule, shared_kv=True, precut=True, counter=N
 
 def beam_search_batch(model, contexts=None, schedules=None, features=None, shared_kv=True,
                       precut=True, counter=None, value_rerank=False, buckets=None,
-                      trunk_depth=None, valid_sids=None, path="auto", _items=None):
+                      trunk_depth=None, valid_sids=None, path="auto", _items=None,
+                      _capacity=None):
     """Batched ``beam_search``: one result list per request.
 
     ``path`` picks the decode kernels: "auto" (the fused per-request kernel
@@ -230,8 +242,8 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
                 raise ValueError("empty context")
             if a.shape[-1] != cfg.feat_dim:
                 raise ValueError(f"feature dim {a.shape[-1]} != expected {cfg.feat_dim}")
-            if not np.isfinite(a).all():
-                raise ValueError("context must be finite")
+        # finiteness: checked once, on the staged fp32 copy (decode._decode_on
+        # raises the reference's ValueError for a non-finite input)
         lens = [a.shape[0] for a in arrs]
         inp = arrs  # concatenated + cast into the decoder's pinned staging buffer
         kind = "features"
@@ -240,8 +252,13 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
         if buckets is None:
             raise ValueError("value_rerank requires buckets")
         reps = getattr(buckets, "representatives", buckets)
+    cap = None
+    if _capacity is not None:  # engine: widths bounded by this schedule (TABS maximum)
+        c = tuple(int(w) for w in getattr(_capacity, "widths", _capacity))
+        if len(c) == cfg.n_levels and all(all(a <= b for a, b in zip(w, c)) for w in per):
+            cap = [c] * B
     out, item_idx = _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path,
-                            inp, kind, _items)
+                            inp, kind, _items, cap)
     if counter is not None:
         for b in range(B):
             record_counter(counter, cfg, per[b], lens[b], shared_kv, value_rerank, k_depth)

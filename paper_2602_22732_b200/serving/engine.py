@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import threading
 import time
+import weakref
 from concurrent.futures import Future
 from dataclasses import dataclass
 
@@ -187,7 +188,10 @@ class LoadEstimator:
                 (1 - self.alpha) * self.capacity + self.alpha * c)
 
     def signal(self, now):
-        """(qps, capacity_slack) at request time ``now``."""
+        """(qps, capacity_slack) at request time ``now`` -- an arrival time:
+        the engine sees arrivals only when they are served, so under a
+        backlog the rate at the serving wall time would count none of them
+        (and read as idle)."""
         qps = self.rate(now)
         cap = self.capacity
         slack = 1.0 if not cap else min(1.0, max(0.0, 1.0 - qps / cap))
@@ -201,26 +205,32 @@ class ItemTable:
     ``items``.  Built once per index version."""
 
     def __init__(self, index, vocab, device):
-        keys, items = [], []
-        for sid in index.all_sids():
+        sids, items = [], []
+        with index._write_lock:  # a consistent snapshot of the forward map
+            fwd = list(index._forward.items())
+        T = len(vocab)
+        for sid, ids in fwd:
             toks = getattr(sid, "tokens", sid)
-            if len(toks) != len(vocab) or any(not 0 <= t < v for t, v in zip(toks, vocab)):
-                continue  # a SID of another vocabulary can never be decoded
-            ids = index.lookup(sid)
-            if not ids:
+            if len(toks) != T or not ids:
                 continue
-            k = 0
-            for t, v in zip(toks, vocab):
-                k = k * int(v) + int(t)
-            keys.append(k)
+            sids.append(toks)
             items.append(min(ids))
-        order = np.argsort(np.asarray(keys, dtype=np.int64), kind="stable")
-        self.n = len(keys)
-        k_sorted = np.asarray(keys, dtype=np.int64)[order] if keys else np.zeros(1, np.int64)
+        tok = np.asarray(sids, dtype=np.int64).reshape(-1, T)
+        voc = np.asarray(vocab, dtype=np.int64)
+        # a SID of another vocabulary can never be decoded
+        ok = ((tok >= 0) & (tok < voc)).all(1) if tok.size else np.zeros(0, bool)
+        tok = tok[ok]
+        keys = np.zeros(tok.shape[0], dtype=np.int64)
+        for t in range(T):
+            keys = keys * voc[t] + tok[:, t]
+        order = np.argsort(keys, kind="stable")
+        self.n = int(keys.size)
+        k_sorted = keys[order] if self.n else np.zeros(1, np.int64)
+        kept = np.flatnonzero(ok)
         self.items = np.empty(max(self.n, 1), dtype=object)
-        for j, o in enumerate(order.tolist()):
-            self.items[j] = items[o]
-        self.keys = torch.from_numpy(k_sorted).to(device)
+        if self.n:
+            self.items[:self.n] = [items[i] for i in kept[order].tolist()]
+        self.keys = torch.from_numpy(np.ascontiguousarray(k_sorted)).to(device)
         self.ids = torch.arange(max(self.n, 1), dtype=torch.int32, device=device)
 
     def args(self):
@@ -237,6 +247,9 @@ class ItemTable:
         return [(o, float(sids[j][1])) for o, j in zip(objs, keep.tolist())]
 
 
+_TABLES = weakref.WeakKeyDictionary()  # SidIndex -> (version, vocab, device, ItemTable)
+
+
 class ServingEngine:
     def __init__(self, store, index, config, buckets=None, counter=None, load=None):
         self.store = store
@@ -250,6 +263,9 @@ class ServingEngine:
         self.requests = 0
         self.load = load if load is not None else LoadEstimator()
         self._table = None  # (index version, vocab, ItemTable)
+        model = store.current()[1] if torch.cuda.is_available() else None
+        if model is not None:  # off the first request's latency
+            self._item_table(model)
 
     def _widths(self, qps, capacity_slack):
         sig = TrafficSignal(qps, self.config.q_threshold, capacity_slack)
@@ -257,13 +273,21 @@ class ServingEngine:
         return scale_schedule(self.config.schedule, active)
 
     def _item_table(self, model):
+        """The device SID -> item table of the current index version, shared
+        by every engine serving the same index (built once per version)."""
         vocab = tuple(model.config.level_vocab_sizes)
         version = self.index.version
         tab = self._table
         if tab is None or tab[0] != version or tab[1] != vocab:
             from ..device import CAPTURE_GATE, require_cuda
-            with CAPTURE_GATE.shared():
-                tab = (version, vocab, ItemTable(self.index, vocab, require_cuda()))
+            dev = require_cuda()
+            shared = _TABLES.get(self.index)
+            if shared is not None and shared[:3] == (version, vocab, str(dev)):
+                tab = (version, vocab, shared[3])
+            else:
+                with CAPTURE_GATE.shared():
+                    tab = (version, vocab, ItemTable(self.index, vocab, dev))
+                _TABLES[self.index] = (version, vocab, str(dev), tab[2])
             self._table = tab
         return tab[2]
 
@@ -313,7 +337,11 @@ class ServingEngine:
         if qps is not None:
             scheds = [self._widths(qps, capacity_slack)] * len(misses)
         elif self.config.load_widths == "batch":
-            scheds = [self._widths(*self.load.signal(now))] * len(misses)
+            # one reading per batch, at its latest arrival (a queued batch's
+            # arrivals all lie in the past: reading at `now` would see none)
+            t_last = max((requests[i][2] for i in misses if len(requests[i]) > 2),
+                         default=now)
+            scheds = [self._widths(*self.load.signal(t_last))] * len(misses)
         else:
             scheds = []
             for i in misses:
@@ -335,7 +363,8 @@ class ServingEngine:
         results, slots = beam_search_batch(
             model, features=dfeats, schedules=dscheds, shared_kv=self.config.shared_kv,
             precut=self.config.precut, value_rerank=self.config.value_rerank,
-            buckets=self.buckets, valid_sids=valid, _items=table.args())
+            buckets=self.buckets, valid_sids=valid, _items=table.args(),
+            _capacity=self._capacity_widths())
         self.load.record_service(n, time.perf_counter() - t0)
         with self._lock:
             self.model_invocations += len(misses)
@@ -354,6 +383,35 @@ class ServingEngine:
         self.counter.add_layer_calls(calls)
         self.counter.add_kv_build(kv_b, kv_f)
         return out
+
+    def warmup(self, features, max_batch=None, widths=None):
+        """Build and graph-capture the pooled decoders of every batch bucket
+        up to ``max_batch`` for one request shape (``features``: an example
+        (S, F) matrix), at the base and the widest TABS schedule, so the
+        first requests of a bucket do not pay for workspace allocation and
+        capture (CUDA-graph warmup at server start).  Nothing is cached."""
+        version, model = self.store.current()
+        f = np.atleast_2d(np.asarray(features, dtype=np.float64))
+        buckets = [b for b in (self.config.batch_buckets or ())
+                   if max_batch is None or b <= max_batch]
+        cap = self._capacity_widths()
+        plans = widths if widths is not None else [self.config.schedule.widths, cap]
+        for b in buckets:
+            for w in plans:
+                for _ in range(2):  # the second use captures the plan's graph
+                    beam_search_batch(model, features=[f] * b, schedules=[tuple(w)] * b,
+                                      shared_kv=self.config.shared_kv,
+                                      value_rerank=self.config.value_rerank,
+                                      buckets=self.buckets, _capacity=cap)
+
+    def _capacity_widths(self):
+        """The widest schedule TABS can produce (slack 1, or the base when
+        boost <= 0): pooled decoders are planned for it and re-planned per
+        batch for the load's widths (BeamDecoder.set_widths)."""
+        base = self.config.schedule
+        wide = scale_schedule(base, tabs_adjust(TrafficSignal(0.0, 1.0, 1.0),
+                                                base.base_width, self.config.boost))
+        return tuple(max(a, b) for a, b in zip(base.widths, wide.widths))
 
     def _closed_form(self, cfg, widths, s_ctx):
         """(layer calls, kv builds, kv floats) of one request's decode

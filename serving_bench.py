@@ -22,6 +22,7 @@ arrival -> ServeResult on the host.  Prints one JSON line per offered load.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import sys
@@ -50,7 +51,23 @@ def main():
     ap.add_argument("--boost", type=float, default=0.6)
     ap.add_argument("--items", type=int, default=100000)
     ap.add_argument("--p99-bound-ms", type=float, default=None)
+    ap.add_argument("--profile", action="store_true",
+                    help="cProfile the sweep; top functions to stderr")
     args = ap.parse_args()
+    if args.profile:
+        import cProfile
+        import pstats
+        prof = cProfile.Profile()
+        prof.enable()
+        try:
+            return _run(args)
+        finally:
+            prof.disable()
+            pstats.Stats(prof, stream=sys.stderr).sort_stats("cumulative").print_stats(45)
+    return _run(args)
+
+
+def _run(args):
 
     import torch
 
@@ -58,6 +75,7 @@ def main():
     from paper_2602_22732_b200.quantizer import SemanticId, SidIndex
     from paper_2602_22732_b200.serving import (BeamSchedule, ServingConfig, ServingEngine,
                                                SnapshotStore)
+    from paper_2602_22732_b200 import decode as DEC
     from paper_2602_22732_b200.serving.engine import LoadEstimator
 
     assert torch.cuda.is_available(), "serving_bench needs a CUDA device"
@@ -87,8 +105,26 @@ def main():
         return ServingEngine(store, index, cfg, load=LoadEstimator(window=1.0))
 
     # capacity at base widths: full batches through the same API (explicit
-    # qps above the threshold -> base widths), warm pools first
+    # qps above the threshold -> base widths), warm pools first (every batch
+    # bucket's decoder built and graph-captured, as a server does at start)
     eng = engine(1e12)
+    # server start-up state (model, 100k-item index, warm pools) moves to the
+    # GC's permanent generation, as a long-running server does after loading
+    gc.collect()
+    gc.freeze()
+    t_w = time.perf_counter()
+    eng.warmup(feats[0], args.max_batch)
+    warm_s = time.perf_counter() - t_w
+    gc_t = {"s": 0.0, "n2": 0, "t0": 0.0}
+
+    def on_gc(phase, info):
+        if phase == "start":
+            gc_t["t0"] = time.perf_counter()
+        else:
+            gc_t["s"] += time.perf_counter() - gc_t["t0"]
+            gc_t["n2"] += info.get("generation") == 2
+
+    gc.callbacks.append(on_gc)
     for _ in range(3):
         eng.serve_batch(requests(args.max_batch, np.zeros(args.max_batch)), 0.0, qps=1e13)
     reps = 5
@@ -98,13 +134,17 @@ def main():
     cap = reps * args.max_batch / (time.perf_counter() - t0)
     print(json.dumps({"model": args.model, "capacity_req_s": cap, "base_widths": list(base),
                       "max_batch": args.max_batch, "api": "ServingEngine.serve_batch",
-                      "items_indexed": args.items}), flush=True)
+                      "items_indexed": args.items, "warmup_s": warm_s}), flush=True)
 
     for rho in [float(x) for x in args.loads.split(",")]:
         lam = rho * cap
         n = max(1, int(lam * args.duration))
         arrivals = np.cumsum(rng.exponential(1.0 / lam, size=n))
         eng = engine(cap)
+        DEC.reset_stats()
+        gc_t["s"], gc_t["n2"] = 0.0, 0
+        call_ms = []
+        slow = []
         eng.load.capacity = cap  # seeded with the calibration; the engine's EWMA refines it
         lat = np.zeros(n)
         widths_seen = []
@@ -118,8 +158,11 @@ def main():
             hi = done
             while hi < n and hi - done < args.max_batch and arrivals[hi] <= now:
                 hi += 1
+            c0 = DEC.STATS["captures"]
             res = eng.serve_batch(requests(hi - done, arrivals[done:hi]), now)
             t_done = time.perf_counter() - start
+            call_ms.append(1e3 * (t_done - now))
+            slow.append((call_ms[-1], batches, hi - done, DEC.STATS["captures"] - c0))
             lat[done:hi] = t_done - arrivals[done:hi]
             widths_seen.extend(r.widths[-1] for r in res)
             n_items += sum(len(r.items) for r in res)
@@ -136,6 +179,15 @@ def main():
                 "latency_ms": {"p50": 1e3 * float(np.percentile(lat, 50)),
                                "p99": 1e3 * float(np.percentile(lat, 99))},
                 "items_resolved": n_items}
+        line["host"] = {k: (round(v, 4) if isinstance(v, float) else v)
+                        for k, v in DEC.STATS.items()}
+        line["host"]["gc_s"] = round(gc_t["s"], 4)
+        line["host"]["gc_gen2"] = gc_t["n2"]
+        cm = np.asarray(call_ms)
+        line["call_ms"] = {"p50": float(np.percentile(cm, 50)),
+                           "p99": float(np.percentile(cm, 99)), "max": float(cm.max()),
+                           "slowest": [[round(a, 2), b, c, d] for a, b, c, d in
+                                       sorted(slow, reverse=True)[:4]]}
         if args.p99_bound_ms is not None:
             line["p99_within_bound"] = line["latency_ms"]["p99"] <= args.p99_bound_ms
         print(json.dumps(line), flush=True)

@@ -3,6 +3,7 @@ checkpoint format against the reference's, SemanticId's contract, the bulk
 result materialisation of the drop-in API, argument validation that must
 fire before any device work, and the engine's online load estimator."""
 
+import gc
 import hashlib
 import os
 import pickle
@@ -113,6 +114,9 @@ def test_bulk_materialisation_matches_per_item_and_is_fast():
                 for j in range(int(count[b]))]
         assert out[b] == want
         assert all(type(s) is type(out[b][0][0]) for s, _ in out[b])
+        # immutable, int/float-only: off the cyclic GC's lists (no full-
+        # collection pauses over a serving cache of millions of results)
+        assert not any(gc.is_tracked(p) or gc.is_tracked(p[0]) for p in out[b])
     n = int(count.sum())
     print(f"materialize: {n} results in {best * 1e3:.1f} ms")
     assert best < 1.0  # generous on a loaded CI host; the bench line reports the figure

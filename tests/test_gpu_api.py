@@ -444,3 +444,86 @@ def test_engine_resolves_items_on_device_and_measures_load():
     want = orc.beam_search(params, ocfg, orc.context_process(c_features(12 % 8, 256), params),
                            tick[12].widths)
     _parity(want, tick[12].sids, "bucket-padded engine batch")
+
+
+@pytest.mark.parametrize("d,path", [(128, "tensor"), (16, "fused")])
+def test_set_widths_replans_inside_one_decoder(d, path):
+    """A decoder planned for the widest TABS schedule re-plans in place for
+    narrower widths (BeamDecoder.set_widths: one table upload, no new
+    buffers); graphs are parked per plan and replayed when a plan returns.
+    Every plan decodes like a decoder built for it, and like the oracle."""
+    M, S = _need()
+    from paper_2602_22732_b200.decode import BeamDecoder
+    model = M.DecoderModel(M.DecoderConfig(16, d, 2 * d, 3, 1, (256, 256, 256), 4, seed=9))
+    lens = [256] * 4
+    cap = [(20, 40, 80)] * 4
+    plans = [[(12, 24, 48)] * 4, [(16, 32, 64), (20, 40, 80), (8, 16, 32), (13, 26, 51)],
+             cap, [(12, 24, 48)] * 4]
+    feats = [c_features(200 + i, 256) for i in range(4)]
+    x = torch.from_numpy(np.concatenate(feats).astype(np.float32)).cuda()
+    dec = BeamDecoder(model, lens, cap, path=path)
+    ws = dec.workspace.data_ptr()
+    ocfg, params = _oracle_of(model)
+    for k, widths in enumerate(plans):
+        assert dec.set_widths(widths)
+        assert dec.workspace.data_ptr() == ws
+        if dec.graph is None:
+            dec.capture(features=x)
+        else:
+            assert k == 3  # the first plan's graph, parked and replayed
+        dec.replay()
+        got = dec.host_results()
+        fresh = BeamDecoder(model, lens, widths, path=path)
+        fresh.run(features=x)
+        assert got == fresh.host_results(), f"plan {k}"
+        for i in (0, 3):
+            want = orc.beam_search(params, ocfg, orc.context_process(feats[i], params),
+                                   widths[i])
+            _parity(want, got[i], f"set_widths {path} plan {k} request {i}")
+    assert not dec.set_widths([(40, 80, 160)] * 4)  # larger than the buffers
+
+
+def test_engine_pools_one_decoder_per_batch_bucket():
+    """ServingEngine: TABS widths change with load, but decoders are pooled
+    per batch bucket at the widest schedule and re-planned, so a sweep of
+    loads builds one decoder per bucket; results stay the oracle's."""
+    M, S = _need()
+    from paper_2602_22732_b200.decode import POOL
+    from paper_2602_22732_b200.quantizer import SidIndex
+    model = _model(M, C1_MODEL)
+    POOL.clear()
+    cfg = S.ServingConfig(S.BeamSchedule(C2_WIDTHS, 256), q_threshold=100.0)
+    eng = S.ServingEngine(S.SnapshotStore(model), SidIndex(), cfg)
+    ocfg, params = _oracle_of(model)
+    seen = set()
+    for step, qps in enumerate([0.0, 30.0, 60.0, 90.0, 200.0, 30.0]):
+        reqs = [(f"s{step}u{i}", c_features(step * 8 + i, 256)) for i in range(5)]
+        res = eng.serve_batch(reqs, now=float(step), qps=qps, capacity_slack=1 - qps / 100.0
+                              if qps < 100 else 0.0)
+        seen.add(res[0].widths)
+        want = orc.beam_search(params, ocfg, orc.context_process(reqs[4][1], params),
+                               res[4].widths)
+        _parity(want, res[4].sids, f"engine qps {qps}")
+    assert len(seen) >= 4
+    assert len(POOL) == 1  # 5 misses -> bucket 8, one capacity decoder
+
+
+def test_non_finite_and_out_of_range_features_raise():
+    """beam_search_batch: a NaN / inf feature raises the reference's
+    ValueError (checked on the staged fp32 copy); a finite value beyond the
+    fp32 range raises InputRangeError; the pooled decoder stays usable."""
+    M, S = _need()
+    from paper_2602_22732_b200.decode import InputRangeError
+    model = _model(M, C1_MODEL)
+    sched = S.BeamSchedule(C2_WIDTHS, 256)
+    good = [c_features(i, 256) for i in range(3)]
+    ref = S.beam_search_batch(model, features=good, schedules=sched)
+    bad = [a.copy() for a in good]
+    bad[1][5, 2] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        S.beam_search_batch(model, features=bad, schedules=sched)
+    big = [a.copy() for a in good]
+    big[2][0, 0] = 1e300
+    with pytest.raises(InputRangeError):
+        S.beam_search_batch(model, features=big, schedules=sched)
+    assert S.beam_search_batch(model, features=good, schedules=sched) == ref
