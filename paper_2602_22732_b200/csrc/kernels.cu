@@ -720,6 +720,24 @@ __device__ void sel_pass_hist(const SelCtx &c, uint32_t *keys, unsigned *hist, i
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int cur = -1;
   unsigned cnt = 0;
+  if (CACHE) {  // keys prefilled in shared memory: flat over all threads
+    const int n = c.n_rows * c.V;
+    for (int fi = threadIdx.x; fi < n; fi += kSelThreads) {
+      const uint32_t u = keys[fi];
+      if ((u & pmask) == prefix) {
+        int bin = (int)((u >> shift) & bmask);
+        if (bin == cur) {
+          ++cnt;
+        } else {
+          if (cnt) atomicAdd(&hist[cur], cnt);
+          cur = bin;
+          cnt = 1;
+        }
+      }
+    }
+    if (cnt) atomicAdd(&hist[cur], cnt);
+    return;
+  }
   for (int r = wid; r < c.n_rows; r += kSelWarps) {
     float cr = 0.f;
     float2 ri = make_float2(0.f, 0.f);
@@ -850,6 +868,19 @@ __global__ void __launch_bounds__(kSelThreads, 2) topk_select_kernel(SelectArgs 
     for (int w = 0; w < kSelWarps; ++w) Rs = fmaxf(Rs, s_red[w]);
     const float scale = 2048.0f / (logf((float)max(c.V, 2)) + 4.0f);
     auto sbin = [&](float s) -> unsigned { return (unsigned)fminf((Rs - s) * scale, 2047.0f); };
+    if (CACHE) {
+      // every candidate key once into shared memory, spread over all threads
+      // (a level with few rows -- level 0 has one -- would otherwise run on
+      // one warp): coalesced loads, later passes read only shared memory
+      const int n = (int)n_cand;
+      for (int fi = tid; fi < n; fi += kSelThreads) {
+        const int r = fi / c.V;
+        const float cr = c.cum[c.hist0 + c.row0 + r];
+        const float2 ri = c.rowinfo ? c.rowinfo[c.row0 + r] : make_float2(0.f, 0.f);
+        keys[fi] = sel_key(c, r, fi - r * c.V, cr, ri);
+      }
+      __syncthreads();
+    }
     // 16-B rows: float4 loads, four candidates per lane and load
     const bool vec4 = !CACHE && c.V % 4 == 0 && c.ld % 4 == 0;
     // attempt 0: window bin from the logits GEMM epilogue's per-64-column maxima
@@ -887,6 +918,18 @@ __global__ void __launch_bounds__(kSelThreads, 2) topk_select_kernel(SelectArgs 
         }
         nprox = warp_sum_u(nprox);
         if (lane == 0 && nprox) atomicAdd(&s_nfin, nprox);
+      } else if (CACHE) {
+        const int n = (int)n_cand;
+        for (int fi = tid; fi < n; fi += kSelThreads) {
+          const int bin = (int)sbin(ord2f(keys[fi]));
+          if (bin == cur) {
+            ++cnt;
+          } else {
+            if (cnt) atomicAdd(&hist[cur], cnt);
+            cur = bin;
+            cnt = 1;
+          }
+        }
       } else {
         for (int r = wid; r < c.n_rows; r += kSelWarps) {
           const float cr = c.cum[c.hist0 + c.row0 + r];
@@ -950,7 +993,24 @@ __global__ void __launch_bounds__(kSelThreads, 2) topk_select_kernel(SelectArgs 
       if (tid == 0) s_gt_pos = 0;
       __syncthreads();
       if (wb == 2047 || (attempt == 1 && cnt_le > (unsigned)GR4AD_MAX_BEAM)) continue;
-      for (int r = wid; r < c.n_rows; r += kSelWarps) {
+      if (CACHE) {
+        const int n = (int)n_cand;
+        for (int f0 = wid * 32; f0 < n; f0 += kSelThreads) {
+          const int fi = f0 + lane;
+          const uint32_t u = fi < n ? keys[fi] : 0u;
+          const bool take = fi < n && sbin(ord2f(u)) <= (unsigned)wb;
+          const unsigned m = __ballot_sync(0xffffffffu, take);
+          if (m) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(&s_gt_pos, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
+            if (take && pos < (unsigned)GR4AD_MAX_BEAM)
+              sbuf[pos] = ((unsigned long long)u << 32) | (0xFFFFFFFFu - (unsigned)fi);
+          }
+        }
+      }
+      for (int r = wid; r < c.n_rows && !CACHE; r += kSelWarps) {
         const float cr = c.cum[c.hist0 + c.row0 + r];
         const float2 ri = c.rowinfo ? c.rowinfo[c.row0 + r] : make_float2(0.f, 0.f);
         if (vec4 && a.proxies) {
