@@ -618,6 +618,7 @@ __global__ void tile_rows_kernel(const float *src, int n_src, int d, float *dst,
 
 // one pre-LN decoder layer over a row set (layers.py:66-119)
 struct RowSet {
+  bool few_rows = false;  // few rows per request (trunk, level 0): small GEMM tiles
   int rows;           // rows in the set
   int max_group_rows; // max rows of one group
   int groups = 0;     // attention groups (0: one per request)
@@ -793,9 +794,10 @@ static int dense(const Plan &p, const GemmArgs &g, const __half *WT, long long a
 // producing LayerNorm / epilogue / self-attention): no on-chip conversion
 static int dense_split(const Plan &p, const GemmArgs &g, const __half *WT, const __half *a_hi,
                        const __half *a_lo, long long a_rows, int epi, cudaStream_t st,
-                       __half *c_hi = nullptr, __half *c_lo = nullptr) {
+                       __half *c_hi = nullptr, __half *c_lo = nullptr, bool few_rows = false) {
   TcArgs t{};
   static_cast<GemmArgs &>(t) = g;
+  t.few_rows = few_rows ? 1 : 0;
   t.b_hi = WT;
   t.b_lo = WT + p.wt_floats;
   t.ldb = g.K;
@@ -910,6 +912,7 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
   const int d = p.d, R = rs.rows;
   const gr4ad_layer &Lw = w->layer[i];
   const LayerT &LT = wt.layer[i];
+  const bool few = rs.few_rows;  // few-row set: small GEMM tiles
   float *N = at<float>(ws, p.o_N), *Q = at<float>(ws, p.o_Q), *A = at<float>(ws, p.o_A);
   float *SC = at<float>(ws, p.o_SC), *Fb = at<float>(ws, p.o_Fb);
   const int *ctx_off = rs.g_ctx_off ? rs.g_ctx_off : at<int>(ws, p.o_ctx_off);
@@ -979,7 +982,7 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
   const bool spl_att = spl && !swap;
   const GemmArgs gq = plain_gemm(N, d, LT.mqk, d, Q, d, R, d, d);  // q' = n (W_q W_k^T)
   if (spl)
-    GR_TRY(dense_split(p, gq, LT.qk, Nh, Nl, R, spl_att ? EPI_STORE_SPLIT : EPI_STORE, st, Qh, Ql));
+    GR_TRY(dense_split(p, gq, LT.qk, Nh, Nl, R, spl_att ? EPI_STORE_SPLIT : EPI_STORE, st, Qh, Ql, few));
   else
     GR_TRY(dense(p, gq, LT.qk, R, EPI_STORE, st));
   GemmArgs qk{};
@@ -1058,7 +1061,7 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
   GemmArgs o = plain_gemm(A, d, LT.mvo, d, Hs, d, R, d, d);  // h += u (W_v W_o)
   o.R = Hs; o.ldr = d;
   if (spl)
-    GR_TRY(dense_split(p, o, LT.vo, Ah, Al, R, EPI_RESID, st));
+    GR_TRY(dense_split(p, o, LT.vo, Ah, Al, R, EPI_RESID, st, nullptr, nullptr, few));
   else
     GR_TRY(dense(p, o, LT.vo, R, EPI_RESID, st));
 
@@ -1073,7 +1076,7 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
                     : plain_gemm(hn, p.hist_ld, LT.msqk, d, hq, p.hist_ld, R, d, d);
   if (spl) {
     sq.lda = ld_n2;  // (in halves: the A operand arrives pre-split)
-    GR_TRY(dense_split(p, sq, LT.sqk, n2h, n2l, R, EPI_STORE, st));
+    GR_TRY(dense_split(p, sq, LT.sqk, n2h, n2l, R, EPI_STORE, st, nullptr, nullptr, few));
   } else {
     GR_TRY(dense(p, sq, LT.sqk, R, EPI_STORE, st));
   }
@@ -1082,7 +1085,7 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
   GemmArgs so = plain_gemm(A, d, LT.msvo, d, Hs, d, R, d, d);  // h += (P n) (W_v W_o)
   so.R = Hs; so.ldr = d;
   if (spl)
-    GR_TRY(dense_split(p, so, LT.svo, Ah, Al, R, EPI_RESID, st));
+    GR_TRY(dense_split(p, so, LT.svo, Ah, Al, R, EPI_RESID, st, nullptr, nullptr, few));
   else
     GR_TRY(dense(p, so, LT.svo, R, EPI_RESID, st));
 
@@ -1094,7 +1097,7 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
   GemmArgs f1 = plain_gemm(N, d, Lw.ffn_W1, p.dff, Fb, p.dff, R, p.dff, d);
   f1.bias = Lw.ffn_b1;
   if (spl)
-    GR_TRY(dense_split(p, f1, LT.w1, Nh, Nl, R, EPI_BIAS_GELU_SPLIT, st, Fh, Fl));
+    GR_TRY(dense_split(p, f1, LT.w1, Nh, Nl, R, EPI_BIAS_GELU_SPLIT, st, Fh, Fl, few));
   else
     GR_TRY(dense(p, f1, LT.w1, R, EPI_BIAS_GELU, st));
   GemmArgs f2 = plain_gemm(Fb, p.dff, Lw.ffn_W2, d, Hs, d, R, d, p.dff);
@@ -1102,7 +1105,7 @@ static int layer_forward_tc(const Plan &p, const gr4ad_weights *w, const Weights
   const bool dual = spl && split_out;
   if (spl)
     GR_TRY(dense_split(p, f2, LT.w2, Fh, Fl, R, dual ? EPI_BIAS_RESID_DUAL : EPI_BIAS_RESID, st,
-                       dual ? Nh : nullptr, dual ? Nl : nullptr));
+                       dual ? Nh : nullptr, dual ? Nl : nullptr, few));
   else
     GR_TRY(dense(p, f2, LT.w2, R, EPI_BIAS_RESID, st));
   if (split_out) *split_out = dual;
@@ -1188,6 +1191,7 @@ static int encode_and_trunk(const Plan &p, const gr4ad_weights *w, const float *
     long long rows = (long long)B * p.n_pos;
     GR_LAUNCH(KC_SMALL, st, tile_rows_kernel<<<ceil_div(rows * d, 256), 256, 0, st>>>(w->pos, p.n_pos, d, Ht, rows));
     RowSet rs{};
+    rs.few_rows = true;
     rs.rows = (int)rows;
     rs.max_group_rows = p.n_pos;
     rs.g_row_off = at<int>(ws, p.o_trow_off);
@@ -1254,7 +1258,7 @@ static int layered_level(const Plan &p, const gr4ad_weights *w, const gr4ad_batc
     GemmArgs gf = plain_gemm(nullptr, d, w->fuse_Wf, d, Hs, d, R, d, d);
     gf.R = Hs;
     gf.ldr = d;
-    GR_TRY(dense_split(p, gf, wt->wf_top, Uh, Ul, R, EPI_RESID, st));
+    GR_TRY(dense_split(p, gf, wt->wf_top, Uh, Ul, R, EPI_RESID, st, nullptr, nullptr, t == 0));
   } else if (K > 0) {
     GR_TRY(level_input(t, R, d, w->bos, emb_prev, tok + h0, nullptr, U, nullptr, st));
     GemmArgs gg = plain_gemm(U + d, 2LL * d, w->fuse_Wg, d, U, 2LL * d, R, d, d);
@@ -1270,6 +1274,7 @@ static int layered_level(const Plan &p, const gr4ad_weights *w, const gr4ad_batc
   }
   // head layers K..L-1 against the shared context KV (beam.py:243-255)
   RowSet rs{};
+  rs.few_rows = t == 0;  // one row per request
   rs.rows = R;
   rs.max_group_rows = p.maxcap[t];
   rs.g_row_off = row_off + (size_t)t * B;
@@ -1309,6 +1314,7 @@ static int layered_level(const Plan &p, const gr4ad_weights *w, const gr4ad_batc
     tl.alpha = lg.alpha / kWeightScale;
     tl.lse_part = at<float4>(ws, p.o_lsep);
     tl.lse_ld = (V + 127) / 128;
+    tl.few_rows = t == 0 ? 1 : 0;
     if (h_split) {
       tl.a_hi = at<__half>(ws, p.o_N);
       tl.a_lo = tl.a_hi + (size_t)p.Rw * d;

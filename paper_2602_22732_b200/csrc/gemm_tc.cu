@@ -210,6 +210,13 @@ __device__ __forceinline__ void split_f16x2(float x0, float x1, float s, uint32_
   lo = *reinterpret_cast<const uint32_t *>(&l);
 }
 
+__device__ __forceinline__ void dbg_stamp(long long *dbg, int slot) {
+  if (!dbg) return;
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  dbg[blockIdx.x * 8 + slot] = t;
+}
+
 struct TileInfo {
   int m0, n0, M, N, K;
   int a_row, a_k, b_row, b_k;  // operand bases (rows, k) of the tile's group
@@ -320,6 +327,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) dbg_stamp(a.dbg, 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -350,6 +358,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (PAIR) cluster_sync_all();  // the leader's barriers exist before any peer traffic
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) dbg_stamp(a.dbg, 1);
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
   const bool leader = rank == 0;
   const int tstep = PAIR ? gridDim.x / 2 : gridDim.x;  // tiles are per pair
@@ -369,6 +378,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (kg >= STAGES) mbar_wait(&empty[s], ((kg / STAGES) - 1) & 1);
           unsigned char *st = smem + s * STAGE_BYTES;
           if constexpr (PAIR) {
+            if (kg == 0) dbg_stamp(a.dbg, 2);
             const uint32_t fb = cluster_addr(&full[s], 0);
             if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);  // both CTAs' bytes
             const int ak = ti.a_k + kt * BK, bk = ti.b_k + kt * BK;
@@ -378,6 +388,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             tma_load_2d_pair(st + A32 + B16, &tmBlo, fb, bk, ti.b_row + ti.n0 + (int)rank * BNL);
             continue;
           }
+          if (kg == 0) dbg_stamp(a.dbg, 2);
           mbar_expect_tx(&full[s], A32 + (BSPLIT ? 2 * B16 : B32));
           tma_load_2d(st, &tmA, &full[s], ti.a_k + kt * BK, ti.a_row + ti.m0);
           if (ASPLIT) tma_load_2d(st + A16, &tmAlo, &full[s], ti.a_k + kt * BK, ti.a_row + ti.m0);
@@ -408,6 +419,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int kt = 0; kt < nk; ++kt, ++kg) {
           const int s = kg % STAGES;
           mbar_wait(PAIR ? &full[s] : &conv[s], (kg / STAGES) & 1);
+          if (kg == 0) dbg_stamp(a.dbg, 3);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
           // in-place split: interleaved hi / lo atoms 1024 B apart; ASPLIT: two tiles
@@ -440,6 +452,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           mma_commit(&accf[acc]);
         ++j;
       }
+      dbg_stamp(a.dbg, 4);
     }
   } else if (warp < kEpiWarp0) {
     // ---- converters: landed fp32 tiles -> fp16 hi / lo operand tiles
@@ -474,6 +487,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if (!ti.valid) continue;
       const int acc = j & 1;
       mbar_wait(&accf[acc], (j >> 1) & 1);
+      if (j == 0 && warp == kEpiWarp0 && lane == 0) dbg_stamp(a.dbg, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int rbase = ti.m0 + q * 32;  // this warp's 32 rows (tile M side)
       const int nrows = min(32, ti.M - rbase);
@@ -484,7 +498,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       // drains one 128-column half (whole log-sum-exp parts); narrower tiles
       // leave the second warp idle
       constexpr int NC = BN / 32;
-      constexpr bool halves = kEpiWarps == 8 && NC >= 8;
+      // (LSE parts need a warp's four consecutive chunks: 128 columns)
+      constexpr bool halves =
+          kEpiWarps == 8 && (NC >= 8 || (NC >= 2 && EPI != EPI_STORE_LSE));
       const int eh = (warp - kEpiWarp0) >> 2;
       const int c_begin = halves ? eh * (NC / 2) : 0;
       const int c_end = halves ? c_begin + NC / 2 : (eh == 0 ? NC : 0);
@@ -722,9 +738,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       ++j;
     }
   }
+  if (warp == kEpiWarp0 && lane == 0) dbg_stamp(a.dbg, 6);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (PAIR) cluster_sync_all();  // no CTA leaves while its peer's traffic targets it
+  if (threadIdx.x == 0) dbg_stamp(a.dbg, 7);
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (PAIR)
@@ -881,6 +899,15 @@ static int launch_tc_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CU
 #undef GR_TC_PAIR
 }
 
+// GR4AD_FEW_ROWS=0 keeps few-row products on the pair tiles (A/B aid)
+static bool few_rows_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("GR4AD_FEW_ROWS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // GR4AD_TC_PAIR=0 keeps the single-CTA kernel for every product (A/B aid)
 static bool pair_enabled() {
   static const bool on = [] {
@@ -895,8 +922,14 @@ bool tc_eligible(long long lda, long long ldb, int K, const void *A, const void 
          (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
 }
 
-int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_rows,
+long long *g_tc_dbg = nullptr;  // gr4ad_debug_tc_timeline
+int g_dbg_few = 0;  // gr4ad_debug_tc_few_rows
+
+int gemm_tc(const TcArgs &a_in, long long a_rows, long long a_cols, long long b_rows,
             long long b_cols, int epi, cudaStream_t st) {
+  TcArgs a = a_in;
+  if (g_tc_dbg) a.dbg = g_tc_dbg;
+  if (g_dbg_few) a.few_rows = 1;
   if (a.M <= 0 || a.N <= 0 || a.groups <= 0) return GR4AD_OK;
   static const bool trace = getenv("GR4AD_TRACE") != nullptr;  // debug aid (read-only)
   if (trace)
@@ -904,9 +937,9 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
                     "A=(%lld,%lld) B=(%lld,%lld) presplit=%d asplit=%d\n",
             a.M, a.N, a.K, a.groups, a.mode, epi, a.lda, a.ldb, a.ldc, a_rows, a_cols, b_rows,
             b_cols, a.b_hi != nullptr, a.a_hi != nullptr);
-  prof_tag("tc M=%d N=%d K=%d g=%d mode=%d epi=%d A=%lldx%lld B=%lldx%lld split=%d%d", a.M, a.N,
-           a.K, a.groups, a.mode, epi, a_rows, a_cols, b_rows, b_cols, a.a_hi != nullptr,
-           a.b_hi != nullptr);
+  prof_tag("tc M=%d N=%d K=%d g=%d mode=%d epi=%d A=%lldx%lld B=%lldx%lld split=%d%d few=%d", a.M,
+           a.N, a.K, a.groups, a.mode, epi, a_rows, a_cols, b_rows, b_cols, a.a_hi != nullptr,
+           a.b_hi != nullptr, a.few_rows);
   if (epi == EPI_KV_SPLIT && (!a.k_hi || !a.vt_hi))
     return set_err(GR4AD_ERR_UNSUPPORTED, "K|V^T split epilogue needs its fp16 outputs");
   const bool wide = a.N >= 256;
@@ -920,6 +953,15 @@ int gemm_tc(const TcArgs &a, long long a_rows, long long a_cols, long long b_row
     GR_TRY(make_map(&mal, a.a_lo, true, a_rows, a_cols, a.lda, BM));
     // (per-request groups of <= 128 rows would leave half of a pair tile empty)
     const bool pair_mode = a.mode == GM_PLAIN || ((a.mode == GM_QK || a.mode == GM_PV) && a.M > BM);
+    // few rows per request (trunk, level 0): 128 x 128 single-CTA tiles --
+    // twice the CTAs of 256 x 256 pairs at the same M, and a two-warp
+    // epilogue per lane quarter; a choice by the rows' role, not the batch
+    // size, so a request decodes bit-identically in any batch
+    if (a.few_rows && a.mode == GM_PLAIN && few_rows_enabled()) {
+      GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, 128));
+      GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, 128));
+      return launch_tc<128, 6, true, true>(ma, mb, mbl, mal, a, epi, st);
+    }
     if (wide && pair_mode && pair_enabled()) {
       GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, 128));
       GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, 128));
@@ -977,3 +1019,9 @@ int gemm_tc_swapped(const TcArgs &a, long long a_rows, long long a_cols, long lo
 }
 
 }  // namespace gr
+
+// debug aid (not part of the ABI header): every tcgen05 GEMM launch writes
+// per-CTA %globaltimer stamps [CTA][8] into buf (NULL: off)
+extern "C" void gr4ad_debug_tc_timeline(long long *buf) { gr::g_tc_dbg = buf; }
+// debug aid: route every tcgen05 GEMM as a few-row product
+extern "C" void gr4ad_debug_tc_few_rows(int on) { gr::g_dbg_few = on; }

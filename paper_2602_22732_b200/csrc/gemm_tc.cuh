@@ -35,6 +35,10 @@ struct TcArgs : GemmArgs {
   // selection's window proxies)
   float4 *lse_part;
   int lse_ld;
+  // few rows per request (trunk rows, level 0): GM_PLAIN products run on
+  // 128 x 128 single-CTA tiles (gemm_tc) -- set by the rows' role
+  int few_rows;
+  long long *dbg;  // debug timeline: [CTA][8] %globaltimer stamps (gr4ad_debug_tc_timeline)
 };
 
 // A is (a_rows, a_cols) with ld lda, B is (b_rows, b_cols) K-major with ld ldb;
