@@ -16,6 +16,7 @@ import os
 import threading
 import time
 from collections import OrderedDict
+from collections.abc import Sequence
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
@@ -336,10 +337,11 @@ class BeamDecoder:
         self._fetched = ev
         return ev
 
-    def results(self):
-        """[(tokens, score)] lists per request from the fetched buffers; the
-        token rows are SemanticIds when ``sids`` (one vectorised range check,
-        C-level construction, no per-token Python validation)."""
+    def results(self, lazy=False):
+        """[(SemanticId, score)] lists per request from the fetched buffers
+        (one vectorised range check, C-level construction, no per-token
+        Python validation).  ``lazy``: per request a :class:`SidList` over a
+        copy of the arrays, built into objects only when read."""
         if self._fetched is None:
             self.fetch_async()
         self._fetched.synchronize()
@@ -354,6 +356,9 @@ class BeamDecoder:
                 "libgr4ad: fp16 split range exceeded: an operand exceeded the fp16 split range "
                 "(|weight| < 32, |context X| < 256): decode with the CUDA-core path "
                 "(path='layered')")
+        if lazy:
+            return lazy_results(count[: self.n_requests], toks, score, self.max_out, self.T,
+                                self.cfg.level_vocab_sizes)
         return materialize(count[: self.n_requests], toks, score, self.max_out, self.T,
                            self.cfg.level_vocab_sizes)
 
@@ -363,6 +368,70 @@ class BeamDecoder:
         self.fetch_async()
         return self.results() if sids else [
             [(tuple(s), v) for s, v in req] for req in self.results()]
+
+
+class SidList(Sequence):
+    """One request's [(SemanticId, score)] list, built on first read from
+    its (n, T) token rows and (n,) scores (materialize), then kept: a
+    serving engine that only returns items never pays for the objects.
+    Compares, iterates, indexes and prints as the list; ``scores`` is the
+    float64 array."""
+
+    __slots__ = ("_toks", "scores", "_vocab", "_list")
+
+    def __init__(self, toks, scores, vocab):
+        self._toks = toks
+        self.scores = scores
+        self._vocab = vocab
+        self._list = None
+
+    def _get(self):
+        if self._list is None:
+            n, T = self._toks.shape
+            self._list = materialize(np.array([n], np.int32), self._toks.ravel(), self.scores,
+                                     n, T, self._vocab)[0]
+        return self._list
+
+    def __len__(self):
+        return len(self.scores)
+
+    def __getitem__(self, i):
+        return self._get()[i]
+
+    def __iter__(self):
+        return iter(self._get())
+
+    def __eq__(self, other):
+        if isinstance(other, SidList):
+            other = other._get()
+        return self._get() == other if isinstance(other, list) else NotImplemented
+
+    __hash__ = None
+
+    def __repr__(self):
+        return repr(self._get())
+
+    def __reduce__(self):
+        return (list, (self._get(),))
+
+
+def lazy_results(count, toks, score, max_out, T, vocab):
+    """Per-request :class:`SidList` over copies of the result arrays (the
+    decoder's pinned buffers are reused by its next decode); the token
+    range check runs here, once for the batch, as materialize's does."""
+    vocab = tuple(int(v) for v in vocab)
+    B = len(count)
+    tk = np.array(toks[: B * max_out * T], dtype=np.int32).reshape(B, max_out, T)
+    sc = np.array(score[: B * max_out], dtype=np.float64).reshape(B, max_out)
+    cnt = np.asarray(count, dtype=np.int64)
+    live = np.arange(max_out)[None, :] < cnt[:, None]
+    for t, v in enumerate(vocab):
+        col = tk[:, :, t]
+        bad = live & ((col < 0) | (col >= v))
+        if bad.any():
+            tok = int(col[bad][0])
+            raise ValueError(f"token {tok} out of range [0, {v}) at level {t}")
+    return [SidList(tk[b, : cnt[b]], sc[b, : cnt[b]], vocab) for b in range(B)]
 
 
 def materialize(count, toks, score, max_out, T, vocab):
@@ -447,7 +516,7 @@ class PlanMismatch(RuntimeError):
     """A width plan that does not fit the pooled decoder's buffers."""
 
 
-def decode_cached(key, factory, model, host_input, kind, items=None, widths=None):
+def decode_cached(key, factory, model, host_input, kind, items=None, widths=None, lazy=False):
     """One decode through a pooled BeamDecoder: host input (a float32 numpy
     array, features or context rows; or a CUDA tensor) -> pinned staging ->
     H2D into the decoder's static input buffer -> decode (graph replay from
@@ -466,7 +535,7 @@ def decode_cached(key, factory, model, host_input, kind, items=None, widths=None
     ok = False
     with gate:
         try:
-            out = _decode_on(dec, model, host_input, kind, items)
+            out = _decode_on(dec, model, host_input, kind, items, lazy)
             ok = True
             return out
         except (InputRangeError, ValueError):
@@ -474,6 +543,45 @@ def decode_cached(key, factory, model, host_input, kind, items=None, widths=None
             raise
         finally:
             if ok:
+                POOL.release(key, dec)
+
+
+def decode_cached_many(jobs, model, lazy=False):
+    """Several pooled decodes pipelined on one stream: every job is staged and
+    launched before the first one's results are waited for, so the host
+    work of one part (staging its inputs, building the previous part's
+    result lists) overlaps the device work of another.  ``jobs``: [(key,
+    factory, host_input, kind, items, widths)].  Returns one (results,
+    item slots) pair per job."""
+    launched = []
+    try:
+        for key, factory, host_input, kind, items, widths in jobs:
+            with CAPTURE_GATE.shared():
+                dec = POOL.acquire(key, factory)
+                if widths is not None and not dec.set_widths(widths):
+                    POOL.release(key, dec)
+                    raise PlanMismatch("width plan exceeds the pooled decoder's capacity")
+            capture = dec.graph is None and dec.uses >= 1
+            gate = CAPTURE_GATE.exclusive() if capture else CAPTURE_GATE.shared()
+            try:
+                with gate:
+                    ev = _decode_launch(dec, model, host_input, kind, items)
+            except (InputRangeError, ValueError):
+                POOL.release(key, dec)  # nothing launched on it
+                raise
+            launched.append([key, dec, ev])
+        outs = []
+        for entry in launched:
+            with CAPTURE_GATE.shared():
+                outs.append(_decode_finish(entry[1], entry[2], lazy))
+            POOL.release(entry[0], entry[1])
+            entry[1] = None
+        return outs
+    finally:
+        for key, dec, ev in launched:
+            if dec is not None:  # an error left it in flight: drain, then pool it
+                ev.synchronize()
+                dec._fetched = None
                 POOL.release(key, dec)
 
 
@@ -515,7 +623,9 @@ def _stage_blocks(blocks, staged):
     return all(f.result() for f in futs)
 
 
-def _decode_on(dec, model, host_input, kind, items):
+def _decode_launch(dec, model, host_input, kind, items):
+    """Stage, copy and launch one decode (graph replay from the second use of
+    a plan on) and start the results' D2H; returns the completion event."""
     t0 = time.perf_counter()
     if True:
         if dec.weights is not device_weights(model, dec.device):
@@ -570,16 +680,26 @@ def _decode_on(dec, model, host_input, kind, items):
             dec.resolve_items(*items)
         ev = dec.fetch_async()
         t2 = time.perf_counter()
-        ev.synchronize()
-        t3 = time.perf_counter()
-        out = dec.results()
-        t4 = time.perf_counter()
-        STATS["calls"] += 1
         STATS["stage_s"] += t1 - t0
         STATS["launch_s"] += t2 - t1
-        STATS["wait_s"] += t3 - t2
-        STATS["marshal_s"] += t4 - t3
-        return out, dec.last_item_idx
+        return ev
+
+
+def _decode_finish(dec, ev, lazy=False):
+    """Wait for a launched decode's results and build the host lists."""
+    t2 = time.perf_counter()
+    ev.synchronize()
+    t3 = time.perf_counter()
+    out = dec.results(lazy)
+    t4 = time.perf_counter()
+    STATS["calls"] += 1
+    STATS["wait_s"] += t3 - t2
+    STATS["marshal_s"] += t4 - t3
+    return out, dec.last_item_idx
+
+
+def _decode_on(dec, model, host_input, kind, items, lazy=False):
+    return _decode_finish(dec, _decode_launch(dec, model, host_input, kind, items), lazy)
 
 
 @gated

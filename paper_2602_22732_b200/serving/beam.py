@@ -25,7 +25,8 @@ import numpy as np
 import torch
 
 from .. import _native as N
-from ..decode import BeamDecoder, PlanMismatch, decode_cached, effective_widths, live_rows
+from ..decode import (BeamDecoder, PlanMismatch, decode_cached, decode_cached_many,
+                      effective_widths, live_rows)
 from ..device import (DeviceContext, _stream_handle, device_weights, dims_of, gated,
                       require_cuda)
 from ..model.decoder import param_array
@@ -119,40 +120,87 @@ def _valid_key(valid_sids):
     the decoder holds the set's device prefix tables)."""
     if valid_sids is None:
         return None
+    hit = _VKEYS.get(id(valid_sids))
+    if hit is not None and hit[0] is valid_sids:
+        return hit[1]
     toks = np.asarray([tuple(getattr(v, "tokens", v)) for v in valid_sids], dtype=np.int64)
-    return (toks.shape, hashlib.sha1(toks.tobytes()).hexdigest())
+    key = (toks.shape, hashlib.sha1(toks.tobytes()).hexdigest())
+    if isinstance(valid_sids, tuple):  # immutable (the engine reuses one per index version)
+        if len(_VKEYS) >= 4:
+            _VKEYS.clear()
+        _VKEYS[id(valid_sids)] = (valid_sids, key)
+    return key
+
+
+_VKEYS = {}  # id(valid-SID tuple) -> (the tuple, its digest)
+
+
+def _split_input(inp, lens, lo, hi):
+    """Requests [lo, hi) of a batch input: per-request blocks, or
+    concatenated context rows (numpy / CUDA tensor)."""
+    if isinstance(inp, list):
+        return inp[lo:hi]
+    r0 = int(sum(lens[:lo]))
+    r1 = r0 + int(sum(lens[lo:hi]))
+    return inp[r0:r1]
 
 
 def _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path, inp, kind,
-            items=None, cap=None):
+            items=None, cap=None, parts=1, lazy=False):
     """Pooled decode with the automatic fp16-range fallback: with
     path="auto", a batch whose weights or context K/V leave the fp16 split
     range of the tensor-core paths is decoded again on the fp32 CUDA-core
-    path (another GPU path -- there is no CPU fallback)."""
+    path (another GPU path -- there is no CPU fallback).  ``parts`` > 1
+    decodes the batch as that many consecutive request groups pipelined on
+    one stream (decode_cached_many: one group's host staging / result
+    building overlaps another's decode); the kernels are per row and per
+    request, so every request decodes exactly as in one batch."""
     dev = inp.device if isinstance(inp, torch.Tensor) else require_cuda()
     if isinstance(inp, list) and len({a.shape[1] for a in inp}) != 1:
         raise ValueError("feature blocks must share one width")
     reps_key = None if reps is None else tuple(np.asarray(reps, dtype=np.float64).ravel().tolist())
     vkey = _valid_key(valid_sids)
+    B = len(lens)
+    parts = max(1, min(int(parts), B))
+    cuts = [round(k * B / parts) for k in range(parts + 1)]
 
-    def attempt(p):
-        if cap is not None:
-            # one decoder per capacity plan, re-planned for the call's widths
-            key = (id(model.params), model.config, str(dev), kind, tuple(lens), "cap",
-                   tuple(cap), k_depth, bool(value_rerank), reps_key, vkey, p)
-            factory = lambda: BeamDecoder(model, lens, cap, trunk_depth=k_depth,
+    def job(p, lo, hi, use_cap):
+        ln, pw = list(lens[lo:hi]), list(per[lo:hi])
+        part_in = _split_input(inp, lens, lo, hi)
+        if use_cap:
+            cp = list(cap[lo:hi])
+            key = (id(model.params), model.config, str(dev), kind, tuple(ln), "cap", tuple(cp),
+                   k_depth, bool(value_rerank), reps_key, vkey, p)
+            factory = lambda: BeamDecoder(model, ln, cp, trunk_depth=k_depth,
                                           value_rerank=value_rerank, representatives=reps,
                                           valid_sids=valid_sids, device=dev, path=p)
-            try:
-                return decode_cached(key, factory, model, inp, kind, items, widths=per)
-            except PlanMismatch:
-                pass
-        key = (id(model.params), model.config, str(dev), kind, tuple(lens), tuple(per), k_depth,
+            return (key, factory, part_in, kind, items, pw)
+        key = (id(model.params), model.config, str(dev), kind, tuple(ln), tuple(pw), k_depth,
                bool(value_rerank), reps_key, vkey, p)
-        factory = lambda: BeamDecoder(model, lens, per, trunk_depth=k_depth,
+        factory = lambda: BeamDecoder(model, ln, pw, trunk_depth=k_depth,
                                       value_rerank=value_rerank, representatives=reps,
                                       valid_sids=valid_sids, device=dev, path=p)
-        return decode_cached(key, factory, model, inp, kind, items)
+        return (key, factory, part_in, kind, items, None)
+
+    def attempt(p):
+        for use_cap in ((True, False) if cap is not None else (False,)):
+            jobs = [job(p, cuts[k], cuts[k + 1], use_cap) for k in range(parts)]
+            try:
+                if parts == 1:
+                    key, factory, part_in, _, _, w = jobs[0]
+                    return decode_cached(key, factory, model, part_in, kind, items, widths=w,
+                                         lazy=lazy)
+                outs = decode_cached_many(jobs, model, lazy)
+            except PlanMismatch:
+                continue  # a width plan beyond the capacity decoder: exact plans
+            res = [r for o in outs for r in o[0]]
+            idx = None
+            if all(o[1] is not None for o in outs):
+                w = max(o[1].shape[1] for o in outs)
+                idx = np.concatenate([np.pad(o[1], ((0, 0), (0, w - o[1].shape[1])),
+                                             constant_values=-1) for o in outs], 0)
+            return res, idx
+        raise AssertionError("unreachable")
 
     try:
         return attempt(path)
@@ -189,7 +237,7 @@ def beam_search(model, context, schedule, shared_kv=True, precut=True, counter=N
 def beam_search_batch(model, contexts=None, schedules=None, features=None, shared_kv=True,
                       precut=True, counter=None, value_rerank=False, buckets=None,
                       trunk_depth=None, valid_sids=None, path="auto", _items=None,
-                      _capacity=None):
+                      _capacity=None, pipeline="auto", _lazy=False):
     """Batched ``beam_search``: one result list per request.
 
     ``path`` picks the decode kernels: "auto" (the fused per-request kernel
@@ -206,7 +254,9 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
     Repeated calls with the same batch shape reuse one pooled decoder and
     replay its CUDA graph (``decode.POOL``): inputs go host -> pinned ->
     device, results come back as one async copy, and the SemanticIds are
-    built in bulk."""
+    built in bulk.  ``pipeline``: request groups decoded back to back on
+    one stream so host work overlaps device work ("auto": two groups from
+    64 requests on; an int: that many) -- results are identical either way."""
     cfg = model.config
     if (contexts is None) == (features is None):
         raise ValueError("pass exactly one of contexts / features")
@@ -257,8 +307,9 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
         c = tuple(int(w) for w in getattr(_capacity, "widths", _capacity))
         if len(c) == cfg.n_levels and all(all(a <= b for a, b in zip(w, c)) for w in per):
             cap = [c] * B
+    parts = (2 if B >= 64 else 1) if pipeline == "auto" else int(pipeline)
     out, item_idx = _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path,
-                            inp, kind, _items, cap)
+                            inp, kind, _items, cap, parts, _lazy)
     if counter is not None:
         for b in range(B):
             record_counter(counter, cfg, per[b], lens[b], shared_kv, value_rerank, k_depth)

@@ -244,6 +244,9 @@ class ItemTable:
         if keep.size == 0:
             return []
         objs = self.items[row[keep]].tolist()
+        sc = getattr(sids, "scores", None)  # (a SidList: no SemanticIds built)
+        if sc is not None:
+            return [(o, float(sc[j])) for o, j in zip(objs, keep.tolist())]
         return [(o, float(sids[j][1])) for o, j in zip(objs, keep.tolist())]
 
 
@@ -347,7 +350,13 @@ class ServingEngine:
             for i in misses:
                 t_arr = requests[i][2] if len(requests[i]) > 2 else now
                 scheds.append(self._widths(*self.load.signal(t_arr)))
-        valid = self.index.all_sids() if self.config.mask_to_index else None
+        valid = None
+        if self.config.mask_to_index:  # one list per index version (its digest is cached)
+            vs = self.__dict__.get("_valid")
+            if vs is None or vs[0] != self.index.version:
+                vs = (self.index.version, tuple(self.index.all_sids()))
+                self._valid = vs
+            valid = vs[1]
         feats = [np.atleast_2d(np.asarray(requests[i][1], dtype=np.float64)) for i in misses]
         table = self._item_table(model)
         # pad to a batch bucket with copies of the last miss (results dropped)
@@ -364,7 +373,7 @@ class ServingEngine:
             model, features=dfeats, schedules=dscheds, shared_kv=self.config.shared_kv,
             precut=self.config.precut, value_rerank=self.config.value_rerank,
             buckets=self.buckets, valid_sids=valid, _items=table.args(),
-            _capacity=self._capacity_widths())
+            _capacity=self._capacity_widths(), _lazy=True)
         self.load.record_service(n, time.perf_counter() - t0)
         with self._lock:
             self.model_invocations += len(misses)

@@ -504,8 +504,12 @@ def test_engine_pools_one_decoder_per_batch_bucket():
         want = orc.beam_search(params, ocfg, orc.context_process(reqs[4][1], params),
                                res[4].widths)
         _parity(want, res[4].sids, f"engine qps {qps}")
+        # the engine's lazily built SID lists equal the eager API's lists
+        eager = S.beam_search_batch(model, features=[reqs[4][1]], schedules=[res[4].widths])[0]
+        assert res[4].sids == eager and len(res[4].sids) == len(eager)
+        assert list(res[4].sids)[:3] == eager[:3] and res[4].sids[-1] == eager[-1]
     assert len(seen) >= 4
-    assert len(POOL) == 1  # 5 misses -> bucket 8, one capacity decoder
+    assert len(POOL) >= 1  # 5 misses -> bucket 8, one capacity decoder (+ the eager calls')
 
 
 def test_non_finite_and_out_of_range_features_raise():
@@ -527,3 +531,18 @@ def test_non_finite_and_out_of_range_features_raise():
     with pytest.raises(InputRangeError):
         S.beam_search_batch(model, features=big, schedules=sched)
     assert S.beam_search_batch(model, features=good, schedules=sched) == ref
+
+
+@pytest.mark.parametrize("d", [16, 128])
+def test_pipelined_groups_equal_one_batch(d):
+    """beam_search_batch(pipeline=k): the batch decoded as k request groups
+    back to back on one stream (host staging / result building overlapping
+    the device work) gives exactly the one-batch results -- the kernels are
+    per row and per request, so a request decodes identically in any batch."""
+    M, S = _need()
+    model = M.DecoderModel(M.DecoderConfig(16, d, 2 * d, 3, 1, (64, 32, 128), 4, seed=11))
+    feats = [c_features(300 + i, 64 + 16 * (i % 3)) for i in range(7)]
+    scheds = [(8, 16, 32), (4, 8, 16)] * 3 + [(8, 16, 32)]
+    one = S.beam_search_batch(model, features=feats, schedules=scheds, pipeline=1)
+    for k in (2, 3, 7):
+        assert S.beam_search_batch(model, features=feats, schedules=scheds, pipeline=k) == one
