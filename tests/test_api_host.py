@@ -169,3 +169,83 @@ def test_load_estimator_rate_and_slack():
     assert abs(est.capacity - 400.0) < 1e-9
     est.record_service(300, 0.5)  # >= half the largest batch: EWMA update
     assert abs(est.capacity - (0.8 * 400.0 + 0.2 * 600.0)) < 1e-9
+
+
+def test_lazy_sid_lists_equal_the_eager_lists():
+    """decode.lazy_results / SidList (the engine's result lists): built on
+    first read from copies of the result arrays, equal to materialize's
+    lists in every list operation, with the batch's token range check done
+    up front (the same ValueError as SemanticId)."""
+    from paper_2602_22732_b200.decode import SidList, lazy_results, materialize
+    rng = np.random.default_rng(3)
+    B, m, T, vocab = 6, 9, 3, (7, 5, 11)
+    toks = np.stack([rng.integers(0, v, size=B * m) for v in vocab], 1).astype(np.int32).ravel()
+    score = -rng.random(B * m)
+    count = np.array([9, 0, 3, 9, 1, 5], np.int32)
+    eager = materialize(count, toks, score, m, T, vocab)
+    lazy = lazy_results(count, toks.copy(), score.copy(), m, T, vocab)
+    toks[:] = 0  # the lazy lists hold copies: the decoder may reuse its buffers
+    for e, z in zip(eager, lazy):
+        assert isinstance(z, SidList) and z._list is None
+        assert len(z) == len(e) and z.scores.tolist() == [s for _, s in e]
+        assert z._list is None  # len / scores never build objects
+        assert z == e and e == z and list(z) == e and repr(z) == repr(e)
+        if e:
+            assert z[0] == e[0] and z[-1] == e[-1] and z[1:] == e[1:]
+    assert lazy[0] != lazy[2] and lazy[1] == []
+    bad = toks.copy()
+    bad[3 * T + 2] = 11  # request 0, entry 3, level 2
+    with pytest.raises(ValueError, match="out of range"):
+        lazy_results(count, bad, score, m, T, vocab)
+    bad[3 * T + 2] = 0
+    bad[m * T + 2] = 99  # request 1 has no live entries: not checked
+    lazy_results(count, bad, score, m, T, vocab)
+
+
+def test_group_split_and_valid_sid_digest_cache():
+    """_split_input cuts per-request blocks or concatenated rows by request;
+    _valid_key caches the digest of an immutable SID tuple only."""
+    from paper_2602_22732_b200.serving import beam as SB
+    lens = [3, 1, 4, 2]
+    rows = np.arange(10 * 2, dtype=np.float32).reshape(10, 2)
+    assert SB._split_input(rows, lens, 1, 3).tolist() == rows[3:8].tolist()
+    blocks = [rows[:3], rows[3:4], rows[4:8], rows[8:]]
+    assert SB._split_input(blocks, lens, 2, 4) == blocks[2:]
+    sids = tuple(SemanticId((i % 3, i % 2), (3, 2)) for i in range(5))
+    k1 = SB._valid_key(sids)
+    assert SB._VKEYS[id(sids)][1] == k1 and SB._valid_key(sids) == k1
+    lst = list(sids)
+    assert SB._valid_key(lst) == k1 and id(lst) not in SB._VKEYS
+    lst[0] = SemanticId((2, 1), (3, 2))  # a mutable list is re-hashed every call
+    assert SB._valid_key(lst) != k1
+
+
+def test_engine_capacity_widths_and_item_table():
+    """ServingEngine._capacity_widths bounds every TABS schedule (pooled
+    decoders are planned for it); ItemTable keys valid SIDs in mixed radix
+    with the min item id and resolves slot rows (CPU tensors here)."""
+    from paper_2602_22732_b200.quantizer import SidIndex
+    from paper_2602_22732_b200.serving.engine import ItemTable, LoadEstimator
+    cfg = DecoderConfig(feat_dim=4, d=4, d_ff=6, n_layers=2, trunk_depth=1,
+                        level_vocab_sizes=(3, 3), n_value_buckets=2, seed=5)
+    from paper_2602_22732_b200.serving.engine import ServingConfig, ServingEngine, SnapshotStore
+    from paper_2602_22732_b200.serving.schedule import (BeamSchedule, TrafficSignal,
+                                                         scale_schedule, tabs_adjust)
+    base = BeamSchedule((2, 5, 9), 9)
+    eng = ServingEngine(SnapshotStore(DecoderModel(cfg), preload=False), SidIndex(),
+                        ServingConfig(base, q_threshold=100.0, boost=0.6), load=LoadEstimator())
+    cap = eng._capacity_widths()
+    for qps in (0.0, 10.0, 50.0, 99.0, 100.0, 1e6):
+        for slack in (0.0, 0.3, 1.0):
+            w = scale_schedule(base, tabs_adjust(TrafficSignal(qps, 100.0, slack), 9, 0.6)).widths
+            assert all(a <= b for a, b in zip(w, cap))
+    index = SidIndex()
+    index.upsert("b", SemanticId((1, 2), (3, 3)))
+    index.upsert("a", SemanticId((1, 2), (3, 3)))
+    index.upsert("c", SemanticId((0, 1), (3, 3)))
+    index.upsert("x", SemanticId((4, 4), (5, 5)))  # another vocabulary: never decodable
+    tab = ItemTable(index, (3, 3), "cpu")
+    assert tab.n == 2 and tab.keys.tolist() == [0 * 3 + 1, 1 * 3 + 2]
+    sids = [(SemanticId((1, 2), (3, 3)), -0.5), (SemanticId((2, 2), (3, 3)), -0.7),
+            (SemanticId((0, 1), (3, 3)), -0.9)]
+    assert tab.resolve(sids, np.array([1, -1, 0, 5], np.int32)) == [("a", -0.5), ("c", -0.9)]

@@ -546,3 +546,29 @@ def test_pipelined_groups_equal_one_batch(d):
     one = S.beam_search_batch(model, features=feats, schedules=scheds, pipeline=1)
     for k in (2, 3, 7):
         assert S.beam_search_batch(model, features=feats, schedules=scheds, pipeline=k) == one
+
+
+@pytest.mark.parametrize("d,path", [(128, "tensor"), (16, "fused"), (16, "layered")])
+def test_set_widths_with_masking_and_rerank(d, path):
+    """Re-planned decoders keep the valid-SID prefix tables and the value
+    re-rank head: every plan equals a decoder built for it."""
+    M, S = _need()
+    from paper_2602_22732_b200.decode import BeamDecoder
+    model = M.DecoderModel(M.DecoderConfig(16, d, 2 * d, 3, 1, (64, 32, 128), 4, seed=13))
+    rng = np.random.default_rng(5)
+    valid = [tuple(int(rng.integers(0, v)) for v in (64, 32, 128)) for _ in range(400)]
+    reps = [0.1, 0.4, 0.9, 2.0]
+    lens = [96, 128, 64]
+    feats = [c_features(400 + i, n) for i, n in enumerate(lens)]
+    x = torch.from_numpy(np.concatenate(feats).astype(np.float32)).cuda()
+    cap = [(24, 48, 96)] * 3
+    dec = BeamDecoder(model, lens, cap, value_rerank=True, representatives=reps,
+                      valid_sids=valid, path=path)
+    for widths in ([(8, 16, 32)] * 3, [(24, 48, 96), (5, 9, 17), (12, 30, 60)], cap):
+        assert dec.set_widths(widths)
+        dec.run(features=x)
+        got = dec.host_results()
+        fresh = BeamDecoder(model, lens, widths, value_rerank=True, representatives=reps,
+                            valid_sids=valid, path=path)
+        fresh.run(features=x)
+        assert got == fresh.host_results(), widths
