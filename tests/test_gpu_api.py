@@ -548,7 +548,7 @@ def test_pipelined_groups_equal_one_batch(d):
         assert S.beam_search_batch(model, features=feats, schedules=scheds, pipeline=k) == one
 
 
-@pytest.mark.parametrize("d,path", [(128, "tensor"), (16, "fused"), (16, "layered")])
+@pytest.mark.parametrize("d,path", [(128, "tensor"), (16, "auto"), (16, "layered")])
 def test_set_widths_with_masking_and_rerank(d, path):
     """Re-planned decoders keep the valid-SID prefix tables and the value
     re-rank head: every plan equals a decoder built for it."""
