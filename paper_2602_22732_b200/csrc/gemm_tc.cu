@@ -820,7 +820,17 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
       default: break;
     }
   }
-  if constexpr (BN < 128) {
+  if constexpr (BN == 64 && BSPLIT && ASPLIT) {  // few-row products (no 128-column LSE parts)
+    switch (epi) {
+      GR_TC_EPI(EPI_STORE)
+      GR_TC_EPI(EPI_RESID)
+      GR_TC_EPI(EPI_BIAS_RESID)
+      GR_TC_EPI(EPI_BIAS_GELU_SPLIT)
+      GR_TC_EPI(EPI_STORE_SPLIT)
+      GR_TC_EPI(EPI_BIAS_RESID_DUAL)
+      default: return set_err(GR4AD_ERR_UNSUPPORTED, "tc epilogue %d at BN=64", epi);
+    }
+  } else if constexpr (BN < 128) {
     return set_err(GR4AD_ERR_UNSUPPORTED, "tc epilogue %d at BN=%d", epi, BN);
   } else if constexpr (ASPLIT) {  // the head layers' dense products on pre-split activations
     switch (epi) {
@@ -908,6 +918,15 @@ static bool few_rows_enabled() {
   return on;
 }
 
+// GR4AD_FEW_BN=64|128: tile width of the few-row products (A/B aid)
+static int few_rows_bn() {
+  static const int bn = [] {
+    const char *e = getenv("GR4AD_FEW_BN");
+    return e && atoi(e) == 128 ? 128 : 64;
+  }();
+  return bn;
+}
+
 // GR4AD_TC_PAIR=0 keeps the single-CTA kernel for every product (A/B aid)
 static bool pair_enabled() {
   static const bool on = [] {
@@ -958,8 +977,16 @@ int gemm_tc(const TcArgs &a_in, long long a_rows, long long a_cols, long long b_
     // epilogue per lane quarter; a choice by the rows' role, not the batch
     // size, so a request decodes bit-identically in any batch
     if (a.few_rows && a.mode == GM_PLAIN && few_rows_enabled()) {
-      GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, 128));
-      GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, 128));
+      // 128 x 64 tiles where the epilogue allows (not the 128-column LSE parts)
+      // and they still fit one wave (tile width does not change any element's
+      // K order, so results are the same either way)
+      const long long narrow_tiles = (long long)((a.M + BM - 1) / BM) * ((a.N + 63) / 64);
+      const bool narrow = few_rows_bn() == 64 && epi != EPI_STORE_LSE && epi != EPI_KV_SPLIT &&
+                          epi != EPI_MULVEC_SPLIT && narrow_tiles <= num_sms();
+      const int bn = narrow ? 64 : 128;
+      GR_TRY(make_map(&mb, a.b_hi, true, b_rows, b_cols, a.ldb, bn));
+      GR_TRY(make_map(&mbl, a.b_lo, true, b_rows, b_cols, a.ldb, bn));
+      if (narrow) return launch_tc<64, 8, true, true>(ma, mb, mbl, mal, a, epi, st);
       return launch_tc<128, 6, true, true>(ma, mb, mbl, mal, a, epi, st);
     }
     if (wide && pair_mode && pair_enabled()) {
