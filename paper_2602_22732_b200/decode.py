@@ -468,11 +468,25 @@ class DecoderPool:
     callers of the same shape get separate decoders); LRU-bounded by total
     workspace bytes."""
 
-    def __init__(self, max_bytes=48 << 30, max_decoders=32):
+    def __init__(self, max_bytes=None, max_decoders=64):
         self._lock = threading.Lock()
         self._idle = OrderedDict()
-        self.max_bytes = max_bytes
+        self._max_bytes = max_bytes  # None: 40 % of the device's memory
         self.max_decoders = max_decoders
+
+    @property
+    def max_bytes(self):
+        if self._max_bytes is None:
+            try:
+                total = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
+            except Exception:  # no device (host-only use): assume a 120 GiB part
+                total = 120 << 30
+            self._max_bytes = int(0.4 * total)
+        return self._max_bytes
+
+    @max_bytes.setter
+    def max_bytes(self, v):
+        self._max_bytes = v
 
     def acquire(self, key, factory):
         with self._lock:
@@ -516,7 +530,8 @@ class PlanMismatch(RuntimeError):
     """A width plan that does not fit the pooled decoder's buffers."""
 
 
-def decode_cached(key, factory, model, host_input, kind, items=None, widths=None, lazy=False):
+def decode_cached(key, factory, model, host_input, kind, items=None, widths=None, lazy=False,
+                  graphs=True):
     """One decode through a pooled BeamDecoder: host input (a float32 numpy
     array, features or context rows; or a CUDA tensor) -> pinned staging ->
     H2D into the decoder's static input buffer -> decode (graph replay from
@@ -530,12 +545,12 @@ def decode_cached(key, factory, model, host_input, kind, items=None, widths=None
         if widths is not None and not dec.set_widths(widths):
             POOL.release(key, dec)
             raise PlanMismatch("width plan exceeds the pooled decoder's capacity")
-    capture = dec.graph is None and dec.uses >= 1
+    capture = graphs and dec.graph is None and dec.uses >= 1
     gate = CAPTURE_GATE.exclusive() if capture else CAPTURE_GATE.shared()
     ok = False
     with gate:
         try:
-            out = _decode_on(dec, model, host_input, kind, items, lazy)
+            out = _decode_on(dec, model, host_input, kind, items, lazy, capture)
             ok = True
             return out
         except (InputRangeError, ValueError):
@@ -546,7 +561,7 @@ def decode_cached(key, factory, model, host_input, kind, items=None, widths=None
                 POOL.release(key, dec)
 
 
-def decode_cached_many(jobs, model, lazy=False):
+def decode_cached_many(jobs, model, lazy=False, graphs=True):
     """Several pooled decodes pipelined on one stream: every job is staged and
     launched before the first one's results are waited for, so the host
     work of one part (staging its inputs, building the previous part's
@@ -561,11 +576,11 @@ def decode_cached_many(jobs, model, lazy=False):
                 if widths is not None and not dec.set_widths(widths):
                     POOL.release(key, dec)
                     raise PlanMismatch("width plan exceeds the pooled decoder's capacity")
-            capture = dec.graph is None and dec.uses >= 1
+            capture = graphs and dec.graph is None and dec.uses >= 1
             gate = CAPTURE_GATE.exclusive() if capture else CAPTURE_GATE.shared()
             try:
                 with gate:
-                    ev = _decode_launch(dec, model, host_input, kind, items)
+                    ev = _decode_launch(dec, model, host_input, kind, items, capture)
             except (InputRangeError, ValueError):
                 POOL.release(key, dec)  # nothing launched on it
                 raise
@@ -623,9 +638,10 @@ def _stage_blocks(blocks, staged):
     return all(f.result() for f in futs)
 
 
-def _decode_launch(dec, model, host_input, kind, items):
+def _decode_launch(dec, model, host_input, kind, items, capture=True):
     """Stage, copy and launch one decode (graph replay from the second use of
-    a plan on) and start the results' D2H; returns the completion event."""
+    a plan on; ``capture=False`` replays an existing graph but captures none)
+    and start the results' D2H; returns the completion event."""
     t0 = time.perf_counter()
     if True:
         if dec.weights is not device_weights(model, dec.device):
@@ -662,7 +678,7 @@ def _decode_launch(dec, model, host_input, kind, items):
         t1 = time.perf_counter()
         if dec.graph is not None:
             dec.graph.replay()
-        elif dec.uses >= 1:
+        elif capture and dec.uses >= 1:
             # second use of this shape: capture once, replay from now on
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream(dec.device)
@@ -698,8 +714,8 @@ def _decode_finish(dec, ev, lazy=False):
     return out, dec.last_item_idx
 
 
-def _decode_on(dec, model, host_input, kind, items, lazy=False):
-    return _decode_finish(dec, _decode_launch(dec, model, host_input, kind, items), lazy)
+def _decode_on(dec, model, host_input, kind, items, lazy=False, capture=True):
+    return _decode_finish(dec, _decode_launch(dec, model, host_input, kind, items, capture), lazy)
 
 
 @gated

@@ -146,7 +146,7 @@ def _split_input(inp, lens, lo, hi):
 
 
 def _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path, inp, kind,
-            items=None, cap=None, parts=1, lazy=False):
+            items=None, cap=None, parts=1, lazy=False, graphs=True):
     """Pooled decode with the automatic fp16-range fallback: with
     path="auto", a batch whose weights or context K/V leave the fp16 split
     range of the tensor-core paths is decoded again on the fp32 CUDA-core
@@ -189,8 +189,8 @@ def _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path, inp
                 if parts == 1:
                     key, factory, part_in, _, _, w = jobs[0]
                     return decode_cached(key, factory, model, part_in, kind, items, widths=w,
-                                         lazy=lazy)
-                outs = decode_cached_many(jobs, model, lazy)
+                                         lazy=lazy, graphs=graphs)
+                outs = decode_cached_many(jobs, model, lazy, graphs)
             except PlanMismatch:
                 continue  # a width plan beyond the capacity decoder: exact plans
             res = [r for o in outs for r in o[0]]
@@ -237,7 +237,7 @@ def beam_search(model, context, schedule, shared_kv=True, precut=True, counter=N
 def beam_search_batch(model, contexts=None, schedules=None, features=None, shared_kv=True,
                       precut=True, counter=None, value_rerank=False, buckets=None,
                       trunk_depth=None, valid_sids=None, path="auto", _items=None,
-                      _capacity=None, pipeline="auto", _lazy=False):
+                      _capacity=None, pipeline="auto", _lazy=False, _graphs=True):
     """Batched ``beam_search``: one result list per request.
 
     ``path`` picks the decode kernels: "auto" (the fused per-request kernel
@@ -309,7 +309,7 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
             cap = [c] * B
     parts = (2 if B >= 64 else 1) if pipeline == "auto" else int(pipeline)
     out, item_idx = _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path,
-                            inp, kind, _items, cap, parts, _lazy)
+                            inp, kind, _items, cap, parts, _lazy, _graphs)
     if counter is not None:
         for b in range(B):
             record_counter(counter, cfg, per[b], lens[b], shared_kv, value_rerank, k_depth)

@@ -106,7 +106,7 @@ class ServingConfig:
     # request per call): a batch's misses are padded to the next of these
     # sizes so the pooled decoders (and their CUDA graphs) are reused across
     # batches; None decodes exactly the misses
-    batch_buckets: tuple = (1, 2, 4, 8, 16, 32, 64, 128, 256, 512)
+    batch_buckets: tuple = (1, 2, 4, 8, 16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512)
     # TABS widths from the engine's own load signal: "batch" measures it once
     # per batch (the reference's per-tick traffic signal, sim/loop.py:239-264),
     # "request" at every request's arrival (per-request widths in one batch)
@@ -350,13 +350,7 @@ class ServingEngine:
             for i in misses:
                 t_arr = requests[i][2] if len(requests[i]) > 2 else now
                 scheds.append(self._widths(*self.load.signal(t_arr)))
-        valid = None
-        if self.config.mask_to_index:  # one list per index version (its digest is cached)
-            vs = self.__dict__.get("_valid")
-            if vs is None or vs[0] != self.index.version:
-                vs = (self.index.version, tuple(self.index.all_sids()))
-                self._valid = vs
-            valid = vs[1]
+        valid = self._valid_sids()
         feats = [np.atleast_2d(np.asarray(requests[i][1], dtype=np.float64)) for i in misses]
         table = self._item_table(model)
         # pad to a batch bucket with copies of the last miss (results dropped)
@@ -373,7 +367,11 @@ class ServingEngine:
             model, features=dfeats, schedules=dscheds, shared_kv=self.config.shared_kv,
             precut=self.config.precut, value_rerank=self.config.value_rerank,
             buckets=self.buckets, valid_sids=valid, _items=table.args(),
-            _capacity=self._capacity_widths(), _lazy=True)
+            _capacity=self._capacity_widths(), _lazy=True,
+            # serving replays the graphs warmup() captured (base and widest
+            # plans) and launches other width plans directly: a capture
+            # (10-40 ms at C5) never lands on a request's latency
+            _graphs=False)
         self.load.record_service(n, time.perf_counter() - t0)
         with self._lock:
             self.model_invocations += len(misses)
@@ -405,13 +403,25 @@ class ServingEngine:
                    if max_batch is None or b <= max_batch]
         cap = self._capacity_widths()
         plans = widths if widths is not None else [self.config.schedule.widths, cap]
+        valid = self._valid_sids()
         for b in buckets:
             for w in plans:
                 for _ in range(2):  # the second use captures the plan's graph
                     beam_search_batch(model, features=[f] * b, schedules=[tuple(w)] * b,
                                       shared_kv=self.config.shared_kv,
                                       value_rerank=self.config.value_rerank,
-                                      buckets=self.buckets, _capacity=cap)
+                                      buckets=self.buckets, valid_sids=valid, _capacity=cap)
+
+    def _valid_sids(self):
+        """The index's SIDs as one tuple per index version (masked decoding;
+        the tuple's digest -- part of the pooled decoder's key -- is cached)."""
+        if not self.config.mask_to_index:
+            return None
+        vs = self.__dict__.get("_valid")
+        if vs is None or vs[0] != self.index.version:
+            vs = (self.index.version, tuple(self.index.all_sids()))
+            self._valid = vs
+        return vs[1]
 
     def _capacity_widths(self):
         """The widest schedule TABS can produce (slack 1, or the base when
