@@ -5,6 +5,9 @@
 #include <stdio.h>
 #include <stdarg.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "gr4ad.h"
 
 namespace gr {
@@ -63,6 +66,31 @@ void prof_end(int cls, cudaStream_t st);
     ::gr::count_launch();                \
     GR_CUDA(cudaGetLastError());         \
   } while (0)
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
+// size): the attribute persists, and setting it before every launch costs
+// host time on the eager (non-graph) launch path
+inline cudaError_t set_smem_attr(const void *kernel, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<unsigned long long, int> done;  // (kernel ^ device) -> bytes
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long key = reinterpret_cast<unsigned long long>(kernel) ^
+                                 ((unsigned long long)dev << 56);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  }
+  const cudaError_t e =
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(mu);
+    int &v = done[key];
+    if (v < bytes) v = bytes;
+  }
+  return e;
+}
 
 // order-preserving float <-> uint32 (larger float -> larger key)
 __device__ __forceinline__ uint32_t f2ord(float f) {

@@ -2400,12 +2400,12 @@ int fused_mma_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStream
   bool masked = false;
   for (int t = 0; t < a.T; ++t) masked |= a.vp_rp[t] != nullptr;
   if (masked) {
-    GR_CUDA(cudaFuncSetAttribute(fused_mma_kernel<16, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(fused_mma_kernel<16, true>),
+                                 (int)smem));
     GR_LAUNCH(KC_FUSED, st, fused_mma_kernel<16, true><<<n_requests, kThreads, smem, st>>>(a));
   } else {
-    GR_CUDA(cudaFuncSetAttribute(fused_mma_kernel<16, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(fused_mma_kernel<16, false>),
+                                 (int)smem));
     GR_LAUNCH(KC_FUSED, st, fused_mma_kernel<16, false><<<n_requests, kThreads, smem, st>>>(a));
   }
   return GR4AD_OK;
@@ -2415,8 +2415,8 @@ int fused_small_launch(const FusedArgs &a, int n_requests, size_t smem, cudaStre
   if (n_requests <= 0) return GR4AD_OK;
 #define GR_FUSED_CASE(DD)                                                                \
   if (a.D == DD) {                                                                       \
-    GR_CUDA(cudaFuncSetAttribute(fused_small_kernel<DD>,                                 \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(fused_small_kernel<DD>),                                 \
+                                 (int)smem)); \
     GR_LAUNCH(KC_FUSED, st, fused_small_kernel<DD><<<n_requests, kThreads, smem, st>>>(a)); \
     return GR4AD_OK;                                                                     \
   }

@@ -789,9 +789,16 @@ static int make_map(CUtensorMap *m, const void *base, bool f16, long long rows, 
 }
 
 static int num_sms() {
-  int dev = 0, n = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n;
+  // per device, queried once (this runs on every launch of the eager path)
+  static int cached[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n;
+  }
+  return cached[dev];
 }
 
 template <int BN, int STAGES, bool BSPLIT, bool ASPLIT = false>
@@ -806,8 +813,8 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
   const int cls = (a.mode == GM_PLAIN) ? KC_GEMM : KC_ATTN_GEMM;
 #define GR_TC_EPI(E)                                                                          \
   case E: {                                                                                   \
-    GR_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, E, BSPLIT, ASPLIT>,               \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(gemm_tc_kernel<BN, STAGES, E, BSPLIT, ASPLIT>),               \
+                                 (int)smem));      \
     GR_LAUNCH(cls, st, gemm_tc_kernel<BN, STAGES, E, BSPLIT, ASPLIT>                           \
                        <<<grid, kTcThreads, smem, st>>>(ma, mb, mbl, mal, a, tiles_m, tiles_n,  \
                                                         n_tiles));                            \
@@ -889,7 +896,7 @@ static int launch_tc_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CU
 #define GR_TC_PAIR(E)                                                                            \
   case E: {                                                                                      \
     auto *k = gemm_tc_kernel<BN, STAGES, E, true, true, true>;                                   \
-    GR_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(k), (int)smem));    \
     GR_LAUNCH(cls, st, GR_CUDA(cudaLaunchKernelEx(&cfg, k, ma, mb, mbl, mal, a, tiles_m,           \
                                                       tiles_n, n_tiles)));                       \
     return GR4AD_OK;                                                                             \

@@ -1358,12 +1358,12 @@ int topk_select(const SelectArgs &a, int n_requests, int u_rows, int u_k,
   size_t sm = sizeof(unsigned long long) * GR4AD_MAX_BEAM + sizeof(unsigned) * 2048 +
               (cache ? sizeof(uint32_t) * kCacheKeys : 0);
   if (cache) {
-    GR_CUDA(cudaFuncSetAttribute(topk_select_kernel<true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(topk_select_kernel<true>),
+                                 (int)sm));
     GR_LAUNCH(KC_TOPK, st, topk_select_kernel<true><<<n_requests, kSelThreads, sm, st>>>(a, u_rows, u_k));
   } else {
-    GR_CUDA(cudaFuncSetAttribute(topk_select_kernel<false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(topk_select_kernel<false>),
+                                 (int)sm));
     GR_LAUNCH(KC_TOPK, st, topk_select_kernel<false><<<n_requests, kSelThreads, sm, st>>>(a, u_rows, u_k));
   }
   return GR4AD_OK;
@@ -1686,8 +1686,7 @@ int collect_results(int n_requests, int T, const int *row_off_T, const int *live
                     int max_out, int *count, int *tokens, double *score, cudaStream_t st) {
   if (n_requests <= 0) return GR4AD_OK;
   size_t sm = vlogits ? (sizeof(double) + sizeof(int)) * GR4AD_MAX_BEAM : 0;
-  if (sm) GR_CUDA(cudaFuncSetAttribute(collect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)sm));
+  if (sm) GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(collect_kernel), (int)sm));
   GR_LAUNCH(KC_COLLECT, st, collect_kernel<<<n_requests, 512, sm, st>>>(T, row_off_T, live_T, hist_off_T, tok, anc,
                                               anc_stride, cum, vlogits, nb, reps, max_out,
                                               count, tokens, score));

@@ -648,8 +648,8 @@ int latent_attn(const float *q, const float *feats, int F, const int *g_row_off,
 #define GR_LA_F(FF)                                                                          \
   if (F == FF) {                                                                             \
     const size_t sm = LatMma<FF>::smem;                                                      \
-    GR_CUDA(cudaFuncSetAttribute(latent_attn_kernel<FF, false>,                              \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));     \
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(latent_attn_kernel<FF, false>),                              \
+                                 (int)sm));     \
     dim3 grid(ceil_div(max_group_rows, rpc), n_groups);                                      \
     GR_LAUNCH(KC_ATTN_GEMM, st, latent_attn_kernel<FF, false><<<grid, 128, sm, st>>>(         \
                                     q, feats, g_row_off, g_rows, g_ctx_off, g_ctx_len, rpc,  \
@@ -674,8 +674,8 @@ int latent_cross_ln(const float *h, int d, const __half *aq_hi, const __half *aq
 #define GR_LA_F(FF)                                                                          \
   if (F == FF) {                                                                             \
     const size_t sm = LatMma<FF>::smem_ln;                                                   \
-    GR_CUDA(cudaFuncSetAttribute(latent_attn_kernel<FF, true>,                               \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));     \
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(latent_attn_kernel<FF, true>),                               \
+                                 (int)sm));     \
     dim3 grid(ceil_div(max_group_rows, rpc), n_groups);                                      \
     GR_LAUNCH(KC_ATTN_GEMM, st, latent_attn_kernel<FF, true><<<grid, 128, sm, st>>>(          \
                                     nullptr, nullptr, g_row_off, g_rows, g_ctx_off,          \
@@ -786,8 +786,8 @@ int latent_out_ln(const float *z, int F, const __half *bo_hi, const __half *bo_l
 #define GR_LO(FF, NW)                                                                        \
   if (F == FF && d == NW * 128) {                                                            \
     const size_t sm = LatOut<NW>::smem;                                                      \
-    GR_CUDA(cudaFuncSetAttribute(latent_out_ln_kernel<FF, NW>,                               \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));     \
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(latent_out_ln_kernel<FF, NW>),                               \
+                                 (int)sm));     \
     GR_LAUNCH(KC_LAYERNORM, st, latent_out_ln_kernel<FF, NW><<<ceil_div(rows, 16), NW * 32,   \
                                                                sm, st>>>(                    \
                                     z, bo_hi, bo_lo, a, c, hs, g2, b2, n_hi, n_lo, ld_n, hn, \

@@ -179,8 +179,7 @@ extern "C" int gr4ad_topk_precut_f64(const double *prev_scores, const double *lo
   int sort_n = 2;
   while (sort_n < kk) sort_n <<= 1;
   const size_t smem = (size_t)sort_n * (sizeof(unsigned long long) + sizeof(unsigned int));
-  GR_CUDA(cudaFuncSetAttribute(topk_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
+  GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(topk_f64_kernel), (int)smem));
   cudaStream_t st = (cudaStream_t)stream;
   GR_LAUNCH(KC_TOPK, st,
             topk_f64_kernel<<<n_problems, kSelThreads, smem, st>>>(

@@ -49,7 +49,7 @@ timeout -s KILL 600 $NF -k regex:gemm_tc -s $W2 -c 1 -o $O/prof_gemm_w2 $B > $O/
 timeout -s KILL 600 $NF -k regex:gemm_tc -s $TW1 -c 1 -o $O/prof_gemm_trunk_w1 $B > $O/ncu4.log 2>&1
 timeout -s KILL 600 $NF -k regex:topk_select -s 1 -c 1 -o $O/prof_topk $B > $O/ncu5.log 2>&1
 timeout -s KILL 600 $NF -k regex:topk_select -s 0 -c 1 -o $O/prof_topk_l0 $B > $O/ncu6.log 2>&1
-timeout -s KILL 600 $NF -k regex:self_attn -s 20 -c 1 -o $O/prof_self $B > $O/ncu7.log 2>&1
+timeout -s KILL 600 $NF -k regex:self_attn -s 23 -c 1 -o $O/prof_self $B > $O/ncu7.log 2>&1
 timeout -s KILL 600 $NF -k regex:latent_attn -s 8 -c 1 -o $O/prof_lat_x $B > $O/ncu8.log 2>&1
 timeout -s KILL 600 $NF -k regex:latent_out -s 8 -c 1 -o $O/prof_lat_y $B > $O/ncu9.log 2>&1
 timeout -s KILL 600 $NF -k regex:ln_rows_split -s 8 -c 1 -o $O/prof_ln3 $B > $O/ncu10.log 2>&1
