@@ -270,15 +270,23 @@ def class_work(cfgd):
     # the fuse: one d x d GEMM per level row (token-side products tabulated)
     gemm += sum(R[t] * ((2 * d * d if K > 0 else 0) + 2 * d * V[t]) for t in range(T))
     attn = layer_rows * (4 * S * F + 2 * d * F)
-    topk = sum(R[t] * V[t] * 4 + R[t] * 12 + R[t + 1] * (20 + 8 * (t + 2)) for t in range(T))
+    # selection on the tensor path: the logits epilogue's per-128-column
+    # partials (float4: max, sum, two 64-column maxima) are the window proxies;
+    # the collect reads only the 64-column blocks whose maximum falls inside
+    # the window (a few % of the logits, data dependent, NOT counted here: the
+    # figure is a floor), plus per-row state and the next level's rows
+    nprox = [(v + 127) // 128 for v in V]
+    topk = sum(R[t] * (nprox[t] * 16 + 12) + R[t + 1] * (20 + 8 * (t + 2)) for t in range(T))
     soft = 0
-    # LN3 (h in, fp16 hi / lo out); the latent output + LN2 kernel (h and z
-    # in; h, hi / lo and the fp32 history row out)
-    ln = layer_rows * (24 * d + 4 * F)
+    # LN3 (h in, fp16 hi / lo out: 8 d); the latent output + LN2 kernel (h and
+    # z in; h and n hi / lo -- straight into the self-attention history -- out:
+    # 12 d + 4 F)
+    ln = layer_rows * (20 * d + 4 * F)
     # q' and the normalised history rows n (fp32), the output as fp16 hi / lo
     sattn = K * n_trunk * 4 * (2 * d + d * T) + (L - K) * sum(
         R[t] * 4 * (2 * d + d * (t + 1)) for t in range(T))
-    lse = sum(R[t] * (V[t] * 4 + 8) for t in range(T))
+    # lse_merge: the per-128-column partials in, (max, log-sum) per row out
+    lse = sum(R[t] * (nprox[t] * 16 + 8) for t in range(T))
     return {"gemm": ("flop", gemm), "attn_gemm": ("flop", attn), "topk_select": ("byte", topk),
             "softmax": ("byte", soft), "layernorm": ("byte", ln), "self_attn": ("byte", sattn),
             "row_lse": ("byte", lse),
