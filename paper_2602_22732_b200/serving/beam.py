@@ -256,7 +256,7 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
     device, results come back as one async copy, and the SemanticIds are
     built in bulk.  ``pipeline``: request groups decoded back to back on
     one stream so host work overlaps device work ("auto": two groups from
-    64 requests on; an int: that many) -- results are identical either way."""
+    96 requests on; an int: that many) -- results are identical either way."""
     cfg = model.config
     if (contexts is None) == (features is None):
         raise ValueError("pass exactly one of contexts / features")
@@ -307,7 +307,7 @@ def beam_search_batch(model, contexts=None, schedules=None, features=None, share
         c = tuple(int(w) for w in getattr(_capacity, "widths", _capacity))
         if len(c) == cfg.n_levels and all(all(a <= b for a, b in zip(w, c)) for w in per):
             cap = [c] * B
-    parts = (2 if B >= 64 else 1) if pipeline == "auto" else int(pipeline)
+    parts = (2 if B >= 96 else 1) if pipeline == "auto" else int(pipeline)
     out, item_idx = _decode(model, lens, per, k_depth, value_rerank, reps, valid_sids, path,
                             inp, kind, _items, cap, parts, _lazy, _graphs)
     if counter is not None:
