@@ -358,6 +358,48 @@ self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
       return reinterpret_cast<const float4 *>(qkv + row * ld3 + off)[lane + 32 * i];
     }
   };
+  float4 o[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (HS && v_off == d) {
+    // factored attention: keys and values are the same history rows n_j, so
+    // one pass reads each ancestor once (online softmax: running max m and
+    // sum l, the accumulator rescaled when the max moves)
+    float m = -INFINITY, l = 0.f;
+#pragma unroll
+    for (int t = 0; t < kMaxPos; ++t) {
+      if (t < np) {
+        const long long row = anc[(long long)g * stride + t];
+        float4 k[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) k[i] = hrow(row, d, i);
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+          acc = fmaf(q[i].x, k[i].x, fmaf(q[i].y, k[i].y, fmaf(q[i].z, k[i].z, fmaf(q[i].w, k[i].w, acc))));
+        const float s = warp_sum(acc) * scale;
+        const float mn = fmaxf(m, s);
+        const float cs = expf(m - mn), ps = expf(s - mn);  // (m = -inf: cs = 0)
+        l = l * cs + ps;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          o[i].x = fmaf(ps, k[i].x, o[i].x * cs);
+          o[i].y = fmaf(ps, k[i].y, o[i].y * cs);
+          o[i].z = fmaf(ps, k[i].z, o[i].z * cs);
+          o[i].w = fmaf(ps, k[i].w, o[i].w * cs);
+        }
+        m = mn;
+      }
+    }
+    const float inv = 1.f / l;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      o[i].x *= inv;
+      o[i].y *= inv;
+      o[i].z *= inv;
+      o[i].w *= inv;
+    }
+  } else {
   float sc[kMaxPos];
   float mx = -INFINITY;
 #pragma unroll
@@ -380,9 +422,6 @@ self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
   for (int t = 0; t < kMaxPos; ++t)
     if (t < np) sum += expf(sc[t] - mx);
   const float lse = logf(sum) + mx;
-  float4 o[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int t = 0; t < kMaxPos; ++t) {
     if (t < np) {
@@ -398,6 +437,7 @@ self_attn_warp_kernel(const float *__restrict__ qkv, long long ld3, int d,
       }
     }
   }
+  }  // (two-pass: separate key / value rows)
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int j = 4 * (lane + 32 * i);
