@@ -176,10 +176,13 @@ class LoadEstimator:
                 upto -= 1
             return (upto - h) / self.window
 
-    def record_service(self, n_requests, seconds):
+    def record_service(self, n_requests, seconds, concurrency=1.0):
+        """A batch of ``n_requests`` decoded in ``seconds`` of wall time while
+        ``concurrency`` batches (on average) were being served at once: the
+        engine's rate is the batch's rate times the overlap."""
         if n_requests <= 0 or seconds <= 0:
             return
-        c = n_requests / seconds
+        c = n_requests * max(1.0, float(concurrency)) / seconds
         with self._lock:
             self._max_batch = max(self._max_batch, int(n_requests))
             if 2 * n_requests < self._max_batch:
@@ -362,6 +365,9 @@ class ServingEngine:
                 break
         dfeats = feats + [feats[-1]] * (pad - n)
         dscheds = list(scheds) + [scheds[-1]] * (pad - n)
+        with self._lock:
+            self._inflight = self.__dict__.get("_inflight", 0) + 1
+            k0 = self._inflight
         t0 = time.perf_counter()
         results, slots = beam_search_batch(
             model, features=dfeats, schedules=dscheds, shared_kv=self.config.shared_kv,
@@ -372,7 +378,12 @@ class ServingEngine:
             # plans) and launches other width plans directly: a capture
             # (10-40 ms at C5) never lands on a request's latency
             _graphs=False)
-        self.load.record_service(n, time.perf_counter() - t0)
+        dt = time.perf_counter() - t0
+        with self._lock:
+            k1 = self._inflight
+            self._inflight -= 1
+        # concurrent serving threads share the GPU: scale by the overlap
+        self.load.record_service(n, dt, 0.5 * (k0 + k1))
         with self._lock:
             self.model_invocations += len(misses)
         calls = kv_b = kv_f = 0

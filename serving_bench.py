@@ -26,8 +26,10 @@ import gc
 import json
 import os
 import sys
+import threading
 import time
 from collections import OrderedDict
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -51,6 +53,8 @@ def main():
     ap.add_argument("--boost", type=float, default=0.6)
     ap.add_argument("--items", type=int, default=100000)
     ap.add_argument("--p99-bound-ms", type=float, default=None)
+    ap.add_argument("--workers", type=int, default=1,
+                    help="serving threads calling serve_batch concurrently (one batch each)")
     ap.add_argument("--profile", action="store_true",
                     help="cProfile the sweep; top functions to stderr")
     args = ap.parse_args()
@@ -127,14 +131,24 @@ def _run(args):
     gc.callbacks.append(on_gc)
     for _ in range(3):
         eng.serve_batch(requests(args.max_batch, np.zeros(args.max_batch)), 0.0, qps=1e13)
-    reps = 5
+    reps = 5 * args.workers
+    pool = ThreadPoolExecutor(args.workers) if args.workers > 1 else None
+    if pool is not None:  # warm every worker thread's decoders / streams
+        list(pool.map(lambda _: eng.serve_batch(
+            requests(args.max_batch, np.zeros(args.max_batch)), 0.0, qps=1e13),
+            range(2 * args.workers)))
     t0 = time.perf_counter()
-    for _ in range(reps):
-        eng.serve_batch(requests(args.max_batch, np.zeros(args.max_batch)), 0.0, qps=1e13)
+    if pool is None:
+        for _ in range(reps):
+            eng.serve_batch(requests(args.max_batch, np.zeros(args.max_batch)), 0.0, qps=1e13)
+    else:
+        batches_cal = [requests(args.max_batch, np.zeros(args.max_batch)) for _ in range(reps)]
+        list(pool.map(lambda b: eng.serve_batch(b, 0.0, qps=1e13), batches_cal))
     cap = reps * args.max_batch / (time.perf_counter() - t0)
     print(json.dumps({"model": args.model, "capacity_req_s": cap, "base_widths": list(base),
                       "max_batch": args.max_batch, "api": "ServingEngine.serve_batch",
-                      "items_indexed": args.items, "warmup_s": warm_s}), flush=True)
+                      "workers": args.workers, "items_indexed": args.items,
+                      "warmup_s": warm_s}), flush=True)
 
     for rho in [float(x) for x in args.loads.split(",")]:
         lam = rho * cap
@@ -148,26 +162,47 @@ def _run(args):
         eng.load.capacity = cap  # seeded with the calibration; the engine's EWMA refines it
         lat = np.zeros(n)
         widths_seen = []
-        done = batches = n_items = 0
+        done = batches = 0
+        n_items = [0]
         start = time.perf_counter()
+        free = threading.Semaphore(args.workers)
+        futs = []
+
+        def serve(lo, hi, now, b_idx):
+            try:
+                c0 = DEC.STATS["captures"]
+                res = eng.serve_batch(requests_cache[b_idx], now)
+                t_done = time.perf_counter() - start
+                call_ms.append(1e3 * (t_done - now))
+                slow.append((call_ms[-1], b_idx, hi - lo, DEC.STATS["captures"] - c0))
+                lat[lo:hi] = t_done - arrivals[lo:hi]
+                widths_seen.extend(r.widths[-1] for r in res)
+                n_items[0] += sum(len(r.items) for r in res)
+            finally:
+                free.release()
+
+        requests_cache = {}
         while done < n:
             now = time.perf_counter() - start
             if arrivals[done] > now:
                 time.sleep(min(0.0005, arrivals[done] - now))
                 continue
+            if not free.acquire(timeout=0.0005):
+                continue  # every worker busy: arrivals keep queueing
+            now = time.perf_counter() - start
             hi = done
             while hi < n and hi - done < args.max_batch and arrivals[hi] <= now:
                 hi += 1
-            c0 = DEC.STATS["captures"]
-            res = eng.serve_batch(requests(hi - done, arrivals[done:hi]), now)
-            t_done = time.perf_counter() - start
-            call_ms.append(1e3 * (t_done - now))
-            slow.append((call_ms[-1], batches, hi - done, DEC.STATS["captures"] - c0))
-            lat[done:hi] = t_done - arrivals[done:hi]
-            widths_seen.extend(r.widths[-1] for r in res)
-            n_items += sum(len(r.items) for r in res)
+            requests_cache[batches] = requests(hi - done, arrivals[done:hi])
+            if pool is None:
+                serve(done, hi, now, batches)
+            else:
+                futs.append(pool.submit(serve, done, hi, now, batches))
             batches += 1
             done = hi
+        for f in futs:
+            f.result()
+        n_items = n_items[0]
         wall = time.perf_counter() - start
         ws = np.asarray(widths_seen)
         line = {"model": args.model, "offered_load": rho, "offered_req_s": lam,
