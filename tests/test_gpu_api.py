@@ -415,7 +415,7 @@ def test_engine_resolves_items_on_device_and_measures_load():
     from paper_2602_22732_b200.serving.engine import LoadEstimator
 
     class Fixed(LoadEstimator):
-        def record_service(self, n, seconds):
+        def record_service(self, *args, **kwargs):
             pass
 
     est = Fixed(window=1.0)
