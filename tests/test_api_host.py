@@ -169,6 +169,10 @@ def test_load_estimator_rate_and_slack():
     assert abs(est.capacity - 400.0) < 1e-9
     est.record_service(300, 0.5)  # >= half the largest batch: EWMA update
     assert abs(est.capacity - (0.8 * 400.0 + 0.2 * 600.0)) < 1e-9
+    # two serving threads overlapping: the engine's rate is the batch's x 2
+    cap0 = est.capacity
+    est.record_service(400, 2.0, concurrency=2.0)
+    assert abs(est.capacity - (0.8 * cap0 + 0.2 * 400.0)) < 1e-9
 
 
 def test_lazy_sid_lists_equal_the_eager_lists():
