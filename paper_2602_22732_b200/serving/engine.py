@@ -209,8 +209,7 @@ class ItemTable:
 
     def __init__(self, index, vocab, device):
         sids, items = [], []
-        with index._write_lock:  # a consistent snapshot of the forward map
-            fwd = list(index._forward.items())
+        fwd = index.snapshot()  # a consistent copy of the forward map
         T = len(vocab)
         for sid, ids in fwd:
             toks = getattr(sid, "tokens", sid)
