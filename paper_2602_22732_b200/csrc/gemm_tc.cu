@@ -359,11 +359,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) dbg_stamp(a.dbg, 1);
-  // programmatic dependent launch: the set-up above (barriers, TMEM, cluster
-  // sync) overlaps the previous kernel's tail; nothing below touches global
-  // memory before the previous kernel's writes are visible (a no-op when
-  // launched without the attribute)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
   const bool leader = rank == 0;
   const int tstep = PAIR ? gridDim.x / 2 : gridDim.x;  // tiles are per pair
@@ -806,15 +801,6 @@ static int num_sms() {
   return cached[dev];
 }
 
-// GR4AD_PDL=0: launch the GEMMs without programmatic dependent launch (A/B aid)
-static bool pdl_enabled() {
-  static const bool on = [] {
-    const char *e = getenv("GR4AD_PDL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 template <int BN, int STAGES, bool BSPLIT, bool ASPLIT = false>
 static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl,
                      const CUtensorMap &mal, const TcArgs &a, int epi, cudaStream_t st) {
@@ -825,22 +811,13 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
   const int n_tiles = tiles_m * tiles_n * a.groups;
   const int grid = std::min(n_tiles, num_sms());
   const int cls = (a.mode == GM_PLAIN) ? KC_GEMM : KC_ATTN_GEMM;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
 #define GR_TC_EPI(E)                                                                          \
   case E: {                                                                                   \
-    auto *k = gemm_tc_kernel<BN, STAGES, E, BSPLIT, ASPLIT>;                                  \
-    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(k), (int)smem));                    \
-    GR_LAUNCH(cls, st, GR_CUDA(cudaLaunchKernelEx(&cfg, k, ma, mb, mbl, mal, a, tiles_m,      \
-                                                  tiles_n, n_tiles)));                        \
+    GR_CUDA(set_smem_attr(reinterpret_cast<const void *>(gemm_tc_kernel<BN, STAGES, E, BSPLIT, ASPLIT>),               \
+                                 (int)smem));      \
+    GR_LAUNCH(cls, st, gemm_tc_kernel<BN, STAGES, E, BSPLIT, ASPLIT>                           \
+                       <<<grid, kTcThreads, smem, st>>>(ma, mb, mbl, mal, a, tiles_m, tiles_n,  \
+                                                        n_tiles));                            \
     return GR4AD_OK;                                                                          \
   }
   if (epi == EPI_STORE_T || epi == EPI_STORE_T_SPLIT) {
@@ -909,15 +886,13 @@ static int launch_tc_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CU
   cfg.blockDim = dim3(kTcThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cfg.numAttrs = 1;
 #define GR_TC_PAIR(E)                                                                            \
   case E: {                                                                                      \
     auto *k = gemm_tc_kernel<BN, STAGES, E, true, true, true>;                                   \
