@@ -572,3 +572,48 @@ def test_set_widths_with_masking_and_rerank(d, path):
                             valid_sids=valid, path=path)
         fresh.run(features=x)
         assert got == fresh.host_results(), widths
+
+
+def test_engine_masked_warmup_and_concurrent_callers():
+    """ServingEngine with valid-SID masking: warm-up builds the masked
+    decoders (the SID tuple's digest is part of their key), every served SID
+    is a prefix-valid one, and two threads calling serve_batch at once get
+    exactly the results of one-at-a-time calls."""
+    import threading
+    M, S = _need()
+    from paper_2602_22732_b200.decode import POOL
+    from paper_2602_22732_b200.quantizer import SemanticId, SidIndex
+    model = _model(M, C1_MODEL)
+    rng = np.random.default_rng(21)
+    index = SidIndex()
+    V = tuple(model.config.level_vocab_sizes)
+    for i in range(3000):
+        index.upsert(f"it{i}", SemanticId(tuple(int(rng.integers(0, v)) for v in V), V))
+    cfg = S.ServingConfig(S.BeamSchedule(C2_WIDTHS, 256), q_threshold=1e9, mask_to_index=True)
+    POOL.clear()
+    eng = S.ServingEngine(S.SnapshotStore(model), index, cfg)
+    eng.warmup(c_features(0, 256), max_batch=8)
+    built = len(POOL)
+    valid = set(index.all_sids())
+    reqs = [[(f"w{k}u{i}", c_features(50 + 8 * k + i, 256)) for i in range(6)] for k in range(2)]
+    seq = [eng.serve_batch(r, now=float(k), qps=1.0, capacity_slack=0.5)
+           for k, r in enumerate(reqs)]
+    assert len(POOL) == built  # served from the warmed decoders
+    for res in seq:
+        for r in res:
+            assert all(sid in valid for sid, _ in r.sids)
+            assert [i for i, _ in r.items] and len(r.items) == len(r.sids)
+    eng2 = S.ServingEngine(S.SnapshotStore(model), index, cfg)
+    out = [None, None]
+
+    def call(k):
+        out[k] = eng2.serve_batch(reqs[k], now=float(k), qps=1.0, capacity_slack=0.5)
+
+    ts = [threading.Thread(target=call, args=(k,)) for k in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for k in range(2):
+        assert [(r.items, list(r.sids)) for r in out[k]] == \
+            [(r.items, list(r.sids)) for r in seq[k]]
