@@ -1,5 +1,5 @@
 #!/bin/bash
-# split-K check: GPU tests, then per-launch attribution of C3 / C5 steps
+# GPU tests, then per-launch attribution (GR4AD_PROF_DUMP) of C3 / C5 steps
 O=${O:-gpurun_out/ks}
 mkdir -p $O
 timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/gpu_tests.txt 2>&1

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (split-K experiment record: the GR4AD_KSPLIT / GR4AD_SMALLM switches were removed with it)
 # ncu of the trunk's first W1 product (M=768, epi 10) under split-K variants
 O=${O:-gpurun_out/ksn}
 mkdir -p $O
