@@ -414,13 +414,17 @@ class ServingEngine:
         cap = self._capacity_widths()
         plans = widths if widths is not None else [self.config.schedule.widths, cap]
         valid = self._valid_sids()
+        table = self._item_table(model)
         for b in buckets:
             for w in plans:
                 for _ in range(2):  # the second use captures the plan's graph
+                    # (with the item resolution serving runs, so the decoders'
+                    # pinned result buffers already have their serving layout)
                     beam_search_batch(model, features=[f] * b, schedules=[tuple(w)] * b,
                                       shared_kv=self.config.shared_kv,
                                       value_rerank=self.config.value_rerank,
-                                      buckets=self.buckets, valid_sids=valid, _capacity=cap)
+                                      buckets=self.buckets, valid_sids=valid,
+                                      _items=table.args(), _capacity=cap, _lazy=True)
 
     def _valid_sids(self):
         """The index's SIDs as one tuple per index version (masked decoding;
