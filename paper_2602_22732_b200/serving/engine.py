@@ -268,6 +268,9 @@ class ServingEngine:
         self.requests = 0
         self.load = load if load is not None else LoadEstimator()
         self._table = None  # (index version, vocab, ItemTable)
+        self._valid = None  # (index version, tuple of its SIDs) for masked decoding
+        self._cf_memo = {}  # (config, widths, S, ...) -> closed-form counters
+        self._inflight = 0  # serve_batch calls decoding right now (load estimate)
         model = store.current()[1] if torch.cuda.is_available() else None
         if model is not None:  # off the first request's latency
             self._item_table(model)
@@ -365,7 +368,7 @@ class ServingEngine:
         dfeats = feats + [feats[-1]] * (pad - n)
         dscheds = list(scheds) + [scheds[-1]] * (pad - n)
         with self._lock:
-            self._inflight = self.__dict__.get("_inflight", 0) + 1
+            self._inflight += 1
             k0 = self._inflight
         t0 = time.perf_counter()
         results, slots = beam_search_batch(
@@ -431,7 +434,7 @@ class ServingEngine:
         the tuple's digest -- part of the pooled decoder's key -- is cached)."""
         if not self.config.mask_to_index:
             return None
-        vs = self.__dict__.get("_valid")
+        vs = self._valid
         if vs is None or vs[0] != self.index.version:
             vs = (self.index.version, tuple(self.index.all_sids()))
             self._valid = vs
@@ -450,7 +453,7 @@ class ServingEngine:
         """(layer calls, kv builds, kv floats) of one request's decode
         (record_counter's closed form), memoised per (config, widths, S)."""
         key = (cfg, tuple(widths), int(s_ctx), self.config.shared_kv, self.config.value_rerank)
-        memo = self.__dict__.setdefault("_cf_memo", {})
+        memo = self._cf_memo
         hit = memo.get(key)
         if hit is None:
             c = LayerCallCounter()
