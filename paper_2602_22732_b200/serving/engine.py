@@ -160,6 +160,11 @@ class LoadEstimator:
         with self._lock:
             self._arrivals.extend([float(now)] * int(n))
 
+    def observe_many(self, times):
+        """Arrivals at each of ``times`` (non-decreasing), one lock."""
+        with self._lock:
+            self._arrivals.extend(float(t) for t in times)
+
     def rate(self, now):
         with self._lock:
             lo = float(now) - self.window
@@ -237,6 +242,25 @@ class ItemTable:
 
     def args(self):
         return (self.keys, self.ids, self.n)
+
+    def resolve_batch(self, sids_list, slots):
+        """resolve() for every request of a batch at once: one pass over the
+        (B, max_out) slot array, item lists built only where SIDs hit."""
+        B = len(sids_list)
+        out = [[] for _ in range(B)]
+        if B == 0:
+            return out
+        slots = np.asarray(slots)[:B]
+        n = np.fromiter((len(x) for x in sids_list), dtype=np.int64, count=B)
+        live = (np.arange(slots.shape[1])[None, :] < n[:, None]) & (slots >= 0)
+        rows, cols = np.nonzero(live)
+        if rows.size:
+            objs = self.items[slots[rows, cols]].tolist()
+            for r, c, o in zip(rows.tolist(), cols.tolist(), objs):
+                sids = sids_list[r]
+                sc = getattr(sids, "scores", None)
+                out[r].append((o, float(sc[c]) if sc is not None else float(sids[c][1])))
+        return out
 
     def resolve(self, sids, slots):
         """[(item, score)] for one request from its SID list and slot row."""
@@ -321,19 +345,19 @@ class ServingEngine:
         encoder K/V, trunk, level steps, compaction and SID -> item
         resolution on the device).  Widths: with an explicit ``qps`` every
         miss gets scale_schedule(tabs_adjust(qps, capacity_slack)) as in the
-        reference; with ``qps=None`` each request gets the widths of the
-        load the engine measured at its own arrival time (per-request TABS
-        widths inside one batch)."""
+        reference; with ``qps=None`` the engine's own load signal sets them --
+        read once at the batch's latest arrival (``load_widths="batch"``), or
+        at every request's arrival (``"request"``: per-request widths inside
+        one batch)."""
         with self._lock:
             self.requests += len(requests)
         version_key = self.index.version
         out = [None] * len(requests)
         misses = []
+        if qps is None:
+            self.load.observe_many([req[2] if len(req) > 2 else now for req in requests])
         for i, req in enumerate(requests):
             uid = req[0]
-            t_arr = req[2] if len(req) > 2 else now
-            if qps is None:
-                self.load.observe(t_arr)
             cached = self.cache.get((uid, version_key), now)
             if cached is not None:
                 out[i] = ServeResult(cached[0], cached[1], True, cached[2], cached[3], 0)
@@ -389,10 +413,11 @@ class ServingEngine:
         with self._lock:
             self.model_invocations += len(misses)
         calls = kv_b = kv_f = 0
+        item_lists = table.resolve_batch(results[:n], slots)
         for j, (i, sids) in enumerate(zip(misses, results)):
             uid = requests[i][0]
             sched = scheds[j]
-            items = table.resolve(sids, slots[j])
+            items = item_lists[j]
             self.cache.put((uid, version_key), (items, sids, version, sched.widths), now)
             # per-request virtual latency: the closed-form layer calls of its decode
             c = self._closed_form(model.config, sched.widths, feats[j].shape[0])

@@ -253,3 +253,7 @@ def test_engine_capacity_widths_and_item_table():
     sids = [(SemanticId((1, 2), (3, 3)), -0.5), (SemanticId((2, 2), (3, 3)), -0.7),
             (SemanticId((0, 1), (3, 3)), -0.9)]
     assert tab.resolve(sids, np.array([1, -1, 0, 5], np.int32)) == [("a", -0.5), ("c", -0.9)]
+    # the batched form equals per-request resolve (slots past a list's end ignored)
+    lists = [sids, sids[:1], [], sids[::-1]]
+    slots = np.array([[1, -1, 0, 5], [1, 0, 0, 0], [0, 0, 0, 0], [0, -1, 1, 1]], np.int32)
+    assert tab.resolve_batch(lists, slots) == [tab.resolve(x, r) for x, r in zip(lists, slots)]
