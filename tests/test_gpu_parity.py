@@ -415,3 +415,30 @@ def test_prefix_masking_c1_model(path, n_valid):
                                valid_sids=valid)
         assert all(sid.tokens in vset for sid, _ in got[i])
         check_parity(want, [(sid.tokens, s) for sid, s in got[i]], f"mask{n_valid}[{i}]")
+
+
+@pytest.mark.parametrize("rerank", [False, True])
+def test_prefix_masking_tensor_path_d128(rerank):
+    """Prefix masking on the layered tcgen05 path with the latent
+    cross-attention (d = 128, features in): masked selection (histogram path)
+    and, with re-rank, the value head over the surviving beams -- against
+    the oracle restatement."""
+    M, S = _pkg()
+    ocfg = orc.OracleConfig(16, 128, 256, 3, 1, (64, 32, 128), 4, 17)
+    model = _model(M, ocfg)
+    params = {k: v.data for k, v in model.params.items()}
+    rng = np.random.default_rng(17)
+    valid = sorted({tuple(int(rng.integers(0, v)) for v in (64, 32, 128)) for _ in range(2000)})
+    reps = [0.2, 0.5, 1.0, 3.0]
+    feats = [c_features(600 + i, 96) for i in range(4)]
+    widths = (8, 16, 32)
+    got = S.beam_search_batch(model, features=feats, schedules=S.BeamSchedule(widths, 32),
+                              valid_sids=valid, value_rerank=rerank,
+                              buckets=reps if rerank else None, path="tensor")
+    vset = set(valid)
+    for i in range(4):
+        want = orc.beam_search(params, ocfg, orc.context_process(feats[i], params), widths,
+                               value_rerank=rerank, representatives=reps if rerank else None,
+                               valid_sids=valid)
+        assert all(sid.tokens in vset for sid, _ in got[i])
+        check_parity(want, [(sid.tokens, s) for sid, s in got[i]], f"mask-tc rr={rerank}[{i}]")
